@@ -1,0 +1,117 @@
+/*
+ * pancake_b200.h -- C-ABI of the B200-native IVF search hot path.
+ *
+ * The reference (arxiv/paper_2602_21477, package `agentmem`, pure Python)
+ * has no C interface; its plugin boundaries are Python protocols.  Each entry
+ * point below names the reference interface it replaces (file:line into
+ * /root/reference/pkg/src/agentmem/).  Plain pointers and sizes only; no torch
+ * types.  All calls return PK_OK (0) or an error code; pk_last_error() gives
+ * the message of the calling thread's last failure.
+ *
+ * Pointer convention: by default every data pointer is HOST memory (pinned or
+ * pageable); the call copies host<->device itself and returns when outputs are
+ * in place.  With PK_DEVICE_PTRS in `flags` the pointers are device pointers on
+ * the index's device and the call is asynchronous on the index stream
+ * (pk_stream / pk_sync).
+ *
+ * Arithmetic is the reference's exactly (ref/kernels.py:73-135): fp32, j
+ * ascending, every op rounded, no FMA; ordering is (distance, id) with ties to
+ * the smaller id (ref/engine.py:411) and (distance, cid) for lists
+ * (ref/graph.py:395).
+ */
+#ifndef PANCAKE_B200_H
+#define PANCAKE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_OK 0
+#define PK_ERR_USAGE 1  /* precondition violated -> agentmem.core.UsageError (core.py:20-21) */
+#define PK_ERR_DEVICE 2 /* CUDA failure -> agentmem.tiering.AcceleratorError (tiering.py:29-30) */
+#define PK_ERR_NOMEM 3  /* device allocation failed -> AcceleratorError("allocation failed") */
+
+#define PK_DEVICE_PTRS 1
+
+#define PK_METRIC_SQ_L2 0  /* Metric.SQUARED_EUCLIDEAN, wire code 0 (core.py:40-58) */
+#define PK_METRIC_IP 1     /* Metric.INNER_PRODUCT (negated) */
+#define PK_METRIC_COSINE 2 /* Metric.COSINE */
+
+typedef struct pk_index pk_index;
+
+/* ---- library ---------------------------------------------------------- */
+const char* pk_last_error(void);
+int pk_version(void);
+int pk_device_count(int* n);
+
+/* ---- kernel table: replaces kernels.BACKENDS[...] (kernels.py:138-158) -- */
+/* out[b][i] = dist(q[b], mat[i]); batch_distances (core.py:98-109) for B
+ * queries at once.  q: [B][d], mat: [n][d], out: [B][n]. */
+int pk_distances(const float* q, int64_t B, const float* mat, int64_t n, int64_t d, int metric,
+                 float* out, int flags);
+/* kmeans_assign_nb (kernels.py:116-135): labels i64[n], dists f64[n]. */
+int pk_kmeans_assign(const float* x, int64_t n, const float* cents, int64_t k, int64_t d,
+                     int64_t* labels, double* dists, int flags);
+/* core.centroid (core.py:112-117): fp64 row-order mean -> f32[d]. */
+int pk_centroid(const float* mat, int64_t n, int64_t d, float* out, int flags);
+
+/* ---- device index: ClusterStore storage + TierManager residency -------- */
+/* (clusters.py:186-362, tiering.py:175-448).  One index per device.        */
+int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
+                    int64_t reserve_lists, pk_index** out);
+int pk_index_destroy(pk_index* ix);
+int pk_sync(pk_index* ix);
+void* pk_stream(pk_index* ix);
+/* Bytes of HBM held by the arena + list table. */
+int pk_index_bytes(pk_index* ix, int64_t* bytes);
+
+/* ClusterStore.create_cluster (clusters.py:250-266): new posting list `cid`
+ * in scope `scope_code` with n seed rows; centroid recomputed on device as in
+ * Cluster.recompute_stats (clusters.py:111-118) and returned in out_centroid
+ * (host f32[d], may be NULL). */
+int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* rows,
+                   const int64_t* ids, int64_t n, float* out_centroid, int flags);
+/* Cluster.add (clusters.py:71-79) / TierManager.buffered_insert
+ * (tiering.py:280-290): append rows in place (relocating when full). */
+int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* ids, int64_t n,
+                   int flags);
+/* Cluster.remove (clusters.py:81-109): swap-with-last compaction of `row`. */
+int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row);
+/* ClusterStore.retire_cluster (clusters.py:352-362). */
+int pk_list_retire(pk_index* ix, int64_t cid);
+/* Cluster.recompute_stats centroid (clusters.py:111-118) on device;
+ * out_centroid host f32[d] (may be NULL). */
+int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid);
+/* Overwrite the routing centroid of `cid` (host f32[d]). */
+int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid);
+int pk_list_size(pk_index* ix, int64_t cid, int64_t* n);
+/* Read back rows (host f32[n][d]) and ids (host i64[n]); either may be NULL. */
+int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids);
+
+/* ---- batched hot path ------------------------------------------------- */
+/* Store._search_read_phase for the bare IVF path (engine.py:319-404) over a
+ * batch: coarse top-nprobe over the in-scope lists (graph.py:321-396 at
+ * exhaustive ef), fused exact scan of every probed list
+ * (tiering.py:294-328), merge to the first kk by (distance, id) with
+ * first-occurrence dedup (engine.py:406-426).
+ *   Q: [B][d]; scope_codes: [nscopes] (<= 64)
+ *   out_ids/out_dists/out_cids: [B][kk] (unused tail: -1 / +inf / -1)
+ *   out_n: [B] hits per query; out_probe: [B][nprobe] cids (may be NULL,
+ *   -1 padded); out_scanned: [B] scanned vectors (SearchStats, may be NULL).
+ * nprobe <= 2048, 1 <= kk <= 64. */
+int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+              int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids, float* out_dists,
+              int64_t* out_cids, int32_t* out_n, int64_t* out_probe, int64_t* out_scanned,
+              int flags);
+/* ClusterStore.assign_nearest (clusters.py:268-279) for n vectors against
+ * the lists of one scope: out_cid [n] (-1 when the scope has no lists),
+ * out_dist [n] (may be NULL). */
+int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
+              float* out_dist, int flags);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PANCAKE_B200_H */

@@ -1,0 +1,742 @@
+// pk_abi.cu -- the device index (HBM arena of posting lists + list table) and
+// the extern "C" boundary declared in include/pancake_b200.h.
+//
+// Layout in HBM:
+//   rows  f32[arena_rows][dp]  every posting list is a contiguous row range
+//                              [off, off+cap) of one arena; dp = d rounded up
+//                              to 32 floats (zero padded, 128-byte rows chunks)
+//   ids   i64[arena_rows]      item id of each row
+//   list table (per slot): off, len, cid, scope code, centroid f32[dp]
+// A list grows in place into its slack (25% + 16 rows, like the reference's
+// device slack, ref/tiering.py:356) and is relocated when full.
+#include "../../include/pancake_b200.h"
+#include "pk_kernels.h"
+
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+using namespace pk;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                           \
+  do {                                                                                     \
+    cudaError_t e_ = (call);                                                               \
+    if (e_ != cudaSuccess) {                                                               \
+      cudaGetLastError();                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? PK_ERR_NOMEM : PK_ERR_DEVICE,          \
+                  "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+    }                                                                                      \
+  } while (0)
+
+#define RET(call)                \
+  do {                           \
+    int r_ = (call);             \
+    if (r_ != PK_OK) return r_;  \
+  } while (0)
+
+inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need, bool zero = false, cudaStream_t st = 0) {
+    if (need <= bytes) return PK_OK;
+    size_t nb = std::max(need, bytes + bytes / 2);
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    CK(cudaMalloc(&p, nb));
+    if (zero) CK(cudaMemsetAsync(p, 0, nb, st));
+    bytes = nb;
+    return PK_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Range {
+  int64_t off, cap;
+};
+
+}  // namespace
+
+struct pk_index {
+  int device = 0;
+  int64_t d = 0, dp = 0;
+  int metric = 0;
+  int num_sms = 148;
+  cudaStream_t st = nullptr;
+
+  // arena
+  float* rows = nullptr;
+  int64_t* ids = nullptr;
+  int64_t arena_cap = 0, arena_top = 0;
+  std::vector<Range> free_ranges;
+  ArenaMaps maps;
+
+  // list table (host mirror + device copy)
+  std::vector<int64_t> h_off, h_len, h_cap, h_cid;
+  std::vector<int32_t> h_scope;
+  std::unordered_map<int64_t, int32_t> cid2slot;
+  std::vector<int32_t> free_slots;
+  int32_t nslots = 0, slot_cap = 0;
+  int64_t *d_off = nullptr, *d_len = nullptr, *d_cid = nullptr;
+  int32_t* d_scope = nullptr;
+  float* d_cent = nullptr;
+  int32_t dirty_lo = INT32_MAX, dirty_hi = -1;
+
+  // search scratch
+  DevBuf q, qnorm, dc, probe, probe_key, counts, fillb, items, nitems, qpairs, slot_off, scanned,
+      cand_key, cand_id, cand_n, cand_list, work, out_ids, out_d, out_cid, out_n, scopes, assign_c,
+      assign_d;
+  int chunk_rows = 512;
+
+  ListTable table() const {
+    ListTable t;
+    t.rows = rows;
+    t.ids = ids;
+    t.off = d_off;
+    t.len = d_len;
+    t.cid = d_cid;
+    t.scope = d_scope;
+    t.cent = d_cent;
+    t.nslots = nslots;
+    t.dp = (int32_t)dp;
+    t.d = (int32_t)d;
+    return t;
+  }
+
+  void mark(int32_t s) {
+    dirty_lo = std::min(dirty_lo, s);
+    dirty_hi = std::max(dirty_hi, s);
+  }
+
+  int sync_table() {
+    if (dirty_hi < dirty_lo) return PK_OK;
+    const int32_t lo = dirty_lo, n = dirty_hi - dirty_lo + 1;
+    // pageable sources: the driver stages them before returning, so the host
+    // mirror may change right after.
+    CK(cudaMemcpyAsync(d_off + lo, h_off.data() + lo, n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_len + lo, h_len.data() + lo, n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_cid + lo, h_cid.data() + lo, n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_scope + lo, h_scope.data() + lo, n * 4, cudaMemcpyHostToDevice, st));
+    dirty_lo = INT32_MAX;
+    dirty_hi = -1;
+    return PK_OK;
+  }
+
+  int encode_maps() {
+    auto enc = get_encode();
+    if (!enc) return fail(PK_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+    for (int i = 0; i < NBOX; i++) {
+      cuuint64_t gdim[2] = {(cuuint64_t)dp, (cuuint64_t)arena_cap};
+      cuuint64_t gstride[1] = {(cuuint64_t)(dp * 4)};
+      cuuint32_t box[2] = {(cuuint32_t)DC, (cuuint32_t)(TILE >> i)};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult r = enc(&maps.box[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, rows, gdim, gstride, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(PK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    }
+    return PK_OK;
+  }
+
+  int grow_arena(int64_t need_rows) {
+    int64_t ncap = std::max<int64_t>({need_rows, arena_cap + arena_cap / 2, 1024});
+    float* nrows = nullptr;
+    int64_t* nids = nullptr;
+    CK(cudaMalloc(&nrows, (size_t)ncap * dp * 4));
+    CK(cudaMalloc(&nids, (size_t)ncap * 8));
+    CK(cudaMemsetAsync(nrows, 0, (size_t)ncap * dp * 4, st));
+    if (rows) {
+      CK(cudaMemcpyAsync(nrows, rows, (size_t)arena_top * dp * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(nids, ids, (size_t)arena_top * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      cudaFree(rows);
+      cudaFree(ids);
+    }
+    rows = nrows;
+    ids = nids;
+    arena_cap = ncap;
+    return encode_maps();
+  }
+
+  // First-fit range allocation; falls back to the bump pointer.
+  int alloc_range(int64_t cap, int64_t* off) {
+    for (size_t i = 0; i < free_ranges.size(); i++) {
+      if (free_ranges[i].cap >= cap) {
+        *off = free_ranges[i].off;
+        free_ranges[i].off += cap;
+        free_ranges[i].cap -= cap;
+        if (free_ranges[i].cap == 0) free_ranges.erase(free_ranges.begin() + i);
+        return PK_OK;
+      }
+    }
+    if (arena_top + cap > arena_cap) RET(grow_arena(arena_top + cap));
+    *off = arena_top;
+    arena_top += cap;
+    return PK_OK;
+  }
+  void free_range(int64_t off, int64_t cap) {
+    if (cap <= 0) return;
+    if (off + cap == arena_top) {
+      arena_top = off;
+      return;
+    }
+    free_ranges.push_back({off, cap});
+  }
+
+  int grow_slots(int32_t need) {
+    int32_t ncap = std::max<int32_t>({need, slot_cap * 2, 64});
+    int64_t *no = nullptr, *nl = nullptr, *nc = nullptr;
+    int32_t* ns = nullptr;
+    float* ncent = nullptr;
+    CK(cudaMalloc(&no, ncap * 8));
+    CK(cudaMalloc(&nl, ncap * 8));
+    CK(cudaMalloc(&nc, ncap * 8));
+    CK(cudaMalloc(&ns, ncap * 4));
+    CK(cudaMalloc(&ncent, (size_t)ncap * dp * 4));
+    CK(cudaMemsetAsync(ncent, 0, (size_t)ncap * dp * 4, st));
+    if (d_cent) {
+      CK(cudaMemcpyAsync(ncent, d_cent, (size_t)nslots * dp * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaStreamSynchronize(st));
+      cudaFree(d_off);
+      cudaFree(d_len);
+      cudaFree(d_cid);
+      cudaFree(d_scope);
+      cudaFree(d_cent);
+    }
+    d_off = no;
+    d_len = nl;
+    d_cid = nc;
+    d_scope = ns;
+    d_cent = ncent;
+    slot_cap = ncap;
+    h_off.resize(ncap, 0);
+    h_len.resize(ncap, 0);
+    h_cap.resize(ncap, 0);
+    h_cid.resize(ncap, -1);
+    h_scope.resize(ncap, -1);
+    // whole table must be re-uploaded into the new arrays
+    if (nslots > 0) {
+      mark(0);
+      mark(nslots - 1);
+    }
+    return PK_OK;
+  }
+
+  int slot_of(int64_t cid, int32_t* s) {
+    auto it = cid2slot.find(cid);
+    if (it == cid2slot.end()) return fail(PK_ERR_USAGE, "unknown cluster %lld", (long long)cid);
+    *s = it->second;
+    return PK_OK;
+  }
+
+  // Copy n rows [n][d] (host or device, contiguous) into arena rows at `at`.
+  int put_rows(int64_t at, const float* src, const int64_t* src_ids, int64_t n, bool dev) {
+    if (n <= 0) return PK_OK;
+    cudaMemcpyKind k = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpy2DAsync(rows + at * dp, dp * 4, src, d * 4, d * 4, n, k, st));
+    CK(cudaMemcpyAsync(ids + at, src_ids, n * 8, k, st));
+    if (!dev) CK(cudaStreamSynchronize(st));  // pageable/pinned source reusable on return
+    return PK_OK;
+  }
+};
+
+// Default context for the stateless kernel-table entry points.
+namespace {
+struct Ctx {
+  cudaStream_t st = nullptr;
+  DevBuf a, b, c, e;
+  std::mutex mu;
+};
+Ctx& ctx() {
+  static Ctx c;
+  static std::once_flag once;
+  std::call_once(once, [] { cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking); });
+  return c;
+}
+
+int stage_padded(DevBuf& buf, const float* src, int64_t n, int64_t d, int64_t dp, bool dev,
+                 cudaStream_t st) {
+  RET(buf.ensure((size_t)std::max<int64_t>(n, 1) * dp * 4));
+  CK(cudaMemsetAsync(buf.p, 0, (size_t)std::max<int64_t>(n, 1) * dp * 4, st));
+  if (n > 0)
+    CK(cudaMemcpy2DAsync(buf.p, dp * 4, src, d * 4, d * 4, n,
+                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  return PK_OK;
+}
+}  // namespace
+
+extern "C" {
+
+const char* pk_last_error(void) { return g_err.c_str(); }
+int pk_version(void) { return 1; }
+int pk_device_count(int* n) {
+  CK(cudaGetDeviceCount(n));
+  return PK_OK;
+}
+
+int pk_distances(const float* q, int64_t B, const float* mat, int64_t n, int64_t d, int metric,
+                 float* out, int flags) {
+  if (B < 0 || n < 0 || d < 1) return fail(PK_ERR_USAGE, "bad shape");
+  if (metric < 0 || metric > 2) return fail(PK_ERR_USAGE, "bad metric %d", metric);
+  if (B == 0 || n == 0) return PK_OK;
+  Ctx& C = ctx();
+  std::lock_guard<std::mutex> lk(C.mu);
+  const bool dev = flags & PK_DEVICE_PTRS;
+  const int64_t dp = round_up(d, DC);
+  RET(stage_padded(C.a, q, B, d, dp, dev, C.st));
+  RET(stage_padded(C.b, mat, n, d, dp, dev, C.st));
+  RET(C.e.ensure(B * 4));
+  if (metric == COSINE) launch_qnorm(C.a.as<float>(), dp, (int)B, (int)d, C.e.as<float>(), C.st);
+  float* D = out;
+  if (!dev) {
+    RET(C.c.ensure((size_t)B * n * 4));
+    D = C.c.as<float>();
+  }
+  launch_dist_dense(metric, C.a.as<float>(), dp, (int)B, C.b.as<float>(), dp, n, (int)dp,
+                    C.e.as<float>(), D, n, C.st);
+  CK(cudaGetLastError());
+  if (!dev) CK(cudaMemcpyAsync(out, D, (size_t)B * n * 4, cudaMemcpyDeviceToHost, C.st));
+  CK(cudaStreamSynchronize(C.st));
+  return PK_OK;
+}
+
+int pk_kmeans_assign(const float* x, int64_t n, const float* cents, int64_t k, int64_t d,
+                     int64_t* labels, double* dists, int flags) {
+  if (n < 0 || k < 1 || d < 1) return fail(PK_ERR_USAGE, "bad shape");
+  if (n == 0) return PK_OK;
+  Ctx& C = ctx();
+  std::lock_guard<std::mutex> lk(C.mu);
+  const bool dev = flags & PK_DEVICE_PTRS;
+  const int64_t dp = round_up(d, DC);
+  RET(stage_padded(C.a, x, n, d, dp, dev, C.st));
+  RET(stage_padded(C.b, cents, k, d, dp, dev, C.st));
+  int64_t* L = labels;
+  double* Dd = dists;
+  if (!dev) {
+    RET(C.c.ensure((size_t)n * 16));
+    L = C.c.as<int64_t>();
+    Dd = reinterpret_cast<double*>(L + n);
+  }
+  launch_kmeans_assign(C.a.as<float>(), dp, n, C.b.as<float>(), dp, k, (int)dp, L, Dd, C.st);
+  CK(cudaGetLastError());
+  if (!dev) {
+    CK(cudaMemcpyAsync(labels, L, n * 8, cudaMemcpyDeviceToHost, C.st));
+    if (dists) CK(cudaMemcpyAsync(dists, Dd, n * 8, cudaMemcpyDeviceToHost, C.st));
+  }
+  CK(cudaStreamSynchronize(C.st));
+  return PK_OK;
+}
+
+int pk_centroid(const float* mat, int64_t n, int64_t d, float* out, int flags) {
+  if (n < 1 || d < 1) return fail(PK_ERR_USAGE, "centroid of empty vector list");
+  Ctx& C = ctx();
+  std::lock_guard<std::mutex> lk(C.mu);
+  const bool dev = flags & PK_DEVICE_PTRS;
+  const int64_t dp = round_up(d, DC);
+  RET(stage_padded(C.a, mat, n, d, dp, dev, C.st));
+  RET(C.c.ensure(dp * 4));
+  launch_centroid(C.a.as<float>(), dp, n, (int)dp, C.c.as<float>(), C.st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, C.c.p, d * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                     C.st));
+  CK(cudaStreamSynchronize(C.st));
+  return PK_OK;
+}
+
+int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
+                    int64_t reserve_lists, pk_index** out) {
+  if (dim < 1) return fail(PK_ERR_USAGE, "dimension must be >= 1, got %lld", (long long)dim);
+  if (metric < 0 || metric > 2) return fail(PK_ERR_USAGE, "bad metric %d", metric);
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(PK_ERR_USAGE, "no CUDA device %d", device);
+  CK(cudaSetDevice(device));
+  pk_index* ix = new pk_index();
+  ix->device = device;
+  ix->d = dim;
+  ix->dp = round_up(dim, DC);
+  ix->metric = metric;
+  cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (const char* e = getenv("PK_CHUNK_ROWS")) ix->chunk_rows = std::max(TILE, atoi(e) / TILE * TILE);
+  cudaError_t e = cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ix;
+    return fail(PK_ERR_DEVICE, "stream create failed: %s", cudaGetErrorString(e));
+  }
+  int r = ix->grow_arena(std::max<int64_t>(reserve_rows, 1024));
+  if (r == PK_OK) r = ix->grow_slots((int32_t)std::max<int64_t>(reserve_lists, 64));
+  if (r != PK_OK) {
+    pk_index_destroy(ix);
+    return r;
+  }
+  *out = ix;
+  return PK_OK;
+}
+
+int pk_index_destroy(pk_index* ix) {
+  if (!ix) return PK_OK;
+  cudaSetDevice(ix->device);
+  if (ix->st) cudaStreamSynchronize(ix->st);
+  cudaFree(ix->rows);
+  cudaFree(ix->ids);
+  cudaFree(ix->d_off);
+  cudaFree(ix->d_len);
+  cudaFree(ix->d_cid);
+  cudaFree(ix->d_scope);
+  cudaFree(ix->d_cent);
+  for (DevBuf* b : {&ix->q, &ix->qnorm, &ix->dc, &ix->probe, &ix->probe_key, &ix->counts,
+                    &ix->fillb, &ix->items, &ix->nitems, &ix->qpairs, &ix->slot_off, &ix->scanned,
+                    &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list, &ix->work,
+                    &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
+                    &ix->assign_c, &ix->assign_d})
+    b->release();
+  if (ix->st) cudaStreamDestroy(ix->st);
+  delete ix;
+  return PK_OK;
+}
+
+int pk_sync(pk_index* ix) {
+  CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+void* pk_stream(pk_index* ix) { return ix ? (void*)ix->st : nullptr; }
+int pk_index_bytes(pk_index* ix, int64_t* bytes) {
+  *bytes = ix->arena_cap * (ix->dp * 4 + 8) + (int64_t)ix->slot_cap * (ix->dp * 4 + 28);
+  return PK_OK;
+}
+
+int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* rows,
+                   const int64_t* ids, int64_t n, float* out_centroid, int flags) {
+  if (n < 1) return fail(PK_ERR_USAGE, "create_cluster needs at least one seed item");
+  if (ix->cid2slot.count(cid)) return fail(PK_ERR_USAGE, "cluster %lld exists", (long long)cid);
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  if (!ix->free_slots.empty()) {
+    s = ix->free_slots.back();
+    ix->free_slots.pop_back();
+  } else {
+    if (ix->nslots == ix->slot_cap) RET(ix->grow_slots(ix->nslots + 1));
+    s = ix->nslots++;
+  }
+  const int64_t cap = n + n / 4 + 16;
+  int64_t off;
+  RET(ix->alloc_range(cap, &off));
+  RET(ix->put_rows(off, rows, ids, n, flags & PK_DEVICE_PTRS));
+  ix->h_off[s] = off;
+  ix->h_len[s] = n;
+  ix->h_cap[s] = cap;
+  ix->h_cid[s] = cid;
+  ix->h_scope[s] = scope_code;
+  ix->cid2slot[cid] = s;
+  ix->mark(s);
+  launch_centroid(ix->rows + off * ix->dp, ix->dp, n, (int)ix->dp, ix->d_cent + (int64_t)s * ix->dp,
+                  ix->st);
+  CK(cudaGetLastError());
+  if (out_centroid) {
+    CK(cudaMemcpyAsync(out_centroid, ix->d_cent + (int64_t)s * ix->dp, ix->d * 4,
+                       cudaMemcpyDeviceToHost, ix->st));
+    CK(cudaStreamSynchronize(ix->st));
+  }
+  return PK_OK;
+}
+
+int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* ids, int64_t n,
+                   int flags) {
+  if (n <= 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  const int64_t len = ix->h_len[s];
+  if (len + n > ix->h_cap[s]) {
+    // relocate into a larger range (Cluster._grow x1.5, ref/clusters.py:61-69)
+    const int64_t ncap = std::max<int64_t>(len + n, ix->h_cap[s] + ix->h_cap[s] / 2) + 16;
+    int64_t noff;
+    RET(ix->alloc_range(ncap, &noff));
+    const int64_t ooff = ix->h_off[s];
+    if (len > 0) {
+      CK(cudaMemcpyAsync(ix->rows + noff * ix->dp, ix->rows + ooff * ix->dp,
+                         (size_t)len * ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
+      CK(cudaMemcpyAsync(ix->ids + noff, ix->ids + ooff, (size_t)len * 8,
+                         cudaMemcpyDeviceToDevice, ix->st));
+    }
+    ix->free_range(ooff, ix->h_cap[s]);
+    ix->h_off[s] = noff;
+    ix->h_cap[s] = ncap;
+  }
+  RET(ix->put_rows(ix->h_off[s] + len, rows, ids, n, flags & PK_DEVICE_PTRS));
+  ix->h_len[s] = len + n;
+  ix->mark(s);
+  return PK_OK;
+}
+
+int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  const int64_t len = ix->h_len[s];
+  if (row < 0 || row >= len) return fail(PK_ERR_USAGE, "row %lld out of range", (long long)row);
+  const int64_t last = len - 1, off = ix->h_off[s];
+  if (row != last) {
+    CK(cudaMemcpyAsync(ix->rows + (off + row) * ix->dp, ix->rows + (off + last) * ix->dp,
+                       ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
+    CK(cudaMemcpyAsync(ix->ids + off + row, ix->ids + off + last, 8, cudaMemcpyDeviceToDevice,
+                       ix->st));
+  }
+  ix->h_len[s] = last;
+  ix->mark(s);
+  return PK_OK;
+}
+
+int pk_list_retire(pk_index* ix, int64_t cid) {
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  ix->free_range(ix->h_off[s], ix->h_cap[s]);
+  ix->h_cid[s] = -1;
+  ix->h_len[s] = 0;
+  ix->h_cap[s] = 0;
+  ix->h_scope[s] = -1;
+  ix->cid2slot.erase(cid);
+  ix->free_slots.push_back(s);
+  ix->mark(s);
+  return PK_OK;
+}
+
+int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  const int64_t n = ix->h_len[s];
+  if (n > 0)
+    launch_centroid(ix->rows + ix->h_off[s] * ix->dp, ix->dp, n, (int)ix->dp,
+                    ix->d_cent + (int64_t)s * ix->dp, ix->st);
+  CK(cudaGetLastError());
+  if (out_centroid) {
+    CK(cudaMemcpyAsync(out_centroid, ix->d_cent + (int64_t)s * ix->dp, ix->d * 4,
+                       cudaMemcpyDeviceToHost, ix->st));
+    CK(cudaStreamSynchronize(ix->st));
+  }
+  return PK_OK;
+}
+
+int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid) {
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  CK(cudaMemcpyAsync(ix->d_cent + (int64_t)s * ix->dp, centroid, ix->d * 4,
+                     cudaMemcpyHostToDevice, ix->st));
+  CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int pk_list_size(pk_index* ix, int64_t cid, int64_t* n) {
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  *n = ix->h_len[s];
+  return PK_OK;
+}
+
+int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  const int64_t n = ix->h_len[s], off = ix->h_off[s];
+  if (n > 0) {
+    if (rows)
+      CK(cudaMemcpy2DAsync(rows, ix->d * 4, ix->rows + off * ix->dp, ix->dp * 4, ix->d * 4, n,
+                           cudaMemcpyDeviceToHost, ix->st));
+    if (ids) CK(cudaMemcpyAsync(ids, ix->ids + off, n * 8, cudaMemcpyDeviceToHost, ix->st));
+  }
+  CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+              int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids, float* out_dists,
+              int64_t* out_cids, int32_t* out_n, int64_t* out_probe, int64_t* out_scanned,
+              int flags) {
+  if (B < 0) return fail(PK_ERR_USAGE, "negative batch");
+  if (nprobe < 1) return fail(PK_ERR_USAGE, "nprobe must be >= 1");
+  if (nprobe > 2048) return fail(PK_ERR_USAGE, "nprobe %d above the device limit 2048", nprobe);
+  if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
+  if (nscopes < 1 || nscopes > 64) return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
+  if (B == 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  const bool dev = flags & PK_DEVICE_PTRS;
+  cudaStream_t st = ix->st;
+  RET(ix->sync_table());
+  const int64_t dp = ix->dp;
+  const int32_t ns = std::max<int32_t>(ix->nslots, 1);
+  // scratch
+  const bool fresh_q = ix->q.bytes < (size_t)B * dp * 4;
+  RET(ix->q.ensure((size_t)B * dp * 4));
+  if (fresh_q) CK(cudaMemsetAsync(ix->q.p, 0, ix->q.bytes, st));  // zero pad columns once
+  RET(ix->qnorm.ensure(B * 4));
+  RET(ix->dc.ensure((size_t)B * ns * 4));
+  RET(ix->probe.ensure((size_t)B * nprobe * 4));
+  RET(ix->probe_key.ensure((size_t)B * nprobe * 4));
+  RET(ix->counts.ensure((size_t)ns * 4));
+  RET(ix->fillb.ensure((size_t)(2 * ns + B * nprobe) * 4));
+  int64_t maxlen = 0;
+  for (int32_t s = 0; s < ix->nslots; s++)
+    if (ix->h_cid[s] >= 0) maxlen = std::max(maxlen, ix->h_len[s]);
+  const int64_t max_nch = std::max<int64_t>(1, (maxlen + ix->chunk_rows - 1) / ix->chunk_rows);
+  const int64_t max_items = B * nprobe * max_nch;
+  RET(ix->items.ensure((size_t)max_items * sizeof(ScanItem)));
+  RET(ix->nitems.ensure(8));
+  RET(ix->qpairs.ensure((size_t)B * nprobe * sizeof(QPair)));
+  RET(ix->slot_off.ensure((size_t)(B + 1) * 4));
+  RET(ix->scanned.ensure((size_t)B * 8));
+  RET(ix->cand_key.ensure((size_t)max_items * kk * 4));
+  RET(ix->cand_id.ensure((size_t)max_items * kk * 8));
+  RET(ix->cand_n.ensure((size_t)max_items * 4));
+  RET(ix->cand_list.ensure((size_t)max_items * 4));
+  RET(ix->work.ensure(8));
+  RET(ix->scopes.ensure(64 * 4));
+  // inputs
+  CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
+                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  const ListTable lt = ix->table();
+  if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
+  // 1. coarse quantizer: exact distances to every list centroid, select top-nprobe in scope
+  launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
+                    ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
+  launch_coarse_select(ix->dc.as<float>(), ns, (int)B, lt, ix->scopes.as<int32_t>(), nscopes,
+                       nprobe, ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), st);
+  // 2. route (query -> lists) into (list -> queries) work items
+  CK(cudaMemsetAsync(ix->counts.p, 0, (size_t)ns * 4, st));
+  launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt, ix->chunk_rows, ix->counts.as<int32_t>(),
+               ix->fillb.as<int32_t>(), ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
+               ix->qpairs.as<QPair>(), ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
+  // 3. fused scan + per-(query, list chunk) top-kk
+  CK(cudaMemsetAsync(ix->work.p, 0, 8, st));
+  launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
+              ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(), (int)std::min<int64_t>(max_items, INT32_MAX),
+              ix->qpairs.as<QPair>(), kk, ix->work.as<int32_t>(), ix->cand_key.as<uint32_t>(),
+              ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
+              ix->num_sms, st);
+  // 4. merge per query
+  int64_t* o_ids = out_ids;
+  float* o_d = out_dists;
+  int64_t* o_cid = out_cids;
+  int32_t* o_n = out_n;
+  if (!dev) {
+    RET(ix->out_ids.ensure((size_t)B * kk * 8));
+    RET(ix->out_d.ensure((size_t)B * kk * 4));
+    RET(ix->out_cid.ensure((size_t)B * kk * 8));
+    RET(ix->out_n.ensure((size_t)B * 4));
+    o_ids = ix->out_ids.as<int64_t>();
+    o_d = ix->out_d.as<float>();
+    o_cid = ix->out_cid.as<int64_t>();
+    o_n = ix->out_n.as<int32_t>();
+  }
+  launch_merge((int)B, ix->slot_off.as<int32_t>(), ix->cand_key.as<uint32_t>(),
+               ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(), kk,
+               lt, o_ids, o_d, o_cid, o_n, st);
+  CK(cudaGetLastError());
+  if (!dev) {
+    CK(cudaMemcpyAsync(out_ids, o_ids, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_dists, o_d, (size_t)B * kk * 4, cudaMemcpyDeviceToHost, st));
+    if (out_cids) CK(cudaMemcpyAsync(out_cids, o_cid, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_n, o_n, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+    if (out_scanned)
+      CK(cudaMemcpyAsync(out_scanned, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+  } else if (out_scanned) {
+    CK(cudaMemcpyAsync(out_scanned, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  if (out_probe) {
+    // probe slots -> cids (host mirror); forces a sync
+    std::vector<int32_t> ps((size_t)B * nprobe);
+    CK(cudaMemcpyAsync(ps.data(), ix->probe.p, ps.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int64_t> pc(ps.size());
+    for (size_t i = 0; i < ps.size(); i++) pc[i] = ps[i] >= 0 ? ix->h_cid[ps[i]] : -1;
+    CK(cudaMemcpyAsync(out_probe, pc.data(), pc.size() * 8,
+                       dev ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost, st));
+  }
+  if (!dev || out_probe) CK(cudaStreamSynchronize(st));
+  return PK_OK;
+}
+
+int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
+              float* out_dist, int flags) {
+  if (n < 0) return fail(PK_ERR_USAGE, "negative count");
+  if (n == 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  const bool dev = flags & PK_DEVICE_PTRS;
+  cudaStream_t st = ix->st;
+  RET(ix->sync_table());
+  const int64_t dp = ix->dp;
+  const int32_t ns = std::max<int32_t>(ix->nslots, 1);
+  const bool fresh_q = ix->q.bytes < (size_t)n * dp * 4;
+  RET(ix->q.ensure((size_t)n * dp * 4));
+  if (fresh_q) CK(cudaMemsetAsync(ix->q.p, 0, ix->q.bytes, st));
+  RET(ix->qnorm.ensure(n * 4));
+  RET(ix->dc.ensure((size_t)n * ns * 4));
+  RET(ix->assign_c.ensure(n * 8));
+  RET(ix->assign_d.ensure(n * 4));
+  CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, X, ix->d * 4, ix->d * 4, n,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)n, (int)ix->d, ix->qnorm.as<float>(), st);
+  launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)n, ix->d_cent, dp, ix->nslots, (int)dp,
+                    ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
+  int64_t* oc = dev ? out_cid : ix->assign_c.as<int64_t>();
+  float* od = dev ? out_dist : ix->assign_d.as<float>();
+  launch_argmin(ix->dc.as<float>(), ns, (int)n, ix->table(), scope_code, oc, od, st);
+  CK(cudaGetLastError());
+  if (!dev) {
+    CK(cudaMemcpyAsync(out_cid, oc, n * 8, cudaMemcpyDeviceToHost, st));
+    if (out_dist) CK(cudaMemcpyAsync(out_dist, od, n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  return PK_OK;
+}
+
+}  // extern "C"

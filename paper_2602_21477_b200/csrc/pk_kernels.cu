@@ -1,0 +1,1096 @@
+// pk_kernels.cu -- sm_100a kernels of the IVF search hot path.
+//
+// Reference arithmetic: every distance below reproduces the
+// reference numba kernels bit for bit -- ref/kernels.py:73-83 (sq_l2),
+// :86-95 (neg_ip), :98-113 (cosine), :116-135 (kmeans_assign) -- fp32, j
+// ascending, each op rounded, no FMA.  Rows are zero-padded to dp (a multiple
+// of 32 floats); the padded terms add exactly +0 at the END of the sum, which
+// leaves every result unchanged.
+//
+// Ordering everywhere is np.lexsort((ids, dists)) (ref/engine.py:411) and the
+// coarse emit order (d, cid) (ref/graph.py:395): a monotone u32 key of the
+// float, then the int64 id.
+#include "pk_kernels.h"
+#include "pk_ptx.cuh"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace pk {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+template <int METRIC>
+__device__ __forceinline__ float finalize(float acc, float nn, float qn) {
+  if (METRIC == SQ_L2) return acc;
+  if (METRIC == IP) return -acc;
+  // cosine_nb: 1 - dot / (sqrt(nn) * qn), all fp32 (ref/kernels.py:112)
+  return __fsub_rn(1.0f, __fdiv_rn(acc, __fmul_rn(__fsqrt_rn(nn), qn)));
+}
+
+template <int METRIC>
+__device__ __forceinline__ float step4(float acc, float4 x, float4 q) {
+  if (METRIC == SQ_L2) {
+    acc = sq_step(acc, x.x, q.x);
+    acc = sq_step(acc, x.y, q.y);
+    acc = sq_step(acc, x.z, q.z);
+    acc = sq_step(acc, x.w, q.w);
+  } else {
+    acc = ip_step(acc, x.x, q.x);
+    acc = ip_step(acc, x.y, q.y);
+    acc = ip_step(acc, x.z, q.z);
+    acc = ip_step(acc, x.w, q.w);
+  }
+  return acc;
+}
+
+// =====================================================================
+// Dense distance matrix  D[b][r] = dist(Q[b], X[r])   (batch_distances,
+// ref/core.py:98-109).  Used by the coarse quantizer over the centroid table,
+// by assign_nearest and by the kernel-table entry points.
+// =====================================================================
+template <int METRIC, int NQ>
+__global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict__ Q, int64_t ldq,
+                                                         int B, const float* __restrict__ X,
+                                                         int64_t ldx, int64_t n, int dp,
+                                                         const float* __restrict__ qnorm,
+                                                         float* __restrict__ D, int64_t ldd) {
+  extern __shared__ float4 qs4[];  // [NQ][dp/4]
+  const float* qs = reinterpret_cast<const float*>(qs4);
+  const int b0 = blockIdx.y * NQ;
+  const int nq = min(NQ, B - b0);
+  const int dp4 = dp / 4;
+  for (int i = threadIdx.x; i < NQ * dp4; i += blockDim.x) {
+    int a = i / dp4, j4 = i - a * dp4;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (a < nq) v = *reinterpret_cast<const float4*>(Q + (int64_t)(b0 + a) * ldq + 4 * j4);
+    qs4[i] = v;
+  }
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = r < n;
+  const float* xr = X + (valid ? r : 0) * ldx;
+  float acc[NQ];
+#pragma unroll
+  for (int a = 0; a < NQ; a++) acc[a] = 0.f;
+  float nn = 0.f;
+  for (int j = 0; j < dp; j += 4) {
+    float4 x = __ldg(reinterpret_cast<const float4*>(xr + j));
+#pragma unroll
+    for (int a = 0; a < NQ; a++) {
+      float4 q = *reinterpret_cast<const float4*>(qs + a * dp + j);
+      acc[a] = step4<METRIC>(acc[a], x, q);
+    }
+    if (METRIC == COSINE) nn = step4<IP>(nn, x, x);
+  }
+  if (!valid) return;
+#pragma unroll
+  for (int a = 0; a < NQ; a++) {
+    if (a < nq) {
+      float qn = (METRIC == COSINE) ? qnorm[b0 + a] : 0.f;
+      D[(int64_t)(b0 + a) * ldd + r] = finalize<METRIC>(acc[a], nn, qn);
+    }
+  }
+}
+
+template <int METRIC>
+static void dist_dense_dispatch(const float* Q, int64_t ldq, int B, const float* X, int64_t ldx,
+                                int64_t n, int dp, const float* qnorm, float* D, int64_t ldd,
+                                cudaStream_t st) {
+  if (B <= 0 || n <= 0) return;
+  int nq = B >= 16 ? 16 : (B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1)));
+  while (nq > 1 && (size_t)nq * dp * 4 > 96 * 1024) nq >>= 1;
+  size_t smem = (size_t)nq * dp * 4;
+  dim3 grid((unsigned)((n + 127) / 128), (unsigned)((B + nq - 1) / nq));
+#define PK_DD(NQV)                                                                                  \
+  case NQV: {                                                                                       \
+    auto k = dist_dense_kernel<METRIC, NQV>;                                                        \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                \
+    k<<<grid, 128, smem, st>>>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd);                            \
+  } break;
+  switch (nq) {
+    PK_DD(1) PK_DD(2) PK_DD(4) PK_DD(8) PK_DD(16)
+  }
+#undef PK_DD
+}
+
+void launch_dist_dense(int metric, const float* Q, int64_t ldq, int B, const float* X, int64_t ldx,
+                       int64_t n, int dp, const float* qnorm, float* D, int64_t ldd,
+                       cudaStream_t st) {
+  if (metric == SQ_L2) dist_dense_dispatch<SQ_L2>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, st);
+  else if (metric == IP) dist_dense_dispatch<IP>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, st);
+  else dist_dense_dispatch<COSINE>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, st);
+}
+
+// =====================================================================
+// kmeans_assign (ref/kernels.py:116-135): t = x - c in fp32, t*t in fp32,
+// sum in fp64 ascending j, strict '<' (first centroid wins ties).
+// One thread per point; centroids stream through shared memory in groups.
+// =====================================================================
+constexpr int KM_G = 8;
+__global__ void __launch_bounds__(128) kmeans_assign_kernel(const float* __restrict__ X, int64_t ldx,
+                                                            int64_t n, const float* __restrict__ C,
+                                                            int64_t ldc, int64_t k, int dp,
+                                                            int64_t* __restrict__ labels,
+                                                            double* __restrict__ dists) {
+  extern __shared__ float4 cs4[];  // [KM_G][dp/4]
+  const float* cs = reinterpret_cast<const float*>(cs4);
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = r < n;
+  const float* xr = X + (valid ? r : 0) * ldx;
+  const int dp4 = dp / 4;
+  double best = 1e300;
+  int64_t arg = 0;
+  for (int64_t c0 = 0; c0 < k; c0 += KM_G) {
+    const int g = (int)(k - c0 < KM_G ? k - c0 : KM_G);
+    __syncthreads();
+    for (int i = threadIdx.x; i < KM_G * dp4; i += blockDim.x) {
+      int a = i / dp4, j4 = i - a * dp4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a < g) v = *reinterpret_cast<const float4*>(C + (c0 + a) * ldc + 4 * j4);
+      cs4[i] = v;
+    }
+    __syncthreads();
+    double acc[KM_G];
+#pragma unroll
+    for (int a = 0; a < KM_G; a++) acc[a] = 0.0;
+    for (int j = 0; j < dp; j += 4) {
+      float4 x = __ldg(reinterpret_cast<const float4*>(xr + j));
+#pragma unroll
+      for (int a = 0; a < KM_G; a++) {
+        float4 c = *reinterpret_cast<const float4*>(cs + a * dp + j);
+        float t;
+        t = __fsub_rn(x.x, c.x); acc[a] = __dadd_rn(acc[a], (double)__fmul_rn(t, t));
+        t = __fsub_rn(x.y, c.y); acc[a] = __dadd_rn(acc[a], (double)__fmul_rn(t, t));
+        t = __fsub_rn(x.z, c.z); acc[a] = __dadd_rn(acc[a], (double)__fmul_rn(t, t));
+        t = __fsub_rn(x.w, c.w); acc[a] = __dadd_rn(acc[a], (double)__fmul_rn(t, t));
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < KM_G; a++) {
+      if (a < g && acc[a] < best) {
+        best = acc[a];
+        arg = c0 + a;
+      }
+    }
+  }
+  if (valid) {
+    labels[r] = arg;
+    dists[r] = best;
+  }
+}
+
+void launch_kmeans_assign(const float* X, int64_t ldx, int64_t n, const float* C, int64_t ldc,
+                          int64_t k, int dp, int64_t* labels, double* dists, cudaStream_t st) {
+  if (n <= 0) return;
+  size_t smem = (size_t)KM_G * dp * 4;
+  cudaFuncSetAttribute(kmeans_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  kmeans_assign_kernel<<<(unsigned)((n + 127) / 128), 128, smem, st>>>(X, ldx, n, C, ldc, k, dp,
+                                                                      labels, dists);
+}
+
+// qn = sqrt(sum_j q_j * q_j) in fp32, j ascending (ref/kernels.py:101-104).
+__global__ void qnorm_kernel(const float* __restrict__ Q, int64_t ldq, int B, int d,
+                             float* __restrict__ qnorm) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const float* q = Q + (int64_t)b * ldq;
+  float acc = 0.f;
+  for (int j = 0; j < d; j++) acc = ip_step(acc, q[j], q[j]);
+  qnorm[b] = __fsqrt_rn(acc);
+}
+void launch_qnorm(const float* Q, int64_t ldq, int B, int d, float* qnorm, cudaStream_t st) {
+  if (B <= 0) return;
+  qnorm_kernel<<<(B + 127) / 128, 128, 0, st>>>(Q, ldq, B, d, qnorm);
+}
+
+// centroid (ref/core.py:112-117): column sums in fp64 in row order, / n, -> f32.
+__global__ void centroid_kernel(const float* __restrict__ rows, int64_t ldr, int64_t n, int dp,
+                                float* __restrict__ out) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= dp) return;
+  double s = 0.0;
+  for (int64_t i = 0; i < n; i++) s = __dadd_rn(s, (double)rows[i * ldr + j]);
+  out[j] = (float)__ddiv_rn(s, (double)n);
+}
+void launch_centroid(const float* rows, int64_t ldr, int64_t n, int dp, float* cent_out,
+                     cudaStream_t st) {
+  if (n <= 0) return;
+  centroid_kernel<<<(dp + 127) / 128, 128, 0, st>>>(rows, ldr, n, dp, cent_out);
+}
+
+// =====================================================================
+// CTA-level sort / select over (key u32, id i64, payload i32) entries.
+// =====================================================================
+struct Entry {
+  uint32_t key;
+  int32_t pay;
+  int64_t id;
+};
+__device__ __forceinline__ bool e_less(const Entry& a, const Entry& b) {
+  return lex_less(a.key, a.id, b.key, b.id);
+}
+__device__ __forceinline__ Entry e_none() {
+  Entry e;
+  e.key = KEY_NONE;
+  e.pay = -1;
+  e.id = ID_NONE;
+  return e;
+}
+
+// Sort buf[0..n) ascending; pads to a power of two with sentinels (cap >= pow2(n)).
+__device__ void cta_bitonic_sort(Entry* buf, int n) {
+  int N = 1;
+  while (N < n) N <<= 1;
+  for (int i = n + threadIdx.x; i < N; i += blockDim.x) buf[i] = e_none();
+  __syncthreads();
+  for (int k = 2; k <= N; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < N; i += blockDim.x) {
+        int ixj = i ^ j;
+        if (ixj > i) {
+          Entry a = buf[i], b = buf[ixj];
+          bool up = (i & k) == 0;
+          if (e_less(b, a) == up) {
+            buf[i] = b;
+            buf[ixj] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Keep the first `kk` entries of a sorted buffer, optionally dropping
+// duplicate (key, id) entries (first occurrence per id, ref/engine.py:414-418).
+// Returns the kept count (thread 0 compacts; result broadcast).
+__device__ int cta_compact_sorted(Entry* buf, int n, int kk, bool dedup, int* s_cnt) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int w = 0;
+    for (int i = 0; i < n && w < kk; i++) {
+      if (dedup && w > 0 && buf[i].id == buf[w - 1].id && buf[i].key == buf[w - 1].key) continue;
+      buf[w++] = buf[i];
+    }
+    *s_cnt = w;
+  }
+  __syncthreads();
+  return *s_cnt;
+}
+
+constexpr int SEL_CAP = 4096;
+
+// Coarse quantizer select: per query the first nprobe in-scope lists by
+// (dist, cid) -- HybridGraphIndex.search emit order at exhaustive ef
+// (ref/graph.py:392-396).  Lists with no members still count
+// (the reference graph keeps emptied clusters).
+__global__ void __launch_bounds__(256) coarse_select_kernel(const float* __restrict__ Dc,
+                                                            int64_t ldd, ListTable lt,
+                                                            const int32_t* __restrict__ scope_codes,
+                                                            int nscopes, int nprobe,
+                                                            int32_t* __restrict__ probe,
+                                                            uint32_t* __restrict__ probe_key) {
+  extern __shared__ Entry sel_buf[];  // [SEL_CAP]
+  __shared__ int s_cnt;
+  __shared__ int s_codes[64];
+  const int b = blockIdx.x;
+  if (threadIdx.x < 64) s_codes[threadIdx.x] = threadIdx.x < nscopes ? scope_codes[threadIdx.x] : -1;
+  __syncthreads();
+  const float* drow = Dc + (int64_t)b * ldd;
+  int kept = 0;
+  Entry tau = e_none();
+  for (int base = 0; base < lt.nslots; base += SEL_CAP - nprobe) {
+    const int end = min(lt.nslots, base + SEL_CAP - nprobe);
+    if (threadIdx.x == 0) s_cnt = kept;
+    __syncthreads();
+    for (int s = base + threadIdx.x; s < end; s += blockDim.x) {
+      if (lt.cid[s] < 0) continue;
+      int sc = lt.scope[s];
+      bool in = false;
+      for (int i = 0; i < nscopes; i++) in |= (s_codes[i] == sc);
+      if (!in) continue;
+      Entry e;
+      e.key = f2key(drow[s]);
+      e.id = lt.cid[s];
+      e.pay = s;
+      if (kept == nprobe && !e_less(e, tau)) continue;
+      int pos = atomicAdd(&s_cnt, 1);
+      sel_buf[pos] = e;
+    }
+    __syncthreads();
+    int n = s_cnt;
+    if (n > kept) {
+      cta_bitonic_sort(sel_buf, n);
+      kept = cta_compact_sorted(sel_buf, n, nprobe, false, &s_cnt);
+      if (kept == nprobe) tau = sel_buf[nprobe - 1];
+    }
+    __syncthreads();
+  }
+  for (int p = threadIdx.x; p < nprobe; p += blockDim.x) {
+    probe[(int64_t)b * nprobe + p] = p < kept ? sel_buf[p].pay : -1;
+    if (probe_key) probe_key[(int64_t)b * nprobe + p] = p < kept ? sel_buf[p].key : KEY_NONE;
+  }
+}
+
+void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
+                          const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
+                          uint32_t* probe_key, cudaStream_t st) {
+  if (B <= 0) return;
+  size_t smem = SEL_CAP * sizeof(Entry);
+  cudaFuncSetAttribute(coarse_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  coarse_select_kernel<<<B, 256, smem, st>>>(Dc, ldd, lt, scope_codes, nscopes, nprobe, probe,
+                                             probe_key);
+}
+
+// =====================================================================
+// Routing: invert (query -> probed lists) into (list -> queries), cut each
+// probed list into row chunks x query groups (the scan work items), and give
+// every (query, list chunk) an output slot.  Single CTA; B*nprobe is small.
+// =====================================================================
+__device__ __forceinline__ int nchunks_of(int64_t len, int chunk) {
+  return (int)((len + chunk - 1) / chunk);
+}
+
+// Block-wide exclusive scan of v (blockDim.x == 1024); returns prefix, *total.
+__device__ int block_exscan(int v, int* s_tmp, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_tmp[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s_tmp[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    s_tmp[lane] = w;
+  }
+  __syncthreads();
+  int pre = (warp > 0 ? s_tmp[warp - 1] : 0) + x - v;
+  *total = s_tmp[31];
+  __syncthreads();
+  return pre;
+}
+
+__global__ void __launch_bounds__(1024) route_kernel(const int32_t* __restrict__ probe, int B,
+                                                     int nprobe, ListTable lt, int chunk_rows,
+                                                     int32_t* __restrict__ counts,
+                                                     int32_t* __restrict__ fill,
+                                                     int32_t* __restrict__ item_off,
+                                                     int32_t* __restrict__ pair_slot,
+                                                     ScanItem* __restrict__ items,
+                                                     int32_t* __restrict__ n_items,
+                                                     QPair* __restrict__ qpairs,
+                                                     int32_t* __restrict__ slot_off,
+                                                     int64_t* __restrict__ scanned) {
+  __shared__ int s_tmp[32];
+  const int npairs = B * nprobe;
+  // 1. per-list query counts
+  for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
+    int s = probe[i];
+    if (s >= 0) atomicAdd(&counts[s], 1);
+  }
+  // 2. per-query output slots (row chunks of its probed lists) and scanned rows
+  int carry = 0;
+  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
+    int b = b0 + threadIdx.x;
+    int nsl = 0;
+    int64_t sc = 0;
+    if (b < B) {
+      for (int p = 0; p < nprobe; p++) {
+        int s = probe[(int64_t)b * nprobe + p];
+        int c = 0;
+        if (s >= 0) {
+          int64_t len = lt.len[s];
+          c = nchunks_of(len, chunk_rows);
+          sc += len;
+        }
+        pair_slot[(int64_t)b * nprobe + p] = nsl;  // relative; made absolute below
+        nsl += c;
+      }
+      scanned[b] = sc;
+    }
+    int tot;
+    int pre = block_exscan(nsl, s_tmp, &tot);
+    if (b < B) slot_off[b] = carry + pre;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) slot_off[B] = carry;
+  __syncthreads();
+  // 3. exclusive scans over lists: query offsets (in place in counts -> fill
+  //    keeps the running fill pointer) and item offsets
+  carry = 0;
+  int icarry = 0;
+  for (int s0 = 0; s0 < lt.nslots; s0 += blockDim.x) {
+    int s = s0 + threadIdx.x;
+    int cnt = 0, nit = 0;
+    if (s < lt.nslots) {
+      cnt = counts[s];
+      if (cnt > 0) nit = nchunks_of(lt.len[s], chunk_rows) * ((cnt + QG - 1) / QG);
+    }
+    int tot, itot;
+    int pre = block_exscan(cnt, s_tmp, &tot);
+    int ipre = block_exscan(nit, s_tmp, &itot);
+    if (s < lt.nslots) {
+      fill[s] = carry + pre;  // query offset; advanced atomically in step 4
+      item_off[s] = icarry + ipre;
+      counts[s] = carry + pre;  // keep the base
+    }
+    carry += tot;
+    icarry += itot;
+  }
+  if (threadIdx.x == 0) *n_items = icarry;
+  __syncthreads();
+  // 4. scatter (query, slot base) pairs into per-list ranges
+  for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
+    int s = probe[i];
+    if (s < 0) continue;
+    int b = i / nprobe;
+    int pos = atomicAdd(&fill[s], 1);
+    QPair qp;
+    qp.b = b;
+    qp.slotbase = slot_off[b] + pair_slot[i];
+    qpairs[pos] = qp;
+  }
+  __syncthreads();
+  // 5. emit work items
+  for (int s = threadIdx.x; s < lt.nslots; s += blockDim.x) {
+    int qbase = counts[s];
+    int cnt = fill[s] - qbase;
+    if (cnt <= 0) continue;
+    int64_t len = lt.len[s];
+    int nch = nchunks_of(len, chunk_rows);
+    int ng = (cnt + QG - 1) / QG;
+    int w = item_off[s];
+    for (int c = 0; c < nch; c++) {
+      for (int g = 0; g < ng; g++) {
+        ScanItem it;
+        it.lslot = s;
+        it.row0 = c * chunk_rows;
+        it.nrows = (int)(len - (int64_t)c * chunk_rows < chunk_rows ? len - (int64_t)c * chunk_rows : chunk_rows);
+        it.qoff = qbase + g * QG;
+        it.nq = min(QG, cnt - g * QG);
+        it.chunk = c;
+        it.pad0 = it.pad1 = 0;
+        items[w++] = it;
+      }
+    }
+  }
+}
+
+void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows,
+                  int32_t* scratch_counts, int32_t* scratch_fill, ScanItem* items,
+                  int32_t* n_items, QPair* qpairs, int32_t* slot_off, int64_t* scanned,
+                  cudaStream_t st) {
+  // scratch_counts: [nslots] zeroed; scratch_fill: [2*nslots + B*nprobe]
+  int32_t* fill = scratch_fill;
+  int32_t* item_off = scratch_fill + lt.nslots;
+  int32_t* pair_slot = scratch_fill + 2 * (int64_t)lt.nslots;
+  route_kernel<<<1, 1024, 0, st>>>(probe, B, nprobe, lt, chunk_rows, scratch_counts, fill,
+                                    item_off, pair_slot, items, n_items, qpairs, slot_off,
+                                    scanned);
+}
+
+// =====================================================================
+// The fused posting-list scan (ref/tiering.py:294-328 merged_search ->
+// ref/core.py:98-109 -> ref/kernels.py:73-113, plus the per-list part of
+// _topk ref/engine.py:406-426).
+//
+// Persistent CTA per SM: warp 8 is the TMA producer, warps 0-7 compute.  A
+// work item is (list chunk of <= chunk_rows rows) x (<= QG queries).  Rows
+// stream through a STAGES-deep ring of [TILE rows x DC floats] tiles (TMA
+// 2-D, SWIZZLE_128B), the item's query chunks ride along as 128-byte bulk
+// copies.  Each compute thread owns one row and accumulates all the item's
+// queries exactly; at the end of a tile the distances go to shared memory
+// and each warp merges two queries' survivors into a sorted per-query
+// (key, id) list of kk entries.
+// =====================================================================
+constexpr int NCW = 8;  // compute warps
+constexpr int SCAN_THREADS = (NCW + 1) * 32;
+
+struct ScanLayout {
+  static constexpr size_t X_BYTES = (size_t)STAGES * TILE * DC * 4;
+  static constexpr size_t QC_BYTES = (size_t)STAGES * QG * DC * 4;
+  static constexpr size_t D_BYTES = (size_t)QG * TILE * 4;
+  static constexpr size_t LK_BYTES = (size_t)QG * KKMAX * 4;
+  static constexpr size_t LI_BYTES = (size_t)QG * KKMAX * 8;
+  static constexpr size_t LN_BYTES = 128;
+  static constexpr size_t BAR_BYTES = 256;
+  static constexpr size_t RING_BYTES = 2 * sizeof(ScanItem);
+  static constexpr size_t TOTAL =
+      X_BYTES + QC_BYTES + D_BYTES + LK_BYTES + LI_BYTES + LN_BYTES + BAR_BYTES + RING_BYTES;
+};
+size_t scan_smem_bytes() { return ScanLayout::TOTAL + 1024; }
+
+struct ScanShared {
+  float* X;
+  float* Qc;
+  float* D;
+  uint32_t* Lkey;
+  int64_t* Lid;
+  int32_t* Ln;
+  uint64_t* full;
+  uint64_t* empty;
+  uint64_t* rfull;
+  uint64_t* rempty;
+  ScanItem* ring;
+};
+
+// Accumulate one tile (this thread's row vs NQ queries) over all d-chunks,
+// consuming stages from the ring; writes distances to D[a][row].
+template <int METRIC, int NQ>
+__device__ __forceinline__ void scan_tile(const ScanShared& S, int nchunk_d, int& s, uint32_t& ph,
+                                          int nq, const float* qn_s) {
+  const int row = threadIdx.x;  // 0..TILE-1
+  const int lane = threadIdx.x & 31;
+  const int swz = row & 7;
+  float acc[NQ];
+#pragma unroll
+  for (int a = 0; a < NQ; a++) acc[a] = 0.f;
+  float nn = 0.f;
+  for (int c = 0; c < nchunk_d; c++) {
+    mbar_wait(&S.full[s], ph);
+    const float* xs = S.X + (size_t)s * TILE * DC + row * DC;
+    const float* qs = S.Qc + (size_t)s * QG * DC;
+#pragma unroll
+    for (int k = 0; k < DC / 4; k++) {
+      float4 x = *reinterpret_cast<const float4*>(xs + ((k ^ swz) << 2));
+#pragma unroll
+      for (int a = 0; a < NQ; a++) {
+        float4 q = *reinterpret_cast<const float4*>(qs + a * DC + (k << 2));
+        acc[a] = step4<METRIC>(acc[a], x, q);
+      }
+      if (METRIC == COSINE) nn = step4<IP>(nn, x, x);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (++s == STAGES) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; a++)
+    if (a < nq) S.D[a * TILE + row] = finalize<METRIC>(acc[a], nn, METRIC == COSINE ? qn_s[a] : 0.f);
+}
+
+// 19-comparator sorting network for 8 (key, id) pairs held in registers.
+__device__ __forceinline__ void ce(uint32_t& ka, int64_t& ia, uint32_t& kb, int64_t& ib) {
+  bool sw = lex_less(kb, ib, ka, ia);
+  uint32_t tk = sw ? kb : ka;
+  int64_t ti = sw ? ib : ia;
+  kb = sw ? ka : kb;
+  ib = sw ? ia : ib;
+  ka = tk;
+  ia = ti;
+}
+__device__ __forceinline__ void sort8(uint32_t* k, int64_t* i) {
+#define PK_CE(a, b) ce(k[a], i[a], k[b], i[b])
+  PK_CE(0, 2); PK_CE(1, 3); PK_CE(4, 6); PK_CE(5, 7);
+  PK_CE(0, 4); PK_CE(1, 5); PK_CE(2, 6); PK_CE(3, 7);
+  PK_CE(0, 1); PK_CE(2, 3); PK_CE(4, 5); PK_CE(6, 7);
+  PK_CE(2, 4); PK_CE(3, 5);
+  PK_CE(1, 4); PK_CE(3, 6);
+  PK_CE(1, 2); PK_CE(3, 4); PK_CE(5, 6);
+#undef PK_CE
+}
+
+// Merge this tile's survivors for query a into its sorted list (warp-wide).
+__device__ void topk_merge_tile(const ScanShared& S, int a, int rows, const int64_t* __restrict__ ids,
+                                int64_t idbase, int kk) {
+  const int lane = threadIdx.x & 31;
+  const float* dq = S.D + a * TILE;
+  const int n_old = S.Ln[a];
+  uint32_t tk = KEY_NONE;
+  int64_t ti = ID_NONE;
+  if (n_old == kk) {
+    tk = S.Lkey[a * KKMAX + kk - 1];
+    ti = S.Lid[a * KKMAX + kk - 1];
+  }
+  uint32_t ck[8];
+  int64_t ci[8];
+  bool have = false;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int row = lane + 32 * i;
+    ck[i] = KEY_NONE;
+    ci[i] = ID_NONE;
+    if (row < rows) {
+      uint32_t k = f2key(dq[row]);
+      if (k <= tk) {
+        int64_t id = ids[idbase + row];
+        if (lex_less(k, id, tk, ti)) {
+          ck[i] = k;
+          ci[i] = id;
+          have = true;
+        }
+      }
+    }
+  }
+  if (!__any_sync(FULL, have)) return;
+  sort8(ck, ci);
+  // old list: lane holds entries lane and lane+32
+  uint32_t ok0 = KEY_NONE, ok1 = KEY_NONE;
+  int64_t oi0 = ID_NONE, oi1 = ID_NONE;
+  if (lane < n_old) {
+    ok0 = S.Lkey[a * KKMAX + lane];
+    oi0 = S.Lid[a * KKMAX + lane];
+  }
+  if (lane + 32 < n_old) {
+    ok1 = S.Lkey[a * KKMAX + lane + 32];
+    oi1 = S.Lid[a * KKMAX + lane + 32];
+  }
+  uint32_t nk0 = KEY_NONE, nk1 = KEY_NONE;
+  int64_t ni0 = ID_NONE, ni1 = ID_NONE;
+  int p_old = 0, cnt = 0;
+  for (; cnt < kk; cnt++) {
+    // warp min over lane heads by (key, id)
+    const uint32_t m = __reduce_min_sync(FULL, ck[0]);
+    const unsigned tie = __ballot_sync(FULL, ck[0] == m);
+    int wl;
+    int64_t wid;
+    if (__popc(tie) == 1) {
+      wl = __ffs(tie) - 1;
+      wid = __shfl_sync(FULL, ci[0], wl);
+    } else {
+      const int64_t my = (ck[0] == m) ? ci[0] : ID_NONE;
+      const uint32_t hi = (uint32_t)((uint64_t)my >> 32) ^ 0x80000000u;
+      const uint32_t mhi = __reduce_min_sync(FULL, hi);
+      const uint32_t lo = (hi == mhi) ? (uint32_t)(uint64_t)my : 0xffffffffu;
+      const uint32_t mlo = __reduce_min_sync(FULL, lo);
+      const unsigned w = __ballot_sync(FULL, ck[0] == m && hi == mhi && lo == mlo);
+      wl = __ffs(w) - 1;
+      wid = (int64_t)(((uint64_t)(mhi ^ 0x80000000u) << 32) | (uint64_t)mlo);
+    }
+    // old-list head
+    uint32_t hk = KEY_NONE;
+    int64_t hid = ID_NONE;
+    if (p_old < n_old) {
+      const int src = p_old & 31;
+      const bool second = p_old >= 32;
+      hk = __shfl_sync(FULL, second ? ok1 : ok0, src);
+      hid = __shfl_sync(FULL, second ? oi1 : oi0, src);
+    }
+    uint32_t sk;
+    int64_t si;
+    if (lex_less(hk, hid, m, wid)) {
+      sk = hk;
+      si = hid;
+      p_old++;
+    } else {
+      sk = m;
+      si = wid;
+      if (lane == wl) {
+#pragma unroll
+        for (int i = 0; i < 7; i++) {
+          ck[i] = ck[i + 1];
+          ci[i] = ci[i + 1];
+        }
+        ck[7] = KEY_NONE;
+        ci[7] = ID_NONE;
+      }
+    }
+    if (sk == KEY_NONE && si == ID_NONE) break;
+    if (lane == (cnt & 31)) {
+      if (cnt < 32) {
+        nk0 = sk;
+        ni0 = si;
+      } else {
+        nk1 = sk;
+        ni1 = si;
+      }
+    }
+  }
+  if (lane < cnt) {
+    S.Lkey[a * KKMAX + lane] = nk0;
+    S.Lid[a * KKMAX + lane] = ni0;
+  }
+  if (lane + 32 < cnt) {
+    S.Lkey[a * KKMAX + lane + 32] = nk1;
+    S.Lid[a * KKMAX + lane + 32] = ni1;
+  }
+  __syncwarp();
+  if (lane == 0) S.Ln[a] = cnt;
+  __syncwarp();
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(SCAN_THREADS, 1)
+    scan_kernel(const __grid_constant__ ArenaMaps maps, ListTable lt, const float* __restrict__ Qd,
+                const float* __restrict__ qnorm, const ScanItem* __restrict__ items,
+                const int32_t* __restrict__ n_items_p, const QPair* __restrict__ qpairs, int kk,
+                int32_t* __restrict__ work_ctr, uint32_t* __restrict__ cand_key,
+                int64_t* __restrict__ cand_id, int32_t* __restrict__ cand_n,
+                int32_t* __restrict__ cand_list) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment for SWIZZLE_128B; index off the __shared__ array so the
+  // compiler keeps shared-space (LDS) addressing.
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  ScanShared S;
+  S.X = reinterpret_cast<float*>(base);
+  S.Qc = reinterpret_cast<float*>(base + ScanLayout::X_BYTES);
+  S.D = reinterpret_cast<float*>(base + ScanLayout::X_BYTES + ScanLayout::QC_BYTES);
+  uint8_t* p = base + ScanLayout::X_BYTES + ScanLayout::QC_BYTES + ScanLayout::D_BYTES;
+  S.Lkey = reinterpret_cast<uint32_t*>(p);
+  p += ScanLayout::LK_BYTES;
+  S.Lid = reinterpret_cast<int64_t*>(p);
+  p += ScanLayout::LI_BYTES;
+  S.Ln = reinterpret_cast<int32_t*>(p);
+  p += ScanLayout::LN_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p);
+  S.full = bars;
+  S.empty = bars + STAGES;
+  S.rfull = bars + 2 * STAGES;
+  S.rempty = bars + 2 * STAGES + 2;
+  p += ScanLayout::BAR_BYTES;
+  S.ring = reinterpret_cast<ScanItem*>(p);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; i++) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], NCW);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&S.rfull[i], 1);
+      mbar_init(&S.rempty[i], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunk_d = lt.dp / DC;
+  const int n_items = *n_items_p;
+
+  if (warp == NCW) {
+    // ------------------------------------------------ producer warp
+    if (lane == 0)
+      for (int i = 0; i < NBOX; i++) tma_prefetch_desc(&maps.box[i]);
+    const uint64_t pol = policy_evict_first();
+    int s = 0, r = 0;
+    uint32_t ph = 0, rph = 0;
+    for (;;) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(work_ctr, 1);
+      it = __shfl_sync(FULL, it, 0);
+      ScanItem item;
+      if (it < n_items) {
+        item = items[it];
+      } else {
+        item.nq = -1;
+      }
+      mbar_wait(&S.rempty[r], rph ^ 1);
+      if (lane == 0) {
+        S.ring[r] = item;
+        mbar_arrive(&S.rfull[r]);
+      }
+      if (++r == 2) {
+        r = 0;
+        rph ^= 1;
+      }
+      if (item.nq < 0) break;
+      const int64_t rbase = lt.off[item.lslot] + item.row0;
+      const int qb = lane < item.nq ? qpairs[item.qoff + lane].b : 0;
+      const float* qrow = Qd + (int64_t)qb * lt.dp;
+      for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+        const int rows = min(TILE, item.nrows - t0);
+        const int rows8 = (rows + 7) & ~7;
+        const uint32_t bytes = (uint32_t)(rows8 * DC * 4 + item.nq * DC * 4);
+        for (int c = 0; c < nchunk_d; c++) {
+          mbar_wait(&S.empty[s], ph ^ 1);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&S.full[s], bytes);
+            int r0 = 0;
+#pragma unroll
+            for (int bi = 0; bi < NBOX; bi++) {
+              const int h = TILE >> bi;
+              if (rows8 - r0 >= h) {
+                tma_load_2d(S.X + (size_t)s * TILE * DC + r0 * DC, &maps.box[bi], &S.full[s],
+                            c * DC, (int)(rbase + t0 + r0), pol);
+                r0 += h;
+              }
+            }
+          }
+          __syncwarp();
+          if (lane < item.nq)
+            bulk_g2s(S.Qc + (size_t)s * QG * DC + lane * DC, qrow + c * DC, DC * 4, &S.full[s]);
+          if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- compute warps
+  __shared__ float qn_s[QG];
+  int s = 0, r = 0;
+  uint32_t ph = 0, rph = 0;
+  for (;;) {
+    mbar_wait(&S.rfull[r], rph);
+    const ScanItem item = S.ring[r];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.rempty[r]);
+    if (++r == 2) {
+      r = 0;
+      rph ^= 1;
+    }
+    if (item.nq < 0) break;
+    const int qa0 = warp, qa1 = warp + NCW;
+    if (lane == 0) {
+      S.Ln[qa0] = 0;
+      S.Ln[qa1] = 0;
+    }
+    if (METRIC == COSINE && threadIdx.x < QG)
+      qn_s[threadIdx.x] = threadIdx.x < item.nq ? qnorm[qpairs[item.qoff + threadIdx.x].b] : 0.f;
+    named_bar_sync(1, NCW * 32);  // Ln reset + qn_s visible
+    const int64_t idbase0 = lt.off[item.lslot] + item.row0;
+    for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+      const int rows = min(TILE, item.nrows - t0);
+      const int nq = item.nq;
+      if (nq <= 1) scan_tile<METRIC, 1>(S, nchunk_d, s, ph, nq, qn_s);
+      else if (nq <= 2) scan_tile<METRIC, 2>(S, nchunk_d, s, ph, nq, qn_s);
+      else if (nq <= 4) scan_tile<METRIC, 4>(S, nchunk_d, s, ph, nq, qn_s);
+      else if (nq <= 6) scan_tile<METRIC, 6>(S, nchunk_d, s, ph, nq, qn_s);
+      else if (nq <= 8) scan_tile<METRIC, 8>(S, nchunk_d, s, ph, nq, qn_s);
+      else if (nq <= 12) scan_tile<METRIC, 12>(S, nchunk_d, s, ph, nq, qn_s);
+      else scan_tile<METRIC, 16>(S, nchunk_d, s, ph, nq, qn_s);
+      named_bar_sync(1, NCW * 32);
+      if (qa0 < nq) topk_merge_tile(S, qa0, rows, lt.ids, idbase0 + t0, kk);
+      if (qa1 < nq) topk_merge_tile(S, qa1, rows, lt.ids, idbase0 + t0, kk);
+      named_bar_sync(1, NCW * 32);
+    }
+    // write this item's per-query lists to their output slots
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int a = h ? qa1 : qa0;
+      if (a >= item.nq) continue;
+      const QPair qp = qpairs[item.qoff + a];
+      const int64_t slot = (int64_t)qp.slotbase + item.chunk;
+      const int n = S.Ln[a];
+      for (int l = lane; l < n; l += 32) {
+        cand_key[slot * kk + l] = S.Lkey[a * KKMAX + l];
+        cand_id[slot * kk + l] = S.Lid[a * KKMAX + l];
+      }
+      if (lane == 0) {
+        cand_n[slot] = n;
+        cand_list[slot] = item.lslot;
+      }
+    }
+  }
+}
+
+void launch_scan(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
+                 const float* qnorm, const ScanItem* items, const int32_t* n_items,
+                 int max_items, const QPair* qpairs, int kk, int32_t* work_ctr,
+                 uint32_t* cand_key, int64_t* cand_id, int32_t* cand_n, int32_t* cand_list,
+                 int num_sms, cudaStream_t st) {
+  if (max_items <= 0) return;
+  size_t smem = scan_smem_bytes();
+  int grid = std::min(num_sms, max_items);
+#define PK_SCAN(M)                                                                                \
+  {                                                                                               \
+    auto k = scan_kernel<M>;                                                                      \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+    k<<<grid, SCAN_THREADS, smem, st>>>(maps, lt, Qd, qnorm, items, n_items, qpairs, kk, work_ctr, \
+                                        cand_key, cand_id, cand_n, cand_list);                    \
+  }
+  if (metric == SQ_L2) PK_SCAN(SQ_L2)
+  else if (metric == IP) PK_SCAN(IP)
+  else PK_SCAN(COSINE)
+#undef PK_SCAN
+}
+
+// =====================================================================
+// Final merge per query: its candidate slots -> top kk by (dist, id),
+// first occurrence per id (ref/engine.py:406-426).
+// =====================================================================
+constexpr int MERGE_CAP = 2048;
+__global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ slot_off,
+                                                    const uint32_t* __restrict__ cand_key,
+                                                    const int64_t* __restrict__ cand_id,
+                                                    const int32_t* __restrict__ cand_n,
+                                                    const int32_t* __restrict__ cand_list, int kk,
+                                                    ListTable lt, int64_t* __restrict__ out_ids,
+                                                    float* __restrict__ out_d,
+                                                    int64_t* __restrict__ out_cid,
+                                                    int32_t* __restrict__ out_n) {
+  extern __shared__ Entry mbuf[];  // [MERGE_CAP]
+  __shared__ int s_cnt;
+  __shared__ uint32_t s_tk[4];
+  __shared__ int64_t s_ti[4];
+  const int b = blockIdx.x;
+  const int so = slot_off[b], eo = slot_off[b + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // tau: best "last entry" among full slots (each full slot has kk distinct ids <= it)
+  uint32_t tk = KEY_NONE;
+  int64_t ti = ID_NONE;
+  for (int sl = so + threadIdx.x; sl < eo; sl += blockDim.x) {
+    if (cand_n[sl] == kk) {
+      uint32_t k = cand_key[(int64_t)sl * kk + kk - 1];
+      int64_t i = cand_id[(int64_t)sl * kk + kk - 1];
+      if (lex_less(k, i, tk, ti)) {
+        tk = k;
+        ti = i;
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint32_t k2 = __shfl_xor_sync(FULL, tk, o);
+    int64_t i2 = __shfl_xor_sync(FULL, ti, o);
+    if (lex_less(k2, i2, tk, ti)) {
+      tk = k2;
+      ti = i2;
+    }
+  }
+  if (lane == 0) {
+    s_tk[warp] = tk;
+    s_ti[warp] = ti;
+  }
+  __syncthreads();
+  tk = s_tk[0];
+  ti = s_ti[0];
+  for (int w = 1; w < 4; w++)
+    if (lex_less(s_tk[w], s_ti[w], tk, ti)) {
+      tk = s_tk[w];
+      ti = s_ti[w];
+    }
+  // collect survivors (<= tau) slot group by slot group, keeping the best kk
+  const int group = max(1, (MERGE_CAP - kk) / kk);
+  int kept = 0;
+  for (int g0 = so; g0 < eo; g0 += group) {
+    const int g1 = min(eo, g0 + group);
+    if (threadIdx.x == 0) s_cnt = kept;
+    __syncthreads();
+    for (int sl = g0 + threadIdx.x; sl < g1; sl += blockDim.x) {
+      const int n = cand_n[sl];
+      const int lst = cand_list[sl];
+      for (int e = 0; e < n; e++) {
+        const uint32_t k = cand_key[(int64_t)sl * kk + e];
+        const int64_t i = cand_id[(int64_t)sl * kk + e];
+        if (lex_less(tk, ti, k, i)) break;  // slot lists are sorted
+        int pos = atomicAdd(&s_cnt, 1);
+        Entry en;
+        en.key = k;
+        en.id = i;
+        en.pay = lst;
+        mbuf[pos] = en;
+      }
+    }
+    __syncthreads();
+    const int n = s_cnt;
+    if (n > kept || g0 == so) {
+      cta_bitonic_sort(mbuf, n);
+      kept = cta_compact_sorted(mbuf, n, kk, true, &s_cnt);
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+    const int64_t o = (int64_t)b * kk + i;
+    if (i < kept) {
+      out_ids[o] = mbuf[i].id;
+      out_d[o] = key2f(mbuf[i].key);
+      if (out_cid) out_cid[o] = lt.cid[mbuf[i].pay];
+    } else {
+      out_ids[o] = -1;
+      out_d[o] = __int_as_float(0x7f800000);
+      if (out_cid) out_cid[o] = -1;
+    }
+  }
+  if (threadIdx.x == 0) out_n[b] = kept;
+}
+
+void launch_merge(int B, const int32_t* slot_off, const uint32_t* cand_key, const int64_t* cand_id,
+                  const int32_t* cand_n, const int32_t* cand_list, int kk, ListTable lt,
+                  int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
+                  cudaStream_t st) {
+  if (B <= 0) return;
+  size_t smem = MERGE_CAP * sizeof(Entry);
+  cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  merge_kernel<<<B, 128, smem, st>>>(slot_off, cand_key, cand_id, cand_n, cand_list, kk, lt,
+                                     out_ids, out_d, out_cid, out_n);
+}
+
+// =====================================================================
+// assign_nearest (ref/clusters.py:268-279): per row argmin by (dist, cid).
+// =====================================================================
+__global__ void __launch_bounds__(256) argmin_kernel(const float* __restrict__ D, int64_t ldd,
+                                                     ListTable lt, int32_t scope_code,
+                                                     int64_t* __restrict__ out_cid,
+                                                     float* __restrict__ out_d) {
+  __shared__ uint32_t s_k[8];
+  __shared__ int64_t s_i[8];
+  const int b = blockIdx.x;
+  const float* row = D + (int64_t)b * ldd;
+  uint32_t bk = KEY_NONE;
+  int64_t bi = ID_NONE;
+  for (int c = threadIdx.x; c < lt.nslots; c += blockDim.x) {
+    const int64_t i = lt.cid[c];
+    if (i < 0 || lt.scope[c] != scope_code) continue;
+    const uint32_t k = f2key(row[c]);
+    if (lex_less(k, i, bk, bi)) {
+      bk = k;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint32_t k2 = __shfl_xor_sync(FULL, bk, o);
+    int64_t i2 = __shfl_xor_sync(FULL, bi, o);
+    if (lex_less(k2, i2, bk, bi)) {
+      bk = k2;
+      bi = i2;
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_k[warp] = bk;
+    s_i[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+      if (lex_less(s_k[w], s_i[w], bk, bi)) {
+        bk = s_k[w];
+        bi = s_i[w];
+      }
+    out_cid[b] = bi == ID_NONE ? -1 : bi;
+    if (out_d) out_d[b] = key2f(bk);
+  }
+}
+void launch_argmin(const float* D, int64_t ldd, int B, ListTable lt, int32_t scope_code,
+                   int64_t* out_cid, float* out_d, cudaStream_t st) {
+  if (B <= 0) return;
+  argmin_kernel<<<B, 256, 0, st>>>(D, ldd, lt, scope_code, out_cid, out_d);
+}
+
+__global__ void scatter_rows_kernel(const float* __restrict__ src, int64_t lds,
+                                    const int64_t* __restrict__ src_ids, int n,
+                                    const int64_t* __restrict__ dst_row, float* __restrict__ dst,
+                                    int64_t* __restrict__ dst_ids, int dp) {
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const int64_t r = dst_row[i];
+  for (int j = threadIdx.x; j < dp / 4; j += blockDim.x)
+    reinterpret_cast<float4*>(dst + r * dp)[j] = reinterpret_cast<const float4*>(src + i * lds)[j];
+  if (threadIdx.x == 0) dst_ids[r] = src_ids[i];
+}
+void launch_scatter_rows(const float* src, int64_t lds, const int64_t* src_ids, int n,
+                         const int64_t* dst_row, float* dst, int64_t* dst_ids, int dp,
+                         cudaStream_t st) {
+  if (n <= 0) return;
+  scatter_rows_kernel<<<n, 128, 0, st>>>(src, lds, src_ids, n, dst_row, dst, dst_ids, dp);
+}
+
+}  // namespace pk

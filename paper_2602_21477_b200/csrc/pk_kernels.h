@@ -1,0 +1,94 @@
+// pk_kernels.h -- launch interface of the sm_100a kernels (host side).
+#pragma once
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace pk {
+
+enum Metric : int { SQ_L2 = 0, IP = 1, COSINE = 2 };
+
+constexpr int DC = 32;          // floats per streamed d-chunk (one 128B swizzle row)
+constexpr int TILE = 256;       // rows per scan tile (one row per compute thread)
+constexpr int QG = 16;          // queries per scan work item
+constexpr int KKMAX = 64;       // max per-query candidates kept by scan / merge
+constexpr int STAGES = 4;       // TMA pipeline depth
+constexpr int NBOX = 6;         // TMA box heights 256,128,64,32,16,8
+
+// One posting-list work item: rows [row0, row0+nrows) of list `lslot`,
+// against queries qpairs[qoff .. qoff+nq).
+struct ScanItem {
+  int32_t lslot;
+  int32_t row0;
+  int32_t nrows;
+  int32_t qoff;
+  int32_t nq;
+  int32_t chunk;
+  int32_t pad0, pad1;
+};
+struct QPair {  // query index and the base of its output slots for this list
+  int32_t b;
+  int32_t slotbase;
+};
+
+struct ArenaMaps {
+  CUtensorMap box[NBOX];  // heights 256,128,64,32,16,8 rows x DC floats, SWIZZLE_128B
+};
+
+// Device view of the list table and arena.
+struct ListTable {
+  const float* rows;     // [arena_rows][dp]
+  const int64_t* ids;    // [arena_rows]
+  const int64_t* off;    // [nslots] first arena row of list
+  const int64_t* len;    // [nslots] live rows
+  const int64_t* cid;    // [nslots] cluster id (-1 = empty slot)
+  const int32_t* scope;  // [nslots] scope code
+  const float* cent;     // [nslots][dp]
+  int32_t nslots;
+  int32_t dp;            // padded row stride (multiple of DC)
+  int32_t d;             // true dimension
+};
+
+// ---- launchers (all async on `st`) ----
+// D[b][r] = dist(Q[b], X[r]) exact reference arithmetic; Q: [B][ldq], X: [n][ldx].
+void launch_dist_dense(int metric, const float* Q, int64_t ldq, int B, const float* X, int64_t ldx,
+                       int64_t n, int dp, const float* qnorm, float* D, int64_t ldd,
+                       cudaStream_t st);
+// kmeans_assign arithmetic (fp32 square, fp64 sum), fused argmin over k rows of C.
+void launch_kmeans_assign(const float* X, int64_t ldx, int64_t n, const float* C, int64_t ldc,
+                          int64_t k, int dp, int64_t* labels, double* dists, cudaStream_t st);
+// qnorm[b] = sqrt(sum_j q_j*q_j) sequential fp32 (cosine only).
+void launch_qnorm(const float* Q, int64_t ldq, int B, int d, float* qnorm, cudaStream_t st);
+// centroid = fp64 row-order mean of rows [off, off+n) -> f32 (written to cent_out[dp]).
+void launch_centroid(const float* rows, int64_t ldr, int64_t n, int dp, float* cent_out,
+                     cudaStream_t st);
+// Coarse select: per query the first `nprobe` in-scope lists by (dist, cid).
+void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
+                          const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
+                          uint32_t* probe_key, cudaStream_t st);
+// Build the (list -> queries) routing and the scan work items.
+void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows,
+                  int32_t* scratch_counts, int32_t* scratch_fill, ScanItem* items,
+                  int32_t* n_items, QPair* qpairs, int32_t* slot_off, int64_t* scanned,
+                  cudaStream_t st);
+// Persistent fused scan + per-(query, item) top-kk.
+void launch_scan(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
+                 const float* qnorm, const ScanItem* items, const int32_t* n_items,
+                 int max_items, const QPair* qpairs, int kk, int32_t* work_ctr,
+                 uint32_t* cand_key, int64_t* cand_id, int32_t* cand_n, int32_t* cand_list,
+                 int num_sms, cudaStream_t st);
+// Per query merge of its slots into the final top-kk (dedup by id).
+void launch_merge(int B, const int32_t* slot_off, const uint32_t* cand_key, const int64_t* cand_id,
+                  const int32_t* cand_n, const int32_t* cand_list, int kk, ListTable lt,
+                  int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
+                  cudaStream_t st);
+// Row argmin over the live lists of one scope by (dist, cid) -- assign_nearest (ref/clusters.py:268-279).
+void launch_argmin(const float* D, int64_t ldd, int B, ListTable lt, int32_t scope_code,
+                   int64_t* out_cid, float* out_d, cudaStream_t st);
+// Scatter rows: dst[dst_row[i]] = src[i] (rows of dp floats) and ids.
+void launch_scatter_rows(const float* src, int64_t lds, const int64_t* src_ids, int n,
+                         const int64_t* dst_row, float* dst, int64_t* dst_ids, int dp,
+                         cudaStream_t st);
+size_t scan_smem_bytes();
+
+}  // namespace pk

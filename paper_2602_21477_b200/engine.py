@@ -1,0 +1,701 @@
+"""Public store facade, a drop-in for the reference's ``agentmem.engine``
+(ref/engine.py:1-839) on the bare IVF path.
+
+Same classes and signatures (``Store``, ``StoreConfig``, ``SearchResult``,
+``SearchStats``, ``OperationBatch``), same validation and error types, same
+results.  What changes is underneath: the coarse quantizer, the posting-list
+scan, the top-k merge, assignment and centroid maintenance run as sm_100a
+kernels over a device-resident index (``DeviceIndex``), and batches of
+queries are answered by ONE device pass (``search_batch`` / ``submit_batch``)
+instead of one Python loop iteration per (query, cluster).
+
+Scope of this build: the bare IVF path -- ``agent=None`` or
+``cache_enabled=False``.  The per-agent multi-level cache, FSM pattern hints
+and prefetch (ref/cache.py, ref/fsm.py) are not part of it; a store
+configured with ``cache_enabled=True`` rejects agent-scoped operations with
+NotImplementedError instead of silently answering differently.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from . import pnck
+from .clusters import ClusterStore, SplitOutcome, kmeans_split_points
+from .concurrency import RWLock, TaskRunner
+from .core import (
+    STATIC_SCOPE,
+    Metric,
+    ScopePermissionError,
+    UsageError,
+    as_matrix,
+    as_vector,
+)
+from .index import DeviceIndex
+from .kernels import centroid as vector_mean
+from .kernels import deviation as vector_spread
+from .tiering import TierManager
+
+SEED_ENV = "PANCAKE_SEED"
+
+
+@dataclass
+class StoreConfig:
+    """ref/engine.py:42-100 (every field kept); ``device`` is new."""
+
+    dimension: int
+    metric: Metric = Metric.SQUARED_EUCLIDEAN
+    seed: int = 0
+    split_threshold: int = 4096
+    split_target: int = 2048
+    maintenance_interval: int = 256
+    n_p: int = 16
+    l0_capacity: int = 64
+    l1_capacity: int = 1024
+    kappa: int = 2
+    alpha_et: float = 0.7
+    window_w: int = 32
+    verify_mode: bool = False
+    cache_enabled: bool = True
+    n_s: int = 8
+    d_merge_factor: float = 0.5
+    theta_match: float = 0.5
+    prefetch_enabled: bool = True
+    pattern_enabled: bool = True
+    m: int = 16
+    ef_search_factor: int = 4
+    alpha_ic: float = 6.0
+    p_size: int = 32
+    coarse_mode: str = "hybrid"
+    profiles_enabled: bool = True
+    accelerator: str = "simulated"
+    budget_bytes: int = 64 << 20
+    b_insert: int = 128
+    decay_half_life: int = 10000
+    slack_fraction: float = 0.25
+    hotset_interval: int = 64
+    splits_enabled: bool = True
+    lazy_maintenance: bool = True
+    static_writable_by_agents: bool = False
+    default_nprobe: int = 8
+    threads: int = 0
+    request_window: int = 64
+    device: int = 0
+
+    def __post_init__(self):
+        if isinstance(self.metric, str):
+            self.metric = Metric(self.metric)
+        if self.dimension < 1:
+            raise UsageError(f"dimension must be >= 1, got {self.dimension}")
+        if not 0.0 <= self.alpha_et <= 1.0:
+            raise UsageError("alpha_et must lie in [0, 1]")
+        if self.split_target >= self.split_threshold:
+            raise UsageError("split_target must be below split_threshold")
+        if self.coarse_mode not in ("hybrid", "per_agent"):
+            raise UsageError(f"unknown coarse_mode {self.coarse_mode!r}")
+        if self.accelerator not in ("none", "simulated", "native"):
+            raise UsageError(f"unknown accelerator {self.accelerator!r}")
+
+
+@dataclass
+class SearchStats:
+    scanned_vectors: int = 0
+    coarse_computations: int = 0
+    level_reached: str = "L2"
+    early_terminated: bool = False
+
+
+@dataclass
+class SearchResult:
+    hits: list[tuple[int, float, str]]
+    stats: SearchStats
+    scan_ids: np.ndarray = field(default_factory=lambda: np.empty(0, dtype=np.int64))
+
+    @property
+    def ids(self) -> list[int]:
+        return [h[0] for h in self.hits]
+
+    @property
+    def distances(self) -> list[float]:
+        return [h[1] for h in self.hits]
+
+
+@dataclass
+class OperationBatch:
+    kind: str
+    agent: str | None
+    ops: list
+
+    def __post_init__(self):
+        if self.kind not in ("search", "insert", "update", "delete"):
+            raise UsageError(f"unknown batch kind {self.kind!r}")
+
+
+class ScopeCodes:
+    """Store-wide scope -> small int interning (ref/pool.py:14-30)."""
+
+    def __init__(self):
+        self.code: dict[str, int] = {}
+        self.name: list[str] = []
+
+    def intern(self, scope: str) -> int:
+        c = self.code.get(scope)
+        if c is None:
+            c = len(self.name)
+            self.code[scope] = c
+            self.name.append(scope)
+        return c
+
+    def mask_codes(self, scopes) -> np.ndarray:
+        return np.asarray(sorted(self.intern(s) for s in scopes), dtype=np.int16)
+
+
+def profile_reorder(entries, default_order):
+    """ref/graph.py:441-451."""
+    default_set = set(default_order)
+    seen, front = set(), []
+    for lid in entries:
+        if lid in default_set and lid not in seen:
+            front.append(lid)
+            seen.add(lid)
+    return front + [lid for lid in default_order if lid not in seen]
+
+
+def profile_promote(entries, hits, p_size):
+    """ref/graph.py:454-463."""
+    hit_seen, front = set(), []
+    for lid in hits:
+        if lid not in hit_seen:
+            front.append(lid)
+            hit_seen.add(lid)
+    return (front + [lid for lid in entries if lid not in hit_seen])[:p_size]
+
+
+class Store:
+    """One memory store: a static scope plus any number of agent scopes."""
+
+    def __init__(self, cfg: StoreConfig):
+        self.cfg = cfg
+        seed = cfg.seed
+        env = os.environ.get(SEED_ENV)
+        if env is not None:
+            seed = int(env)
+        self.seed = seed
+        self.rng = np.random.default_rng(np.random.PCG64(seed))
+        self.metric = cfg.metric
+        self.scope_codes = ScopeCodes()
+        self.index = DeviceIndex(cfg.dimension, cfg.metric.wire_code, cfg.device)
+        self.clusters = ClusterStore(
+            cfg.dimension, cfg.metric, self.rng, self.index, self.scope_codes,
+            split_threshold=cfg.split_threshold, split_target=cfg.split_target,
+            maintenance_interval=cfg.maintenance_interval,
+        )
+        self.runner = TaskRunner(cfg.threads)
+        self.tier = TierManager(self.clusters, self.index, budget_bytes=cfg.budget_bytes,
+                                b_insert=cfg.b_insert, decay_half_life=cfg.decay_half_life,
+                                slack_fraction=cfg.slack_fraction)
+        self.agents: set[str] = set()
+        self.sequences: dict[str, list[np.ndarray]] = {}
+        self.payloads: dict[int, bytes] = {}
+        self._next_item_id = 0
+        self._op_count = 0
+        self._lock = RWLock()
+        self._agent_locks: dict[str, threading.RLock] = {}
+        self._ingest_lock = threading.RLock()
+        self.clusters.register_scope(STATIC_SCOPE)
+        self.scope_codes.intern(STATIC_SCOPE)
+
+    # --- lifecycle --------------------------------------------------------
+    @classmethod
+    def create(cls, cfg: StoreConfig) -> "Store":
+        return cls(cfg)
+
+    def close(self):
+        self.runner.shutdown()
+        self.index.close()
+
+    def _centroid_of(self, cid: int) -> np.ndarray:
+        return self.clusters.clusters[cid].centroid
+
+    # --- scopes -----------------------------------------------------------
+    def register_agent(self, agent_id: str) -> str:
+        """ref/engine.py:211-241."""
+        if agent_id == STATIC_SCOPE:
+            raise UsageError(f"{STATIC_SCOPE!r} is reserved for the shared base scope")
+        if agent_id in self.agents:
+            raise UsageError(f"agent {agent_id!r} already registered")
+        self.clusters.register_scope(agent_id)
+        self.scope_codes.intern(agent_id)
+        self.agents.add(agent_id)
+        self.sequences[agent_id] = []
+        self._agent_locks[agent_id] = threading.RLock()
+        return agent_id
+
+    def unregister_agent(self, agent_id: str):
+        if agent_id not in self.agents:
+            raise UsageError(f"unknown agent {agent_id!r}")
+        for cid in list(self.clusters.scope_clusters(agent_id)):
+            self.clusters.retire_cluster(cid)
+        for item_id in list(self.clusters.staged.get(agent_id, {})):
+            self.clusters.unstage(agent_id, item_id)
+            self.payloads.pop(item_id, None)
+        self.agents.discard(agent_id)
+        del self.sequences[agent_id]
+        del self._agent_locks[agent_id]
+
+    def registered_scopes(self) -> list[str]:
+        return list(self.clusters.by_scope)
+
+    def _serialized(self, agent):
+        if agent is None:
+            return self._ingest_lock
+        return self._agent_locks[agent]
+
+    def _check_scopes(self, scopes) -> set[str]:
+        out = set(scopes)
+        if not out:
+            raise UsageError("scope set must be non-empty")
+        for sc in out:
+            if sc not in self.clusters.by_scope:
+                raise UsageError(f"unknown scope {sc!r}")
+        return out
+
+    def _check_writable(self, agent, scope: str):
+        if scope not in self.clusters.by_scope:
+            raise UsageError(f"unknown scope {scope!r}")
+        if agent is None or scope == agent:
+            return
+        if scope == STATIC_SCOPE and self.cfg.static_writable_by_agents:
+            return
+        raise ScopePermissionError(f"agent {agent!r} may not write scope {scope!r}")
+
+    def _require_bare(self, agent):
+        if agent is not None and self.cfg.cache_enabled:
+            raise NotImplementedError(
+                "the per-agent multi-level cache path (ref/cache.py) is not part of this build; "
+                "use agent=None or StoreConfig(cache_enabled=False)")
+
+    # --- search -----------------------------------------------------------
+    def search(self, agent, scopes, q, k: int, nprobe: int | None = None, _internal: bool = False,
+               _no_cache: bool = False) -> SearchResult:
+        """ref/engine.py:287-317."""
+        if k < 1:
+            raise UsageError("k must be >= 1")
+        scopes = self._check_scopes(scopes)
+        if agent is not None and agent not in self.agents:
+            raise UsageError(f"unknown agent {agent!r}")
+        q = as_vector(q, self.cfg.dimension)
+        nprobe = nprobe if nprobe is not None else self.cfg.default_nprobe
+        if nprobe < 1:
+            raise UsageError("nprobe must be >= 1")
+        self._require_bare(agent if not _no_cache else None)
+        with self._serialized(agent):
+            self._lock.acquire_read()
+            try:
+                result = self._search_read_phase_batch(agent, scopes, q[None, :], k, nprobe,
+                                                       want_scan_ids=True)[0]
+            finally:
+                self._lock.release_read()
+            if agent is not None:
+                self._search_side_effects(agent, q, result, _internal)
+            self._tick()
+            return result
+
+    def search_batch(self, agent, scopes, Q, k: int, nprobe: int | None = None,
+                     want_scan_ids: bool = False) -> list[SearchResult]:
+        """B queries with the same (agent, scopes, k, nprobe) in one device
+        pass; equal to B calls of ``search`` (``scan_ids`` only on request)."""
+        if k < 1:
+            raise UsageError("k must be >= 1")
+        scopes = self._check_scopes(scopes)
+        if agent is not None and agent not in self.agents:
+            raise UsageError(f"unknown agent {agent!r}")
+        Q = as_matrix(Q, self.cfg.dimension)
+        nprobe = nprobe if nprobe is not None else self.cfg.default_nprobe
+        if nprobe < 1:
+            raise UsageError("nprobe must be >= 1")
+        self._require_bare(agent)
+        with self._serialized(agent):
+            self._lock.acquire_read()
+            try:
+                results = self._search_read_phase_batch(agent, scopes, Q, k, nprobe, want_scan_ids)
+            finally:
+                self._lock.release_read()
+            for b, res in enumerate(results):
+                if agent is not None:
+                    self._search_side_effects(agent, Q[b], res, False)
+                self._tick()
+            return results
+
+    def _search_read_phase_batch(self, agent, scopes, Q, k, nprobe, want_scan_ids):
+        """Store._search_read_phase (ref/engine.py:319-404) for a batch on the
+        bare path: staged scan, coarse top-nprobe (flat == graph at exhaustive
+        ef), merged scan of every probed list, _topk (ref/engine.py:406-426)."""
+        B = Q.shape[0]
+        if k > N.KKMAX:
+            raise UsageError(f"k above {N.KKMAX} is not supported by the device top-k")
+        exhaustive_edge = k >= self.clusters.live_count()
+        for sc in scopes:
+            if self.clusters.staged.get(sc):
+                raise NotImplementedError("staged (cache-owned) items need the cache path")
+        eff_nprobe = nprobe
+        if exhaustive_edge:
+            eff_nprobe = max(nprobe, len(self.clusters.clusters) or 1)
+        in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
+        dev_nprobe = max(1, min(eff_nprobe, in_scope))
+        if dev_nprobe > N.NPROBE_MAX:
+            raise UsageError(f"nprobe above {N.NPROBE_MAX} in-scope lists is not supported")
+        codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
+        need_probe = True  # access counters + scan_ids follow the probe order
+        out = self.index.search(Q, codes, dev_nprobe, k, want_probe=need_probe)
+        results = []
+        clusters = self.clusters.clusters
+        for b in range(B):
+            n = int(out.counts[b])
+            ids = out.ids[b, :n].tolist()
+            dd = out.dists[b, :n].tolist()
+            cs = out.cids[b, :n].tolist()
+            hits = [(ids[i], dd[i], clusters[cs[i]].scope) for i in range(n)]
+            stats = SearchStats(scanned_vectors=int(out.scanned[b]), coarse_computations=in_scope,
+                                level_reached="L2", early_terminated=False)
+            probe = [c for c in out.probe[b].tolist() if c >= 0]
+            scan_chunks = []
+            for cid in probe:
+                cl = clusters[cid]
+                cl.access_count += 1
+                self.tier.record_access(cid)
+                if want_scan_ids:
+                    if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
+                        order = profile_reorder(cl.profiles[agent], list(range(cl.size)))
+                        scan_chunks.append(cl.member_ids[order])
+                    else:
+                        scan_chunks.append(cl.member_ids.copy())
+            scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
+            results.append(SearchResult(hits, stats, scan_ids))
+        return results
+
+    def _search_side_effects(self, agent, q, result, internal):
+        """ref/engine.py:448-501 without the cache/FSM branches."""
+        if self.cfg.profiles_enabled:
+            by_cluster: dict[int, list[int]] = {}
+            for iid, _, _ in result.hits:
+                owner = self.clusters.owner.get(iid)
+                if owner and owner[0] == "cluster":
+                    cl = self.clusters.clusters[owner[1]]
+                    by_cluster.setdefault(owner[1], []).append(cl.id_to_row[iid])
+            for cid, rows in by_cluster.items():
+                cl = self.clusters.clusters[cid]
+                cl.profiles[agent] = profile_promote(cl.profiles.get(agent, []), rows,
+                                                     self.cfg.p_size)
+        if not internal:
+            self._append_sequence(agent, q)
+
+    # --- mutation ---------------------------------------------------------
+    def insert(self, agent, scope: str, vectors, payloads=None, ids=None) -> list[int]:
+        """ref/engine.py:557-569."""
+        self._require_bare(agent)
+        with self._serialized(agent):
+            with self._lock.write():
+                accepted = self._insert_impl(agent, scope, vectors, payloads, ids)
+                self._tick(locked=True)
+            return accepted
+
+    def _insert_impl(self, agent, scope, vectors, payloads=None, ids=None) -> list[int]:
+        """ref/engine.py:571-605 on the direct-place path, with the batch's
+        assignments computed in one device call and recomputed only after a
+        centroid change."""
+        self._check_writable(agent, scope)
+        vecs = [as_vector(v, self.cfg.dimension) for v in vectors]
+        if payloads is None:
+            payloads = [b""] * len(vecs)
+        if len(payloads) != len(vecs):
+            raise UsageError("vectors and payloads must have equal length")
+        if ids is not None:
+            if len(ids) != len(vecs):
+                raise UsageError("vectors and ids must have equal length")
+            for iid in ids:
+                if iid in self.clusters.owner:
+                    raise UsageError(f"item id {iid} already live")
+        accepted: list[int] = []
+        n = len(vecs)
+        i = 0
+        assigned = None
+        assigned_from = -1
+        while i < n:
+            vec = vecs[i]
+            iid = self._take_id(ids[i] if ids is not None else None)
+            payload = payloads[i]
+            if isinstance(payload, str):
+                payload = payload.encode("utf-8")
+            self.payloads[iid] = payload
+            cands = self.clusters.by_scope[scope]
+            if not cands:
+                self.clusters.create_cluster(scope, [(iid, vec)])
+                assigned = None
+            else:
+                if assigned is None:
+                    assigned = self.clusters.assign_nearest_batch(np.stack(vecs[i:]), scope)
+                    assigned_from = i
+                cid = int(assigned[i - assigned_from])
+                self.tier.buffered_insert(cid, iid, vec)
+                if self._after_cluster_mutation(cid):
+                    assigned = None  # a centroid moved: later vectors re-assign
+            if agent is not None:
+                self._append_sequence(agent, vec)
+            accepted.append(iid)
+            i += 1
+        return accepted
+
+    def _take_id(self, explicit) -> int:
+        if explicit is None:
+            iid = self._next_item_id
+            self._next_item_id += 1
+            return iid
+        self._next_item_id = max(self._next_item_id, explicit + 1)
+        return explicit
+
+    def _after_cluster_mutation(self, cid: int) -> bool:
+        """ref/engine.py:656-660; True when a centroid changed."""
+        if self.cfg.splits_enabled and self.clusters.needs_split(cid):
+            self.tier.split_offload(cid)
+            return True
+        if self.cfg.lazy_maintenance:
+            cl = self.clusters.clusters.get(cid)
+            if cl is not None and cl.dirty >= self.clusters.maintenance_interval:
+                self.clusters.maintenance(cid)
+                return True
+        return False
+
+    def bulk_build(self, scope: str, vectors, payloads=None) -> list[int]:
+        """ref/engine.py:615-645 (k-means on device)."""
+        with self._serialized(None), self._lock.write():
+            self._check_writable(None, scope)
+            mat = as_matrix(vectors, self.cfg.dimension) if len(vectors) else np.empty(
+                (0, self.cfg.dimension), np.float32)
+            n = len(mat)
+            if n == 0:
+                return []
+            ids = [self._take_id(None) for _ in range(n)]
+            if payloads is not None:
+                for iid, p in zip(ids, payloads):
+                    self.payloads[iid] = p.encode("utf-8") if isinstance(p, str) else p
+            k = max(1, -(-n // self.cfg.split_target))
+            id_arr = np.asarray(ids, dtype=np.int64)
+            if k == 1:
+                self.clusters.create_cluster(scope, (id_arr, mat))
+                return ids
+            center = vector_mean(mat)
+            spread = vector_spread(mat, center, Metric.SQUARED_EUCLIDEAN)
+            labels, _ = kmeans_split_points(mat, k, self.rng, spread)
+            for c in range(int(labels.max()) + 1):
+                rows = np.where(labels == c)[0]
+                if len(rows):
+                    self.clusters.create_cluster(scope, (id_arr[rows], mat[rows]))
+            return ids
+
+    def update(self, agent, item_id: int, vector=None, payload=None) -> bool:
+        """ref/engine.py:680-694."""
+        self._require_bare(agent)
+        with self._serialized(agent), self._lock.write():
+            owner = self.clusters.owner.get(item_id)
+            if owner is None:
+                return False
+            scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
+            self._check_writable(agent, scope)
+            old_vec = self._vector_of(item_id)
+            new_vec = as_vector(vector, self.cfg.dimension) if vector is not None else old_vec
+            new_payload = payload if payload is not None else self.payloads.get(item_id, b"")
+            self._delete_internal(item_id)
+            self._insert_impl(agent, scope, [new_vec], [new_payload], ids=[item_id])
+            self._tick(locked=True)
+            return True
+
+    def delete(self, agent, item_id: int) -> bool:
+        """ref/engine.py:696-705."""
+        self._require_bare(agent)
+        with self._serialized(agent), self._lock.write():
+            owner = self.clusters.owner.get(item_id)
+            if owner is None:
+                return False
+            scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
+            self._check_writable(agent, scope)
+            ok = self._delete_internal(item_id)
+            self._tick(locked=True)
+            return ok
+
+    def _delete_internal(self, item_id: int) -> bool:
+        owner = self.clusters.owner.get(item_id)
+        if owner is None:
+            return False
+        if owner[0] == "cluster":
+            cid = owner[1]
+            self.clusters.delete_item(item_id)
+            if cid in self.clusters.clusters and self.cfg.lazy_maintenance:
+                self.clusters.maintenance(cid)
+        else:
+            self.clusters.delete_item(item_id)
+        self.payloads.pop(item_id, None)
+        return True
+
+    def end_request(self, agent: str):
+        if agent not in self.sequences:
+            raise UsageError(f"unknown agent {agent!r}")
+        self.sequences[agent] = []
+
+    def _append_sequence(self, agent: str, v: np.ndarray):
+        seq = self.sequences[agent]
+        seq.append(v)
+        if len(seq) > self.cfg.request_window:
+            del seq[0]
+
+    def flush_caches(self):
+        """No cache levels on this path: L2 is always complete."""
+        return None
+
+    def _tick(self, locked: bool = False):
+        self._op_count += 1
+
+    # --- item access -------------------------------------------------------
+    def _vector_of(self, item_id: int):
+        owner = self.clusters.owner.get(item_id)
+        if owner is None:
+            return None
+        if owner[0] == "staged":
+            return self.clusters.staged[owner[1]].get(item_id)
+        cl = self.clusters.clusters[owner[1]]
+        row = cl.id_to_row.get(item_id)
+        return cl.vectors[row].copy() if row is not None else None
+
+    def get_item(self, item_id: int):
+        vec = self._vector_of(item_id)
+        if vec is None:
+            return None
+        owner = self.clusters.owner[item_id]
+        scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
+        return vec, self.payloads.get(item_id, b""), scope
+
+    def live_count(self) -> int:
+        return self.clusters.live_count()
+
+    def split_cluster(self, cid: int) -> SplitOutcome:
+        return self.tier.split_offload(cid)
+
+    # --- async surface ------------------------------------------------------
+    def submit_batch(self, batch: OperationBatch):
+        """ref/engine.py:784-801.  A homogeneous search batch (same scopes, k,
+        nprobe) runs as one device pass."""
+
+        def run():
+            if batch.kind == "search" and batch.ops:
+                groups = {}
+                for op in batch.ops:
+                    scopes, _q, k, *rest = op
+                    key = (tuple(sorted(scopes)), k, rest[0] if rest else None)
+                    groups.setdefault(key, 0)
+                if len(groups) == 1:
+                    scopes, _, k, *rest = batch.ops[0]
+                    Q = np.stack([np.asarray(op[1], dtype=np.float32) for op in batch.ops])
+                    return self.search_batch(batch.agent, scopes, Q, k, rest[0] if rest else None,
+                                             want_scan_ids=True)
+            out = []
+            for op in batch.ops:
+                if batch.kind == "search":
+                    out.append(self.search(batch.agent, *op))
+                elif batch.kind == "insert":
+                    out.append(self.insert(batch.agent, *op))
+                elif batch.kind == "update":
+                    out.append(self.update(batch.agent, *op))
+                else:
+                    out.append(self.delete(batch.agent, *op))
+            return out
+
+        role = "search" if batch.kind == "search" else "update"
+        return self.runner.submit(role, run)
+
+    def submit_search(self, agent, scopes, q, k, nprobe=None):
+        return self.runner.submit("search", self.search, agent, scopes, q, k, nprobe)
+
+    def submit_insert(self, agent, scope, vectors, payloads=None):
+        return self.runner.submit("update", self.insert, agent, scope, vectors, payloads)
+
+    # --- persistence / ingestion -------------------------------------------
+    def snapshot(self, path):
+        raise NotImplementedError("snapshot/restore (ref/persist.py:136-380) is out of scope; "
+                                  "use export_ivf / load_external_ivf")
+
+    @classmethod
+    def restore(cls, path):
+        raise NotImplementedError("snapshot/restore (ref/persist.py:136-380) is out of scope")
+
+    def export_ivf(self, path, scopes=None):
+        """ref/persist.py:386-394."""
+        if scopes is None:
+            scopes = list(self.clusters.by_scope)
+        cids = sorted(c for c, cl in self.clusters.clusters.items() if cl.scope in scopes)
+        pnck.write_pnck(path, self.cfg.dimension, self.metric,
+                        [(self.clusters.clusters[c].centroid, self.clusters.clusters[c].member_ids,
+                          self.clusters.clusters[c].vectors) for c in cids])
+
+    def load_external_ivf(self, path, scope: str) -> int:
+        """ref/persist.py:397-424: import PNCK records as clusters of `scope`
+        (centroids recomputed from the members, on device)."""
+        if scope not in self.clusters.by_scope:
+            raise UsageError(f"unknown scope {scope!r}")
+        dimension, metric, records = pnck.read_pnck(path)
+        if dimension != self.cfg.dimension:
+            raise UsageError(
+                f"dimension mismatch: file has {dimension}, store has {self.cfg.dimension}")
+        if metric is not self.metric:
+            raise UsageError(f"metric mismatch: file has {metric}, store has {self.metric}")
+        return self.load_lists(scope, [(ids, rows) for _, ids, rows in records])
+
+    def load_lists(self, scope: str, lists) -> int:
+        """Import ready-made posting lists [(ids, rows)] into `scope`."""
+        with self._serialized(None), self._lock.write():
+            for ids, _ in lists:
+                for iid in np.asarray(ids).tolist():
+                    if iid in self.clusters.owner:
+                        raise UsageError(f"item id {iid} already live in store")
+            count = 0
+            for ids, rows in lists:
+                ids = np.asarray(ids, dtype=np.int64)
+                if len(ids) == 0:
+                    continue
+                self.clusters.create_cluster(scope, (ids, rows))
+                self._next_item_id = max(self._next_item_id, int(ids.max()) + 1)
+                count += 1
+            return count
+
+    def ingest_fvecs(self, path, scope: str, limit: int | None = None) -> list[int]:
+        import struct
+
+        from .core import ParseError
+
+        vecs = []
+        with open(path, "rb") as f:
+            offset = 0
+            while True:
+                head = f.read(4)
+                if not head:
+                    break
+                if len(head) != 4:
+                    raise ParseError("truncated fvecs record header", offset)
+                d = struct.unpack("<i", head)[0]
+                if d <= 0:
+                    raise ParseError(f"bad fvecs dimension {d}", offset)
+                if d != self.cfg.dimension:
+                    raise UsageError(f"dimension mismatch: fvecs has {d}, expected {self.cfg.dimension}")
+                body = f.read(4 * d)
+                if len(body) != 4 * d:
+                    raise ParseError("truncated fvecs record body", offset + 4)
+                vecs.append(np.frombuffer(body, dtype=np.float32).copy())
+                offset += 4 + 4 * d
+                if limit is not None and len(vecs) >= limit:
+                    break
+        return self.insert(None, scope, vecs)

@@ -1,0 +1,142 @@
+"""DeviceIndex: Python handle on one device-resident IVF (the C-ABI pk_index).
+
+Owns the HBM arena of posting lists, the list table and the centroid table
+of one GPU.  It is the storage half of the reference's ``ClusterStore``
+(ref/clusters.py:186-362) plus the residency half of ``TierManager``
+(ref/tiering.py:175-448): every list the store owns is resident here.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+
+
+class SearchOutput:
+    """Batched search result arrays (host)."""
+
+    __slots__ = ("ids", "dists", "cids", "counts", "probe", "scanned")
+
+    def __init__(self, ids, dists, cids, counts, probe, scanned):
+        self.ids = ids
+        self.dists = dists
+        self.cids = cids
+        self.counts = counts
+        self.probe = probe
+        self.scanned = scanned
+
+
+class DeviceIndex:
+    def __init__(self, dimension: int, metric_code: int = 0, device: int = 0,
+                 reserve_rows: int = 0, reserve_lists: int = 0):
+        self.dimension = int(dimension)
+        self.metric_code = int(metric_code)
+        self.device = int(device)
+        h = ctypes.c_void_p()
+        N.check(N.lib().pk_index_create(self.dimension, self.metric_code, self.device,
+                                        int(reserve_rows), int(reserve_lists), ctypes.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            N.lib().pk_index_destroy(self._h)
+        self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown ordering
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def sync(self):
+        N.check(N.lib().pk_sync(self._h))
+
+    def nbytes(self) -> int:
+        v = ctypes.c_int64(0)
+        N.check(N.lib().pk_index_bytes(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    # ---- posting lists -------------------------------------------------
+    def create_list(self, cid: int, scope_code: int, rows, ids) -> np.ndarray:
+        rows = N.f32(rows, self.dimension)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        cent = np.empty(self.dimension, dtype=np.float32)
+        N.check(N.lib().pk_list_create(self._h, int(cid), int(scope_code), N.ptr(rows), N.ptr(ids),
+                                       len(ids), N.ptr(cent), 0))
+        return cent
+
+    def append(self, cid: int, rows, ids):
+        rows = N.f32(rows, self.dimension)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        if len(ids):
+            N.check(N.lib().pk_list_append(self._h, int(cid), N.ptr(rows), N.ptr(ids), len(ids), 0))
+
+    def remove_row(self, cid: int, row: int):
+        N.check(N.lib().pk_list_remove_row(self._h, int(cid), int(row)))
+
+    def retire(self, cid: int):
+        N.check(N.lib().pk_list_retire(self._h, int(cid)))
+
+    def recompute(self, cid: int) -> np.ndarray:
+        cent = np.empty(self.dimension, dtype=np.float32)
+        N.check(N.lib().pk_list_recompute(self._h, int(cid), N.ptr(cent)))
+        return cent
+
+    def set_centroid(self, cid: int, centroid):
+        c = N.f32(centroid).reshape(-1)
+        N.check(N.lib().pk_list_set_centroid(self._h, int(cid), N.ptr(c)))
+
+    def size(self, cid: int) -> int:
+        v = ctypes.c_int64(0)
+        N.check(N.lib().pk_list_size(self._h, int(cid), ctypes.byref(v)))
+        return int(v.value)
+
+    def read(self, cid: int):
+        n = self.size(cid)
+        rows = np.empty((n, self.dimension), dtype=np.float32)
+        ids = np.empty(n, dtype=np.int64)
+        N.check(N.lib().pk_list_read(self._h, int(cid), N.ptr(rows), N.ptr(ids)))
+        return rows, ids
+
+    # ---- hot path ------------------------------------------------------
+    def search(self, Q, scope_codes, nprobe: int, kk: int, want_probe: bool = False,
+               want_scanned: bool = True) -> SearchOutput:
+        Q = N.f32(Q, self.dimension)
+        B = Q.shape[0]
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        ids = np.empty((B, kk), dtype=np.int64)
+        dd = np.empty((B, kk), dtype=np.float32)
+        cids = np.empty((B, kk), dtype=np.int64)
+        cnt = np.empty(B, dtype=np.int32)
+        probe = np.empty((B, nprobe), dtype=np.int64) if want_probe else None
+        scanned = np.empty(B, dtype=np.int64) if want_scanned else None
+        N.check(N.lib().pk_search(self._h, N.ptr(Q), B, N.ptr(codes), len(codes), int(nprobe),
+                                  int(kk), N.ptr(ids), N.ptr(dd), N.ptr(cids), N.ptr(cnt),
+                                  N.ptr(probe), N.ptr(scanned), 0))
+        return SearchOutput(ids, dd, cids, cnt, probe, scanned)
+
+    def search_device(self, Q, scope_codes, nprobe: int, kk: int, out_ids, out_d, out_cid,
+                      out_n, out_scanned=None):
+        """Device-pointer variant (torch tensors on this device); async on the
+        index stream."""
+        N.check(N.lib().pk_search(self._h, N.ptr(Q), Q.shape[0], N.ptr(scope_codes),
+                                  scope_codes.shape[0], int(nprobe), int(kk), N.ptr(out_ids),
+                                  N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), None,
+                                  N.ptr(out_scanned), N.PK_DEVICE_PTRS))
+
+    def assign(self, X, scope_code: int):
+        X = N.f32(X, self.dimension)
+        n = X.shape[0]
+        cid = np.empty(n, dtype=np.int64)
+        dist = np.empty(n, dtype=np.float32)
+        if n:
+            N.check(N.lib().pk_assign(self._h, N.ptr(X), n, int(scope_code), N.ptr(cid),
+                                      N.ptr(dist), 0))
+        return cid, dist
