@@ -1,0 +1,462 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200-native IVF search hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one batched search: 256 queries against the configs[1] index
+(1M x 768 fp32 unit-sphere vectors, nlist 1024, nprobe 32, k 10), exact
+reference arithmetic.  Prints ONE JSON line (rank 0).
+
+  value   device QPS with queries already resident in HBM (CUDA events on the
+          index stream around exactly K steps, max over ranks)
+  e2e     QPS through the C-ABI with host buffers (pinned), H2D of the queries
+          and D2H of the results inside the timed region
+  roofline  the fused scan kernel: algorithmic bytes of the distinct posting
+          lists each batch reads / its CUDA-event duration, against the
+          measured HBM copy bandwidth (MEASURED_PEAKS.json)
+  cpu_baseline  the C oracle port (oracle/, the parity checker) on a bounded
+          sample of the same queries, all host threads
+
+--impl reference times that oracle port alone (the reference itself is a Python
+package; its hot path restated in C is the CPU implementation of the path).
+Multi-GPU (torchrun, N>1): weak scaling -- every rank owns a 1M x 768 shard of
+a N-million-vector index (lists sharded by rank, centroids replicated), each
+rank scans its probed local lists and the per-rank top-k are merged through
+an NCCL all-gather.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "search QPS at recall@10 (=CPU ref) + scan HBM GB/s, 1/2/4/8 B200"
+UNIT = "queries/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=1_000_000)
+    p.add_argument("--d", type=int, default=768)
+    p.add_argument("--nlist", type=int, default=1024)
+    p.add_argument("--nprobe", type=int, default=32)
+    p.add_argument("--k", type=int, default=10)
+    p.add_argument("--batch", type=int, default=256)
+    p.add_argument("--kmeans-iters", type=int, default=2)
+    p.add_argument("--cpu-sample", type=int, default=0, help="oracle sample queries (0 = auto)")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--seed", type=int, default=0)
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- workload
+def make_base(n, d, seed):
+    """Unit-sphere fp32 rows (bench/workload.py:108-111 semantics), PCG64."""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    out = np.empty((n, d), dtype=np.float32)
+    step = 1 << 17
+    for i in range(0, n, step):
+        x = rng.standard_normal(size=(min(step, n - i), d), dtype=np.float32)
+        x /= np.linalg.norm(x, axis=1, keepdims=True)
+        out[i:i + len(x)] = x
+    return out
+
+
+def make_queries(base, count, seed):
+    """Half perturbed base rows (x + 0.01 N(0, I)), half fresh unit vectors."""
+    rng = np.random.default_rng(np.random.PCG64(seed + 7919))
+    n, d = base.shape
+    q = np.empty((count, d), dtype=np.float32)
+    h = count // 2
+    q[:h] = base[rng.integers(0, n, h)] + 0.01 * rng.standard_normal(size=(h, d), dtype=np.float32)
+    x = rng.standard_normal(size=(count - h, d), dtype=np.float32)
+    q[h:] = x / np.linalg.norm(x, axis=1, keepdims=True)
+    perm = rng.permutation(count)
+    return np.ascontiguousarray(q[perm])
+
+
+def seed_rows(n, nlist, seed):
+    rng = np.random.default_rng(np.random.PCG64(seed + 104729))
+    return np.sort(rng.choice(n, nlist, replace=False))
+
+
+# ---------------------------------------------------------------- helpers
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic():
+    p = os.path.join(ROOT, "profiles", "scan_ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device=0, period=0.005):
+        self.samples, self.reasons = [], set()
+        self.period = period
+        self._stop = threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def oracle_time(flat, Q, nprobe, k, threads):
+    t0 = time.perf_counter()
+    res = flat.search(Q, nprobe, k, threads=threads)
+    return time.perf_counter() - t0, res
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return  # rank 0 alone runs the CPU arm
+    from oracle import oracle as O
+
+    t_build = time.perf_counter()
+    base = make_base(a.n, a.d, a.seed)
+    seeds = base[seed_rows(a.n, a.nlist, a.seed)].astype(np.float32)
+    lab = None
+    cents = seeds
+    for _ in range(max(1, a.kmeans_iters)):
+        lab = np.empty(a.n, dtype=np.int64)
+        cn = (cents * cents).sum(1)
+        for i in range(0, a.n, 65536):
+            blk = base[i:i + 65536]
+            lab[i:i + len(blk)] = np.argmin(cn[None, :] - 2.0 * (blk @ cents.T), axis=1)
+        cents = np.stack([base[lab == c].mean(0) if np.any(lab == c) else seeds[c]
+                          for c in range(a.nlist)]).astype(np.float32)
+    order = np.argsort(lab, kind="stable")
+    lens = np.bincount(lab, minlength=a.nlist).astype(np.int64)
+    off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    rows = np.ascontiguousarray(base[order])
+    ids = order.astype(np.int64)
+    live = np.where(lens > 0)[0]
+    cent_exact = np.stack([O.centroid(rows[off[c]:off[c] + lens[c]]) for c in live])
+    flat = O.FlatIVF(rows, ids, off[live], lens[live], cent_exact, live.astype(np.int64))
+    build_s = time.perf_counter() - t_build
+    threads = os.cpu_count() or 1
+    Qall = make_queries(base, (a.warmup + a.steps) * a.batch, a.seed)
+    # size each step's sample so the run stays within ~a minute
+    probe_t, _ = oracle_time(flat, Qall[:threads], a.nprobe, a.k, threads)
+    per_q = probe_t / threads
+    sample = max(1, min(a.batch, int(60.0 / max(1, a.steps) / max(per_q, 1e-6))))
+    if a.cpu_sample:
+        sample = a.cpu_sample
+    for w in range(a.warmup):
+        oracle_time(flat, Qall[w * a.batch: w * a.batch + sample], a.nprobe, a.k, threads)
+    t_total = 0.0
+    for s in range(a.steps):
+        lo = (a.warmup + s) * a.batch
+        dt, _ = oracle_time(flat, Qall[lo: lo + sample], a.nprobe, a.k, threads)
+        t_total += dt
+    qps = a.steps * sample / t_total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": a.gpus,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * t_total / a.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": "configs[1]: 1M x 768 fp32 IVF, nlist 1024, nprobe 32, k 10, batch 256",
+                   "n": a.n, "d": a.d, "nlist": a.nlist, "nprobe": a.nprobe, "k": a.k,
+                   "batch": a.batch, "sample_queries_per_step": sample},
+        "cpu_baseline": {"value": qps, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{sample} of each step's {a.batch} queries, C oracle "
+                                   f"(oracle/pancake_oracle.c) on {threads} threads"},
+        "e2e": {"value": qps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "build_s": build_s,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(a):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2602_21477_b200 import DeviceIndex
+    from paper_2602_21477_b200 import build as B
+    from paper_2602_21477_b200 import _native as N
+
+    if rank == 0:
+        B.build()
+    if dist:
+        dist.barrier()
+    N.load()
+
+    t_build = time.perf_counter()
+    base = make_base(a.n, a.d, a.seed + rank)  # rank r owns shard r (weak scaling)
+    dev = torch.device("cuda", local)
+    X = torch.from_numpy(base).to(dev)
+    seeds = X[torch.from_numpy(seed_rows(a.n, a.nlist, a.seed + rank)).to(dev)].contiguous()
+    cents = seeds
+    labels = torch.empty(a.n, dtype=torch.int64, device=dev)
+    dists = torch.empty(a.n, dtype=torch.float64, device=dev)
+    for _ in range(max(1, a.kmeans_iters)):
+        N.check(N.lib().pk_kmeans_assign(X.data_ptr(), a.n, cents.data_ptr(), a.nlist, a.d,
+                                         labels.data_ptr(), dists.data_ptr(), N.PK_DEVICE_PTRS))
+        sums = torch.zeros(a.nlist, a.d, dtype=torch.float64, device=dev)
+        sums.index_add_(0, labels, X.double())
+        cnt = torch.bincount(labels, minlength=a.nlist).clamp(min=1).double()
+        cents = (sums / cnt[:, None]).float().contiguous()
+    order = torch.argsort(labels, stable=True)
+    Xs = X[order].contiguous()
+    ids_sorted = (order + rank * a.n).contiguous()
+    lens = torch.bincount(labels, minlength=a.nlist).cpu().numpy().astype(np.int64)
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+    del X, labels, dists
+    ix = DeviceIndex(a.d, 0, local, reserve_rows=int(a.n * 1.3) + 4096, reserve_lists=a.nlist * world)
+    # local lists: cid = rank * nlist + c ; remote lists: centroid only (no rows)
+    cent_tab = {}
+    live = [c for c in range(a.nlist) if lens[c] > 0]
+    for c in live:
+        cid = rank * a.nlist + c
+        cent_tab[cid] = ix.create_list_device(cid, 0, Xs[offs[c]:offs[c] + lens[c]],
+                                              ids_sorted[offs[c]:offs[c] + lens[c]])
+    if dist:
+        # replicate every rank's centroid table (coarse quantizer sees all lists)
+        mine = torch.from_numpy(np.stack([cent_tab[rank * a.nlist + c] for c in live])).to(dev)
+        mine_ids = torch.tensor([rank * a.nlist + c for c in live], dtype=torch.int64, device=dev)
+        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(sizes, torch.tensor([len(live)], dtype=torch.int64, device=dev))
+        mx = int(max(int(s.item()) for s in sizes))
+        pad = torch.zeros(mx, a.d, device=dev)
+        pad[:len(live)] = mine
+        padi = torch.full((mx,), -1, dtype=torch.int64, device=dev)
+        padi[:len(live)] = mine_ids
+        allc = [torch.zeros_like(pad) for _ in range(world)]
+        alli = [torch.zeros_like(padi) for _ in range(world)]
+        dist.all_gather(allc, pad)
+        dist.all_gather(alli, padi)
+        for r in range(world):
+            if r == rank:
+                continue
+            cc, ii = allc[r].cpu().numpy(), alli[r].cpu().numpy()
+            for j in range(int(sizes[r].item())):
+                ix.add_remote_list(int(ii[j]), 0, cc[j])
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+
+    Qall_h = make_queries(base, (a.warmup + a.steps) * a.batch, a.seed)  # same queries on all ranks
+    Qall = torch.from_numpy(Qall_h).to(dev).view(a.warmup + a.steps, a.batch, a.d)
+    codes = torch.zeros(1, dtype=torch.int32, device=dev)
+    kk = a.k
+    o_ids = torch.empty(a.batch, kk, dtype=torch.int64, device=dev)
+    o_d = torch.empty(a.batch, kk, dtype=torch.float32, device=dev)
+    o_c = torch.empty(a.batch, kk, dtype=torch.int64, device=dev)
+    o_n = torch.empty(a.batch, dtype=torch.int32, device=dev)
+    o_s = torch.empty(a.batch, dtype=torch.int64, device=dev)
+    stream = torch.cuda.ExternalStream(ix.stream_handle(), device=dev)
+    g_ids = g_d = None
+    if dist:
+        g_ids = [torch.empty_like(o_ids) for _ in range(world)]
+        g_d = [torch.empty_like(o_d) for _ in range(world)]
+        m_ids = torch.empty_like(o_ids)
+        m_d = torch.empty_like(o_d)
+        m_n = torch.empty_like(o_n)
+
+    def step(s):
+        ix.search_device(Qall[s], codes, a.nprobe, kk, o_ids, o_d, o_c, o_n, o_s)
+        if dist:
+            with torch.cuda.stream(stream):
+                dist.all_gather(g_ids, o_ids)
+                dist.all_gather(g_d, o_d)
+                ix.merge_ranked(torch.stack(g_d), torch.stack(g_ids), kk, m_ids, m_d, m_n)
+
+    for w in range(a.warmup):
+        step(w)
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ix.profile_begin()
+    with ClockSampler(local) as clk:
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+        for s in range(a.steps):
+            step(a.warmup + s)
+        with torch.cuda.stream(stream):
+            ev1.record(stream)
+        torch.cuda.synchronize()
+    stage_ms, ncalls = ix.profile_end()
+    ms = ev0.elapsed_time(ev1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_q = a.steps * a.batch  # every rank serves the same queries over its shard
+    qps = total_q / (ms / 1000.0)
+
+    # ---- roofline of the fused scan: algorithmic bytes of distinct lists per batch
+    row_bytes = 4 * a.d + 8
+    alg_bytes = []
+    for s in range(a.steps):
+        out = ix.search(Qall_h[(a.warmup + s) * a.batch:(a.warmup + s + 1) * a.batch], [0],
+                        a.nprobe, kk, want_probe=True)
+        pr = np.unique(out.probe[out.probe >= 0])
+        loc = pr[(pr // a.nlist) == rank] % a.nlist
+        alg_bytes.append(float(lens[loc].sum()) * row_bytes)
+    scan_ms = stage_ms["scan"] / max(ncalls, 1)
+    achieved = float(np.mean(alg_bytes)) / (scan_ms / 1000.0) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = load_traffic()
+
+    # ---- e2e through the C-ABI with host buffers
+    e2e = None
+    if not a.no_e2e:
+        Qpin = torch.from_numpy(Qall_h).pin_memory().numpy().reshape(a.warmup + a.steps, a.batch, a.d)
+        for w in range(min(a.warmup, 3)):
+            ix.search(Qpin[w], [0], a.nprobe, kk)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for s in range(a.steps):
+            ix.search(Qpin[a.warmup + s], [0], a.nprobe, kk)
+        e2e_s = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": total_q / e2e_s, "unit": UNIT, "h2d_bytes_per_step": a.batch * a.d * 4,
+               "d2h_bytes_per_step": a.batch * (kk * (8 + 4 + 8) + 4 + 8),
+               "path": "pk_search C-ABI, pinned host query buffer, results to host, per-step sync"}
+
+    # ---- CPU baseline (oracle port) + parity on the same sample, rank 0 only
+    cpu = parity = None
+    if rank == 0:
+        from oracle import oracle as O
+
+        threads = os.cpu_count() or 1
+        rows_h = Xs.cpu().numpy()
+        ids_h = ids_sorted.cpu().numpy()
+        cids_l = np.array([rank * a.nlist + c for c in live], dtype=np.int64)
+        flat = O.FlatIVF(rows_h, ids_h, offs[live], lens[live],
+                         np.stack([cent_tab[c] for c in cids_l]), cids_l)
+        sample = a.cpu_sample or min(a.batch, max(16, 4 * threads))
+        Qs = Qall_h[a.warmup * a.batch: a.warmup * a.batch + sample]
+        t_cpu, (r_ids, r_d, r_n, r_p, r_sc) = oracle_time(flat, Qs, a.nprobe, kk, threads)
+        cpu = {"value": sample / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"first {sample} queries of timed step 0 on this rank's shard, "
+                         f"C oracle (oracle/pancake_oracle.c), {threads} threads"}
+        if world == 1:
+            g = ix.search(Qs, [0], a.nprobe, kk, want_probe=True)
+            parity = {"queries": sample,
+                      "id_mismatch": int((g.ids != r_ids).sum()),
+                      "dist_bit_mismatch": int((g.dists.view(np.uint32) != r_d.view(np.uint32)).sum()),
+                      "probe_mismatch": int((g.probe != r_p).sum())}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "configs[1]: 1M x 768 fp32 IVF per GPU, nlist 1024 per GPU, "
+                                   "nprobe 32, k 10, batch 256 queries per step",
+                       "n_per_gpu": a.n, "d": a.d, "nlist_per_gpu": a.nlist, "nprobe": a.nprobe,
+                       "k": a.k, "batch": a.batch,
+                       "l2": "inputs larger than L2 (index 3.1 GB per GPU; each batch reads "
+                             "~all lists)",
+                       "parallelism": f"list-sharded x{world}" + (", NCCL all-gather top-k merge" if world > 1 else "")},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                         "kernel": "scan_kernel<SQ_L2> (fused posting-list scan + per-list top-k)",
+                         "algorithmic_bytes_per_launch": float(np.mean(alg_bytes)),
+                         "kernel_ms_per_launch": scan_ms, "peak_source": peak_src},
+            "stage_ms_per_step": {k_: v / max(ncalls, 1) for k_, v in stage_ms.items()},
+            "gpu_launches": a.steps * 5 + (a.steps if world > 1 else 0),
+            "clocks": clk.summary(),
+            "e2e": e2e, "cpu_baseline": cpu, "parity_vs_oracle": parity, "build_s": build_s,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    ix.close()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -111,6 +111,15 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags);
 
+/* ---- measurement ------------------------------------------------------ */
+/* Between begin and end every pk_search records CUDA events on the index
+ * stream around its stages: [0] input copy, [1] coarse distances,
+ * [2] coarse select, [3] routing, [4] fused scan, [5] merge + outputs.
+ * pk_profile_end synchronizes and returns the per-stage device time summed
+ * over the calls (ms) and the call count. */
+int pk_profile_begin(pk_index* ix);
+int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,7 +58,10 @@ _SIGS = [
     ("pk_list_read", [_vp, _i64, _vp, _vp], _int),
     ("pk_search", [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _int], _int),
     ("pk_assign", [_vp, _vp, _i64, _i32, _vp, _vp, _int], _int),
+    ("pk_profile_begin", [_vp], _int),
+    ("pk_profile_end", [_vp, _vp, _int, _i32p], _int),
 ]
+STAGES = ("input", "coarse_dist", "coarse_select", "route", "scan", "merge_out")
 EXPORTED = [s[0] for s in _SIGS]
 
 _lib = None

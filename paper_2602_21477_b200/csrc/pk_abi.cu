@@ -134,6 +134,23 @@ struct pk_index {
       assign_d;
   int chunk_rows = 512;
 
+  // stage timing (pk_profile_begin / pk_profile_end): events around each
+  // stage of every pk_search while enabled.
+  static constexpr int NSTAGE = 6;  // input, coarse dist, coarse select, route, scan, merge+output
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_ev;  // (NSTAGE+1) per call
+  int prof_calls = 0;
+  int prof_mark(int call, int stage) {
+    size_t i = (size_t)call * (NSTAGE + 1) + stage;
+    while (prof_ev.size() <= i) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      prof_ev.push_back(e);
+    }
+    CK(cudaEventRecord(prof_ev[i], st));
+    return PK_OK;
+  }
+
   ListTable table() const {
     ListTable t;
     t.rows = rows;
@@ -430,6 +447,7 @@ int pk_index_destroy(pk_index* ix) {
   cudaFree(ix->d_cid);
   cudaFree(ix->d_scope);
   cudaFree(ix->d_cent);
+  for (cudaEvent_t e : ix->prof_ev) cudaEventDestroy(e);
   for (DevBuf* b : {&ix->q, &ix->qnorm, &ix->dc, &ix->probe, &ix->probe_key, &ix->counts,
                     &ix->fillb, &ix->items, &ix->nitems, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list, &ix->work,
@@ -638,6 +656,10 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
   RET(ix->cand_list.ensure((size_t)max_items * 4));
   RET(ix->work.ensure(8));
   RET(ix->scopes.ensure(64 * 4));
+  const int pc = ix->prof_calls;
+#define PROF(stage) \
+  if (ix->prof) RET(ix->prof_mark(pc, stage))
+  PROF(0);
   // inputs
   CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
@@ -645,11 +667,14 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
                      dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   const ListTable lt = ix->table();
   if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
+  PROF(1);
   // 1. coarse quantizer: exact distances to every list centroid, select top-nprobe in scope
   launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
                     ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
+  PROF(2);
   launch_coarse_select(ix->dc.as<float>(), ns, (int)B, lt, ix->scopes.as<int32_t>(), nscopes,
                        nprobe, ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), st);
+  PROF(3);
   // 2. route (query -> lists) into (list -> queries) work items
   CK(cudaMemsetAsync(ix->counts.p, 0, (size_t)ns * 4, st));
   launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt, ix->chunk_rows, ix->counts.as<int32_t>(),
@@ -657,11 +682,13 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
                ix->qpairs.as<QPair>(), ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
   // 3. fused scan + per-(query, list chunk) top-kk
   CK(cudaMemsetAsync(ix->work.p, 0, 8, st));
+  PROF(4);
   launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
               ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(), (int)std::min<int64_t>(max_items, INT32_MAX),
               ix->qpairs.as<QPair>(), kk, ix->work.as<int32_t>(), ix->cand_key.as<uint32_t>(),
               ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
               ix->num_sms, st);
+  PROF(5);
   // 4. merge per query
   int64_t* o_ids = out_ids;
   float* o_d = out_dists;
@@ -691,6 +718,9 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
   } else if (out_scanned) {
     CK(cudaMemcpyAsync(out_scanned, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
   }
+  PROF(6);
+  if (ix->prof) ix->prof_calls++;
+#undef PROF
   if (out_probe) {
     // probe slots -> cids (host mirror); forces a sync
     std::vector<int32_t> ps((size_t)B * nprobe);
@@ -702,6 +732,30 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
                        dev ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost, st));
   }
   if (!dev || out_probe) CK(cudaStreamSynchronize(st));
+  return PK_OK;
+}
+
+int pk_profile_begin(pk_index* ix) {
+  ix->prof = true;
+  ix->prof_calls = 0;
+  return PK_OK;
+}
+
+int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls) {
+  CK(cudaStreamSynchronize(ix->st));
+  const int ns = std::min(nstages, pk_index::NSTAGE);
+  for (int k = 0; k < nstages; k++) stage_ms[k] = 0.0;
+  for (int c = 0; c < ix->prof_calls; c++) {
+    for (int k = 0; k < ns; k++) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ix->prof_ev[(size_t)c * (pk_index::NSTAGE + 1) + k],
+                              ix->prof_ev[(size_t)c * (pk_index::NSTAGE + 1) + k + 1]));
+      stage_ms[k] += ms;
+    }
+  }
+  *ncalls = ix->prof_calls;
+  ix->prof = false;
+  ix->prof_calls = 0;
   return PK_OK;
 }
 

@@ -72,6 +72,25 @@ class DeviceIndex:
                                        len(ids), N.ptr(cent), 0))
         return cent
 
+    def create_list_device(self, cid: int, scope_code: int, rows, ids) -> np.ndarray:
+        """rows/ids are device tensors ([n, d] f32 contiguous, [n] i64)."""
+        cent = np.empty(self.dimension, dtype=np.float32)
+        N.check(N.lib().pk_list_create(self._h, int(cid), int(scope_code), N.ptr(rows), N.ptr(ids),
+                                       int(ids.shape[0]), N.ptr(cent), N.PK_DEVICE_PTRS))
+        return cent
+
+    def stream_handle(self) -> int:
+        return int(N.lib().pk_stream(self._h) or 0)
+
+    def profile_begin(self):
+        N.check(N.lib().pk_profile_begin(self._h))
+
+    def profile_end(self):
+        out = np.zeros(len(N.STAGES), dtype=np.float64)
+        calls = ctypes.c_int32(0)
+        N.check(N.lib().pk_profile_end(self._h, N.ptr(out), len(out), ctypes.byref(calls)))
+        return dict(zip(N.STAGES, out.tolist())), int(calls.value)
+
     def append(self, cid: int, rows, ids):
         rows = N.f32(rows, self.dimension)
         ids = np.ascontiguousarray(ids, dtype=np.int64)

@@ -1,0 +1,124 @@
+"""Host-side logic that needs no GPU: config validation, PNCK exchange format,
+scope interning, locking, the graph-RNG mirror, shard planning."""
+
+import os
+import struct
+import threading
+
+import numpy as np
+import pytest
+
+from paper_2602_21477_b200 import Metric, ParseError, StoreConfig, UsageError, VersionMismatchError
+from paper_2602_21477_b200.clusters import CoarseRngMirror
+from paper_2602_21477_b200.concurrency import RWLock, TaskRunner
+from paper_2602_21477_b200.engine import OperationBatch, ScopeCodes, profile_promote, profile_reorder
+from paper_2602_21477_b200.pnck import read_pnck, write_pnck
+
+
+class TestConfig:
+    def test_defaults_match_reference(self):
+        c = StoreConfig(dimension=8)
+        assert (c.split_threshold, c.split_target, c.maintenance_interval) == (4096, 2048, 256)
+        assert (c.kappa, c.alpha_et, c.b_insert, c.default_nprobe) == (2, 0.7, 128, 8)
+        assert c.metric is Metric.SQUARED_EUCLIDEAN
+
+    @pytest.mark.parametrize("kw", [dict(dimension=0), dict(dimension=4, alpha_et=1.5),
+                                    dict(dimension=4, split_target=10, split_threshold=10),
+                                    dict(dimension=4, coarse_mode="x"), dict(dimension=4, accelerator="gpu")])
+    def test_invalid(self, kw):
+        with pytest.raises(UsageError):
+            StoreConfig(**kw)
+
+    def test_metric_string(self):
+        assert StoreConfig(dimension=3, metric="cosine").metric is Metric.COSINE
+
+    def test_batch_kind(self):
+        with pytest.raises(UsageError):
+            OperationBatch("frobnicate", None, [])
+
+
+class TestPnck:
+    def test_round_trip(self, tmp_path):
+        rng = np.random.default_rng(0)
+        d = 5
+        cl = [(rng.normal(size=d).astype(np.float32), np.array([3, 1, 2 ** 40]),
+               rng.normal(size=(3, d)).astype(np.float32)),
+              (np.zeros(d, np.float32), np.array([], dtype=np.int64), np.zeros((0, d), np.float32))]
+        p = tmp_path / "x.pnck"
+        write_pnck(p, d, Metric.COSINE, cl, sections=[(b"META", b"{}")])
+        dim, metric, recs = read_pnck(p)
+        assert dim == d and metric is Metric.COSINE and len(recs) == 2
+        assert recs[0][1].tolist() == [3, 1, 2 ** 40]
+        assert np.array_equal(recs[0][2], cl[0][2]) and np.array_equal(recs[0][0], cl[0][0])
+        assert len(recs[1][1]) == 0
+
+    def test_layout_bytes(self, tmp_path):
+        """Byte layout of ref/persist.py:66-94."""
+        p = tmp_path / "y.pnck"
+        write_pnck(p, 2, Metric.SQUARED_EUCLIDEAN, [(np.array([1, 2], np.float32), np.array([7]),
+                                                     np.array([[3, 4]], np.float32))])
+        b = open(p, "rb").read()
+        want = b"PNCK" + struct.pack("<IIB", 1, 2, 0) + struct.pack("<I", 1)
+        want += struct.pack("<2f", 1, 2) + struct.pack("<I", 1) + struct.pack("<Q", 7) + struct.pack("<2f", 3, 4)
+        assert b == want
+
+    def test_errors(self, tmp_path):
+        p = tmp_path / "z.pnck"
+        p.write_bytes(b"NOPE")
+        with pytest.raises(ParseError):
+            read_pnck(p)
+        p.write_bytes(b"PNCK" + struct.pack("<IIB", 2, 4, 0))
+        with pytest.raises(VersionMismatchError):
+            read_pnck(p)
+        p.write_bytes(b"PNCK" + struct.pack("<IIB", 1, 4, 0) + struct.pack("<I", 1) + b"\0" * 10)
+        with pytest.raises(ParseError):
+            read_pnck(p)
+
+
+def test_scope_codes():
+    s = ScopeCodes()
+    assert s.intern("static") == 0 and s.intern("a") == 1 and s.intern("static") == 0
+    assert s.mask_codes(["a", "static"]).tolist() == [0, 1]
+
+
+def test_profiles():
+    assert profile_reorder([3, 1, 9], [0, 1, 2, 3]) == [3, 1, 0, 2]
+    assert profile_promote([1, 2, 3], [3, 5, 3], 3) == [3, 5, 1]
+
+
+def test_rwlock_and_runner():
+    lock = RWLock()
+    hits = []
+
+    def reader():
+        with lock.read():
+            hits.append(1)
+
+    ts = [threading.Thread(target=reader) for _ in range(4)]
+    with lock.write():
+        for t in ts:
+            t.start()
+    for t in ts:
+        t.join()
+    assert len(hits) == 4
+    r = TaskRunner(0)
+    assert r.submit("search", lambda x: x + 1, 1).result() == 2
+    r2 = TaskRunner(4)
+    assert r2.submit("update", lambda: 5).result() == 5
+    r2.shutdown()
+
+
+def test_coarse_rng_mirror_matches_model():
+    """Same draws as the oracle store model's graph-insert restatement."""
+    from oracle.store_model import StoreModel
+
+    m = StoreModel(4, seed=9)
+    m.register("a")
+    rng = np.random.default_rng(np.random.PCG64(9))
+    mirror = CoarseRngMirror(rng)
+    mirror.register_scope("static")
+    mirror.register_scope("a")
+    for scope in ["static", "a", "static", "a", "a", "static"]:
+        m._graph_insert(scope)
+        mirror.on_insert(scope)
+    assert m.rng.random() == rng.random()

@@ -1,0 +1,104 @@
+"""The oracle (oracle/pancake_oracle.c + oracle/store_model.py) against the
+golden vectors produced by the reference itself (tests/golden/make_golden.py).
+CPU only: this pins the checker before it is trusted to judge the GPU path."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from oracle.store_model import bulk_build_model
+from replay import compare_records, gen, load_golden, replay_model
+
+
+def bits(a):
+    return np.asarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.fixture(scope="module")
+def kern():
+    return load_golden("kernels.npz")
+
+
+@pytest.mark.parametrize("case", gen.KERNEL_CASES, ids=[c[0] for c in gen.KERNEL_CASES])
+def test_oracle_kernels_bit_exact(kern, case):
+    name, d, n, kind = case
+    q, mat, cents = gen.kernel_case(name, d, n, kind)
+    assert gen.digest(q, mat, cents) == str(kern[f"{name}/digest"])
+    assert np.array_equal(bits(O.sq_l2(q, mat)), bits(kern[f"{name}/sq_l2"]))
+    assert np.array_equal(bits(O.neg_ip(q, mat)), bits(kern[f"{name}/neg_ip"]))
+    if f"{name}/cosine" in kern:
+        assert np.array_equal(bits(O.cosine(q, mat)), bits(kern[f"{name}/cosine"]))
+    lab, dist = O.kmeans_assign(mat, cents)
+    assert np.array_equal(lab, kern[f"{name}/km_labels"])
+    assert np.array_equal(dist.view(np.uint64), kern[f"{name}/km_dists"].view(np.uint64))
+    assert np.array_equal(bits(O.centroid(mat)), bits(kern[f"{name}/centroid"]))
+
+
+def test_oracle_fma_emulation_would_fail(kern):
+    """Guard that the fixtures discriminate: fused (FMA) accumulation differs."""
+    q, mat, _ = gen.kernel_case("d768", 768, 29, "unit")
+    fused = np.zeros(len(mat), dtype=np.float32)
+    for j in range(768):
+        t = (mat[:, j] - q[j]).astype(np.float64)
+        fused = (fused.astype(np.float64) + t * t).astype(np.float32)
+    assert not np.array_equal(bits(fused), bits(kern["d768/sq_l2"]))
+
+
+def test_oracle_assign_nearest_ties():
+    g = load_golden("assign.npz")
+    got = np.array([O.assign_nearest(q, g["cents"], g["cids"]) for q in g["qs"]])
+    assert np.array_equal(got, g["got"])
+    assert got[-3] == got[-2] == 2  # duplicate centroids -> lower cid
+
+
+@pytest.mark.parametrize("name", list(gen.TRACE_SPECS))
+def test_store_model_matches_reference_trace(name):
+    want = load_golden(f"trace_{name}.npz")
+    got = replay_model(gen.TRACE_SPECS[name])
+    mism = compare_records(got, want)
+    assert not mism, "\n".join(mism[:10])
+
+
+def test_bulk_build_model_matches_reference():
+    g = load_golden("bulk.npz")
+    x, qs = gen.bulk_case()
+    assert gen.digest(x, qs) == str(g["digest"])
+    m, ids = bulk_build_model(x, seed=3, split_target=200)
+    cids = sorted(m.clusters)
+    assert np.array_equal(np.array(ids), g["ids"])
+    assert np.array_equal(np.array(cids), g["cids"])
+    assert np.array_equal(np.concatenate([m.clusters[c].ids for c in cids]), g["members"])
+    assert np.array_equal(bits(np.stack([m.clusters[c].centroid for c in cids])), bits(g["centroids"]))
+    assert m.rng.random() == float(g["rng"])
+    for i, q in enumerate(qs):
+        hits, _, _ = m.search(["static"], q, 10, 3)
+        assert [h[0] for h in hits] == g[f"q{i}/ids"].tolist()
+        assert np.array_equal(bits([h[1] for h in hits]), bits(g[f"q{i}/d"]))
+
+
+def test_flat_ivf_matches_store_model():
+    """The arena-form flat IVF search (used at bench scale) equals the store
+    model's search on the same lists."""
+    rng = np.random.default_rng(3)
+    d, nl = 24, 12
+    lists = []
+    nid = 0
+    for c in range(nl):
+        n = int(rng.integers(0 if c == 3 else 1, 90))
+        lists.append((np.arange(nid, nid + n), rng.normal(size=(n, d)).astype(np.float32)))
+        nid += n
+    cents = rng.normal(size=(nl, d)).astype(np.float32)
+    flat = O.FlatIVF.from_lists(lists, cents, np.arange(nl) * 3 + 1)
+    Q = rng.normal(size=(17, d)).astype(np.float32)
+    ids, dd, cnt, probe, scanned = flat.search(Q, nprobe=4, kk=7, threads=3)
+    for b in range(len(Q)):
+        dc = O.sq_l2(Q[b], cents)
+        ca = np.arange(nl) * 3 + 1
+        p = ca[np.lexsort((ca, dc))[:4]]
+        assert probe[b].tolist() == p.tolist()
+        allid = np.concatenate([lists[(c - 1) // 3][0] for c in p])
+        alld = np.concatenate([O.sq_l2(Q[b], lists[(c - 1) // 3][1]) for c in p])
+        o = np.lexsort((allid, alld))[:7]
+        assert ids[b, :cnt[b]].tolist() == allid[o].tolist()
+        assert np.array_equal(bits(dd[b, :cnt[b]]), bits(alld[o]))
+        assert scanned[b] == len(allid)
