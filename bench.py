@@ -372,6 +372,14 @@ def run_ours(a):
         pr = np.unique(out.probe[out.probe >= 0])
         loc = pr[(pr // a.nlist) == rank] % a.nlist
         alg_bytes.append(float(lens[loc].sum()) * row_bytes)
+    pool = None
+    try:
+        out = ix.search(Qall_h[a.warmup * a.batch:(a.warmup + 1) * a.batch], [0], a.nprobe, kk)
+        pc = ix.pool_counts(a.batch)
+        pool = {"mean": float(pc.mean()), "max": int(pc.max()), "p50": float(np.median(pc)),
+                "rows_reranked_per_step": int(pc.sum())}
+    except Exception:
+        pass
     scan_ms = stage_ms["scan"] / max(ncalls, 1)
     achieved = float(np.mean(alg_bytes)) / (scan_ms / 1000.0) / 1e9
     peak, peak_src = load_peaks()
@@ -442,6 +450,7 @@ def run_ours(a):
             "gpu_launches": a.steps * 5 + (a.steps if world > 1 else 0),
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu, "parity_vs_oracle": parity, "build_s": build_s,
+            "screen_candidates_per_query": pool,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -119,6 +119,9 @@ int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64
  * over the calls (ms) and the call count. */
 int pk_profile_begin(pk_index* ix);
 int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls);
+/* Candidate-pool size per query of the last screened search (host int32[B]);
+ * values above the pool capacity mean that query took the exact overflow path. */
+int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B);
 
 #ifdef __cplusplus
 }

@@ -60,6 +60,7 @@ _SIGS = [
     ("pk_assign", [_vp, _vp, _i64, _i32, _vp, _vp, _int], _int),
     ("pk_profile_begin", [_vp], _int),
     ("pk_profile_end", [_vp, _vp, _int, _i32p], _int),
+    ("pk_debug_pool_counts", [_vp, _vp, _i64], _int),
 ]
 STAGES = ("input", "coarse_dist", "coarse_select", "route", "scan", "merge_out")
 EXPORTED = [s[0] for s in _SIGS]

@@ -133,6 +133,9 @@ struct pk_index {
       cand_key, cand_id, cand_n, cand_list, work, out_ids, out_d, out_cid, out_n, scopes, assign_c,
       assign_d;
   int chunk_rows = 512;
+  bool screen = true;  // FFMA screen + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
+  int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
+  DevBuf qnorm2, uq, cpool, ccount, ckey;
 
   // stage timing (pk_profile_begin / pk_profile_end): events around each
   // stage of every pk_search while enabled.
@@ -421,6 +424,10 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   ix->metric = metric;
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (const char* e = getenv("PK_CHUNK_ROWS")) ix->chunk_rows = std::max(TILE, atoi(e) / TILE * TILE);
+  if (const char* e = getenv("PK_SCAN_EXACT")) ix->screen = atoi(e) == 0;
+  if (const char* e = getenv("PK_POOL_CAP")) ix->pool_cap = std::max(1, atoi(e));
+  if (metric == COSINE) ix->screen = false;
+  if (ix->screen) ix->chunk_rows = std::min(ix->chunk_rows, 2 * TILE);
   cudaError_t e = cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     delete ix;
@@ -452,7 +459,7 @@ int pk_index_destroy(pk_index* ix) {
                     &ix->fillb, &ix->items, &ix->nitems, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list, &ix->work,
                     &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d})
+                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -667,6 +674,10 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
                      dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   const ListTable lt = ix->table();
   if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
+  if (ix->screen) {
+    RET(ix->qnorm2.ensure(B * 4));
+    launch_qnorm2(ix->q.as<float>(), dp, (int)B, (int)dp, ix->qnorm2.as<float>(), st);
+  }
   PROF(1);
   // 1. coarse quantizer: exact distances to every list centroid, select top-nprobe in scope
   launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
@@ -683,11 +694,24 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
   // 3. fused scan + per-(query, list chunk) top-kk
   CK(cudaMemsetAsync(ix->work.p, 0, 8, st));
   PROF(4);
-  launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
-              ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(), (int)std::min<int64_t>(max_items, INT32_MAX),
-              ix->qpairs.as<QPair>(), kk, ix->work.as<int32_t>(), ix->cand_key.as<uint32_t>(),
-              ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
-              ix->num_sms, st);
+  if (ix->screen) {
+    RET(ix->uq.ensure((size_t)B * 4));
+    RET(ix->ccount.ensure((size_t)B * 4));
+    RET(ix->cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));
+    CK(cudaMemsetAsync(ix->uq.p, 0xff, (size_t)B * 4, st));
+    CK(cudaMemsetAsync(ix->ccount.p, 0, (size_t)B * 4, st));
+    launch_scan_screen(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
+                       ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
+                       (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
+                       ix->work.as<int32_t>(), ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
+                       ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
+                       ix->pool_cap, ix->num_sms, st);
+  } else
+    launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
+                ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(), (int)std::min<int64_t>(max_items, INT32_MAX),
+                ix->qpairs.as<QPair>(), kk, ix->work.as<int32_t>(), ix->cand_key.as<uint32_t>(),
+                ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
+                ix->num_sms, st);
   PROF(5);
   // 4. merge per query
   int64_t* o_ids = out_ids;
@@ -704,9 +728,15 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
     o_cid = ix->out_cid.as<int64_t>();
     o_n = ix->out_n.as<int32_t>();
   }
-  launch_merge((int)B, ix->slot_off.as<int32_t>(), ix->cand_key.as<uint32_t>(),
-               ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(), kk,
-               lt, o_ids, o_d, o_cid, o_n, st);
+  if (ix->screen)
+    launch_rerank_merge(ix->metric, (int)B, ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
+                        ix->pool_cap, ix->cand_key.as<uint32_t>(), ix->cand_n.as<int32_t>(),
+                        ix->slot_off.as<int32_t>(), lt, ix->q.as<float>(), ix->probe.as<int32_t>(),
+                        nprobe, kk, o_ids, o_d, o_cid, o_n, st);
+  else
+    launch_merge((int)B, ix->slot_off.as<int32_t>(), ix->cand_key.as<uint32_t>(),
+                 ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(), kk,
+                 lt, o_ids, o_d, o_cid, o_n, st);
   CK(cudaGetLastError());
   if (!dev) {
     CK(cudaMemcpyAsync(out_ids, o_ids, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
@@ -732,6 +762,14 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
                        dev ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost, st));
   }
   if (!dev || out_probe) CK(cudaStreamSynchronize(st));
+  return PK_OK;
+}
+
+int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B) {
+  if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
+  if ((size_t)B * 4 > ix->ccount.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
+  CK(cudaMemcpyAsync(out, ix->ccount.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
+  CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 

@@ -534,7 +534,11 @@ size_t scan_smem_bytes() { return ScanLayout::TOTAL + 1024; }
 struct ScanShared {
   float* X;
   float* Qc;
-  float* D;
+  float* D;      // exact kernel: [QG][TILE] tile distances
+  float* A;      // screen kernel: [QG][CHUNK_MAX] screened (then exact) distances
+  float* NX;     // screen kernel: [CHUNK_MAX] row norms
+  uint16_t* CR;  // screen kernel: [QG][CHUNK_MAX] candidate rows
+  int32_t* Cn;   // screen kernel: [QG] candidate counts
   uint32_t* Lkey;
   int64_t* Lid;
   int32_t* Ln;
@@ -604,39 +608,11 @@ __device__ __forceinline__ void sort8(uint32_t* k, int64_t* i) {
 #undef PK_CE
 }
 
-// Merge this tile's survivors for query a into its sorted list (warp-wide).
-__device__ void topk_merge_tile(const ScanShared& S, int a, int rows, const int64_t* __restrict__ ids,
-                                int64_t idbase, int kk) {
+// Merge up to 8 lane-local (key, id) candidates per lane (unsorted, KEY_NONE
+// padded) into query a's sorted list of at most kk entries (warp-wide).
+__device__ __forceinline__ void warp_merge_into_list(const ScanShared& S, int a, int kk, uint32_t* ck, int64_t* ci) {
   const int lane = threadIdx.x & 31;
-  const float* dq = S.D + a * TILE;
   const int n_old = S.Ln[a];
-  uint32_t tk = KEY_NONE;
-  int64_t ti = ID_NONE;
-  if (n_old == kk) {
-    tk = S.Lkey[a * KKMAX + kk - 1];
-    ti = S.Lid[a * KKMAX + kk - 1];
-  }
-  uint32_t ck[8];
-  int64_t ci[8];
-  bool have = false;
-#pragma unroll
-  for (int i = 0; i < 8; i++) {
-    const int row = lane + 32 * i;
-    ck[i] = KEY_NONE;
-    ci[i] = ID_NONE;
-    if (row < rows) {
-      uint32_t k = f2key(dq[row]);
-      if (k <= tk) {
-        int64_t id = ids[idbase + row];
-        if (lex_less(k, id, tk, ti)) {
-          ck[i] = k;
-          ci[i] = id;
-          have = true;
-        }
-      }
-    }
-  }
-  if (!__any_sync(FULL, have)) return;
   sort8(ck, ci);
   // old list: lane holds entries lane and lane+32
   uint32_t ok0 = KEY_NONE, ok1 = KEY_NONE;
@@ -723,6 +699,112 @@ __device__ void topk_merge_tile(const ScanShared& S, int a, int rows, const int6
   __syncwarp();
 }
 
+// Merge this tile's survivors for query a into its sorted list (warp-wide).
+__device__ void topk_merge_tile(const ScanShared& S, int a, int rows, const int64_t* __restrict__ ids,
+                                int64_t idbase, int kk) {
+  const int lane = threadIdx.x & 31;
+  const float* dq = S.D + a * TILE;
+  const int n_old = S.Ln[a];
+  uint32_t tk = KEY_NONE;
+  int64_t ti = ID_NONE;
+  if (n_old == kk) {
+    tk = S.Lkey[a * KKMAX + kk - 1];
+    ti = S.Lid[a * KKMAX + kk - 1];
+  }
+  uint32_t ck[8];
+  int64_t ci[8];
+  bool have = false;
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const int row = lane + 32 * i;
+    ck[i] = KEY_NONE;
+    ci[i] = ID_NONE;
+    if (row < rows) {
+      uint32_t k = f2key(dq[row]);
+      if (k <= tk) {
+        int64_t id = ids[idbase + row];
+        if (lex_less(k, id, tk, ti)) {
+          ck[i] = k;
+          ci[i] = id;
+          have = true;
+        }
+      }
+    }
+  }
+  if (!__any_sync(FULL, have)) return;
+  warp_merge_into_list(S, a, kk, ck, ci);
+}
+
+// Producer warp of the persistent scans: claims work items, publishes them
+// through a 2-deep ring, and streams each item's row tiles (TMA 2-D,
+// SWIZZLE_128B, box heights 256..8 to cover ragged tails) and the matching
+// 128-byte query chunks (bulk copies) through the STAGES-deep stage ring.
+__device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMaps& maps,
+                                              const ListTable& lt, const float* __restrict__ Qd,
+                                              const ScanItem* __restrict__ items, int n_items,
+                                              const QPair* __restrict__ qpairs,
+                                              int32_t* __restrict__ work_ctr, int nchunk_d,
+                                              bool keep_in_l2) {
+  const int lane = threadIdx.x & 31;
+  if (lane == 0)
+    for (int i = 0; i < NBOX; i++) tma_prefetch_desc(&maps.box[i]);
+  const uint64_t pol = keep_in_l2 ? policy_evict_normal() : policy_evict_first();
+  int s = 0, r = 0;
+  uint32_t ph = 0, rph = 0;
+  for (;;) {
+    int it = 0;
+    if (lane == 0) it = atomicAdd(work_ctr, 1);
+    it = __shfl_sync(FULL, it, 0);
+    ScanItem item;
+    if (it < n_items) {
+      item = items[it];
+    } else {
+      item.nq = -1;
+    }
+    mbar_wait(&S.rempty[r], rph ^ 1);
+    if (lane == 0) {
+      S.ring[r] = item;
+      mbar_arrive(&S.rfull[r]);
+    }
+    if (++r == 2) {
+      r = 0;
+      rph ^= 1;
+    }
+    if (item.nq < 0) break;
+    const int64_t rbase = lt.off[item.lslot] + item.row0;
+    const int qb = lane < item.nq ? qpairs[item.qoff + lane].b : 0;
+    const float* qrow = Qd + (int64_t)qb * lt.dp;
+    for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+      const int rows = min(TILE, item.nrows - t0);
+      const int rows8 = (rows + 7) & ~7;
+      const uint32_t bytes = (uint32_t)(rows8 * DC * 4 + item.nq * DC * 4);
+      for (int c = 0; c < nchunk_d; c++) {
+        mbar_wait(&S.empty[s], ph ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&S.full[s], bytes);
+          int r0 = 0;
+#pragma unroll
+          for (int bi = 0; bi < NBOX; bi++) {
+            const int h = TILE >> bi;
+            if (rows8 - r0 >= h) {
+              tma_load_2d(S.X + (size_t)s * TILE * DC + r0 * DC, &maps.box[bi], &S.full[s],
+                          c * DC, (int)(rbase + t0 + r0), pol);
+              r0 += h;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane < item.nq)
+          bulk_g2s(S.Qc + (size_t)s * QG * DC + lane * DC, qrow + c * DC, DC * 4, &S.full[s]);
+        if (++s == STAGES) {
+          s = 0;
+          ph ^= 1;
+        }
+      }
+    }
+  }
+}
+
 template <int METRIC>
 __global__ void __launch_bounds__(SCAN_THREADS, 1)
     scan_kernel(const __grid_constant__ ArenaMaps maps, ListTable lt, const float* __restrict__ Qd,
@@ -771,64 +853,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   const int n_items = *n_items_p;
 
   if (warp == NCW) {
-    // ------------------------------------------------ producer warp
-    if (lane == 0)
-      for (int i = 0; i < NBOX; i++) tma_prefetch_desc(&maps.box[i]);
-    const uint64_t pol = policy_evict_first();
-    int s = 0, r = 0;
-    uint32_t ph = 0, rph = 0;
-    for (;;) {
-      int it = 0;
-      if (lane == 0) it = atomicAdd(work_ctr, 1);
-      it = __shfl_sync(FULL, it, 0);
-      ScanItem item;
-      if (it < n_items) {
-        item = items[it];
-      } else {
-        item.nq = -1;
-      }
-      mbar_wait(&S.rempty[r], rph ^ 1);
-      if (lane == 0) {
-        S.ring[r] = item;
-        mbar_arrive(&S.rfull[r]);
-      }
-      if (++r == 2) {
-        r = 0;
-        rph ^= 1;
-      }
-      if (item.nq < 0) break;
-      const int64_t rbase = lt.off[item.lslot] + item.row0;
-      const int qb = lane < item.nq ? qpairs[item.qoff + lane].b : 0;
-      const float* qrow = Qd + (int64_t)qb * lt.dp;
-      for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
-        const int rows = min(TILE, item.nrows - t0);
-        const int rows8 = (rows + 7) & ~7;
-        const uint32_t bytes = (uint32_t)(rows8 * DC * 4 + item.nq * DC * 4);
-        for (int c = 0; c < nchunk_d; c++) {
-          mbar_wait(&S.empty[s], ph ^ 1);
-          if (lane == 0) {
-            mbar_arrive_expect_tx(&S.full[s], bytes);
-            int r0 = 0;
-#pragma unroll
-            for (int bi = 0; bi < NBOX; bi++) {
-              const int h = TILE >> bi;
-              if (rows8 - r0 >= h) {
-                tma_load_2d(S.X + (size_t)s * TILE * DC + r0 * DC, &maps.box[bi], &S.full[s],
-                            c * DC, (int)(rbase + t0 + r0), pol);
-                r0 += h;
-              }
-            }
-          }
-          __syncwarp();
-          if (lane < item.nq)
-            bulk_g2s(S.Qc + (size_t)s * QG * DC + lane * DC, qrow + c * DC, DC * 4, &S.full[s]);
-          if (++s == STAGES) {
-            s = 0;
-            ph ^= 1;
-          }
-        }
-      }
-    }
+    scan_producer(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false);
     return;
   }
 
@@ -1020,6 +1045,510 @@ void launch_merge(int B, const int32_t* slot_off, const uint32_t* cand_key, cons
   cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   merge_kernel<<<B, 128, smem, st>>>(slot_off, cand_key, cand_id, cand_n, cand_list, kk, lt,
                                      out_ids, out_d, out_cid, out_n);
+}
+
+// =====================================================================
+// Screened fused scan (sq_l2 and neg_ip) + exact re-rank.
+//
+// The exact reference distance costs 3 separately rounded FP32 ops per
+// (query, element) -- more FP32 issue than HBM delivers elements at ~8 queries
+// per list.  The screen kernel streams the same tiles
+// but computes, per (row, query), an FFMA approximation with a PROVEN error
+// bound eps against the reference value E:
+//   sq_l2: A = (nx + nq) - 2 dot,  nx = sum x*x, dot = sum x*q (FFMA chains)
+//   neg_ip: A = -dot
+//   |A - E| <= eps = coef * (nx + nq)    (coef from d, screen_coef())
+// Per (item, query) U_item = kk-th smallest (A + eps) over the item's rows is
+// an upper bound of the query's final kk-th exact distance; the query's global
+// bound Uq[b] is the atomic min of those.  A row can only be in the query's
+// top-kk if A - eps <= Uq[b] (kk rows have E <= A + eps <= Uq), so exactly
+// those rows are appended to the query's candidate pool, and
+// rerank_merge_kernel computes their reference distances and the top-kk.
+// Directed rounding (ru/rd) keeps the bound valid through the fp32 ops;
+// non-finite values become unconditional candidates.
+// =====================================================================
+constexpr int CHUNK_MAX = 2 * TILE;  // rows per screened work item
+
+struct ScreenLayout {
+  static constexpr size_t X_BYTES = (size_t)STAGES * TILE * DC * 4;
+  static constexpr size_t QC_BYTES = (size_t)STAGES * QG * DC * 4;
+  static constexpr size_t A_BYTES = (size_t)QG * CHUNK_MAX * 4;
+  static constexpr size_t NX_BYTES = (size_t)CHUNK_MAX * 4;
+  static constexpr size_t BAR_BYTES = 256;
+  static constexpr size_t RING_BYTES = 2 * sizeof(ScanItem);
+  static constexpr size_t TOTAL = X_BYTES + QC_BYTES + A_BYTES + NX_BYTES + BAR_BYTES + RING_BYTES;
+};
+size_t screen_smem_bytes() { return ScreenLayout::TOTAL + 1024; }
+
+// FFMA screen of one tile: this thread's row against NQ queries.
+template <int METRIC, int NQ>
+__device__ __forceinline__ void screen_tile(const ScanShared& S, int nchunk_d, int& s, uint32_t& ph,
+                                            int nq, int tile_row0, const float* nq2_s) {
+  const int row = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int swz = row & 7;
+  float acc[NQ];
+#pragma unroll
+  for (int a = 0; a < NQ; a++) acc[a] = 0.f;
+  float nx = 0.f;
+  for (int c = 0; c < nchunk_d; c++) {
+    mbar_wait(&S.full[s], ph);
+    const float* xs = S.X + (size_t)s * TILE * DC + row * DC;
+    const float* qs = S.Qc + (size_t)s * QG * DC;
+#pragma unroll
+    for (int k = 0; k < DC / 4; k++) {
+      const float4 x = *reinterpret_cast<const float4*>(xs + ((k ^ swz) << 2));
+      nx = __fmaf_rn(x.x, x.x, nx);
+      nx = __fmaf_rn(x.y, x.y, nx);
+      nx = __fmaf_rn(x.z, x.z, nx);
+      nx = __fmaf_rn(x.w, x.w, nx);
+#pragma unroll
+      for (int a = 0; a < NQ; a++) {
+        const float4 q = *reinterpret_cast<const float4*>(qs + a * DC + (k << 2));
+        acc[a] = __fmaf_rn(x.x, q.x, acc[a]);
+        acc[a] = __fmaf_rn(x.y, q.y, acc[a]);
+        acc[a] = __fmaf_rn(x.z, q.z, acc[a]);
+        acc[a] = __fmaf_rn(x.w, q.w, acc[a]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.empty[s]);
+    if (++s == STAGES) {
+      s = 0;
+      ph ^= 1;
+    }
+  }
+  S.NX[tile_row0 + row] = nx;
+#pragma unroll
+  for (int a = 0; a < NQ; a++) {
+    if (a < nq) {
+      float A;
+      if (METRIC == SQ_L2) A = __fsub_rn(__fadd_rn(nx, nq2_s[a]), __fmul_rn(2.f, acc[a]));
+      else A = -acc[a];
+      S.A[a * CHUNK_MAX + tile_row0 + row] = A;
+    }
+  }
+}
+
+// Per (item, query a): publish the item's kk smallest upper bounds (hi) to
+// the (query, item) slot, tighten the query's running bound Uq with the
+// item's kk-th smallest hi, and append every row whose lower bound (lo) is
+// not above min(U_item, Uq) to the query's pool together with lo.
+__device__ __forceinline__ void screen_select(const ScanShared& S, int a, int R, int kk, float coef,
+                                              float nqa, int b, int lslot, int64_t rbase,
+                                              int64_t slot, uint32_t* __restrict__ Uq,
+                                              uint32_t* __restrict__ slot_hi,
+                                              int32_t* __restrict__ slot_n,
+                                              int4* __restrict__ cpool,
+                                              int32_t* __restrict__ ccount, int cap) {
+  const int lane = threadIdx.x & 31;
+  constexpr int PER = CHUNK_MAX / 32;
+  uint32_t hk[PER], lk[PER];
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int row = lane + 32 * i;
+    hk[i] = KEY_NONE;
+    lk[i] = KEY_NONE;
+    if (row < R) {
+      const float A = S.A[a * CHUNK_MAX + row];
+      const float eps = __fmul_ru(coef, __fadd_ru(S.NX[row], nqa));
+      float hi = __fadd_ru(A, eps), lo = __fsub_rd(A, eps);
+      if (!isfinite(hi) || !isfinite(lo)) {
+        hi = __int_as_float(0x7f800000);
+        lo = __int_as_float(0xff800000);
+      }
+      hk[i] = f2key(hi);
+      lk[i] = f2key(lo);
+    }
+  }
+  // U_item = kk-th smallest hi of the item (KEY_NONE when R < kk)
+  uint32_t Uitem = KEY_NONE;
+  if (R >= kk) {
+    uint32_t mn = KEY_NONE, mx = 0;
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+      if (lane + 32 * i < R) {
+        mn = min(mn, hk[i]);
+        mx = max(mx, hk[i]);
+      }
+    }
+    uint32_t L = __reduce_min_sync(FULL, mn), H = __reduce_max_sync(FULL, mx);
+    while (L < H) {
+      const uint32_t mid = L + ((H - L) >> 1);
+      unsigned cc = 0;
+#pragma unroll
+      for (int i = 0; i < PER; i++) cc += (hk[i] <= mid);
+      if (__reduce_add_sync(FULL, cc) >= (unsigned)kk) H = mid;
+      else L = mid + 1;
+    }
+    Uitem = L;
+    if (lane == 0) atomicMin(&Uq[b], Uitem);
+  }
+  // the item's kk smallest hi: every hi < U_item, then U_item repeated
+  {
+    int base = 0;
+#pragma unroll
+    for (int i = 0; i < PER; i++) {
+      const bool below = (lane + 32 * i < R) && hk[i] < Uitem;
+      const unsigned bal = __ballot_sync(FULL, below);
+      if (below) slot_hi[slot * kk + base + __popc(bal & ((1u << lane) - 1u))] = hk[i];
+      base += __popc(bal);
+    }
+    const int nfill = (R >= kk) ? kk : R;
+    for (int l = base + lane; l < nfill; l += 32) slot_hi[slot * kk + l] = Uitem;
+    if (lane == 0) slot_n[slot] = nfill;
+  }
+  const uint32_t U = min(Uitem, *(volatile uint32_t*)&Uq[b]);
+  unsigned tot = 0;
+#pragma unroll
+  for (int i = 0; i < PER; i++) tot += (lane + 32 * i < R && lk[i] <= U);
+  tot = __reduce_add_sync(FULL, tot);
+  if (tot == 0) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(&ccount[b], (int)tot);
+  base = __shfl_sync(FULL, base, 0);
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int row = lane + 32 * i;
+    const bool cand = row < R && lk[i] <= U;
+    const unsigned bal = __ballot_sync(FULL, cand);
+    const int pos = base + __popc(bal & ((1u << lane) - 1u));
+    if (cand && pos < cap)
+      cpool[(int64_t)b * cap + pos] = make_int4((int)(rbase + row), lslot, (int)lk[i], 0);
+    base += __popc(bal);
+  }
+}
+
+template <int METRIC>
+__global__ void __launch_bounds__(SCAN_THREADS, 1)
+    scan_screen_kernel(const __grid_constant__ ArenaMaps maps, ListTable lt,
+                       const float* __restrict__ Qd, const float* __restrict__ qnorm2,
+                       const ScanItem* __restrict__ items, const int32_t* __restrict__ n_items_p,
+                       const QPair* __restrict__ qpairs, int kk, float coef,
+                       int32_t* __restrict__ work_ctr, uint32_t* __restrict__ Uq,
+                       uint32_t* __restrict__ slot_hi, int32_t* __restrict__ slot_n,
+                       int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  ScanShared S;
+  uint8_t* p = base;
+  S.X = reinterpret_cast<float*>(p);
+  p += ScreenLayout::X_BYTES;
+  S.Qc = reinterpret_cast<float*>(p);
+  p += ScreenLayout::QC_BYTES;
+  S.A = reinterpret_cast<float*>(p);
+  p += ScreenLayout::A_BYTES;
+  S.NX = reinterpret_cast<float*>(p);
+  p += ScreenLayout::NX_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p);
+  S.full = bars;
+  S.empty = bars + STAGES;
+  S.rfull = bars + 2 * STAGES;
+  S.rempty = bars + 2 * STAGES + 2;
+  p += ScreenLayout::BAR_BYTES;
+  S.ring = reinterpret_cast<ScanItem*>(p);
+  S.D = nullptr;
+  S.Lkey = nullptr;
+  S.Lid = nullptr;
+  S.Ln = nullptr;
+  S.CR = nullptr;
+  S.Cn = nullptr;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; i++) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], NCW);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&S.rfull[i], 1);
+      mbar_init(&S.rempty[i], NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int nchunk_d = lt.dp / DC;
+  const int n_items = *n_items_p;
+  if (warp == NCW) {
+    scan_producer(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false);
+    return;
+  }
+
+  __shared__ float nq2_s[QG];
+  __shared__ int32_t qb_s[QG];
+  int s = 0, r = 0;
+  uint32_t ph = 0, rph = 0;
+  for (;;) {
+    mbar_wait(&S.rfull[r], rph);
+    const ScanItem item = S.ring[r];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&S.rempty[r]);
+    if (++r == 2) {
+      r = 0;
+      rph ^= 1;
+    }
+    if (item.nq < 0) break;
+    const int nq = item.nq;
+    if (threadIdx.x < QG) {
+      const int b = threadIdx.x < nq ? qpairs[item.qoff + threadIdx.x].b : 0;
+      qb_s[threadIdx.x] = b;
+      nq2_s[threadIdx.x] = threadIdx.x < nq ? qnorm2[b] : 0.f;
+    }
+    named_bar_sync(1, NCW * 32);
+    for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+      if (nq <= 1) screen_tile<METRIC, 1>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+      else if (nq <= 2) screen_tile<METRIC, 2>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+      else if (nq <= 4) screen_tile<METRIC, 4>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+      else if (nq <= 6) screen_tile<METRIC, 6>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+      else if (nq <= 8) screen_tile<METRIC, 8>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+      else if (nq <= 12) screen_tile<METRIC, 12>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+      else screen_tile<METRIC, 16>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+    }
+    named_bar_sync(1, NCW * 32);
+    const int64_t rbase = lt.off[item.lslot] + item.row0;
+    for (int a = warp; a < nq; a += NCW)
+      screen_select(S, a, item.nrows, kk, coef, nq2_s[a], qb_s[a], item.lslot, rbase,
+                    (int64_t)qpairs[item.qoff + a].slotbase + item.chunk, Uq, slot_hi, slot_n,
+                    cpool, ccount, cap);
+    named_bar_sync(1, NCW * 32);  // A / NX reuse by the next item
+  }
+}
+
+// Bound coefficient: |A - E| <= coef * (nx + nq) for d terms.
+float screen_coef(int metric, int dp) {
+  const double u = 1.0 / 16777216.0;
+  auto gam = [u](double n) { return n * u / (1.0 - n * u); };
+  double c;
+  if (metric == SQ_L2) c = (2.0 * gam(dp) + 2.0 * gam(dp + 3) + 4.0 * u) / (1.0 - gam(dp));
+  else c = (gam(dp) + 2.0 * u) / (1.0 - gam(dp));
+  return (float)(c * 1.0625);  // slack for the fp32 evaluation of eps itself
+}
+
+// qn2[b] = sum of q_j^2 (FFMA, any order: the bound holds for any
+// evaluation tree of d terms).  One warp per query.
+__global__ void qnorm2_kernel(const float* __restrict__ Q, int64_t ldq, int B, int dp,
+                              float* __restrict__ out) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const float* q = Q + (int64_t)b * ldq;
+  float acc = 0.f;
+  for (int j = lane; j < dp; j += 32) acc = __fmaf_rn(q[j], q[j], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+  if (lane == 0) out[b] = acc;
+}
+void launch_qnorm2(const float* Q, int64_t ldq, int B, int dp, float* out, cudaStream_t st) {
+  if (B <= 0) return;
+  qnorm2_kernel<<<(B + 7) / 8, 256, 0, st>>>(Q, ldq, B, dp, out);
+}
+
+void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
+                        const float* qnorm2, const ScanItem* items, const int32_t* n_items,
+                        int max_items, const QPair* qpairs, int kk, int32_t* work_ctr,
+                        uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
+                        int32_t* ccount, int cap, int num_sms, cudaStream_t st) {
+  if (max_items <= 0) return;
+  const size_t smem = screen_smem_bytes();
+  const int grid = std::min(num_sms, max_items);
+  const float coef = screen_coef(metric, lt.dp);
+  if (metric == SQ_L2) {
+    auto k = scan_screen_kernel<SQ_L2>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, SCAN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
+                                        work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap);
+  } else {
+    auto k = scan_screen_kernel<IP>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k<<<grid, SCAN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
+                                        work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap);
+  }
+}
+
+// ---------------------------------------------------------------------
+// Per query: global bound, exact re-rank of the surviving pool entries, merge.
+//
+// 1. U_q = kk-th smallest of all hi values its (query, item) slots published:
+//    kk rows of the query have E <= hi <= U_q, so a row with lo > U_q cannot
+//    be in the top-kk.
+// 2. Pool entries with lo <= U_q are compacted; their rows are staged into
+//    shared memory with coalesced 16-byte loads (a group at a time) and one
+//    thread per candidate runs the reference's sequential fp32 sum.
+// 3. First kk by (dist, id), first occurrence per id (ref/engine.py:406-426).
+// A query whose pool overflowed is answered by an exact scan of every row of
+// its probed lists (slow path; correct for any input).
+// ---------------------------------------------------------------------
+constexpr int RR_THREADS = 256;
+constexpr int RR_SURV = 4096;  // survivors handled per pass
+
+template <int METRIC>
+__global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
+    const int4* __restrict__ cpool, const int32_t* __restrict__ ccount, int cap,
+    const uint32_t* __restrict__ slot_hi, const int32_t* __restrict__ slot_n,
+    const int32_t* __restrict__ slot_off, ListTable lt, const float* __restrict__ Qd,
+    const int32_t* __restrict__ probe, int nprobe, int kk, int group, int64_t* __restrict__ out_ids,
+    float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n) {
+  extern __shared__ __align__(16) uint8_t rr_smem[];
+  Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [MERGE_CAP]
+  float4* qs4 = reinterpret_cast<float4*>(rr_smem + MERGE_CAP * sizeof(Entry));     // [dp/4]
+  float4* rows4 = qs4 + lt.dp / 4;                                                   // [group][dp/4]
+  int32_t* surv = reinterpret_cast<int32_t*>(rows4 + (size_t)group * (lt.dp / 4));  // [RR_SURV]
+  __shared__ int s_cnt, s_ns;
+  __shared__ uint32_t s_u[RR_THREADS / 32];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int dp4 = lt.dp / 4;
+  for (int j = threadIdx.x; j < dp4; j += blockDim.x)
+    qs4[j] = reinterpret_cast<const float4*>(Qd + (int64_t)b * lt.dp)[j];
+  const int n = ccount[b];
+  const bool overflow = n > cap;
+  // 1. global bound U_q: smallest v with #(slot hi <= v) >= kk (KEY_NONE if fewer)
+  const int so = slot_off[b], eo = slot_off[b + 1];
+  uint32_t U = KEY_NONE;
+  if (!overflow) {
+    uint32_t L = 0, H = KEY_NONE;
+    int have = 0;
+    for (int sl = so + threadIdx.x; sl < eo; sl += blockDim.x) have += slot_n[sl];
+    have = __reduce_add_sync(FULL, have);
+    if (lane == 0) s_u[warp] = have;
+    __syncthreads();
+    int total_hi = 0;
+    for (int w = 0; w < RR_THREADS / 32; w++) total_hi += s_u[w];
+    __syncthreads();
+    if (total_hi >= kk) {
+      while (L < H) {
+        const uint32_t mid = L + ((H - L) >> 1);
+        int c = 0;
+        for (int sl = so + threadIdx.x; sl < eo; sl += blockDim.x) {
+          const int m = slot_n[sl];
+          for (int e = 0; e < m; e++) c += slot_hi[(int64_t)sl * kk + e] <= mid;
+        }
+        c = __reduce_add_sync(FULL, c);
+        if (lane == 0) s_u[warp] = c;
+        __syncthreads();
+        int tot = 0;
+        for (int w = 0; w < RR_THREADS / 32; w++) tot += s_u[w];
+        __syncthreads();
+        if (tot >= kk) H = mid;
+        else L = mid + 1;
+      }
+      U = L;
+    }
+  }
+  __syncthreads();
+  int kept = 0;
+  const int room = MERGE_CAP - kk;
+  if (!overflow) {
+    for (int p0 = 0; p0 < n; p0 += RR_SURV) {
+      // 2a. compact survivors of this pass
+      if (threadIdx.x == 0) s_ns = 0;
+      __syncthreads();
+      const int pm = min(RR_SURV, n - p0);
+      for (int i = threadIdx.x; i < pm; i += blockDim.x) {
+        const int4 c = cpool[(int64_t)b * cap + p0 + i];
+        if ((uint32_t)c.z <= U) surv[atomicAdd(&s_ns, 1)] = p0 + i;
+      }
+      __syncthreads();
+      const int ns = s_ns;
+      // 2b. exact distances, `group` candidates at a time, into buf after the kept ones
+      for (int g0 = 0; g0 < ns; g0 += group) {
+        const int m = min(group, ns - g0);
+        for (int i = threadIdx.x; i < m * dp4; i += blockDim.x) {
+          const int c = i / dp4, j = i - c * dp4;
+          const int4 e = cpool[(int64_t)b * cap + surv[g0 + c]];
+          rows4[(size_t)c * dp4 + j] =
+              __ldg(reinterpret_cast<const float4*>(lt.rows + (int64_t)e.x * lt.dp) + j);
+        }
+        __syncthreads();
+        if (threadIdx.x < m) {
+          const float4* x4 = rows4 + (size_t)threadIdx.x * dp4;
+          float acc = 0.f;
+          for (int j = 0; j < dp4; j++) acc = step4<METRIC>(acc, x4[j], qs4[j]);
+          const int4 e = cpool[(int64_t)b * cap + surv[g0 + threadIdx.x]];
+          Entry en;
+          en.key = f2key(finalize<METRIC>(acc, 0.f, 0.f));
+          en.id = lt.ids[e.x];
+          en.pay = e.y;
+          buf[kept + threadIdx.x] = en;
+        }
+        __syncthreads();
+        const int tot = kept + m;
+        if (tot > room || g0 + m >= ns) {
+          cta_bitonic_sort(buf, tot);
+          kept = cta_compact_sorted(buf, tot, kk, true, &s_cnt);
+        } else {
+          kept = tot;
+        }
+      }
+    }
+  } else {
+    // slow path: exact scan of every row of every probed list
+    int64_t total = 0;
+    for (int p = 0; p < nprobe; p++) {
+      const int sl = probe[(int64_t)b * nprobe + p];
+      if (sl >= 0) total += lt.len[sl];
+    }
+    __syncthreads();
+    for (int64_t base = 0; base < total; base += room) {
+      const int m = (int)(total - base < room ? total - base : (int64_t)room);
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        int64_t r = base + i;
+        int p = 0;
+        for (; p < nprobe; p++) {
+          const int sl = probe[(int64_t)b * nprobe + p];
+          const int64_t len = sl >= 0 ? lt.len[sl] : 0;
+          if (r < len) break;
+          r -= len;
+        }
+        const int lslot = probe[(int64_t)b * nprobe + p];
+        const int64_t arow = lt.off[lslot] + r;
+        const float4* x4 = reinterpret_cast<const float4*>(lt.rows + arow * lt.dp);
+        float acc = 0.f;
+        for (int j = 0; j < dp4; j++) acc = step4<METRIC>(acc, __ldg(x4 + j), qs4[j]);
+        Entry e;
+        e.key = f2key(finalize<METRIC>(acc, 0.f, 0.f));
+        e.id = lt.ids[arow];
+        e.pay = lslot;
+        buf[kept + i] = e;
+      }
+      __syncthreads();
+      cta_bitonic_sort(buf, kept + m);
+      kept = cta_compact_sorted(buf, kept + m, kk, true, &s_cnt);
+    }
+  }
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+    const int64_t o = (int64_t)b * kk + i;
+    if (i < kept) {
+      out_ids[o] = buf[i].id;
+      out_d[o] = key2f(buf[i].key);
+      if (out_cid) out_cid[o] = lt.cid[buf[i].pay];
+    } else {
+      out_ids[o] = -1;
+      out_d[o] = __int_as_float(0x7f800000);
+      if (out_cid) out_cid[o] = -1;
+    }
+  }
+  if (threadIdx.x == 0) out_n[b] = kept;
+}
+
+void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* ccount, int cap,
+                         const uint32_t* slot_hi, const int32_t* slot_n, const int32_t* slot_off,
+                         ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
+                         int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
+                         cudaStream_t st) {
+  if (B <= 0) return;
+  const int group = std::max(1, std::min(RR_THREADS / 8, (int)(96 * 1024 / (lt.dp * 4))));
+  const size_t smem = MERGE_CAP * sizeof(Entry) + (size_t)(group + 1) * lt.dp * 4 + RR_SURV * 4;
+#define PK_RR(M)                                                                                \
+  {                                                                                             \
+    auto k = rerank_merge_kernel<M>;                                                            \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    k<<<B, RR_THREADS, smem, st>>>(cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
+                                   nprobe, kk, group, out_ids, out_d, out_cid, out_n);          \
+  }
+  if (metric == SQ_L2) PK_RR(SQ_L2)
+  else PK_RR(IP)
+#undef PK_RR
 }
 
 // =====================================================================

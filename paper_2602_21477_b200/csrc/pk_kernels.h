@@ -90,5 +90,26 @@ void launch_scatter_rows(const float* src, int64_t lds, const int64_t* src_ids, 
                          const int64_t* dst_row, float* dst, int64_t* dst_ids, int dp,
                          cudaStream_t st);
 size_t scan_smem_bytes();
+size_t screen_smem_bytes();
+// qn2[b] = FFMA-chain squared norm of query b (screen input).
+void launch_qnorm2(const float* Q, int64_t ldq, int B, int dp, float* out, cudaStream_t st);
+// Screened persistent scan (sq_l2 / neg_ip): FFMA screen with a proven error
+// bound.  Per (query, item) slot: the item's kk smallest upper bounds
+// (slot_hi[slot][..slot_n]); per query: running bound Uq (KEY_NONE-initialised)
+// and the pool of rows that can still reach the top-kk (cpool[b][0..cap):
+// arena row, list slot, lower-bound key; count ccount[b], zero-initialised).
+void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
+                        const float* qnorm2, const ScanItem* items, const int32_t* n_items,
+                        int max_items, const QPair* qpairs, int kk, int32_t* work_ctr,
+                        uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
+                        int32_t* ccount, int cap, int num_sms, cudaStream_t st);
+// Per query: global bound from the slots, exact re-rank of the surviving pool
+// entries, top-kk merge (one CTA per query).
+void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* ccount, int cap,
+                         const uint32_t* slot_hi, const int32_t* slot_n, const int32_t* slot_off,
+                         ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
+                         int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
+                         cudaStream_t st);
+float screen_coef(int metric, int dp);
 
 }  // namespace pk

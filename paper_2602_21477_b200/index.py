@@ -91,6 +91,12 @@ class DeviceIndex:
         N.check(N.lib().pk_profile_end(self._h, N.ptr(out), len(out), ctypes.byref(calls)))
         return dict(zip(N.STAGES, out.tolist())), int(calls.value)
 
+    def pool_counts(self, B: int) -> np.ndarray:
+        """Candidate-pool size per query of the last screened search."""
+        out = np.empty(B, dtype=np.int32)
+        N.check(N.lib().pk_debug_pool_counts(self._h, N.ptr(out), B))
+        return out
+
     def append(self, cid: int, rows, ids):
         rows = N.f32(rows, self.dimension)
         ids = np.ascontiguousarray(ids, dtype=np.int64)

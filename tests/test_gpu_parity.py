@@ -135,8 +135,19 @@ def _random_index(pk, rng, d, nlist, sizes, metric=0, dup=False, ids_shuffle=Tru
     return ix, lists, np.stack(cents), np.arange(nlist) * 2 + 5
 
 
+@pytest.fixture(params=["screen", "exact", "overflow"])
+def scan_mode(request, monkeypatch):
+    """Both scan kernels: the FFMA-screened one (default for sq_l2 / ip), the
+    all-exact one (PK_SCAN_EXACT=1; always used for cosine), and the screened
+    one with a 3-entry candidate pool so every query takes the exact
+    overflow path."""
+    monkeypatch.setenv("PK_SCAN_EXACT", "1" if request.param == "exact" else "0")
+    monkeypatch.setenv("PK_POOL_CAP", "3" if request.param == "overflow" else "4096")
+    return request.param
+
+
 @pytest.mark.parametrize("d,metric", [(32, 0), (128, 0), (384, 0), (768, 0), (96, 1), (96, 2), (20, 0)])
-def test_device_search_matches_oracle(pk, d, metric):
+def test_device_search_matches_oracle(pk, d, metric, scan_mode):
     rng = np.random.default_rng(d * 10 + metric)
     nlist = 40
     sizes = rng.integers(0, 700, nlist)
@@ -241,3 +252,44 @@ def test_cfg1_scale_parity(pk):
     assert np.array_equal(out.ids, ids)
     assert np.array_equal(bits(out.dists), bits(dd))
     ix.close()
+
+
+@pytest.mark.parametrize("kind", ["shell", "offset", "dups", "tiny"])
+def test_screen_adversarial(pk, kind, scan_mode):
+    """Inputs that stress the screen's error bound: rows on a shell around the
+    query (near-ties everywhere), a large common offset (cancellation in
+    nx + nq - 2 dot), massive exact duplicates, subnormal-scale values."""
+    from paper_2602_21477_b200 import DeviceIndex
+
+    rng = np.random.default_rng({"shell": 1, "offset": 2, "dups": 3, "tiny": 4}[kind])
+    d, nl, n = 64, 6, 700
+    Q = rng.normal(size=(24, d)).astype(np.float32)
+    lists = []
+    for c in range(nl):
+        if kind == "shell":
+            u = rng.normal(size=(n, d))
+            u /= np.linalg.norm(u, axis=1, keepdims=True)
+            rows = (Q[c % len(Q)] + 3.0 * u).astype(np.float32)
+        elif kind == "offset":
+            rows = (100.0 + rng.normal(size=(n, d))).astype(np.float32)
+        elif kind == "dups":
+            base = rng.normal(size=(3, d)).astype(np.float32)
+            rows = base[rng.integers(0, 3, n)]
+        else:
+            rows = (rng.normal(size=(n, d)) * 1e-19).astype(np.float32)
+        lists.append((np.arange(c * n, (c + 1) * n, dtype=np.int64)[::-1].copy(), rows))
+    if kind == "offset":
+        Q = (100.0 + rng.normal(size=(24, d))).astype(np.float32)
+    if kind == "tiny":
+        Q = (Q * 1e-19).astype(np.float32)
+    for metric in (0, 1):
+        ix = DeviceIndex(d, metric, 0)
+        cents = np.stack([ix.create_list(c, 0, rows, ids) for c, (ids, rows) in enumerate(lists)])
+        flat = O.FlatIVF.from_lists(lists, cents, np.arange(nl), metric=["sq_l2", "ip"][metric])
+        for nprobe, kk in ((2, 10), (6, 64)):
+            out = ix.search(Q, [0], nprobe, kk, want_probe=True)
+            ids, dd, cnt, probe, scanned = flat.search(Q, nprobe, kk, threads=8)
+            assert np.array_equal(out.probe, probe)
+            assert np.array_equal(out.ids, ids), (kind, metric, nprobe)
+            assert np.array_equal(bits(out.dists), bits(dd))
+        ix.close()
