@@ -113,6 +113,7 @@ struct pk_index {
   // arena
   float* rows = nullptr;
   int64_t* ids = nullptr;
+  float* nrm = nullptr;  // squared row norms (tensor-core screen)
   int64_t arena_cap = 0, arena_top = 0;
   std::vector<Range> free_ranges;
   ArenaMaps maps;
@@ -133,9 +134,10 @@ struct pk_index {
       cand_key, cand_id, cand_n, cand_list, work, out_ids, out_d, out_cid, out_n, scopes, assign_c,
       assign_d;
   int chunk_rows = 512;
-  bool screen = true;  // FFMA screen + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
+  bool screen = true;  // screened scan + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
+  bool tensor = true;  // screen dots on tcgen05 (TF32); PK_SCREEN=ffma uses CUDA-core FFMA
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
-  DevBuf qnorm2, uq, cpool, ccount, ckey;
+  DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
 
   // stage timing (pk_profile_begin / pk_profile_end): events around each
   // stage of every pk_search while enabled.
@@ -163,6 +165,7 @@ struct pk_index {
     t.cid = d_cid;
     t.scope = d_scope;
     t.cent = d_cent;
+    t.nrm = nrm;
     t.nslots = nslots;
     t.dp = (int32_t)dp;
     t.d = (int32_t)d;
@@ -208,18 +211,24 @@ struct pk_index {
     int64_t ncap = std::max<int64_t>({need_rows, arena_cap + arena_cap / 2, 1024});
     float* nrows = nullptr;
     int64_t* nids = nullptr;
+    float* nnrm = nullptr;
     CK(cudaMalloc(&nrows, (size_t)ncap * dp * 4));
     CK(cudaMalloc(&nids, (size_t)ncap * 8));
+    CK(cudaMalloc(&nnrm, (size_t)ncap * 4));
     CK(cudaMemsetAsync(nrows, 0, (size_t)ncap * dp * 4, st));
+    CK(cudaMemsetAsync(nnrm, 0, (size_t)ncap * 4, st));
     if (rows) {
       CK(cudaMemcpyAsync(nrows, rows, (size_t)arena_top * dp * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(nids, ids, (size_t)arena_top * 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(nnrm, nrm, (size_t)arena_top * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaStreamSynchronize(st));
       cudaFree(rows);
       cudaFree(ids);
+      cudaFree(nrm);
     }
     rows = nrows;
     ids = nids;
+    nrm = nnrm;
     arena_cap = ncap;
     return encode_maps();
   }
@@ -301,6 +310,8 @@ struct pk_index {
     cudaMemcpyKind k = dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CK(cudaMemcpy2DAsync(rows + at * dp, dp * 4, src, d * 4, d * 4, n, k, st));
     CK(cudaMemcpyAsync(ids + at, src_ids, n * 8, k, st));
+    launch_row_norms(rows + at * dp, n, (int)dp, nrm + at, st);
+    CK(cudaGetLastError());
     if (!dev) CK(cudaStreamSynchronize(st));  // pageable/pinned source reusable on return
     return PK_OK;
   }
@@ -426,6 +437,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   if (const char* e = getenv("PK_CHUNK_ROWS")) ix->chunk_rows = std::max(TILE, atoi(e) / TILE * TILE);
   if (const char* e = getenv("PK_SCAN_EXACT")) ix->screen = atoi(e) == 0;
   if (const char* e = getenv("PK_POOL_CAP")) ix->pool_cap = std::max(1, atoi(e));
+  if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
   if (metric == COSINE) ix->screen = false;
   if (ix->screen) ix->chunk_rows = std::min(ix->chunk_rows, 2 * TILE);
   cudaError_t e = cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking);
@@ -449,6 +461,7 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->st) cudaStreamSynchronize(ix->st);
   cudaFree(ix->rows);
   cudaFree(ix->ids);
+  cudaFree(ix->nrm);
   cudaFree(ix->d_off);
   cudaFree(ix->d_len);
   cudaFree(ix->d_cid);
@@ -459,7 +472,7 @@ int pk_index_destroy(pk_index* ix) {
                     &ix->fillb, &ix->items, &ix->nitems, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list, &ix->work,
                     &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey})
+                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -529,6 +542,8 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
                          (size_t)len * ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
       CK(cudaMemcpyAsync(ix->ids + noff, ix->ids + ooff, (size_t)len * 8,
                          cudaMemcpyDeviceToDevice, ix->st));
+      CK(cudaMemcpyAsync(ix->nrm + noff, ix->nrm + ooff, (size_t)len * 4,
+                         cudaMemcpyDeviceToDevice, ix->st));
     }
     ix->free_range(ooff, ix->h_cap[s]);
     ix->h_off[s] = noff;
@@ -551,6 +566,8 @@ int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
     CK(cudaMemcpyAsync(ix->rows + (off + row) * ix->dp, ix->rows + (off + last) * ix->dp,
                        ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
     CK(cudaMemcpyAsync(ix->ids + off + row, ix->ids + off + last, 8, cudaMemcpyDeviceToDevice,
+                       ix->st));
+    CK(cudaMemcpyAsync(ix->nrm + off + row, ix->nrm + off + last, 4, cudaMemcpyDeviceToDevice,
                        ix->st));
   }
   ix->h_len[s] = last;
@@ -700,12 +717,22 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
     RET(ix->cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));
     CK(cudaMemsetAsync(ix->uq.p, 0xff, (size_t)B * 4, st));
     CK(cudaMemsetAsync(ix->ccount.p, 0, (size_t)B * 4, st));
-    launch_scan_screen(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
-                       ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
-                       (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
-                       ix->work.as<int32_t>(), ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
-                       ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
-                       ix->pool_cap, ix->num_sms, st);
+    if (ix->tensor) {
+      RET(ix->qsw.ensure((size_t)8 * B * dp * 4));
+      launch_scan_tc(ix->metric, lt, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(),
+                     ix->qnorm2.as<float>(), ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
+                     (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
+                     ix->work.as<int32_t>(), ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
+                     ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
+                     ix->pool_cap, ix->num_sms, st);
+    } else {
+      launch_scan_screen(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
+                         ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
+                         (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
+                         ix->work.as<int32_t>(), ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
+                         ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
+                         ix->pool_cap, ix->num_sms, st);
+    }
   } else
     launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
                 ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(), (int)std::min<int64_t>(max_items, INT32_MAX),

@@ -12,6 +12,7 @@
 // float, then the int64 id.
 #include "pk_kernels.h"
 #include "pk_ptx.cuh"
+#include "pk_umma.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -739,12 +740,13 @@ __device__ void topk_merge_tile(const ScanShared& S, int a, int rows, const int6
 // through a 2-deep ring, and streams each item's row tiles (TMA 2-D,
 // SWIZZLE_128B, box heights 256..8 to cover ragged tails) and the matching
 // 128-byte query chunks (bulk copies) through the STAGES-deep stage ring.
+template <int NSTAGE>
 __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMaps& maps,
                                               const ListTable& lt, const float* __restrict__ Qd,
                                               const ScanItem* __restrict__ items, int n_items,
                                               const QPair* __restrict__ qpairs,
                                               int32_t* __restrict__ work_ctr, int nchunk_d,
-                                              bool keep_in_l2) {
+                                              bool keep_in_l2, int64_t qsw_stride) {
   const int lane = threadIdx.x & 31;
   if (lane == 0)
     for (int i = 0; i < NBOX; i++) tma_prefetch_desc(&maps.box[i]);
@@ -773,7 +775,11 @@ __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMa
     if (item.nq < 0) break;
     const int64_t rbase = lt.off[item.lslot] + item.row0;
     const int qb = lane < item.nq ? qpairs[item.qoff + lane].b : 0;
-    const float* qrow = Qd + (int64_t)qb * lt.dp;
+    // qsw_stride > 0: Qd holds 8 copies of the batch, copy p with the 16-byte
+    // pieces of every 128-byte chunk XOR-permuted by p, so query slot `lane`
+    // lands SWIZZLE_128B-ready in row `lane` of the stage's query tile.
+    const float* qrow =
+        Qd + ((qsw_stride ? (int64_t)(lane & 7) * qsw_stride : 0) + qb) * (int64_t)lt.dp;
     for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
       const int rows = min(TILE, item.nrows - t0);
       const int rows8 = (rows + 7) & ~7;
@@ -796,7 +802,7 @@ __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMa
         __syncwarp();
         if (lane < item.nq)
           bulk_g2s(S.Qc + (size_t)s * QG * DC + lane * DC, qrow + c * DC, DC * 4, &S.full[s]);
-        if (++s == STAGES) {
+        if (++s == NSTAGE) {
           s = 0;
           ph ^= 1;
         }
@@ -853,7 +859,7 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   const int n_items = *n_items_p;
 
   if (warp == NCW) {
-    scan_producer(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false);
+    scan_producer<STAGES>(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false, 0);
     return;
   }
 
@@ -1080,35 +1086,61 @@ struct ScreenLayout {
 };
 size_t screen_smem_bytes() { return ScreenLayout::TOTAL + 1024; }
 
-// FFMA screen of one tile: this thread's row against NQ queries.
-template <int METRIC, int NQ>
+// FFMA screen of one tile, register-blocked 4 rows x NQT queries per thread
+// (LDS : FFMA = 8 : 64 -- one-row-per-thread blocking is shared-memory-issue
+// bound).  Thread tid < 256: row group rg = tid % 64 owns rows rg + 64 r,
+// query group qg = tid / 64 owns queries 4 qg .. 4 qg + 3; group 0 also
+// accumulates the row norms.  Threads with no query group only keep the
+// stage ring in step.  Stores raw dots; screen_finalize forms A.
+template <int NQT>
 __device__ __forceinline__ void screen_tile(const ScanShared& S, int nchunk_d, int& s, uint32_t& ph,
-                                            int nq, int tile_row0, const float* nq2_s) {
-  const int row = threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int swz = row & 7;
-  float acc[NQ];
+                                            int nq, int tile_row0) {
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int rg = tid & 63, qg = tid >> 6;
+  const int qbase = qg * 4;
+  const bool active = qbase < nq;
+  const bool do_norm = qg == 0;
+  const int swz = rg & 7;
+  float acc[4][NQT];
+  float nx[4];
 #pragma unroll
-  for (int a = 0; a < NQ; a++) acc[a] = 0.f;
-  float nx = 0.f;
+  for (int r = 0; r < 4; r++) {
+    nx[r] = 0.f;
+#pragma unroll
+    for (int a = 0; a < NQT; a++) acc[r][a] = 0.f;
+  }
   for (int c = 0; c < nchunk_d; c++) {
     mbar_wait(&S.full[s], ph);
-    const float* xs = S.X + (size_t)s * TILE * DC + row * DC;
-    const float* qs = S.Qc + (size_t)s * QG * DC;
+    if (active) {
+      const float* xs = S.X + (size_t)s * TILE * DC + rg * DC;
+      const float* qs = S.Qc + (size_t)s * QG * DC + qbase * DC;
 #pragma unroll
-    for (int k = 0; k < DC / 4; k++) {
-      const float4 x = *reinterpret_cast<const float4*>(xs + ((k ^ swz) << 2));
-      nx = __fmaf_rn(x.x, x.x, nx);
-      nx = __fmaf_rn(x.y, x.y, nx);
-      nx = __fmaf_rn(x.z, x.z, nx);
-      nx = __fmaf_rn(x.w, x.w, nx);
+      for (int k = 0; k < DC / 4; k++) {
+        float4 x[4];
 #pragma unroll
-      for (int a = 0; a < NQ; a++) {
-        const float4 q = *reinterpret_cast<const float4*>(qs + a * DC + (k << 2));
-        acc[a] = __fmaf_rn(x.x, q.x, acc[a]);
-        acc[a] = __fmaf_rn(x.y, q.y, acc[a]);
-        acc[a] = __fmaf_rn(x.z, q.z, acc[a]);
-        acc[a] = __fmaf_rn(x.w, q.w, acc[a]);
+        for (int r = 0; r < 4; r++)
+          x[r] = *reinterpret_cast<const float4*>(xs + r * 64 * DC + ((k ^ swz) << 2));
+        if (do_norm) {
+#pragma unroll
+          for (int r = 0; r < 4; r++) {
+            nx[r] = __fmaf_rn(x[r].x, x[r].x, nx[r]);
+            nx[r] = __fmaf_rn(x[r].y, x[r].y, nx[r]);
+            nx[r] = __fmaf_rn(x[r].z, x[r].z, nx[r]);
+            nx[r] = __fmaf_rn(x[r].w, x[r].w, nx[r]);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < NQT; a++) {
+          const float4 q = *reinterpret_cast<const float4*>(qs + a * DC + (k << 2));
+#pragma unroll
+          for (int r = 0; r < 4; r++) {
+            acc[r][a] = __fmaf_rn(x[r].x, q.x, acc[r][a]);
+            acc[r][a] = __fmaf_rn(x[r].y, q.y, acc[r][a]);
+            acc[r][a] = __fmaf_rn(x[r].z, q.z, acc[r][a]);
+            acc[r][a] = __fmaf_rn(x[r].w, q.w, acc[r][a]);
+          }
+        }
       }
     }
     __syncwarp();
@@ -1118,15 +1150,31 @@ __device__ __forceinline__ void screen_tile(const ScanShared& S, int nchunk_d, i
       ph ^= 1;
     }
   }
-  S.NX[tile_row0 + row] = nx;
+  if (do_norm) {
 #pragma unroll
-  for (int a = 0; a < NQ; a++) {
-    if (a < nq) {
-      float A;
-      if (METRIC == SQ_L2) A = __fsub_rn(__fadd_rn(nx, nq2_s[a]), __fmul_rn(2.f, acc[a]));
-      else A = -acc[a];
-      S.A[a * CHUNK_MAX + tile_row0 + row] = A;
-    }
+    for (int r = 0; r < 4; r++) S.NX[tile_row0 + rg + 64 * r] = nx[r];
+  }
+  if (active) {
+#pragma unroll
+    for (int a = 0; a < NQT; a++)
+      if (qbase + a < nq) {
+#pragma unroll
+        for (int r = 0; r < 4; r++)
+          S.A[(qbase + a) * CHUNK_MAX + tile_row0 + rg + 64 * r] = acc[r][a];
+      }
+  }
+}
+
+// A = nx + nq - 2 dot (sq_l2) or -dot (ip), in place over the item's rows.
+template <int METRIC>
+__device__ __forceinline__ void screen_finalize(const ScanShared& S, int nq, int R,
+                                                const float* nq2_s, int tid, int nthreads) {
+  for (int i = tid; i < nq * R; i += nthreads) {
+    const int a = i / R, row = i - a * R;
+    const float dot = S.A[a * CHUNK_MAX + row];
+    S.A[a * CHUNK_MAX + row] = (METRIC == SQ_L2)
+                                   ? __fsub_rn(__fadd_rn(S.NX[row], nq2_s[a]), __fmul_rn(2.f, dot))
+                                   : -dot;
   }
 }
 
@@ -1219,15 +1267,19 @@ __device__ __forceinline__ void screen_select(const ScanShared& S, int a, int R,
   }
 }
 
+constexpr int NCW_S = 8;  // screen kernel compute warps (256 threads: 64 row groups x 4 query groups)
+constexpr int SCREEN_THREADS = (NCW_S + 1) * 32;
+
 template <int METRIC>
-__global__ void __launch_bounds__(SCAN_THREADS, 1)
+__global__ void __launch_bounds__(SCREEN_THREADS, 1)
     scan_screen_kernel(const __grid_constant__ ArenaMaps maps, ListTable lt,
                        const float* __restrict__ Qd, const float* __restrict__ qnorm2,
                        const ScanItem* __restrict__ items, const int32_t* __restrict__ n_items_p,
                        const QPair* __restrict__ qpairs, int kk, float coef,
                        int32_t* __restrict__ work_ctr, uint32_t* __restrict__ Uq,
                        uint32_t* __restrict__ slot_hi, int32_t* __restrict__ slot_n,
-                       int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap) {
+                       int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap,
+                       int debug_nocompute) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ScanShared S;
@@ -1258,19 +1310,19 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < STAGES; i++) {
       mbar_init(&S.full[i], 1);
-      mbar_init(&S.empty[i], NCW);
+      mbar_init(&S.empty[i], NCW_S);
     }
     for (int i = 0; i < 2; i++) {
       mbar_init(&S.rfull[i], 1);
-      mbar_init(&S.rempty[i], NCW);
+      mbar_init(&S.rempty[i], NCW_S);
     }
     fence_mbar_init();
   }
   __syncthreads();
   const int nchunk_d = lt.dp / DC;
   const int n_items = *n_items_p;
-  if (warp == NCW) {
-    scan_producer(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false);
+  if (warp == NCW_S) {
+    scan_producer<STAGES>(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false, 0);
     return;
   }
 
@@ -1294,24 +1346,303 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
       qb_s[threadIdx.x] = b;
       nq2_s[threadIdx.x] = threadIdx.x < nq ? qnorm2[b] : 0.f;
     }
-    named_bar_sync(1, NCW * 32);
-    for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
-      if (nq <= 1) screen_tile<METRIC, 1>(S, nchunk_d, s, ph, nq, t0, nq2_s);
-      else if (nq <= 2) screen_tile<METRIC, 2>(S, nchunk_d, s, ph, nq, t0, nq2_s);
-      else if (nq <= 4) screen_tile<METRIC, 4>(S, nchunk_d, s, ph, nq, t0, nq2_s);
-      else if (nq <= 6) screen_tile<METRIC, 6>(S, nchunk_d, s, ph, nq, t0, nq2_s);
-      else if (nq <= 8) screen_tile<METRIC, 8>(S, nchunk_d, s, ph, nq, t0, nq2_s);
-      else if (nq <= 12) screen_tile<METRIC, 12>(S, nchunk_d, s, ph, nq, t0, nq2_s);
-      else screen_tile<METRIC, 16>(S, nchunk_d, s, ph, nq, t0, nq2_s);
+    named_bar_sync(1, NCW_S * 32);
+    {
+      const int nqc = debug_nocompute == 1 ? 0 : nq;
+      for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+        if (nqc <= 1) screen_tile<1>(S, nchunk_d, s, ph, nqc, t0);
+        else if (nqc <= 2) screen_tile<2>(S, nchunk_d, s, ph, nqc, t0);
+        else if (nqc <= 3) screen_tile<3>(S, nchunk_d, s, ph, nqc, t0);
+        else screen_tile<4>(S, nchunk_d, s, ph, nqc, t0);
+      }
     }
-    named_bar_sync(1, NCW * 32);
+    named_bar_sync(1, NCW_S * 32);
+    if (debug_nocompute) continue;  // measurement only: 1 = memory pipeline, 2 = + screen math
+    screen_finalize<METRIC>(S, nq, item.nrows, nq2_s, threadIdx.x, NCW_S * 32);
+    named_bar_sync(1, NCW_S * 32);
     const int64_t rbase = lt.off[item.lslot] + item.row0;
-    for (int a = warp; a < nq; a += NCW)
+    for (int a = warp; a < nq; a += NCW_S)
       screen_select(S, a, item.nrows, kk, coef, nq2_s[a], qb_s[a], item.lslot, rbase,
                     (int64_t)qpairs[item.qoff + a].slotbase + item.chunk, Uq, slot_hi, slot_n,
                     cpool, ccount, cap);
-    named_bar_sync(1, NCW * 32);  // A / NX reuse by the next item
+    named_bar_sync(1, NCW_S * 32);  // A / NX reuse by the next item
   }
+}
+
+// =====================================================================
+// Tensor-core screened scan (sq_l2 / neg_ip): the same streaming, bound and
+// candidate logic as scan_screen_kernel, with the (row, query) dot products
+// computed by tcgen05.mma kind::tf32 straight from the TMA-staged tiles.
+//
+// Roles (320 threads, one CTA per SM):
+//   warp 8      TMA producer: row tiles [256 x 32 fp32] SWIZZLE_128B + the
+//               query chunks from 8 pre-swizzled copies of the batch, through
+//               a TC_STAGES-deep mbarrier ring
+//   warp 9      MMA issuer (one lane): per stage 2 halves x 4 K-steps of
+//               M=128, N=16, K=8 TF32 MMAs into a TMEM accumulator
+//               (double-buffered per tile); tcgen05.commit frees the stage
+//   warps 0-7   epilogue: tcgen05.ld of the tile's [256 x 16] dots, then per
+//               item the bound, publication and candidate pool (as above)
+// TF32 bound (validated by tools/microbench/umma_check.cu): |dot' - x.q| <=
+// c_dot * sum|x_j q_j|, c_dot = 2.0011*2^-10 + d*2^-21 (input truncation +
+// accumulation), used with a 2x safety factor in screen_coef_tf32().
+// Row norms come from the arena's norm array (FFMA, any order).
+// =====================================================================
+constexpr int TC_STAGES = 5;
+constexpr int TC_EPI_WARPS = 8;
+constexpr int TC_THREADS = (TC_EPI_WARPS + 2) * 32;
+constexpr int TC_TMEM_COLS = 64;  // 2 tile buffers x 2 halves x 16 queries
+
+struct TcLayout {
+  static constexpr size_t X_BYTES = (size_t)TC_STAGES * TILE * DC * 4;
+  static constexpr size_t QC_BYTES = (size_t)TC_STAGES * QG * DC * 4;
+  static constexpr size_t A_BYTES = (size_t)QG * CHUNK_MAX * 4;
+  static constexpr size_t NX_BYTES = (size_t)CHUNK_MAX * 4;
+  static constexpr size_t BAR_BYTES = 256;
+  static constexpr size_t RING_BYTES = 2 * sizeof(ScanItem);
+  static constexpr size_t TOTAL = X_BYTES + QC_BYTES + A_BYTES + NX_BYTES + BAR_BYTES + RING_BYTES + 64;
+};
+size_t tc_smem_bytes() { return TcLayout::TOTAL + 1024; }
+
+template <int METRIC>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    scan_tc_kernel(const __grid_constant__ ArenaMaps maps, ListTable lt, const float* __restrict__ Qsw,
+                   int64_t qsw_stride, const float* __restrict__ qnorm2,
+                   const ScanItem* __restrict__ items, const int32_t* __restrict__ n_items_p,
+                   const QPair* __restrict__ qpairs, int kk, float coef,
+                   int32_t* __restrict__ work_ctr, uint32_t* __restrict__ Uq,
+                   uint32_t* __restrict__ slot_hi, int32_t* __restrict__ slot_n,
+                   int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  ScanShared S;
+  uint8_t* p = base;
+  S.X = reinterpret_cast<float*>(p);
+  p += TcLayout::X_BYTES;
+  S.Qc = reinterpret_cast<float*>(p);
+  p += TcLayout::QC_BYTES;
+  S.A = reinterpret_cast<float*>(p);
+  p += TcLayout::A_BYTES;
+  S.NX = reinterpret_cast<float*>(p);
+  p += TcLayout::NX_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(p);
+  S.full = bars;
+  S.empty = bars + TC_STAGES;
+  uint64_t* tfull = bars + 2 * TC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  S.rfull = tempty + 2;
+  S.rempty = S.rfull + 2;
+  p += TcLayout::BAR_BYTES;
+  S.ring = reinterpret_cast<ScanItem*>(p);
+  p += TcLayout::RING_BYTES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p);
+  S.D = nullptr;
+  S.Lkey = nullptr;
+  S.Lid = nullptr;
+  S.Ln = nullptr;
+  S.CR = nullptr;
+  S.Cn = nullptr;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TC_STAGES; i++) {
+      mbar_init(&S.full[i], 1);
+      mbar_init(&S.empty[i], 1);  // tcgen05.commit
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], TC_EPI_WARPS);
+      mbar_init(&S.rfull[i], 1);
+      mbar_init(&S.rempty[i], TC_EPI_WARPS + 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == TC_EPI_WARPS + 1) tmem_alloc(tmem_slot, TC_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nchunk_d = lt.dp / DC;
+  const int n_items = *n_items_p;
+
+  if (warp == TC_EPI_WARPS) {
+    // ---------------------------------------------------------- producer
+    scan_producer<TC_STAGES>(S, maps, lt, Qsw, items, n_items, qpairs, work_ctr, nchunk_d, false,
+                             qsw_stride);
+  } else if (warp == TC_EPI_WARPS + 1) {
+    // ---------------------------------------------------------- MMA issuer
+    const uint32_t idesc = umma_idesc_tf32(128, QG);
+    int s = 0, r = 0, tcount = 0;
+    uint32_t ph = 0, rph = 0;
+    for (;;) {
+      mbar_wait(&S.rfull[r], rph);
+      const ScanItem item = S.ring[r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.rempty[r]);
+      if (++r == 2) {
+        r = 0;
+        rph ^= 1;
+      }
+      if (item.nq < 0) break;
+      for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+        const int buf = tcount & 1;
+        mbar_wait(&tempty[buf], ((tcount >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem + buf * 2 * QG;
+        const bool two = item.nrows - t0 > 128;
+        for (int c = 0; c < nchunk_d; c++) {
+          mbar_wait(&S.full[s], ph);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t xa = smem_u32(S.X + (size_t)s * TILE * DC);
+            const uint32_t qa = smem_u32(S.Qc + (size_t)s * QG * DC);
+#pragma unroll
+            for (int k = 0; k < DC / 8; k++) {
+              const uint64_t bd = umma_desc_sw128(qa + k * 32);
+              const uint32_t acc = (c | k) != 0;
+              umma_tf32(dcol, umma_desc_sw128(xa + k * 32), bd, idesc, acc);
+              if (two) umma_tf32(dcol + QG, umma_desc_sw128(xa + 16384 + k * 32), bd, idesc, acc);
+            }
+            umma_commit(&S.empty[s]);
+          }
+          __syncwarp();
+          if (++s == TC_STAGES) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+        if (lane == 0) umma_commit(&tfull[buf]);
+        __syncwarp();
+        tcount++;
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    __shared__ float nq2_s[QG];
+    __shared__ int32_t qb_s[QG];
+    const int nthr = TC_EPI_WARPS * 32;
+    int r = 0, tcount = 0;
+    uint32_t rph = 0;
+    for (;;) {
+      mbar_wait(&S.rfull[r], rph);
+      const ScanItem item = S.ring[r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.rempty[r]);
+      if (++r == 2) {
+        r = 0;
+        rph ^= 1;
+      }
+      if (item.nq < 0) break;
+      const int nq = item.nq;
+      if (threadIdx.x < QG) {
+        const int b = threadIdx.x < nq ? qpairs[item.qoff + threadIdx.x].b : 0;
+        qb_s[threadIdx.x] = b;
+        nq2_s[threadIdx.x] = threadIdx.x < nq ? qnorm2[b] : 0.f;
+      }
+      const int64_t rbase = lt.off[item.lslot] + item.row0;
+      for (int i = threadIdx.x; i < item.nrows; i += nthr) S.NX[i] = lt.nrm[rbase + i];
+      const int h = warp >> 2, g = warp & 3;
+      for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
+        const int buf = tcount & 1;
+        mbar_wait(&tfull[buf], (tcount >> 1) & 1);
+        tc_fence_after();
+        float v[QG];
+        tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + buf * 2 * QG + h * QG, v);
+        const int row = t0 + 128 * h + 32 * g + lane;
+        if (row < item.nrows) {
+#pragma unroll
+          for (int a = 0; a < QG; a++)
+            if (a < nq) S.A[a * CHUNK_MAX + row] = v[a];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+        tcount++;
+      }
+      named_bar_sync(1, nthr);
+      for (int i = threadIdx.x; i < nq * item.nrows; i += nthr) {
+        const int a = i / item.nrows, row = i - a * item.nrows;
+        const float dot = S.A[a * CHUNK_MAX + row];
+        S.A[a * CHUNK_MAX + row] =
+            (METRIC == SQ_L2) ? __fsub_rn(__fadd_rn(S.NX[row], nq2_s[a]), __fmul_rn(2.f, dot)) : -dot;
+      }
+      named_bar_sync(1, nthr);
+      for (int a = warp; a < nq; a += TC_EPI_WARPS)
+        screen_select(S, a, item.nrows, kk, coef, nq2_s[a], qb_s[a], item.lslot, rbase,
+                      (int64_t)qpairs[item.qoff + a].slotbase + item.chunk, Uq, slot_hi, slot_n,
+                      cpool, ccount, cap);
+      named_bar_sync(1, nthr);  // A / NX / qb_s reuse by the next item
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == TC_EPI_WARPS + 1) tmem_dealloc(tmem, TC_TMEM_COLS);
+}
+
+// |A - E| <= coef * (nx + nq) with the TF32 dot (2x safety on c_dot).
+float screen_coef_tf32(int metric, int dp) {
+  const double u = 1.0 / 16777216.0;
+  auto gam = [u](double n) { return n * u / (1.0 - n * u); };
+  const double c_dot = 2.0 * (2.0011 / 1024.0 + dp / 2097152.0);
+  double c;
+  if (metric == SQ_L2) c = (c_dot + gam(dp) + 2.0 * gam(dp + 3) + 4.0 * u) / (1.0 - gam(dp));
+  else c = (0.5 * c_dot + gam(dp) + 2.0 * u) / (1.0 - gam(dp));
+  return (float)(c * 1.0625);
+}
+
+// 8 copies of the batch's queries, copy p with the 16-byte pieces of every
+// 128-byte chunk permuted by ^p (the SWIZZLE_128B pattern of tile row p mod 8).
+__global__ void qswizzle_kernel(const float* __restrict__ Qd, int B, int dp, float* __restrict__ out) {
+  const int64_t n4 = (int64_t)B * dp / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < 8 * n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int p = (int)(i / n4);
+    const int64_t e = i - p * n4;            // float4 index inside the batch
+    const int64_t piece = e & 7, chunk = e >> 3;
+    reinterpret_cast<float4*>(out)[p * n4 + (chunk << 3) + (piece ^ p)] =
+        reinterpret_cast<const float4*>(Qd)[e];
+  }
+}
+
+// Row squared norms (FFMA, any order) for rows [0, n) of `rows`.
+__global__ void row_norms_kernel(const float* __restrict__ rows, int64_t n, int dp,
+                                 float* __restrict__ out) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const float* x = rows + r * dp;
+  float acc = 0.f;
+  for (int j = lane; j < dp; j += 32) acc = __fmaf_rn(x[j], x[j], acc);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+  if (lane == 0) out[r] = acc;
+}
+void launch_row_norms(const float* rows, int64_t n, int dp, float* out, cudaStream_t st) {
+  if (n <= 0) return;
+  row_norms_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(rows, n, dp, out);
+}
+
+void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd, int B,
+                    float* qsw, const float* qnorm2, const ScanItem* items, const int32_t* n_items,
+                    int max_items, const QPair* qpairs, int kk, int32_t* work_ctr, uint32_t* Uq,
+                    uint32_t* slot_hi, int32_t* slot_n, int4* cpool, int32_t* ccount, int cap,
+                    int num_sms, cudaStream_t st) {
+  if (max_items <= 0) return;
+  qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
+  const size_t smem = tc_smem_bytes();
+  const int grid = std::min(num_sms, max_items);
+  const float coef = screen_coef_tf32(metric, lt.dp);
+#define PK_TC(M)                                                                                 \
+  {                                                                                              \
+    auto k = scan_tc_kernel<M>;                                                                  \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    k<<<grid, TC_THREADS, smem, st>>>(maps, lt, qsw, (int64_t)B, qnorm2, items, n_items, qpairs, \
+                                      kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool, ccount,    \
+                                      cap);                                                      \
+  }
+  if (metric == SQ_L2) PK_TC(SQ_L2)
+  else PK_TC(IP)
+#undef PK_TC
 }
 
 // Bound coefficient: |A - E| <= coef * (nx + nq) for d terms.
@@ -1352,16 +1683,19 @@ void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const f
   const size_t smem = screen_smem_bytes();
   const int grid = std::min(num_sms, max_items);
   const float coef = screen_coef(metric, lt.dp);
+  static const int debug_nocompute = getenv("PK_DEBUG_SCAN_NOCOMPUTE") ? atoi(getenv("PK_DEBUG_SCAN_NOCOMPUTE")) : 0;
   if (metric == SQ_L2) {
     auto k = scan_screen_kernel<SQ_L2>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, SCAN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
-                                        work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap);
+    k<<<grid, SCREEN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
+                                          work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap,
+                                          debug_nocompute);
   } else {
     auto k = scan_screen_kernel<IP>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k<<<grid, SCAN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
-                                        work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap);
+    k<<<grid, SCREEN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
+                                          work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap,
+                                          debug_nocompute);
   }
 }
 
@@ -1380,6 +1714,7 @@ void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const f
 // ---------------------------------------------------------------------
 constexpr int RR_THREADS = 256;
 constexpr int RR_SURV = 4096;  // survivors handled per pass
+constexpr int RR_HI_PER = 8;   // published upper bounds per thread (2048 per query)
 
 template <int METRIC>
 __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
@@ -1402,27 +1737,43 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     qs4[j] = reinterpret_cast<const float4*>(Qd + (int64_t)b * lt.dp)[j];
   const int n = ccount[b];
   const bool overflow = n > cap;
-  // 1. global bound U_q: smallest v with #(slot hi <= v) >= kk (KEY_NONE if fewer)
+  // 1. global bound U_q: smallest v with #(slot hi <= v) >= kk (KEY_NONE if
+  //    fewer).  The query's published hi values (<= RR_HI_PER per thread) are
+  //    gathered into registers once, then bisected.
   const int so = slot_off[b], eo = slot_off[b + 1];
   uint32_t U = KEY_NONE;
   if (!overflow) {
-    uint32_t L = 0, H = KEY_NONE;
-    int have = 0;
-    for (int sl = so + threadIdx.x; sl < eo; sl += blockDim.x) have += slot_n[sl];
-    have = __reduce_add_sync(FULL, have);
+    uint32_t hv[RR_HI_PER];
+    int nh = 0;
+#pragma unroll
+    for (int i = 0; i < RR_HI_PER; i++) hv[i] = KEY_NONE;
+    // flattened (slot, entry) index space; slots hold <= kk entries each
+    const int nflat = (eo - so) * kk;
+    bool fits = nflat <= RR_HI_PER * RR_THREADS;
+#pragma unroll
+    for (int i = 0; i < RR_HI_PER; i++) {
+      const int f = threadIdx.x + i * RR_THREADS;
+      if (fits && f < nflat) {
+        const int sl = so + f / kk, e = f - (f / kk) * kk;
+        if (e < slot_n[sl]) {
+          hv[i] = slot_hi[(int64_t)sl * kk + e];
+          nh++;
+        }
+      }
+    }
+    int have = __reduce_add_sync(FULL, nh);
     if (lane == 0) s_u[warp] = have;
     __syncthreads();
     int total_hi = 0;
     for (int w = 0; w < RR_THREADS / 32; w++) total_hi += s_u[w];
     __syncthreads();
-    if (total_hi >= kk) {
+    if (fits && total_hi >= kk) {
+      uint32_t L = 0, H = KEY_NONE;
       while (L < H) {
         const uint32_t mid = L + ((H - L) >> 1);
         int c = 0;
-        for (int sl = so + threadIdx.x; sl < eo; sl += blockDim.x) {
-          const int m = slot_n[sl];
-          for (int e = 0; e < m; e++) c += slot_hi[(int64_t)sl * kk + e] <= mid;
-        }
+#pragma unroll
+        for (int i = 0; i < RR_HI_PER; i++) c += hv[i] <= mid;
         c = __reduce_add_sync(FULL, c);
         if (lane == 0) s_u[warp] = c;
         __syncthreads();
@@ -1537,7 +1888,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                          cudaStream_t st) {
   if (B <= 0) return;
-  const int group = std::max(1, std::min(RR_THREADS / 8, (int)(96 * 1024 / (lt.dp * 4))));
+  const int group = std::max(1, std::min(16, (int)(48 * 1024 / (lt.dp * 4))));
   const size_t smem = MERGE_CAP * sizeof(Entry) + (size_t)(group + 1) * lt.dp * 4 + RR_SURV * 4;
 #define PK_RR(M)                                                                                \
   {                                                                                             \

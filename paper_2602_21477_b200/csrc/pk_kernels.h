@@ -44,6 +44,7 @@ struct ListTable {
   const int64_t* cid;    // [nslots] cluster id (-1 = empty slot)
   const int32_t* scope;  // [nslots] scope code
   const float* cent;     // [nslots][dp]
+  const float* nrm;      // [arena_rows] squared row norms (FFMA; tensor-core screen input)
   int32_t nslots;
   int32_t dp;            // padded row stride (multiple of DC)
   int32_t d;             // true dimension
@@ -111,5 +112,16 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                          cudaStream_t st);
 float screen_coef(int metric, int dp);
+float screen_coef_tf32(int metric, int dp);
+size_t tc_smem_bytes();
+// Row squared norms for the arena (tensor-core screen input).
+void launch_row_norms(const float* rows, int64_t n, int dp, float* out, cudaStream_t st);
+// Tensor-core screened persistent scan (tcgen05 TF32); same outputs as
+// launch_scan_screen.  qsw: scratch of 8 * B * dp floats.
+void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd, int B,
+                    float* qsw, const float* qnorm2, const ScanItem* items, const int32_t* n_items,
+                    int max_items, const QPair* qpairs, int kk, int32_t* work_ctr, uint32_t* Uq,
+                    uint32_t* slot_hi, int32_t* slot_n, int4* cpool, int32_t* ccount, int cap,
+                    int num_sms, cudaStream_t st);
 
 }  // namespace pk
