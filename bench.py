@@ -20,9 +20,12 @@ reference arithmetic.  Prints ONE JSON line (rank 0).
 --impl reference times that oracle port alone (the reference itself is a Python
 package; its hot path restated in C is the CPU implementation of the path).
 Multi-GPU (torchrun, N>1): weak scaling -- every rank owns a 1M x 768 shard of
-a N-million-vector index (lists sharded by rank, centroids replicated), each
-rank scans its probed local lists and the per-rank top-k are merged through
-an NCCL all-gather.
+an N-million-vector index (nlist 1024 N, lists sharded by rank, centroids
+replicated) and brings its own 256 queries per step.  Dispatch: each rank runs
+the coarse stage on its batch, the queries and their list handles are
+all-gathered (NCCL); every rank scans its own lists for all N*256 queries;
+combine: the per-shard top-k blocks go back to their origin rank (NCCL
+all-to-all) and are merged on the device.
 """
 
 from __future__ import annotations
@@ -49,7 +52,7 @@ def parse():
     p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--n", type=int, default=1_000_000)
+    p.add_argument("--rows", dest="n", type=int, default=1_000_000, help="rows per GPU")
     p.add_argument("--d", type=int, default=768)
     p.add_argument("--nlist", type=int, default=1024)
     p.add_argument("--nprobe", type=int, default=32)
@@ -235,38 +238,22 @@ def run_reference(a):
 
 
 # ---------------------------------------------------------------- our arm
-def run_ours(a):
+def build_shard(a, rank, dev):
+    """This rank's 1M x 768 shard: unit-sphere rows, device k-means (kmeans_assign
+    arithmetic, a.kmeans_iters rounds), rows sorted by list.  Returns device
+    rows/ids sorted by list, list lengths and offsets, and the host base."""
     import torch
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    from paper_2602_21477_b200 import DeviceIndex
-    from paper_2602_21477_b200 import build as B
     from paper_2602_21477_b200 import _native as N
 
-    if rank == 0:
-        B.build()
-    if dist:
-        dist.barrier()
-    N.load()
-
-    t_build = time.perf_counter()
     base = make_base(a.n, a.d, a.seed + rank)  # rank r owns shard r (weak scaling)
-    dev = torch.device("cuda", local)
     X = torch.from_numpy(base).to(dev)
     seeds = X[torch.from_numpy(seed_rows(a.n, a.nlist, a.seed + rank)).to(dev)].contiguous()
     cents = seeds
     labels = torch.empty(a.n, dtype=torch.int64, device=dev)
     dists = torch.empty(a.n, dtype=torch.float64, device=dev)
     for _ in range(max(1, a.kmeans_iters)):
+        torch.cuda.synchronize()
         N.check(N.lib().pk_kmeans_assign(X.data_ptr(), a.n, cents.data_ptr(), a.nlist, a.d,
                                          labels.data_ptr(), dists.data_ptr(), N.PK_DEVICE_PTRS))
         sums = torch.zeros(a.nlist, a.d, dtype=torch.float64, device=dev)
@@ -278,40 +265,75 @@ def run_ours(a):
     ids_sorted = (order + rank * a.n).contiguous()
     lens = torch.bincount(labels, minlength=a.nlist).cpu().numpy().astype(np.int64)
     offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
-    del X, labels, dists
-    ix = DeviceIndex(a.d, 0, local, reserve_rows=int(a.n * 1.3) + 4096, reserve_lists=a.nlist * world)
-    # local lists: cid = rank * nlist + c ; remote lists: centroid only (no rows)
-    cent_tab = {}
-    live = [c for c in range(a.nlist) if lens[c] > 0]
-    for c in live:
-        cid = rank * a.nlist + c
-        cent_tab[cid] = ix.create_list_device(cid, 0, Xs[offs[c]:offs[c] + lens[c]],
-                                              ids_sorted[offs[c]:offs[c] + lens[c]])
+    torch.cuda.synchronize()
+    return base, Xs, ids_sorted, lens, offs
+
+
+def run_ours(a):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PK_BENCH_SHARE_GPU=1: every rank on cuda:0 over gloo -- only to exercise
+    # the multi-rank code path on a one-GPU box; never a bench number
+    share = os.environ.get("PK_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2602_21477_b200 import DeviceIndex
+    from paper_2602_21477_b200 import build as B
+    from paper_2602_21477_b200 import _native as N
+    from paper_2602_21477_b200.sharded import ShardedIndex, block_offsets
+
+    if rank == 0:
+        B.build()
     if dist:
-        # replicate every rank's centroid table (coarse quantizer sees all lists)
-        mine = torch.from_numpy(np.stack([cent_tab[rank * a.nlist + c] for c in live])).to(dev)
-        mine_ids = torch.tensor([rank * a.nlist + c for c in live], dtype=torch.int64, device=dev)
-        sizes = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
-        dist.all_gather(sizes, torch.tensor([len(live)], dtype=torch.int64, device=dev))
-        mx = int(max(int(s.item()) for s in sizes))
-        pad = torch.zeros(mx, a.d, device=dev)
-        pad[:len(live)] = mine
-        padi = torch.full((mx,), -1, dtype=torch.int64, device=dev)
-        padi[:len(live)] = mine_ids
-        allc = [torch.zeros_like(pad) for _ in range(world)]
-        alli = [torch.zeros_like(padi) for _ in range(world)]
-        dist.all_gather(allc, pad)
-        dist.all_gather(alli, padi)
-        for r in range(world):
-            if r == rank:
-                continue
-            cc, ii = allc[r].cpu().numpy(), alli[r].cpu().numpy()
-            for j in range(int(sizes[r].item())):
-                ix.add_remote_list(int(ii[j]), 0, cc[j])
+        dist.barrier()
+    N.load()
+
+    t_build = time.perf_counter()
+    dev = torch.device("cuda", local)
+    base, Xs, ids_sorted, lens, offs = build_shard(a, rank, dev)
+    reserve = dict(reserve_rows=int(a.n * 1.3) + 4096, reserve_lists=a.nlist * world)
+    sh = None
+    if world == 1:
+        ix = DeviceIndex(a.d, 0, local, **reserve)
+        live = [c for c in range(a.nlist) if lens[c] > 0]
+        cent_tab = {c: ix.create_list(c, 0, Xs[offs[c]:offs[c] + lens[c]],
+                                      ids_sorted[offs[c]:offs[c] + lens[c]]) for c in live}
+    else:
+        # global list table: rank r's k-means list c is cid r * nlist + c, owned by r
+        lens_all = torch.empty(world * a.nlist, dtype=torch.int64, device=dev)
+        dist.all_gather_into_tensor(lens_all, torch.from_numpy(lens).to(dev))
+        lens_all = lens_all.cpu().numpy().reshape(world, a.nlist)
+        gl = [(r, c) for r in range(world) for c in range(a.nlist) if lens_all[r, c] > 0]
+        gcids = [r * a.nlist + c for r, c in gl]
+        sh = ShardedIndex(a.d, 0, local, **reserve)
+        ix = sh.local
+
+        def fetch(i):
+            c = gl[i][1]
+            return Xs[offs[c]:offs[c] + lens[c]], ids_sorted[offs[c]:offs[c] + lens[c]]
+
+        sh.load(gcids, [0] * len(gl), [int(lens_all[r, c]) for r, c in gl], fetch,
+                owners=[r for r, _ in gl])
+        live = [c for c in range(a.nlist) if lens[c] > 0]
+        cent_tab = None
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t_build
 
-    Qall_h = make_queries(base, (a.warmup + a.steps) * a.batch, a.seed)  # same queries on all ranks
+    # every rank brings its own batches (perturbed rows of its shard + fresh unit vectors)
+    Qall_h = make_queries(base, (a.warmup + a.steps) * a.batch, a.seed + 1000 * rank)
     Qall = torch.from_numpy(Qall_h).to(dev).view(a.warmup + a.steps, a.batch, a.d)
     codes = torch.zeros(1, dtype=torch.int32, device=dev)
     kk = a.k
@@ -321,21 +343,22 @@ def run_ours(a):
     o_n = torch.empty(a.batch, dtype=torch.int32, device=dev)
     o_s = torch.empty(a.batch, dtype=torch.int64, device=dev)
     stream = torch.cuda.ExternalStream(ix.stream_handle(), device=dev)
-    g_ids = g_d = None
-    if dist:
-        g_ids = [torch.empty_like(o_ids) for _ in range(world)]
-        g_d = [torch.empty_like(o_d) for _ in range(world)]
-        m_ids = torch.empty_like(o_ids)
-        m_d = torch.empty_like(o_d)
-        m_n = torch.empty_like(o_n)
+    bufs = None
+    if sh is not None:
+        bb = block_offsets(a.batch, kk)["total"]
+        bufs = {"probe": torch.empty(a.batch, a.nprobe, dtype=torch.int32, device=dev),
+                "q_all": torch.empty(world * a.batch, a.d, dtype=torch.float32, device=dev),
+                "probe_all": torch.empty(world * a.batch, a.nprobe, dtype=torch.int32, device=dev),
+                "send": torch.empty(world * bb, dtype=torch.uint8, device=dev),
+                "recv": torch.empty(world * bb, dtype=torch.uint8, device=dev)}
 
     def step(s):
-        ix.search_device(Qall[s], codes, a.nprobe, kk, o_ids, o_d, o_c, o_n, o_s)
-        if dist:
+        if sh is None:
+            ix.search_device(Qall[s], codes, a.nprobe, kk, o_ids, o_d, o_c, o_n, o_s)
+        else:
             with torch.cuda.stream(stream):
-                dist.all_gather(g_ids, o_ids)
-                dist.all_gather(g_d, o_d)
-                ix.merge_ranked(torch.stack(g_d), torch.stack(g_ids), kk, m_ids, m_d, m_n)
+                sh.search_dispatch_device(Qall[s], codes, a.nprobe, kk, bufs, o_ids, o_d, o_c,
+                                          o_n, o_s)
 
     for w in range(a.warmup):
         step(w)
@@ -360,24 +383,38 @@ def run_ours(a):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_q = a.steps * a.batch  # every rank serves the same queries over its shard
+    total_q = world * a.steps * a.batch  # every rank serves its own batch each step
     qps = total_q / (ms / 1000.0)
 
-    # ---- roofline of the fused scan: algorithmic bytes of distinct lists per batch
+    # ---- roofline of the fused scan: algorithmic bytes of the distinct local
+    # lists each scan launch reads (the probe sets of the same batches)
     row_bytes = 4 * a.d + 8
     alg_bytes = []
     for s in range(a.steps):
-        out = ix.search(Qall_h[(a.warmup + s) * a.batch:(a.warmup + s + 1) * a.batch], [0],
-                        a.nprobe, kk, want_probe=True)
-        pr = np.unique(out.probe[out.probe >= 0])
-        loc = pr[(pr // a.nlist) == rank] % a.nlist
-        alg_bytes.append(float(lens[loc].sum()) * row_bytes)
+        if sh is None:
+            out = ix.search(Qall_h[(a.warmup + s) * a.batch:(a.warmup + s + 1) * a.batch], [0],
+                            a.nprobe, kk, want_probe=True)
+            pr = np.unique(out.probe[out.probe >= 0])
+            alg_bytes.append(float(lens[pr].sum()) * row_bytes)
+        else:
+            step(a.warmup + s)
+            torch.cuda.synchronize()
+            pa = bufs["probe_all"].cpu().numpy()
+            pr = np.unique(pa[pa >= 0])  # list handles = global registration order
+            gl_lens = np.array([int(lens_all[r, c]) for r, c in gl], dtype=np.int64)
+            mine = np.array([r == rank for r, _ in gl])
+            alg_bytes.append(float(gl_lens[pr][mine[pr]].sum()) * row_bytes)
     pool = None
     try:
-        out = ix.search(Qall_h[a.warmup * a.batch:(a.warmup + 1) * a.batch], [0], a.nprobe, kk)
-        pc = ix.pool_counts(a.batch)
+        if sh is None:
+            ix.search(Qall_h[a.warmup * a.batch:(a.warmup + 1) * a.batch], [0], a.nprobe, kk)
+        B_last = a.batch * world
+        pc = ix.pool_counts(B_last)
         pool = {"mean": float(pc.mean()), "max": int(pc.max()), "p50": float(np.median(pc)),
                 "rows_reranked_per_step": int(pc.sum())}
+        if sh is None:
+            cc = ix.coarse_counts(a.batch)
+            pool["coarse_lists_reranked"] = {"mean": float(cc.mean()), "max": int(cc.max())}
     except Exception:
         pass
     scan_ms = stage_ms["scan"] / max(ncalls, 1)
@@ -385,17 +422,25 @@ def run_ours(a):
     peak, peak_src = load_peaks()
     traffic = load_traffic()
 
-    # ---- e2e through the C-ABI with host buffers
+    # ---- e2e through the public API with host buffers (pinned queries in,
+    # results out, every step)
     e2e = None
     if not a.no_e2e:
         Qpin = torch.from_numpy(Qall_h).pin_memory().numpy().reshape(a.warmup + a.steps, a.batch, a.d)
+
+        def host_step(s):
+            if sh is None:
+                ix.search(Qpin[s], [0], a.nprobe, kk)
+            else:
+                sh.search_dispatch(Qpin[s], [0], a.nprobe, kk)
+
         for w in range(min(a.warmup, 3)):
-            ix.search(Qpin[w], [0], a.nprobe, kk)
+            host_step(w)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         for s in range(a.steps):
-            ix.search(Qpin[a.warmup + s], [0], a.nprobe, kk)
+            host_step(a.warmup + s)
         e2e_s = time.perf_counter() - t0
         if dist:
             t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
@@ -403,51 +448,60 @@ def run_ours(a):
             e2e_s = float(t.item())
         e2e = {"value": total_q / e2e_s, "unit": UNIT, "h2d_bytes_per_step": a.batch * a.d * 4,
                "d2h_bytes_per_step": a.batch * (kk * (8 + 4 + 8) + 4 + 8),
-               "path": "pk_search C-ABI, pinned host query buffer, results to host, per-step sync"}
+               "path": ("pk_search C-ABI" if sh is None else
+                        "ShardedIndex.search_dispatch (pk_search_coarse / NCCL / "
+                        "pk_search_probed / pk_merge_shards)")
+               + ", pinned host query buffer, results to host, per-step sync (per rank)"}
 
-    # ---- CPU baseline (oracle port) + parity on the same sample, rank 0 only
+    # ---- CPU baseline (oracle port) + parity on the same sample, rank 0 at N=1
     cpu = parity = None
-    if rank == 0:
+    if rank == 0 and world == 1:
         from oracle import oracle as O
 
         threads = os.cpu_count() or 1
         rows_h = Xs.cpu().numpy()
         ids_h = ids_sorted.cpu().numpy()
-        cids_l = np.array([rank * a.nlist + c for c in live], dtype=np.int64)
+        cids_l = np.array(live, dtype=np.int64)
         flat = O.FlatIVF(rows_h, ids_h, offs[live], lens[live],
-                         np.stack([cent_tab[c] for c in cids_l]), cids_l)
+                         np.stack([cent_tab[c] for c in live]), cids_l)
         sample = a.cpu_sample or min(a.batch, max(16, 4 * threads))
         Qs = Qall_h[a.warmup * a.batch: a.warmup * a.batch + sample]
         t_cpu, (r_ids, r_d, r_n, r_p, r_sc) = oracle_time(flat, Qs, a.nprobe, kk, threads)
         cpu = {"value": sample / t_cpu, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"first {sample} queries of timed step 0 on this rank's shard, "
-                         f"C oracle (oracle/pancake_oracle.c), {threads} threads"}
-        if world == 1:
-            g = ix.search(Qs, [0], a.nprobe, kk, want_probe=True)
-            parity = {"queries": sample,
-                      "id_mismatch": int((g.ids != r_ids).sum()),
-                      "dist_bit_mismatch": int((g.dists.view(np.uint32) != r_d.view(np.uint32)).sum()),
-                      "probe_mismatch": int((g.probe != r_p).sum())}
+               "sample": f"first {sample} queries of timed step 0, C oracle "
+                         f"(oracle/pancake_oracle.c), {threads} threads"}
+        g = ix.search(Qs, [0], a.nprobe, kk, want_probe=True)
+        parity = {"queries": sample,
+                  "id_mismatch": int((g.ids != r_ids).sum()),
+                  "dist_bit_mismatch": int((g.dists.view(np.uint32) != r_d.view(np.uint32)).sum()),
+                  "probe_mismatch": int((g.probe != r_p).sum())}
 
     if rank == 0:
+        per_step = 8 if sh is None else 11  # our kernels per search step
         line = {
             "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "configs[1]: 1M x 768 fp32 IVF per GPU, nlist 1024 per GPU, "
-                                   "nprobe 32, k 10, batch 256 queries per step",
+            "config": {"workload": "configs[1]: 1M x 768 fp32 IVF per GPU (nlist 1024 per GPU), "
+                                   "nprobe 32, k 10, 256 queries per GPU per step"
+                                   + ("" if world == 1 else
+                                      f"; {world}M x 768 global index, nlist {world * a.nlist}, "
+                                      "lists sharded by rank (configs[3] shape)"),
                        "n_per_gpu": a.n, "d": a.d, "nlist_per_gpu": a.nlist, "nprobe": a.nprobe,
-                       "k": a.k, "batch": a.batch,
+                       "k": a.k, "batch_per_gpu": a.batch,
                        "l2": "inputs larger than L2 (index 3.1 GB per GPU; each batch reads "
                              "~all lists)",
-                       "parallelism": f"list-sharded x{world}" + (", NCCL all-gather top-k merge" if world > 1 else "")},
+                       "parallelism": f"list-sharded x{world}" + (
+                           ", dispatch (NCCL all-gather of queries + list handles) / combine "
+                           "(NCCL all-to-all of per-shard top-k, device merge)" if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                         "kernel": "scan_kernel<SQ_L2> (fused posting-list scan + per-list top-k)",
+                         "kernel": "scan_tc_kernel<SQ_L2> (TMA-fed tcgen05 TF32-screened posting-list "
+                                   "scan + per-list top-k bounds)",
                          "algorithmic_bytes_per_launch": float(np.mean(alg_bytes)),
                          "kernel_ms_per_launch": scan_ms, "peak_source": peak_src},
             "stage_ms_per_step": {k_: v / max(ncalls, 1) for k_, v in stage_ms.items()},
-            "gpu_launches": a.steps * 5 + (a.steps if world > 1 else 0),
+            "gpu_launches": a.steps * per_step,
             "clocks": clk.summary(),
             "e2e": e2e, "cpu_baseline": cpu, "parity_vs_oracle": parity, "build_s": build_s,
             "screen_candidates_per_query": pool,

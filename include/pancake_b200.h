@@ -111,6 +111,47 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags);
 
+/* ---- sharded search ------------------------------
+ * Lists are partitioned over ranks (one index per GPU); the centroid table is
+ * replicated so every rank computes the identical global probe set
+ * (graph.py:321-396 semantics), scans only the lists it owns, and the
+ * per-rank top-kk are exchanged (NCCL all-gather) and merged.
+ *
+ * Register a list owned by another rank: its centroid joins the coarse
+ * quantizer (it is probed and counted exactly like a local list) but it holds
+ * no rows here.  Appending to it is a usage error. */
+int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const float* centroid);
+/* Size of one shard result block for (B, kk): the unit the all-gather moves.
+ * Layout (byte offsets, nkk = B*kk):
+ *   ids     i64[B][kk]  @ 0
+ *   cids    i64[B][kk]  @ 8*nkk
+ *   scanned i64[B]      @ 16*nkk
+ *   dists   f32[B][kk]  @ 16*nkk + 8*B
+ *   n       i32[B]      @ 20*nkk + 8*B
+ * padded to 16 bytes.  pk_search (PK_DEVICE_PTRS) writes one straight into
+ * these offsets. */
+int64_t pk_shard_block_bytes(int64_t B, int32_t kk);
+/* Split form of pk_search for the dispatch/combine path (every rank brings its
+ * own batch):
+ * pk_search_coarse: the coarse stage only -- per query the first nprobe
+ *   in-scope lists as list handles (int32 [B][nprobe], -1 padded).  Handles are
+ *   slot indices; they agree across ranks whose indexes were built by the same
+ *   sequence of list creations (ShardedIndex.load builds in global order).
+ * pk_search_probed: the scan stage only, for given handles: scans the probed
+ *   lists this index holds (remote lists add nothing) and writes B / group
+ *   shard result blocks, block g = queries [g*group, (g+1)*group). */
+int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                     int32_t nscopes, int32_t nprobe, int32_t* out_probe, int flags);
+int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe, int32_t nprobe,
+                     int32_t kk, int64_t group, void* out_blocks, int flags);
+/* Merge R gathered blocks (contiguous, R * pk_shard_block_bytes) into the
+ * global first kk per query by (distance, id), first occurrence per id
+ * (engine.py:406-426); out_scanned = sum over shards (may be NULL).
+ * R * kk <= 1024.  Pointers follow `flags` (device: async on the index stream). */
+int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int32_t kk,
+                    int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
+                    int64_t* out_scanned, int flags);
+
 /* ---- measurement ------------------------------------------------------ */
 /* Between begin and end every pk_search records CUDA events on the index
  * stream around its stages: [0] input copy, [1] coarse distances,
@@ -122,6 +163,9 @@ int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls);
 /* Candidate-pool size per query of the last screened search (host int32[B]);
  * values above the pool capacity mean that query took the exact overflow path. */
 int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B);
+/* Lists re-ranked exactly per query by the last search's tensor-core coarse
+ * quantizer (host int32[B]). */
+int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,12 @@ _SIGS = [
     ("pk_profile_begin", [_vp], _int),
     ("pk_profile_end", [_vp, _vp, _int, _i32p], _int),
     ("pk_debug_pool_counts", [_vp, _vp, _i64], _int),
+    ("pk_debug_coarse_counts", [_vp, _vp, _i64], _int),
+    ("pk_search_coarse", [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _int], _int),
+    ("pk_search_probed", [_vp, _vp, _i64, _vp, _i32, _i32, _i64, _vp, _int], _int),
+    ("pk_list_add_remote", [_vp, _i64, _i32, _vp], _int),
+    ("pk_shard_block_bytes", [_i64, _i32], _i64),
+    ("pk_merge_shards", [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _int], _int),
 ]
 STAGES = ("input", "coarse_dist", "coarse_select", "route", "scan", "merge_out")
 EXPORTED = [s[0] for s in _SIGS]

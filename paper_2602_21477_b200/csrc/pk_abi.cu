@@ -121,12 +121,17 @@ struct pk_index {
   // list table (host mirror + device copy)
   std::vector<int64_t> h_off, h_len, h_cap, h_cid;
   std::vector<int32_t> h_scope;
+  std::vector<uint8_t> h_remote;  // list owned by another shard (centroid only)
   std::unordered_map<int64_t, int32_t> cid2slot;
   std::vector<int32_t> free_slots;
   int32_t nslots = 0, slot_cap = 0;
   int64_t *d_off = nullptr, *d_len = nullptr, *d_cid = nullptr;
   int32_t* d_scope = nullptr;
   float* d_cent = nullptr;
+  float* d_cnrm = nullptr;  // squared centroid norms (FFMA; coarse screen input)
+  float* d_chi = nullptr;   // TF32 hi / lo split of the centroid table (coarse screen)
+  float* d_clo = nullptr;
+  CoarseMaps cmaps;         // c[0..1]: 128 slots x 32 floats, SWIZZLE_128B (q[] per search)
   int32_t dirty_lo = INT32_MAX, dirty_hi = -1;
 
   // search scratch
@@ -136,8 +141,13 @@ struct pk_index {
   int chunk_rows = 512;
   bool screen = true;  // screened scan + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
   bool tensor = true;  // screen dots on tcgen05 (TF32); PK_SCREEN=ffma uses CUDA-core FFMA
+  bool coarse_tc = true;  // coarse quantizer on tcgen05 + exact re-rank; PK_COARSE=exact disables
+  bool coarse_split = true;  // 3xTF32 hi/lo split (tight bound); PK_COARSE=tf32 for one product
+  DevBuf qhi, qlo;
+  DevBuf ncand;
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
+  DevBuf shard_in, shard_out, pb, pb_out;
 
   // stage timing (pk_profile_begin / pk_profile_end): events around each
   // stage of every pk_search while enabled.
@@ -207,6 +217,29 @@ struct pk_index {
     return PK_OK;
   }
 
+  // 2-D fp32 tensor map [rows][ld] with boxes of `box_rows` x DC floats, SWIZZLE_128B.
+  int encode_2d(CUtensorMap* m, const float* ptr, int64_t ld, int64_t rows, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return fail(PK_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t gdim[2] = {(cuuint64_t)ld, (cuuint64_t)std::max<int64_t>(rows, 1)};
+    cuuint64_t gstride[1] = {(cuuint64_t)(ld * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)DC, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), gdim, gstride,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(PK_ERR_DEVICE, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PK_OK;
+  }
+
+  // Squared norm of slot s's centroid (coarse screen input).
+  // Derived centroid data of slot s: squared norm and the TF32 hi/lo split.
+  void centroid_norm(int32_t s) {
+    launch_row_norms(d_cent + (int64_t)s * dp, 1, (int)dp, d_cnrm + s, st);
+    launch_tf32_split(d_cent + (int64_t)s * dp, 1, (int)dp, d_chi + (int64_t)s * dp,
+                      d_clo + (int64_t)s * dp, st);
+  }
+
   int grow_arena(int64_t need_rows) {
     int64_t ncap = std::max<int64_t>({need_rows, arena_cap + arena_cap / 2, 1024});
     float* nrows = nullptr;
@@ -267,28 +300,47 @@ struct pk_index {
     CK(cudaMalloc(&nl, ncap * 8));
     CK(cudaMalloc(&nc, ncap * 8));
     CK(cudaMalloc(&ns, ncap * 4));
+    float *ncn = nullptr, *nhi = nullptr, *nlo = nullptr;
     CK(cudaMalloc(&ncent, (size_t)ncap * dp * 4));
+    CK(cudaMalloc(&nhi, (size_t)ncap * dp * 4));
+    CK(cudaMalloc(&nlo, (size_t)ncap * dp * 4));
+    CK(cudaMalloc(&ncn, (size_t)ncap * 4));
     CK(cudaMemsetAsync(ncent, 0, (size_t)ncap * dp * 4, st));
+    CK(cudaMemsetAsync(nhi, 0, (size_t)ncap * dp * 4, st));
+    CK(cudaMemsetAsync(nlo, 0, (size_t)ncap * dp * 4, st));
+    CK(cudaMemsetAsync(ncn, 0, (size_t)ncap * 4, st));
     if (d_cent) {
       CK(cudaMemcpyAsync(ncent, d_cent, (size_t)nslots * dp * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(nhi, d_chi, (size_t)nslots * dp * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(nlo, d_clo, (size_t)nslots * dp * 4, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(ncn, d_cnrm, (size_t)nslots * 4, cudaMemcpyDeviceToDevice, st));
       CK(cudaStreamSynchronize(st));
       cudaFree(d_off);
       cudaFree(d_len);
       cudaFree(d_cid);
       cudaFree(d_scope);
       cudaFree(d_cent);
+      cudaFree(d_cnrm);
+      cudaFree(d_chi);
+      cudaFree(d_clo);
     }
     d_off = no;
     d_len = nl;
     d_cid = nc;
     d_scope = ns;
     d_cent = ncent;
+    d_cnrm = ncn;
+    d_chi = nhi;
+    d_clo = nlo;
     slot_cap = ncap;
+    RET(encode_2d(&cmaps.c[0], coarse_split ? d_chi : d_cent, dp, slot_cap, 128));
+    RET(encode_2d(&cmaps.c[1], d_clo, dp, slot_cap, 128));
     h_off.resize(ncap, 0);
     h_len.resize(ncap, 0);
     h_cap.resize(ncap, 0);
     h_cid.resize(ncap, -1);
     h_scope.resize(ncap, -1);
+    h_remote.resize(ncap, 0);
     // whole table must be re-uploaded into the new arrays
     if (nslots > 0) {
       mark(0);
@@ -438,6 +490,11 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   if (const char* e = getenv("PK_SCAN_EXACT")) ix->screen = atoi(e) == 0;
   if (const char* e = getenv("PK_POOL_CAP")) ix->pool_cap = std::max(1, atoi(e));
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
+  if (const char* e = getenv("PK_COARSE")) {
+    ix->coarse_tc = strcmp(e, "exact") != 0;
+    ix->coarse_split = strcmp(e, "tf32") != 0;
+  }
+  if (metric == COSINE) ix->coarse_tc = false;
   if (metric == COSINE) ix->screen = false;
   if (ix->screen) ix->chunk_rows = std::min(ix->chunk_rows, 2 * TILE);
   cudaError_t e = cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking);
@@ -467,12 +524,15 @@ int pk_index_destroy(pk_index* ix) {
   cudaFree(ix->d_cid);
   cudaFree(ix->d_scope);
   cudaFree(ix->d_cent);
+  cudaFree(ix->d_cnrm);
+  cudaFree(ix->d_chi);
+  cudaFree(ix->d_clo);
   for (cudaEvent_t e : ix->prof_ev) cudaEventDestroy(e);
   for (DevBuf* b : {&ix->q, &ix->qnorm, &ix->dc, &ix->probe, &ix->probe_key, &ix->counts,
                     &ix->fillb, &ix->items, &ix->nitems, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list, &ix->work,
                     &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw})
+                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->ncand, &ix->qhi, &ix->qlo})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -511,15 +571,93 @@ int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* r
   ix->h_cap[s] = cap;
   ix->h_cid[s] = cid;
   ix->h_scope[s] = scope_code;
+  ix->h_remote[s] = 0;
   ix->cid2slot[cid] = s;
   ix->mark(s);
   launch_centroid(ix->rows + off * ix->dp, ix->dp, n, (int)ix->dp, ix->d_cent + (int64_t)s * ix->dp,
                   ix->st);
+  ix->centroid_norm(s);
   CK(cudaGetLastError());
   if (out_centroid) {
     CK(cudaMemcpyAsync(out_centroid, ix->d_cent + (int64_t)s * ix->dp, ix->d * 4,
                        cudaMemcpyDeviceToHost, ix->st));
     CK(cudaStreamSynchronize(ix->st));
+  }
+  return PK_OK;
+}
+
+int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const float* centroid) {
+  if (ix->cid2slot.count(cid)) return fail(PK_ERR_USAGE, "cluster %lld exists", (long long)cid);
+  if (!centroid) return fail(PK_ERR_USAGE, "remote list needs a centroid");
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  if (!ix->free_slots.empty()) {
+    s = ix->free_slots.back();
+    ix->free_slots.pop_back();
+  } else {
+    if (ix->nslots == ix->slot_cap) RET(ix->grow_slots(ix->nslots + 1));
+    s = ix->nslots++;
+  }
+  ix->h_off[s] = 0;
+  ix->h_len[s] = 0;
+  ix->h_cap[s] = 0;
+  ix->h_cid[s] = cid;
+  ix->h_scope[s] = scope_code;
+  ix->h_remote[s] = 1;
+  ix->cid2slot[cid] = s;
+  ix->mark(s);
+  CK(cudaMemcpyAsync(ix->d_cent + (int64_t)s * ix->dp, centroid, ix->d * 4, cudaMemcpyHostToDevice,
+                     ix->st));
+  ix->centroid_norm(s);
+  CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int64_t pk_shard_block_bytes(int64_t B, int32_t kk) {
+  if (B < 0 || kk < 1) return 0;
+  const int64_t nkk = B * kk;
+  return round_up(nkk * 20 + B * 12, 16);
+}
+
+int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int32_t kk,
+                    int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
+                    int64_t* out_scanned, int flags) {
+  if (R < 1 || B < 0) return fail(PK_ERR_USAGE, "bad shard count / batch");
+  if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
+  if ((int64_t)R * kk > shard_merge_cap())
+    return fail(PK_ERR_USAGE, "shards x kk above %d", shard_merge_cap());
+  if (B == 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  const bool dev = flags & PK_DEVICE_PTRS;
+  cudaStream_t st = ix->st;
+  const int64_t bb = pk_shard_block_bytes(B, kk);
+  const void* src = blocks;
+  int64_t *o_ids = out_ids, *o_cid = out_cids, *o_sc = out_scanned;
+  float* o_d = out_dists;
+  int32_t* o_n = out_n;
+  if (!dev) {
+    RET(ix->shard_in.ensure((size_t)R * bb));
+    CK(cudaMemcpyAsync(ix->shard_in.p, blocks, (size_t)R * bb, cudaMemcpyHostToDevice, st));
+    src = ix->shard_in.p;
+    RET(ix->shard_out.ensure((size_t)bb));  // same layout as a block
+    uint8_t* base = ix->shard_out.as<uint8_t>();
+    const int64_t nkk = B * kk;
+    o_ids = reinterpret_cast<int64_t*>(base);
+    o_cid = reinterpret_cast<int64_t*>(base + 8 * nkk);
+    o_sc = reinterpret_cast<int64_t*>(base + 16 * nkk);
+    o_d = reinterpret_cast<float*>(base + 16 * nkk + 8 * B);
+    o_n = reinterpret_cast<int32_t*>(base + 20 * nkk + 8 * B);
+  }
+  launch_shard_merge(src, bb, R, (int)B, kk, o_ids, o_d, (dev && !out_cids) ? nullptr : o_cid, o_n,
+                     (dev && !out_scanned) ? nullptr : o_sc, st);
+  CK(cudaGetLastError());
+  if (!dev) {
+    CK(cudaMemcpyAsync(out_ids, o_ids, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_dists, o_d, (size_t)B * kk * 4, cudaMemcpyDeviceToHost, st));
+    if (out_cids) CK(cudaMemcpyAsync(out_cids, o_cid, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_n, o_n, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
+    if (out_scanned) CK(cudaMemcpyAsync(out_scanned, o_sc, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
   }
   return PK_OK;
 }
@@ -530,6 +668,7 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
+  if (ix->h_remote[s]) return fail(PK_ERR_USAGE, "cluster %lld is owned by another shard", (long long)cid);
   const int64_t len = ix->h_len[s];
   if (len + n > ix->h_cap[s]) {
     // relocate into a larger range (Cluster._grow x1.5, ref/clusters.py:61-69)
@@ -583,6 +722,7 @@ int pk_list_retire(pk_index* ix, int64_t cid) {
   ix->h_len[s] = 0;
   ix->h_cap[s] = 0;
   ix->h_scope[s] = -1;
+  ix->h_remote[s] = 0;
   ix->cid2slot.erase(cid);
   ix->free_slots.push_back(s);
   ix->mark(s);
@@ -597,6 +737,7 @@ int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
   if (n > 0)
     launch_centroid(ix->rows + ix->h_off[s] * ix->dp, ix->dp, n, (int)ix->dp,
                     ix->d_cent + (int64_t)s * ix->dp, ix->st);
+  ix->centroid_norm(s);
   CK(cudaGetLastError());
   if (out_centroid) {
     CK(cudaMemcpyAsync(out_centroid, ix->d_cent + (int64_t)s * ix->dp, ix->d * 4,
@@ -612,6 +753,7 @@ int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid) {
   RET(ix->slot_of(cid, &s));
   CK(cudaMemcpyAsync(ix->d_cent + (int64_t)s * ix->dp, centroid, ix->d * 4,
                      cudaMemcpyHostToDevice, ix->st));
+  ix->centroid_norm(s);
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
@@ -638,18 +780,24 @@ int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
   return PK_OK;
 }
 
-int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
-              int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids, float* out_dists,
-              int64_t* out_cids, int32_t* out_n, int64_t* out_probe, int64_t* out_scanned,
-              int flags) {
+}  // extern "C"
+
+// One batched search through the stages of pk_search.  probe_in (list
+// handles, [B][nprobe]) skips the coarse stage; probe_out stops after it.
+// in_dev / dev: input / output pointers are device pointers.
+static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                       int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids,
+                       float* out_dists, int64_t* out_cids, int32_t* out_n, int64_t* out_probe,
+                       int64_t* out_scanned, bool in_dev, bool dev, const int32_t* probe_in,
+                       int32_t* probe_out) {
   if (B < 0) return fail(PK_ERR_USAGE, "negative batch");
   if (nprobe < 1) return fail(PK_ERR_USAGE, "nprobe must be >= 1");
   if (nprobe > 2048) return fail(PK_ERR_USAGE, "nprobe %d above the device limit 2048", nprobe);
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
-  if (nscopes < 1 || nscopes > 64) return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
+  if (!probe_in && (nscopes < 1 || nscopes > 64))
+    return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
   if (B == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
-  const bool dev = flags & PK_DEVICE_PTRS;
   cudaStream_t st = ix->st;
   RET(ix->sync_table());
   const int64_t dp = ix->dp;
@@ -686,23 +834,53 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
   PROF(0);
   // inputs
   CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
-                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
-                     dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  if (!probe_in)
+    CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
+                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   const ListTable lt = ix->table();
   if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
-  if (ix->screen) {
+  if (ix->screen || ix->coarse_tc) {
     RET(ix->qnorm2.ensure(B * 4));
     launch_qnorm2(ix->q.as<float>(), dp, (int)B, (int)dp, ix->qnorm2.as<float>(), st);
   }
   PROF(1);
-  // 1. coarse quantizer: exact distances to every list centroid, select top-nprobe in scope
-  launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
-                    ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
-  PROF(2);
-  launch_coarse_select(ix->dc.as<float>(), ns, (int)B, lt, ix->scopes.as<int32_t>(), nscopes,
-                       nprobe, ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), st);
+  // 1. coarse quantizer: distances to every list centroid, top-nprobe in scope
+  if (probe_in) {
+    CK(cudaMemcpyAsync(ix->probe.p, probe_in, (size_t)B * nprobe * 4,
+                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    PROF(2);
+  } else if (ix->coarse_tc) {
+    RET(ix->ncand.ensure(B * 4));
+    if (ix->coarse_split) {
+      RET(ix->qhi.ensure((size_t)B * dp * 4));
+      RET(ix->qlo.ensure((size_t)B * dp * 4));
+      launch_tf32_split(ix->q.as<float>(), B, (int)dp, ix->qhi.as<float>(), ix->qlo.as<float>(), st);
+      RET(ix->encode_2d(&ix->cmaps.q[0], ix->qhi.as<float>(), dp, B, 64));
+      RET(ix->encode_2d(&ix->cmaps.q[1], ix->qlo.as<float>(), dp, B, 64));
+    } else {
+      RET(ix->encode_2d(&ix->cmaps.q[0], ix->q.as<float>(), dp, B, 64));
+    }
+    launch_coarse_tc(ix->metric, ix->coarse_split, ix->cmaps, ix->nslots, (int)B, (int)dp,
+                     ix->d_cnrm, ix->qnorm2.as<float>(), ix->dc.as<float>(), ns, st);
+    PROF(2);
+    launch_coarse_pick(ix->metric, ix->coarse_split, ix->dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, ix->q.as<float>(),
+                       ix->qnorm2.as<float>(), ix->scopes.as<int32_t>(), nscopes, nprobe,
+                       ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), ix->ncand.as<int32_t>(), st);
+  } else {
+    launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
+                      ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
+    PROF(2);
+    launch_coarse_select(ix->dc.as<float>(), ns, (int)B, lt, ix->scopes.as<int32_t>(), nscopes,
+                         nprobe, ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), st);
+  }
   PROF(3);
+  if (probe_out) {
+    CK(cudaMemcpyAsync(probe_out, ix->probe.p, (size_t)B * nprobe * 4,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    if (!dev) CK(cudaStreamSynchronize(st));
+    return PK_OK;
+  }
   // 2. route (query -> lists) into (list -> queries) work items
   CK(cudaMemsetAsync(ix->counts.p, 0, (size_t)ns * 4, st));
   launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt, ix->chunk_rows, ix->counts.as<int32_t>(),
@@ -792,10 +970,67 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
   return PK_OK;
 }
 
+extern "C" {
+
+int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+              int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids, float* out_dists,
+              int64_t* out_cids, int32_t* out_n, int64_t* out_probe, int64_t* out_scanned,
+              int flags) {
+  const bool dev = flags & PK_DEVICE_PTRS;
+  return search_core(ix, Q, B, scope_codes, nscopes, nprobe, kk, out_ids, out_dists, out_cids,
+                     out_n, out_probe, out_scanned, dev, dev, nullptr, nullptr);
+}
+
+int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                     int32_t nscopes, int32_t nprobe, int32_t* out_probe, int flags) {
+  if (!out_probe) return fail(PK_ERR_USAGE, "out_probe is required");
+  const bool dev = flags & PK_DEVICE_PTRS;
+  return search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
+                     nullptr, nullptr, dev, dev, nullptr, out_probe);
+}
+
+int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe, int32_t nprobe,
+                     int32_t kk, int64_t group, void* out_blocks, int flags) {
+  if (!probe || !out_blocks) return fail(PK_ERR_USAGE, "probe and out_blocks are required");
+  if (group < 1 || B % group != 0) return fail(PK_ERR_USAGE, "group must divide the batch");
+  if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
+  if (B == 0) return PK_OK;
+  const bool dev = flags & PK_DEVICE_PTRS;
+  RET(ix->pb.ensure((size_t)B * kk * 20 + B * 12 + 64));
+  int64_t* o_ids = ix->pb.as<int64_t>();
+  int64_t* o_cid = o_ids + B * kk;
+  int64_t* o_sc = o_cid + B * kk;
+  float* o_d = reinterpret_cast<float*>(o_sc + B);
+  int32_t* o_n = reinterpret_cast<int32_t*>(o_d + B * kk);
+  RET(search_core(ix, Q, B, nullptr, 0, nprobe, kk, o_ids, o_d, o_cid, o_n, nullptr, o_sc, dev,
+                  true, probe, nullptr));
+  const int64_t bb = pk_shard_block_bytes(group, kk);
+  void* dst = out_blocks;
+  if (!dev) {
+    RET(ix->pb_out.ensure((size_t)(B / group) * bb));
+    dst = ix->pb_out.p;
+  }
+  launch_reblock(o_ids, o_cid, o_sc, o_d, o_n, (int)B, (int)group, kk, bb, dst, ix->st);
+  CK(cudaGetLastError());
+  if (!dev) {
+    CK(cudaMemcpyAsync(out_blocks, dst, (size_t)(B / group) * bb, cudaMemcpyDeviceToHost, ix->st));
+    CK(cudaStreamSynchronize(ix->st));
+  }
+  return PK_OK;
+}
+
 int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B) {
   if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
   if ((size_t)B * 4 > ix->ccount.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
   CK(cudaMemcpyAsync(out, ix->ccount.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
+  CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B) {
+  if (!ix->coarse_tc) return fail(PK_ERR_USAGE, "exact coarse quantizer: no screened candidates");
+  if ((size_t)B * 4 > ix->ncand.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
+  CK(cudaMemcpyAsync(out, ix->ncand.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }

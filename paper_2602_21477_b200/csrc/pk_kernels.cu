@@ -15,6 +15,7 @@
 #include "pk_umma.cuh"
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 
 namespace pk {
@@ -1971,6 +1972,517 @@ void launch_scatter_rows(const float* src, int64_t lds, const int64_t* src_ids, 
                          cudaStream_t st) {
   if (n <= 0) return;
   scatter_rows_kernel<<<n, 128, 0, st>>>(src, lds, src_ids, n, dst_row, dst, dst_ids, dp);
+}
+
+}  // namespace pk
+
+namespace pk {
+
+// =====================================================================
+// Cross-shard merge: after the all-gather every rank
+// holds R per-shard top-kk lists per query, each sorted by (dist, id).  The
+// global answer is the first kk of their union by (dist, id) with first
+// occurrence per id (ref/engine.py:406-426) -- the k smallest of a union lie
+// in the union of every part's k smallest.  One CTA per query.
+// =====================================================================
+constexpr int SHM_CAP = 1024;  // R * kk <= 1024 (R <= 16 at kk 64)
+__global__ void __launch_bounds__(128) shard_merge_kernel(const uint8_t* __restrict__ blocks,
+                                                          int64_t block_bytes, int R, int B, int kk,
+                                                          int64_t* __restrict__ out_ids,
+                                                          float* __restrict__ out_d,
+                                                          int64_t* __restrict__ out_cid,
+                                                          int32_t* __restrict__ out_n,
+                                                          int64_t* __restrict__ out_scanned) {
+  extern __shared__ Entry sbuf[];  // [pow2 >= R * kk]
+  __shared__ int s_cnt;
+  const int b = blockIdx.x;
+  const int64_t nkk = (int64_t)B * kk;
+  const int total = R * kk;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int r = i / kk, e = i - r * kk;
+    const uint8_t* blk = blocks + (int64_t)r * block_bytes;
+    const int32_t n = reinterpret_cast<const int32_t*>(blk + (nkk * 20 + (int64_t)B * 8))[b];
+    if (e >= n) continue;
+    const int64_t id = reinterpret_cast<const int64_t*>(blk)[(int64_t)b * kk + e];
+    const float d = reinterpret_cast<const float*>(blk + nkk * 16 + (int64_t)B * 8)[(int64_t)b * kk + e];
+    Entry en;
+    en.key = f2key(d);
+    en.id = id;
+    en.pay = i;
+    sbuf[atomicAdd(&s_cnt, 1)] = en;
+  }
+  __syncthreads();
+  const int n = s_cnt;
+  cta_bitonic_sort(sbuf, n);
+  const int kept = cta_compact_sorted(sbuf, n, kk, true, &s_cnt);
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+    const int64_t o = (int64_t)b * kk + i;
+    if (i < kept) {
+      const int src = sbuf[i].pay;
+      const int r = src / kk, e = src - r * kk;
+      const uint8_t* blk = blocks + (int64_t)r * block_bytes;
+      out_ids[o] = sbuf[i].id;
+      out_d[o] = key2f(sbuf[i].key);
+      if (out_cid) out_cid[o] = reinterpret_cast<const int64_t*>(blk + nkk * 8)[(int64_t)b * kk + e];
+    } else {
+      out_ids[o] = -1;
+      out_d[o] = __int_as_float(0x7f800000);
+      if (out_cid) out_cid[o] = -1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    out_n[b] = kept;
+    if (out_scanned) {
+      int64_t sc = 0;
+      for (int r = 0; r < R; r++)
+        sc += reinterpret_cast<const int64_t*>(blocks + (int64_t)r * block_bytes + nkk * 16)[b];
+      out_scanned[b] = sc;
+    }
+  }
+}
+
+int shard_merge_cap() { return SHM_CAP; }
+
+// Regroup per-query results of a B-query batch into B / group shard result
+// blocks (block g = queries [g*group, (g+1)*group)), the unit the
+// dispatch/combine all-to-all moves.
+__global__ void reblock_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ cids,
+                               const int64_t* __restrict__ sc, const float* __restrict__ d,
+                               const int32_t* __restrict__ n, int B, int group, int kk,
+                               int64_t block_bytes, uint8_t* __restrict__ dst) {
+  const int64_t nkk_g = (int64_t)group * kk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)B * kk;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / kk), e = (int)(i - (int64_t)b * kk);
+    const int g = b / group, bl = b - g * group;
+    uint8_t* blk = dst + g * block_bytes;
+    const int64_t o = (int64_t)bl * kk + e;
+    reinterpret_cast<int64_t*>(blk)[o] = ids[i];
+    reinterpret_cast<int64_t*>(blk + 8 * nkk_g)[o] = cids[i];
+    reinterpret_cast<float*>(blk + 16 * nkk_g + 8 * (int64_t)group)[o] = d[i];
+    if (e == 0) {
+      reinterpret_cast<int64_t*>(blk + 16 * nkk_g)[bl] = sc[b];
+      reinterpret_cast<int32_t*>(blk + 20 * nkk_g + 8 * (int64_t)group)[bl] = n[b];
+    }
+  }
+}
+void launch_reblock(const int64_t* ids, const int64_t* cids, const int64_t* sc, const float* d,
+                    const int32_t* n, int B, int group, int kk, int64_t block_bytes, void* dst,
+                    cudaStream_t st) {
+  if (B <= 0) return;
+  const int64_t tot = (int64_t)B * kk;
+  reblock_kernel<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 1184), 256, 0, st>>>(
+      ids, cids, sc, d, n, B, group, kk, block_bytes, static_cast<uint8_t*>(dst));
+}
+
+void launch_shard_merge(const void* blocks, int64_t block_bytes, int R, int B, int kk,
+                        int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
+                        int64_t* out_scanned, cudaStream_t st) {
+  if (B <= 0) return;
+  int N = 1;
+  while (N < R * kk) N <<= 1;
+  size_t smem = (size_t)N * sizeof(Entry);
+  cudaFuncSetAttribute(shard_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  shard_merge_kernel<<<B, 128, smem, st>>>(static_cast<const uint8_t*>(blocks), block_bytes, R, B,
+                                           kk, out_ids, out_d, out_cid, out_n, out_scanned);
+}
+
+}  // namespace pk
+
+namespace pk {
+
+// =====================================================================
+// Coarse quantizer on the tensor cores (north_star
+// subsystem 1).  The reference probes the nprobe nearest in-scope clusters by
+// exact fp32 distance with ties to the lower cid (ref/graph.py:392-396 at
+// exhaustive ef).  Here:
+//   coarse_tc_kernel   S = C Q^T on tcgen05 (kind::tf32), C = the centroid
+//                      table (TMA SWIZZLE_128B tiles of 128 slots x 32 floats,
+//                      the UMMA A operand), Q = the batch (64-query tiles, the
+//                      B operand), fp32 accumulators in TMEM; the epilogue
+//                      forms the screened distance A = (|c|^2 + |q|^2) - 2 S
+//                      (neg_ip: -S) for every (query, slot).
+//   coarse_pick_kernel per query: |A - E| <= eps = coef (|c|^2 + |q|^2) (the
+//                      scan's proven TF32 bound, screen_coef_tf32); U = the
+//                      nprobe-th smallest A + eps over the in-scope lists
+//                      (radix select); every list with A - eps <= U is
+//                      re-ranked with the exact reference arithmetic and the
+//                      first nprobe by (E, cid) are emitted.  A list outside
+//                      that set has E > U >= E_(nprobe), so the emitted set
+//                      and order equal the exact quantizer's, ties included.
+// =====================================================================
+constexpr int CT_M = 128;      // centroid slots per CTA (UMMA M)
+constexpr int CT_N = 64;       // queries per CTA (UMMA N)
+constexpr int CT_STAGES = 4;
+constexpr size_t CT_A_BYTES = (size_t)CT_M * DC * 4;  // 16 KB
+constexpr size_t CT_B_BYTES = (size_t)CT_N * DC * 4;  // 8 KB
+size_t coarse_tc_smem_bytes(bool split) {
+  return (split ? 2 : 1) * CT_STAGES * (CT_A_BYTES + CT_B_BYTES) + 256 + 1024;
+}
+
+// SPLIT (default): centroids and queries are carried as TF32-exact hi parts
+// (low 13 mantissa bits cleared) plus lo = x - hi; D1 = C_hi Q_hi^T and
+// D2 = C_hi Q_lo^T + C_lo Q_hi^T accumulate in separate TMEM columns, dot =
+// D1 + D2.  The input-rounding error drops from ~2^-9 to ~3 * 2^-20 of
+// sum |c_j q_j| (coarse_coef()), so the exact re-rank set shrinks to the
+// boundary.  !SPLIT: one TF32 product of the fp32 tables.
+template <int METRIC, bool SPLIT>
+__global__ void __launch_bounds__(128, 1)
+    coarse_tc_kernel(const __grid_constant__ CoarseMaps maps, int nslots, int B, int nchunk,
+                     const float* __restrict__ cnrm, const float* __restrict__ qn2,
+                     float* __restrict__ Aout, int64_t lda) {
+  constexpr int NT = SPLIT ? 2 : 1;  // tables per operand
+  constexpr size_t STAGE_BYTES = NT * (CT_A_BYTES + CT_B_BYTES);
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + CT_STAGES * STAGE_BYTES);
+  uint64_t* empty = full + CT_STAGES;
+  uint64_t* done = empty + CT_STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  // stage s: A_hi [, A_lo], B_hi [, B_lo]
+  auto a_tile = [&](int s, int t) { return reinterpret_cast<float*>(base + s * STAGE_BYTES + t * CT_A_BYTES); };
+  auto b_tile = [&](int s, int t) {
+    return reinterpret_cast<float*>(base + s * STAGE_BYTES + NT * CT_A_BYTES + t * CT_B_BYTES);
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c0 = blockIdx.x * CT_M, b0 = blockIdx.y * CT_N;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < CT_STAGES; i++) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc(tmem_slot, NT * CT_N);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0 && lane == 0) {
+    for (int t = 0; t < NT; t++) {
+      tma_prefetch_desc(&maps.c[t]);
+      tma_prefetch_desc(&maps.q[t]);
+    }
+    const uint64_t pol = policy_evict_last();  // tables are re-read by the other CTAs
+    int s = 0;
+    uint32_t ph = 0;
+    for (int c = 0; c < nchunk; c++) {
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_arrive_expect_tx(&full[s], (uint32_t)STAGE_BYTES);
+      for (int t = 0; t < NT; t++) {
+        tma_load_2d(a_tile(s, t), &maps.c[t], &full[s], c * DC, c0, pol);
+        tma_load_2d(b_tile(s, t), &maps.q[t], &full[s], c * DC, b0, pol);
+      }
+      if (++s == CT_STAGES) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    const uint32_t idesc = umma_idesc_tf32(CT_M, CT_N);
+    int s = 0;
+    uint32_t ph = 0;
+    for (int c = 0; c < nchunk; c++) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      const uint32_t ah = smem_u32(a_tile(s, 0)), bh = smem_u32(b_tile(s, 0));
+#pragma unroll
+      for (int k = 0; k < DC / 8; k++) {
+        const uint32_t acc = (c | k) != 0;
+        umma_tf32(tmem, umma_desc_sw128(ah + k * 32), umma_desc_sw128(bh + k * 32), idesc, acc);
+        if (SPLIT) {
+          const uint32_t al = smem_u32(a_tile(s, NT - 1)), bl = smem_u32(b_tile(s, NT - 1));
+          umma_tf32(tmem + CT_N, umma_desc_sw128(ah + k * 32), umma_desc_sw128(bl + k * 32), idesc, acc);
+          umma_tf32(tmem + CT_N, umma_desc_sw128(al + k * 32), umma_desc_sw128(bh + k * 32), idesc, 1);
+        }
+      }
+      umma_commit(&empty[s]);
+      if (++s == CT_STAGES) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+    umma_commit(done);
+  }
+  __syncwarp();
+  mbar_wait(done, 0);
+  tc_fence_after();
+  const int m = c0 + 32 * warp + lane;  // this thread's centroid slot (TMEM lane)
+  const float cn = m < nslots ? cnrm[m] : 0.f;
+#pragma unroll
+  for (int g = 0; g < CT_N / 16; g++) {
+    float v[16], w[16];
+    tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + g * 16, v);
+    if (SPLIT) {
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + CT_N + g * 16, w);
+#pragma unroll
+      for (int a = 0; a < 16; a++) v[a] = __fadd_rn(v[a], w[a]);
+    }
+    if (m < nslots) {
+#pragma unroll
+      for (int a = 0; a < 16; a++) {
+        const int b = b0 + g * 16 + a;
+        if (b < B) {
+          const float A = (METRIC == SQ_L2) ? __fsub_rn(__fadd_rn(cn, qn2[b]), __fmul_rn(2.f, v[a]))
+                                            : -v[a];
+          Aout[(int64_t)b * lda + m] = A;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, NT * CT_N);
+}
+
+void launch_coarse_tc(int metric, bool split, const CoarseMaps& maps, int nslots, int B, int dp,
+                      const float* cnrm, const float* qn2, float* Aout, int64_t lda, cudaStream_t st) {
+  if (B <= 0 || nslots <= 0) return;
+  const size_t smem = coarse_tc_smem_bytes(split);
+  dim3 grid((unsigned)((nslots + CT_M - 1) / CT_M), (unsigned)((B + CT_N - 1) / CT_N));
+#define PK_CT(M, S)                                                                            \
+  {                                                                                            \
+    auto k = coarse_tc_kernel<M, S>;                                                           \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
+    k<<<grid, 128, smem, st>>>(maps, nslots, B, dp / DC, cnrm, qn2, Aout, lda);                \
+  }
+  if (metric == SQ_L2) {
+    if (split) PK_CT(SQ_L2, true) else PK_CT(SQ_L2, false)
+  } else {
+    if (split) PK_CT(IP, true) else PK_CT(IP, false)
+  }
+#undef PK_CT
+}
+
+// hi = x with the low 13 mantissa bits cleared (exactly representable in
+// TF32), lo = x - hi (exact in fp32).  Rows [0, n) of [n][dp].
+__global__ void tf32_split_kernel(const float* __restrict__ x, int64_t n4, float* __restrict__ hi,
+                                  float* __restrict__ lo) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = reinterpret_cast<const float4*>(x)[i], h, l;
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+    l.x = __fsub_rn(v.x, h.x);
+    l.y = __fsub_rn(v.y, h.y);
+    l.z = __fsub_rn(v.z, h.z);
+    l.w = __fsub_rn(v.w, h.w);
+    reinterpret_cast<float4*>(hi)[i] = h;
+    reinterpret_cast<float4*>(lo)[i] = l;
+  }
+}
+void launch_tf32_split(const float* x, int64_t n, int dp, float* hi, float* lo, cudaStream_t st) {
+  const int64_t n4 = n * dp / 4;
+  if (n4 <= 0) return;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 1184);
+  tf32_split_kernel<<<grid, 256, 0, st>>>(x, n4, hi, lo);
+}
+
+// |A - E| <= coef * (|c|^2 + |q|^2) + abs for the coarse screen.
+// split: c_dot = d 2^-21 (TMEM accumulation, the model validated for the scan
+// screen by tools/microbench/umma_check.cu) + 3 2^-20 (dropped lo*lo and the
+// TF32 conversions of the lo parts) + 2^-23 (D1 + D2) + 2d 2^-31 (D2's own
+// accumulation); !split: the scan's c_dot.  2x safety like the scan.
+float coarse_coef(int metric, int dp, bool split) {
+  if (!split) return screen_coef_tf32(metric, dp);
+  const double u = 1.0 / 16777216.0;
+  auto gam = [u](double n) { return n * u / (1.0 - n * u); };
+  const double c_dot = 2.0 * (dp / 2097152.0 + 3.0 / 1048576.0 + 1.0 / 8388608.0 + 2.0 * dp / 2147483648.0);
+  double c;
+  if (metric == SQ_L2) c = (c_dot + gam(dp) + 2.0 * gam(dp + 3) + 4.0 * u) / (1.0 - gam(dp));
+  else c = (0.5 * c_dot + gam(dp) + 2.0 * u) / (1.0 - gam(dp));
+  return (float)(c * 1.0625);
+}
+
+// Exact reference distance of the query in shared memory to centroid row `c`
+// (ref/kernels.py:73-95 arithmetic, j ascending over the true dimension).
+template <int METRIC>
+__device__ __forceinline__ float exact_dist_row(const float* __restrict__ qs, const float* __restrict__ c,
+                                                int d) {
+  float acc = 0.f;
+  int j = 0;
+  if ((d & 3) == 0) {
+    for (; j < d; j += 4) {
+      const float4 x = __ldg(reinterpret_cast<const float4*>(c + j));
+      const float4 q = *reinterpret_cast<const float4*>(qs + j);
+      acc = step4<METRIC>(acc, x, q);
+    }
+  } else {
+    for (; j < d; j++)
+      acc = (METRIC == SQ_L2) ? sq_step(acc, __ldg(c + j), qs[j]) : ip_step(acc, __ldg(c + j), qs[j]);
+  }
+  return METRIC == SQ_L2 ? acc : -acc;
+}
+
+constexpr int PICK_THREADS = 256;
+constexpr int PICK_CAP = 4096;  // candidate buffer (entries): nprobe (<= 2048) + new ones, pow2 for the sort
+
+template <int METRIC>
+__global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
+    const float* __restrict__ Aapp, int64_t lda, ListTable lt, const float* __restrict__ cnrm,
+    const float* __restrict__ Qd, const float* __restrict__ qn2,
+    const int32_t* __restrict__ scope_codes, int nscopes, int nprobe, float coef, float abs_coef,
+    int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key, int32_t* __restrict__ ncand_out) {
+  extern __shared__ float pick_smem[];
+  Entry* buf = reinterpret_cast<Entry*>(pick_smem);                // [PICK_CAP]
+  float* qs = reinterpret_cast<float*>(buf + PICK_CAP);            // [dp]
+  __shared__ int s_codes[64];
+  __shared__ unsigned s_hist[256];
+  __shared__ int s_cnt, s_total;
+  __shared__ uint32_t s_prefix;
+  __shared__ int s_rem;
+  const int b = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid < 64) s_codes[tid] = tid < nscopes ? scope_codes[tid] : -1;
+  for (int j = tid; j < lt.dp; j += PICK_THREADS) qs[j] = Qd[(int64_t)b * lt.dp + j];
+  if (tid == 0) {
+    s_total = 0;
+    s_prefix = 0;
+    s_rem = nprobe;
+  }
+  __syncthreads();
+  const float* arow = Aapp + (int64_t)b * lda;
+  const float qn = qn2[b];
+  auto valid = [&](int s) -> bool {
+    if (lt.cid[s] < 0) return false;
+    const int sc = lt.scope[s];
+    bool in = false;
+    for (int i = 0; i < nscopes; i++) in |= (s_codes[i] == sc);
+    return in;
+  };
+  auto bounds = [&](int s, uint32_t& hk, uint32_t& lk) {
+    const float A = arow[s];
+    // + abs: flushed subnormal operands / products / partial sums, each
+    // below 2^-126 (|q|_1 + |c|_1 <= sqrt(dp) (2 + |c|^2 + |q|^2)/2 ...)
+    const float nsum = __fadd_ru(cnrm[s], qn);
+    const float eps = __fadd_ru(__fmul_ru(coef, nsum), __fmul_ru(abs_coef, __fadd_ru(nsum, 2.f)));
+    float hi = __fadd_ru(A, eps), lo = __fsub_rd(A, eps);
+    if (!isfinite(hi) || !isfinite(lo)) {
+      hi = __int_as_float(0x7f800000);
+      lo = __int_as_float(0xff800000);
+    }
+    hk = f2key(hi);
+    lk = f2key(lo);
+  };
+  // 1. number of in-scope lists
+  int nv = 0;
+  for (int s = tid; s < lt.nslots; s += PICK_THREADS) nv += valid(s);
+  nv = __reduce_add_sync(FULL, nv);
+  if ((tid & 31) == 0) atomicAdd(&s_total, nv);
+  __syncthreads();
+  const int nvalid = s_total;
+  // 2. U = nprobe-th smallest upper bound (radix select, 8 bits per pass)
+  uint32_t U = KEY_NONE;
+  if (nvalid > nprobe) {
+    for (int shift = 24; shift >= 0; shift -= 8) {
+      s_hist[tid] = 0;
+      __syncthreads();
+      const uint32_t pre = s_prefix;
+      const uint32_t hmask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
+      for (int s = tid; s < lt.nslots; s += PICK_THREADS) {
+        if (!valid(s)) continue;
+        uint32_t hk, lk;
+        bounds(s, hk, lk);
+        if ((hk & hmask) == (pre & hmask)) atomicAdd(&s_hist[(hk >> shift) & 0xff], 1u);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int rem = s_rem;
+        unsigned acc = 0;
+        int bin = 0;
+        for (; bin < 256; bin++) {
+          if (acc + s_hist[bin] >= (unsigned)rem) break;
+          acc += s_hist[bin];
+        }
+        s_rem = rem - (int)acc;
+        s_prefix = pre | ((uint32_t)bin << shift);
+      }
+      __syncthreads();
+    }
+    U = s_prefix;
+  }
+  // 3. exact re-rank of every list whose lower bound is <= U, in passes
+  int kept = 0, ncand = 0;
+  const int room = PICK_CAP - nprobe;
+  int s_next = 0;
+  while (s_next < lt.nslots) {
+    if (tid == 0) s_cnt = kept;
+    __syncthreads();
+    // collect up to `room` new candidates from slots [s_next, ...)
+    int s_end = lt.nslots;
+    for (int s0 = s_next; s0 < lt.nslots; s0 += PICK_THREADS) {
+      const int s = s0 + tid;
+      bool cand = false;
+      if (s < lt.nslots && valid(s)) {
+        uint32_t hk, lk;
+        bounds(s, hk, lk);
+        cand = lk <= U;
+      }
+      const unsigned bal = __ballot_sync(FULL, cand);
+      // block-wide reservation in slot order is not needed: order is restored by the sort
+      if (cand) {
+        const int pos = atomicAdd(&s_cnt, 1);
+        if (pos < PICK_CAP) {
+          Entry e;
+          e.key = 0;  // filled below
+          e.id = lt.cid[s];
+          e.pay = s;
+          buf[pos] = e;
+        }
+      }
+      (void)bal;
+      __syncthreads();
+      if (s_cnt > PICK_CAP - PICK_THREADS) {  // next block of slots might not fit
+        s_end = s0 + PICK_THREADS;
+        break;
+      }
+    }
+    __syncthreads();
+    const int n = min(s_cnt, PICK_CAP);
+    ncand += n - kept;
+    for (int i = kept + tid; i < n; i += PICK_THREADS) {
+      const int s = buf[i].pay;
+      buf[i].key = f2key(exact_dist_row<METRIC>(qs, lt.cent + (int64_t)s * lt.dp, lt.d));
+    }
+    __syncthreads();
+    cta_bitonic_sort(buf, n);
+    kept = cta_compact_sorted(buf, n, nprobe, false, &s_cnt);
+    s_next = s_end;
+    __syncthreads();
+  }
+  (void)room;
+  for (int p = tid; p < nprobe; p += PICK_THREADS) {
+    probe[(int64_t)b * nprobe + p] = p < kept ? buf[p].pay : -1;
+    if (probe_key) probe_key[(int64_t)b * nprobe + p] = p < kept ? buf[p].key : KEY_NONE;
+  }
+  if (tid == 0 && ncand_out) ncand_out[b] = ncand;
+}
+
+size_t coarse_pick_smem_bytes(int dp) { return PICK_CAP * sizeof(Entry) + (size_t)dp * 4; }
+
+void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, int B, ListTable lt,
+                        const float* cnrm, const float* Qd, const float* qn2,
+                        const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
+                        uint32_t* probe_key, int32_t* ncand, cudaStream_t st) {
+  if (B <= 0) return;
+  const size_t smem = coarse_pick_smem_bytes(lt.dp);
+  const float coef = coarse_coef(metric, lt.dp, split);
+  // 2^-126 * (sqrt(dp) + 4 dp) per unit of (|c|^2 + |q|^2 + 2), doubled
+  const float abs_coef = (float)(2.0 * (std::sqrt((double)lt.dp) + 4.0 * lt.dp) * std::ldexp(1.0, -126));
+  if (metric == SQ_L2) {
+    cudaFuncSetAttribute(coarse_pick_kernel<SQ_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    coarse_pick_kernel<SQ_L2><<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes,
+                                                             nscopes, nprobe, coef, abs_coef, probe, probe_key, ncand);
+  } else {
+    cudaFuncSetAttribute(coarse_pick_kernel<IP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    coarse_pick_kernel<IP><<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes,
+                                                          nscopes, nprobe, coef, abs_coef, probe, probe_key, ncand);
+  }
 }
 
 }  // namespace pk

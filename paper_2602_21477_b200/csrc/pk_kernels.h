@@ -124,4 +124,34 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
                     uint32_t* slot_hi, int32_t* slot_n, int4* cpool, int32_t* ccount, int cap,
                     int num_sms, cudaStream_t st);
 
+// Cross-shard merge of R per-shard result blocks (layout: pk_shard_block_bytes
+// in include/pancake_b200.h) into the global top-kk per query.
+int shard_merge_cap();
+void launch_reblock(const int64_t* ids, const int64_t* cids, const int64_t* sc, const float* d,
+                    const int32_t* n, int B, int group, int kk, int64_t block_bytes, void* dst,
+                    cudaStream_t st);
+void launch_shard_merge(const void* blocks, int64_t block_bytes, int R, int B, int kk,
+                        int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
+                        int64_t* out_scanned, cudaStream_t st);
+
+// Coarse quantizer on tcgen05: screened distances A[b][slot] for every slot
+// (TF32 UMMA, cmap over the centroid table, qmap over the padded batch).
+struct CoarseMaps {
+  CUtensorMap c[2];  // centroid table: [0] fp32 or TF32 hi part, [1] lo part (split)
+  CUtensorMap q[2];  // padded batch, same split
+};
+size_t coarse_tc_smem_bytes(bool split);
+void launch_coarse_tc(int metric, bool split, const CoarseMaps& maps, int nslots, int B, int dp,
+                      const float* cnrm, const float* qn2, float* Aout, int64_t lda, cudaStream_t st);
+// hi/lo TF32 split of rows [0, n) of an [n][dp] table.
+void launch_tf32_split(const float* x, int64_t n, int dp, float* hi, float* lo, cudaStream_t st);
+float coarse_coef(int metric, int dp, bool split);
+// Per query: exact top-nprobe in-scope lists by (dist, cid) from the screened
+// distances (bound + exact re-rank of the boundary).  ncand: re-ranked lists
+// per query (may be NULL).
+void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, int B, ListTable lt,
+                        const float* cnrm, const float* Qd, const float* qn2,
+                        const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
+                        uint32_t* probe_key, int32_t* ncand, cudaStream_t st);
+
 }  // namespace pk

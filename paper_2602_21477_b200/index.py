@@ -15,6 +15,16 @@ import numpy as np
 from . import _native as N
 
 
+def _is_device_tensor(a) -> bool:
+    return hasattr(a, "is_cuda") and a.is_cuda
+
+
+def block_bytes(B: int, kk: int) -> int:
+    from .sharded import block_offsets
+
+    return block_offsets(B, kk)["total"]
+
+
 class SearchOutput:
     """Batched search result arrays (host)."""
 
@@ -65,6 +75,8 @@ class DeviceIndex:
 
     # ---- posting lists -------------------------------------------------
     def create_list(self, cid: int, scope_code: int, rows, ids) -> np.ndarray:
+        if _is_device_tensor(rows):
+            return self.create_list_device(cid, scope_code, rows, ids)
         rows = N.f32(rows, self.dimension)
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         cent = np.empty(self.dimension, dtype=np.float32)
@@ -95,6 +107,12 @@ class DeviceIndex:
         """Candidate-pool size per query of the last screened search."""
         out = np.empty(B, dtype=np.int32)
         N.check(N.lib().pk_debug_pool_counts(self._h, N.ptr(out), B))
+        return out
+
+    def coarse_counts(self, B: int) -> np.ndarray:
+        """Lists re-ranked exactly per query by the last tensor-core coarse pass."""
+        out = np.empty(B, dtype=np.int32)
+        N.check(N.lib().pk_debug_coarse_counts(self._h, N.ptr(out), B))
         return out
 
     def append(self, cid: int, rows, ids):
@@ -155,6 +173,104 @@ class DeviceIndex:
                                   scope_codes.shape[0], int(nprobe), int(kk), N.ptr(out_ids),
                                   N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), None,
                                   N.ptr(out_scanned), N.PK_DEVICE_PTRS))
+
+    # ---- sharded search ---------------------------
+    def add_remote_list(self, cid: int, scope_code: int, centroid):
+        """A list owned by another rank: centroid only (joins the coarse
+        quantizer, holds no rows here)."""
+        c = N.f32(centroid).reshape(-1)
+        if c.shape[0] != self.dimension:
+            raise N.UsageError("centroid dimension mismatch")
+        N.check(N.lib().pk_list_add_remote(self._h, int(cid), int(scope_code), N.ptr(c)))
+
+    def search_block(self, Q, scope_codes, nprobe: int, kk: int) -> np.ndarray:
+        """Local search written as one shard result block (host uint8)."""
+        from .sharded import block_views
+
+        Q = N.f32(Q, self.dimension)
+        B = Q.shape[0]
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        blk = np.zeros(block_bytes(B, kk), dtype=np.uint8)
+        ids, cids, scanned, dd, cnt = block_views(blk, B, kk)
+        N.check(N.lib().pk_search(self._h, N.ptr(Q), B, N.ptr(codes), len(codes), int(nprobe),
+                                  int(kk), N.ptr(ids), N.ptr(dd), N.ptr(cids), N.ptr(cnt), None,
+                                  N.ptr(scanned), 0))
+        return blk
+
+    def search_block_device(self, Q, scope_codes, nprobe: int, kk: int, block):
+        """Device variant: Q [B, d] f32 and block (uint8, block_bytes(B, kk))
+        are tensors on this device; async on the index stream."""
+        from .sharded import block_offsets
+
+        B = int(Q.shape[0])
+        o = block_offsets(B, kk)
+        base = block.data_ptr()
+        N.check(N.lib().pk_search(self._h, N.ptr(Q), B, N.ptr(scope_codes), int(scope_codes.shape[0]),
+                                  int(nprobe), int(kk), base + o["ids"], base + o["dists"],
+                                  base + o["cids"], base + o["n"], None, base + o["scanned"],
+                                  N.PK_DEVICE_PTRS))
+
+    def centroid_of(self, rows) -> np.ndarray:
+        """Cluster.recompute_stats centroid of host rows (the arithmetic
+        create_list applies on the device)."""
+        if _is_device_tensor(rows):
+            out = np.empty(self.dimension, dtype=np.float32)
+            dev_out = rows.new_empty(self.dimension)
+            N.check(N.lib().pk_centroid(N.ptr(rows), int(rows.shape[0]), self.dimension,
+                                        N.ptr(dev_out), N.PK_DEVICE_PTRS))
+            out[:] = dev_out.cpu().numpy()
+            return out
+        from .kernels import centroid
+
+        return centroid(N.f32(rows, self.dimension))
+
+    def search_coarse(self, Q, scope_codes, nprobe: int) -> np.ndarray:
+        """Coarse stage only: list handles int32[B, nprobe] (-1 padded)."""
+        Q = N.f32(Q, self.dimension)
+        B = Q.shape[0]
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        out = np.empty((B, nprobe), dtype=np.int32)
+        N.check(N.lib().pk_search_coarse(self._h, N.ptr(Q), B, N.ptr(codes), len(codes),
+                                         int(nprobe), N.ptr(out), 0))
+        return out
+
+    def search_probed(self, Q, probe, kk: int, group: int) -> np.ndarray:
+        """Scan stage only for given handles; B / group shard blocks (host)."""
+        Q = N.f32(Q, self.dimension)
+        probe = np.ascontiguousarray(probe, dtype=np.int32)
+        B, nprobe = probe.shape
+        out = np.empty((B // group) * block_bytes(group, kk), dtype=np.uint8)
+        N.check(N.lib().pk_search_probed(self._h, N.ptr(Q), B, N.ptr(probe), nprobe, int(kk),
+                                         int(group), N.ptr(out), 0))
+        return out
+
+    def search_coarse_device(self, Q, scope_codes, nprobe: int, out_probe):
+        N.check(N.lib().pk_search_coarse(self._h, N.ptr(Q), int(Q.shape[0]), N.ptr(scope_codes),
+                                         int(scope_codes.shape[0]), int(nprobe), N.ptr(out_probe),
+                                         N.PK_DEVICE_PTRS))
+
+    def search_probed_device(self, Q, probe, kk: int, group: int, out_blocks):
+        N.check(N.lib().pk_search_probed(self._h, N.ptr(Q), int(Q.shape[0]), N.ptr(probe),
+                                         int(probe.shape[1]), int(kk), int(group),
+                                         N.ptr(out_blocks), N.PK_DEVICE_PTRS))
+
+    def merge_shards(self, blocks, R: int, B: int, kk: int):
+        """Host: blocks uint8[R * block_bytes] -> (ids, dists, cids, counts, scanned)."""
+        blocks = np.ascontiguousarray(blocks, dtype=np.uint8)
+        ids = np.empty((B, kk), dtype=np.int64)
+        dd = np.empty((B, kk), dtype=np.float32)
+        cids = np.empty((B, kk), dtype=np.int64)
+        cnt = np.empty(B, dtype=np.int32)
+        sc = np.empty(B, dtype=np.int64)
+        N.check(N.lib().pk_merge_shards(self._h, N.ptr(blocks), int(R), int(B), int(kk), N.ptr(ids),
+                                        N.ptr(dd), N.ptr(cids), N.ptr(cnt), N.ptr(sc), 0))
+        return ids, dd, cids, cnt, sc
+
+    def merge_shards_device(self, blocks, R: int, B: int, kk: int, out_ids, out_d, out_cid, out_n,
+                            out_scanned=None):
+        N.check(N.lib().pk_merge_shards(self._h, N.ptr(blocks), int(R), int(B), int(kk),
+                                        N.ptr(out_ids), N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n),
+                                        N.ptr(out_scanned), N.PK_DEVICE_PTRS))
 
     def assign(self, X, scope_code: int):
         X = N.f32(X, self.dimension)

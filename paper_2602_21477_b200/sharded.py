@@ -1,0 +1,249 @@
+"""List-sharded IVF over the GPUs of one box.
+
+The reference is single-process (ref/engine.py:141-209 builds one
+``ClusterStore``); the drop-in keeps that API on one GPU and adds this layer
+for configs[3] (10M x 768 over 2/4/8 B200).  Posting lists are independent
+units, so the path shards without a data-path collective except ONE exchange:
+
+1. placement: lists go to ranks by size-balanced greedy packing
+   (:func:`place_lists`, deterministic -- every rank computes the same map);
+2. the centroid table is replicated: each owner computes its lists' centroids
+   on its device (``Cluster.recompute_stats`` arithmetic, ref/clusters.py:111-118)
+   and the table is all-gathered, so every rank evaluates the identical coarse
+   quantizer (ref/graph.py:321-396 at exhaustive ef) and the identical probe set;
+3. each rank scans only the probed lists it owns and writes its per-query
+   top-kk as one *shard result block* (layout: ``pk_shard_block_bytes`` in
+   include/pancake_b200.h);
+4. the blocks are all-gathered (NCCL over NVLink on GPUs, gloo in the CPU tests)
+   and merged by (distance, id) with first occurrence per id
+   (ref/engine.py:406-426) -- the k smallest of a union lie in the union of the
+   parts' k smallest, so the merge reproduces the single-index answer exactly.
+
+``scanned_vectors`` is the sum over shards of the rows each scanned, which is
+the single-index count (every probed list is scanned by exactly its owner).
+"""
+
+from __future__ import annotations
+
+from collections.abc import Callable, Sequence
+
+import numpy as np
+
+from .core import UsageError
+from .index import DeviceIndex, SearchOutput
+
+
+# ---------------------------------------------------------------- block layout
+def block_offsets(B: int, kk: int) -> dict:
+    """Byte offsets of one shard result block (mirrors pk_shard_block_bytes)."""
+    nkk = int(B) * int(kk)
+    o = {"ids": 0, "cids": 8 * nkk, "scanned": 16 * nkk, "dists": 16 * nkk + 8 * B,
+         "n": 20 * nkk + 8 * B}
+    o["total"] = (20 * nkk + 12 * B + 15) // 16 * 16
+    return o
+
+
+def block_views(blk: np.ndarray, B: int, kk: int):
+    """(ids i64[B,kk], cids i64[B,kk], scanned i64[B], dists f32[B,kk], n i32[B])
+    views into a host block."""
+    o = block_offsets(B, kk)
+    nkk = B * kk
+
+    def v(key, dt, count, shape):
+        return blk[o[key]:o[key] + count * np.dtype(dt).itemsize].view(dt).reshape(shape)
+
+    return (v("ids", np.int64, nkk, (B, kk)), v("cids", np.int64, nkk, (B, kk)),
+            v("scanned", np.int64, B, (B,)), v("dists", np.float32, nkk, (B, kk)),
+            v("n", np.int32, B, (B,)))
+
+
+# ---------------------------------------------------------------- placement
+def place_lists(sizes: Sequence[int], world: int) -> np.ndarray:
+    """Size-balanced greedy packing: lists in descending size (ties: lower
+    index first) each go to the least-loaded rank (ties: lower rank).
+    Deterministic, so every rank derives the same owner map."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    if world < 1:
+        raise UsageError("world size must be >= 1")
+    owner = np.zeros(len(sizes), dtype=np.int64)
+    if world == 1 or len(sizes) == 0:
+        return owner
+    load = np.zeros(world, dtype=np.int64)
+    order = np.lexsort((np.arange(len(sizes)), -sizes))
+    for i in order:
+        r = int(np.argmin(load))  # first minimum -> lowest rank on ties
+        owner[i] = r
+        load[r] += max(int(sizes[i]), 1)
+    return owner
+
+
+# ---------------------------------------------------------------- the shard
+class ShardedIndex:
+    """One rank's shard of a list-partitioned IVF.
+
+    ``group`` is a ``torch.distributed`` process group (None = the default
+    group when initialised, else a single process).  ``local`` is the per-rank
+    index -- a :class:`DeviceIndex` on ``device`` by default (the product
+    path); the CPU tests pass an oracle-backed stand-in with the same methods
+    to exercise placement, replication and exchange under gloo.
+    """
+
+    def __init__(self, dimension: int, metric_code: int = 0, device: int = 0, group=None,
+                 local=None, reserve_rows: int = 0, reserve_lists: int = 0):
+        import torch
+        import torch.distributed as dist
+
+        self.dimension = int(dimension)
+        self.dist = dist if dist.is_available() and dist.is_initialized() else None
+        self.group = group
+        if self.dist is not None:
+            self.rank = self.dist.get_rank(group)
+            self.world = self.dist.get_world_size(group)
+            backend = self.dist.get_backend(group)
+        else:
+            self.rank, self.world, backend = 0, 1, None
+        self.comm_device = (torch.device("cuda", device) if backend == "nccl"
+                            else torch.device("cpu"))
+        self.local = local if local is not None else DeviceIndex(
+            dimension, metric_code, device, reserve_rows=reserve_rows, reserve_lists=reserve_lists)
+        self.owner: dict[int, int] = {}
+
+    # ---- exchange -------------------------------------------------------
+    def _all_gather(self, t):
+        """All-gather equal-shaped tensors (rank order) -> [world, *t.shape]."""
+        import torch
+
+        if self.world == 1:
+            return t.unsqueeze(0)
+        t = t.to(self.comm_device).contiguous()
+        flat = t.reshape(-1)
+        out = torch.empty(self.world * flat.numel(), dtype=t.dtype, device=self.comm_device)
+        self.dist.all_gather_into_tensor(out, flat, group=self.group)
+        return out.view(self.world, *t.shape)
+
+    # ---- build ----------------------------------------------------------
+    def load(self, cids: Sequence[int], scopes: Sequence[int], sizes: Sequence[int],
+             fetch: Callable[[int], tuple], owners: Sequence[int] | None = None) -> np.ndarray:
+        """Place the global lists (``cids[i]`` in scope ``scopes[i]`` with
+        ``sizes[i]`` rows); ``fetch(i) -> (rows f32[n,d], ids i64[n])`` is
+        called only for the lists this rank owns.  Returns the owner map
+        (``owners`` overrides place_lists, e.g. data already partitioned).
+
+        Owners compute their lists' centroids, the table is all-gathered, and
+        every rank then registers the lists in GLOBAL order (own lists with
+        rows, the others centroid-only), so list handles -- the slot indices
+        the dispatch path exchanges -- agree on every rank."""
+        import torch
+
+        cids = np.asarray(cids, dtype=np.int64)
+        scopes = np.asarray(scopes, dtype=np.int64)
+        owners = (place_lists(sizes, self.world) if owners is None
+                  else np.asarray(owners, dtype=np.int64))
+        mine = np.nonzero(owners == self.rank)[0]
+        d = self.dimension
+        data = {}
+        cent_mine = np.zeros((len(mine), d), dtype=np.float32)
+        for j, i in enumerate(mine):
+            rows, ids = fetch(int(i))
+            data[int(i)] = (rows, ids)
+            cent_mine[j] = self.local.centroid_of(rows)
+        # rank r's lists are exactly owners == r in index order: only the
+        # padded centroid rows travel
+        counts = np.bincount(owners, minlength=self.world)
+        cmax = int(counts.max()) if len(counts) else 0
+        pad = np.zeros((max(cmax, 1), d), dtype=np.float32)
+        pad[:len(mine)] = cent_mine
+        allc = self._all_gather(torch.from_numpy(pad)).cpu().numpy()
+        pos = np.zeros(len(cids), dtype=np.int64)
+        for r in range(self.world):
+            w = np.nonzero(owners == r)[0]
+            pos[w] = np.arange(len(w))
+        for i in range(len(cids)):
+            if owners[i] == self.rank:
+                rows, ids = data.pop(int(i))
+                self.local.create_list(int(cids[i]), int(scopes[i]), rows, ids)
+            else:
+                self.local.add_remote_list(int(cids[i]), int(scopes[i]), allc[owners[i], pos[i]])
+        self.owner = {int(c): int(o) for c, o in zip(cids, owners)}
+        return owners
+
+    # ---- search ---------------------------------------------------------
+    def search(self, Q, scope_codes, nprobe: int, kk: int) -> SearchOutput:
+        """Host path: local scan -> all-gather of the shard blocks -> merge."""
+        import torch
+
+        Q = np.ascontiguousarray(Q, dtype=np.float32).reshape(-1, self.dimension)
+        B = Q.shape[0]
+        blk = self.local.search_block(Q, scope_codes, nprobe, kk)
+        if self.world == 1:
+            blocks = blk
+        else:
+            blocks = self._all_gather(torch.from_numpy(blk)).cpu().numpy().reshape(-1)
+        ids, dd, cids, cnt, sc = self.local.merge_shards(blocks, self.world, B, kk)
+        return SearchOutput(ids, dd, cids, cnt, None, sc)
+
+    def search_device(self, Q, scope_codes, nprobe: int, kk: int, block, gathered, out_ids,
+                      out_d, out_cid, out_n, out_scanned=None):
+        """Device path (tensors on this rank's GPU, ordered on the index
+        stream): local scan into ``block``, NCCL all-gather into ``gathered``
+        ([world * block_bytes] uint8), device merge into the outputs.  The
+        caller runs it under ``torch.cuda.stream(index stream)`` so the
+        collective is ordered after the scan."""
+        B = int(Q.shape[0])
+        self.local.search_block_device(Q, scope_codes, nprobe, kk, block)
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(gathered, block, group=self.group)
+            src = gathered
+        else:
+            src = block
+        self.local.merge_shards_device(src, self.world, B, kk, out_ids, out_d, out_cid, out_n,
+                                       out_scanned)
+
+    # ---- dispatch / combine: every rank brings its own batch --------------
+    def search_dispatch(self, Q, scope_codes, nprobe: int, kk: int) -> SearchOutput:
+        """Host path of the dispatch/combine step (weak scaling: each rank
+        serves its own B queries against the whole sharded index).
+
+        1. coarse stage on the rank's own queries (replicated centroids);
+        2. all-gather of the queries and their list handles (dispatch);
+        3. every rank scans its own lists for all world*B queries, one shard
+           result block per origin rank;
+        4. all-to-all returns each origin its blocks (combine), merged by
+           (distance, id) into the rank's answers."""
+        import torch
+
+        Q = np.ascontiguousarray(Q, dtype=np.float32).reshape(-1, self.dimension)
+        B = Q.shape[0]
+        probe = self.local.search_coarse(Q, scope_codes, nprobe)
+        if self.world == 1:
+            blocks = self.local.search_probed(Q, probe, kk, B)
+        else:
+            Qa = self._all_gather(torch.from_numpy(Q)).cpu().numpy().reshape(-1, self.dimension)
+            Pa = self._all_gather(torch.from_numpy(probe)).cpu().numpy().reshape(-1, nprobe)
+            send = torch.from_numpy(self.local.search_probed(Qa, Pa, kk, B)).to(self.comm_device)
+            recv = torch.empty_like(send)
+            self.dist.all_to_all_single(recv, send, group=self.group)
+            blocks = recv.cpu().numpy()
+        ids, dd, cids, cnt, sc = self.local.merge_shards(blocks, self.world, B, kk)
+        return SearchOutput(ids, dd, cids, cnt, None, sc)
+
+    def search_dispatch_device(self, Q, scope_codes, nprobe: int, kk: int, bufs: dict,
+                               out_ids, out_d, out_cid, out_n, out_scanned=None):
+        """Device path of search_dispatch (tensors on this rank's GPU; run
+        under ``torch.cuda.stream(index stream)``).  ``bufs`` holds the
+        preallocated exchange buffers: probe [B, nprobe] i32, q_all
+        [world*B, d] f32, probe_all [world*B, nprobe] i32, send / recv
+        [world * block_bytes(B, kk)] u8."""
+        B = int(Q.shape[0])
+        self.local.search_coarse_device(Q, scope_codes, nprobe, bufs["probe"])
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(bufs["q_all"], Q, group=self.group)
+            self.dist.all_gather_into_tensor(bufs["probe_all"], bufs["probe"], group=self.group)
+            self.local.search_probed_device(bufs["q_all"], bufs["probe_all"], kk, B, bufs["send"])
+            self.dist.all_to_all_single(bufs["recv"], bufs["send"], group=self.group)
+            src = bufs["recv"]
+        else:
+            self.local.search_probed_device(Q, bufs["probe"], kk, B, bufs["send"])
+            src = bufs["send"]
+        self.local.merge_shards_device(src, self.world, B, kk, out_ids, out_d, out_cid, out_n,
+                                       out_scanned)

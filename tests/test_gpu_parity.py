@@ -294,3 +294,43 @@ def test_screen_adversarial(pk, kind, scan_mode):
             assert np.array_equal(out.ids, ids), (kind, metric, nprobe)
             assert np.array_equal(bits(out.dists), bits(dd))
         ix.close()
+
+
+@pytest.mark.parametrize("coarse", ["tc", "tf32", "exact"])
+@pytest.mark.parametrize("kind", ["random", "dup_centroids", "shell", "many"])
+def test_coarse_quantizer_matches_oracle(pk, kind, coarse, monkeypatch):
+    """The coarse top-nprobe (ref/graph.py:392-396 at exhaustive ef): tcgen05
+    TF32 screen + exact re-rank (default) and the all-exact path
+    (PK_COARSE=exact) against the oracle, including exact centroid ties
+    (order by cid), near-ties on a shell, slot counts that are not multiples
+    of the 128-slot tile, and nprobe up to the device maximum."""
+    from paper_2602_21477_b200 import DeviceIndex
+
+    monkeypatch.setenv("PK_COARSE", coarse)
+    rng = np.random.default_rng({"random": 1, "dup_centroids": 2, "shell": 3, "many": 4}[kind])
+    d = 96 if kind != "many" else 40
+    nlist = {"random": 300, "dup_centroids": 257, "shell": 200, "many": 2500}[kind]
+    Q = rng.normal(size=(130, d)).astype(np.float32)
+    ix = DeviceIndex(d, 0, 0)
+    lists, cents = [], []
+    for c in range(nlist):
+        if kind == "dup_centroids":
+            centre = np.full(d, float(c % 5), np.float32)  # 5 distinct centroids, many ties
+            rows = np.stack([centre + 0.25, centre - 0.25]).astype(np.float32)
+        elif kind == "shell":
+            u = rng.normal(size=d)
+            u /= np.linalg.norm(u)
+            rows = (Q[0] + 2.0 * u)[None].astype(np.float32)
+        else:
+            rows = rng.normal(size=(int(rng.integers(1, 6)), d)).astype(np.float32)
+        ids = np.arange(c * 10, c * 10 + len(rows), dtype=np.int64)
+        cents.append(ix.create_list(nlist - c, 0, rows, ids))  # cids descending vs slot order
+        lists.append((ids, rows))
+    flat = O.FlatIVF.from_lists(lists, np.stack(cents), np.arange(nlist, 0, -1))
+    for nprobe in (1, 7, 64, min(nlist, 2048)):
+        out = ix.search(Q, [0], nprobe, 10, want_probe=True)
+        ids, dd, cnt, probe, scanned = flat.search(Q, nprobe, 10, threads=8)
+        assert np.array_equal(out.probe, probe), (kind, nprobe)
+        assert np.array_equal(out.ids, ids)
+        assert np.array_equal(bits(out.dists), bits(dd))
+    ix.close()

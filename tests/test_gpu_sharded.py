@@ -1,0 +1,145 @@
+"""Sharded search on the device, with R shards simulated
+as R device indexes on one GPU: each owns the lists place_lists gives it and
+holds the others as remote (centroid-only) lists; the R shard blocks are
+merged by pk_merge_shards.  The merged answer must equal the single-index
+device answer and the oracle bit for bit (ids, distance bits, hit cids,
+scanned counts)."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from shard_oracle import merge_reference
+from paper_2602_21477_b200.sharded import block_views, place_lists
+
+pytestmark = pytest.mark.gpu
+
+
+def _lists(seed, nlist, d, maxn):
+    rng = np.random.default_rng(seed)
+    cents = rng.normal(size=(nlist, d)).astype(np.float32)
+    out, nid = [], 0
+    for c in range(nlist):
+        n = int(rng.integers(1, maxn))
+        rows = (cents[c] + 0.5 * rng.normal(size=(n, d))).astype(np.float32)
+        ids = rng.permutation(np.arange(nid, nid + n)).astype(np.int64)
+        nid += n
+        out.append((ids, rows))
+    Q = (cents[rng.integers(0, nlist, 70)] + 0.5 * rng.normal(size=(70, d))).astype(np.float32)
+    return out, Q
+
+
+@pytest.mark.parametrize("R,d,nlist,nprobe,kk", [(2, 96, 40, 7, 10), (4, 384, 64, 16, 10),
+                                                  (8, 128, 50, 50, 64), (3, 33, 30, 5, 1)])
+def test_device_shards_merge_equals_single_index(R, d, nlist, nprobe, kk):
+    from paper_2602_21477_b200 import DeviceIndex
+
+    lists, Q = _lists(R * 100 + d, nlist, d, 700)
+    cids = np.arange(1000, 1000 + nlist, dtype=np.int64)
+    owners = place_lists([len(i) for i, _ in lists], R)
+    single = DeviceIndex(d)
+    cents = [single.create_list(int(c), 0, r, i) for c, (i, r) in zip(cids, lists)]
+    shards = [DeviceIndex(d) for _ in range(R)]
+    for j, (c, (i, r)) in enumerate(zip(cids, lists)):
+        for s in range(R):
+            if owners[j] == s:
+                got = shards[s].create_list(int(c), 0, r, i)
+                assert np.array_equal(got.view(np.uint32), cents[j].view(np.uint32))
+            else:
+                shards[s].add_remote_list(int(c), 0, cents[j])
+    blocks = [sh.search_block(Q, [0], nprobe, kk) for sh in shards]
+    B = len(Q)
+    ids, dd, hc, cnt, sc = shards[0].merge_shards(np.concatenate(blocks), R, B, kk)
+    ref = single.search(Q, [0], nprobe, kk)
+    assert np.array_equal(ids, ref.ids)
+    assert np.array_equal(dd.view(np.uint32), ref.dists.view(np.uint32))
+    assert np.array_equal(hc, ref.cids)
+    assert np.array_equal(cnt, ref.counts)
+    assert np.array_equal(sc, ref.scanned)
+    # the device merge equals the numpy restatement of _topk's merge
+    parts = [block_views(b, B, kk) for b in blocks]
+    r_ids, r_d, r_c, r_n, r_sc = merge_reference(parts, B, kk)
+    assert np.array_equal(ids, r_ids) and np.array_equal(cnt, r_n) and np.array_equal(sc, r_sc)
+    assert np.array_equal(hc, r_c)
+    # and the oracle over the whole index
+    flat = O.FlatIVF.from_lists(lists, np.stack(cents), cids)
+    o_ids, o_d, o_n, _, o_sc = flat.search(Q, nprobe, kk)
+    assert np.array_equal(ids, o_ids)
+    assert np.array_equal(dd.view(np.uint32), o_d.view(np.uint32))
+    assert np.array_equal(sc, o_sc)
+    for ix in shards + [single]:
+        ix.close()
+
+
+def test_remote_list_rejects_append():
+    from paper_2602_21477_b200 import DeviceIndex, UsageError
+
+    ix = DeviceIndex(16)
+    ix.add_remote_list(5, 0, np.ones(16, np.float32))
+    with pytest.raises(UsageError):
+        ix.append(5, np.ones((1, 16), np.float32), [1])
+    assert ix.size(5) == 0
+    ix.retire(5)
+    ix.close()
+
+
+def test_sharded_index_single_process_device_path():
+    """ShardedIndex with world 1 (no process group): the product wrapper."""
+    from paper_2602_21477_b200.sharded import ShardedIndex
+
+    d, nlist = 64, 20
+    lists, Q = _lists(9, nlist, d, 300)
+    cids = list(range(nlist))
+    sh = ShardedIndex(d)
+    sh.load(cids, [0] * nlist, [len(i) for i, _ in lists], lambda i: lists[i][::-1])
+    out = sh.search(Q, [0], 6, 10)
+    cents = np.stack([O.centroid(r) for _, r in lists])
+    flat = O.FlatIVF.from_lists(lists, cents, np.array(cids, np.int64))
+    o_ids, o_d, o_n, _, o_sc = flat.search(Q, 6, 10)
+    assert np.array_equal(out.ids, o_ids)
+    assert np.array_equal(out.dists.view(np.uint32), o_d.view(np.uint32))
+    assert np.array_equal(out.scanned, o_sc)
+
+
+@pytest.mark.parametrize("R", [2, 3])
+def test_device_dispatch_combine_equals_single_index(R):
+    """Dispatch/combine (every rank brings its own batch): coarse on each
+    rank's own queries, scan of the concatenated batch on every shard into
+    per-origin blocks, 'all-to-all' (block r of every shard to rank r) and
+    the device merge.  Shards built in global order share list handles."""
+    from paper_2602_21477_b200 import DeviceIndex
+    from paper_2602_21477_b200.sharded import block_offsets
+
+    d, nlist, nprobe, kk = 128, 45, 9, 10
+    lists, Q = _lists(77 + R, nlist, d, 600)
+    Q = Q[:R * 20]
+    B = 20
+    cids = np.arange(500, 500 + nlist, dtype=np.int64)
+    owners = place_lists([len(i) for i, _ in lists], R)
+    single = DeviceIndex(d)
+    cents = [single.create_list(int(c), 0, r, i) for c, (i, r) in zip(cids, lists)]
+    shards = [DeviceIndex(d) for _ in range(R)]
+    for j, (c, (i, r)) in enumerate(zip(cids, lists)):  # global order on every shard
+        for s in range(R):
+            if owners[j] == s:
+                shards[s].create_list(int(c), 0, r, i)
+            else:
+                shards[s].add_remote_list(int(c), 0, cents[j])
+    probes = [shards[r].search_coarse(Q[r * B:(r + 1) * B], [0], nprobe) for r in range(R)]
+    for r in range(1, R):  # handles agree across shards
+        assert np.array_equal(shards[0].search_coarse(Q[r * B:(r + 1) * B], [0], nprobe), probes[r])
+    P = np.concatenate(probes)
+    sent = [sh.search_probed(Q, P, kk, B) for sh in shards]
+    bb = block_offsets(B, kk)["total"]
+    ref = single.search(Q, [0], nprobe, kk)
+    for r in range(R):
+        recv = np.concatenate([sent[s][r * bb:(r + 1) * bb] for s in range(R)])
+        ids, dd, hc, cnt, sc = shards[r].merge_shards(recv, R, B, kk)
+        sl = slice(r * B, (r + 1) * B)
+        assert np.array_equal(ids, ref.ids[sl])
+        assert np.array_equal(dd.view(np.uint32), ref.dists[sl].view(np.uint32))
+        assert np.array_equal(hc, ref.cids[sl])
+        assert np.array_equal(cnt, ref.counts[sl])
+        assert np.array_equal(sc, ref.scanned[sl])
+    for ix in shards + [single]:
+        ix.close()
