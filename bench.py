@@ -415,6 +415,8 @@ def run_ours(a):
         if sh is None:
             cc = ix.coarse_counts(a.batch)
             pool["coarse_lists_reranked"] = {"mean": float(cc.mean()), "max": int(cc.max())}
+        rc = ix.rerank_counts(B_last)
+        pool["rows_reranked_exactly"] = {"mean": float(rc.mean()), "max": int(rc.max())}
     except Exception:
         pass
     scan_ms = stage_ms["scan"] / max(ncalls, 1)

@@ -166,6 +166,9 @@ int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B);
 /* Lists re-ranked exactly per query by the last search's tensor-core coarse
  * quantizer (host int32[B]). */
 int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B);
+/* Pool entries that survived the final bound and were re-ranked exactly per
+ * query by the last screened search (host int32[B]; -1 = overflow path). */
+int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B);
 
 #ifdef __cplusplus
 }

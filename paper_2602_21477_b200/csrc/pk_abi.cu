@@ -135,7 +135,7 @@ struct pk_index {
   int32_t dirty_lo = INT32_MAX, dirty_hi = -1;
 
   // search scratch
-  DevBuf q, qnorm, dc, probe, probe_key, counts, fillb, items, nitems, qpairs, slot_off, scanned,
+  DevBuf q, qnorm, dc, probe, probe_key, counts, items, qpairs, slot_off, scanned,
       cand_key, cand_id, cand_n, cand_list, work, out_ids, out_d, out_cid, out_n, scopes, assign_c,
       assign_d;
   int chunk_rows = 512;
@@ -147,7 +147,7 @@ struct pk_index {
   DevBuf ncand;
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
-  DevBuf shard_in, shard_out, pb, pb_out;
+  DevBuf shard_in, shard_out, pb, pb_out, nsurv;
 
   // stage timing (pk_profile_begin / pk_profile_end): events around each
   // stage of every pk_search while enabled.
@@ -529,10 +529,10 @@ int pk_index_destroy(pk_index* ix) {
   cudaFree(ix->d_clo);
   for (cudaEvent_t e : ix->prof_ev) cudaEventDestroy(e);
   for (DevBuf* b : {&ix->q, &ix->qnorm, &ix->dc, &ix->probe, &ix->probe_key, &ix->counts,
-                    &ix->fillb, &ix->items, &ix->nitems, &ix->qpairs, &ix->slot_off, &ix->scanned,
-                    &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list, &ix->work,
+                    &ix->items, &ix->qpairs, &ix->slot_off, &ix->scanned,
+                    &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list,
                     &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->ncand, &ix->qhi, &ix->qlo})
+                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->nsurv, &ix->ncand, &ix->qhi, &ix->qlo})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -811,22 +811,22 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   RET(ix->probe.ensure((size_t)B * nprobe * 4));
   RET(ix->probe_key.ensure((size_t)B * nprobe * 4));
   RET(ix->counts.ensure((size_t)ns * 4));
-  RET(ix->fillb.ensure((size_t)(2 * ns + B * nprobe) * 4));
   int64_t maxlen = 0;
   for (int32_t s = 0; s < ix->nslots; s++)
     if (ix->h_cid[s] >= 0) maxlen = std::max(maxlen, ix->h_len[s]);
   const int64_t max_nch = std::max<int64_t>(1, (maxlen + ix->chunk_rows - 1) / ix->chunk_rows);
   const int64_t max_items = B * nprobe * max_nch;
   RET(ix->items.ensure((size_t)max_items * sizeof(ScanItem)));
-  RET(ix->nitems.ensure(8));
-  RET(ix->qpairs.ensure((size_t)B * nprobe * sizeof(QPair)));
-  RET(ix->slot_off.ensure((size_t)(B + 1) * 4));
+  const int64_t smax = nprobe * max_nch;  // output slots per query
+  // per-list query buckets (B entries each) + lcount [ns] | n_items | work counter
+  RET(ix->qpairs.ensure((size_t)ns * B * sizeof(QPair)));
+  RET(ix->counts.ensure((size_t)(ns + 2) * 4));
+  RET(ix->slot_off.ensure((size_t)2 * B * 4));
   RET(ix->scanned.ensure((size_t)B * 8));
   RET(ix->cand_key.ensure((size_t)max_items * kk * 4));
   RET(ix->cand_id.ensure((size_t)max_items * kk * 8));
   RET(ix->cand_n.ensure((size_t)max_items * 4));
   RET(ix->cand_list.ensure((size_t)max_items * 4));
-  RET(ix->work.ensure(8));
   RET(ix->scopes.ensure(64 * 4));
   const int pc = ix->prof_calls;
 #define PROF(stage) \
@@ -882,12 +882,14 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     return PK_OK;
   }
   // 2. route (query -> lists) into (list -> queries) work items
-  CK(cudaMemsetAsync(ix->counts.p, 0, (size_t)ns * 4, st));
-  launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt, ix->chunk_rows, ix->counts.as<int32_t>(),
-               ix->fillb.as<int32_t>(), ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
-               ix->qpairs.as<QPair>(), ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
+  int32_t* lcount = ix->counts.as<int32_t>();
+  int32_t* n_items = lcount + ns;
+  int32_t* work_ctr = lcount + ns + 1;
+  CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, st));
+  launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt, ix->chunk_rows, (int)smax, (int)B,
+               lcount, ix->items.as<ScanItem>(), n_items, ix->qpairs.as<QPair>(),
+               ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
   // 3. fused scan + per-(query, list chunk) top-kk
-  CK(cudaMemsetAsync(ix->work.p, 0, 8, st));
   PROF(4);
   if (ix->screen) {
     RET(ix->uq.ensure((size_t)B * 4));
@@ -898,23 +900,23 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     if (ix->tensor) {
       RET(ix->qsw.ensure((size_t)8 * B * dp * 4));
       launch_scan_tc(ix->metric, lt, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(),
-                     ix->qnorm2.as<float>(), ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
+                     ix->qnorm2.as<float>(), ix->items.as<ScanItem>(), n_items,
                      (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
-                     ix->work.as<int32_t>(), ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
+                     work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
                      ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
                      ix->pool_cap, ix->num_sms, st);
     } else {
       launch_scan_screen(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
-                         ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(),
+                         ix->items.as<ScanItem>(), n_items,
                          (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
-                         ix->work.as<int32_t>(), ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
+                         work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
                          ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
                          ix->pool_cap, ix->num_sms, st);
     }
   } else
     launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
-                ix->items.as<ScanItem>(), ix->nitems.as<int32_t>(), (int)std::min<int64_t>(max_items, INT32_MAX),
-                ix->qpairs.as<QPair>(), kk, ix->work.as<int32_t>(), ix->cand_key.as<uint32_t>(),
+                ix->items.as<ScanItem>(), n_items, (int)std::min<int64_t>(max_items, INT32_MAX),
+                ix->qpairs.as<QPair>(), kk, work_ctr, ix->cand_key.as<uint32_t>(),
                 ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
                 ix->num_sms, st);
   PROF(5);
@@ -933,11 +935,12 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     o_cid = ix->out_cid.as<int64_t>();
     o_n = ix->out_n.as<int32_t>();
   }
+  if (ix->screen) RET(ix->nsurv.ensure((size_t)B * 4));
   if (ix->screen)
     launch_rerank_merge(ix->metric, (int)B, ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
                         ix->pool_cap, ix->cand_key.as<uint32_t>(), ix->cand_n.as<int32_t>(),
                         ix->slot_off.as<int32_t>(), lt, ix->q.as<float>(), ix->probe.as<int32_t>(),
-                        nprobe, kk, o_ids, o_d, o_cid, o_n, st);
+                        nprobe, kk, o_ids, o_d, o_cid, o_n, ix->nsurv.as<int32_t>(), st);
   else
     launch_merge((int)B, ix->slot_off.as<int32_t>(), ix->cand_key.as<uint32_t>(),
                  ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(), kk,
@@ -1023,6 +1026,14 @@ int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B) {
   if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
   if ((size_t)B * 4 > ix->ccount.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
   CK(cudaMemcpyAsync(out, ix->ccount.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
+  CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B) {
+  if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
+  if ((size_t)B * 4 > ix->nsurv.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
+  CK(cudaMemcpyAsync(out, ix->nsurv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }

@@ -282,6 +282,29 @@ __device__ int cta_compact_sorted(Entry* buf, int n, int kk, bool dedup, int* s_
   return *s_cnt;
 }
 
+// Block-wide: thread t holds cnt (bin t of a 256-bin histogram); returns the
+// bin holding the rem-th smallest element and the count below it.
+__device__ __forceinline__ void pick_bin(unsigned cnt, int rem, int* s_bin, int* s_below, unsigned* s_w) {
+  // (blockDim.x == 256)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned x = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  unsigned pre = 0;
+  for (int w = 0; w < warp; w++) pre += s_w[w];
+  const unsigned incl = pre + x, excl = incl - cnt;
+  if (excl < (unsigned)rem && incl >= (unsigned)rem) {
+    *s_bin = threadIdx.x;
+    *s_below = (int)excl;
+  }
+  __syncthreads();
+}
+
 constexpr int SEL_CAP = 4096;
 
 // Coarse quantizer select: per query the first nprobe in-scope lists by
@@ -348,158 +371,117 @@ void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
 }
 
 // =====================================================================
-// Routing: invert (query -> probed lists) into (list -> queries), cut each
-// probed list into row chunks x query groups (the scan work items), and give
-// every (query, list chunk) an output slot.  Single CTA; B*nprobe is small.
+// Routing: invert (query -> probed lists) into (list -> queries) and cut each
+// probed list into row chunks x query groups (the scan work items).
+//   route_emit_kernel  one CTA per query: its output slots (one per probed
+//                      list chunk, fixed stride smax per query, so no
+//                      batch-wide scan is needed), scanned rows, and one
+//                      (query, slot base) pair appended to each probed list's
+//                      bucket (bcap entries per list).
+//   route_items_kernel one thread per list: chunks x ceil(queries / QG)
+//                      items, appended through one atomic counter.
+// Item and bucket order depend on atomic arrival; results do not (the merge
+// orders by (dist, id)).
 // =====================================================================
 __device__ __forceinline__ int nchunks_of(int64_t len, int chunk) {
   return (int)((len + chunk - 1) / chunk);
 }
 
-// Block-wide exclusive scan of v (blockDim.x == 1024); returns prefix, *total.
-__device__ int block_exscan(int v, int* s_tmp, int* total) {
+constexpr int RE_THREADS = 128;
+__global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
+    const int32_t* __restrict__ probe, int nprobe, ListTable lt, int chunk_rows, int smax, int bcap,
+    int32_t* __restrict__ lcount, QPair* __restrict__ bucket, int32_t* __restrict__ slot_off,
+    int64_t* __restrict__ scanned) {
+  __shared__ int s_w[RE_THREADS / 32];
+  __shared__ long long s_sc[RE_THREADS / 32];
+  const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s_tmp[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = s_tmp[lane];
+  int carry = 0;
+  int64_t sc = 0;
+  for (int p0 = 0; p0 < nprobe; p0 += RE_THREADS) {
+    const int p = p0 + threadIdx.x;
+    const int s = p < nprobe ? probe[(int64_t)b * nprobe + p] : -1;
+    int64_t len = 0;
+    int c = 0;
+    if (s >= 0) {
+      len = lt.len[s];
+      c = nchunks_of(len, chunk_rows);
+    }
+    sc += len;
+    // block exclusive scan of c
+    int x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(FULL, w, o);
-      if (lane >= o) w += y;
+      const int y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
     }
-    s_tmp[lane] = w;
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    int wpre = 0, tot = 0;
+    for (int w = 0; w < RE_THREADS / 32; w++) {
+      if (w < warp) wpre += s_w[w];
+      tot += s_w[w];
+    }
+    if (s >= 0) {
+      const int pos = atomicAdd(&lcount[s], 1);
+      QPair qp;
+      qp.b = b;
+      qp.slotbase = b * smax + carry + wpre + x - c;
+      bucket[(int64_t)s * bcap + pos] = qp;
+    }
+    carry += tot;
+    __syncthreads();
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sc += __shfl_xor_sync(FULL, sc, o);
+  if (lane == 0) s_sc[warp] = (long long)sc;
   __syncthreads();
-  int pre = (warp > 0 ? s_tmp[warp - 1] : 0) + x - v;
-  *total = s_tmp[31];
-  __syncthreads();
-  return pre;
+  if (threadIdx.x == 0) {
+    long long t = 0;
+    for (int w = 0; w < RE_THREADS / 32; w++) t += s_sc[w];
+    scanned[b] = t;
+    slot_off[2 * b] = b * smax;
+    slot_off[2 * b + 1] = b * smax + carry;
+  }
 }
 
-__global__ void __launch_bounds__(1024) route_kernel(const int32_t* __restrict__ probe, int B,
-                                                     int nprobe, ListTable lt, int chunk_rows,
-                                                     int32_t* __restrict__ counts,
-                                                     int32_t* __restrict__ fill,
-                                                     int32_t* __restrict__ item_off,
-                                                     int32_t* __restrict__ pair_slot,
-                                                     ScanItem* __restrict__ items,
-                                                     int32_t* __restrict__ n_items,
-                                                     QPair* __restrict__ qpairs,
-                                                     int32_t* __restrict__ slot_off,
-                                                     int64_t* __restrict__ scanned) {
-  __shared__ int s_tmp[32];
-  const int npairs = B * nprobe;
-  // 1. per-list query counts
-  for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
-    int s = probe[i];
-    if (s >= 0) atomicAdd(&counts[s], 1);
-  }
-  // 2. per-query output slots (row chunks of its probed lists) and scanned rows
-  int carry = 0;
-  for (int b0 = 0; b0 < B; b0 += blockDim.x) {
-    int b = b0 + threadIdx.x;
-    int nsl = 0;
-    int64_t sc = 0;
-    if (b < B) {
-      for (int p = 0; p < nprobe; p++) {
-        int s = probe[(int64_t)b * nprobe + p];
-        int c = 0;
-        if (s >= 0) {
-          int64_t len = lt.len[s];
-          c = nchunks_of(len, chunk_rows);
-          sc += len;
-        }
-        pair_slot[(int64_t)b * nprobe + p] = nsl;  // relative; made absolute below
-        nsl += c;
-      }
-      scanned[b] = sc;
-    }
-    int tot;
-    int pre = block_exscan(nsl, s_tmp, &tot);
-    if (b < B) slot_off[b] = carry + pre;
-    carry += tot;
-  }
-  if (threadIdx.x == 0) slot_off[B] = carry;
-  __syncthreads();
-  // 3. exclusive scans over lists: query offsets (in place in counts -> fill
-  //    keeps the running fill pointer) and item offsets
-  carry = 0;
-  int icarry = 0;
-  for (int s0 = 0; s0 < lt.nslots; s0 += blockDim.x) {
-    int s = s0 + threadIdx.x;
-    int cnt = 0, nit = 0;
-    if (s < lt.nslots) {
-      cnt = counts[s];
-      if (cnt > 0) nit = nchunks_of(lt.len[s], chunk_rows) * ((cnt + QG - 1) / QG);
-    }
-    int tot, itot;
-    int pre = block_exscan(cnt, s_tmp, &tot);
-    int ipre = block_exscan(nit, s_tmp, &itot);
-    if (s < lt.nslots) {
-      fill[s] = carry + pre;  // query offset; advanced atomically in step 4
-      item_off[s] = icarry + ipre;
-      counts[s] = carry + pre;  // keep the base
-    }
-    carry += tot;
-    icarry += itot;
-  }
-  if (threadIdx.x == 0) *n_items = icarry;
-  __syncthreads();
-  // 4. scatter (query, slot base) pairs into per-list ranges
-  for (int i = threadIdx.x; i < npairs; i += blockDim.x) {
-    int s = probe[i];
-    if (s < 0) continue;
-    int b = i / nprobe;
-    int pos = atomicAdd(&fill[s], 1);
-    QPair qp;
-    qp.b = b;
-    qp.slotbase = slot_off[b] + pair_slot[i];
-    qpairs[pos] = qp;
-  }
-  __syncthreads();
-  // 5. emit work items
-  for (int s = threadIdx.x; s < lt.nslots; s += blockDim.x) {
-    int qbase = counts[s];
-    int cnt = fill[s] - qbase;
-    if (cnt <= 0) continue;
-    int64_t len = lt.len[s];
-    int nch = nchunks_of(len, chunk_rows);
-    int ng = (cnt + QG - 1) / QG;
-    int w = item_off[s];
-    for (int c = 0; c < nch; c++) {
-      for (int g = 0; g < ng; g++) {
-        ScanItem it;
-        it.lslot = s;
-        it.row0 = c * chunk_rows;
-        it.nrows = (int)(len - (int64_t)c * chunk_rows < chunk_rows ? len - (int64_t)c * chunk_rows : chunk_rows);
-        it.qoff = qbase + g * QG;
-        it.nq = min(QG, cnt - g * QG);
-        it.chunk = c;
-        it.pad0 = it.pad1 = 0;
-        items[w++] = it;
-      }
+__global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
+                                   const int32_t* __restrict__ lcount, ScanItem* __restrict__ items,
+                                   int32_t* __restrict__ n_items) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= lt.nslots) return;
+  const int cnt = lcount[s];
+  if (cnt <= 0) return;
+  const int64_t len = lt.len[s];
+  const int nch = nchunks_of(len, chunk_rows);
+  const int ng = (cnt + QG - 1) / QG;
+  if (nch == 0) return;
+  int w = atomicAdd(n_items, nch * ng);
+  for (int c = 0; c < nch; c++) {
+    for (int g = 0; g < ng; g++) {
+      ScanItem it;
+      it.lslot = s;
+      it.row0 = c * chunk_rows;
+      it.nrows = (int)(len - (int64_t)c * chunk_rows < chunk_rows ? len - (int64_t)c * chunk_rows : chunk_rows);
+      it.qoff = s * bcap + g * QG;
+      it.nq = min(QG, cnt - g * QG);
+      it.chunk = c;
+      it.pad0 = it.pad1 = 0;
+      items[w++] = it;
     }
   }
 }
 
-void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows,
-                  int32_t* scratch_counts, int32_t* scratch_fill, ScanItem* items,
-                  int32_t* n_items, QPair* qpairs, int32_t* slot_off, int64_t* scanned,
-                  cudaStream_t st) {
-  // scratch_counts: [nslots] zeroed; scratch_fill: [2*nslots + B*nprobe]
-  int32_t* fill = scratch_fill;
-  int32_t* item_off = scratch_fill + lt.nslots;
-  int32_t* pair_slot = scratch_fill + 2 * (int64_t)lt.nslots;
-  route_kernel<<<1, 1024, 0, st>>>(probe, B, nprobe, lt, chunk_rows, scratch_counts, fill,
-                                    item_off, pair_slot, items, n_items, qpairs, slot_off,
-                                    scanned);
+void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows, int smax,
+                  int bcap, int32_t* lcount, ScanItem* items, int32_t* n_items, QPair* bucket,
+                  int32_t* slot_off, int64_t* scanned, cudaStream_t st) {
+  // lcount [nslots] and *n_items zeroed by the caller
+  if (B <= 0) return;
+  route_emit_kernel<<<B, RE_THREADS, 0, st>>>(probe, nprobe, lt, chunk_rows, smax, bcap, lcount,
+                                              bucket, slot_off, scanned);
+  if (lt.nslots > 0)
+    route_items_kernel<<<(lt.nslots + 255) / 256, 256, 0, st>>>(lt, chunk_rows, bcap, lcount, items,
+                                                                 n_items);
 }
 
 // =====================================================================
@@ -962,7 +944,7 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
   __shared__ uint32_t s_tk[4];
   __shared__ int64_t s_ti[4];
   const int b = blockIdx.x;
-  const int so = slot_off[b], eo = slot_off[b + 1];
+  const int so = slot_off[2 * b], eo = slot_off[2 * b + 1];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   // tau: best "last entry" among full slots (each full slot has kk distinct ids <= it)
   uint32_t tk = KEY_NONE;
@@ -1714,6 +1696,7 @@ void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const f
 // its probed lists (slow path; correct for any input).
 // ---------------------------------------------------------------------
 constexpr int RR_THREADS = 256;
+constexpr int RR_CAP = 512;     // kept (<= 64) + one chunk of survivors, pow2 for the sort
 constexpr int RR_SURV = 4096;  // survivors handled per pass
 constexpr int RR_HI_PER = 8;   // published upper bounds per thread (2048 per query)
 
@@ -1722,14 +1705,24 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     const int4* __restrict__ cpool, const int32_t* __restrict__ ccount, int cap,
     const uint32_t* __restrict__ slot_hi, const int32_t* __restrict__ slot_n,
     const int32_t* __restrict__ slot_off, ListTable lt, const float* __restrict__ Qd,
-    const int32_t* __restrict__ probe, int nprobe, int kk, int group, int64_t* __restrict__ out_ids,
-    float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n) {
+    const int32_t* __restrict__ probe, int nprobe, int kk, int stage_floats, int64_t* __restrict__ out_ids,
+    float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n,
+    int32_t* __restrict__ nsurv) {
   extern __shared__ __align__(16) uint8_t rr_smem[];
-  Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [MERGE_CAP]
-  float4* qs4 = reinterpret_cast<float4*>(rr_smem + MERGE_CAP * sizeof(Entry));     // [dp/4]
-  float4* rows4 = qs4 + lt.dp / 4;                                                   // [group][dp/4]
-  int32_t* surv = reinterpret_cast<int32_t*>(rows4 + (size_t)group * (lt.dp / 4));  // [RR_SURV]
-  __shared__ int s_cnt, s_ns;
+  Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [RR_CAP]
+  float4* qs4 = reinterpret_cast<float4*>(rr_smem + RR_CAP * sizeof(Entry));     // [dp/4]
+  float* stage = reinterpret_cast<float*>(qs4 + lt.dp / 4);                         // [stage_floats]
+  int32_t* surv = reinterpret_cast<int32_t*>(stage + stage_floats);                 // [RR_SURV]
+  __shared__ int s_cnt, s_ns, s_bin, s_below;
+  __shared__ unsigned s_hist[256];
+  __shared__ unsigned s_wu[RR_THREADS / 32];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  uint32_t bar_ph[2] = {0, 0};
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
+  }
   __shared__ uint32_t s_u[RR_THREADS / 32];
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1741,7 +1734,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
   // 1. global bound U_q: smallest v with #(slot hi <= v) >= kk (KEY_NONE if
   //    fewer).  The query's published hi values (<= RR_HI_PER per thread) are
   //    gathered into registers once, then bisected.
-  const int so = slot_off[b], eo = slot_off[b + 1];
+  const int so = slot_off[2 * b], eo = slot_off[2 * b + 1];
   uint32_t U = KEY_NONE;
   if (!overflow) {
     uint32_t hv[RR_HI_PER];
@@ -1769,27 +1762,29 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     for (int w = 0; w < RR_THREADS / 32; w++) total_hi += s_u[w];
     __syncthreads();
     if (fits && total_hi >= kk) {
-      uint32_t L = 0, H = KEY_NONE;
-      while (L < H) {
-        const uint32_t mid = L + ((H - L) >> 1);
-        int c = 0;
+      // radix select of the kk-th smallest published hi (8 bits per pass)
+      uint32_t prefix = 0;
+      int rem = kk;
+      for (int shift = 24; shift >= 0; shift -= 8) {
+        s_hist[threadIdx.x] = 0;
+        __syncthreads();
+        const uint32_t hmask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
 #pragma unroll
-        for (int i = 0; i < RR_HI_PER; i++) c += hv[i] <= mid;
-        c = __reduce_add_sync(FULL, c);
-        if (lane == 0) s_u[warp] = c;
+        for (int i = 0; i < RR_HI_PER; i++)
+          if (hv[i] != KEY_NONE && (hv[i] & hmask) == (prefix & hmask))
+            atomicAdd(&s_hist[(hv[i] >> shift) & 0xff], 1u);
         __syncthreads();
-        int tot = 0;
-        for (int w = 0; w < RR_THREADS / 32; w++) tot += s_u[w];
+        pick_bin(s_hist[threadIdx.x], rem, &s_bin, &s_below, s_wu);
+        prefix |= (uint32_t)s_bin << shift;
+        rem -= s_below;
         __syncthreads();
-        if (tot >= kk) H = mid;
-        else L = mid + 1;
       }
-      U = L;
+      U = prefix;
     }
   }
   __syncthreads();
-  int kept = 0;
-  const int room = MERGE_CAP - kk;
+  int kept = 0, surv_total = 0;
+  const int room = RR_CAP - kk;
   if (!overflow) {
     for (int p0 = 0; p0 < n; p0 += RR_SURV) {
       // 2a. compact survivors of this pass
@@ -1802,20 +1797,47 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
       }
       __syncthreads();
       const int ns = s_ns;
-      // 2b. exact distances, `group` candidates at a time, into buf after the kept ones
-      for (int g0 = 0; g0 < ns; g0 += group) {
-        const int m = min(group, ns - g0);
-        for (int i = threadIdx.x; i < m * dp4; i += blockDim.x) {
-          const int c = i / dp4, j = i - c * dp4;
-          const int4 e = cpool[(int64_t)b * cap + surv[g0 + c]];
-          rows4[(size_t)c * dp4 + j] =
-              __ldg(reinterpret_cast<const float4*>(lt.rows + (int64_t)e.x * lt.dp) + j);
+      surv_total += ns;
+      // 2b. exact distances of the survivors, up to RR_THREADS at a time
+      //     (thread t runs survivor t's chain), rows streamed through
+      //     shared memory in column blocks of W floats (bulk copies,
+      //     2-deep ring) so every chain advances together
+      const int chunk = min(RR_THREADS, stage_floats / (2 * (DC + 4)));
+      for (int g0 = 0; g0 < ns; g0 += chunk) {
+        const int m = min(chunk, ns - g0);
+        const int nd32 = dp4 / 8;
+        int kq = 1;
+        for (int k2 = nd32; k2 >= 1; k2--)
+          if (nd32 % k2 == 0 && 2 * m * (DC * k2 + 4) <= stage_floats) {
+            kq = k2;
+            break;
+          }
+        const int W = DC * kq, rs = W + 4, nblk = nd32 / kq;
+        auto issue = [&](int blk) {
+          float* dst = stage + (blk & 1) * m * rs;
+          if (threadIdx.x == 0) mbar_arrive_expect_tx(&s_bar[blk & 1], (uint32_t)(m * W * 4));
+          __syncwarp();
+          for (int r = threadIdx.x; r < m; r += 32) {
+            const int4 e = cpool[(int64_t)b * cap + surv[g0 + r]];
+            bulk_g2s(dst + r * rs, lt.rows + (int64_t)e.x * lt.dp + blk * W, (uint32_t)(W * 4),
+                     &s_bar[blk & 1]);
+          }
+        };
+        if (threadIdx.x < 32) issue(0);
+        float acc = 0.f;
+        for (int blk = 0; blk < nblk; blk++) {
+          if (threadIdx.x < 32 && blk + 1 < nblk) issue(blk + 1);
+          mbar_wait(&s_bar[blk & 1], bar_ph[blk & 1]);
+          bar_ph[blk & 1] ^= 1;
+          if (threadIdx.x < m) {
+            const float4* x4 = reinterpret_cast<const float4*>(stage + (blk & 1) * m * rs + threadIdx.x * rs);
+            const float4* q4 = qs4 + blk * (W / 4);
+#pragma unroll 4
+            for (int j = 0; j < W / 4; j++) acc = step4<METRIC>(acc, x4[j], q4[j]);
+          }
+          __syncthreads();  // ring slot (blk & 1) is refilled for block blk + 2
         }
-        __syncthreads();
         if (threadIdx.x < m) {
-          const float4* x4 = rows4 + (size_t)threadIdx.x * dp4;
-          float acc = 0.f;
-          for (int j = 0; j < dp4; j++) acc = step4<METRIC>(acc, x4[j], qs4[j]);
           const int4 e = cpool[(int64_t)b * cap + surv[g0 + threadIdx.x]];
           Entry en;
           en.key = f2key(finalize<METRIC>(acc, 0.f, 0.f));
@@ -1825,12 +1847,8 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
         }
         __syncthreads();
         const int tot = kept + m;
-        if (tot > room || g0 + m >= ns) {
-          cta_bitonic_sort(buf, tot);
-          kept = cta_compact_sorted(buf, tot, kk, true, &s_cnt);
-        } else {
-          kept = tot;
-        }
+        cta_bitonic_sort(buf, tot);
+        kept = cta_compact_sorted(buf, tot, kk, true, &s_cnt);
       }
     }
   } else {
@@ -1880,23 +1898,27 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
       if (out_cid) out_cid[o] = -1;
     }
   }
-  if (threadIdx.x == 0) out_n[b] = kept;
+  if (threadIdx.x == 0) {
+    out_n[b] = kept;
+    if (nsurv) nsurv[b] = overflow ? -1 : surv_total;
+  }
 }
 
 void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* ccount, int cap,
                          const uint32_t* slot_hi, const int32_t* slot_n, const int32_t* slot_off,
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
-                         cudaStream_t st) {
+                         int32_t* nsurv, cudaStream_t st) {
   if (B <= 0) return;
-  const int group = std::max(1, std::min(16, (int)(48 * 1024 / (lt.dp * 4))));
-  const size_t smem = MERGE_CAP * sizeof(Entry) + (size_t)(group + 1) * lt.dp * 4 + RR_SURV * 4;
+  // column-block stage of ~56 KB (two CTAs per SM)
+  const int stage_floats = 56 * 1024 / 4;
+  const size_t smem = RR_CAP * sizeof(Entry) + (size_t)lt.dp * 4 + (size_t)stage_floats * 4 + RR_SURV * 4;
 #define PK_RR(M)                                                                                \
   {                                                                                             \
     auto k = rerank_merge_kernel<M>;                                                            \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     k<<<B, RR_THREADS, smem, st>>>(cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
-                                   nprobe, kk, group, out_ids, out_d, out_cid, out_n);          \
+                                   nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv); \
   }
   if (metric == SQ_L2) PK_RR(SQ_L2)
   else PK_RR(IP)
@@ -2319,46 +2341,66 @@ __device__ __forceinline__ float exact_dist_row(const float* __restrict__ qs, co
   return METRIC == SQ_L2 ? acc : -acc;
 }
 
+template <int METRIC>
+__device__ __forceinline__ float exact_dist_row_smem(const float* __restrict__ qs,
+                                                     const float* __restrict__ x, int d) {
+  float acc = 0.f;
+  int j = 0;
+  for (; j + 4 <= d; j += 4)
+    acc = step4<METRIC>(acc, *reinterpret_cast<const float4*>(x + j),
+                        *reinterpret_cast<const float4*>(qs + j));
+  for (; j < d; j++) acc = (METRIC == SQ_L2) ? sq_step(acc, x[j], qs[j]) : ip_step(acc, x[j], qs[j]);
+  return METRIC == SQ_L2 ? acc : -acc;
+}
+
 constexpr int PICK_THREADS = 256;
-constexpr int PICK_CAP = 4096;  // candidate buffer (entries): nprobe (<= 2048) + new ones, pow2 for the sort
+constexpr int PICK_SMEM_SLOTS = 8192;  // upper-bound keys staged in shared memory up to this
 
 template <int METRIC>
 __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     const float* __restrict__ Aapp, int64_t lda, ListTable lt, const float* __restrict__ cnrm,
     const float* __restrict__ Qd, const float* __restrict__ qn2,
     const int32_t* __restrict__ scope_codes, int nscopes, int nprobe, float coef, float abs_coef,
-    int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key, int32_t* __restrict__ ncand_out) {
-  extern __shared__ float pick_smem[];
-  Entry* buf = reinterpret_cast<Entry*>(pick_smem);                // [PICK_CAP]
-  float* qs = reinterpret_cast<float*>(buf + PICK_CAP);            // [dp]
+    int cap, int stage_floats, int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key,
+    int32_t* __restrict__ ncand_out) {
+  extern __shared__ __align__(16) uint8_t pick_smem[];
+  Entry* buf = reinterpret_cast<Entry*>(pick_smem);                  // [cap] (pow2)
+  float* qs = reinterpret_cast<float*>(buf + cap);                   // [dp]
+  float* rows_st = qs + lt.dp;                                       // [stage_floats]
+  uint32_t* hks = reinterpret_cast<uint32_t*>(rows_st + stage_floats);  // [nslots] when staged
+  __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_codes[64];
   __shared__ unsigned s_hist[256];
-  __shared__ int s_cnt, s_total;
-  __shared__ uint32_t s_prefix;
-  __shared__ int s_rem;
+  __shared__ unsigned s_w[PICK_THREADS / 32];
+  __shared__ int s_cnt, s_total, s_bin, s_below;
   const int b = blockIdx.x;
   const int tid = threadIdx.x;
+  const bool staged = lt.nslots <= PICK_SMEM_SLOTS;
   if (tid < 64) s_codes[tid] = tid < nscopes ? scope_codes[tid] : -1;
-  for (int j = tid; j < lt.dp; j += PICK_THREADS) qs[j] = Qd[(int64_t)b * lt.dp + j];
+  for (int j = tid; j < lt.dp / 4; j += PICK_THREADS)
+    reinterpret_cast<float4*>(qs)[j] = reinterpret_cast<const float4*>(Qd + (int64_t)b * lt.dp)[j];
   if (tid == 0) {
     s_total = 0;
-    s_prefix = 0;
-    s_rem = nprobe;
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_mbar_init();
   }
   __syncthreads();
+  uint32_t bar_ph[2] = {0, 0};
   const float* arow = Aapp + (int64_t)b * lda;
   const float qn = qn2[b];
-  auto valid = [&](int s) -> bool {
-    if (lt.cid[s] < 0) return false;
+  // bounds of list s: hk = key(A + eps), lk = key(A - eps); out of scope /
+  // retired -> KEY_NONE (never a candidate: a finite or -inf lower bound is
+  // never KEY_NONE)
+  auto bounds = [&](int s, uint32_t& hk, uint32_t& lk) {
+    hk = lk = KEY_NONE;
+    if (lt.cid[s] < 0) return;
     const int sc = lt.scope[s];
     bool in = false;
     for (int i = 0; i < nscopes; i++) in |= (s_codes[i] == sc);
-    return in;
-  };
-  auto bounds = [&](int s, uint32_t& hk, uint32_t& lk) {
+    if (!in) return;
     const float A = arow[s];
-    // + abs: flushed subnormal operands / products / partial sums, each
-    // below 2^-126 (|q|_1 + |c|_1 <= sqrt(dp) (2 + |c|^2 + |q|^2)/2 ...)
+    // + abs: flushed subnormal operands / products / partial sums (< 2^-126 each)
     const float nsum = __fadd_ru(cnrm[s], qn);
     const float eps = __fadd_ru(__fmul_ru(coef, nsum), __fmul_ru(abs_coef, __fadd_ru(nsum, 2.f)));
     float hi = __fadd_ru(A, eps), lo = __fsub_rd(A, eps);
@@ -2368,86 +2410,113 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     }
     hk = f2key(hi);
     lk = f2key(lo);
+    if (hk == KEY_NONE) hk = KEY_NONE - 1;  // keep valid lists distinguishable
   };
-  // 1. number of in-scope lists
+  // 1. upper-bound keys (staged) and the number of in-scope lists
   int nv = 0;
-  for (int s = tid; s < lt.nslots; s += PICK_THREADS) nv += valid(s);
+  for (int s = tid; s < lt.nslots; s += PICK_THREADS) {
+    uint32_t hk, lk;
+    bounds(s, hk, lk);
+    nv += hk != KEY_NONE;
+    if (staged) hks[s] = hk;
+  }
   nv = __reduce_add_sync(FULL, nv);
   if ((tid & 31) == 0) atomicAdd(&s_total, nv);
   __syncthreads();
   const int nvalid = s_total;
   // 2. U = nprobe-th smallest upper bound (radix select, 8 bits per pass)
-  uint32_t U = KEY_NONE;
+  uint32_t U = KEY_NONE - 1;
   if (nvalid > nprobe) {
+    uint32_t prefix = 0;
+    int rem = nprobe;
     for (int shift = 24; shift >= 0; shift -= 8) {
       s_hist[tid] = 0;
       __syncthreads();
-      const uint32_t pre = s_prefix;
       const uint32_t hmask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
       for (int s = tid; s < lt.nslots; s += PICK_THREADS) {
-        if (!valid(s)) continue;
         uint32_t hk, lk;
-        bounds(s, hk, lk);
-        if ((hk & hmask) == (pre & hmask)) atomicAdd(&s_hist[(hk >> shift) & 0xff], 1u);
+        if (staged) hk = hks[s];
+        else bounds(s, hk, lk);
+        if (hk != KEY_NONE && (hk & hmask) == (prefix & hmask))
+          atomicAdd(&s_hist[(hk >> shift) & 0xff], 1u);
       }
       __syncthreads();
-      if (tid == 0) {
-        int rem = s_rem;
-        unsigned acc = 0;
-        int bin = 0;
-        for (; bin < 256; bin++) {
-          if (acc + s_hist[bin] >= (unsigned)rem) break;
-          acc += s_hist[bin];
-        }
-        s_rem = rem - (int)acc;
-        s_prefix = pre | ((uint32_t)bin << shift);
-      }
+      pick_bin(s_hist[tid], rem, &s_bin, &s_below, s_w);
+      prefix |= (uint32_t)s_bin << shift;
+      rem -= s_below;
       __syncthreads();
     }
-    U = s_prefix;
+    U = prefix;
   }
-  // 3. exact re-rank of every list whose lower bound is <= U, in passes
+  // 3. exact re-rank of every list whose lower bound is <= U, in rounds of
+  //    up to cap - nprobe candidates merged with the running first nprobe
   int kept = 0, ncand = 0;
-  const int room = PICK_CAP - nprobe;
   int s_next = 0;
+  const int room = cap - nprobe;
   while (s_next < lt.nslots) {
     if (tid == 0) s_cnt = kept;
     __syncthreads();
-    // collect up to `room` new candidates from slots [s_next, ...)
     int s_end = lt.nslots;
     for (int s0 = s_next; s0 < lt.nslots; s0 += PICK_THREADS) {
       const int s = s0 + tid;
-      bool cand = false;
-      if (s < lt.nslots && valid(s)) {
+      if (s < lt.nslots) {
         uint32_t hk, lk;
         bounds(s, hk, lk);
-        cand = lk <= U;
-      }
-      const unsigned bal = __ballot_sync(FULL, cand);
-      // block-wide reservation in slot order is not needed: order is restored by the sort
-      if (cand) {
-        const int pos = atomicAdd(&s_cnt, 1);
-        if (pos < PICK_CAP) {
-          Entry e;
-          e.key = 0;  // filled below
-          e.id = lt.cid[s];
-          e.pay = s;
-          buf[pos] = e;
+        if (lk <= U) {
+          const int pos = atomicAdd(&s_cnt, 1);
+          buf[pos].id = lt.cid[s];
+          buf[pos].pay = s;
         }
       }
-      (void)bal;
       __syncthreads();
-      if (s_cnt > PICK_CAP - PICK_THREADS) {  // next block of slots might not fit
+      if (s_cnt - kept > room - PICK_THREADS) {  // the next block of slots might not fit
         s_end = s0 + PICK_THREADS;
         break;
       }
     }
-    __syncthreads();
-    const int n = min(s_cnt, PICK_CAP);
+    const int n = s_cnt;
     ncand += n - kept;
-    for (int i = kept + tid; i < n; i += PICK_THREADS) {
-      const int s = buf[i].pay;
-      buf[i].key = f2key(exact_dist_row<METRIC>(qs, lt.cent + (int64_t)s * lt.dp, lt.d));
+    // exact distances of this round's candidates buf[kept, n) (<= PICK_THREADS):
+    // thread t runs candidate t's chain; the rows stream through shared memory
+    // in column blocks of W floats (bulk copies, 2-deep ring) so every chain
+    // advances together
+    for (int c0 = kept; c0 < n; c0 += PICK_THREADS) {
+      const int nr = min(PICK_THREADS, n - c0);
+      const int nd32 = lt.dp / DC;
+      int k = 1;  // W = 32 k floats, k | dp/32, 2 * nr * (W + 4) floats fit the stage
+      for (int kk2 = nd32; kk2 >= 1; kk2--)
+        if (nd32 % kk2 == 0 && 2 * nr * (DC * kk2 + 4) <= stage_floats) {
+          k = kk2;
+          break;
+        }
+      const int W = DC * k, rs = W + 4, nblk = nd32 / k;
+      auto issue = [&](int blk) {
+        float* dst = rows_st + (blk & 1) * nr * rs;
+        if (tid == 0) mbar_arrive_expect_tx(&s_bar[blk & 1], (uint32_t)(nr * W * 4));
+        __syncwarp();
+        for (int r = tid; r < nr; r += 32)
+          bulk_g2s(dst + r * rs, lt.cent + (int64_t)buf[c0 + r].pay * lt.dp + blk * W,
+                   (uint32_t)(W * 4), &s_bar[blk & 1]);
+      };
+      if (tid < 32 && nr > 0) issue(0);
+      float acc = 0.f;
+      for (int blk = 0; blk < nblk && nr > 0; blk++) {
+        if (tid < 32 && blk + 1 < nblk) issue(blk + 1);
+        mbar_wait(&s_bar[blk & 1], bar_ph[blk & 1]);
+        bar_ph[blk & 1] ^= 1;
+        if (tid < nr) {
+          const float* x = rows_st + (blk & 1) * nr * rs + tid * rs;
+          const float* q = qs + blk * W;
+          const int jn = min(W, lt.d - blk * W);
+          int j = 0;
+          for (; j + 4 <= jn; j += 4)
+            acc = step4<METRIC>(acc, *reinterpret_cast<const float4*>(x + j),
+                                *reinterpret_cast<const float4*>(q + j));
+          for (; j < jn; j++) acc = (METRIC == SQ_L2) ? sq_step(acc, x[j], q[j]) : ip_step(acc, x[j], q[j]);
+        }
+        __syncthreads();  // ring slot (blk & 1) is refilled for block blk + 2
+      }
+      if (tid < nr) buf[c0 + tid].key = f2key(METRIC == SQ_L2 ? acc : -acc);
     }
     __syncthreads();
     cta_bitonic_sort(buf, n);
@@ -2455,7 +2524,6 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     s_next = s_end;
     __syncthreads();
   }
-  (void)room;
   for (int p = tid; p < nprobe; p += PICK_THREADS) {
     probe[(int64_t)b * nprobe + p] = p < kept ? buf[p].pay : -1;
     if (probe_key) probe_key[(int64_t)b * nprobe + p] = p < kept ? buf[p].key : KEY_NONE;
@@ -2463,26 +2531,48 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
   if (tid == 0 && ncand_out) ncand_out[b] = ncand;
 }
 
-size_t coarse_pick_smem_bytes(int dp) { return PICK_CAP * sizeof(Entry) + (size_t)dp * 4; }
+static int pick_cap(int nprobe) {
+  int c = 1;
+  while (c < nprobe + 2 * PICK_THREADS) c <<= 1;
+  return c;
+}
+// Column-block stage: what is left of ~110 KB (two CTAs per SM), at least
+// 2 x 256 rows x 36 floats.
+static int pick_stage_floats(int dp, int nslots, int nprobe) {
+  const size_t fixed = pick_cap(nprobe) * sizeof(Entry) + (size_t)dp * 4 +
+                       (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 4 : 0);
+  const size_t want = 110 * 1024;
+  const size_t minf = 2 * PICK_THREADS * (DC + 4);
+  size_t f = fixed < want ? (want - fixed) / 4 : 0;
+  return (int)std::max(f, minf);
+}
+size_t coarse_pick_smem_bytes(int dp, int nslots, int nprobe) {
+  return pick_cap(nprobe) * sizeof(Entry) + (size_t)dp * 4 +
+         (size_t)pick_stage_floats(dp, nslots, nprobe) * 4 +
+         (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 4 : 0);
+}
 
 void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, int B, ListTable lt,
                         const float* cnrm, const float* Qd, const float* qn2,
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
                         uint32_t* probe_key, int32_t* ncand, cudaStream_t st) {
   if (B <= 0) return;
-  const size_t smem = coarse_pick_smem_bytes(lt.dp);
+  const size_t smem = coarse_pick_smem_bytes(lt.dp, lt.nslots, nprobe);
+  const int cap = pick_cap(nprobe);
+  const int stage_floats = pick_stage_floats(lt.dp, lt.nslots, nprobe);
   const float coef = coarse_coef(metric, lt.dp, split);
   // 2^-126 * (sqrt(dp) + 4 dp) per unit of (|c|^2 + |q|^2 + 2), doubled
   const float abs_coef = (float)(2.0 * (std::sqrt((double)lt.dp) + 4.0 * lt.dp) * std::ldexp(1.0, -126));
-  if (metric == SQ_L2) {
-    cudaFuncSetAttribute(coarse_pick_kernel<SQ_L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    coarse_pick_kernel<SQ_L2><<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes,
-                                                             nscopes, nprobe, coef, abs_coef, probe, probe_key, ncand);
-  } else {
-    cudaFuncSetAttribute(coarse_pick_kernel<IP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    coarse_pick_kernel<IP><<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes,
-                                                          nscopes, nprobe, coef, abs_coef, probe, probe_key, ncand);
+#define PK_PK(M)                                                                                     \
+  {                                                                                                  \
+    auto k = coarse_pick_kernel<M>;                                                                  \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
+    k<<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe,     \
+                                     coef, abs_coef, cap, stage_floats, probe, probe_key, ncand);    \
   }
+  if (metric == SQ_L2) PK_PK(SQ_L2)
+  else PK_PK(IP)
+#undef PK_PK
 }
 
 }  // namespace pk

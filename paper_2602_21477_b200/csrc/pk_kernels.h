@@ -67,11 +67,12 @@ void launch_centroid(const float* rows, int64_t ldr, int64_t n, int dp, float* c
 void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
                           const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
                           uint32_t* probe_key, cudaStream_t st);
-// Build the (list -> queries) routing and the scan work items.
-void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows,
-                  int32_t* scratch_counts, int32_t* scratch_fill, ScanItem* items,
-                  int32_t* n_items, QPair* qpairs, int32_t* slot_off, int64_t* scanned,
-                  cudaStream_t st);
+// Build the (list -> queries) routing and the scan work items: per query
+// slots [slot_off[2b], slot_off[2b+1]) (stride smax), per list a bucket of
+// bcap (query, slot base) pairs.  lcount [nslots] and *n_items must be zero.
+void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows, int smax,
+                  int bcap, int32_t* lcount, ScanItem* items, int32_t* n_items, QPair* bucket,
+                  int32_t* slot_off, int64_t* scanned, cudaStream_t st);
 // Persistent fused scan + per-(query, item) top-kk.
 void launch_scan(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
                  const float* qnorm, const ScanItem* items, const int32_t* n_items,
@@ -110,7 +111,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          const uint32_t* slot_hi, const int32_t* slot_n, const int32_t* slot_off,
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
-                         cudaStream_t st);
+                         int32_t* nsurv, cudaStream_t st);
 float screen_coef(int metric, int dp);
 float screen_coef_tf32(int metric, int dp);
 size_t tc_smem_bytes();

@@ -115,6 +115,12 @@ class DeviceIndex:
         N.check(N.lib().pk_debug_coarse_counts(self._h, N.ptr(out), B))
         return out
 
+    def rerank_counts(self, B: int) -> np.ndarray:
+        """Pool entries re-ranked exactly per query by the last screened search."""
+        out = np.empty(B, dtype=np.int32)
+        N.check(N.lib().pk_debug_rerank_counts(self._h, N.ptr(out), B))
+        return out
+
     def append(self, cid: int, rows, ids):
         rows = N.f32(rows, self.dimension)
         ids = np.ascontiguousarray(ids, dtype=np.int64)
