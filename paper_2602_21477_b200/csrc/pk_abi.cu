@@ -840,9 +840,16 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                        in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   const ListTable lt = ix->table();
   if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
-  if (ix->screen || ix->coarse_tc) {
+  const bool use_tc = ix->coarse_tc && !probe_in;
+  if (ix->screen || use_tc) {
     RET(ix->qnorm2.ensure(B * 4));
-    launch_qnorm2(ix->q.as<float>(), dp, (int)B, (int)dp, ix->qnorm2.as<float>(), st);
+    if (use_tc && ix->coarse_split) {
+      RET(ix->qhi.ensure((size_t)B * dp * 4));
+      RET(ix->qlo.ensure((size_t)B * dp * 4));
+    }
+    const bool sp = use_tc && ix->coarse_split;
+    launch_qprep(ix->q.as<float>(), (int)B, (int)dp, ix->qnorm2.as<float>(),
+                 sp ? ix->qhi.as<float>() : nullptr, sp ? ix->qlo.as<float>() : nullptr, st);
   }
   PROF(1);
   // 1. coarse quantizer: distances to every list centroid, top-nprobe in scope
@@ -852,19 +859,18 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     PROF(2);
   } else if (ix->coarse_tc) {
     RET(ix->ncand.ensure(B * 4));
+    const int ks = coarse_split_k(ix->nslots, (int)B, (int)dp, ix->num_sms);
+    RET(ix->dc.ensure((size_t)ks * B * ns * 4));
     if (ix->coarse_split) {
-      RET(ix->qhi.ensure((size_t)B * dp * 4));
-      RET(ix->qlo.ensure((size_t)B * dp * 4));
-      launch_tf32_split(ix->q.as<float>(), B, (int)dp, ix->qhi.as<float>(), ix->qlo.as<float>(), st);
       RET(ix->encode_2d(&ix->cmaps.q[0], ix->qhi.as<float>(), dp, B, 64));
       RET(ix->encode_2d(&ix->cmaps.q[1], ix->qlo.as<float>(), dp, B, 64));
     } else {
       RET(ix->encode_2d(&ix->cmaps.q[0], ix->q.as<float>(), dp, B, 64));
     }
-    launch_coarse_tc(ix->metric, ix->coarse_split, ix->cmaps, ix->nslots, (int)B, (int)dp,
-                     ix->d_cnrm, ix->qnorm2.as<float>(), ix->dc.as<float>(), ns, st);
+    launch_coarse_tc(ix->coarse_split, ks, ix->cmaps, ix->nslots, (int)B, (int)dp,
+                     ix->dc.as<float>(), ns, st);
     PROF(2);
-    launch_coarse_pick(ix->metric, ix->coarse_split, ix->dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, ix->q.as<float>(),
+    launch_coarse_pick(ix->metric, ix->coarse_split, ks, ix->dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, ix->q.as<float>(),
                        ix->qnorm2.as<float>(), ix->scopes.as<int32_t>(), nscopes, nprobe,
                        ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), ix->ncand.as<int32_t>(), st);
   } else {

@@ -2150,11 +2150,10 @@ size_t coarse_tc_smem_bytes(bool split) {
 // D1 + D2.  The input-rounding error drops from ~2^-9 to ~3 * 2^-20 of
 // sum |c_j q_j| (coarse_coef()), so the exact re-rank set shrinks to the
 // boundary.  !SPLIT: one TF32 product of the fp32 tables.
-template <int METRIC, bool SPLIT>
+template <bool SPLIT>
 __global__ void __launch_bounds__(128, 1)
     coarse_tc_kernel(const __grid_constant__ CoarseMaps maps, int nslots, int B, int nchunk,
-                     const float* __restrict__ cnrm, const float* __restrict__ qn2,
-                     float* __restrict__ Aout, int64_t lda) {
+                     float* __restrict__ Dout, int64_t lda) {
   constexpr int NT = SPLIT ? 2 : 1;  // tables per operand
   constexpr size_t STAGE_BYTES = NT * (CT_A_BYTES + CT_B_BYTES);
   extern __shared__ uint8_t smem_raw[];
@@ -2170,6 +2169,10 @@ __global__ void __launch_bounds__(128, 1)
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * CT_M, b0 = blockIdx.y * CT_N;
+  // split-K: this CTA's chunk range
+  const int kc0 = (int)((int64_t)nchunk * blockIdx.z / gridDim.z);
+  const int kc1 = (int)((int64_t)nchunk * (blockIdx.z + 1) / gridDim.z);
+  float* Aout = Dout + (int64_t)blockIdx.z * B * lda;
   if (threadIdx.x == 0) {
     for (int i = 0; i < CT_STAGES; i++) {
       mbar_init(&full[i], 1);
@@ -2191,7 +2194,7 @@ __global__ void __launch_bounds__(128, 1)
     const uint64_t pol = policy_evict_last();  // tables are re-read by the other CTAs
     int s = 0;
     uint32_t ph = 0;
-    for (int c = 0; c < nchunk; c++) {
+    for (int c = kc0; c < kc1; c++) {
       mbar_wait(&empty[s], ph ^ 1);
       mbar_arrive_expect_tx(&full[s], (uint32_t)STAGE_BYTES);
       for (int t = 0; t < NT; t++) {
@@ -2207,13 +2210,13 @@ __global__ void __launch_bounds__(128, 1)
     const uint32_t idesc = umma_idesc_tf32(CT_M, CT_N);
     int s = 0;
     uint32_t ph = 0;
-    for (int c = 0; c < nchunk; c++) {
+    for (int c = kc0; c < kc1; c++) {
       mbar_wait(&full[s], ph);
       tc_fence_after();
       const uint32_t ah = smem_u32(a_tile(s, 0)), bh = smem_u32(b_tile(s, 0));
 #pragma unroll
       for (int k = 0; k < DC / 8; k++) {
-        const uint32_t acc = (c | k) != 0;
+        const uint32_t acc = ((c - kc0) | k) != 0;
         umma_tf32(tmem, umma_desc_sw128(ah + k * 32), umma_desc_sw128(bh + k * 32), idesc, acc);
         if (SPLIT) {
           const uint32_t al = smem_u32(a_tile(s, NT - 1)), bl = smem_u32(b_tile(s, NT - 1));
@@ -2233,7 +2236,6 @@ __global__ void __launch_bounds__(128, 1)
   mbar_wait(done, 0);
   tc_fence_after();
   const int m = c0 + 32 * warp + lane;  // this thread's centroid slot (TMEM lane)
-  const float cn = m < nslots ? cnrm[m] : 0.f;
 #pragma unroll
   for (int g = 0; g < CT_N / 16; g++) {
     float v[16], w[16];
@@ -2247,11 +2249,7 @@ __global__ void __launch_bounds__(128, 1)
 #pragma unroll
       for (int a = 0; a < 16; a++) {
         const int b = b0 + g * 16 + a;
-        if (b < B) {
-          const float A = (METRIC == SQ_L2) ? __fsub_rn(__fadd_rn(cn, qn2[b]), __fmul_rn(2.f, v[a]))
-                                            : -v[a];
-          Aout[(int64_t)b * lda + m] = A;
-        }
+        if (b < B) Aout[(int64_t)b * lda + m] = v[a];  // dot (partial over this K range)
       }
     }
   }
@@ -2260,23 +2258,61 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 0) tmem_dealloc(tmem, NT * CT_N);
 }
 
-void launch_coarse_tc(int metric, bool split, const CoarseMaps& maps, int nslots, int B, int dp,
-                      const float* cnrm, const float* qn2, float* Aout, int64_t lda, cudaStream_t st) {
+int coarse_split_k(int nslots, int B, int dp, int num_sms) {
+  const int tiles = ((nslots + CT_M - 1) / CT_M) * ((B + CT_N - 1) / CT_N);
+  return std::max(1, std::min(dp / DC / 2, num_sms / std::max(tiles, 1)));
+}
+
+void launch_coarse_tc(bool split, int ks, const CoarseMaps& maps, int nslots, int B, int dp,
+                      float* Dout, int64_t lda, cudaStream_t st) {
   if (B <= 0 || nslots <= 0) return;
   const size_t smem = coarse_tc_smem_bytes(split);
-  dim3 grid((unsigned)((nslots + CT_M - 1) / CT_M), (unsigned)((B + CT_N - 1) / CT_N));
-#define PK_CT(M, S)                                                                            \
-  {                                                                                            \
-    auto k = coarse_tc_kernel<M, S>;                                                           \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);           \
-    k<<<grid, 128, smem, st>>>(maps, nslots, B, dp / DC, cnrm, qn2, Aout, lda);                \
-  }
-  if (metric == SQ_L2) {
-    if (split) PK_CT(SQ_L2, true) else PK_CT(SQ_L2, false)
+  dim3 grid((unsigned)((nslots + CT_M - 1) / CT_M), (unsigned)((B + CT_N - 1) / CT_N), (unsigned)ks);
+  if (split) {
+    cudaFuncSetAttribute(coarse_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    coarse_tc_kernel<true><<<grid, 128, smem, st>>>(maps, nslots, B, dp / DC, Dout, lda);
   } else {
-    if (split) PK_CT(IP, true) else PK_CT(IP, false)
+    cudaFuncSetAttribute(coarse_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    coarse_tc_kernel<false><<<grid, 128, smem, st>>>(maps, nslots, B, dp / DC, Dout, lda);
   }
-#undef PK_CT
+}
+
+// Query prep for the screens: qn2[b] = sum q_j^2 (FFMA, any order) and, when
+// hi/lo are given, the TF32 hi/lo split of the row.  One warp per query.
+__global__ void qprep_kernel(const float* __restrict__ Q, int B, int dp, float* __restrict__ qn2,
+                             float* __restrict__ hi, float* __restrict__ lo) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)b * dp);
+  float acc = 0.f;
+  for (int j = lane; j < dp / 4; j += 32) {
+    const float4 v = q4[j];
+    acc = __fmaf_rn(v.x, v.x, acc);
+    acc = __fmaf_rn(v.y, v.y, acc);
+    acc = __fmaf_rn(v.z, v.z, acc);
+    acc = __fmaf_rn(v.w, v.w, acc);
+    if (hi) {
+      float4 h, l;
+      h.x = __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+      h.y = __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+      h.z = __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+      h.w = __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+      l.x = __fsub_rn(v.x, h.x);
+      l.y = __fsub_rn(v.y, h.y);
+      l.z = __fsub_rn(v.z, h.z);
+      l.w = __fsub_rn(v.w, h.w);
+      reinterpret_cast<float4*>(hi + (int64_t)b * dp)[j] = h;
+      reinterpret_cast<float4*>(lo + (int64_t)b * dp)[j] = l;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+  if (lane == 0) qn2[b] = acc;
+}
+void launch_qprep(const float* Q, int B, int dp, float* qn2, float* hi, float* lo, cudaStream_t st) {
+  if (B <= 0) return;
+  qprep_kernel<<<(B + 7) / 8, 256, 0, st>>>(Q, B, dp, qn2, hi, lo);
 }
 
 // hi = x with the low 13 mantissa bits cleared (exactly representable in
@@ -2310,11 +2346,13 @@ void launch_tf32_split(const float* x, int64_t n, int dp, float* hi, float* lo, 
 // screen by tools/microbench/umma_check.cu) + 3 2^-20 (dropped lo*lo and the
 // TF32 conversions of the lo parts) + 2^-23 (D1 + D2) + 2d 2^-31 (D2's own
 // accumulation); !split: the scan's c_dot.  2x safety like the scan.
-float coarse_coef(int metric, int dp, bool split) {
-  if (!split) return screen_coef_tf32(metric, dp);
+float coarse_coef(int metric, int dp, bool split, int ks) {
   const double u = 1.0 / 16777216.0;
   auto gam = [u](double n) { return n * u / (1.0 - n * u); };
-  const double c_dot = 2.0 * (dp / 2097152.0 + 3.0 / 1048576.0 + 1.0 / 8388608.0 + 2.0 * dp / 2147483648.0);
+  // split-K: ks partial dots summed in fp32 (ks - 1 rounded adds)
+  const double c_ks = (ks - 1) * 2.0 * u;
+  if (!split) return (float)(screen_coef_tf32(metric, dp) + 2.0 * 1.0625 * 2.0 * c_ks);
+  const double c_dot = 2.0 * (dp / 2097152.0 + 3.0 / 1048576.0 + 1.0 / 8388608.0 + 2.0 * dp / 2147483648.0 + c_ks);
   double c;
   if (metric == SQ_L2) c = (c_dot + gam(dp) + 2.0 * gam(dp + 3) + 4.0 * u) / (1.0 - gam(dp));
   else c = (0.5 * c_dot + gam(dp) + 2.0 * u) / (1.0 - gam(dp));
@@ -2361,13 +2399,14 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     const float* __restrict__ Aapp, int64_t lda, ListTable lt, const float* __restrict__ cnrm,
     const float* __restrict__ Qd, const float* __restrict__ qn2,
     const int32_t* __restrict__ scope_codes, int nscopes, int nprobe, float coef, float abs_coef,
-    int cap, int stage_floats, int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key,
+    int cap, int stage_floats, int ks, int64_t zstride, int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key,
     int32_t* __restrict__ ncand_out) {
   extern __shared__ __align__(16) uint8_t pick_smem[];
   Entry* buf = reinterpret_cast<Entry*>(pick_smem);                  // [cap] (pow2)
   float* qs = reinterpret_cast<float*>(buf + cap);                   // [dp]
   float* rows_st = qs + lt.dp;                                       // [stage_floats]
   uint32_t* hks = reinterpret_cast<uint32_t*>(rows_st + stage_floats);  // [nslots] when staged
+  uint32_t* lks = hks + lt.nslots;                                        // [nslots] when staged
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_codes[64];
   __shared__ unsigned s_hist[256];
@@ -2394,14 +2433,19 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
   // never KEY_NONE)
   auto bounds = [&](int s, uint32_t& hk, uint32_t& lk) {
     hk = lk = KEY_NONE;
-    if (lt.cid[s] < 0) return;
+    // all loads first (independent), then the arithmetic
+    const int64_t cid = lt.cid[s];
     const int sc = lt.scope[s];
+    const float cn = cnrm[s];
+    float dot = arow[s];
+    for (int z = 1; z < ks; z++) dot = __fadd_rn(dot, arow[(int64_t)z * zstride + s]);
+    if (cid < 0) return;
     bool in = false;
     for (int i = 0; i < nscopes; i++) in |= (s_codes[i] == sc);
     if (!in) return;
-    const float A = arow[s];
+    const float A = (METRIC == SQ_L2) ? __fsub_rn(__fadd_rn(cn, qn), __fmul_rn(2.f, dot)) : -dot;
     // + abs: flushed subnormal operands / products / partial sums (< 2^-126 each)
-    const float nsum = __fadd_ru(cnrm[s], qn);
+    const float nsum = __fadd_ru(cn, qn);
     const float eps = __fadd_ru(__fmul_ru(coef, nsum), __fmul_ru(abs_coef, __fadd_ru(nsum, 2.f)));
     float hi = __fadd_ru(A, eps), lo = __fsub_rd(A, eps);
     if (!isfinite(hi) || !isfinite(lo)) {
@@ -2414,11 +2458,15 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
   };
   // 1. upper-bound keys (staged) and the number of in-scope lists
   int nv = 0;
+#pragma unroll 4
   for (int s = tid; s < lt.nslots; s += PICK_THREADS) {
     uint32_t hk, lk;
     bounds(s, hk, lk);
     nv += hk != KEY_NONE;
-    if (staged) hks[s] = hk;
+    if (staged) {
+      hks[s] = hk;
+      lks[s] = lk;
+    }
   }
   nv = __reduce_add_sync(FULL, nv);
   if ((tid & 31) == 0) atomicAdd(&s_total, nv);
@@ -2461,7 +2509,8 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
       const int s = s0 + tid;
       if (s < lt.nslots) {
         uint32_t hk, lk;
-        bounds(s, hk, lk);
+        if (staged) lk = lks[s];
+        else bounds(s, hk, lk);
         if (lk <= U) {
           const int pos = atomicAdd(&s_cnt, 1);
           buf[pos].id = lt.cid[s];
@@ -2540,7 +2589,7 @@ static int pick_cap(int nprobe) {
 // 2 x 256 rows x 36 floats.
 static int pick_stage_floats(int dp, int nslots, int nprobe) {
   const size_t fixed = pick_cap(nprobe) * sizeof(Entry) + (size_t)dp * 4 +
-                       (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 4 : 0);
+                       (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 8 : 0);
   const size_t want = 110 * 1024;
   const size_t minf = 2 * PICK_THREADS * (DC + 4);
   size_t f = fixed < want ? (want - fixed) / 4 : 0;
@@ -2549,10 +2598,10 @@ static int pick_stage_floats(int dp, int nslots, int nprobe) {
 size_t coarse_pick_smem_bytes(int dp, int nslots, int nprobe) {
   return pick_cap(nprobe) * sizeof(Entry) + (size_t)dp * 4 +
          (size_t)pick_stage_floats(dp, nslots, nprobe) * 4 +
-         (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 4 : 0);
+         (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 8 : 0);
 }
 
-void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, int B, ListTable lt,
+void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64_t lda, int B, ListTable lt,
                         const float* cnrm, const float* Qd, const float* qn2,
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
                         uint32_t* probe_key, int32_t* ncand, cudaStream_t st) {
@@ -2560,7 +2609,7 @@ void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, 
   const size_t smem = coarse_pick_smem_bytes(lt.dp, lt.nslots, nprobe);
   const int cap = pick_cap(nprobe);
   const int stage_floats = pick_stage_floats(lt.dp, lt.nslots, nprobe);
-  const float coef = coarse_coef(metric, lt.dp, split);
+  const float coef = coarse_coef(metric, lt.dp, split, ks);
   // 2^-126 * (sqrt(dp) + 4 dp) per unit of (|c|^2 + |q|^2 + 2), doubled
   const float abs_coef = (float)(2.0 * (std::sqrt((double)lt.dp) + 4.0 * lt.dp) * std::ldexp(1.0, -126));
 #define PK_PK(M)                                                                                     \
@@ -2568,7 +2617,8 @@ void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, 
     auto k = coarse_pick_kernel<M>;                                                                  \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
     k<<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe,     \
-                                     coef, abs_coef, cap, stage_floats, probe, probe_key, ncand);    \
+                                     coef, abs_coef, cap, stage_floats, ks, (int64_t)B * lda, probe, \
+                                     probe_key, ncand);                                              \
   }
   if (metric == SQ_L2) PK_PK(SQ_L2)
   else PK_PK(IP)

@@ -142,15 +142,20 @@ struct CoarseMaps {
   CUtensorMap q[2];  // padded batch, same split
 };
 size_t coarse_tc_smem_bytes(bool split);
-void launch_coarse_tc(int metric, bool split, const CoarseMaps& maps, int nslots, int B, int dp,
-                      const float* cnrm, const float* qn2, float* Aout, int64_t lda, cudaStream_t st);
+// Split-K factor for the coarse GEMM (grid ~ one CTA per SM).
+int coarse_split_k(int nslots, int B, int dp, int num_sms);
+// Dout[z][b][slot] = partial dot over K range z of ks (the pick sums them in z order).
+void launch_coarse_tc(bool split, int ks, const CoarseMaps& maps, int nslots, int B, int dp,
+                      float* Dout, int64_t lda, cudaStream_t st);
+// qn2[b] = FFMA squared norm; hi/lo (may be NULL) = TF32 split of the batch.
+void launch_qprep(const float* Q, int B, int dp, float* qn2, float* hi, float* lo, cudaStream_t st);
 // hi/lo TF32 split of rows [0, n) of an [n][dp] table.
 void launch_tf32_split(const float* x, int64_t n, int dp, float* hi, float* lo, cudaStream_t st);
-float coarse_coef(int metric, int dp, bool split);
+float coarse_coef(int metric, int dp, bool split, int ks);
 // Per query: exact top-nprobe in-scope lists by (dist, cid) from the screened
 // distances (bound + exact re-rank of the boundary).  ncand: re-ranked lists
 // per query (may be NULL).
-void launch_coarse_pick(int metric, bool split, const float* Aapp, int64_t lda, int B, ListTable lt,
+void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64_t lda, int B, ListTable lt,
                         const float* cnrm, const float* Qd, const float* qn2,
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
                         uint32_t* probe_key, int32_t* ncand, cudaStream_t st);
