@@ -111,6 +111,25 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags);
 
+/* ---- cold tier (TierManager, tiering.py:175-448) --
+ * pk_index_enable_tier (before any list exists): every list keeps a copy in
+ * a pinned, device-mapped host arena (the source of truth, tiering.py:9-12);
+ * lists are created cold and HBM holds only the lists made resident.  A
+ * search streams the probed cold lists into HBM staging over PCIe (one gather
+ * kernel per batch); results are identical in every residency state
+ * (tiering.py:294-328, SPEC "merged = single-tier").
+ * pk_list_set_resident: 1 = admit (HBM copy on a side stream; the list
+ *   switches resident when the copy completes, MigrationTicket phases
+ *   tiering.py:332-416), 0 = evict (release the HBM copy).
+ * pk_list_residency: 0 cold, 1 resident, 2 admission in flight.
+ * pk_tier_stats out[10]: resident lists, cold lists, resident HBM bytes,
+ *   lists / bytes staged by the last search, bytes staged in total, searches
+ *   that staged, admissions started, admissions completed, host arena bytes. */
+int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows);
+int pk_list_set_resident(pk_index* ix, int64_t cid, int resident);
+int pk_list_residency(pk_index* ix, int64_t cid, int* state);
+int pk_tier_stats(pk_index* ix, int64_t* out, int n);
+
 /* ---- sharded search ------------------------------
  * Lists are partitioned over ranks (one index per GPU); the centroid table is
  * replicated so every rank computes the identical global probe set

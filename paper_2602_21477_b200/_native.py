@@ -65,6 +65,10 @@ _SIGS = [
     ("pk_debug_rerank_counts", [_vp, _vp, _i64], _int),
     ("pk_search_coarse", [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _int], _int),
     ("pk_search_probed", [_vp, _vp, _i64, _vp, _i32, _i32, _i64, _vp, _int], _int),
+    ("pk_index_enable_tier", [_vp, _i64], _int),
+    ("pk_list_set_resident", [_vp, _i64, _int], _int),
+    ("pk_list_residency", [_vp, _i64, ctypes.POINTER(_int)], _int),
+    ("pk_tier_stats", [_vp, _vp, _int], _int),
     ("pk_list_add_remote", [_vp, _i64, _i32, _vp], _int),
     ("pk_shard_block_bytes", [_i64, _i32], _i64),
     ("pk_merge_shards", [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _int], _int),

@@ -136,7 +136,7 @@ struct pk_index {
 
   // search scratch
   DevBuf q, qnorm, dc, probe, probe_key, counts, items, qpairs, slot_off, scanned,
-      cand_key, cand_id, cand_n, cand_list, work, out_ids, out_d, out_cid, out_n, scopes, assign_c,
+      cand_key, cand_id, cand_n, cand_list, out_ids, out_d, out_cid, out_n, scopes, assign_c,
       assign_d;
   int chunk_rows = 512;
   bool screen = true;  // screened scan + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
@@ -148,6 +148,33 @@ struct pk_index {
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
   DevBuf shard_in, shard_out, pb, pb_out, nsurv;
+
+  // ---- cold tier (pk_index_enable_tier).  Every list keeps a copy in a
+  // pinned, device-mapped host arena -- the source of truth, as the
+  // reference's host rows are (ref/tiering.py:9-12) -- and HBM holds the
+  // resident lists only.  A batch streams its probed cold lists into arena
+  // staging ranges (gather kernel over PCIe); admissions copy a list into HBM
+  // on the migration stream and switch it resident once the copy is done
+  // (searches stay exact in every phase, ref/tiering.py:332-416).
+  bool tiered = false;
+  float* hrows = nullptr;    // [hcap][dp] pinned
+  int64_t* hids = nullptr;   // [hcap] pinned
+  float* hrows_d = nullptr;  // device aliases (mapped)
+  int64_t* hids_d = nullptr;
+  int64_t hcap = 0, htop = 0;
+  std::vector<Range> hfree;
+  std::vector<int64_t> h_hoff, h_hcap;
+  std::vector<uint8_t> h_res;        // HBM copy at h_off valid
+  std::vector<cudaEvent_t> mig_ev;   // in-flight admission copy (null = none)
+  std::vector<int64_t> mig_off, mig_cap;
+  std::vector<int32_t> mig_list;
+  cudaStream_t mst = nullptr;        // migration side stream
+  std::vector<Range> staged;         // arena ranges of the last batch's cold lists
+  cudaEvent_t stage_ev = nullptr;
+  bool stage_pending = false;
+  int64_t st_lists_last = 0, st_rows_last = 0, st_rows_total = 0, st_batches = 0;
+  int64_t mig_started = 0, mig_done = 0;
+  DevBuf stage_desc, tmp_rows;
 
   // stage timing (pk_profile_begin / pk_profile_end): events around each
   // stage of every pk_search while enabled.
@@ -241,6 +268,7 @@ struct pk_index {
   }
 
   int grow_arena(int64_t need_rows) {
+    if (mst) CK(cudaStreamSynchronize(mst));  // in-flight admission copies target the old arena
     int64_t ncap = std::max<int64_t>({need_rows, arena_cap + arena_cap / 2, 1024});
     float* nrows = nullptr;
     int64_t* nids = nullptr;
@@ -341,11 +369,171 @@ struct pk_index {
     h_cid.resize(ncap, -1);
     h_scope.resize(ncap, -1);
     h_remote.resize(ncap, 0);
+    h_hoff.resize(ncap, 0);
+    h_hcap.resize(ncap, 0);
+    h_res.resize(ncap, 1);
+    mig_ev.resize(ncap, nullptr);
+    mig_off.resize(ncap, 0);
+    mig_cap.resize(ncap, 0);
     // whole table must be re-uploaded into the new arrays
     if (nslots > 0) {
       mark(0);
       mark(nslots - 1);
     }
+    return PK_OK;
+  }
+
+  // ---- cold tier helpers ----------------------------------------------
+  int host_grow(int64_t need) {
+    if (st) CK(cudaStreamSynchronize(st));  // gathers / migrations read the old host arena
+    if (mst) CK(cudaStreamSynchronize(mst));
+    const int64_t ncap = std::max<int64_t>({need, hcap + hcap / 2, 1024});
+    float* nr = nullptr;
+    int64_t* ni = nullptr;
+    CK(cudaHostAlloc((void**)&nr, (size_t)ncap * dp * 4, cudaHostAllocMapped | cudaHostAllocPortable));
+    CK(cudaHostAlloc((void**)&ni, (size_t)ncap * 8, cudaHostAllocMapped | cudaHostAllocPortable));
+    if (hrows) {
+      memcpy(nr, hrows, (size_t)htop * dp * 4);
+      memcpy(ni, hids, (size_t)htop * 8);
+      cudaFreeHost(hrows);
+      cudaFreeHost(hids);
+    }
+    hrows = nr;
+    hids = ni;
+    hcap = ncap;
+    CK(cudaHostGetDevicePointer((void**)&hrows_d, hrows, 0));
+    CK(cudaHostGetDevicePointer((void**)&hids_d, hids, 0));
+    return PK_OK;
+  }
+  int host_alloc(int64_t cap, int64_t* off) {
+    for (size_t i = 0; i < hfree.size(); i++) {
+      if (hfree[i].cap >= cap) {
+        *off = hfree[i].off;
+        hfree[i].off += cap;
+        hfree[i].cap -= cap;
+        if (hfree[i].cap == 0) hfree.erase(hfree.begin() + i);
+        return PK_OK;
+      }
+    }
+    if (htop + cap > hcap) RET(host_grow(htop + cap));
+    *off = htop;
+    htop += cap;
+    return PK_OK;
+  }
+  void host_free(int64_t off, int64_t cap) {
+    if (cap <= 0) return;
+    if (off + cap == htop) {
+      htop = off;
+      return;
+    }
+    hfree.push_back({off, cap});
+  }
+  // n rows (d floats each, host or device source) into host arena rows at `at`
+  // (padded to dp with zeros), ids alongside.
+  int host_put(int64_t at, const float* src, const int64_t* src_ids, int64_t n, bool dev) {
+    if (n <= 0) return PK_OK;
+    if (dev) {
+      CK(cudaMemcpy2DAsync(hrows + at * dp, dp * 4, src, d * 4, d * 4, n, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(hids + at, src_ids, n * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
+      for (int64_t r = 0; r < n; r++) memcpy(hrows + (at + r) * dp, src + r * d, d * 4);
+      memcpy(hids + at, src_ids, n * 8);
+    }
+    if (dp > d)
+      for (int64_t r = 0; r < n; r++) memset(hrows + (at + r) * dp + d, 0, (dp - d) * 4);
+    return PK_OK;
+  }
+  // Switch a finished admission copy resident (wait: block until it is done).
+  int finish_migration(int32_t s, bool wait) {
+    cudaEvent_t ev = mig_ev[s];
+    if (!ev) return PK_OK;
+    if (wait) {
+      CK(cudaEventSynchronize(ev));
+    } else {
+      cudaError_t q = cudaEventQuery(ev);
+      if (q == cudaErrorNotReady) return PK_OK;
+      if (q != cudaSuccess) CK(q);
+    }
+    cudaEventDestroy(ev);
+    mig_ev[s] = nullptr;
+    h_off[s] = mig_off[s];
+    h_cap[s] = mig_cap[s];
+    h_res[s] = 1;
+    mark(s);
+    mig_done++;
+    return PK_OK;
+  }
+  int poll_migrations() {
+    if (mig_list.empty()) return PK_OK;
+    std::vector<int32_t> keep;
+    for (int32_t s : mig_list) {
+      RET(finish_migration(s, false));
+      if (mig_ev[s]) keep.push_back(s);
+    }
+    mig_list.swap(keep);
+    return PK_OK;
+  }
+  // Free the previous batch's staging ranges once that batch has finished.
+  int release_staged() {
+    if (!stage_pending) return PK_OK;
+    CK(cudaEventSynchronize(stage_ev));
+    for (const Range& r : staged) free_range(r.off, r.cap);
+    staged.clear();
+    stage_pending = false;
+    return PK_OK;
+  }
+  // Stream every cold list probed by the batch into arena staging ranges.
+  int stage_cold(int64_t B, int32_t nprobe) {
+    bool any = false;
+    for (int32_t s = 0; s < nslots && !any; s++)
+      any = h_cid[s] >= 0 && !h_res[s] && h_len[s] > 0;
+    st_lists_last = st_rows_last = 0;
+    if (!any) return PK_OK;
+    std::vector<int32_t> pr((size_t)B * nprobe);
+    CK(cudaMemcpyAsync(pr.data(), probe.p, pr.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<uint8_t> seen(nslots, 0);
+    std::vector<StageCopy> desc;
+    for (int32_t v : pr) {
+      if (v < 0 || seen[v]) continue;
+      seen[v] = 1;
+      if (h_res[v] || h_cid[v] < 0 || h_len[v] == 0) continue;
+      int64_t off;
+      RET(alloc_range(h_len[v], &off));
+      StageCopy c;
+      c.src_row = h_hoff[v];
+      c.dst_row = off;
+      c.n = (int32_t)h_len[v];
+      c.pad = 0;
+      desc.push_back(c);
+      staged.push_back({off, h_len[v]});
+      h_off[v] = off;
+      mark(v);
+      st_rows_last += h_len[v];
+    }
+    if (desc.empty()) return PK_OK;
+    st_lists_last = (int64_t)desc.size();
+    st_rows_total += st_rows_last;
+    st_batches++;
+    RET(stage_desc.ensure(desc.size() * sizeof(StageCopy)));
+    CK(cudaMemcpyAsync(stage_desc.p, desc.data(), desc.size() * sizeof(StageCopy),
+                       cudaMemcpyHostToDevice, st));
+    launch_gather_rows(stage_desc.as<StageCopy>(), (int)desc.size(), hrows_d, hids_d, rows, ids, nrm,
+                       (int)dp, st);
+    CK(cudaGetLastError());
+    return sync_table();
+  }
+  // Padded device copy of slot s's rows (resident: the arena itself).
+  int rows_on_device(int32_t s, const float** out) {
+    if (!tiered || h_res[s]) {
+      *out = rows + h_off[s] * dp;
+      return PK_OK;
+    }
+    RET(tmp_rows.ensure((size_t)std::max<int64_t>(h_len[s], 1) * dp * 4));
+    CK(cudaMemcpyAsync(tmp_rows.p, hrows + h_hoff[s] * dp, (size_t)h_len[s] * dp * 4,
+                       cudaMemcpyHostToDevice, st));
+    *out = tmp_rows.as<float>();
     return PK_OK;
   }
 
@@ -528,6 +716,15 @@ int pk_index_destroy(pk_index* ix) {
   cudaFree(ix->d_chi);
   cudaFree(ix->d_clo);
   for (cudaEvent_t e : ix->prof_ev) cudaEventDestroy(e);
+  if (ix->mst) cudaStreamSynchronize(ix->mst);
+  for (cudaEvent_t e : ix->mig_ev)
+    if (e) cudaEventDestroy(e);
+  if (ix->stage_ev) cudaEventDestroy(ix->stage_ev);
+  if (ix->mst) cudaStreamDestroy(ix->mst);
+  if (ix->hrows) cudaFreeHost(ix->hrows);
+  if (ix->hids) cudaFreeHost(ix->hids);
+  ix->stage_desc.release();
+  ix->tmp_rows.release();
   for (DevBuf* b : {&ix->q, &ix->qnorm, &ix->dc, &ix->probe, &ix->probe_key, &ix->counts,
                     &ix->items, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list,
@@ -563,19 +760,40 @@ int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* r
     s = ix->nslots++;
   }
   const int64_t cap = n + n / 4 + 16;
-  int64_t off;
-  RET(ix->alloc_range(cap, &off));
-  RET(ix->put_rows(off, rows, ids, n, flags & PK_DEVICE_PTRS));
-  ix->h_off[s] = off;
+  const bool dev = flags & PK_DEVICE_PTRS;
+  const float* crow = nullptr;  // padded device rows the centroid is computed from
+  if (ix->tiered) {
+    // cold on creation (the reference admits lists through hotset_update):
+    // host arena copy, centroid from a padded device staging copy
+    int64_t hoff;
+    RET(ix->host_alloc(cap, &hoff));
+    RET(ix->host_put(hoff, rows, ids, n, dev));
+    ix->h_hoff[s] = hoff;
+    ix->h_hcap[s] = cap;
+    ix->h_res[s] = 0;
+    ix->h_off[s] = 0;
+    ix->h_cap[s] = 0;
+    RET(ix->tmp_rows.ensure((size_t)n * ix->dp * 4));
+    CK(cudaMemsetAsync(ix->tmp_rows.p, 0, (size_t)n * ix->dp * 4, ix->st));
+    CK(cudaMemcpy2DAsync(ix->tmp_rows.p, ix->dp * 4, rows, ix->d * 4, ix->d * 4, n,
+                         dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ix->st));
+    crow = ix->tmp_rows.as<float>();
+  } else {
+    int64_t off;
+    RET(ix->alloc_range(cap, &off));
+    RET(ix->put_rows(off, rows, ids, n, dev));
+    ix->h_off[s] = off;
+    ix->h_cap[s] = cap;
+    ix->h_res[s] = 1;
+    crow = ix->rows + off * ix->dp;
+  }
   ix->h_len[s] = n;
-  ix->h_cap[s] = cap;
   ix->h_cid[s] = cid;
   ix->h_scope[s] = scope_code;
   ix->h_remote[s] = 0;
   ix->cid2slot[cid] = s;
   ix->mark(s);
-  launch_centroid(ix->rows + off * ix->dp, ix->dp, n, (int)ix->dp, ix->d_cent + (int64_t)s * ix->dp,
-                  ix->st);
+  launch_centroid(crow, ix->dp, n, (int)ix->dp, ix->d_cent + (int64_t)s * ix->dp, ix->st);
   ix->centroid_norm(s);
   CK(cudaGetLastError());
   if (out_centroid) {
@@ -604,6 +822,7 @@ int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const floa
   ix->h_cid[s] = cid;
   ix->h_scope[s] = scope_code;
   ix->h_remote[s] = 1;
+  ix->h_res[s] = 1;  // never staged: no rows here
   ix->cid2slot[cid] = s;
   ix->mark(s);
   CK(cudaMemcpyAsync(ix->d_cent + (int64_t)s * ix->dp, centroid, ix->d * 4, cudaMemcpyHostToDevice,
@@ -670,6 +889,25 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
   RET(ix->slot_of(cid, &s));
   if (ix->h_remote[s]) return fail(PK_ERR_USAGE, "cluster %lld is owned by another shard", (long long)cid);
   const int64_t len = ix->h_len[s];
+  if (ix->tiered) {
+    RET(ix->finish_migration(s, true));
+    if (len + n > ix->h_hcap[s]) {  // relocate the host copy (x1.5)
+      const int64_t ncap = std::max<int64_t>(len + n, ix->h_hcap[s] + ix->h_hcap[s] / 2) + 16;
+      int64_t noff;
+      RET(ix->host_alloc(ncap, &noff));
+      memcpy(ix->hrows + noff * ix->dp, ix->hrows + ix->h_hoff[s] * ix->dp, (size_t)len * ix->dp * 4);
+      memcpy(ix->hids + noff, ix->hids + ix->h_hoff[s], (size_t)len * 8);
+      ix->host_free(ix->h_hoff[s], ix->h_hcap[s]);
+      ix->h_hoff[s] = noff;
+      ix->h_hcap[s] = ncap;
+    }
+    RET(ix->host_put(ix->h_hoff[s] + len, rows, ids, n, flags & PK_DEVICE_PTRS));
+    if (!ix->h_res[s]) {
+      ix->h_len[s] = len + n;
+      ix->mark(s);
+      return PK_OK;
+    }
+  }
   if (len + n > ix->h_cap[s]) {
     // relocate into a larger range (Cluster._grow x1.5, ref/clusters.py:61-69)
     const int64_t ncap = std::max<int64_t>(len + n, ix->h_cap[s] + ix->h_cap[s] / 2) + 16;
@@ -701,6 +939,19 @@ int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
   const int64_t len = ix->h_len[s];
   if (row < 0 || row >= len) return fail(PK_ERR_USAGE, "row %lld out of range", (long long)row);
   const int64_t last = len - 1, off = ix->h_off[s];
+  if (ix->tiered) {
+    RET(ix->finish_migration(s, true));
+    const int64_t ho = ix->h_hoff[s];
+    if (row != last) {
+      memcpy(ix->hrows + (ho + row) * ix->dp, ix->hrows + (ho + last) * ix->dp, ix->dp * 4);
+      ix->hids[ho + row] = ix->hids[ho + last];
+    }
+    if (!ix->h_res[s]) {
+      ix->h_len[s] = last;
+      ix->mark(s);
+      return PK_OK;
+    }
+  }
   if (row != last) {
     CK(cudaMemcpyAsync(ix->rows + (off + row) * ix->dp, ix->rows + (off + last) * ix->dp,
                        ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
@@ -717,7 +968,13 @@ int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
 int pk_list_retire(pk_index* ix, int64_t cid) {
   int32_t s;
   RET(ix->slot_of(cid, &s));
-  ix->free_range(ix->h_off[s], ix->h_cap[s]);
+  if (ix->tiered) {
+    RET(ix->finish_migration(s, true));
+    ix->host_free(ix->h_hoff[s], ix->h_hcap[s]);
+    ix->h_hoff[s] = ix->h_hcap[s] = 0;
+  }
+  if (ix->h_res[s]) ix->free_range(ix->h_off[s], ix->h_cap[s]);
+  ix->h_res[s] = 1;
   ix->h_cid[s] = -1;
   ix->h_len[s] = 0;
   ix->h_cap[s] = 0;
@@ -734,9 +991,11 @@ int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
   int32_t s;
   RET(ix->slot_of(cid, &s));
   const int64_t n = ix->h_len[s];
-  if (n > 0)
-    launch_centroid(ix->rows + ix->h_off[s] * ix->dp, ix->dp, n, (int)ix->dp,
-                    ix->d_cent + (int64_t)s * ix->dp, ix->st);
+  if (n > 0) {
+    const float* r = nullptr;
+    RET(ix->rows_on_device(s, &r));
+    launch_centroid(r, ix->dp, n, (int)ix->dp, ix->d_cent + (int64_t)s * ix->dp, ix->st);
+  }
   ix->centroid_norm(s);
   CK(cudaGetLastError());
   if (out_centroid) {
@@ -770,6 +1029,12 @@ int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
   int32_t s;
   RET(ix->slot_of(cid, &s));
   const int64_t n = ix->h_len[s], off = ix->h_off[s];
+  if (ix->tiered) {  // the host copy is always current
+    const int64_t ho = ix->h_hoff[s];
+    for (int64_t r = 0; rows && r < n; r++) memcpy(rows + r * ix->d, ix->hrows + (ho + r) * ix->dp, ix->d * 4);
+    if (ids && n > 0) memcpy(ids, ix->hids + ho, n * 8);
+    return PK_OK;
+  }
   if (n > 0) {
     if (rows)
       CK(cudaMemcpy2DAsync(rows, ix->d * 4, ix->rows + off * ix->dp, ix->dp * 4, ix->d * 4, n,
@@ -777,6 +1042,90 @@ int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
     if (ids) CK(cudaMemcpyAsync(ids, ix->ids + off, n * 8, cudaMemcpyDeviceToHost, ix->st));
   }
   CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows) {
+  if (ix->tiered) return PK_OK;
+  if (ix->cid2slot.size() > 0) return fail(PK_ERR_USAGE, "enable the cold tier before creating lists");
+  CK(cudaSetDevice(ix->device));
+  CK(cudaStreamCreateWithFlags(&ix->mst, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ix->stage_ev, cudaEventDisableTiming));
+  RET(ix->host_grow(std::max<int64_t>(reserve_rows, 1024)));
+  ix->tiered = true;
+  return PK_OK;
+}
+
+int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
+  if (!ix->tiered) return fail(PK_ERR_USAGE, "no cold tier: every list is HBM-resident");
+  CK(cudaSetDevice(ix->device));
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  if (ix->h_remote[s]) return fail(PK_ERR_USAGE, "cluster %lld is owned by another shard", (long long)cid);
+  if (resident) {
+    if (ix->h_res[s] || ix->mig_ev[s]) return PK_OK;
+    // admission: Allocated -> Copying (side stream) -> Switching at the next
+    // poll once the copy event completes (TierManager.step_migration)
+    const int64_t len = ix->h_len[s];
+    const int64_t cap = len + len / 4 + 16;  // 25% device slack (ref/tiering.py:356)
+    int64_t off;
+    RET(ix->alloc_range(cap, &off));
+    if (len > 0) {
+      CK(cudaMemcpyAsync(ix->rows + off * ix->dp, ix->hrows + ix->h_hoff[s] * ix->dp,
+                         (size_t)len * ix->dp * 4, cudaMemcpyHostToDevice, ix->mst));
+      CK(cudaMemcpyAsync(ix->ids + off, ix->hids + ix->h_hoff[s], (size_t)len * 8,
+                         cudaMemcpyHostToDevice, ix->mst));
+      launch_row_norms(ix->rows + off * ix->dp, len, (int)ix->dp, ix->nrm + off, ix->mst);
+      CK(cudaGetLastError());
+    }
+    cudaEvent_t ev;
+    CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CK(cudaEventRecord(ev, ix->mst));
+    ix->mig_ev[s] = ev;
+    ix->mig_off[s] = off;
+    ix->mig_cap[s] = cap;
+    ix->mig_list.push_back(s);
+    ix->mig_started++;
+    return PK_OK;
+  }
+  RET(ix->finish_migration(s, true));
+  if (ix->h_res[s]) {
+    ix->free_range(ix->h_off[s], ix->h_cap[s]);
+    ix->h_res[s] = 0;
+    ix->h_off[s] = ix->h_cap[s] = 0;
+    ix->mark(s);
+  }
+  return PK_OK;
+}
+
+int pk_list_residency(pk_index* ix, int64_t cid, int* state) {
+  int32_t s;
+  RET(ix->slot_of(cid, &s));
+  RET(ix->finish_migration(s, false));
+  *state = ix->h_res[s] ? 1 : (ix->mig_ev[s] ? 2 : 0);
+  return PK_OK;
+}
+
+int pk_tier_stats(pk_index* ix, int64_t* out, int n) {
+  int64_t v[10] = {0};
+  if (ix->tiered) RET(ix->poll_migrations());
+  for (int32_t s = 0; s < ix->nslots; s++) {
+    if (ix->h_cid[s] < 0 || ix->h_remote[s]) continue;
+    if (ix->h_res[s]) {
+      v[0]++;
+      v[2] += ix->h_cap[s] * (ix->dp * 4 + 8);
+    } else {
+      v[1]++;
+    }
+  }
+  v[3] = ix->st_lists_last;
+  v[4] = ix->st_rows_last * (ix->dp * 4 + 8);
+  v[5] = ix->st_rows_total * (ix->dp * 4 + 8);
+  v[6] = ix->st_batches;
+  v[7] = ix->mig_started;
+  v[8] = ix->mig_done;
+  v[9] = ix->tiered ? ix->hcap * (ix->dp * 4 + 8) : 0;
+  for (int i = 0; i < n && i < 10; i++) out[i] = v[i];
   return PK_OK;
 }
 
@@ -799,6 +1148,10 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (B == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   cudaStream_t st = ix->st;
+  if (ix->tiered) {
+    RET(ix->release_staged());
+    RET(ix->poll_migrations());
+  }
   RET(ix->sync_table());
   const int64_t dp = ix->dp;
   const int32_t ns = std::max<int32_t>(ix->nslots, 1);
@@ -887,12 +1240,15 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     if (!dev) CK(cudaStreamSynchronize(st));
     return PK_OK;
   }
+  // cold tier: stream the probed lists that are not HBM-resident into staging
+  if (ix->tiered) RET(ix->stage_cold(B, nprobe));
+  const ListTable lt2 = ix->table();  // staging may have grown the arena
   // 2. route (query -> lists) into (list -> queries) work items
   int32_t* lcount = ix->counts.as<int32_t>();
   int32_t* n_items = lcount + ns;
   int32_t* work_ctr = lcount + ns + 1;
   CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, st));
-  launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt, ix->chunk_rows, (int)smax, (int)B,
+  launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt2, ix->chunk_rows, (int)smax, (int)B,
                lcount, ix->items.as<ScanItem>(), n_items, ix->qpairs.as<QPair>(),
                ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
   // 3. fused scan + per-(query, list chunk) top-kk
@@ -905,14 +1261,14 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     CK(cudaMemsetAsync(ix->ccount.p, 0, (size_t)B * 4, st));
     if (ix->tensor) {
       RET(ix->qsw.ensure((size_t)8 * B * dp * 4));
-      launch_scan_tc(ix->metric, lt, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(),
+      launch_scan_tc(ix->metric, lt2, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(),
                      ix->qnorm2.as<float>(), ix->items.as<ScanItem>(), n_items,
                      (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
                      work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
                      ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
                      ix->pool_cap, ix->num_sms, st);
     } else {
-      launch_scan_screen(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
+      launch_scan_screen(ix->metric, lt2, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
                          ix->items.as<ScanItem>(), n_items,
                          (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
                          work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
@@ -920,7 +1276,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                          ix->pool_cap, ix->num_sms, st);
     }
   } else
-    launch_scan(ix->metric, lt, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
+    launch_scan(ix->metric, lt2, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
                 ix->items.as<ScanItem>(), n_items, (int)std::min<int64_t>(max_items, INT32_MAX),
                 ix->qpairs.as<QPair>(), kk, work_ctr, ix->cand_key.as<uint32_t>(),
                 ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
@@ -945,12 +1301,12 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (ix->screen)
     launch_rerank_merge(ix->metric, (int)B, ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
                         ix->pool_cap, ix->cand_key.as<uint32_t>(), ix->cand_n.as<int32_t>(),
-                        ix->slot_off.as<int32_t>(), lt, ix->q.as<float>(), ix->probe.as<int32_t>(),
+                        ix->slot_off.as<int32_t>(), lt2, ix->q.as<float>(), ix->probe.as<int32_t>(),
                         nprobe, kk, o_ids, o_d, o_cid, o_n, ix->nsurv.as<int32_t>(), st);
   else
     launch_merge((int)B, ix->slot_off.as<int32_t>(), ix->cand_key.as<uint32_t>(),
                  ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(), kk,
-                 lt, o_ids, o_d, o_cid, o_n, st);
+                 lt2, o_ids, o_d, o_cid, o_n, st);
   CK(cudaGetLastError());
   if (!dev) {
     CK(cudaMemcpyAsync(out_ids, o_ids, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));

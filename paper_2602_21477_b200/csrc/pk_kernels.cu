@@ -2626,3 +2626,51 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
 }
 
 }  // namespace pk
+
+namespace pk {
+
+// =====================================================================
+// Cold tier (north_star subsystem 4): lists that
+// are not HBM-resident live in a pinned, device-mapped host arena.  Before a
+// batch scans them, this kernel streams every probed cold list from host
+// memory (PCIe, zero-copy 16-byte loads, coalesced per warp) into a staging
+// range of the HBM arena, with ids and the squared row norms the tensor-core
+// screen needs.  One CTA per list, one warp per row.
+// =====================================================================
+__global__ void __launch_bounds__(256) gather_rows_kernel(const StageCopy* __restrict__ desc,
+                                                          const float* __restrict__ hrows,
+                                                          const int64_t* __restrict__ hids,
+                                                          float* __restrict__ rows,
+                                                          int64_t* __restrict__ ids,
+                                                          float* __restrict__ nrm, int dp) {
+  const StageCopy c = desc[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int dp4 = dp / 4;
+  for (int r = warp; r < c.n; r += 8) {
+    const float4* src = reinterpret_cast<const float4*>(hrows + (c.src_row + r) * (int64_t)dp);
+    float4* dst = reinterpret_cast<float4*>(rows + (c.dst_row + r) * (int64_t)dp);
+    float acc = 0.f;
+    for (int j = lane; j < dp4; j += 32) {
+      const float4 v = src[j];
+      dst[j] = v;
+      acc = __fmaf_rn(v.x, v.x, acc);
+      acc = __fmaf_rn(v.y, v.y, acc);
+      acc = __fmaf_rn(v.z, v.z, acc);
+      acc = __fmaf_rn(v.w, v.w, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+    if (lane == 0) {
+      nrm[c.dst_row + r] = acc;
+      ids[c.dst_row + r] = hids[c.src_row + r];
+    }
+  }
+}
+
+void launch_gather_rows(const StageCopy* desc, int ndesc, const float* hrows, const int64_t* hids,
+                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st) {
+  if (ndesc <= 0) return;
+  gather_rows_kernel<<<ndesc, 256, 0, st>>>(desc, hrows, hids, rows, ids, nrm, dp);
+}
+
+}  // namespace pk

@@ -160,4 +160,15 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
                         uint32_t* probe_key, int32_t* ncand, cudaStream_t st);
 
+// Cold tier: copy host-arena rows [src_row, src_row+n) (pinned, device-mapped)
+// to HBM arena rows [dst_row, ...), with ids and squared norms.
+struct StageCopy {
+  int64_t src_row;
+  int64_t dst_row;
+  int32_t n;
+  int32_t pad;
+};
+void launch_gather_rows(const StageCopy* desc, int ndesc, const float* hrows, const int64_t* hids,
+                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st);
+
 }  // namespace pk

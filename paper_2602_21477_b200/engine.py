@@ -191,6 +191,9 @@ class Store:
         self.metric = cfg.metric
         self.scope_codes = ScopeCodes()
         self.index = DeviceIndex(cfg.dimension, cfg.metric.wire_code, cfg.device)
+        native_tier = cfg.accelerator == "native"
+        if native_tier:  # cold tier: pinned host memory, HBM holds the hotset
+            self.index.enable_tier()
         self.clusters = ClusterStore(
             cfg.dimension, cfg.metric, self.rng, self.index, self.scope_codes,
             split_threshold=cfg.split_threshold, split_target=cfg.split_target,
@@ -199,7 +202,7 @@ class Store:
         self.runner = TaskRunner(cfg.threads)
         self.tier = TierManager(self.clusters, self.index, budget_bytes=cfg.budget_bytes,
                                 b_insert=cfg.b_insert, decay_half_life=cfg.decay_half_life,
-                                slack_fraction=cfg.slack_fraction)
+                                slack_fraction=cfg.slack_fraction, native=native_tier)
         self.agents: set[str] = set()
         self.sequences: dict[str, list[np.ndarray]] = {}
         self.payloads: dict[int, bytes] = {}
@@ -559,7 +562,15 @@ class Store:
         return None
 
     def _tick(self, locked: bool = False):
+        """ref/engine.py:745-752: the hotset policy runs every hotset_interval
+        operations (only the native cold tier has a budget to enforce)."""
         self._op_count += 1
+        if self.tier.native and self._op_count % self.cfg.hotset_interval == 0:
+            if locked:
+                self.tier.hotset_update()
+            else:
+                with self._lock.write():
+                    self.tier.hotset_update()
 
     # --- item access -------------------------------------------------------
     def _vector_of(self, item_id: int):

@@ -180,6 +180,30 @@ class DeviceIndex:
                                   N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), None,
                                   N.ptr(out_scanned), N.PK_DEVICE_PTRS))
 
+    # ---- cold tier (TierManager residency, ref/tiering.py:175-448) --------
+    TIER_STATS = ("resident_lists", "cold_lists", "resident_bytes", "staged_lists_last",
+                  "staged_bytes_last", "staged_bytes_total", "staged_searches",
+                  "admissions_started", "admissions_done", "host_arena_bytes")
+
+    def enable_tier(self, reserve_rows: int = 0):
+        """Cold tier on: lists live in pinned host memory, HBM holds the
+        resident ones (call before creating lists)."""
+        N.check(N.lib().pk_index_enable_tier(self._h, int(reserve_rows)))
+
+    def set_resident(self, cid: int, resident: bool):
+        N.check(N.lib().pk_list_set_resident(self._h, int(cid), 1 if resident else 0))
+
+    def residency(self, cid: int) -> int:
+        """0 cold, 1 HBM-resident, 2 admission in flight."""
+        v = ctypes.c_int(0)
+        N.check(N.lib().pk_list_residency(self._h, int(cid), ctypes.byref(v)))
+        return int(v.value)
+
+    def tier_stats(self) -> dict:
+        out = np.zeros(len(self.TIER_STATS), dtype=np.int64)
+        N.check(N.lib().pk_tier_stats(self._h, N.ptr(out), len(out)))
+        return dict(zip(self.TIER_STATS, out.tolist()))
+
     # ---- sharded search (SURVEY.md section 8e) ---------------------------
     def add_remote_list(self, cid: int, scope_code: int, centroid):
         """A list owned by another rank: centroid only (joins the coarse

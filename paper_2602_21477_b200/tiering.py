@@ -8,13 +8,16 @@ hotset is "all lists" and inserts never need a buffer flush.  The decayed
 access frequencies (ref/tiering.py:210-218) and ``metrics()`` are kept so the
 store's observable counters have the reference's meaning.
 
-The pinned-host cold tier (clusters beyond ``budget_bytes`` streamed on a side
-stream) is the next step of this module ("What comes next").
+With ``StoreConfig(accelerator="native")`` the cold tier is on: clusters
+outside the budgeted hotset live in pinned host memory and are streamed to
+HBM when probed, admissions copy on a side stream (TierManager below).
 """
 
 from __future__ import annotations
 
 from dataclasses import dataclass
+
+import numpy as np
 
 from .core import AcceleratorError  # noqa: F401  (re-exported name)
 
@@ -50,20 +53,51 @@ def derive_b_insert(model: CostModel, max_n: int = 1 << 20) -> int:
     return n
 
 
+@dataclass
+class ResidentCopy:
+    """ref/tiering.py:150-154: an HBM copy of a cluster (here the device list
+    itself; ``nbytes`` is the budget charge of the admission)."""
+
+    handle: int
+    ids: np.ndarray
+    nbytes: int
+
+
 class TierManager:
+    """Hotset selection and residency (ref/tiering.py:175-448).
+
+    ``native=False`` (accelerator "none" / "simulated"): every posting list is
+    HBM-resident -- 180 GB holds configs[1]-[4] whole -- so the hotset is all
+    lists and inserts append in place.  ``native=True`` (accelerator
+    "native", configs[4]): the device index runs its cold tier -- lists live
+    in pinned host memory, HBM holds the hotset -- and this class is the
+    reference's policy verbatim: decayed access frequency (half-life
+    ``decay_half_life``), greedy admission by (-frequency, cid) under
+    ``budget_bytes``, eviction hysteresis 1.2, run every ``hotset_interval``
+    operations by the store.  Admissions copy on a side stream and switch when
+    complete; a search scans a cold or in-flight list from a staged copy, so
+    results never depend on residency (ref/tiering.py:294-328).
+    """
+
     def __init__(self, store, index, budget_bytes: int = 64 << 20, b_insert: int = 128,
-                 decay_half_life: int = 10000, slack_fraction: float = 0.25):
+                 decay_half_life: int = 10000, slack_fraction: float = 0.25,
+                 hysteresis: float = 1.2, native: bool = False):
         self.store = store
         self.index = index
         self.budget_bytes = budget_bytes
         self.b_insert = b_insert
         self.decay_half_life = decay_half_life
         self.slack_fraction = slack_fraction
+        self.hysteresis = hysteresis
+        self.native = native
         self.freq: dict[int, tuple[float, int]] = {}
         self.clock = 0
+        self._hot: set[int] = set()
+        self.resident_bytes = 0
         self.flush_count = 0
         self.migration_us: list[float] = []
 
+    # --- frequency tracking (ref/tiering.py:210-218) ---
     def record_access(self, cid: int):
         self.clock += 1
         value, last = self.freq.get(cid, (0.0, self.clock))
@@ -76,36 +110,103 @@ class TierManager:
 
     @property
     def hotset(self) -> set[int]:
-        return set(self.store.clusters)
+        if not self.native:
+            return set(self.store.clusters)
+        return set(self._hot)
 
-    def hotset_update(self):
-        return []
+    # --- hotset (ref/tiering.py:222-262) ---
+    def hotset_update(self) -> list[tuple[str, int]]:
+        if not self.native:
+            return []
+        clusters = self.store.clusters
+        self._hot &= set(clusters)  # retired clusters left with their device copies
+        live = [cid for cid in clusters if clusters[cid].size > 0]
+        ranked = sorted(live, key=lambda c: (-self.decayed_freq(c), c))
+        actions: list[tuple[str, int]] = []
+        target: list[int] = []
+        used = 0
+        for cid in ranked:
+            nb = clusters[cid].nbytes
+            if nb == 0 or self.decayed_freq(cid) <= 0.0:
+                continue
+            if used + nb <= self.budget_bytes:
+                target.append(cid)
+                used += nb
+        target_set = set(target)
+        for cid in sorted(self._hot - target_set):
+            displacers = [c for c in target_set - self._hot]
+            if displacers:
+                hottest = max(self.decayed_freq(c) for c in displacers)
+                if hottest < self.hysteresis * self.decayed_freq(cid):
+                    target_set.add(cid)
+                    continue
+            actions.append(("evict", cid))
+            self._evict(cid)
+        for cid in sorted(target_set - self._hot):
+            actions.append(("admit", cid))
+            self._admit(cid)
+        return actions
 
+    def _admit(self, cid: int):
+        cl = self.store.clusters[cid]
+        nbytes = int(cl.size * cl.dimension * 4 * (1 + self.slack_fraction))
+        self.index.set_resident(cid, True)
+        cl.resident = ResidentCopy(cid, cl.member_ids.copy(), nbytes)
+        self.resident_bytes += nbytes
+        self._hot.add(cid)
+
+    def _evict(self, cid: int):
+        self._hot.discard(cid)
+        cl = self.store.clusters.get(cid)
+        if cl is None or cl.resident is None:
+            return
+        self.index.set_resident(cid, False)
+        self.resident_bytes -= cl.resident.nbytes
+        cl.resident = None
+        cl.buffer = []
+
+    # --- insertion path (ref/tiering.py:280-290) ---
     def buffered_insert(self, cid: int, item_id: int, vector) -> str:
-        """ref/tiering.py:280-290: the device list is appended in place."""
+        """The device list (and the host copy of a tiered index) is appended
+        in place, so there is no insertion buffer to flush."""
         self.store.add_member(cid, item_id, vector)
+        cl = self.store.clusters[cid]
+        if self.native and cl.resident is None:
+            return "DirectHost"
         return "DeviceInPlace"
 
+    # --- splitting (ref/tiering.py:420-434) ---
     def split_offload(self, cid: int):
-        """ref/tiering.py:420-434: split with the device k-means."""
+        cl = self.store.clusters[cid]
+        was_resident = self.native and cl.resident is not None
+        if was_resident:
+            self._evict(cid)
         outcome = self.store.split_cluster(cid)
         parent_freq = self.decayed_freq(cid)
         self.freq.pop(cid, None)
         for child in outcome.children:
             self.freq[child] = (parent_freq / max(len(outcome.children), 1), self.clock)
+        if was_resident:
+            self.hotset_update()
         return outcome
 
-    def _evict(self, cid: int):
-        return None
-
+    # --- metrics (ref/tiering.py:438-448) ---
     def metrics(self) -> dict:
         live = [c for c in self.store.clusters.values() if c.size > 0]
-        return {
-            "residency_ratio": 1.0 if live else 0.0,
+        if self.native:
+            resident = sum(1 for c in live if c.resident is not None)
+            ratio = resident / len(live) if live else 0.0
+        else:
+            ratio = 1.0 if live else 0.0
+        out = {
+            "residency_ratio": ratio,
             "buffer_flush_count": self.flush_count,
             "migration_us": list(self.migration_us),
-            "resident_bytes": sum(c.nbytes for c in live),
+            "resident_bytes": self.resident_bytes if self.native else sum(c.nbytes for c in live),
             "host_us": 0.0,
             "accel_us": 0.0,
             "device_bytes": self.index.nbytes(),
         }
+        if self.native:
+            out.update({f"tier_{k}": v for k, v in self.index.tier_stats().items()})
+        return out

@@ -62,8 +62,10 @@ def replay_model(spec):
     return rec
 
 
-def replay_store(spec, batch_searches=False):
-    """Replay on paper_2602_21477_b200.Store (needs the GPU)."""
+def replay_store(spec, batch_searches=False, overrides=None, tier_log=None):
+    """Replay on paper_2602_21477_b200.Store (needs the GPU).  ``overrides``
+    change StoreConfig fields that must not change results (e.g. the native
+    cold tier); ``tier_log`` collects tier metrics after every search."""
     import tempfile
 
     from paper_2602_21477_b200 import Store, StoreConfig
@@ -71,7 +73,9 @@ def replay_store(spec, batch_searches=False):
     from paper_2602_21477_b200.pnck import write_pnck
 
     base, ops = gen.trace_ops(spec)
-    store = Store(StoreConfig(**gen.store_config_kwargs(spec)))
+    kw = gen.store_config_kwargs(spec)
+    kw.update(overrides or {})
+    store = Store(StoreConfig(**kw))
     for i in range(spec["agents"]):
         store.register_agent(f"agent{i}")
     rec = {"digest": gen.digest(base)}
@@ -103,6 +107,8 @@ def replay_store(spec, batch_searches=False):
             rec[f"{i}/hit_scope"] = np.array([h[2] for h in res.hits], dtype="U16")
             rec[f"{i}/scanned"] = np.array(res.stats.scanned_vectors)
             rec[f"{i}/scan_ids"] = np.asarray(res.scan_ids, dtype=np.int64)
+            if tier_log is not None:
+                tier_log.append(store.tier.metrics())
     cids = sorted(store.clusters.clusters)
     cl = store.clusters.clusters
     rec["final/cids"] = np.array(cids, dtype=np.int64)

@@ -1,0 +1,106 @@
+"""The native cold tier (ref/tiering.py:175-448):
+lists live in pinned host memory, HBM holds the hotset, probed cold lists are
+streamed into HBM staging, admissions copy on a side stream.  Residency must
+never change a result (ref/tiering.py:294-328): every check below is
+bit-exact against the oracle / the reference fixtures."""
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from replay import compare_records, gen, load_golden, replay_store
+
+pytestmark = pytest.mark.gpu
+
+
+def bits(a):
+    return np.asarray(a, dtype=np.float32).view(np.uint32)
+
+
+def _check(ix, lists, cents, cids, Q, nprobe, kk):
+    flat = O.FlatIVF.from_lists(lists, np.stack(cents), np.asarray(cids, np.int64))
+    out = ix.search(Q, [0], nprobe, kk, want_probe=True)
+    ids, dd, cnt, probe, sc = flat.search(Q, nprobe, kk, threads=8)
+    assert np.array_equal(out.probe, probe)
+    assert np.array_equal(out.ids, ids)
+    assert np.array_equal(bits(out.dists), bits(dd))
+    assert np.array_equal(out.scanned, sc)
+
+
+def test_tiered_index_every_residency_state():
+    from paper_2602_21477_b200 import DeviceIndex
+
+    rng = np.random.default_rng(21)
+    d, nlist = 96, 30
+    ix = DeviceIndex(d)
+    ix.enable_tier()
+    centers = rng.normal(size=(nlist, d)).astype(np.float32)
+    lists, cents, cids, nid = [], [], [], 0
+    for c in range(nlist):
+        n = int(rng.integers(1, 900))
+        rows = (centers[c] + 0.5 * rng.normal(size=(n, d))).astype(np.float32)
+        ids = rng.permutation(np.arange(nid, nid + n)).astype(np.int64)
+        nid += n
+        cents.append(ix.create_list(c + 7, 0, rows, ids))
+        lists.append([ids, rows])
+        cids.append(c + 7)
+        assert ix.residency(c + 7) == 0  # created cold
+        assert np.array_equal(bits(cents[-1]), bits(O.centroid(rows)))
+    Q = (centers[rng.integers(0, nlist, 90)] + 0.5 * rng.normal(size=(90, d))).astype(np.float32)
+    _check(ix, [tuple(x) for x in lists], cents, cids, Q, 6, 10)  # all cold: staged
+    st = ix.tier_stats()
+    assert st["cold_lists"] == nlist and st["staged_lists_last"] > 0
+    # admit a third; search immediately (copies may be in flight) and again
+    for c in cids[::3]:
+        ix.set_resident(c, True)
+    _check(ix, [tuple(x) for x in lists], cents, cids, Q, 6, 10)
+    ix.sync()
+    _check(ix, [tuple(x) for x in lists], cents, cids, Q, 9, 20)
+    assert all(ix.residency(c) == 1 for c in cids[::3])
+    # mutations on resident, cold and in-flight lists, then evictions
+    for j, c in enumerate(cids[:8]):
+        if j == 5:
+            ix.set_resident(c, True)  # in flight while appended to
+        add = rng.normal(size=(300, d)).astype(np.float32)
+        aid = np.arange(nid, nid + 300)
+        nid += 300
+        ix.append(c, add, aid)
+        lists[j][0] = np.concatenate([lists[j][0], aid])
+        lists[j][1] = np.concatenate([lists[j][1], add])
+        for _ in range(7):
+            r = int(rng.integers(0, len(lists[j][0])))
+            ix.remove_row(c, r)
+            last = len(lists[j][0]) - 1
+            lists[j][0][r] = lists[j][0][last]
+            lists[j][1][r] = lists[j][1][last]
+            lists[j][0] = lists[j][0][:last]
+            lists[j][1] = lists[j][1][:last]
+        cents[j] = ix.recompute(c)
+        assert np.array_equal(bits(cents[j]), bits(O.centroid(lists[j][1])))
+        rows, ids = ix.read(c)
+        assert np.array_equal(ids, lists[j][0]) and np.array_equal(bits(rows), bits(lists[j][1]))
+    _check(ix, [tuple(x) for x in lists], cents, cids, Q, 6, 10)
+    for c in cids[::3]:
+        ix.set_resident(c, False)
+    ix.set_resident(cids[1], True)
+    _check(ix, [tuple(x) for x in lists], cents, cids, Q, 30, 64)
+    st = ix.tier_stats()
+    assert st["admissions_started"] >= 11 and st["staged_bytes_total"] > 0
+    ix.close()
+
+
+@pytest.mark.parametrize("name,budget", [("ivf_small", 40_000), ("ivf_splits", 8_000)])
+def test_store_trace_with_native_cold_tier(name, budget):
+    """The reference's recorded traces (inserts, deletes, updates, centroid
+    maintenance, k-means splits, multi-scope searches) replayed on a Store
+    whose budget keeps only part of the index in HBM, with the hotset policy
+    running every 3 operations: identical results, real residency churn."""
+    want = load_golden(f"trace_{name}.npz")
+    log = []
+    got = replay_store(gen.TRACE_SPECS[name], overrides=dict(accelerator="native", budget_bytes=budget,
+                                                              hotset_interval=3), tier_log=log)
+    mism = compare_records(got, want)
+    assert not mism, "\n".join(mism[:10])
+    assert any(m["tier_cold_lists"] > 0 for m in log), "budget never left a list cold"
+    assert any(m["tier_resident_lists"] > 0 for m in log), "hotset never admitted a list"
+    assert max(m["tier_staged_searches"] for m in log) > 0

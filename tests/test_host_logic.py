@@ -122,3 +122,100 @@ def test_coarse_rng_mirror_matches_model():
         m._graph_insert(scope)
         mirror.on_insert(scope)
     assert m.rng.random() == rng.random()
+
+
+class _FakeCluster:
+    def __init__(self, cid, n, d=8):
+        self.id, self.size, self.dimension = cid, n, d
+        self.member_ids = np.arange(n, dtype=np.int64)
+        self.resident = None
+        self.buffer = []
+
+    @property
+    def nbytes(self):
+        return self.size * self.dimension * 4
+
+
+class _FakeIndex:
+    def __init__(self):
+        self.res = {}
+
+    def set_resident(self, cid, on):
+        self.res[cid] = bool(on)
+
+
+class _FakeStore:
+    def __init__(self):
+        self.clusters = {}
+
+
+def _tier(budget):
+    from paper_2602_21477_b200.tiering import TierManager
+
+    st, ix = _FakeStore(), _FakeIndex()
+    return st, ix, TierManager(st, ix, budget_bytes=budget, native=True)
+
+
+class TestHotsetPolicy:
+    """The native tier's policy is the reference's TierManager.hotset_update
+    (ref/tiering.py:222-262); these mirror ref tests/test_tiering.py:51-104."""
+
+    def test_zero_budget_empty(self):
+        st, ix, tier = _tier(0)
+        st.clusters[0] = _FakeCluster(0, 1)
+        tier.record_access(0)
+        tier.hotset_update()
+        assert tier.hotset == set() and ix.res == {}
+
+    def test_single_cluster_admitted(self):
+        st, ix, tier = _tier(1 << 30)
+        st.clusters[0] = _FakeCluster(0, 1)
+        tier.record_access(0)
+        assert tier.hotset_update() == [("admit", 0)]
+        assert tier.hotset == {0} and ix.res == {0: True}
+        assert st.clusters[0].resident is not None
+
+    def test_budget_invariant(self):
+        st, ix, tier = _tier(10 * 8 * 4 * 3)  # room for three 10-vector clusters
+        for g in range(6):
+            st.clusters[g] = _FakeCluster(g, 10)
+            for _ in range(g + 1):
+                tier.record_access(g)
+        tier.hotset_update()
+        assert sum(st.clusters[c].nbytes for c in tier.hotset) <= tier.budget_bytes
+        assert tier.hotset == {5, 4, 3}  # hottest first, greedy under the budget
+
+    def test_hysteresis_and_eviction(self):
+        st, ix, tier = _tier(8 * 4 * 10)  # room for one 10-vector cluster
+        st.clusters[0] = _FakeCluster(0, 10)
+        st.clusters[1] = _FakeCluster(1, 10)
+        for _ in range(10):
+            tier.record_access(0)
+        tier.hotset_update()
+        assert tier.hotset == {0}
+        for _ in range(11):  # 1 is hotter, but not by the 1.2 hysteresis factor:
+            tier.record_access(1)  # 0 is retained next to it (ref/tiering.py:244-252)
+        assert tier.hotset_update() == [("admit", 1)]
+        assert tier.hotset == {0, 1}
+        for _ in range(20):
+            tier.record_access(1)  # no new displacer: 0 falls out of the target
+        assert tier.hotset_update() == [("evict", 0)]
+        assert tier.hotset == {1} and ix.res == {0: False, 1: True}
+
+    def test_zipf_hit_rate_near_offline_oracle(self):
+        rng = np.random.default_rng(0)
+        st, ix, tier = _tier(8 * 8 * 4 * 100)
+        for i in range(1000):
+            st.clusters[i] = _FakeCluster(i, 1, 8)
+        zipf = 1.0 / np.arange(1, 1001)
+        zipf /= zipf.sum()
+        trace = rng.choice(1000, size=20000, p=zipf)
+        hits = 0
+        for t, cid in enumerate(trace.tolist()):
+            hits += cid in tier.hotset
+            tier.record_access(cid)
+            if t % 200 == 0:
+                tier.hotset_update()
+        counts = np.bincount(trace, minlength=1000)
+        oracle = counts[np.argsort(-counts)[:100]].sum()
+        assert hits / len(trace) >= oracle / len(trace) - 0.05
