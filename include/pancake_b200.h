@@ -77,6 +77,11 @@ int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* r
  * (tiering.py:280-290): append rows in place (relocating when full). */
 int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* ids, int64_t n,
                    int flags);
+/* A whole insert batch (engine.py:571-605 after assignment): row i (host
+ * f32[d]) appended to list cids[i] in batch order, one H2D copy and one
+ * scatter kernel for all lists (host pointers). */
+int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const float* rows,
+                         const int64_t* ids);
 /* Cluster.remove (clusters.py:81-109): swap-with-last compaction of `row`. */
 int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row);
 /* ClusterStore.retire_cluster (clusters.py:352-362). */

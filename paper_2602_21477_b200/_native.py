@@ -50,6 +50,7 @@ _SIGS = [
     ("pk_index_bytes", [_vp, _i64p], _int),
     ("pk_list_create", [_vp, _i64, _i32, _vp, _vp, _i64, _vp, _int], _int),
     ("pk_list_append", [_vp, _i64, _vp, _vp, _i64, _int], _int),
+    ("pk_list_append_batch", [_vp, _i64, _vp, _vp, _vp], _int),
     ("pk_list_remove_row", [_vp, _i64, _i64], _int),
     ("pk_list_retire", [_vp, _i64], _int),
     ("pk_list_recompute", [_vp, _i64, _vp], _int),

@@ -932,6 +932,88 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
   return PK_OK;
 }
 
+int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const float* rows,
+                         const int64_t* ids) {
+  if (n <= 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  // pre-pass: slots, per-slot counts, capacity (one relocation per list at most)
+  std::vector<int32_t> slot(n);
+  std::unordered_map<int32_t, int64_t> add;
+  for (int64_t i = 0; i < n; i++) {
+    RET(ix->slot_of(cids[i], &slot[i]));
+    if (ix->h_remote[slot[i]])
+      return fail(PK_ERR_USAGE, "cluster %lld is owned by another shard", (long long)cids[i]);
+    add[slot[i]] += 1;
+  }
+  for (auto& kv : add) {
+    const int32_t s = kv.first;
+    const int64_t len = ix->h_len[s], m = kv.second;
+    if (ix->tiered) {
+      RET(ix->finish_migration(s, true));
+      if (len + m > ix->h_hcap[s]) {
+        const int64_t ncap = std::max<int64_t>(len + m, ix->h_hcap[s] + ix->h_hcap[s] / 2) + 16;
+        int64_t noff;
+        RET(ix->host_alloc(ncap, &noff));
+        memcpy(ix->hrows + noff * ix->dp, ix->hrows + ix->h_hoff[s] * ix->dp, (size_t)len * ix->dp * 4);
+        memcpy(ix->hids + noff, ix->hids + ix->h_hoff[s], (size_t)len * 8);
+        ix->host_free(ix->h_hoff[s], ix->h_hcap[s]);
+        ix->h_hoff[s] = noff;
+        ix->h_hcap[s] = ncap;
+      }
+    }
+    if (ix->h_res[s] && len + m > ix->h_cap[s]) {
+      const int64_t ncap = std::max<int64_t>(len + m, ix->h_cap[s] + ix->h_cap[s] / 2) + 16;
+      int64_t noff;
+      RET(ix->alloc_range(ncap, &noff));
+      const int64_t ooff = ix->h_off[s];
+      if (len > 0) {
+        CK(cudaMemcpyAsync(ix->rows + noff * ix->dp, ix->rows + ooff * ix->dp,
+                           (size_t)len * ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
+        CK(cudaMemcpyAsync(ix->ids + noff, ix->ids + ooff, (size_t)len * 8,
+                           cudaMemcpyDeviceToDevice, ix->st));
+        CK(cudaMemcpyAsync(ix->nrm + noff, ix->nrm + ooff, (size_t)len * 4,
+                           cudaMemcpyDeviceToDevice, ix->st));
+      }
+      ix->free_range(ooff, ix->h_cap[s]);
+      ix->h_off[s] = noff;
+      ix->h_cap[s] = ncap;
+    }
+  }
+  // placement in batch order; host copies now, device rows by one scatter
+  std::vector<int64_t> dst;
+  std::vector<int64_t> pick;
+  for (int64_t i = 0; i < n; i++) {
+    const int32_t s = slot[i];
+    const int64_t pos = ix->h_len[s]++;
+    if (ix->tiered) RET(ix->host_put(ix->h_hoff[s] + pos, rows + i * ix->d, ids + i, 1, false));
+    if (ix->h_res[s]) {
+      dst.push_back(ix->h_off[s] + pos);
+      pick.push_back(i);
+    }
+    ix->mark(s);
+  }
+  const int64_t m = (int64_t)dst.size();
+  if (m > 0) {
+    std::vector<float> stage((size_t)m * ix->dp, 0.f);
+    std::vector<int64_t> sid(m);
+    for (int64_t j = 0; j < m; j++) {
+      memcpy(stage.data() + j * ix->dp, rows + pick[j] * ix->d, ix->d * 4);
+      sid[j] = ids[pick[j]];
+    }
+    RET(ix->tmp_rows.ensure((size_t)m * ix->dp * 4 + (size_t)m * 16));
+    float* d_src = ix->tmp_rows.as<float>();
+    int64_t* d_ids = reinterpret_cast<int64_t*>(d_src + m * ix->dp);
+    int64_t* d_dst = d_ids + m;
+    CK(cudaMemcpyAsync(d_src, stage.data(), (size_t)m * ix->dp * 4, cudaMemcpyHostToDevice, ix->st));
+    CK(cudaMemcpyAsync(d_ids, sid.data(), (size_t)m * 8, cudaMemcpyHostToDevice, ix->st));
+    CK(cudaMemcpyAsync(d_dst, dst.data(), (size_t)m * 8, cudaMemcpyHostToDevice, ix->st));
+    launch_append_rows(d_src, d_ids, d_dst, (int)m, ix->rows, ix->ids, ix->nrm, (int)ix->dp, ix->st);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ix->st));  // host staging vectors go out of scope
+  }
+  return PK_OK;
+}
+
 int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
   CK(cudaSetDevice(ix->device));
   int32_t s;

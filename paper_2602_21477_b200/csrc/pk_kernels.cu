@@ -2674,3 +2674,44 @@ void launch_gather_rows(const StageCopy* desc, int ndesc, const float* hrows, co
 }
 
 }  // namespace pk
+
+namespace pk {
+
+// Batched in-place append (Cluster.add, ref/clusters.py:71-79, for a whole
+// insert batch): row i of the padded staging block goes to arena row
+// dst_row[i], with its id and squared norm.  One warp per row.
+__global__ void __launch_bounds__(256) append_rows_kernel(const float* __restrict__ src,
+                                                          const int64_t* __restrict__ src_ids,
+                                                          const int64_t* __restrict__ dst_row, int n,
+                                                          float* __restrict__ rows,
+                                                          int64_t* __restrict__ ids,
+                                                          float* __restrict__ nrm, int dp) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const int64_t r = dst_row[i];
+  const float4* s4 = reinterpret_cast<const float4*>(src + (int64_t)i * dp);
+  float4* d4 = reinterpret_cast<float4*>(rows + r * dp);
+  float acc = 0.f;
+  for (int j = lane; j < dp / 4; j += 32) {
+    const float4 v = s4[j];
+    d4[j] = v;
+    acc = __fmaf_rn(v.x, v.x, acc);
+    acc = __fmaf_rn(v.y, v.y, acc);
+    acc = __fmaf_rn(v.z, v.z, acc);
+    acc = __fmaf_rn(v.w, v.w, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+  if (lane == 0) {
+    nrm[r] = acc;
+    ids[r] = src_ids[i];
+  }
+}
+void launch_append_rows(const float* src, const int64_t* src_ids, const int64_t* dst_row, int n,
+                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st) {
+  if (n <= 0) return;
+  append_rows_kernel<<<(n + 7) / 8, 256, 0, st>>>(src, src_ids, dst_row, n, rows, ids, nrm, dp);
+}
+
+}  // namespace pk

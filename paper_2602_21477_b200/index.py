@@ -49,6 +49,7 @@ class DeviceIndex:
         N.check(N.lib().pk_index_create(self.dimension, self.metric_code, self.device,
                                         int(reserve_rows), int(reserve_lists), ctypes.byref(h)))
         self._h = h
+        self._pend: list = []  # queued appends (flushed before any other operation)
 
     @property
     def handle(self):
@@ -56,6 +57,7 @@ class DeviceIndex:
 
     def close(self):
         if self._h is not None and self._h.value:
+            self.flush()
             N.lib().pk_index_destroy(self._h)
         self._h = None
 
@@ -66,15 +68,18 @@ class DeviceIndex:
             pass
 
     def sync(self):
+        self.flush()
         N.check(N.lib().pk_sync(self._h))
 
     def nbytes(self) -> int:
+        self.flush()
         v = ctypes.c_int64(0)
         N.check(N.lib().pk_index_bytes(self._h, ctypes.byref(v)))
         return int(v.value)
 
     # ---- posting lists -------------------------------------------------
     def create_list(self, cid: int, scope_code: int, rows, ids) -> np.ndarray:
+        self.flush()
         if _is_device_tensor(rows):
             return self.create_list_device(cid, scope_code, rows, ids)
         rows = N.f32(rows, self.dimension)
@@ -86,6 +91,7 @@ class DeviceIndex:
 
     def create_list_device(self, cid: int, scope_code: int, rows, ids) -> np.ndarray:
         """rows/ids are device tensors ([n, d] f32 contiguous, [n] i64)."""
+        self.flush()
         cent = np.empty(self.dimension, dtype=np.float32)
         N.check(N.lib().pk_list_create(self._h, int(cid), int(scope_code), N.ptr(rows), N.ptr(ids),
                                        int(ids.shape[0]), N.ptr(cent), N.PK_DEVICE_PTRS))
@@ -122,32 +128,51 @@ class DeviceIndex:
         return out
 
     def append(self, cid: int, rows, ids):
+        """Cluster.add (ref/clusters.py:71-79).  Appends are queued and sent as
+        one pk_list_append_batch call (one H2D copy, one scatter kernel)
+        before the next operation that reads the index; a usage error (e.g.
+        a remote list) surfaces at that flush and leaves the index unchanged."""
         rows = N.f32(rows, self.dimension)
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         if len(ids):
-            N.check(N.lib().pk_list_append(self._h, int(cid), N.ptr(rows), N.ptr(ids), len(ids), 0))
+            self._pend.append((int(cid), rows, ids))
+
+    def flush(self):
+        if not self._pend:
+            return
+        pend, self._pend = self._pend, []
+        cids = np.concatenate([np.full(len(i), c, dtype=np.int64) for c, _, i in pend])
+        rows = np.ascontiguousarray(np.concatenate([r for _, r, _ in pend]))
+        ids = np.ascontiguousarray(np.concatenate([i for _, _, i in pend]))
+        N.check(N.lib().pk_list_append_batch(self._h, len(ids), N.ptr(cids), N.ptr(rows), N.ptr(ids)))
 
     def remove_row(self, cid: int, row: int):
+        self.flush()
         N.check(N.lib().pk_list_remove_row(self._h, int(cid), int(row)))
 
     def retire(self, cid: int):
+        self.flush()
         N.check(N.lib().pk_list_retire(self._h, int(cid)))
 
     def recompute(self, cid: int) -> np.ndarray:
+        self.flush()
         cent = np.empty(self.dimension, dtype=np.float32)
         N.check(N.lib().pk_list_recompute(self._h, int(cid), N.ptr(cent)))
         return cent
 
     def set_centroid(self, cid: int, centroid):
+        self.flush()
         c = N.f32(centroid).reshape(-1)
         N.check(N.lib().pk_list_set_centroid(self._h, int(cid), N.ptr(c)))
 
     def size(self, cid: int) -> int:
+        self.flush()
         v = ctypes.c_int64(0)
         N.check(N.lib().pk_list_size(self._h, int(cid), ctypes.byref(v)))
         return int(v.value)
 
     def read(self, cid: int):
+        self.flush()
         n = self.size(cid)
         rows = np.empty((n, self.dimension), dtype=np.float32)
         ids = np.empty(n, dtype=np.int64)
@@ -157,6 +182,7 @@ class DeviceIndex:
     # ---- hot path ------------------------------------------------------
     def search(self, Q, scope_codes, nprobe: int, kk: int, want_probe: bool = False,
                want_scanned: bool = True) -> SearchOutput:
+        self.flush()
         Q = N.f32(Q, self.dimension)
         B = Q.shape[0]
         codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
@@ -175,6 +201,7 @@ class DeviceIndex:
                       out_n, out_scanned=None):
         """Device-pointer variant (torch tensors on this device); async on the
         index stream."""
+        self.flush()
         N.check(N.lib().pk_search(self._h, N.ptr(Q), Q.shape[0], N.ptr(scope_codes),
                                   scope_codes.shape[0], int(nprobe), int(kk), N.ptr(out_ids),
                                   N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), None,
@@ -188,18 +215,22 @@ class DeviceIndex:
     def enable_tier(self, reserve_rows: int = 0):
         """Cold tier on: lists live in pinned host memory, HBM holds the
         resident ones (call before creating lists)."""
+        self.flush()
         N.check(N.lib().pk_index_enable_tier(self._h, int(reserve_rows)))
 
     def set_resident(self, cid: int, resident: bool):
+        self.flush()
         N.check(N.lib().pk_list_set_resident(self._h, int(cid), 1 if resident else 0))
 
     def residency(self, cid: int) -> int:
         """0 cold, 1 HBM-resident, 2 admission in flight."""
+        self.flush()
         v = ctypes.c_int(0)
         N.check(N.lib().pk_list_residency(self._h, int(cid), ctypes.byref(v)))
         return int(v.value)
 
     def tier_stats(self) -> dict:
+        self.flush()
         out = np.zeros(len(self.TIER_STATS), dtype=np.int64)
         N.check(N.lib().pk_tier_stats(self._h, N.ptr(out), len(out)))
         return dict(zip(self.TIER_STATS, out.tolist()))
@@ -208,6 +239,7 @@ class DeviceIndex:
     def add_remote_list(self, cid: int, scope_code: int, centroid):
         """A list owned by another rank: centroid only (joins the coarse
         quantizer, holds no rows here)."""
+        self.flush()
         c = N.f32(centroid).reshape(-1)
         if c.shape[0] != self.dimension:
             raise N.UsageError("centroid dimension mismatch")
@@ -215,6 +247,7 @@ class DeviceIndex:
 
     def search_block(self, Q, scope_codes, nprobe: int, kk: int) -> np.ndarray:
         """Local search written as one shard result block (host uint8)."""
+        self.flush()
         from .sharded import block_views
 
         Q = N.f32(Q, self.dimension)
@@ -230,6 +263,7 @@ class DeviceIndex:
     def search_block_device(self, Q, scope_codes, nprobe: int, kk: int, block):
         """Device variant: Q [B, d] f32 and block (uint8, block_bytes(B, kk))
         are tensors on this device; async on the index stream."""
+        self.flush()
         from .sharded import block_offsets
 
         B = int(Q.shape[0])
@@ -256,6 +290,7 @@ class DeviceIndex:
 
     def search_coarse(self, Q, scope_codes, nprobe: int) -> np.ndarray:
         """Coarse stage only: list handles int32[B, nprobe] (-1 padded)."""
+        self.flush()
         Q = N.f32(Q, self.dimension)
         B = Q.shape[0]
         codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
@@ -266,6 +301,7 @@ class DeviceIndex:
 
     def search_probed(self, Q, probe, kk: int, group: int) -> np.ndarray:
         """Scan stage only for given handles; B / group shard blocks (host)."""
+        self.flush()
         Q = N.f32(Q, self.dimension)
         probe = np.ascontiguousarray(probe, dtype=np.int32)
         B, nprobe = probe.shape
@@ -275,11 +311,13 @@ class DeviceIndex:
         return out
 
     def search_coarse_device(self, Q, scope_codes, nprobe: int, out_probe):
+        self.flush()
         N.check(N.lib().pk_search_coarse(self._h, N.ptr(Q), int(Q.shape[0]), N.ptr(scope_codes),
                                          int(scope_codes.shape[0]), int(nprobe), N.ptr(out_probe),
                                          N.PK_DEVICE_PTRS))
 
     def search_probed_device(self, Q, probe, kk: int, group: int, out_blocks):
+        self.flush()
         N.check(N.lib().pk_search_probed(self._h, N.ptr(Q), int(Q.shape[0]), N.ptr(probe),
                                          int(probe.shape[1]), int(kk), int(group),
                                          N.ptr(out_blocks), N.PK_DEVICE_PTRS))
@@ -303,6 +341,7 @@ class DeviceIndex:
                                         N.ptr(out_scanned), N.PK_DEVICE_PTRS))
 
     def assign(self, X, scope_code: int):
+        self.flush()
         X = N.f32(X, self.dimension)
         n = X.shape[0]
         cid = np.empty(n, dtype=np.int64)

@@ -76,8 +76,9 @@ def test_remote_list_rejects_append():
 
     ix = DeviceIndex(16)
     ix.add_remote_list(5, 0, np.ones(16, np.float32))
-    with pytest.raises(UsageError):
+    with pytest.raises(UsageError):  # appends are queued: the error surfaces at the flush
         ix.append(5, np.ones((1, 16), np.float32), [1])
+        ix.flush()
     assert ix.size(5) == 0
     ix.retire(5)
     ix.close()
