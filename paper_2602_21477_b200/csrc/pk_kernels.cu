@@ -2673,6 +2673,33 @@ void launch_gather_rows(const StageCopy* desc, int ndesc, const float* hrows, co
   gather_rows_kernel<<<ndesc, 256, 0, st>>>(desc, hrows, hids, rows, ids, nrm, dp);
 }
 
+// Squared norms of the staged rows after a DMA (copy-engine) staging pass.
+__global__ void __launch_bounds__(256) stage_norms_kernel(const StageCopy* __restrict__ desc,
+                                                          const float* __restrict__ rows,
+                                                          float* __restrict__ nrm, int dp) {
+  const StageCopy c = desc[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int r = warp; r < c.n; r += 8) {
+    const float4* x = reinterpret_cast<const float4*>(rows + (c.dst_row + r) * (int64_t)dp);
+    float acc = 0.f;
+    for (int j = lane; j < dp / 4; j += 32) {
+      const float4 v = x[j];
+      acc = __fmaf_rn(v.x, v.x, acc);
+      acc = __fmaf_rn(v.y, v.y, acc);
+      acc = __fmaf_rn(v.z, v.z, acc);
+      acc = __fmaf_rn(v.w, v.w, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
+    if (lane == 0) nrm[c.dst_row + r] = acc;
+  }
+}
+void launch_stage_norms(const StageCopy* desc, int ndesc, const float* rows, float* nrm, int dp,
+                        cudaStream_t st) {
+  if (ndesc <= 0) return;
+  stage_norms_kernel<<<ndesc, 256, 0, st>>>(desc, rows, nrm, dp);
+}
+
 }  // namespace pk
 
 namespace pk {
