@@ -2742,3 +2742,52 @@ void launch_append_rows(const float* src, const int64_t* src_ids, const int64_t*
 }
 
 }  // namespace pk
+
+namespace pk {
+
+// =====================================================================
+// Per-list exact distances for one query (agent-mode L2 scan with early
+// termination, ref/engine.py:377-396): rows of m lists -- HBM arena ranges
+// or, for cold lists, the device-mapped host arena -- concatenated in probe
+// order, one thread per row, reference arithmetic over the true dimension.
+// =====================================================================
+template <int METRIC>
+__global__ void lists_dist_kernel(const float* __restrict__ q, float qn, const ListSrc* __restrict__ src,
+                                  const int64_t* __restrict__ prefix, int m, int dp, int d,
+                                  float* __restrict__ out_d, int64_t* __restrict__ out_ids) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t total = prefix[m];
+  if (r >= total) return;
+  int lo = 0, hi = m - 1;  // list holding row r
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  const int64_t i = r - prefix[lo];
+  const float* x = src[lo].rows + i * dp;
+  float acc = 0.f, nn = 0.f;
+  for (int j = 0; j < d; j++) {
+    const float xv = x[j], qv = q[j];
+    if (METRIC == SQ_L2) {
+      acc = sq_step(acc, xv, qv);
+    } else {
+      acc = ip_step(acc, xv, qv);
+      if (METRIC == COSINE) nn = ip_step(nn, xv, xv);
+    }
+  }
+  out_d[r] = finalize<METRIC>(acc, nn, qn);
+  out_ids[r] = src[lo].ids[i];
+}
+
+void launch_lists_dist(int metric, const float* q, float qn, const ListSrc* src, const int64_t* prefix,
+                       int m, int64_t total, int dp, int d, float* out_d, int64_t* out_ids,
+                       cudaStream_t st) {
+  if (total <= 0 || m <= 0) return;
+  const unsigned grid = (unsigned)((total + 127) / 128);
+  if (metric == SQ_L2) lists_dist_kernel<SQ_L2><<<grid, 128, 0, st>>>(q, qn, src, prefix, m, dp, d, out_d, out_ids);
+  else if (metric == IP) lists_dist_kernel<IP><<<grid, 128, 0, st>>>(q, qn, src, prefix, m, dp, d, out_d, out_ids);
+  else lists_dist_kernel<COSINE><<<grid, 128, 0, st>>>(q, qn, src, prefix, m, dp, d, out_d, out_ids);
+}
+
+}  // namespace pk
