@@ -116,6 +116,20 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags);
 
+/* ---- agent-mode L2 scan (engine.py:366-396) ------------------------------
+ * pk_search_coarse_cids: the coarse stage for B queries, probed list ids
+ *   (host i64 [B][nprobe], -1 padded) in coarse order.
+ * pk_scan_lists: one query's reference-arithmetic distances to every row of the
+ *   lists cids[0..m) (resident in HBM or cold in the host arena), concatenated
+ *   in the given order; list l's rows are out rows [out_prefix[l],
+ *   out_prefix[l+1]) (out_prefix: host i64[m+1], out_ids / out_dists sized by
+ *   the lists' total length).  The caller replays the per-list early
+ *   termination on these values (MultiLevelCache._kth). */
+int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                          int32_t nscopes, int32_t nprobe, int64_t* out_cids);
+int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, int64_t* out_ids,
+                  float* out_dists, int64_t* out_prefix);
+
 /* ---- cold tier (TierManager, tiering.py:175-448) --
  * pk_index_enable_tier (before any list exists): every list keeps a copy in
  * a pinned, device-mapped host arena (the source of truth, tiering.py:9-12);

@@ -70,6 +70,8 @@ _SIGS = [
     ("pk_list_set_resident", [_vp, _i64, _int], _int),
     ("pk_list_residency", [_vp, _i64, ctypes.POINTER(_int)], _int),
     ("pk_tier_stats", [_vp, _vp, _int], _int),
+    ("pk_search_coarse_cids", [_vp, _vp, _i64, _vp, _i32, _i32, _vp], _int),
+    ("pk_scan_lists", [_vp, _vp, _vp, _i32, _vp, _vp, _vp], _int),
     ("pk_list_add_remote", [_vp, _i64, _i32, _vp], _int),
     ("pk_shard_block_bytes", [_i64, _i32], _i64),
     ("pk_merge_shards", [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _int], _int),

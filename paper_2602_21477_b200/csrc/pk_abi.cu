@@ -147,7 +147,7 @@ struct pk_index {
   DevBuf ncand;
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
-  DevBuf shard_in, shard_out, pb, pb_out, nsurv;
+  DevBuf shard_in, shard_out, pb, pb_out, nsurv, sl_buf;
 
   // ---- cold tier (pk_index_enable_tier).  Every list keeps a copy in a
   // pinned, device-mapped host arena -- the source of truth, as the
@@ -753,7 +753,7 @@ int pk_index_destroy(pk_index* ix) {
                     &ix->items, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list,
                     &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->nsurv, &ix->ncand, &ix->qhi, &ix->qlo})
+                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->nsurv, &ix->sl_buf, &ix->ncand, &ix->qhi, &ix->qlo})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -1487,6 +1487,63 @@ int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* pro
     CK(cudaMemcpyAsync(out_blocks, dst, (size_t)(B / group) * bb, cudaMemcpyDeviceToHost, ix->st));
     CK(cudaStreamSynchronize(ix->st));
   }
+  return PK_OK;
+}
+
+int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                          int32_t nscopes, int32_t nprobe, int64_t* out_cids) {
+  if (!out_cids) return fail(PK_ERR_USAGE, "out_cids is required");
+  std::vector<int32_t> pr((size_t)std::max<int64_t>(B, 0) * std::max(nprobe, 1));
+  RET(search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, nullptr, false, false, nullptr, pr.data()));
+  for (size_t i = 0; i < (size_t)B * nprobe; i++) out_cids[i] = pr[i] >= 0 ? ix->h_cid[pr[i]] : -1;
+  return PK_OK;
+}
+
+int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, int64_t* out_ids,
+                  float* out_dists, int64_t* out_prefix) {
+  if (m < 0) return fail(PK_ERR_USAGE, "negative list count");
+  out_prefix[0] = 0;
+  if (m == 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  cudaStream_t st = ix->st;
+  if (ix->tiered) RET(ix->poll_migrations());
+  std::vector<ListSrc> src(m);
+  for (int32_t l = 0; l < m; l++) {
+    int32_t s;
+    RET(ix->slot_of(cids[l], &s));
+    out_prefix[l + 1] = out_prefix[l] + ix->h_len[s];
+    if (!ix->tiered || ix->h_res[s]) {
+      src[l].rows = ix->rows + ix->h_off[s] * ix->dp;
+      src[l].ids = ix->ids + ix->h_off[s];
+    } else {  // cold list: read in place from the mapped host arena
+      src[l].rows = ix->hrows_d + ix->h_hoff[s] * ix->dp;
+      src[l].ids = ix->hids_d + ix->h_hoff[s];
+    }
+  }
+  const int64_t total = out_prefix[m];
+  const int64_t dp = ix->dp;
+  RET(ix->sl_buf.ensure((size_t)dp * 4 + (size_t)m * sizeof(ListSrc) + (size_t)(m + 1) * 8 +
+                        (size_t)std::max<int64_t>(total, 1) * 12 + 128));
+  uint8_t* base = ix->sl_buf.as<uint8_t>();
+  float* d_q = reinterpret_cast<float*>(base);
+  ListSrc* d_src = reinterpret_cast<ListSrc*>(base + round_up(dp * 4, 16));
+  int64_t* d_pre = reinterpret_cast<int64_t*>(reinterpret_cast<uint8_t*>(d_src) + round_up(m * sizeof(ListSrc), 16));
+  int64_t* d_ids = d_pre + (m + 1);
+  float* d_d = reinterpret_cast<float*>(d_ids + std::max<int64_t>(total, 1));
+  CK(cudaMemsetAsync(d_q, 0, dp * 4, st));
+  CK(cudaMemcpyAsync(d_q, q, ix->d * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_src, src.data(), m * sizeof(ListSrc), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_pre, out_prefix, (m + 1) * 8, cudaMemcpyHostToDevice, st));
+  float* d_qn = d_d + std::max<int64_t>(total, 1);  // |q| for cosine (qnorm_kernel, sequential fp32)
+  if (ix->metric == COSINE) launch_qnorm(d_q, dp, 1, (int)ix->d, d_qn, st);
+  launch_lists_dist(ix->metric, d_q, d_qn, d_src, d_pre, m, total, (int)dp, (int)ix->d, d_d, d_ids, st);
+  CK(cudaGetLastError());
+  if (total > 0) {
+    CK(cudaMemcpyAsync(out_ids, d_ids, total * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(out_dists, d_d, total * 4, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
   return PK_OK;
 }
 

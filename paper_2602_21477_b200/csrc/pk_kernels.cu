@@ -2752,7 +2752,7 @@ namespace pk {
 // order, one thread per row, reference arithmetic over the true dimension.
 // =====================================================================
 template <int METRIC>
-__global__ void lists_dist_kernel(const float* __restrict__ q, float qn, const ListSrc* __restrict__ src,
+__global__ void lists_dist_kernel(const float* __restrict__ q, const float* __restrict__ qn_p, const ListSrc* __restrict__ src,
                                   const int64_t* __restrict__ prefix, int m, int dp, int d,
                                   float* __restrict__ out_d, int64_t* __restrict__ out_ids) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -2776,11 +2776,11 @@ __global__ void lists_dist_kernel(const float* __restrict__ q, float qn, const L
       if (METRIC == COSINE) nn = ip_step(nn, xv, xv);
     }
   }
-  out_d[r] = finalize<METRIC>(acc, nn, qn);
+  out_d[r] = finalize<METRIC>(acc, nn, METRIC == COSINE ? *qn_p : 0.f);
   out_ids[r] = src[lo].ids[i];
 }
 
-void launch_lists_dist(int metric, const float* q, float qn, const ListSrc* src, const int64_t* prefix,
+void launch_lists_dist(int metric, const float* q, const float* qn, const ListSrc* src, const int64_t* prefix,
                        int m, int64_t total, int dp, int d, float* out_d, int64_t* out_ids,
                        cudaStream_t st) {
   if (total <= 0 || m <= 0) return;

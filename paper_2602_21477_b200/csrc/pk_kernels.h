@@ -179,12 +179,12 @@ void launch_append_rows(const float* src, const int64_t* src_ids, const int64_t*
 
 // Per-list exact distances of one query (agent-mode L2 scan): list l's rows
 // at src[l].rows ([n][dp], HBM or mapped host), ids at src[l].ids; rows of
-// list l are out rows [prefix[l], prefix[l+1]).  qn = |q| (cosine only).
+// list l are out rows [prefix[l], prefix[l+1]).  *qn = |q| (device; cosine only).
 struct ListSrc {
   const float* rows;
   const int64_t* ids;
 };
-void launch_lists_dist(int metric, const float* q, float qn, const ListSrc* src, const int64_t* prefix,
+void launch_lists_dist(int metric, const float* q, const float* qn, const ListSrc* src, const int64_t* prefix,
                        int m, int64_t total, int dp, int d, float* out_d, int64_t* out_ids,
                        cudaStream_t st);
 

@@ -9,11 +9,13 @@ kernels over a device-resident index (``DeviceIndex``), and batches of
 queries are answered by ONE device pass (``search_batch`` / ``submit_batch``)
 instead of one Python loop iteration per (query, cluster).
 
-Scope of this build: the bare IVF path -- ``agent=None`` or
-``cache_enabled=False``.  The per-agent multi-level cache, FSM pattern hints
-and prefetch (ref/cache.py, ref/fsm.py) are not part of it; a store
-configured with ``cache_enabled=True`` rejects agent-scoped operations with
-NotImplementedError instead of silently answering differently.
+Two read paths: a batch of bare queries (``agent=None``, or an agent
+without a cache, and no staged items in scope) is ONE device pass
+(coarse on tcgen05, screened scan, exact re-rank); an agent query with its
+multi-level cache (ref/cache.py), staged items (ref/engine.py:353-363) or
+early termination (ref/engine.py:376-396) runs the reference's per-query
+pipeline with every distance on the device -- the cache pools in one call,
+the probed lists in one call -- and the stop rules replayed on those values.
 """
 
 from __future__ import annotations
@@ -27,7 +29,10 @@ import numpy as np
 
 from . import _native as N
 from . import pnck
+from .cache import DEFAULT_KEY, MultiLevelCache, kth_smallest
 from .clusters import ClusterStore, SplitOutcome, kmeans_split_points
+from .fsm import PatternHint, PatternTable
+from .kernels import batch_distances
 from .concurrency import RWLock, TaskRunner
 from .core import (
     STATIC_SCOPE,
@@ -204,6 +209,9 @@ class Store:
                                 b_insert=cfg.b_insert, decay_half_life=cfg.decay_half_life,
                                 slack_fraction=cfg.slack_fraction, native=native_tier)
         self.agents: set[str] = set()
+        self.caches: dict[str, MultiLevelCache] = {}
+        self.patterns: dict[str, PatternTable] = {}
+        self._prefetch_inflight: set = set()
         self.sequences: dict[str, list[np.ndarray]] = {}
         self.payloads: dict[int, bytes] = {}
         self._next_item_id = 0
@@ -236,6 +244,14 @@ class Store:
         self.clusters.register_scope(agent_id)
         self.scope_codes.intern(agent_id)
         self.agents.add(agent_id)
+        c = self.cfg
+        self.caches[agent_id] = MultiLevelCache(
+            agent_id, c.dimension, self.metric, self.scope_codes, n_p=c.n_p,
+            l0_capacity=c.l0_capacity, l1_capacity=c.l1_capacity, kappa=c.kappa,
+            alpha_et=c.alpha_et, window_w=c.window_w, verify_mode=c.verify_mode)
+        self.patterns[agent_id] = PatternTable(n_p=c.n_p, n_s=c.n_s, metric=self.metric,
+                                               theta_match=c.theta_match,
+                                               d_merge_factor=c.d_merge_factor)
         self.sequences[agent_id] = []
         self._agent_locks[agent_id] = threading.RLock()
         return agent_id
@@ -244,11 +260,14 @@ class Store:
         if agent_id not in self.agents:
             raise UsageError(f"unknown agent {agent_id!r}")
         for cid in list(self.clusters.scope_clusters(agent_id)):
+            self.tier._evict(cid)
             self.clusters.retire_cluster(cid)
         for item_id in list(self.clusters.staged.get(agent_id, {})):
             self.clusters.unstage(agent_id, item_id)
             self.payloads.pop(item_id, None)
         self.agents.discard(agent_id)
+        self.caches.pop(agent_id, None)
+        self.patterns.pop(agent_id, None)
         del self.sequences[agent_id]
         del self._agent_locks[agent_id]
 
@@ -278,11 +297,16 @@ class Store:
             return
         raise ScopePermissionError(f"agent {agent!r} may not write scope {scope!r}")
 
-    def _require_bare(self, agent):
-        if agent is not None and self.cfg.cache_enabled:
-            raise NotImplementedError(
-                "the per-agent multi-level cache path (ref/cache.py) is not part of this build; "
-                "use agent=None or StoreConfig(cache_enabled=False)")
+    def _agent_path(self, agent, scopes, no_cache=False) -> bool:
+        """True when a query needs the per-query agent pipeline: an agent
+        cache in use, pattern hints (prefetch), or staged (cache-owned) items
+        in a searched scope."""
+        if agent is not None and agent in self.caches:
+            if self.cfg.cache_enabled and not no_cache:
+                return True
+            if self.cfg.pattern_enabled:  # hints drive prefetch (ref/engine.py:498-501)
+                return True
+        return any(self.clusters.staged.get(sc) for sc in scopes)
 
     # --- search -----------------------------------------------------------
     def search(self, agent, scopes, q, k: int, nprobe: int | None = None, _internal: bool = False,
@@ -297,16 +321,20 @@ class Store:
         nprobe = nprobe if nprobe is not None else self.cfg.default_nprobe
         if nprobe < 1:
             raise UsageError("nprobe must be >= 1")
-        self._require_bare(agent if not _no_cache else None)
         with self._serialized(agent):
             self._lock.acquire_read()
             try:
-                result = self._search_read_phase_batch(agent, scopes, q[None, :], k, nprobe,
-                                                       want_scan_ids=True)[0]
+                if self._agent_path(agent, scopes, _no_cache):
+                    result, hint, extended = self._search_read_phase(agent, scopes, q, k, nprobe,
+                                                                     _internal, _no_cache)
+                else:
+                    result = self._search_read_phase_batch(agent, scopes, q[None, :], k, nprobe,
+                                                           want_scan_ids=True)[0]
+                    hint, extended = PatternHint(), None
             finally:
                 self._lock.release_read()
             if agent is not None:
-                self._search_side_effects(agent, q, result, _internal)
+                self._search_side_effects(agent, q, k, hint, result, extended, _internal)
             self._tick()
             return result
 
@@ -323,7 +351,8 @@ class Store:
         nprobe = nprobe if nprobe is not None else self.cfg.default_nprobe
         if nprobe < 1:
             raise UsageError("nprobe must be >= 1")
-        self._require_bare(agent)
+        if self._agent_path(agent, scopes):  # per-query pipeline, B calls of search()
+            return [self.search(agent, scopes, Q[b], k, nprobe) for b in range(Q.shape[0])]
         with self._serialized(agent):
             self._lock.acquire_read()
             try:
@@ -332,7 +361,7 @@ class Store:
                 self._lock.release_read()
             for b, res in enumerate(results):
                 if agent is not None:
-                    self._search_side_effects(agent, Q[b], res, False)
+                    self._search_side_effects(agent, Q[b], k, PatternHint(), res, None, False)
                 self._tick()
             return results
 
@@ -344,9 +373,6 @@ class Store:
         if k > N.KKMAX:
             raise UsageError(f"k above {N.KKMAX} is not supported by the device top-k")
         exhaustive_edge = k >= self.clusters.live_count()
-        for sc in scopes:
-            if self.clusters.staged.get(sc):
-                raise NotImplementedError("staged (cache-owned) items need the cache path")
         eff_nprobe = nprobe
         if exhaustive_edge:
             eff_nprobe = max(nprobe, len(self.clusters.clusters) or 1)
@@ -383,8 +409,152 @@ class Store:
             results.append(SearchResult(hits, stats, scan_ids))
         return results
 
-    def _search_side_effects(self, agent, q, result, internal):
-        """ref/engine.py:448-501 without the cache/FSM branches."""
+    def _search_read_phase(self, agent, scopes, q, k, nprobe, internal, no_cache=False):
+        """Store._search_read_phase (ref/engine.py:319-404) for one query:
+        cache levels, staged items, coarse, probed lists with per-list early
+        termination, _topk to max(k, kappa k).  Distances come from the
+        device: the cache pools in one call, the staged rows in one call, every
+        probed list's rows in one call (pk_scan_lists); the stop rules run on
+        those values in the reference's scan order."""
+        exhaustive_edge = k >= self.clusters.live_count()
+        stats = SearchStats()
+        scope_mask = self.scope_codes.mask_codes(scopes)
+        hint = self._hint_for(agent, q) if not internal else PatternHint()
+        id_chunks, dist_chunks, scan_chunks = [], [], []
+        use_cache = self.cfg.cache_enabled and agent and not no_cache
+        cache = self.caches.get(agent) if use_cache else None
+        early = False
+        if cache is not None:
+            cres = cache.cached_search(q, k, scope_mask, hint_keys=hint.predicted_clusters,
+                                       termination_enabled=not exhaustive_edge)
+            if len(cres.ids):
+                id_chunks.append(cres.ids)
+                dist_chunks.append(cres.dists)
+            scan_chunks.extend(cres.scan_ids)
+            stats.scanned_vectors += cres.scanned
+            early = cres.early_terminated
+            stats.level_reached = cres.level_reached
+            stats.early_terminated = early
+        if not early:
+            stats.level_reached = "L2"
+            for sc in sorted(scopes):  # staging areas: items not yet merged into clusters
+                staged = self.clusters.staged.get(sc)
+                if not staged:
+                    continue
+                ids = np.fromiter(staged.keys(), dtype=np.int64, count=len(staged))
+                d = batch_distances(q, np.stack(list(staged.values())), self.metric)
+                id_chunks.append(ids)
+                dist_chunks.append(d)
+                scan_chunks.append(ids)
+                stats.scanned_vectors += len(ids)
+            eff_nprobe = nprobe
+            if exhaustive_edge:
+                eff_nprobe = max(nprobe, len(self.clusters.clusters) or 1)
+            in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
+            stats.coarse_computations = in_scope
+            selected = []
+            if in_scope:
+                dev_nprobe = max(1, min(eff_nprobe, in_scope))
+                if dev_nprobe > N.NPROBE_MAX:
+                    raise UsageError(f"nprobe above {N.NPROBE_MAX} in-scope lists is not supported")
+                codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
+                selected = [int(c) for c in self.index.coarse_cids(q[None, :], codes, dev_nprobe)[0]
+                            if c >= 0]
+            thresh = cache.threshold() if (cache is not None and not exhaustive_edge) else None
+            clusters = self.clusters.clusters
+            total = sum(clusters[c].size for c in selected)
+            all_ids, all_d, pre = self.index.scan_lists(q, selected, total)
+            for li, cid in enumerate(selected):
+                cl = clusters[cid]
+                cl.access_count += 1
+                self.tier.record_access(cid)
+                ids = all_ids[pre[li]:pre[li + 1]]
+                if len(ids):
+                    id_chunks.append(ids)
+                    dist_chunks.append(all_d[pre[li]:pre[li + 1]])
+                stats.scanned_vectors += len(ids)
+                if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
+                    order = profile_reorder(cl.profiles[agent], list(range(cl.size)))
+                    scan_chunks.append(cl.member_ids[order])
+                else:
+                    scan_chunks.append(cl.member_ids.copy())
+                if thresh is not None and len(dist_chunks):
+                    kth = kth_smallest(dist_chunks, k)
+                    if kth is not None and kth < thresh:
+                        early = True
+                        stats.early_terminated = True
+                        break
+        extended = self._topk(id_chunks, dist_chunks, max(k, self.cfg.kappa * k))
+        scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
+        return SearchResult(extended[:k], stats, scan_ids), hint, extended
+
+    def _topk(self, id_chunks, dist_chunks, k):
+        """ref/engine.py:406-426: lexsort by (dist, id), first occurrence per
+        id, owners only (a cached copy of a deleted item is skipped)."""
+        if not id_chunks:
+            return []
+        ids = np.concatenate(id_chunks)
+        dists = np.concatenate(dist_chunks).astype(np.float32)
+        hits, seen = [], set()
+        for idx in np.lexsort((ids, dists)):
+            iid = int(ids[idx])
+            if iid in seen:
+                continue
+            seen.add(iid)
+            owner = self.clusters.owner.get(iid)
+            if owner is None:
+                continue
+            scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
+            hits.append((iid, float(dists[idx]), scope))
+            if len(hits) >= k:
+                break
+        return hits
+
+    def _hint_for(self, agent, q) -> PatternHint:
+        """ref/engine.py:428-435."""
+        if not (agent and self.cfg.pattern_enabled):
+            return PatternHint()
+        cache = self.caches.get(agent)
+        listing = cache.l1_listing() if cache else None
+        prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [q]
+        return self.patterns[agent].match_and_predict(prefix, listing)
+
+    def _state_key_for(self, agent, v):
+        """ref/engine.py:437-446: the matched pattern's aligned state keys L0."""
+        if not self.cfg.pattern_enabled:
+            return DEFAULT_KEY
+        table = self.patterns[agent]
+        prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [v]
+        idx, _ = table.match(prefix)
+        if idx is None:
+            return DEFAULT_KEY
+        return (idx, table.fsms[idx].align(v, self.metric))
+
+    def _cache_items(self, hits):
+        out = []
+        for iid, _, sc in hits:
+            vec = self._vector_of(iid)
+            if vec is not None:
+                out.append((iid, vec, self.scope_codes.intern(sc), False))
+        return out
+
+    def _search_side_effects(self, agent, q, k, hint, result, extended, internal):
+        """ref/engine.py:448-501."""
+        cache = self.caches.get(agent) if self.cfg.cache_enabled else None
+        if cache is not None and result.hits:
+            if extended is None:  # bare pass: the extended list is the kappa k prefix
+                extended = result.hits
+            if not result.stats.early_terminated:
+                if not internal:
+                    cache.record_completed(float(np.mean([h[1] for h in result.hits])))
+            elif cache.verify_mode and not internal:
+                self.runner.submit("search", self._verify_early_return, agent, q, k, result)
+            state_key = self._state_key_for(agent, q)
+            outcomes = cache.promote_to_l0(self._cache_items(result.hits), state_key)
+            outcomes += cache.l1_capture(q, self._cache_items(extended))
+            if any(not o.empty for o in outcomes):
+                with self._lock.write():
+                    self._materialize(agent, outcomes)
         if self.cfg.profiles_enabled:
             by_cluster: dict[int, list[int]] = {}
             for iid, _, _ in result.hits:
@@ -398,11 +568,62 @@ class Store:
                                                      self.cfg.p_size)
         if not internal:
             self._append_sequence(agent, q)
+            if self.cfg.prefetch_enabled and not hint.empty:
+                self.prefetch(agent, hint, k)
+
+    def _verify_early_return(self, agent, q, k, early):
+        """ref/engine.py:503-512: background full search vs an early return."""
+        cache = self.caches[agent]
+        full = self.search(agent, list(self.clusters.by_scope), q, k,
+                           nprobe=max(len(self.clusters.clusters), 1), _internal=True, _no_cache=True)
+        cache.verified_count += 1
+        if early.ids != full.ids:
+            cache.miss_count += 1
+        if full.hits:
+            cache.record_completed(float(np.mean([h[1] for h in full.hits])))
+
+    def prefetch(self, agent, hint, k: int = 5):
+        """ref/engine.py:524-555: repopulate the predicted L0 entry."""
+        if hint.empty or hint.predicted_state is None:
+            return
+        key = hint.predicted_clusters[0] if hint.predicted_clusters else None
+        cache = self.caches.get(agent)
+        if cache is None or key is None or key in cache.l0:
+            return
+        token = (agent, key)
+        if token in self._prefetch_inflight:
+            return
+        self._prefetch_inflight.add(token)
+
+        def run():
+            try:
+                res = self.search(agent, list(self.clusters.by_scope), hint.predicted_state.c, k,
+                                  _internal=True)
+                if res.hits and cache is not None:
+                    self._materialize(agent, cache.promote_to_l0(self._cache_items(res.hits), key))
+            finally:
+                self._prefetch_inflight.discard(token)
+
+        self.runner.submit("cache", run)
+
+    def _materialize(self, agent, outcomes):
+        """ref/engine.py:662-678: merged-down staged items become base clusters."""
+        for outcome in outcomes:
+            for scope_code, items in outcome.staged.items():
+                scope = self.scope_codes.name[scope_code]
+                live = [(iid, vec) for iid, vec in items
+                        if self.clusters.owner.get(iid) == ("staged", scope)]
+                if not live:
+                    continue
+                self.clusters.create_cluster(scope, live)
+                self.clusters.consume_staged(scope, [iid for iid, _ in live])
+                merged = {iid for iid, _ in live}
+                for c in self.caches.values():
+                    c.mark_merged(merged)
 
     # --- mutation ---------------------------------------------------------
     def insert(self, agent, scope: str, vectors, payloads=None, ids=None) -> list[int]:
         """ref/engine.py:557-569."""
-        self._require_bare(agent)
         with self._serialized(agent):
             with self._lock.write():
                 accepted = self._insert_impl(agent, scope, vectors, payloads, ids)
@@ -430,6 +651,7 @@ class Store:
         i = 0
         assigned = None
         assigned_from = -1
+        cache = self.caches.get(agent) if (self.cfg.cache_enabled and agent) else None
         while i < n:
             vec = vecs[i]
             iid = self._take_id(ids[i] if ids is not None else None)
@@ -437,6 +659,16 @@ class Store:
             if isinstance(payload, str):
                 payload = payload.encode("utf-8")
             self.payloads[iid] = payload
+            if cache is not None:  # staged, owned by the agent's cache until merge-down
+                state_key = self._state_key_for(agent, vec)
+                self.clusters.stage_item(scope, iid, vec)
+                self._materialize(agent, cache.promote_to_l0(
+                    [(iid, vec, self.scope_codes.intern(scope), True)], state_key))
+                self._append_sequence(agent, vec)
+                accepted.append(iid)
+                i += 1
+                assigned = None  # a merge-down may have created clusters
+                continue
             cands = self.clusters.by_scope[scope]
             if not cands:
                 self.clusters.create_cluster(scope, [(iid, vec)])
@@ -504,7 +736,6 @@ class Store:
 
     def update(self, agent, item_id: int, vector=None, payload=None) -> bool:
         """ref/engine.py:680-694."""
-        self._require_bare(agent)
         with self._serialized(agent), self._lock.write():
             owner = self.clusters.owner.get(item_id)
             if owner is None:
@@ -521,7 +752,6 @@ class Store:
 
     def delete(self, agent, item_id: int) -> bool:
         """ref/engine.py:696-705."""
-        self._require_bare(agent)
         with self._serialized(agent), self._lock.write():
             owner = self.clusters.owner.get(item_id)
             if owner is None:
@@ -543,12 +773,18 @@ class Store:
                 self.clusters.maintenance(cid)
         else:
             self.clusters.delete_item(item_id)
+        for c in self.caches.values():
+            c.drop_item(item_id)
         self.payloads.pop(item_id, None)
         return True
 
     def end_request(self, agent: str):
+        """ref/engine.py:724-731: fold the finished request into the agent's patterns."""
         if agent not in self.sequences:
             raise UsageError(f"unknown agent {agent!r}")
+        seq = self.sequences[agent]
+        if seq and self.cfg.pattern_enabled:
+            self.patterns[agent].observe_completed(seq)
         self.sequences[agent] = []
 
     def _append_sequence(self, agent: str, v: np.ndarray):
@@ -558,8 +794,10 @@ class Store:
             del seq[0]
 
     def flush_caches(self):
-        """No cache levels on this path: L2 is always complete."""
-        return None
+        """ref/engine.py:739-743: merge every cache level down."""
+        with self._lock.write():
+            for agent, cache in self.caches.items():
+                self._materialize(agent, cache.flush())
 
     def _tick(self, locked: bool = False):
         """ref/engine.py:745-752: the hotset policy runs every hotset_interval

@@ -207,6 +207,30 @@ class DeviceIndex:
                                   N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), None,
                                   N.ptr(out_scanned), N.PK_DEVICE_PTRS))
 
+    # ---- agent-mode L2 scan ---------------------------------------------------
+    def coarse_cids(self, Q, scope_codes, nprobe: int) -> np.ndarray:
+        """Coarse stage only: probed list ids i64[B, nprobe] in coarse order."""
+        self.flush()
+        Q = N.f32(Q, self.dimension)
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        out = np.empty((Q.shape[0], nprobe), dtype=np.int64)
+        N.check(N.lib().pk_search_coarse_cids(self._h, N.ptr(Q), Q.shape[0], N.ptr(codes), len(codes),
+                                              int(nprobe), N.ptr(out)))
+        return out
+
+    def scan_lists(self, q, cids, total: int):
+        """Distances of one query to every row of the lists ``cids`` in that
+        order: (ids i64[total], dists f32[total], prefix i64[m + 1])."""
+        self.flush()
+        q = N.f32(q).reshape(-1)
+        cids = np.ascontiguousarray(cids, dtype=np.int64)
+        ids = np.empty(max(total, 1), dtype=np.int64)
+        dd = np.empty(max(total, 1), dtype=np.float32)
+        pre = np.zeros(len(cids) + 1, dtype=np.int64)
+        N.check(N.lib().pk_scan_lists(self._h, N.ptr(q), N.ptr(cids), len(cids), N.ptr(ids), N.ptr(dd),
+                                      N.ptr(pre)))
+        return ids[:pre[-1]], dd[:pre[-1]], pre
+
     # ---- cold tier (TierManager residency, ref/tiering.py:175-448) --------
     TIER_STATS = ("resident_lists", "cold_lists", "resident_bytes", "staged_lists_last",
                   "staged_bytes_last", "staged_bytes_total", "staged_searches",

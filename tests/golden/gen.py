@@ -181,3 +181,135 @@ def bulk_case(seed=21):
     x[7] = x[3]  # duplicate rows
     qs = unit_sphere(rng, 20, d)
     return x, qs
+
+
+# ---------------------------------------------------------------- agent-mode traces
+AGENT_TRACE_SPECS = {
+    # per-agent caches (small L0 / L1 so evictions, write-backs and merge-downs
+    # happen), staged agent inserts, early termination (short window), FSM
+    # pattern hints, prefetch, profiles, request boundaries, verify mode
+    "agents_small": dict(d=24, n_base=1500, nlist=12, n_agents=2, n_ops=260, seed=31, k=5,
+                         nprobe=3, n_p=4, l0=8, l1=24, window=6, alpha=0.7, verify=False),
+    "agents_verify": dict(d=16, n_base=900, nlist=8, n_agents=3, n_ops=220, seed=32, k=4,
+                          nprobe=2, n_p=3, l0=6, l1=16, window=4, alpha=0.9, verify=True),
+}
+
+
+def agent_trace_ops(spec):
+    """Agent-mode op list: themed agent streams (each agent walks between a few
+    centres, so patterns and cache locality exist), store-level ops mixed in.
+    ops as trace_ops plus ("end_request", agent) and ("flush",)."""
+    d = spec["d"]
+    rng = np.random.default_rng(np.random.PCG64(2000 + spec["seed"]))
+    base = unit_sphere(rng, spec["n_base"], d)
+    lists = partition(rng, base, spec["nlist"])
+    agents = [f"agent{i}" for i in range(spec["n_agents"])]
+    themes = {a: base[rng.choice(len(base), 3, replace=False)] for a in agents}
+    sigma = 0.2 * np.sqrt(2.0) / np.sqrt(d)  # bench/workload.py:73-76
+    ops = [("load", "static", lists)]
+    k, nprobe = spec["k"], spec["nprobe"]
+    live_guess = spec["n_base"]
+    step = {a: 0 for a in agents}
+    for t in range(spec["n_ops"]):
+        a = agents[int(rng.integers(0, len(agents)))]
+        centre = themes[a][step[a] % 3]
+        r = rng.random()
+        if r < 0.55:
+            q = (centre + sigma * rng.normal(size=d)).astype(np.float32)
+            scopes = sorted([a, "static"]) if rng.random() < 0.8 else [a]
+            ops.append(("search", a, scopes, q, k, nprobe))
+            step[a] += 1
+        elif r < 0.8:
+            vecs = (centre + sigma * rng.normal(size=(int(rng.integers(1, 5)), d))).astype(np.float32)
+            ops.append(("insert", a, a, vecs, None))
+            live_guess += len(vecs)
+        elif r < 0.86:
+            ops.append(("end_request", a))
+        elif r < 0.91:
+            ops.append(("delete", None, int(rng.integers(0, live_guess))))
+        elif r < 0.95:
+            ops.append(("update", None, int(rng.integers(0, live_guess)),
+                        unit_sphere(rng, 1, d)[0]))
+        elif r < 0.98:
+            q = unit_sphere(rng, 1, d)[0]
+            ops.append(("search", None, sorted(["static"] + agents), q, k, nprobe))
+        else:
+            ops.append(("flush",))
+    ops.append(("flush",))
+    for a in agents:
+        ops.append(("search", a, sorted([a, "static"]), themes[a][0], k, nprobe))
+    return base, ops
+
+
+def agent_store_config_kwargs(spec):
+    """Reference StoreConfig of the agent traces (exhaustive coarse ef)."""
+    return dict(
+        dimension=spec["d"], seed=spec["seed"], ef_search_factor=1 << 20,
+        alpha_et=spec["alpha"], window_w=spec["window"], n_p=spec["n_p"],
+        l0_capacity=spec["l0"], l1_capacity=spec["l1"], verify_mode=spec["verify"],
+        cache_enabled=True, pattern_enabled=True, prefetch_enabled=True, profiles_enabled=True,
+        accelerator="none", split_threshold=1 << 30, split_target=1 << 20, splits_enabled=False,
+        maintenance_interval=16, threads=0,
+    )
+
+
+def run_agent_ops(store, spec, base, ops, write_pnck, metric):
+    """Apply an agent trace to a Store (the reference's or this package's --
+    the same code drives both sides) and record what it returns."""
+    import os
+    import tempfile
+
+    rec = {"digest": np.array(digest(base)), "n_ops": np.array(len(ops))}
+    for a in range(spec["n_agents"]):
+        store.register_agent(f"agent{a}")
+    for i, op in enumerate(ops):
+        kind = op[0]
+        if kind == "load":
+            _, scope, lists = op
+            with tempfile.TemporaryDirectory() as td:
+                path = os.path.join(td, "base.pnck")
+                write_pnck(path, spec["d"], metric,
+                           [(np.zeros(spec["d"], np.float32), rows.astype(np.int64), base[rows])
+                            for rows in lists])
+                rec[f"{i}/count"] = np.array(store.load_external_ivf(path, scope))
+        elif kind == "insert":
+            _, agent, scope, vecs, ids = op
+            rec[f"{i}/ids"] = np.array(store.insert(agent, scope, list(vecs), ids=ids), dtype=np.int64)
+        elif kind == "delete":
+            rec[f"{i}/ok"] = np.array(store.delete(op[1], op[2]))
+        elif kind == "update":
+            rec[f"{i}/ok"] = np.array(store.update(op[1], op[2], vector=op[3]))
+        elif kind == "end_request":
+            store.end_request(op[1])
+        elif kind == "flush":
+            store.flush_caches()
+        elif kind == "search":
+            _, agent, scopes, q, k, nprobe = op
+            res = store.search(agent, scopes, q, k, nprobe)
+            rec[f"{i}/hit_ids"] = np.array([h[0] for h in res.hits], dtype=np.int64)
+            rec[f"{i}/hit_d"] = np.array([h[1] for h in res.hits], dtype=np.float32)
+            rec[f"{i}/hit_scope"] = np.array([h[2] for h in res.hits], dtype="U16")
+            rec[f"{i}/scanned"] = np.array(res.stats.scanned_vectors)
+            rec[f"{i}/scan_ids"] = np.asarray(res.scan_ids, dtype=np.int64)
+            rec[f"{i}/level"] = np.array(res.stats.level_reached, dtype="U4")
+            rec[f"{i}/early"] = np.array(bool(res.stats.early_terminated))
+    cl = store.clusters.clusters
+    cids = sorted(cl)
+    rec["final/cids"] = np.array(cids, dtype=np.int64)
+    rec["final/scopes"] = np.array([cl[c].scope for c in cids], dtype="U16")
+    rec["final/centroids"] = np.stack([cl[c].centroid for c in cids])
+    rec["final/sizes"] = np.array([cl[c].size for c in cids], dtype=np.int64)
+    rec["final/members"] = np.concatenate([cl[c].member_ids for c in cids])
+    rec["final/live"] = np.array(store.live_count())
+    rec["final/rng"] = np.array(store.rng.random())
+    for a in range(spec["n_agents"]):
+        name = f"agent{a}"
+        c = store.caches[name]
+        rec[f"final/{name}/staged"] = np.array(sorted(store.clusters.staged.get(name, {})), dtype=np.int64)
+        rec[f"final/{name}/completed"] = np.array(c.completed_queries)
+        rec[f"final/{name}/verified"] = np.array(c.verified_count)
+        rec[f"final/{name}/misses"] = np.array(c.miss_count)
+        rec[f"final/{name}/l0_sizes"] = np.array([len(e.pool) for e in c.l0.values()], dtype=np.int64)
+        rec[f"final/{name}/l1_sizes"] = np.array([len(x) for x in c.l1], dtype=np.int64)
+        rec[f"final/{name}/n_fsms"] = np.array(len(store.patterns[name].fsms))
+    return rec

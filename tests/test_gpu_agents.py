@@ -1,0 +1,32 @@
+"""Agent mode (SURVEY.md 8a rows a9-a11, configs[2]): per-agent multi-level
+caches, staged inserts merged down into base clusters, early termination,
+FSM pattern hints, prefetch, profiles and verify mode, replayed against
+traces recorded from the reference Store (tests/golden/make_golden.py
+--agents).  Bit-exact: hits, distances, scopes, scanned counts, scan_ids,
+level reached, early-termination flags, final clusters, staged sets and
+cache statistics."""
+
+import numpy as np
+import pytest
+
+from replay import compare_records, gen, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", list(gen.AGENT_TRACE_SPECS))
+def test_agent_trace_matches_reference(name):
+    from paper_2602_21477_b200 import Store, StoreConfig
+    from paper_2602_21477_b200.core import Metric
+    from paper_2602_21477_b200.pnck import write_pnck
+
+    spec = gen.AGENT_TRACE_SPECS[name]
+    want = load_golden(f"agent_{name}.npz")
+    base, ops = gen.agent_trace_ops(spec)
+    store = Store(StoreConfig(**gen.agent_store_config_kwargs(spec)))
+    got = gen.run_agent_ops(store, spec, base, ops, write_pnck, Metric.SQUARED_EUCLIDEAN)
+    mism = compare_records(got, want)
+    assert not mism, "\n".join(mism[:10])
+    early = sum(1 for k in want if k.endswith("/early") and bool(want[k]))
+    assert early > 10, "the trace must exercise early termination"
+    store.close()
