@@ -192,6 +192,13 @@ AGENT_TRACE_SPECS = {
                          nprobe=3, n_p=4, l0=8, l1=24, window=6, alpha=0.7, verify=False),
     "agents_verify": dict(d=16, n_base=900, nlist=8, n_agents=3, n_ops=220, seed=32, k=4,
                           nprobe=2, n_p=3, l0=6, l1=16, window=4, alpha=0.9, verify=True),
+    "agents_ip": dict(d=32, n_base=1200, nlist=10, n_agents=2, n_ops=240, seed=33, k=6,
+                      nprobe=3, n_p=4, l0=8, l1=20, window=6, alpha=0.7, verify=False,
+                      metric="ip"),
+    # (no cosine agent trace: the reference raises ZeroDivisionError once an L1
+    # pool empties -- its zero centroid has no cosine distance, ref/core.py:106-109)
+    "agents_many": dict(d=48, n_base=3000, nlist=24, n_agents=5, n_ops=700, seed=35, k=8,
+                        nprobe=4, n_p=6, l0=12, l1=40, window=8, alpha=0.6, verify=False),
 }
 
 
@@ -245,7 +252,7 @@ def agent_store_config_kwargs(spec):
     """Reference StoreConfig of the agent traces (exhaustive coarse ef)."""
     return dict(
         dimension=spec["d"], seed=spec["seed"], ef_search_factor=1 << 20,
-        alpha_et=spec["alpha"], window_w=spec["window"], n_p=spec["n_p"],
+        metric=spec.get("metric", "sq_l2"), alpha_et=spec["alpha"], window_w=spec["window"], n_p=spec["n_p"],
         l0_capacity=spec["l0"], l1_capacity=spec["l1"], verify_mode=spec["verify"],
         cache_enabled=True, pattern_enabled=True, prefetch_enabled=True, profiles_enabled=True,
         accelerator="none", split_threshold=1 << 30, split_target=1 << 20, splits_enabled=False,

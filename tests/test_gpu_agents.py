@@ -24,9 +24,11 @@ def test_agent_trace_matches_reference(name):
     want = load_golden(f"agent_{name}.npz")
     base, ops = gen.agent_trace_ops(spec)
     store = Store(StoreConfig(**gen.agent_store_config_kwargs(spec)))
-    got = gen.run_agent_ops(store, spec, base, ops, write_pnck, Metric.SQUARED_EUCLIDEAN)
+    got = gen.run_agent_ops(store, spec, base, ops, write_pnck, Metric(spec.get("metric", "sq_l2")))
     mism = compare_records(got, want)
     assert not mism, "\n".join(mism[:10])
     early = sum(1 for k in want if k.endswith("/early") and bool(want[k]))
     assert early > 10, "the trace must exercise early termination"
+    if spec["verify"]:
+        assert sum(int(want[f"final/agent{a}/verified"]) for a in range(spec["n_agents"])) > 0
     store.close()

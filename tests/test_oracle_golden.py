@@ -102,3 +102,17 @@ def test_flat_ivf_matches_store_model():
         assert ids[b, :cnt[b]].tolist() == allid[o].tolist()
         assert np.array_equal(bits(dd[b, :cnt[b]]), bits(alld[o]))
         assert scanned[b] == len(allid)
+
+
+@pytest.mark.parametrize("name", list(gen.AGENT_TRACE_SPECS))
+def test_agent_fixture_matches_its_workload(name):
+    """The agent-mode fixtures (recorded from the reference Store) belong to
+    the workload gen.py regenerates here: same data digest, same op count,
+    and they exercise every cache level and early termination."""
+    g = load_golden(f"agent_{name}.npz")
+    base, ops = gen.agent_trace_ops(gen.AGENT_TRACE_SPECS[name])
+    assert str(g["digest"]) == gen.digest(base)
+    assert int(g["n_ops"]) == len(ops)
+    levels = {str(g[k]) for k in g if k.endswith("/level")}
+    assert levels == {"L0", "L1", "L2"}
+    assert sum(bool(g[k]) for k in g if k.endswith("/early")) > 10
