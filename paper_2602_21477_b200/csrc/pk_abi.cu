@@ -108,6 +108,7 @@ struct pk_index {
   int64_t d = 0, dp = 0;
   int metric = 0;
   int num_sms = 148;
+  int scan_sms = 148;  // persistent scan grid (PK_SCAN_SMS; < num_sms leaves SMs to overlapped work)
   cudaStream_t st = nullptr;
 
   // arena
@@ -697,6 +698,8 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   ix->dp = round_up(dim, DC);
   ix->metric = metric;
   cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, device);
+  ix->scan_sms = ix->num_sms;
+  if (const char* e = getenv("PK_SCAN_SMS")) ix->scan_sms = std::max(1, std::min(ix->num_sms, atoi(e)));
   if (const char* e = getenv("PK_CHUNK_ROWS")) ix->chunk_rows = std::max(TILE, atoi(e) / TILE * TILE);
   if (const char* e = getenv("PK_SCAN_EXACT")) ix->screen = atoi(e) == 0;
   if (const char* e = getenv("PK_POOL_CAP")) ix->pool_cap = std::max(1, atoi(e));
@@ -1372,7 +1375,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                      (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
                      work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
                      ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
-                     ix->pool_cap, ix->num_sms, st);
+                     ix->pool_cap, ix->scan_sms, st);
     } else {
       launch_scan_screen(ix->metric, lt2, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
                          ix->items.as<ScanItem>(), n_items,
