@@ -149,6 +149,8 @@ struct pk_index {
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
   DevBuf shard_in, shard_out, pb, pb_out, nsurv, sl_buf;
+  uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
+  size_t hout_bytes = 0;
 
   // ---- cold tier (pk_index_enable_tier).  Every list keeps a copy in a
   // pinned, device-mapped host arena -- the source of truth, as the
@@ -748,6 +750,7 @@ int pk_index_destroy(pk_index* ix) {
     if (e) cudaEventDestroy(e);
   if (ix->stage_ev) cudaEventDestroy(ix->stage_ev);
   if (ix->mst) cudaStreamDestroy(ix->mst);
+  if (ix->hout) cudaFreeHost(ix->hout);
   if (ix->hrows) cudaFreeHost(ix->hrows);
   if (ix->hids) cudaFreeHost(ix->hids);
   ix->stage_desc.release();
@@ -1396,15 +1399,17 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   float* o_d = out_dists;
   int64_t* o_cid = out_cids;
   int32_t* o_n = out_n;
+  const int64_t ob = pk_shard_block_bytes(B, kk);  // host path: one packed result block
   if (!dev) {
-    RET(ix->out_ids.ensure((size_t)B * kk * 8));
-    RET(ix->out_d.ensure((size_t)B * kk * 4));
-    RET(ix->out_cid.ensure((size_t)B * kk * 8));
-    RET(ix->out_n.ensure((size_t)B * 4));
-    o_ids = ix->out_ids.as<int64_t>();
-    o_d = ix->out_d.as<float>();
-    o_cid = ix->out_cid.as<int64_t>();
-    o_n = ix->out_n.as<int32_t>();
+    // results land in one device block (shard-block layout) and come back in
+    // ONE copy into a pinned staging buffer, then fan out on the host
+    RET(ix->out_ids.ensure((size_t)ob));
+    uint8_t* base = ix->out_ids.as<uint8_t>();
+    const int64_t nkk = B * kk;
+    o_ids = reinterpret_cast<int64_t*>(base);
+    o_cid = reinterpret_cast<int64_t*>(base + 8 * nkk);
+    o_d = reinterpret_cast<float*>(base + 16 * nkk + 8 * B);
+    o_n = reinterpret_cast<int32_t*>(base + 20 * nkk + 8 * B);
   }
   if (ix->screen) RET(ix->nsurv.ensure((size_t)B * 4));
   if (ix->screen)
@@ -1418,12 +1423,24 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                  lt2, o_ids, o_d, o_cid, o_n, st);
   CK(cudaGetLastError());
   if (!dev) {
-    CK(cudaMemcpyAsync(out_ids, o_ids, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(out_dists, o_d, (size_t)B * kk * 4, cudaMemcpyDeviceToHost, st));
-    if (out_cids) CK(cudaMemcpyAsync(out_cids, o_cid, (size_t)B * kk * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(out_n, o_n, (size_t)B * 4, cudaMemcpyDeviceToHost, st));
-    if (out_scanned)
-      CK(cudaMemcpyAsync(out_scanned, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToHost, st));
+    const int64_t nkk = B * kk;
+    uint8_t* base = ix->out_ids.as<uint8_t>();
+    CK(cudaMemcpyAsync(base + 16 * nkk, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+    if ((int64_t)ix->hout_bytes < ob) {
+      if (ix->hout) cudaFreeHost(ix->hout);
+      ix->hout = nullptr;
+      ix->hout_bytes = 0;
+      CK(cudaHostAlloc((void**)&ix->hout, (size_t)ob, cudaHostAllocDefault));
+      ix->hout_bytes = (size_t)ob;
+    }
+    CK(cudaMemcpyAsync(ix->hout, base, (size_t)ob, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const uint8_t* h = ix->hout;
+    memcpy(out_ids, h, nkk * 8);
+    if (out_cids) memcpy(out_cids, h + 8 * nkk, nkk * 8);
+    if (out_scanned) memcpy(out_scanned, h + 16 * nkk, B * 8);
+    memcpy(out_dists, h + 16 * nkk + 8 * B, nkk * 4);
+    memcpy(out_n, h + 20 * nkk + 8 * B, B * 4);
   } else if (out_scanned) {
     CK(cudaMemcpyAsync(out_scanned, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
   }

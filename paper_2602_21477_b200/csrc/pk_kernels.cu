@@ -15,6 +15,7 @@
 #include "pk_umma.cuh"
 
 #include <algorithm>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 
@@ -1716,13 +1717,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
   __shared__ int s_cnt, s_ns, s_bin, s_below;
   __shared__ unsigned s_hist[256];
   __shared__ unsigned s_wu[RR_THREADS / 32];
-  __shared__ __align__(8) uint64_t s_bar[2];
-  uint32_t bar_ph[2] = {0, 0};
-  if (threadIdx.x == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    fence_mbar_init();
-  }
+
   __shared__ uint32_t s_u[RR_THREADS / 32];
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1815,20 +1810,24 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
         const int W = DC * kq, rs = W + 4, nblk = nd32 / kq;
         auto issue = [&](int blk) {
           float* dst = stage + (blk & 1) * m * rs;
-          if (threadIdx.x == 0) mbar_arrive_expect_tx(&s_bar[blk & 1], (uint32_t)(m * W * 4));
-          __syncwarp();
-          for (int r = threadIdx.x; r < m; r += 32) {
+          const int w4 = W / 4;
+          for (int i = threadIdx.x; i < m * w4; i += RR_THREADS) {
+            const int r = i / w4, c = i - r * w4;
             const int4 e = cpool[(int64_t)b * cap + surv[g0 + r]];
-            bulk_g2s(dst + r * rs, lt.rows + (int64_t)e.x * lt.dp + blk * W, (uint32_t)(W * 4),
-                     &s_bar[blk & 1]);
+            cp_async16(dst + r * rs + 4 * c, lt.rows + (int64_t)e.x * lt.dp + blk * W + 4 * c);
           }
+          cp_async_commit();
         };
-        if (threadIdx.x < 32) issue(0);
+        issue(0);
         float acc = 0.f;
         for (int blk = 0; blk < nblk; blk++) {
-          if (threadIdx.x < 32 && blk + 1 < nblk) issue(blk + 1);
-          mbar_wait(&s_bar[blk & 1], bar_ph[blk & 1]);
-          bar_ph[blk & 1] ^= 1;
+          if (blk + 1 < nblk) {
+            issue(blk + 1);
+            cp_async_wait<1>();
+          } else {
+            cp_async_wait<0>();
+          }
+          __syncthreads();
           if (threadIdx.x < m) {
             const float4* x4 = reinterpret_cast<const float4*>(stage + (blk & 1) * m * rs + threadIdx.x * rs);
             const float4* q4 = qs4 + blk * (W / 4);
@@ -2400,14 +2399,21 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     const float* __restrict__ Qd, const float* __restrict__ qn2,
     const int32_t* __restrict__ scope_codes, int nscopes, int nprobe, float coef, float abs_coef,
     int cap, int stage_floats, int ks, int64_t zstride, int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key,
-    int32_t* __restrict__ ncand_out) {
+    int32_t* __restrict__ ncand_out, uint64_t* __restrict__ dbg) {
+  auto mark = [&](int i) {  // phase timestamps (PK_DEBUG_PICK)
+    if (dbg && threadIdx.x == 0) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      dbg[blockIdx.x * 8 + i] = t;
+    }
+  };
+  mark(0);
   extern __shared__ __align__(16) uint8_t pick_smem[];
   Entry* buf = reinterpret_cast<Entry*>(pick_smem);                  // [cap] (pow2)
   float* qs = reinterpret_cast<float*>(buf + cap);                   // [dp]
   float* rows_st = qs + lt.dp;                                       // [stage_floats]
   uint32_t* hks = reinterpret_cast<uint32_t*>(rows_st + stage_floats);  // [nslots] when staged
   uint32_t* lks = hks + lt.nslots;                                        // [nslots] when staged
-  __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ int s_codes[64];
   __shared__ unsigned s_hist[256];
   __shared__ unsigned s_w[PICK_THREADS / 32];
@@ -2418,14 +2424,8 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
   if (tid < 64) s_codes[tid] = tid < nscopes ? scope_codes[tid] : -1;
   for (int j = tid; j < lt.dp / 4; j += PICK_THREADS)
     reinterpret_cast<float4*>(qs)[j] = reinterpret_cast<const float4*>(Qd + (int64_t)b * lt.dp)[j];
-  if (tid == 0) {
-    s_total = 0;
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    fence_mbar_init();
-  }
+  if (tid == 0) s_total = 0;
   __syncthreads();
-  uint32_t bar_ph[2] = {0, 0};
   const float* arow = Aapp + (int64_t)b * lda;
   const float qn = qn2[b];
   // bounds of list s: hk = key(A + eps), lk = key(A - eps); out of scope /
@@ -2456,6 +2456,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     lk = f2key(lo);
     if (hk == KEY_NONE) hk = KEY_NONE - 1;  // keep valid lists distinguishable
   };
+  mark(1);
   // 1. upper-bound keys (staged) and the number of in-scope lists
   int nv = 0;
 #pragma unroll 4
@@ -2472,6 +2473,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
   if ((tid & 31) == 0) atomicAdd(&s_total, nv);
   __syncthreads();
   const int nvalid = s_total;
+  mark(2);
   // 2. U = nprobe-th smallest upper bound (radix select, 8 bits per pass)
   uint32_t U = KEY_NONE - 1;
   if (nvalid > nprobe) {
@@ -2496,6 +2498,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     }
     U = prefix;
   }
+  mark(3);
   // 3. exact re-rank of every list whose lower bound is <= U, in rounds of
   //    up to cap - nprobe candidates merged with the running first nprobe
   int kept = 0, ncand = 0;
@@ -2525,6 +2528,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     }
     const int n = s_cnt;
     ncand += n - kept;
+    mark(4);
     // exact distances of this round's candidates buf[kept, n) (<= PICK_THREADS):
     // thread t runs candidate t's chain; the rows stream through shared memory
     // in column blocks of W floats (bulk copies, 2-deep ring) so every chain
@@ -2539,20 +2543,26 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
           break;
         }
       const int W = DC * k, rs = W + 4, nblk = nd32 / k;
+      // every thread streams 16-byte pieces of the block (cp.async, 2-deep ring)
       auto issue = [&](int blk) {
         float* dst = rows_st + (blk & 1) * nr * rs;
-        if (tid == 0) mbar_arrive_expect_tx(&s_bar[blk & 1], (uint32_t)(nr * W * 4));
-        __syncwarp();
-        for (int r = tid; r < nr; r += 32)
-          bulk_g2s(dst + r * rs, lt.cent + (int64_t)buf[c0 + r].pay * lt.dp + blk * W,
-                   (uint32_t)(W * 4), &s_bar[blk & 1]);
+        const int w4 = W / 4;
+        for (int i = tid; i < nr * w4; i += PICK_THREADS) {
+          const int r = i / w4, c = i - r * w4;
+          cp_async16(dst + r * rs + 4 * c, lt.cent + (int64_t)buf[c0 + r].pay * lt.dp + blk * W + 4 * c);
+        }
+        cp_async_commit();
       };
-      if (tid < 32 && nr > 0) issue(0);
+      issue(0);
       float acc = 0.f;
-      for (int blk = 0; blk < nblk && nr > 0; blk++) {
-        if (tid < 32 && blk + 1 < nblk) issue(blk + 1);
-        mbar_wait(&s_bar[blk & 1], bar_ph[blk & 1]);
-        bar_ph[blk & 1] ^= 1;
+      for (int blk = 0; blk < nblk; blk++) {
+        if (blk + 1 < nblk) {
+          issue(blk + 1);
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
         if (tid < nr) {
           const float* x = rows_st + (blk & 1) * nr * rs + tid * rs;
           const float* q = qs + blk * W;
@@ -2568,8 +2578,10 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
       if (tid < nr) buf[c0 + tid].key = f2key(METRIC == SQ_L2 ? acc : -acc);
     }
     __syncthreads();
+    mark(5);
     cta_bitonic_sort(buf, n);
     kept = cta_compact_sorted(buf, n, nprobe, false, &s_cnt);
+    mark(6);
     s_next = s_end;
     __syncthreads();
   }
@@ -2578,6 +2590,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     if (probe_key) probe_key[(int64_t)b * nprobe + p] = p < kept ? buf[p].key : KEY_NONE;
   }
   if (tid == 0 && ncand_out) ncand_out[b] = ncand;
+  mark(7);
 }
 
 static int pick_cap(int nprobe) {
@@ -2606,6 +2619,10 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
                         uint32_t* probe_key, int32_t* ncand, cudaStream_t st) {
   if (B <= 0) return;
+  // PK_DEBUG_PICK=1: per-CTA phase timestamps, averaged to stderr (measurement aid)
+  static const bool debug = getenv("PK_DEBUG_PICK") != nullptr;
+  uint64_t* dbg = nullptr;
+  if (debug) cudaMallocAsync((void**)&dbg, (size_t)B * 8 * 8, st);
   const size_t smem = coarse_pick_smem_bytes(lt.dp, lt.nslots, nprobe);
   const int cap = pick_cap(nprobe);
   const int stage_floats = pick_stage_floats(lt.dp, lt.nslots, nprobe);
@@ -2618,11 +2635,28 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
     k<<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe,     \
                                      coef, abs_coef, cap, stage_floats, ks, (int64_t)B * lda, probe, \
-                                     probe_key, ncand);                                              \
+                                     probe_key, ncand, dbg);                                         \
   }
   if (metric == SQ_L2) PK_PK(SQ_L2)
   else PK_PK(IP)
 #undef PK_PK
+  if (dbg) {
+    std::vector<uint64_t> h((size_t)B * 8);
+    cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double acc[8] = {0};
+    uint64_t t0 = UINT64_MAX, t1 = 0;
+    for (int b = 0; b < B; b++) {
+      for (int i = 1; i < 8; i++) acc[i] += (double)(h[b * 8 + i] - h[b * 8 + i - 1]);
+      t0 = std::min(t0, h[b * 8]);
+      t1 = std::max(t1, h[b * 8 + 7]);
+    }
+    fprintf(stderr, "pick phases (us, mean per CTA): prologue %.2f bounds %.2f radix %.2f collect %.2f "
+                    "exact %.2f sort %.2f out %.2f | span %.2f\n",
+            acc[1] / B / 1e3, acc[2] / B / 1e3, acc[3] / B / 1e3, acc[4] / B / 1e3, acc[5] / B / 1e3,
+            acc[6] / B / 1e3, acc[7] / B / 1e3, (t1 - t0) / 1e3);
+    cudaFreeAsync(dbg, st);
+  }
 }
 
 }  // namespace pk
