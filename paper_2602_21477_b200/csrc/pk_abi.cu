@@ -104,6 +104,7 @@ struct Range {
 }  // namespace
 
 struct pk_index {
+  std::recursive_mutex mu;  // one caller at a time per index (Store read locks admit concurrent searches)
   int device = 0;
   int64_t d = 0, dp = 0;
   int metric = 0;
@@ -767,17 +768,20 @@ int pk_index_destroy(pk_index* ix) {
 }
 
 int pk_sync(pk_index* ix) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 void* pk_stream(pk_index* ix) { return ix ? (void*)ix->st : nullptr; }
 int pk_index_bytes(pk_index* ix, int64_t* bytes) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   *bytes = ix->arena_cap * (ix->dp * 4 + 8) + (int64_t)ix->slot_cap * (ix->dp * 4 + 28);
   return PK_OK;
 }
 
 int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* rows,
                    const int64_t* ids, int64_t n, float* out_centroid, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (n < 1) return fail(PK_ERR_USAGE, "create_cluster needs at least one seed item");
   if (ix->cid2slot.count(cid)) return fail(PK_ERR_USAGE, "cluster %lld exists", (long long)cid);
   CK(cudaSetDevice(ix->device));
@@ -835,6 +839,7 @@ int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* r
 }
 
 int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const float* centroid) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (ix->cid2slot.count(cid)) return fail(PK_ERR_USAGE, "cluster %lld exists", (long long)cid);
   if (!centroid) return fail(PK_ERR_USAGE, "remote list needs a centroid");
   CK(cudaSetDevice(ix->device));
@@ -871,6 +876,7 @@ int64_t pk_shard_block_bytes(int64_t B, int32_t kk) {
 int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int32_t kk,
                     int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
                     int64_t* out_scanned, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (R < 1 || B < 0) return fail(PK_ERR_USAGE, "bad shard count / batch");
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
   if ((int64_t)R * kk > shard_merge_cap())
@@ -913,6 +919,7 @@ int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int3
 
 int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* ids, int64_t n,
                    int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (n <= 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   int32_t s;
@@ -964,6 +971,7 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
 
 int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const float* rows,
                          const int64_t* ids) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (n <= 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   // pre-pass: slots, per-slot counts, capacity (one relocation per list at most)
@@ -1045,6 +1053,7 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
 }
 
 int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1078,6 +1087,7 @@ int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
 }
 
 int pk_list_retire(pk_index* ix, int64_t cid) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   int32_t s;
   RET(ix->slot_of(cid, &s));
   if (ix->tiered) {
@@ -1099,6 +1109,7 @@ int pk_list_retire(pk_index* ix, int64_t cid) {
 }
 
 int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1119,6 +1130,7 @@ int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
 }
 
 int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1130,6 +1142,7 @@ int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid) {
 }
 
 int pk_list_size(pk_index* ix, int64_t cid, int64_t* n) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   int32_t s;
   RET(ix->slot_of(cid, &s));
   *n = ix->h_len[s];
@@ -1137,6 +1150,7 @@ int pk_list_size(pk_index* ix, int64_t cid, int64_t* n) {
 }
 
 int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1158,6 +1172,7 @@ int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
 }
 
 int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (ix->tiered) return PK_OK;
   if (ix->cid2slot.size() > 0) return fail(PK_ERR_USAGE, "enable the cold tier before creating lists");
   CK(cudaSetDevice(ix->device));
@@ -1169,6 +1184,7 @@ int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows) {
 }
 
 int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!ix->tiered) return fail(PK_ERR_USAGE, "no cold tier: every list is HBM-resident");
   CK(cudaSetDevice(ix->device));
   int32_t s;
@@ -1211,6 +1227,7 @@ int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
 }
 
 int pk_list_residency(pk_index* ix, int64_t cid, int* state) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   int32_t s;
   RET(ix->slot_of(cid, &s));
   RET(ix->finish_migration(s, false));
@@ -1219,6 +1236,7 @@ int pk_list_residency(pk_index* ix, int64_t cid, int* state) {
 }
 
 int pk_tier_stats(pk_index* ix, int64_t* out, int n) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   int64_t v[10] = {0};
   if (ix->tiered) RET(ix->poll_migrations());
   for (int32_t s = 0; s < ix->nslots; s++) {
@@ -1467,6 +1485,7 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
               int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids, float* out_dists,
               int64_t* out_cids, int32_t* out_n, int64_t* out_probe, int64_t* out_scanned,
               int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   const bool dev = flags & PK_DEVICE_PTRS;
   return search_core(ix, Q, B, scope_codes, nscopes, nprobe, kk, out_ids, out_dists, out_cids,
                      out_n, out_probe, out_scanned, dev, dev, nullptr, nullptr);
@@ -1474,6 +1493,7 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 
 int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
                      int32_t nscopes, int32_t nprobe, int32_t* out_probe, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!out_probe) return fail(PK_ERR_USAGE, "out_probe is required");
   const bool dev = flags & PK_DEVICE_PTRS;
   return search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
@@ -1482,6 +1502,7 @@ int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* sco
 
 int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe, int32_t nprobe,
                      int32_t kk, int64_t group, void* out_blocks, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!probe || !out_blocks) return fail(PK_ERR_USAGE, "probe and out_blocks are required");
   if (group < 1 || B % group != 0) return fail(PK_ERR_USAGE, "group must divide the batch");
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
@@ -1512,6 +1533,7 @@ int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* pro
 
 int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
                           int32_t nscopes, int32_t nprobe, int64_t* out_cids) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!out_cids) return fail(PK_ERR_USAGE, "out_cids is required");
   std::vector<int32_t> pr((size_t)std::max<int64_t>(B, 0) * std::max(nprobe, 1));
   RET(search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
@@ -1522,6 +1544,7 @@ int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t
 
 int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, int64_t* out_ids,
                   float* out_dists, int64_t* out_prefix) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (m < 0) return fail(PK_ERR_USAGE, "negative list count");
   out_prefix[0] = 0;
   if (m == 0) return PK_OK;
@@ -1568,6 +1591,7 @@ int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, 
 }
 
 int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
   if ((size_t)B * 4 > ix->ccount.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
   CK(cudaMemcpyAsync(out, ix->ccount.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
@@ -1576,6 +1600,7 @@ int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B) {
 }
 
 int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
   if ((size_t)B * 4 > ix->nsurv.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
   CK(cudaMemcpyAsync(out, ix->nsurv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
@@ -1584,6 +1609,7 @@ int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B) {
 }
 
 int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (!ix->coarse_tc) return fail(PK_ERR_USAGE, "exact coarse quantizer: no screened candidates");
   if ((size_t)B * 4 > ix->ncand.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
   CK(cudaMemcpyAsync(out, ix->ncand.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
@@ -1592,12 +1618,14 @@ int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B) {
 }
 
 int pk_profile_begin(pk_index* ix) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   ix->prof = true;
   ix->prof_calls = 0;
   return PK_OK;
 }
 
 int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   CK(cudaStreamSynchronize(ix->st));
   const int ns = std::min(nstages, pk_index::NSTAGE);
   for (int k = 0; k < nstages; k++) stage_ms[k] = 0.0;
@@ -1617,6 +1645,7 @@ int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls) {
 
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
   if (n < 0) return fail(PK_ERR_USAGE, "negative count");
   if (n == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));

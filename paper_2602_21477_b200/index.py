@@ -9,6 +9,7 @@ of one GPU.  It is the storage half of the reference's ``ClusterStore``
 from __future__ import annotations
 
 import ctypes
+import threading
 
 import numpy as np
 
@@ -50,6 +51,7 @@ class DeviceIndex:
                                         int(reserve_rows), int(reserve_lists), ctypes.byref(h)))
         self._h = h
         self._pend: list = []  # queued appends (flushed before any other operation)
+        self._pend_lock = threading.Lock()
 
     @property
     def handle(self):
@@ -135,12 +137,16 @@ class DeviceIndex:
         rows = N.f32(rows, self.dimension)
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         if len(ids):
-            self._pend.append((int(cid), rows, ids))
+            with self._pend_lock:
+                self._pend.append((int(cid), rows, ids))
 
     def flush(self):
         if not self._pend:
             return
-        pend, self._pend = self._pend, []
+        with self._pend_lock:
+            pend, self._pend = self._pend, []
+        if not pend:
+            return
         cids = np.concatenate([np.full(len(i), c, dtype=np.int64) for c, _, i in pend])
         rows = np.ascontiguousarray(np.concatenate([r for _, r, _ in pend]))
         ids = np.ascontiguousarray(np.concatenate([i for _, _, i in pend]))

@@ -334,3 +334,28 @@ def test_coarse_quantizer_matches_oracle(pk, kind, coarse, monkeypatch):
         assert np.array_equal(out.ids, ids)
         assert np.array_equal(bits(out.dists), bits(dd))
     ix.close()
+
+
+def test_concurrent_searches_equal_serial(pk):
+    """Store read locks admit concurrent searches (ref/engine.py:306-317); the
+    device index serialises its callers, so answers from 8 threads equal the
+    serial answers."""
+    import concurrent.futures as cf
+
+    from paper_2602_21477_b200 import Store, StoreConfig
+
+    rng = np.random.default_rng(3)
+    d = 64
+    store = Store(StoreConfig(dimension=d, cache_enabled=False, accelerator="none", threads=8,
+                              splits_enabled=False))
+    base = rng.normal(size=(6000, d)).astype(np.float32)
+    store.load_lists("static", [(np.arange(i * 500, (i + 1) * 500), base[i * 500:(i + 1) * 500])
+                                for i in range(12)])
+    Q = rng.normal(size=(64, d)).astype(np.float32)
+    serial = [store.search(None, ["static"], q, 10, 4).hits for q in Q]
+    with cf.ThreadPoolExecutor(8) as ex:
+        par = list(ex.map(lambda q: store.search(None, ["static"], q, 10, 4).hits, Q))
+    futs = [store.submit_search(None, ["static"], q, 10, 4) for q in Q]
+    assert par == serial
+    assert [f.result().hits for f in futs] == serial
+    store.close()
