@@ -212,6 +212,7 @@ class Store:
         self.caches: dict[str, MultiLevelCache] = {}
         self.patterns: dict[str, PatternTable] = {}
         self._prefetch_inflight: set = set()
+        self._match_memo: dict = {}
         self.sequences: dict[str, list[np.ndarray]] = {}
         self.payloads: dict[int, bytes] = {}
         self._next_item_id = 0
@@ -490,25 +491,39 @@ class Store:
 
     def _topk(self, id_chunks, dist_chunks, k):
         """ref/engine.py:406-426: lexsort by (dist, id), first occurrence per
-        id, owners only (a cached copy of a deleted item is skipped)."""
+        id, owners only (a cached copy of a deleted item is skipped).  Only a
+        prefix of the order is ever consumed, so it sorts the smallest
+        entries first (every entry tied with the cut is included) and falls
+        back to the full order when duplicates / deleted ids exhaust it."""
         if not id_chunks:
             return []
         ids = np.concatenate(id_chunks)
         dists = np.concatenate(dist_chunks).astype(np.float32)
-        hits, seen = [], set()
-        for idx in np.lexsort((ids, dists)):
-            iid = int(ids[idx])
-            if iid in seen:
-                continue
-            seen.add(iid)
-            owner = self.clusters.owner.get(iid)
-            if owner is None:
-                continue
-            scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
-            hits.append((iid, float(dists[idx]), scope))
-            if len(hits) >= k:
-                break
-        return hits
+        n = len(ids)
+        take = min(n, 4 * k + 16)
+        while True:
+            if take < n:
+                cut = np.partition(dists, take - 1)[take - 1]
+                sel = np.nonzero(dists <= cut)[0]  # ties at the cut kept whole
+            else:
+                sel = np.arange(n)
+            order = sel[np.lexsort((ids[sel], dists[sel]))]
+            hits, seen = [], set()
+            for idx in order:
+                iid = int(ids[idx])
+                if iid in seen:
+                    continue
+                seen.add(iid)
+                owner = self.clusters.owner.get(iid)
+                if owner is None:
+                    continue
+                scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
+                hits.append((iid, float(dists[idx]), scope))
+                if len(hits) >= k:
+                    return hits
+            if len(sel) >= n:
+                return hits
+            take = min(n, 4 * take)
 
     def _hint_for(self, agent, q) -> PatternHint:
         """ref/engine.py:428-435."""
@@ -517,15 +532,22 @@ class Store:
         cache = self.caches.get(agent)
         listing = cache.l1_listing() if cache else None
         prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [q]
-        return self.patterns[agent].match_and_predict(prefix, listing)
+        hint = self.patterns[agent].match_and_predict(prefix, listing)
+        # the side effects key L0 by the same prefix's match: remember it
+        self._match_memo[agent] = (q.tobytes(), len(self.sequences[agent]), hint.matched_fsm)
+        return hint
 
     def _state_key_for(self, agent, v):
         """ref/engine.py:437-446: the matched pattern's aligned state keys L0."""
         if not self.cfg.pattern_enabled:
             return DEFAULT_KEY
         table = self.patterns[agent]
-        prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [v]
-        idx, _ = table.match(prefix)
+        memo = self._match_memo.pop(agent, None)
+        if memo is not None and memo[0] == v.tobytes() and memo[1] == len(self.sequences[agent]):
+            idx = memo[2]  # same prefix, same table: the hint's match
+        else:
+            prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [v]
+            idx, _ = table.match(prefix)
         if idx is None:
             return DEFAULT_KEY
         return (idx, table.fsms[idx].align(v, self.metric))

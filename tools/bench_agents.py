@@ -95,6 +95,9 @@ def main():
                                      for c in range(nlist) if lens[c] > 0])
         build_s = time.perf_counter() - t0
         sigma = 0.2 * np.sqrt(2.0) / np.sqrt(a.d)
+        for s in range(1, a.agents + 1):  # untimed warm-up op per agent (first-call costs)
+            ag = f"agent{s - 1}"
+            store.search(ag, [ag, "static"], themes[s][7], 10, a.nprobe)
         n_s = n_i = 0
         levels = {"L0": 0, "L1": 0, "L2": 0}
         early = 0
