@@ -145,7 +145,7 @@ struct pk_index {
   bool tensor = true;  // screen dots on tcgen05 (TF32); PK_SCREEN=ffma uses CUDA-core FFMA
   bool coarse_tc = true;  // coarse quantizer on tcgen05 + exact re-rank; PK_COARSE=exact disables
   bool coarse_split = true;  // 3xTF32 hi/lo split (tight bound); PK_COARSE=tf32 for one product
-  DevBuf qhi, qlo;
+  DevBuf qhi, qlo, qin;
   DevBuf ncand;
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
@@ -760,7 +760,7 @@ int pk_index_destroy(pk_index* ix) {
                     &ix->items, &ix->qpairs, &ix->slot_off, &ix->scanned,
                     &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list,
                     &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->nsurv, &ix->sl_buf, &ix->ncand, &ix->qhi, &ix->qlo})
+                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->nsurv, &ix->sl_buf, &ix->ncand, &ix->qhi, &ix->qlo, &ix->qin})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -1314,26 +1314,48 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   const int pc = ix->prof_calls;
 #define PROF(stage) \
   if (ix->prof) RET(ix->prof_mark(pc, stage))
+  int32_t* lcount = ix->counts.as<int32_t>();  // [ns] | n_items | work counter
+  int32_t* n_items = lcount + ns;
+  int32_t* work_ctr = lcount + ns + 1;
+  const bool use_tc = ix->coarse_tc && !probe_in;
+  // one fused prep kernel (padded copy, norms, TF32 split, swizzled copies,
+  // counter resets) on the screened paths; plain copies otherwise
+  const bool prep = ix->screen || use_tc;
+  const bool tc_scan = ix->screen && ix->tensor && !probe_out;
   PROF(0);
-  // inputs
-  CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
-                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   if (!probe_in)
     CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
                        in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   const ListTable lt = ix->table();
-  if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
-  const bool use_tc = ix->coarse_tc && !probe_in;
-  if (ix->screen || use_tc) {
+  if (prep) {
+    const float* qin = Q;
+    if (!in_dev) {  // host rows: one contiguous H2D, the prep kernel pads them
+      RET(ix->qin.ensure((size_t)B * ix->d * 4));
+      CK(cudaMemcpyAsync(ix->qin.p, Q, (size_t)B * ix->d * 4, cudaMemcpyHostToDevice, st));
+      qin = ix->qin.as<float>();
+    }
     RET(ix->qnorm2.ensure(B * 4));
-    if (use_tc && ix->coarse_split) {
+    const bool sp = use_tc && ix->coarse_split;
+    if (sp) {
       RET(ix->qhi.ensure((size_t)B * dp * 4));
       RET(ix->qlo.ensure((size_t)B * dp * 4));
     }
-    const bool sp = use_tc && ix->coarse_split;
-    launch_qprep(ix->q.as<float>(), (int)B, (int)dp, ix->qnorm2.as<float>(),
-                 sp ? ix->qhi.as<float>() : nullptr, sp ? ix->qlo.as<float>() : nullptr, st);
+    if (tc_scan) RET(ix->qsw.ensure((size_t)8 * B * dp * 4));
+    if (ix->screen) {
+      RET(ix->uq.ensure((size_t)B * 4));
+      RET(ix->ccount.ensure((size_t)B * 4));
+    }
+    launch_qprep(qin, ix->d, (int)ix->d, (int)B, (int)dp, ix->q.as<float>(), ix->qnorm2.as<float>(),
+                 sp ? ix->qhi.as<float>() : nullptr, sp ? ix->qlo.as<float>() : nullptr,
+                 tc_scan ? ix->qsw.as<float>() : nullptr, lcount, (int)(ns + 2),
+                 ix->screen ? ix->ccount.as<int32_t>() : nullptr, ix->screen ? (int)B : 0,
+                 ix->screen ? ix->uq.as<uint32_t>() : nullptr, ix->screen ? (int)B : 0, st);
+  } else {
+    CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
+                         in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, st));
   }
+  if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
   PROF(1);
   // 1. coarse quantizer: distances to every list centroid, top-nprobe in scope
   if (probe_in) {
@@ -1374,24 +1396,15 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (ix->tiered) RET(ix->stage_cold(B, nprobe));
   const ListTable lt2 = ix->table();  // staging may have grown the arena
   // 2. route (query -> lists) into (list -> queries) work items
-  int32_t* lcount = ix->counts.as<int32_t>();
-  int32_t* n_items = lcount + ns;
-  int32_t* work_ctr = lcount + ns + 1;
-  CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, st));
   launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt2, ix->chunk_rows, (int)smax, (int)B,
                lcount, ix->items.as<ScanItem>(), n_items, ix->qpairs.as<QPair>(),
                ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
   // 3. fused scan + per-(query, list chunk) top-kk
   PROF(4);
   if (ix->screen) {
-    RET(ix->uq.ensure((size_t)B * 4));
-    RET(ix->ccount.ensure((size_t)B * 4));
-    RET(ix->cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));
-    CK(cudaMemsetAsync(ix->uq.p, 0xff, (size_t)B * 4, st));
-    CK(cudaMemsetAsync(ix->ccount.p, 0, (size_t)B * 4, st));
+    RET(ix->cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));  // uq / ccount reset by prep
     if (ix->tensor) {
-      RET(ix->qsw.ensure((size_t)8 * B * dp * 4));
-      launch_scan_tc(ix->metric, lt2, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(),
+      launch_scan_tc(ix->metric, lt2, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(), true,
                      ix->qnorm2.as<float>(), ix->items.as<ScanItem>(), n_items,
                      (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
                      work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),

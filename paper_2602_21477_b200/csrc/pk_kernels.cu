@@ -1607,12 +1607,12 @@ void launch_row_norms(const float* rows, int64_t n, int dp, float* out, cudaStre
 }
 
 void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd, int B,
-                    float* qsw, const float* qnorm2, const ScanItem* items, const int32_t* n_items,
-                    int max_items, const QPair* qpairs, int kk, int32_t* work_ctr, uint32_t* Uq,
-                    uint32_t* slot_hi, int32_t* slot_n, int4* cpool, int32_t* ccount, int cap,
-                    int num_sms, cudaStream_t st) {
+                    float* qsw, bool qsw_ready, const float* qnorm2, const ScanItem* items,
+                    const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
+                    int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
+                    int32_t* ccount, int cap, int num_sms, cudaStream_t st) {
   if (max_items <= 0) return;
-  qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
+  if (!qsw_ready) qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
   const size_t smem = tc_smem_bytes();
   const int grid = std::min(num_sms, max_items);
   const float coef = screen_coef_tf32(metric, lt.dp);
@@ -1637,25 +1637,6 @@ float screen_coef(int metric, int dp) {
   if (metric == SQ_L2) c = (2.0 * gam(dp) + 2.0 * gam(dp + 3) + 4.0 * u) / (1.0 - gam(dp));
   else c = (gam(dp) + 2.0 * u) / (1.0 - gam(dp));
   return (float)(c * 1.0625);  // slack for the fp32 evaluation of eps itself
-}
-
-// qn2[b] = sum of q_j^2 (FFMA, any order: the bound holds for any
-// evaluation tree of d terms).  One warp per query.
-__global__ void qnorm2_kernel(const float* __restrict__ Q, int64_t ldq, int B, int dp,
-                              float* __restrict__ out) {
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (b >= B) return;
-  const float* q = Q + (int64_t)b * ldq;
-  float acc = 0.f;
-  for (int j = lane; j < dp; j += 32) acc = __fmaf_rn(q[j], q[j], acc);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
-  if (lane == 0) out[b] = acc;
-}
-void launch_qnorm2(const float* Q, int64_t ldq, int B, int dp, float* out, cudaStream_t st) {
-  if (B <= 0) return;
-  qnorm2_kernel<<<(B + 7) / 8, 256, 0, st>>>(Q, ldq, B, dp, out);
 }
 
 void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
@@ -2276,17 +2257,44 @@ void launch_coarse_tc(bool split, int ks, const CoarseMaps& maps, int nslots, in
   }
 }
 
-// Query prep for the screens: qn2[b] = sum q_j^2 (FFMA, any order) and, when
-// hi/lo are given, the TF32 hi/lo split of the row.  One warp per query.
-__global__ void qprep_kernel(const float* __restrict__ Q, int B, int dp, float* __restrict__ qn2,
-                             float* __restrict__ hi, float* __restrict__ lo) {
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (b >= B) return;
-  const float4* q4 = reinterpret_cast<const float4*>(Q + (int64_t)b * dp);
+// Query prep, one pass per batch (one warp per query): the padded copy of
+// the user's rows (Qin, stride ldin, true dimension d; pad columns zero), the
+// FFMA squared norm qn2 (screen input; any order), optionally the TF32 hi/lo
+// split (coarse screen) and the 8 SWIZZLE_128B-permuted copies the scan's
+// query tiles are bulk-copied from (copy p has the 16-byte pieces of every
+// 128-byte chunk permuted by ^p); block 0 also resets the batch's counters.
+constexpr int QP_THREADS = 64;
+__global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const float* __restrict__ Qin, int64_t ldin, int d, int B, int dp,
+                             float* __restrict__ q, float* __restrict__ qn2, float* __restrict__ hi,
+                             float* __restrict__ lo, float* __restrict__ qsw,
+                             int32_t* __restrict__ zero_i32, int nzero, int32_t* __restrict__ zero2,
+                             int nzero2, uint32_t* __restrict__ ones_u32, int nones) {
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero_i32[i] = 0;
+    for (int i = threadIdx.x; i < nzero2; i += blockDim.x) zero2[i] = 0;
+    for (int i = threadIdx.x; i < nones; i += blockDim.x) ones_u32[i] = 0xffffffffu;
+  }
+  // one CTA (QP_THREADS) per query; partial norms combined in a fixed order
+  __shared__ float s_part[QP_THREADS / 32];
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float* src = Qin + (int64_t)b * ldin;
+  const bool vec_in = (d & 3) == 0 && (ldin & 3) == 0;
+  const int64_t n4 = (int64_t)B * dp / 4;
   float acc = 0.f;
-  for (int j = lane; j < dp / 4; j += 32) {
-    const float4 v = q4[j];
+  for (int j4 = threadIdx.x; j4 < dp / 4; j4 += QP_THREADS) {
+    float4 v;
+    const int j = 4 * j4;
+    if (vec_in && j + 3 < d) {
+      v = *reinterpret_cast<const float4*>(src + j);
+    } else {
+      v.x = j < d ? src[j] : 0.f;
+      v.y = j + 1 < d ? src[j + 1] : 0.f;
+      v.z = j + 2 < d ? src[j + 2] : 0.f;
+      v.w = j + 3 < d ? src[j + 3] : 0.f;
+    }
+    const int64_t e = (int64_t)b * (dp / 4) + j4;
+    reinterpret_cast<float4*>(q)[e] = v;
     acc = __fmaf_rn(v.x, v.x, acc);
     acc = __fmaf_rn(v.y, v.y, acc);
     acc = __fmaf_rn(v.z, v.z, acc);
@@ -2301,17 +2309,32 @@ __global__ void qprep_kernel(const float* __restrict__ Q, int B, int dp, float* 
       l.y = __fsub_rn(v.y, h.y);
       l.z = __fsub_rn(v.z, h.z);
       l.w = __fsub_rn(v.w, h.w);
-      reinterpret_cast<float4*>(hi + (int64_t)b * dp)[j] = h;
-      reinterpret_cast<float4*>(lo + (int64_t)b * dp)[j] = l;
+      reinterpret_cast<float4*>(hi)[e] = h;
+      reinterpret_cast<float4*>(lo)[e] = l;
+    }
+    if (qsw) {
+      const int64_t base8 = e & ~(int64_t)7;
+      const int piece = (int)(e & 7);
+#pragma unroll
+      for (int pp = 0; pp < 8; pp++) reinterpret_cast<float4*>(qsw)[pp * n4 + base8 + (piece ^ pp)] = v;
     }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = __fadd_rn(acc, __shfl_xor_sync(FULL, acc, o));
-  if (lane == 0) qn2[b] = acc;
+  if (lane == 0) s_part[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = s_part[0];
+    for (int w = 1; w < QP_THREADS / 32; w++) t = __fadd_rn(t, s_part[w]);
+    qn2[b] = t;
+  }
 }
-void launch_qprep(const float* Q, int B, int dp, float* qn2, float* hi, float* lo, cudaStream_t st) {
+void launch_qprep(const float* Qin, int64_t ldin, int d, int B, int dp, float* q, float* qn2, float* hi,
+                  float* lo, float* qsw, int32_t* zero_i32, int nzero, int32_t* zero2, int nzero2,
+                  uint32_t* ones_u32, int nones, cudaStream_t st) {
   if (B <= 0) return;
-  qprep_kernel<<<(B + 7) / 8, 256, 0, st>>>(Q, B, dp, qn2, hi, lo);
+  qprep_kernel<<<B, QP_THREADS, 0, st>>>(Qin, ldin, d, B, dp, q, qn2, hi, lo, qsw, zero_i32, nzero,
+                                         zero2, nzero2, ones_u32, nones);
 }
 
 // hi = x with the low 13 mantissa bits cleared (exactly representable in

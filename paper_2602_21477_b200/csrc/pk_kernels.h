@@ -93,8 +93,6 @@ void launch_scatter_rows(const float* src, int64_t lds, const int64_t* src_ids, 
                          cudaStream_t st);
 size_t scan_smem_bytes();
 size_t screen_smem_bytes();
-// qn2[b] = FFMA-chain squared norm of query b (screen input).
-void launch_qnorm2(const float* Q, int64_t ldq, int B, int dp, float* out, cudaStream_t st);
 // Screened persistent scan (sq_l2 / neg_ip): FFMA screen with a proven error
 // bound.  Per (query, item) slot: the item's kk smallest upper bounds
 // (slot_hi[slot][..slot_n]); per query: running bound Uq (KEY_NONE-initialised)
@@ -120,10 +118,10 @@ void launch_row_norms(const float* rows, int64_t n, int dp, float* out, cudaStre
 // Tensor-core screened persistent scan (tcgen05 TF32); same outputs as
 // launch_scan_screen.  qsw: scratch of 8 * B * dp floats.
 void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd, int B,
-                    float* qsw, const float* qnorm2, const ScanItem* items, const int32_t* n_items,
-                    int max_items, const QPair* qpairs, int kk, int32_t* work_ctr, uint32_t* Uq,
-                    uint32_t* slot_hi, int32_t* slot_n, int4* cpool, int32_t* ccount, int cap,
-                    int num_sms, cudaStream_t st);
+                    float* qsw, bool qsw_ready, const float* qnorm2, const ScanItem* items,
+                    const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
+                    int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
+                    int32_t* ccount, int cap, int num_sms, cudaStream_t st);
 
 // Cross-shard merge of R per-shard result blocks (layout: pk_shard_block_bytes
 // in include/pancake_b200.h) into the global top-kk per query.
@@ -147,8 +145,13 @@ int coarse_split_k(int nslots, int B, int dp, int num_sms);
 // Dout[z][b][slot] = partial dot over K range z of ks (the pick sums them in z order).
 void launch_coarse_tc(bool split, int ks, const CoarseMaps& maps, int nslots, int B, int dp,
                       float* Dout, int64_t lda, cudaStream_t st);
-// qn2[b] = FFMA squared norm; hi/lo (may be NULL) = TF32 split of the batch.
-void launch_qprep(const float* Q, int B, int dp, float* qn2, float* hi, float* lo, cudaStream_t st);
+// One-pass query prep: padded copy q of Qin (stride ldin, dimension d), FFMA
+// squared norms qn2, optional TF32 hi/lo split and 8 swizzled copies for the
+// scan (NULL to skip), and the batch's counter resets (zero_i32[nzero] = 0,
+// zero2[nzero2] = 0, ones_u32[nones] = ~0).
+void launch_qprep(const float* Qin, int64_t ldin, int d, int B, int dp, float* q, float* qn2, float* hi,
+                  float* lo, float* qsw, int32_t* zero_i32, int nzero, int32_t* zero2, int nzero2,
+                  uint32_t* ones_u32, int nones, cudaStream_t st);
 // hi/lo TF32 split of rows [0, n) of an [n][dp] table.
 void launch_tf32_split(const float* x, int64_t n, int dp, float* hi, float* lo, cudaStream_t st);
 float coarse_coef(int metric, int dp, bool split, int ks);
