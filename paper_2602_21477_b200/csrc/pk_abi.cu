@@ -1322,6 +1322,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // counter resets) on the screened paths; plain copies otherwise
   const bool prep = ix->screen || use_tc;
   const bool tc_scan = ix->screen && ix->tensor && !probe_out;
+  RouteArgs ra;  // set when the coarse pick emits the routes itself
   PROF(0);
   if (!probe_in)
     CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
@@ -1375,9 +1376,19 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     launch_coarse_tc(ix->coarse_split, ks, ix->cmaps, ix->nslots, (int)B, (int)dp,
                      ix->dc.as<float>(), ns, st);
     PROF(2);
+    // the pick also routes its query unless the cold tier may still move lists
+    if (!probe_out && !ix->tiered) {
+      ra.lcount = lcount;
+      ra.bucket = ix->qpairs.as<QPair>();
+      ra.slot_off = ix->slot_off.as<int32_t>();
+      ra.scanned = ix->scanned.as<int64_t>();
+      ra.chunk_rows = ix->chunk_rows;
+      ra.smax = (int)smax;
+      ra.bcap = (int)B;
+    }
     launch_coarse_pick(ix->metric, ix->coarse_split, ks, ix->dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, ix->q.as<float>(),
                        ix->qnorm2.as<float>(), ix->scopes.as<int32_t>(), nscopes, nprobe,
-                       ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), ix->ncand.as<int32_t>(), st);
+                       ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), ix->ncand.as<int32_t>(), ra, st);
   } else {
     launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
                       ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
@@ -1398,7 +1409,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // 2. route (query -> lists) into (list -> queries) work items
   launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt2, ix->chunk_rows, (int)smax, (int)B,
                lcount, ix->items.as<ScanItem>(), n_items, ix->qpairs.as<QPair>(),
-               ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), st);
+               ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), ra.lcount != nullptr, st);
   // 3. fused scan + per-(query, list chunk) top-kk
   PROF(4);
   if (ix->screen) {

@@ -389,19 +389,21 @@ __device__ __forceinline__ int nchunks_of(int64_t len, int chunk) {
 }
 
 constexpr int RE_THREADS = 128;
-__global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
-    const int32_t* __restrict__ probe, int nprobe, ListTable lt, int chunk_rows, int smax, int bcap,
-    int32_t* __restrict__ lcount, QPair* __restrict__ bucket, int32_t* __restrict__ slot_off,
-    int64_t* __restrict__ scanned) {
-  __shared__ int s_w[RE_THREADS / 32];
-  __shared__ long long s_sc[RE_THREADS / 32];
-  const int b = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+// Routing of one query (the calling CTA, any blockDim multiple of 32): its
+// output slots (fixed stride smax), scanned rows, and one (query, slot base)
+// pair per probed list appended to that list's bucket.
+__device__ void emit_routes(int b, const int32_t* __restrict__ prow, int nprobe, const ListTable& lt,
+                            int chunk_rows, int smax, int bcap, int32_t* __restrict__ lcount,
+                            QPair* __restrict__ bucket, int32_t* __restrict__ slot_off,
+                            int64_t* __restrict__ scanned) {
+  __shared__ int s_w[32];
+  __shared__ long long s_sc[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int carry = 0;
   int64_t sc = 0;
-  for (int p0 = 0; p0 < nprobe; p0 += RE_THREADS) {
+  for (int p0 = 0; p0 < nprobe; p0 += blockDim.x) {
     const int p = p0 + threadIdx.x;
-    const int s = p < nprobe ? probe[(int64_t)b * nprobe + p] : -1;
+    const int s = p < nprobe ? prow[p] : -1;
     int64_t len = 0;
     int c = 0;
     if (s >= 0) {
@@ -409,8 +411,7 @@ __global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
       c = nchunks_of(len, chunk_rows);
     }
     sc += len;
-    // block exclusive scan of c
-    int x = c;
+    int x = c;  // block exclusive scan of c
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int y = __shfl_up_sync(FULL, x, o);
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
     int wpre = 0, tot = 0;
-    for (int w = 0; w < RE_THREADS / 32; w++) {
+    for (int w = 0; w < nw; w++) {
       if (w < warp) wpre += s_w[w];
       tot += s_w[w];
     }
@@ -439,11 +440,19 @@ __global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
   __syncthreads();
   if (threadIdx.x == 0) {
     long long t = 0;
-    for (int w = 0; w < RE_THREADS / 32; w++) t += s_sc[w];
+    for (int w = 0; w < nw; w++) t += s_sc[w];
     scanned[b] = t;
     slot_off[2 * b] = b * smax;
     slot_off[2 * b + 1] = b * smax + carry;
   }
+}
+
+__global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
+    const int32_t* __restrict__ probe, int nprobe, ListTable lt, int chunk_rows, int smax, int bcap,
+    int32_t* __restrict__ lcount, QPair* __restrict__ bucket, int32_t* __restrict__ slot_off,
+    int64_t* __restrict__ scanned) {
+  emit_routes(blockIdx.x, probe + (int64_t)blockIdx.x * nprobe, nprobe, lt, chunk_rows, smax, bcap, lcount,
+              bucket, slot_off, scanned);
 }
 
 __global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
@@ -475,11 +484,13 @@ __global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
 
 void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows, int smax,
                   int bcap, int32_t* lcount, ScanItem* items, int32_t* n_items, QPair* bucket,
-                  int32_t* slot_off, int64_t* scanned, cudaStream_t st) {
-  // lcount [nslots] and *n_items zeroed by the caller
+                  int32_t* slot_off, int64_t* scanned, bool emitted, cudaStream_t st) {
+  // lcount [nslots] and *n_items zeroed by the caller; `emitted`: the coarse
+  // pick already ran emit_routes for every query
   if (B <= 0) return;
-  route_emit_kernel<<<B, RE_THREADS, 0, st>>>(probe, nprobe, lt, chunk_rows, smax, bcap, lcount,
-                                              bucket, slot_off, scanned);
+  if (!emitted)
+    route_emit_kernel<<<B, RE_THREADS, 0, st>>>(probe, nprobe, lt, chunk_rows, smax, bcap, lcount,
+                                                bucket, slot_off, scanned);
   if (lt.nslots > 0)
     route_items_kernel<<<(lt.nslots + 255) / 256, 256, 0, st>>>(lt, chunk_rows, bcap, lcount, items,
                                                                  n_items);
@@ -2422,7 +2433,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     const float* __restrict__ Qd, const float* __restrict__ qn2,
     const int32_t* __restrict__ scope_codes, int nscopes, int nprobe, float coef, float abs_coef,
     int cap, int stage_floats, int ks, int64_t zstride, int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key,
-    int32_t* __restrict__ ncand_out, uint64_t* __restrict__ dbg) {
+    int32_t* __restrict__ ncand_out, uint64_t* __restrict__ dbg, RouteArgs ra) {
   auto mark = [&](int i) {  // phase timestamps (PK_DEBUG_PICK)
     if (dbg && threadIdx.x == 0) {
       uint64_t t;
@@ -2613,6 +2624,11 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     if (probe_key) probe_key[(int64_t)b * nprobe + p] = p < kept ? buf[p].key : KEY_NONE;
   }
   if (tid == 0 && ncand_out) ncand_out[b] = ncand;
+  if (ra.lcount) {  // fused routing of this query (route_emit_kernel's work)
+    __syncthreads();
+    emit_routes(b, probe + (int64_t)b * nprobe, nprobe, lt, ra.chunk_rows, ra.smax, ra.bcap, ra.lcount,
+                ra.bucket, ra.slot_off, ra.scanned);
+  }
   mark(7);
 }
 
@@ -2640,7 +2656,7 @@ size_t coarse_pick_smem_bytes(int dp, int nslots, int nprobe) {
 void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64_t lda, int B, ListTable lt,
                         const float* cnrm, const float* Qd, const float* qn2,
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
-                        uint32_t* probe_key, int32_t* ncand, cudaStream_t st) {
+                        uint32_t* probe_key, int32_t* ncand, const RouteArgs& ra, cudaStream_t st) {
   if (B <= 0) return;
   // PK_DEBUG_PICK=1: per-CTA phase timestamps, averaged to stderr (measurement aid)
   static const bool debug = getenv("PK_DEBUG_PICK") != nullptr;
@@ -2658,7 +2674,7 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
     k<<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe,     \
                                      coef, abs_coef, cap, stage_floats, ks, (int64_t)B * lda, probe, \
-                                     probe_key, ncand, dbg);                                         \
+                                     probe_key, ncand, dbg, ra);                                     \
   }
   if (metric == SQ_L2) PK_PK(SQ_L2)
   else PK_PK(IP)

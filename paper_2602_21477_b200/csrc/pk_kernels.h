@@ -72,7 +72,16 @@ void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
 // bcap (query, slot base) pairs.  lcount [nslots] and *n_items must be zero.
 void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows, int smax,
                   int bcap, int32_t* lcount, ScanItem* items, int32_t* n_items, QPair* bucket,
-                  int32_t* slot_off, int64_t* scanned, cudaStream_t st);
+                  int32_t* slot_off, int64_t* scanned, bool emitted, cudaStream_t st);
+// Routing outputs for a kernel that emits its queries' routes itself (lcount
+// NULL = no routing).
+struct RouteArgs {
+  int32_t* lcount = nullptr;
+  QPair* bucket = nullptr;
+  int32_t* slot_off = nullptr;
+  int64_t* scanned = nullptr;
+  int chunk_rows = 0, smax = 0, bcap = 0;
+};
 // Persistent fused scan + per-(query, item) top-kk.
 void launch_scan(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
                  const float* qnorm, const ScanItem* items, const int32_t* n_items,
@@ -161,7 +170,7 @@ float coarse_coef(int metric, int dp, bool split, int ks);
 void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64_t lda, int B, ListTable lt,
                         const float* cnrm, const float* Qd, const float* qn2,
                         const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,
-                        uint32_t* probe_key, int32_t* ncand, cudaStream_t st);
+                        uint32_t* probe_key, int32_t* ncand, const RouteArgs& ra, cudaStream_t st);
 
 // Cold tier: copy host-arena rows [src_row, src_row+n) (pinned, device-mapped)
 // to HBM arena rows [dst_row, ...), with ids and squared norms.
