@@ -257,13 +257,17 @@ def build_shard(a, rank, dev):
         N.check(N.lib().pk_kmeans_assign(X.data_ptr(), a.n, cents.data_ptr(), a.nlist, a.d,
                                          labels.data_ptr(), dists.data_ptr(), N.PK_DEVICE_PTRS))
         sums = torch.zeros(a.nlist, a.d, dtype=torch.float64, device=dev)
-        sums.index_add_(0, labels, X.double())
+        for i in range(0, a.n, 1 << 20):  # fp64 sums in row chunks (10M x 768 would need 61 GB)
+            sums.index_add_(0, labels[i:i + (1 << 20)], X[i:i + (1 << 20)].double())
         cnt = torch.bincount(labels, minlength=a.nlist).clamp(min=1).double()
         cents = (sums / cnt[:, None]).float().contiguous()
     order = torch.argsort(labels, stable=True)
-    Xs = X[order].contiguous()
-    ids_sorted = (order + rank * a.n).contiguous()
     lens = torch.bincount(labels, minlength=a.nlist).cpu().numpy().astype(np.int64)
+    del labels, dists
+    Xs = X[order].contiguous()
+    del X
+    ids_sorted = (order + rank * a.n).contiguous()
+    torch.cuda.empty_cache()  # the index arena is cudaMalloc'd outside torch's cache
     offs = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
     torch.cuda.synchronize()
     return base, Xs, ids_sorted, lens, offs
@@ -304,7 +308,7 @@ def run_ours(a):
     t_build = time.perf_counter()
     dev = torch.device("cuda", local)
     base, Xs, ids_sorted, lens, offs = build_shard(a, rank, dev)
-    reserve = dict(reserve_rows=int(a.n * 1.3) + 4096, reserve_lists=a.nlist * world)
+    reserve = dict(reserve_rows=int(a.n * 1.26) + 32 * a.nlist + 4096, reserve_lists=a.nlist * world)
     sh = None
     if world == 1:
         ix = DeviceIndex(a.d, 0, local, **reserve)

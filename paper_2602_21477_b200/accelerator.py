@@ -1,0 +1,164 @@
+"""NativeAccelerator: the reference's executor plugin protocol on the B200
+(layer 2; protocol of ``SimulatedAccelerator``,
+ref/tiering.py:85-147).
+
+For a maintainer who keeps the reference's own ``TierManager`` and swaps only
+the executor (``StoreConfig(accelerator=...)`` -> this class), every call
+maps onto the device index of this package:
+
+  alloc(nbytes)               -> a fresh empty posting list (the handle)
+  upload(h, mat, ids, local)  -> appended rows (ref upload appends, tiering.py:112-123)
+  release(h, nbytes)          -> list retired, HBM range freed
+  scan(h, q, metric)          -> (ids, distances) of the snapshot in row order,
+                                 reference arithmetic on the device
+                                 (pk_scan_lists; batch_distances semantics)
+  kmeans(mat, k, rng, delta)  -> kmeans_split_points on the device, consuming
+                                 ``rng`` exactly like the reference (F6)
+
+plus the observable attributes the reference and its tests read:
+``allocated_bytes``, ``call_log``, ``simulated_us`` (cost-model accounting,
+unchanged), ``fail_next_alloc`` / ``fail_next_scan`` and ``_mem[handle] ->
+(mat, ids)`` (read back from the device, tiering.py:387-390).  Errors raise
+``AcceleratorError`` as the protocol expects.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from .clusters import kmeans_split_points
+from .core import AcceleratorError, Metric
+from .index import DeviceIndex
+from .tiering import CostModel
+
+
+class _MemView:
+    """``accel._mem[handle] -> (mat f32[n, d], ids i64[n])`` read from HBM."""
+
+    def __init__(self, acc: "NativeAccelerator"):
+        self._acc = acc
+
+    def __contains__(self, handle) -> bool:
+        return handle in self._acc._live
+
+    def __getitem__(self, handle):
+        if handle not in self._acc._live:
+            raise KeyError(handle)
+        return self._acc._read(handle)
+
+    def get(self, handle, default=None):
+        return self[handle] if handle in self._acc._live else default
+
+    def pop(self, handle, default=None):
+        if handle not in self._acc._live:
+            return default
+        out = self._acc._read(handle)
+        self._acc._drop(handle)
+        return out
+
+    def __len__(self):
+        return len(self._acc._live)
+
+
+class NativeAccelerator:
+    kind = "accelerator"
+    capabilities = frozenset({"scan", "kmeans"})
+
+    def __init__(self, model: CostModel | None = None, dimension: int | None = None,
+                 metric: Metric = Metric.SQUARED_EUCLIDEAN, device: int = 0):
+        self.model = model or CostModel()
+        self.call_log: list[tuple] = []
+        self.simulated_us = 0.0
+        self.allocated_bytes = 0
+        self.fail_next_alloc = False
+        self.fail_next_scan = False
+        self._metric = metric
+        self._device = device
+        self._dimension = dimension
+        self._index: DeviceIndex | None = None
+        self._next_handle = 0
+        self._live: dict[int, int] = {}  # handle -> rows held
+        self._mem = _MemView(self)
+
+    # ---- device index (created at the first upload: the dimension is the
+    # first matrix's width unless given) ----------------------------------------
+    def _ix(self, d: int) -> DeviceIndex:
+        if self._index is None:
+            self._dimension = self._dimension or d
+            self._index = DeviceIndex(self._dimension, self._metric.wire_code, self._device)
+        if d != self._dimension:
+            raise AcceleratorError(f"dimension mismatch: {d} vs {self._dimension}")
+        return self._index
+
+    def _read(self, handle):
+        n = self._live[handle]
+        if n == 0 or self._index is None:
+            return (np.empty((0, 0), dtype=np.float32), np.empty(0, dtype=np.int64))
+        rows, ids = self._index.read(handle)
+        return rows, ids
+
+    def _drop(self, handle):
+        if self._live.pop(handle, 0) > 0 and self._index is not None:
+            self._index.retire(handle)
+
+    # ---- protocol (ref/tiering.py:101-147) -------------------------------
+    def alloc(self, nbytes: int) -> int:
+        if self.fail_next_alloc:
+            self.fail_next_alloc = False
+            raise AcceleratorError("allocation failed")
+        handle = self._next_handle
+        self._next_handle += 1
+        self._live[handle] = 0
+        self.allocated_bytes += nbytes
+        self.simulated_us += self.model.alloc_us
+        self.call_log.append(("alloc", handle, nbytes))
+        return handle
+
+    def upload(self, handle: int, mat: np.ndarray, ids: np.ndarray, tier_local: bool):
+        if handle not in self._live:
+            raise AcceleratorError(f"unknown handle {handle}")
+        mat = np.ascontiguousarray(mat, dtype=np.float32)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        if len(ids):
+            ix = self._ix(mat.shape[1])
+            if self._live[handle] == 0:  # first rows: the list comes into existence
+                ix.create_list(handle, 0, mat, ids)
+            else:
+                ix.append(handle, mat, ids)
+            self._live[handle] += len(ids)
+        kb = (self._live[handle] * (self._dimension or 0) * 4) / 1024.0
+        rate = self.model.tier_local_per_kb_us if tier_local else self.model.cross_tier_per_kb_us
+        self.simulated_us += kb * rate
+        self.call_log.append(("upload", handle, len(ids), tier_local))
+
+    def release(self, handle: int, nbytes: int):
+        if handle in self._live:
+            self._drop(handle)
+        self.allocated_bytes -= nbytes
+        self.call_log.append(("release", handle))
+
+    def scan(self, handle: int, q: np.ndarray, metric: Metric):
+        if self.fail_next_scan:
+            self.fail_next_scan = False
+            raise AcceleratorError("device scan failed")
+        if handle not in self._live:
+            raise AcceleratorError(f"unknown handle {handle}")
+        n = self._live[handle]
+        self.call_log.append(("scan", handle, n))
+        self.simulated_us += self.model.accel_scan_us(n)
+        if n == 0:
+            return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float32)
+        if metric is not self._metric:
+            raise AcceleratorError(f"index built for {self._metric}, scan asked {metric}")
+        ids, dists, _ = self._index.scan_lists(np.asarray(q, dtype=np.float32), [handle], n)
+        return ids, dists
+
+    def kmeans(self, mat, k, rng, base_delta):
+        self.call_log.append(("kmeans", len(mat), k))
+        self.simulated_us += self.model.accel_scan_us(len(mat)) * k
+        return kmeans_split_points(np.ascontiguousarray(mat, dtype=np.float32), k, rng, base_delta)
+
+    def close(self):
+        if self._index is not None:
+            self._index.close()
+            self._index = None
