@@ -106,6 +106,16 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def load_read_peak():
+    """Read-only streaming peak measured on this hardware
+    (tools/microbench/hbm_read.cu -> profiles/hbm_read_peak.json)."""
+    p = os.path.join(ROOT, "profiles", "hbm_read_peak.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["read_gbs"])
+    return None
+
+
 def load_traffic():
     p = os.path.join(ROOT, "profiles", "scan_ncu_traffic.json")
     if os.path.exists(p):
@@ -426,6 +436,7 @@ def run_ours(a):
     scan_ms = stage_ms["scan"] / max(ncalls, 1)
     achieved = float(np.mean(alg_bytes)) / (scan_ms / 1000.0) / 1e9
     peak, peak_src = load_peaks()
+    read_peak = load_read_peak()
     traffic = load_traffic()
 
     # ---- e2e through the public API with host buffers (pinned queries in,
@@ -505,7 +516,9 @@ def run_ours(a):
                          "kernel": "scan_tc_kernel<SQ_L2> (TMA-fed tcgen05 TF32-screened posting-list "
                                    "scan + per-list top-k bounds)",
                          "algorithmic_bytes_per_launch": float(np.mean(alg_bytes)),
-                         "kernel_ms_per_launch": scan_ms, "peak_source": peak_src},
+                         "kernel_ms_per_launch": scan_ms, "peak_source": peak_src,
+                         "read_only_peak": read_peak,
+                         "frac_of_read_only_peak": (achieved / read_peak) if read_peak else None},
             "stage_ms_per_step": {k_: v / max(ncalls, 1) for k_, v in stage_ms.items()},
             "gpu_launches": a.steps * per_step,
             "clocks": clk.summary(),
