@@ -366,13 +366,30 @@ def run_ours(a):
                 "send": torch.empty(world * bb, dtype=torch.uint8, device=dev),
                 "recv": torch.empty(world * bb, dtype=torch.uint8, device=dev)}
 
+    # N>1 combine: results written straight into their origin rank's HBM over
+    # NVLink (CUDA IPC + device flags, PK_COMBINE=peer, default) or an NCCL
+    # all-to-all (PK_COMBINE=nccl, or when the peer mapping cannot be set up)
+    combine = None
+    if sh is not None:
+        combine = os.environ.get("PK_COMBINE", "peer")
+        if combine == "peer":
+            try:
+                sh.setup_peer_combine(a.batch, kk)
+            except Exception as exc:  # no P2P mapping between these devices
+                print(f"peer combine unavailable ({exc}); using NCCL all-to-all", file=sys.stderr)
+                combine = "nccl"
+
     def step(s):
         if sh is None:
             ix.search_device(Qall[s], codes, a.nprobe, kk, o_ids, o_d, o_c, o_n, o_s)
         else:
             with torch.cuda.stream(stream):
-                sh.search_dispatch_device(Qall[s], codes, a.nprobe, kk, bufs, o_ids, o_d, o_c,
-                                          o_n, o_s)
+                if combine == "peer":
+                    sh.search_dispatch_peer(Qall[s], codes, a.nprobe, kk, bufs, o_ids, o_d, o_c,
+                                            o_n, o_s)
+                else:
+                    sh.search_dispatch_device(Qall[s], codes, a.nprobe, kk, bufs, o_ids, o_d, o_c,
+                                              o_n, o_s)
 
     for w in range(a.warmup):
         step(w)
@@ -393,6 +410,8 @@ def run_ours(a):
         torch.cuda.synchronize()
     stage_ms, ncalls = ix.profile_end()
     ms = ev0.elapsed_time(ev1)
+    if combine == "peer" and ix.combine_status() != 0:
+        raise RuntimeError("peer combine timed out waiting for a rank's results")
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -509,8 +528,11 @@ def run_ours(a):
                        "l2": "inputs larger than L2 (index 3.1 GB per GPU; each batch reads "
                              "~all lists)",
                        "parallelism": f"list-sharded x{world}" + (
-                           ", dispatch (NCCL all-gather of queries + list handles) / combine "
-                           "(NCCL all-to-all of per-shard top-k, device merge)" if world > 1 else "")},
+                           ", dispatch (NCCL all-gather of queries + list handles) / combine ("
+                           + ("per-shard top-k written into the origin rank's HBM over NVLink P2P, "
+                              "device flags, device merge" if combine == "peer" else
+                              "NCCL all-to-all of per-shard top-k, device merge") + ")"
+                           if world > 1 else "")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                          "kernel": "scan_tc_kernel<SQ_L2> (TMA-fed tcgen05 TF32-screened posting-list "

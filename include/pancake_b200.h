@@ -190,6 +190,27 @@ int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int3
                     int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
                     int64_t* out_scanned, int flags);
 
+/* ---- peer combine (fused combine over NVLink P2P) --
+ * The combine step of dispatch/combine without NCCL: every rank owns a
+ * receive area (R shard blocks + R ready flags) in its HBM, exported as a CUDA
+ * IPC handle (64 bytes) and mapped by the peers.  pk_combine_search_probed runs
+ * the scan stage for the gathered batch (R x group queries) and writes block g
+ * of its results STRAIGHT INTO rank g's area (P2P stores), then publishes
+ * flag[my_rank] = epoch in every area (system-scope release).  pk_combine_merge
+ * acquires all R flags of `epoch` on the device (bounded wait; a timeout sets
+ * the error word read by pk_combine_status) and merges, as pk_merge_shards.
+ * pk_combine_open: peer's IPC handle, or area_ptr for ranks in the same
+ * process.  Device pointers only (PK_DEVICE_PTRS); epochs strictly increase. */
+int pk_combine_create(pk_index* ix, int32_t R, int32_t my_rank, int64_t group, int32_t kk,
+                      void* ipc_handle_out);
+int pk_combine_open(pk_index* ix, int32_t peer, const void* ipc_handle, void* area_ptr);
+void* pk_combine_area(pk_index* ix);
+int pk_combine_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe,
+                             int32_t nprobe, int64_t epoch, int flags);
+int pk_combine_merge(pk_index* ix, int64_t epoch, double timeout_s, int64_t* out_ids, float* out_dists,
+                     int64_t* out_cids, int32_t* out_n, int64_t* out_scanned, int flags);
+int pk_combine_status(pk_index* ix, int32_t* err);
+
 /* ---- measurement ------------------------------------------------------ */
 /* Between begin and end every pk_search records CUDA events on the index
  * stream around its stages: [0] input copy, [1] coarse distances,

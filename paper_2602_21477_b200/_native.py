@@ -72,6 +72,12 @@ _SIGS = [
     ("pk_tier_stats", [_vp, _vp, _int], _int),
     ("pk_search_coarse_cids", [_vp, _vp, _i64, _vp, _i32, _i32, _vp], _int),
     ("pk_scan_lists", [_vp, _vp, _vp, _i32, _vp, _vp, _vp], _int),
+    ("pk_combine_create", [_vp, _i32, _i32, _i64, _i32, _vp], _int),
+    ("pk_combine_open", [_vp, _i32, _vp, _vp], _int),
+    ("pk_combine_area", [_vp], _vp),
+    ("pk_combine_search_probed", [_vp, _vp, _i64, _vp, _i32, _i64, _int], _int),
+    ("pk_combine_merge", [_vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _int], _int),
+    ("pk_combine_status", [_vp, _vp], _int),
     ("pk_list_add_remote", [_vp, _i64, _i32, _vp], _int),
     ("pk_shard_block_bytes", [_i64, _i32], _i64),
     ("pk_merge_shards", [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _int], _int),

@@ -153,6 +153,20 @@ struct pk_index {
   uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
   size_t hout_bytes = 0;
 
+  // ---- peer combine (pk_combine_*): this rank's receive area (R shard blocks
+  // + R flags, IPC-exported) and the peers' areas mapped into this process
+  struct Combine {
+    int R = 0, my_rank = 0, kk = 0;
+    int64_t group = 0, bb = 0;
+    uint8_t* area = nullptr;                 // own area (cudaMalloc)
+    std::vector<uint8_t*> peers;             // [R] area base per rank (own / IPC / in-process)
+    std::vector<uint8_t*> opened;            // IPC mappings to close
+    uint8_t** d_peers = nullptr;
+    bool peers_dirty = true;
+    uint32_t* done_ctr = nullptr;
+    int32_t* err = nullptr;
+  } comb;
+
   // ---- cold tier (pk_index_enable_tier).  Every list keeps a copy in a
   // pinned, device-mapped host arena -- the source of truth, as the
   // reference's host rows are (ref/tiering.py:9-12) -- and HBM holds the
@@ -752,6 +766,10 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->stage_ev) cudaEventDestroy(ix->stage_ev);
   if (ix->mst) cudaStreamDestroy(ix->mst);
   if (ix->hout) cudaFreeHost(ix->hout);
+  for (uint8_t* p : ix->comb.opened) cudaIpcCloseMemHandle(p);
+  if (ix->comb.area) cudaFree(ix->comb.area);
+  if (ix->comb.d_peers) cudaFree(ix->comb.d_peers);
+  if (ix->comb.done_ctr) cudaFree(ix->comb.done_ctr);
   if (ix->hrows) cudaFreeHost(ix->hrows);
   if (ix->hids) cudaFreeHost(ix->hids);
   ix->stage_desc.release();
@@ -1552,6 +1570,112 @@ int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* pro
     CK(cudaMemcpyAsync(out_blocks, dst, (size_t)(B / group) * bb, cudaMemcpyDeviceToHost, ix->st));
     CK(cudaStreamSynchronize(ix->st));
   }
+  return PK_OK;
+}
+
+int pk_combine_create(pk_index* ix, int32_t R, int32_t my_rank, int64_t group, int32_t kk,
+                      void* ipc_handle_out) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  if (R < 1 || my_rank < 0 || my_rank >= R || group < 1 || kk < 1 || kk > KKMAX)
+    return fail(PK_ERR_USAGE, "bad combine shape");
+  if ((int64_t)R * kk > shard_merge_cap()) return fail(PK_ERR_USAGE, "ranks x kk above %d", shard_merge_cap());
+  CK(cudaSetDevice(ix->device));
+  auto& c = ix->comb;
+  if (c.area) return fail(PK_ERR_USAGE, "combine area exists");
+  c.R = R;
+  c.my_rank = my_rank;
+  c.group = group;
+  c.kk = kk;
+  c.bb = pk_shard_block_bytes(group, kk);
+  const size_t bytes = (size_t)R * c.bb + (size_t)R * 128;
+  CK(cudaMalloc((void**)&c.area, bytes));
+  CK(cudaMemset(c.area, 0, bytes));  // flags start at epoch 0
+  CK(cudaMalloc((void**)&c.d_peers, (size_t)R * sizeof(uint8_t*)));
+  CK(cudaMalloc((void**)&c.done_ctr, 64));
+  c.err = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(c.done_ctr) + 32);
+  CK(cudaMemset(c.done_ctr, 0, 64));
+  c.peers.assign(R, nullptr);
+  c.peers[my_rank] = c.area;
+  c.peers_dirty = true;
+  if (ipc_handle_out) {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c.area));
+    memcpy(ipc_handle_out, &h, sizeof(h));
+  }
+  return PK_OK;
+}
+
+int pk_combine_open(pk_index* ix, int32_t peer, const void* ipc_handle, void* area_ptr) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  auto& c = ix->comb;
+  if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
+  if (peer < 0 || peer >= c.R) return fail(PK_ERR_USAGE, "bad peer %d", peer);
+  if (peer == c.my_rank) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  if (area_ptr) {  // same process (simulated ranks)
+    c.peers[peer] = static_cast<uint8_t*>(area_ptr);
+  } else {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, ipc_handle, sizeof(h));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c.peers[peer] = static_cast<uint8_t*>(p);
+    c.opened.push_back(static_cast<uint8_t*>(p));
+  }
+  c.peers_dirty = true;
+  return PK_OK;
+}
+
+void* pk_combine_area(pk_index* ix) { return ix ? ix->comb.area : nullptr; }
+
+int pk_combine_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe,
+                             int32_t nprobe, int64_t epoch, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  auto& c = ix->comb;
+  if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
+  if (!(flags & PK_DEVICE_PTRS)) return fail(PK_ERR_USAGE, "peer combine takes device pointers");
+  if (B != (int64_t)c.R * c.group) return fail(PK_ERR_USAGE, "batch must be ranks x group");
+  for (uint8_t* p : c.peers)
+    if (!p) return fail(PK_ERR_USAGE, "a peer area is not open");
+  const int kk = c.kk;
+  RET(ix->pb.ensure((size_t)B * kk * 20 + B * 12 + 64));
+  int64_t* o_ids = ix->pb.as<int64_t>();
+  int64_t* o_cid = o_ids + B * kk;
+  int64_t* o_sc = o_cid + B * kk;
+  float* o_d = reinterpret_cast<float*>(o_sc + B);
+  int32_t* o_n = reinterpret_cast<int32_t*>(o_d + B * kk);
+  RET(search_core(ix, Q, B, nullptr, 0, nprobe, kk, o_ids, o_d, o_cid, o_n, nullptr, o_sc, true,
+                  true, probe, nullptr));
+  if (c.peers_dirty) {
+    CK(cudaMemcpyAsync(c.d_peers, c.peers.data(), (size_t)c.R * sizeof(uint8_t*), cudaMemcpyHostToDevice,
+                       ix->st));
+    c.peers_dirty = false;
+  }
+  CK(cudaMemsetAsync(c.done_ctr, 0, 4, ix->st));
+  launch_peer_send(o_ids, o_cid, o_sc, o_d, o_n, (int)B, (int)c.group, kk, c.bb, c.d_peers, c.R,
+                   c.my_rank, (uint64_t)epoch, c.done_ctr, ix->st);
+  CK(cudaGetLastError());
+  return PK_OK;
+}
+
+int pk_combine_merge(pk_index* ix, int64_t epoch, double timeout_s, int64_t* out_ids, float* out_dists,
+                     int64_t* out_cids, int32_t* out_n, int64_t* out_scanned, int flags) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  auto& c = ix->comb;
+  if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
+  if (!(flags & PK_DEVICE_PTRS)) return fail(PK_ERR_USAGE, "peer combine takes device pointers");
+  CK(cudaSetDevice(ix->device));
+  launch_peer_merge(c.area, c.bb, c.R, (int)c.group, c.kk, (uint64_t)epoch, (int64_t)(timeout_s * 1e9),
+                    c.err, out_ids, out_dists, out_cids, out_n, out_scanned, ix->st);
+  CK(cudaGetLastError());
+  return PK_OK;
+}
+
+int pk_combine_status(pk_index* ix, int32_t* err) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  if (!ix->comb.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
+  CK(cudaMemcpyAsync(err, ix->comb.err, 4, cudaMemcpyDeviceToHost, ix->st));
+  CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 

@@ -1407,7 +1407,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    const QPair* __restrict__ qpairs, int kk, float coef,
                    int32_t* __restrict__ work_ctr, uint32_t* __restrict__ Uq,
                    uint32_t* __restrict__ slot_hi, int32_t* __restrict__ slot_n,
-                   int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap) {
+                   int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap, int dbg_skip) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ScanShared S;
@@ -1562,7 +1562,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             (METRIC == SQ_L2) ? __fsub_rn(__fadd_rn(S.NX[row], nq2_s[a]), __fmul_rn(2.f, dot)) : -dot;
       }
       named_bar_sync(1, nthr);
-      for (int a = warp; a < nq; a += TC_EPI_WARPS)
+      for (int a = warp; a < nq && !dbg_skip; a += TC_EPI_WARPS)
         screen_select(S, a, item.nrows, kk, coef, nq2_s[a], qb_s[a], item.lslot, rbase,
                       (int64_t)qpairs[item.qoff + a].slotbase + item.chunk, Uq, slot_hi, slot_n,
                       cpool, ccount, cap);
@@ -1627,13 +1627,16 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   const size_t smem = tc_smem_bytes();
   const int grid = std::min(num_sms, max_items);
   const float coef = screen_coef_tf32(metric, lt.dp);
+  // PK_DEBUG_SCAN_NOSELECT=1: skip the per-(query, item) selection (timing
+  // experiments only -- results are wrong)
+  static const int dbg_skip = getenv("PK_DEBUG_SCAN_NOSELECT") ? atoi(getenv("PK_DEBUG_SCAN_NOSELECT")) : 0;
 #define PK_TC(M)                                                                                 \
   {                                                                                              \
     auto k = scan_tc_kernel<M>;                                                                  \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
     k<<<grid, TC_THREADS, smem, st>>>(maps, lt, qsw, (int64_t)B, qnorm2, items, n_items, qpairs, \
                                       kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool, ccount,    \
-                                      cap);                                                      \
+                                      cap, dbg_skip);                                            \
   }
   if (metric == SQ_L2) PK_TC(SQ_L2)
   else PK_TC(IP)
@@ -2861,6 +2864,169 @@ void launch_lists_dist(int metric, const float* q, const float* qn, const ListSr
   if (metric == SQ_L2) lists_dist_kernel<SQ_L2><<<grid, 128, 0, st>>>(q, qn, src, prefix, m, dp, d, out_d, out_ids);
   else if (metric == IP) lists_dist_kernel<IP><<<grid, 128, 0, st>>>(q, qn, src, prefix, m, dp, d, out_d, out_ids);
   else lists_dist_kernel<COSINE><<<grid, 128, 0, st>>>(q, qn, src, prefix, m, dp, d, out_d, out_ids);
+}
+
+}  // namespace pk
+
+namespace pk {
+
+// =====================================================================
+// Peer combine (the combine half of dispatch/combine,
+// fused with the result write-out): instead of writing local result blocks
+// and running an NCCL all-to-all, the scan's per-query results are written
+// straight into each origin rank's receive area in ITS HBM (CUDA IPC
+// mapping; P2P stores over NVLink / NVSwitch), then flagged:
+//   peer_send_kernel   block g of this rank's results -> peer g's area, slot
+//                      my_rank; every CTA fences at system scope and counts
+//                      itself; the last CTA publishes flag[my_rank] = epoch in
+//                      every peer's area with a release store.
+//   peer_merge_kernel  each query's CTA acquires all R flags of the epoch
+//                      (bounded spin; timeout -> error word), then merges the
+//                      R blocks exactly like shard_merge_kernel.
+// Area layout: R shard blocks of block_bytes, then R flags of 128 bytes.
+// =====================================================================
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void peer_send_kernel(const int64_t* __restrict__ ids, const int64_t* __restrict__ cids,
+                                 const int64_t* __restrict__ sc, const float* __restrict__ d,
+                                 const int32_t* __restrict__ n, int B, int group, int kk,
+                                 int64_t block_bytes, uint8_t* const* __restrict__ peers, int R,
+                                 int my_rank, uint64_t epoch, uint32_t* __restrict__ done_ctr) {
+  const int64_t nkk_g = (int64_t)group * kk;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)B * kk;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(i / kk), e = (int)(i - (int64_t)b * kk);
+    const int g = b / group, bl = b - g * group;
+    uint8_t* blk = peers[g] + (int64_t)my_rank * block_bytes;
+    const int64_t o = (int64_t)bl * kk + e;
+    reinterpret_cast<int64_t*>(blk)[o] = ids[i];
+    reinterpret_cast<int64_t*>(blk + 8 * nkk_g)[o] = cids[i];
+    reinterpret_cast<float*>(blk + 16 * nkk_g + 8 * (int64_t)group)[o] = d[i];
+    if (e == 0) {
+      reinterpret_cast<int64_t*>(blk + 16 * nkk_g)[bl] = sc[b];
+      reinterpret_cast<int32_t*>(blk + 20 * nkk_g + 8 * (int64_t)group)[bl] = n[b];
+    }
+  }
+  __threadfence_system();  // this CTA's stores before its arrival
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(done_ctr, 1u);
+    if ((prev + 1) % gridDim.x == 0) {  // last CTA of this launch: publish the epoch
+      __threadfence_system();
+      for (int g = 0; g < R; g++)
+        st_release_sys(reinterpret_cast<uint64_t*>(peers[g] + (int64_t)R * block_bytes) + 16 * my_rank,
+                       epoch);
+    }
+  }
+}
+
+void launch_peer_send(const int64_t* ids, const int64_t* cids, const int64_t* sc, const float* d,
+                      const int32_t* n, int B, int group, int kk, int64_t block_bytes,
+                      uint8_t* const* peers, int R, int my_rank, uint64_t epoch, uint32_t* done_ctr,
+                      cudaStream_t st) {
+  const int64_t tot = (int64_t)B * kk;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 592));
+  peer_send_kernel<<<grid, 256, 0, st>>>(ids, cids, sc, d, n, B, group, kk, block_bytes, peers, R,
+                                         my_rank, epoch, done_ctr);
+}
+
+__global__ void __launch_bounds__(128) peer_merge_kernel(const uint8_t* __restrict__ area,
+                                                         int64_t block_bytes, int R, int B, int kk,
+                                                         uint64_t epoch, int64_t timeout_ns,
+                                                         int32_t* __restrict__ err,
+                                                         int64_t* __restrict__ out_ids,
+                                                         float* __restrict__ out_d,
+                                                         int64_t* __restrict__ out_cid,
+                                                         int32_t* __restrict__ out_n,
+                                                         int64_t* __restrict__ out_scanned) {
+  extern __shared__ Entry sbuf[];
+  __shared__ int s_cnt, s_ok;
+  const uint64_t* flags = reinterpret_cast<const uint64_t*>(area + (int64_t)R * block_bytes);
+  if (threadIdx.x == 0) {
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int ok = 1;
+    for (int r = 0; r < R && ok; r++) {
+      while (ld_acquire_sys(flags + 16 * r) < epoch) {
+        __nanosleep(200);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if ((int64_t)(t - t0) > timeout_ns) {
+          ok = 0;
+          atomicExch(err, 1);
+          break;
+        }
+      }
+    }
+    s_ok = ok;
+    s_cnt = 0;
+  }
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int64_t nkk = (int64_t)B * kk;
+  if (!s_ok) {
+    for (int i = threadIdx.x; i < kk; i += blockDim.x) out_ids[(int64_t)b * kk + i] = -1;
+    if (threadIdx.x == 0) out_n[b] = 0;
+    return;
+  }
+  const int total = R * kk;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int r = i / kk, e = i - r * kk;
+    const uint8_t* blk = area + (int64_t)r * block_bytes;
+    const int32_t n = reinterpret_cast<const int32_t*>(blk + (nkk * 20 + (int64_t)B * 8))[b];
+    if (e >= n) continue;
+    Entry en;
+    en.key = f2key(reinterpret_cast<const float*>(blk + nkk * 16 + (int64_t)B * 8)[(int64_t)b * kk + e]);
+    en.id = reinterpret_cast<const int64_t*>(blk)[(int64_t)b * kk + e];
+    en.pay = i;
+    sbuf[atomicAdd(&s_cnt, 1)] = en;
+  }
+  __syncthreads();
+  const int n = s_cnt;
+  cta_bitonic_sort(sbuf, n);
+  const int kept = cta_compact_sorted(sbuf, n, kk, true, &s_cnt);
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) {
+    const int64_t o = (int64_t)b * kk + i;
+    if (i < kept) {
+      const int src = sbuf[i].pay;
+      const int r = src / kk, e = src - r * kk;
+      out_ids[o] = sbuf[i].id;
+      out_d[o] = key2f(sbuf[i].key);
+      if (out_cid)
+        out_cid[o] = reinterpret_cast<const int64_t*>(area + (int64_t)r * block_bytes + nkk * 8)[(int64_t)b * kk + e];
+    } else {
+      out_ids[o] = -1;
+      out_d[o] = __int_as_float(0x7f800000);
+      if (out_cid) out_cid[o] = -1;
+    }
+  }
+  if (threadIdx.x == 0) {
+    out_n[b] = kept;
+    if (out_scanned) {
+      int64_t s = 0;
+      for (int r = 0; r < R; r++)
+        s += reinterpret_cast<const int64_t*>(area + (int64_t)r * block_bytes + nkk * 16)[b];
+      out_scanned[b] = s;
+    }
+  }
+}
+
+void launch_peer_merge(const void* area, int64_t block_bytes, int R, int B, int kk, uint64_t epoch,
+                       int64_t timeout_ns, int32_t* err, int64_t* out_ids, float* out_d,
+                       int64_t* out_cid, int32_t* out_n, int64_t* out_scanned, cudaStream_t st) {
+  if (B <= 0) return;
+  int N = 1;
+  while (N < R * kk) N <<= 1;
+  const size_t smem = (size_t)N * sizeof(Entry);
+  cudaFuncSetAttribute(peer_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  peer_merge_kernel<<<B, 128, smem, st>>>(static_cast<const uint8_t*>(area), block_bytes, R, B, kk, epoch,
+                                          timeout_ns, err, out_ids, out_d, out_cid, out_n, out_scanned);
 }
 
 }  // namespace pk

@@ -200,4 +200,14 @@ void launch_lists_dist(int metric, const float* q, const float* qn, const ListSr
                        int m, int64_t total, int dp, int d, float* out_d, int64_t* out_ids,
                        cudaStream_t st);
 
+// Peer combine: results -> peers' receive areas (IPC-mapped) + release flags;
+// merge after acquiring every rank's flag for the epoch (bounded wait, *err).
+void launch_peer_send(const int64_t* ids, const int64_t* cids, const int64_t* sc, const float* d,
+                      const int32_t* n, int B, int group, int kk, int64_t block_bytes,
+                      uint8_t* const* peers, int R, int my_rank, uint64_t epoch, uint32_t* done_ctr,
+                      cudaStream_t st);
+void launch_peer_merge(const void* area, int64_t block_bytes, int R, int B, int kk, uint64_t epoch,
+                       int64_t timeout_ns, int32_t* err, int64_t* out_ids, float* out_d,
+                       int64_t* out_cid, int32_t* out_n, int64_t* out_scanned, cudaStream_t st);
+
 }  // namespace pk

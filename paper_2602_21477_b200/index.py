@@ -352,6 +352,37 @@ class DeviceIndex:
                                          int(probe.shape[1]), int(kk), int(group),
                                          N.ptr(out_blocks), N.PK_DEVICE_PTRS))
 
+    # ---- peer combine (pk_combine_*) -----------------------------------------
+    def combine_create(self, R: int, my_rank: int, group: int, kk: int) -> bytes:
+        """Receive area for the peer combine; returns its 64-byte IPC handle."""
+        self.flush()
+        h = ctypes.create_string_buffer(64)
+        N.check(N.lib().pk_combine_create(self._h, int(R), int(my_rank), int(group), int(kk), h))
+        return h.raw
+
+    def combine_open(self, peer: int, handle: bytes | None = None, area_ptr: int | None = None):
+        buf = ctypes.create_string_buffer(handle, 64) if handle is not None else None
+        N.check(N.lib().pk_combine_open(self._h, int(peer), buf, area_ptr))
+
+    def combine_area(self) -> int:
+        return int(N.lib().pk_combine_area(self._h) or 0)
+
+    def combine_search_probed_device(self, Q, probe, epoch: int):
+        self.flush()
+        N.check(N.lib().pk_combine_search_probed(self._h, N.ptr(Q), int(Q.shape[0]), N.ptr(probe),
+                                                 int(probe.shape[1]), int(epoch), N.PK_DEVICE_PTRS))
+
+    def combine_merge_device(self, epoch: int, out_ids, out_d, out_cid, out_n, out_scanned=None,
+                             timeout_s: float = 10.0):
+        N.check(N.lib().pk_combine_merge(self._h, int(epoch), float(timeout_s), N.ptr(out_ids),
+                                         N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), N.ptr(out_scanned),
+                                         N.PK_DEVICE_PTRS))
+
+    def combine_status(self) -> int:
+        v = ctypes.c_int32(0)
+        N.check(N.lib().pk_combine_status(self._h, ctypes.byref(v)))
+        return int(v.value)
+
     def merge_shards(self, blocks, R: int, B: int, kk: int):
         """Host: blocks uint8[R * block_bytes] -> (ids, dists, cids, counts, scanned)."""
         blocks = np.ascontiguousarray(blocks, dtype=np.uint8)

@@ -247,3 +247,34 @@ class ShardedIndex:
             src = bufs["send"]
         self.local.merge_shards_device(src, self.world, B, kk, out_ids, out_d, out_cid, out_n,
                                        out_scanned)
+
+    # ---- fused combine over peer memory ----------------------------------------
+    def setup_peer_combine(self, B: int, kk: int):
+        """Map every rank's receive area into this process (CUDA IPC handles
+        exchanged over the process group); afterwards search_dispatch_device
+        can combine by P2P stores instead of an all-to-all."""
+        handle = self.local.combine_create(self.world, self.rank, B, kk)
+        if self.world > 1:
+            handles = [None] * self.world
+            self.dist.all_gather_object(handles, handle, group=self.group)
+            for r, h in enumerate(handles):
+                if r != self.rank:
+                    self.local.combine_open(r, handle=h)
+        self._epoch = 0
+
+    def search_dispatch_peer(self, Q, scope_codes, nprobe: int, kk: int, bufs: dict, out_ids,
+                             out_d, out_cid, out_n, out_scanned=None):
+        """search_dispatch_device with the combine fused into the scan's
+        write-out: results go straight into their origin rank's HBM (P2P) and
+        the merge waits on device-side flags -- no all-to-all."""
+        self._epoch += 1
+        self.local.search_coarse_device(Q, scope_codes, nprobe, bufs["probe"])
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(bufs["q_all"], Q, group=self.group)
+            self.dist.all_gather_into_tensor(bufs["probe_all"], bufs["probe"], group=self.group)
+            qa, pa = bufs["q_all"], bufs["probe_all"]
+        else:
+            qa, pa = Q, bufs["probe"]
+        self.local.combine_search_probed_device(qa, pa, self._epoch)
+        self.local.combine_merge_device(self._epoch, out_ids, out_d, out_cid, out_n, out_scanned)
+

@@ -144,3 +144,65 @@ def test_device_dispatch_combine_equals_single_index(R):
         assert np.array_equal(sc, ref.scanned[sl])
     for ix in shards + [single]:
         ix.close()
+
+
+def test_peer_combine_in_process_equals_single_index():
+    """The fused combine (P2P stores into each origin's area + device flags),
+    R ranks simulated in one process: two epochs, every rank's answers equal
+    the single index's."""
+    from paper_2602_21477_b200 import DeviceIndex
+    import torch
+
+    R, d, nlist, nprobe, kk, B = 3, 64, 36, 7, 10, 16
+    lists, Q = _lists(5150, nlist, d, 500)
+    cids = np.arange(nlist, dtype=np.int64) + 70
+    owners = place_lists([len(i) for i, _ in lists], R)
+    single = DeviceIndex(d)
+    cents = [single.create_list(int(c), 0, r, i) for c, (i, r) in zip(cids, lists)]
+    shards = [DeviceIndex(d) for _ in range(R)]
+    for j, (c, (i, r)) in enumerate(zip(cids, lists)):
+        for s in range(R):
+            if owners[j] == s:
+                shards[s].create_list(int(c), 0, r, i)
+            else:
+                shards[s].add_remote_list(int(c), 0, cents[j])
+    for s, sh in enumerate(shards):
+        sh.combine_create(R, s, B, kk)
+    for s, sh in enumerate(shards):
+        for g in range(R):
+            if g != s:
+                sh.combine_open(g, area_ptr=shards[g].combine_area())
+    dev = torch.device("cuda", 0)
+    for epoch in (1, 2):
+        Qe = Q[(epoch - 1) * 8:(epoch - 1) * 8 + R * B] if epoch == 1 else Q[-R * B:]
+        ref = single.search(Qe, [0], nprobe, kk)
+        probes = [shards[r].search_coarse(Qe[r * B:(r + 1) * B], [0], nprobe) for r in range(R)]
+        qa = torch.from_numpy(np.ascontiguousarray(Qe)).to(dev)
+        pa = torch.from_numpy(np.concatenate(probes)).to(dev)
+        for sh in shards:
+            sh.combine_search_probed_device(qa, pa, epoch)
+        for sh in shards:
+            sh.sync()
+        for r, sh in enumerate(shards):
+            o_ids = torch.empty(B, kk, dtype=torch.int64, device=dev)
+            o_d = torch.empty(B, kk, dtype=torch.float32, device=dev)
+            o_c = torch.empty(B, kk, dtype=torch.int64, device=dev)
+            o_n = torch.empty(B, dtype=torch.int32, device=dev)
+            o_s = torch.empty(B, dtype=torch.int64, device=dev)
+            sh.combine_merge_device(epoch, o_ids, o_d, o_c, o_n, o_s, timeout_s=5.0)
+            sh.sync()
+            assert sh.combine_status() == 0
+            sl = slice(r * B, (r + 1) * B)
+            assert np.array_equal(o_ids.cpu().numpy(), ref.ids[sl])
+            assert np.array_equal(o_d.cpu().numpy().view(np.uint32), ref.dists[sl].view(np.uint32))
+            assert np.array_equal(o_c.cpu().numpy(), ref.cids[sl])
+            assert np.array_equal(o_n.cpu().numpy(), ref.counts[sl])
+            assert np.array_equal(o_s.cpu().numpy(), ref.scanned[sl])
+    # a merge for an epoch nobody produced times out instead of hanging
+    o = [torch.empty(B, kk, dtype=torch.int64, device=dev), torch.empty(B, kk, dtype=torch.float32, device=dev),
+         torch.empty(B, kk, dtype=torch.int64, device=dev), torch.empty(B, dtype=torch.int32, device=dev)]
+    shards[0].combine_merge_device(99, *o, timeout_s=0.05)
+    shards[0].sync()
+    assert shards[0].combine_status() == 1
+    for ix in shards + [single]:
+        ix.close()
