@@ -78,6 +78,8 @@ _SIGS = [
     ("pk_combine_search_probed", [_vp, _vp, _i64, _vp, _i32, _i64, _int], _int),
     ("pk_combine_merge", [_vp, _i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _int], _int),
     ("pk_combine_status", [_vp, _vp], _int),
+    ("pk_search_submit", [_vp, _i32, _vp, _i64, _vp, _i32, _i32, _i32], _int),
+    ("pk_search_collect", [_vp, _i32, _vp, _vp, _vp, _vp, _vp], _int),
     ("pk_list_add_remote", [_vp, _i64, _i32, _vp], _int),
     ("pk_shard_block_bytes", [_i64, _i32], _i64),
     ("pk_merge_shards", [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _int], _int),

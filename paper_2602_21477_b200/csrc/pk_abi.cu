@@ -153,6 +153,20 @@ struct pk_index {
   uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
   size_t hout_bytes = 0;
 
+  // ---- asynchronous host-pointer searches (pk_search_submit / collect): two
+  // slots, so the H2D of batch i+1 (copy stream) and the caller's host work
+  // overlap the device pass of batch i
+  struct AsyncSlot {
+    DevBuf qin, blk;
+    uint8_t* hblk = nullptr;  // pinned result block
+    size_t hbytes = 0;
+    cudaEvent_t copied = nullptr, done = nullptr, consumed = nullptr;
+    int64_t B = 0;
+    int32_t kk = 0;
+    bool busy = false;
+  } aslot[2];
+  cudaStream_t cst = nullptr;  // copy stream
+
   // ---- peer combine (pk_combine_*): this rank's receive area (R shard blocks
   // + R flags, IPC-exported) and the peers' areas mapped into this process
   struct Combine {
@@ -766,6 +780,15 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->stage_ev) cudaEventDestroy(ix->stage_ev);
   if (ix->mst) cudaStreamDestroy(ix->mst);
   if (ix->hout) cudaFreeHost(ix->hout);
+  for (auto& a : ix->aslot) {
+    if (a.hblk) cudaFreeHost(a.hblk);
+    if (a.copied) cudaEventDestroy(a.copied);
+    if (a.done) cudaEventDestroy(a.done);
+    if (a.consumed) cudaEventDestroy(a.consumed);
+    a.qin.release();
+    a.blk.release();
+  }
+  if (ix->cst) cudaStreamDestroy(ix->cst);
   for (uint8_t* p : ix->comb.opened) cudaIpcCloseMemHandle(p);
   if (ix->comb.area) cudaFree(ix->comb.area);
   if (ix->comb.d_peers) cudaFree(ix->comb.d_peers);
@@ -1286,7 +1309,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                        int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids,
                        float* out_dists, int64_t* out_cids, int32_t* out_n, int64_t* out_probe,
                        int64_t* out_scanned, bool in_dev, bool dev, const int32_t* probe_in,
-                       int32_t* probe_out) {
+                       int32_t* probe_out, bool host_scopes = false) {
   if (B < 0) return fail(PK_ERR_USAGE, "negative batch");
   if (nprobe < 1) return fail(PK_ERR_USAGE, "nprobe must be >= 1");
   if (nprobe > 2048) return fail(PK_ERR_USAGE, "nprobe %d above the device limit 2048", nprobe);
@@ -1344,7 +1367,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   PROF(0);
   if (!probe_in)
     CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
-                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+                       (in_dev && !host_scopes) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
   const ListTable lt = ix->table();
   if (prep) {
     const float* qin = Q;
@@ -1531,6 +1554,71 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
   const bool dev = flags & PK_DEVICE_PTRS;
   return search_core(ix, Q, B, scope_codes, nscopes, nprobe, kk, out_ids, out_dists, out_cids,
                      out_n, out_probe, out_scanned, dev, dev, nullptr, nullptr);
+}
+
+int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
+                     const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk) {
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  if (slot < 0 || slot > 1) return fail(PK_ERR_USAGE, "slot must be 0 or 1");
+  if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
+  auto& a = ix->aslot[slot];
+  if (a.busy) return fail(PK_ERR_USAGE, "slot %d has an uncollected search", slot);
+  if (B <= 0) return fail(PK_ERR_USAGE, "empty batch");
+  CK(cudaSetDevice(ix->device));
+  if (!ix->cst) CK(cudaStreamCreateWithFlags(&ix->cst, cudaStreamNonBlocking));
+  if (!a.copied) {
+    CK(cudaEventCreateWithFlags(&a.copied, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.consumed, cudaEventDisableTiming));
+    CK(cudaEventRecord(a.consumed, ix->st));
+  }
+  const int64_t ob = pk_shard_block_bytes(B, kk);
+  RET(a.qin.ensure((size_t)B * ix->d * 4));
+  RET(a.blk.ensure((size_t)ob));
+  if ((int64_t)a.hbytes < ob) {
+    if (a.hblk) cudaFreeHost(a.hblk);
+    a.hblk = nullptr;
+    a.hbytes = 0;
+    CK(cudaHostAlloc((void**)&a.hblk, (size_t)ob, cudaHostAllocDefault));
+    a.hbytes = (size_t)ob;
+  }
+  // H2D on the copy stream once the slot's previous batch has read its input
+  CK(cudaStreamWaitEvent(ix->cst, a.consumed, 0));
+  CK(cudaMemcpyAsync(a.qin.p, Q, (size_t)B * ix->d * 4, cudaMemcpyHostToDevice, ix->cst));
+  CK(cudaEventRecord(a.copied, ix->cst));
+  CK(cudaStreamWaitEvent(ix->st, a.copied, 0));
+  uint8_t* base = a.blk.as<uint8_t>();
+  const int64_t nkk = B * kk;
+  RET(search_core(ix, a.qin.as<float>(), B, scope_codes, nscopes, nprobe, kk,
+                  reinterpret_cast<int64_t*>(base), reinterpret_cast<float*>(base + 16 * nkk + 8 * B),
+                  reinterpret_cast<int64_t*>(base + 8 * nkk), reinterpret_cast<int32_t*>(base + 20 * nkk + 8 * B),
+                  nullptr, reinterpret_cast<int64_t*>(base + 16 * nkk), true, true, nullptr, nullptr,
+                  /*host_scopes=*/true));
+  CK(cudaEventRecord(a.consumed, ix->st));
+  CK(cudaMemcpyAsync(a.hblk, base, (size_t)ob, cudaMemcpyDeviceToHost, ix->st));
+  CK(cudaEventRecord(a.done, ix->st));
+  a.B = B;
+  a.kk = kk;
+  a.busy = true;
+  return PK_OK;
+}
+
+int pk_search_collect(pk_index* ix, int32_t slot, int64_t* out_ids, float* out_dists, int64_t* out_cids,
+                      int32_t* out_n, int64_t* out_scanned) {
+  if (slot < 0 || slot > 1) return fail(PK_ERR_USAGE, "slot must be 0 or 1");
+  auto& a = ix->aslot[slot];
+  if (!a.busy) return fail(PK_ERR_USAGE, "slot %d has no search in flight", slot);
+  CK(cudaEventSynchronize(a.done));  // outside the index lock: the other slot may submit meanwhile
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  const int64_t B = a.B, nkk = B * a.kk;
+  const uint8_t* h = a.hblk;
+  memcpy(out_ids, h, nkk * 8);
+  if (out_cids) memcpy(out_cids, h + 8 * nkk, nkk * 8);
+  if (out_scanned) memcpy(out_scanned, h + 16 * nkk, B * 8);
+  memcpy(out_dists, h + 16 * nkk + 8 * B, nkk * 4);
+  memcpy(out_n, h + 20 * nkk + 8 * B, B * 4);
+  a.busy = false;
+  return PK_OK;
 }
 
 int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,

@@ -52,6 +52,7 @@ class DeviceIndex:
         self._h = h
         self._pend: list = []  # queued appends (flushed before any other operation)
         self._pend_lock = threading.Lock()
+        self._next_slot = 0
 
     @property
     def handle(self):
@@ -202,6 +203,30 @@ class DeviceIndex:
                                   int(kk), N.ptr(ids), N.ptr(dd), N.ptr(cids), N.ptr(cnt),
                                   N.ptr(probe), N.ptr(scanned), 0))
         return SearchOutput(ids, dd, cids, cnt, probe, scanned)
+
+    def search_submit(self, Q, scope_codes, nprobe: int, kk: int):
+        """Asynchronous search of a host batch (two slots in flight); returns
+        a ticket for search_collect.  Keep Q alive (ideally pinned) until
+        collected."""
+        self.flush()
+        Q = N.f32(Q, self.dimension)
+        slot = self._next_slot
+        self._next_slot ^= 1
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        N.check(N.lib().pk_search_submit(self._h, slot, N.ptr(Q), Q.shape[0], N.ptr(codes), len(codes),
+                                         int(nprobe), int(kk)))
+        return (slot, Q.shape[0], int(kk), Q)
+
+    def search_collect(self, ticket) -> SearchOutput:
+        slot, B, kk, _ = ticket
+        ids = np.empty((B, kk), dtype=np.int64)
+        dd = np.empty((B, kk), dtype=np.float32)
+        cids = np.empty((B, kk), dtype=np.int64)
+        cnt = np.empty(B, dtype=np.int32)
+        scanned = np.empty(B, dtype=np.int64)
+        N.check(N.lib().pk_search_collect(self._h, slot, N.ptr(ids), N.ptr(dd), N.ptr(cids), N.ptr(cnt),
+                                          N.ptr(scanned)))
+        return SearchOutput(ids, dd, cids, cnt, None, scanned)
 
     def search_device(self, Q, scope_codes, nprobe: int, kk: int, out_ids, out_d, out_cid,
                       out_n, out_scanned=None):

@@ -359,3 +359,26 @@ def test_concurrent_searches_equal_serial(pk):
     assert par == serial
     assert [f.result().hits for f in futs] == serial
     store.close()
+
+
+def test_async_submit_collect_equals_search(pk):
+    """pk_search_submit / pk_search_collect (two slots in flight) return
+    exactly pk_search's answers, in submission order."""
+    rng = np.random.default_rng(8)
+    d, nlist = 96, 30
+    sizes = rng.integers(1, 600, nlist)
+    ix, lists, cents, cids = _random_index(pk, rng, d, nlist, sizes)
+    batches = [rng.normal(size=(int(rng.integers(1, 90)), d)).astype(np.float32) for _ in range(7)]
+    want = [ix.search(Q, [0], 6, 12) for Q in batches]
+    got, prev = [], None
+    for Q in batches:
+        t = ix.search_submit(Q, [0], 6, 12)
+        if prev is not None:
+            got.append(ix.search_collect(prev))
+        prev = t
+    got.append(ix.search_collect(prev))
+    for w, g in zip(want, got):
+        assert np.array_equal(w.ids, g.ids) and np.array_equal(w.counts, g.counts)
+        assert np.array_equal(bits(w.dists), bits(g.dists)) and np.array_equal(w.cids, g.cids)
+        assert np.array_equal(w.scanned, g.scanned)
+    ix.close()
