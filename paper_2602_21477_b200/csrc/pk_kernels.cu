@@ -23,6 +23,25 @@ namespace pk {
 
 constexpr unsigned FULL = 0xffffffffu;
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// while the previous kernel on the stream drains; it calls pdl_wait() before
+// touching that kernel's outputs.
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 template <int METRIC>
 __device__ __forceinline__ float finalize(float acc, float nn, float qn) {
   if (METRIC == SQ_L2) return acc;
@@ -458,6 +477,8 @@ __global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
 __global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
                                    const int32_t* __restrict__ lcount, ScanItem* __restrict__ items,
                                    int32_t* __restrict__ n_items) {
+  pdl_trigger();
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= lt.nslots) return;
   const int cnt = lcount[s];
@@ -492,8 +513,8 @@ void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chu
     route_emit_kernel<<<B, RE_THREADS, 0, st>>>(probe, nprobe, lt, chunk_rows, smax, bcap, lcount,
                                                 bucket, slot_off, scanned);
   if (lt.nslots > 0)
-    route_items_kernel<<<(lt.nslots + 255) / 256, 256, 0, st>>>(lt, chunk_rows, bcap, lcount, items,
-                                                                 n_items);
+    launch_pdl(route_items_kernel, dim3((lt.nslots + 255) / 256), dim3(256), 0, st, lt, chunk_rows, bcap,
+               lcount, items, n_items);
 }
 
 // =====================================================================
@@ -1386,7 +1407,8 @@ __global__ void __launch_bounds__(SCREEN_THREADS, 1)
 constexpr int TC_STAGES = 5;
 constexpr int TC_EPI_WARPS = 8;
 constexpr int TC_THREADS = (TC_EPI_WARPS + 2) * 32;
-constexpr int TC_TMEM_COLS = 64;  // 2 tile buffers x 2 halves x 16 queries
+constexpr int TC_TBUF = 4;         // TMEM accumulator buffers (tiles in flight between MMA and epilogue)
+constexpr int TC_TMEM_COLS = TC_TBUF * 2 * QG;  // x 2 halves x 16 queries
 
 struct TcLayout {
   static constexpr size_t X_BYTES = (size_t)TC_STAGES * TILE * DC * 4;
@@ -1424,8 +1446,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   S.full = bars;
   S.empty = bars + TC_STAGES;
   uint64_t* tfull = bars + 2 * TC_STAGES;
-  uint64_t* tempty = tfull + 2;
-  S.rfull = tempty + 2;
+  uint64_t* tempty = tfull + TC_TBUF;
+  S.rfull = tempty + TC_TBUF;
   S.rempty = S.rfull + 2;
   p += TcLayout::BAR_BYTES;
   S.ring = reinterpret_cast<ScanItem*>(p);
@@ -1444,9 +1466,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&S.full[i], 1);
       mbar_init(&S.empty[i], 1);  // tcgen05.commit
     }
-    for (int i = 0; i < 2; i++) {
+    for (int i = 0; i < TC_TBUF; i++) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], TC_EPI_WARPS);
+    }
+    for (int i = 0; i < 2; i++) {
       mbar_init(&S.rfull[i], 1);
       mbar_init(&S.rempty[i], TC_EPI_WARPS + 1);
     }
@@ -1456,6 +1480,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();  // items, queries and counters come from the kernels before
   const uint32_t tmem = *tmem_slot;
   const int nchunk_d = lt.dp / DC;
   const int n_items = *n_items_p;
@@ -1480,8 +1506,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       if (item.nq < 0) break;
       for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
-        const int buf = tcount & 1;
-        mbar_wait(&tempty[buf], ((tcount >> 1) & 1) ^ 1);
+        const int buf = tcount % TC_TBUF;
+        mbar_wait(&tempty[buf], ((tcount / TC_TBUF) & 1) ^ 1);
         tc_fence_after();
         const uint32_t dcol = tmem + buf * 2 * QG;
         const bool two = item.nrows - t0 > 128;
@@ -1538,8 +1564,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int i = threadIdx.x; i < item.nrows; i += nthr) S.NX[i] = lt.nrm[rbase + i];
       const int h = warp >> 2, g = warp & 3;
       for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
-        const int buf = tcount & 1;
-        mbar_wait(&tfull[buf], (tcount >> 1) & 1);
+        const int buf = tcount % TC_TBUF;
+        mbar_wait(&tfull[buf], (tcount / TC_TBUF) & 1);
         tc_fence_after();
         float v[QG];
         tmem_ld16(tmem + ((uint32_t)(32 * g) << 16) + buf * 2 * QG + h * QG, v);
@@ -1634,9 +1660,9 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   {                                                                                              \
     auto k = scan_tc_kernel<M>;                                                                  \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    k<<<grid, TC_THREADS, smem, st>>>(maps, lt, qsw, (int64_t)B, qnorm2, items, n_items, qpairs, \
-                                      kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool, ccount,    \
-                                      cap, dbg_skip);                                            \
+    launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, st, maps, lt, (const float*)qsw, (int64_t)B, \
+               qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
+               ccount, cap, dbg_skip);                                                             \
   }
   if (metric == SQ_L2) PK_TC(SQ_L2)
   else PK_TC(IP)
@@ -1704,6 +1730,8 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     const int32_t* __restrict__ probe, int nprobe, int kk, int stage_floats, int64_t* __restrict__ out_ids,
     float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n,
     int32_t* __restrict__ nsurv) {
+  pdl_trigger();
+  pdl_wait();
   extern __shared__ __align__(16) uint8_t rr_smem[];
   Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [RR_CAP]
   float4* qs4 = reinterpret_cast<float4*>(rr_smem + RR_CAP * sizeof(Entry));     // [dp/4]
@@ -1911,7 +1939,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
   {                                                                                             \
     auto k = rerank_merge_kernel<M>;                                                            \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
-    k<<<B, RR_THREADS, smem, st>>>(cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
+    launch_pdl(k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
                                    nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv); \
   }
   if (metric == SQ_L2) PK_RR(SQ_L2)
@@ -2179,6 +2207,8 @@ __global__ void __launch_bounds__(128, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
+  pdl_wait();  // the batch's TF32 split comes from qprep
   const uint32_t tmem = *tmem_slot;
   if (warp == 0 && lane == 0) {
     for (int t = 0; t < NT; t++) {
@@ -2264,10 +2294,10 @@ void launch_coarse_tc(bool split, int ks, const CoarseMaps& maps, int nslots, in
   dim3 grid((unsigned)((nslots + CT_M - 1) / CT_M), (unsigned)((B + CT_N - 1) / CT_N), (unsigned)ks);
   if (split) {
     cudaFuncSetAttribute(coarse_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    coarse_tc_kernel<true><<<grid, 128, smem, st>>>(maps, nslots, B, dp / DC, Dout, lda);
+    launch_pdl(coarse_tc_kernel<true>, grid, dim3(128), smem, st, maps, nslots, B, dp / DC, Dout, lda);
   } else {
     cudaFuncSetAttribute(coarse_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    coarse_tc_kernel<false><<<grid, 128, smem, st>>>(maps, nslots, B, dp / DC, Dout, lda);
+    launch_pdl(coarse_tc_kernel<false>, grid, dim3(128), smem, st, maps, nslots, B, dp / DC, Dout, lda);
   }
 }
 
@@ -2283,6 +2313,7 @@ __global__ void __launch_bounds__(QP_THREADS) qprep_kernel(const float* __restri
                              float* __restrict__ lo, float* __restrict__ qsw,
                              int32_t* __restrict__ zero_i32, int nzero, int32_t* __restrict__ zero2,
                              int nzero2, uint32_t* __restrict__ ones_u32, int nones) {
+  pdl_trigger();
   if (blockIdx.x == 0) {
     for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero_i32[i] = 0;
     for (int i = threadIdx.x; i < nzero2; i += blockDim.x) zero2[i] = 0;
@@ -2437,6 +2468,8 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     const int32_t* __restrict__ scope_codes, int nscopes, int nprobe, float coef, float abs_coef,
     int cap, int stage_floats, int ks, int64_t zstride, int32_t* __restrict__ probe, uint32_t* __restrict__ probe_key,
     int32_t* __restrict__ ncand_out, uint64_t* __restrict__ dbg, RouteArgs ra) {
+  pdl_trigger();
+  pdl_wait();  // coarse partial dots
   auto mark = [&](int i) {  // phase timestamps (PK_DEBUG_PICK)
     if (dbg && threadIdx.x == 0) {
       uint64_t t;
@@ -2675,7 +2708,7 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
   {                                                                                                  \
     auto k = coarse_pick_kernel<M>;                                                                  \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
-    k<<<B, PICK_THREADS, smem, st>>>(Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe,     \
+    launch_pdl(k, dim3(B), dim3(PICK_THREADS), smem, st, Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe, \
                                      coef, abs_coef, cap, stage_floats, ks, (int64_t)B * lda, probe, \
                                      probe_key, ncand, dbg, ra);                                     \
   }
