@@ -373,10 +373,16 @@ def run_ours(a):
     if sh is not None:
         combine = os.environ.get("PK_COMBINE", "peer")
         if combine == "peer":
+            ok = 1
             try:
                 sh.setup_peer_combine(a.batch, kk)
             except Exception as exc:  # no P2P mapping between these devices
-                print(f"peer combine unavailable ({exc}); using NCCL all-to-all", file=sys.stderr)
+                print(f"rank {rank}: peer combine unavailable ({exc})", file=sys.stderr)
+                ok = 0
+            # every rank must take the same combine path
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
                 combine = "nccl"
 
     def step(s):
