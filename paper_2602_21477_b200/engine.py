@@ -298,10 +298,13 @@ class Store:
             return
         raise ScopePermissionError(f"agent {agent!r} may not write scope {scope!r}")
 
-    def _agent_path(self, agent, scopes, no_cache=False) -> bool:
-        """True when a query needs the per-query agent pipeline: an agent
-        cache in use, pattern hints (prefetch), or staged (cache-owned) items
-        in a searched scope."""
+    def _agent_path(self, agent, scopes, no_cache=False, k: int = 1) -> bool:
+        """True when a query needs the per-query pipeline: an agent cache in
+        use, pattern hints (prefetch), staged (cache-owned) items in a
+        searched scope, or k above the batched device top-k (KKMAX): that
+        pipeline ranks every probed row (pk_scan_lists) for any k."""
+        if k > N.KKMAX:
+            return True
         if agent is not None and agent in self.caches:
             if self.cfg.cache_enabled and not no_cache:
                 return True
@@ -325,7 +328,7 @@ class Store:
         with self._serialized(agent):
             self._lock.acquire_read()
             try:
-                if self._agent_path(agent, scopes, _no_cache):
+                if self._agent_path(agent, scopes, _no_cache, k):
                     result, hint, extended = self._search_read_phase(agent, scopes, q, k, nprobe,
                                                                      _internal, _no_cache)
                 else:
@@ -352,7 +355,7 @@ class Store:
         nprobe = nprobe if nprobe is not None else self.cfg.default_nprobe
         if nprobe < 1:
             raise UsageError("nprobe must be >= 1")
-        if self._agent_path(agent, scopes):  # per-query pipeline, B calls of search()
+        if self._agent_path(agent, scopes, k=k):  # per-query pipeline, B calls of search()
             return [self.search(agent, scopes, Q[b], k, nprobe) for b in range(Q.shape[0])]
         with self._serialized(agent):
             self._lock.acquire_read()
@@ -371,8 +374,6 @@ class Store:
         bare path: staged scan, coarse top-nprobe (flat == graph at exhaustive
         ef), merged scan of every probed list, _topk (ref/engine.py:406-426)."""
         B = Q.shape[0]
-        if k > N.KKMAX:
-            raise UsageError(f"k above {N.KKMAX} is not supported by the device top-k")
         exhaustive_edge = k >= self.clusters.live_count()
         eff_nprobe = nprobe
         if exhaustive_edge:

@@ -382,3 +382,33 @@ def test_async_submit_collect_equals_search(pk):
         assert np.array_equal(bits(w.dists), bits(g.dists)) and np.array_equal(w.cids, g.cids)
         assert np.array_equal(w.scanned, g.scanned)
     ix.close()
+
+
+def test_large_k_uses_the_per_query_pipeline(pk):
+    """k above the batched device top-k (64) is answered exactly through the
+    per-query pipeline (every probed row ranked, ref/engine.py:406-426)."""
+    from paper_2602_21477_b200 import Store, StoreConfig
+
+    rng = np.random.default_rng(12)
+    d = 32
+    store = Store(StoreConfig(dimension=d, cache_enabled=False, accelerator="none", splits_enabled=False))
+    base = rng.normal(size=(3000, d)).astype(np.float32)
+    lists = [(np.arange(i * 300, (i + 1) * 300), base[i * 300:(i + 1) * 300]) for i in range(10)]
+    store.load_lists("static", lists)
+    cl = store.clusters.clusters
+    cids = sorted(cl)
+    flat = O.FlatIVF.from_lists([(cl[c].member_ids, cl[c].vectors) for c in cids],
+                                np.stack([cl[c].centroid for c in cids]), np.array(cids, np.int64))
+    Q = rng.normal(size=(5, d)).astype(np.float32)
+    for k in (65, 200, 700):
+        res = store.search_batch(None, ["static"], Q, k, 3)
+        for b, r in enumerate(res):
+            # oracle: exact distances of every row of the same probed lists
+            _, _, _, probe, _ = flat.search(Q[b:b + 1], 3, 1)
+            rows = np.concatenate([cl[c].vectors for c in probe[0]])
+            ids = np.concatenate([cl[c].member_ids for c in probe[0]])
+            dd = O.distances(Q[b], rows)
+            order = np.lexsort((ids, dd))[:k]
+            assert r.ids == ids[order].tolist()
+            assert np.array_equal(bits(r.distances), bits(dd[order]))
+    store.close()
