@@ -57,6 +57,13 @@ int pk_kmeans_assign(const float* x, int64_t n, const float* cents, int64_t k, i
 /* core.centroid (core.py:112-117): fp64 row-order mean -> f32[d]. */
 int pk_centroid(const float* mat, int64_t n, int64_t d, float* out, int flags);
 
+/* k-means update (kmeans_split_points, clusters.py:166-171): rows [n][d]
+ * grouped by label in original order, segment c = rows [off[c], off[c+1]);
+ * out[c] = core.centroid of the segment (fp64 row-order mean -> f32);
+ * empty segments are left untouched.  Device pointers (PK_DEVICE_PTRS). */
+int pk_centroids_segmented(const float* rows, int64_t n, int64_t d, const int64_t* off, int64_t k,
+                           float* out, int flags);
+
 /* ---- device index: ClusterStore storage + TierManager residency -------- */
 /* (clusters.py:186-362, tiering.py:175-448).  One index per device.        */
 int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,

@@ -43,6 +43,7 @@ _SIGS = [
     ("pk_distances", [_vp, _i64, _vp, _i64, _i64, _int, _vp, _int], _int),
     ("pk_kmeans_assign", [_vp, _i64, _vp, _i64, _i64, _vp, _vp, _int], _int),
     ("pk_centroid", [_vp, _i64, _i64, _vp, _int], _int),
+    ("pk_centroids_segmented", [_vp, _i64, _i64, _vp, _i64, _vp, _int], _int),
     ("pk_index_create", [_i64, _int, _int, _i64, _i64, ctypes.POINTER(_vp)], _int),
     ("pk_index_destroy", [_vp], _int),
     ("pk_sync", [_vp], _int),

@@ -156,7 +156,8 @@ class NativeAccelerator:
     def kmeans(self, mat, k, rng, base_delta):
         self.call_log.append(("kmeans", len(mat), k))
         self.simulated_us += self.model.accel_scan_us(len(mat)) * k
-        return kmeans_split_points(np.ascontiguousarray(mat, dtype=np.float32), k, rng, base_delta)
+        return kmeans_split_points(np.ascontiguousarray(mat, dtype=np.float32), k, rng, base_delta,
+                                   device=self._device)
 
     def close(self):
         if self._index is not None:

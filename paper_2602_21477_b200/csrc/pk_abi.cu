@@ -655,17 +655,24 @@ int pk_distances(const float* q, int64_t B, const float* mat, int64_t n, int64_t
   std::lock_guard<std::mutex> lk(C.mu);
   const bool dev = flags & PK_DEVICE_PTRS;
   const int64_t dp = round_up(d, DC);
-  RET(stage_padded(C.a, q, B, d, dp, dev, C.st));
-  RET(stage_padded(C.b, mat, n, d, dp, dev, C.st));
+  // device rows already at the padded stride are used in place (no staging copy)
+  const bool inplace = dev && dp == d;
+  const float* qa = q;
+  const float* xa = mat;
+  if (!inplace) {
+    RET(stage_padded(C.a, q, B, d, dp, dev, C.st));
+    RET(stage_padded(C.b, mat, n, d, dp, dev, C.st));
+    qa = C.a.as<float>();
+    xa = C.b.as<float>();
+  }
   RET(C.e.ensure(B * 4));
-  if (metric == COSINE) launch_qnorm(C.a.as<float>(), dp, (int)B, (int)d, C.e.as<float>(), C.st);
+  if (metric == COSINE) launch_qnorm(qa, dp, (int)B, (int)d, C.e.as<float>(), C.st);
   float* D = out;
   if (!dev) {
     RET(C.c.ensure((size_t)B * n * 4));
     D = C.c.as<float>();
   }
-  launch_dist_dense(metric, C.a.as<float>(), dp, (int)B, C.b.as<float>(), dp, n, (int)dp,
-                    C.e.as<float>(), D, n, C.st);
+  launch_dist_dense(metric, qa, dp, (int)B, xa, dp, n, (int)dp, C.e.as<float>(), D, n, C.st);
   CK(cudaGetLastError());
   if (!dev) CK(cudaMemcpyAsync(out, D, (size_t)B * n * 4, cudaMemcpyDeviceToHost, C.st));
   CK(cudaStreamSynchronize(C.st));
@@ -680,8 +687,14 @@ int pk_kmeans_assign(const float* x, int64_t n, const float* cents, int64_t k, i
   std::lock_guard<std::mutex> lk(C.mu);
   const bool dev = flags & PK_DEVICE_PTRS;
   const int64_t dp = round_up(d, DC);
-  RET(stage_padded(C.a, x, n, d, dp, dev, C.st));
-  RET(stage_padded(C.b, cents, k, d, dp, dev, C.st));
+  const float* xa = x;
+  const float* ca = cents;
+  if (!(dev && dp == d)) {  // device rows at the padded stride are used in place
+    RET(stage_padded(C.a, x, n, d, dp, dev, C.st));
+    RET(stage_padded(C.b, cents, k, d, dp, dev, C.st));
+    xa = C.a.as<float>();
+    ca = C.b.as<float>();
+  }
   int64_t* L = labels;
   double* Dd = dists;
   if (!dev) {
@@ -689,7 +702,7 @@ int pk_kmeans_assign(const float* x, int64_t n, const float* cents, int64_t k, i
     L = C.c.as<int64_t>();
     Dd = reinterpret_cast<double*>(L + n);
   }
-  launch_kmeans_assign(C.a.as<float>(), dp, n, C.b.as<float>(), dp, k, (int)dp, L, Dd, C.st);
+  launch_kmeans_assign(xa, dp, n, ca, dp, k, (int)dp, L, Dd, C.st);
   CK(cudaGetLastError());
   if (!dev) {
     CK(cudaMemcpyAsync(labels, L, n * 8, cudaMemcpyDeviceToHost, C.st));
@@ -711,6 +724,18 @@ int pk_centroid(const float* mat, int64_t n, int64_t d, float* out, int flags) {
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, C.c.p, d * 4, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                      C.st));
+  CK(cudaStreamSynchronize(C.st));
+  return PK_OK;
+}
+
+int pk_centroids_segmented(const float* rows, int64_t n, int64_t d, const int64_t* off, int64_t k,
+                           float* out, int flags) {
+  if (n < 0 || d < 1 || k < 1) return fail(PK_ERR_USAGE, "bad shape");
+  if (!(flags & PK_DEVICE_PTRS)) return fail(PK_ERR_USAGE, "segmented centroids take device pointers");
+  Ctx& C = ctx();
+  std::lock_guard<std::mutex> lk(C.mu);
+  launch_seg_centroid(rows, d, off, (int)k, (int)d, out, C.st);
+  CK(cudaGetLastError());
   CK(cudaStreamSynchronize(C.st));
   return PK_OK;
 }

@@ -242,6 +242,28 @@ void launch_centroid(const float* rows, int64_t ldr, int64_t n, int dp, float* c
   centroid_kernel<<<(dp + 127) / 128, 128, 0, st>>>(rows, ldr, n, dp, cent_out);
 }
 
+// Segmented centroids for k-means (kmeans_split_points, ref/clusters.py:166-
+// 171): rows grouped by label in their original order, segment c = rows
+// [off[c], off[c+1]); out[c] = fp64 row-order column mean -> f32 (the
+// core.centroid arithmetic), one thread per (segment, column).
+__global__ void seg_centroid_kernel(const float* __restrict__ rows, int64_t ldr,
+                                    const int64_t* __restrict__ off, int k, int d,
+                                    float* __restrict__ out) {
+  const int c = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= k || j >= d) return;
+  const int64_t a = off[c], b = off[c + 1];
+  if (b <= a) return;  // empty cluster: caller fills it
+  double s = 0.0;
+  for (int64_t i = a; i < b; i++) s = __dadd_rn(s, (double)rows[i * ldr + j]);
+  out[(int64_t)c * d + j] = (float)__ddiv_rn(s, (double)(b - a));
+}
+void launch_seg_centroid(const float* rows, int64_t ldr, const int64_t* off, int k, int d, float* out,
+                         cudaStream_t st) {
+  if (k <= 0 || d <= 0) return;
+  seg_centroid_kernel<<<dim3((d + 127) / 128, k), 128, 0, st>>>(rows, ldr, off, k, d, out);
+}
+
 // =====================================================================
 // CTA-level sort / select over (key u32, id i64, payload i32) entries.
 // =====================================================================

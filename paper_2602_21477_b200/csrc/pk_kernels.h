@@ -63,6 +63,9 @@ void launch_qnorm(const float* Q, int64_t ldq, int B, int d, float* qnorm, cudaS
 // centroid = fp64 row-order mean of rows [off, off+n) -> f32 (written to cent_out[dp]).
 void launch_centroid(const float* rows, int64_t ldr, int64_t n, int dp, float* cent_out,
                      cudaStream_t st);
+// Per-segment fp64 row-order mean (k-means update): segment c = rows [off[c], off[c+1]).
+void launch_seg_centroid(const float* rows, int64_t ldr, const int64_t* off, int k, int d, float* out,
+                         cudaStream_t st);
 // Coarse select: per query the first `nprobe` in-scope lists by (dist, cid).
 void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
                           const int32_t* scope_codes, int nscopes, int nprobe, int32_t* probe,

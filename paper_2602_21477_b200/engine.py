@@ -750,9 +750,11 @@ class Store:
                 return ids
             center = vector_mean(mat)
             spread = vector_spread(mat, center, Metric.SQUARED_EUCLIDEAN)
-            labels, _ = kmeans_split_points(mat, k, self.rng, spread)
+            labels, _ = kmeans_split_points(mat, k, self.rng, spread, device=self.cfg.device)
+            order = np.argsort(labels, kind="stable")  # each cluster's rows in row order
+            bounds = np.concatenate([[0], np.cumsum(np.bincount(labels))])
             for c in range(int(labels.max()) + 1):
-                rows = np.where(labels == c)[0]
+                rows = order[bounds[c]:bounds[c + 1]]
                 if len(rows):
                     self.clusters.create_cluster(scope, (id_arr[rows], mat[rows]))
             return ids

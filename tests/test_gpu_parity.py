@@ -412,3 +412,30 @@ def test_large_k_uses_the_per_query_pipeline(pk):
             assert r.ids == ids[order].tolist()
             assert np.array_equal(bits(r.distances), bits(dd[order]))
     store.close()
+
+
+@pytest.mark.parametrize("n,d,target", [(20000, 48, 1500), (6000, 100, 700)])
+def test_bulk_build_device_kmeans_matches_oracle(pk, n, d, target):
+    """bulk_build's k-means with the matrix resident in HBM (seeding distances,
+    assignments, segmented means on the device) equals the oracle's
+    restatement of ref/clusters.py:121-183: same clusters, members, centroids
+    and the same position of the store's random stream."""
+    from oracle.store_model import bulk_build_model
+    from paper_2602_21477_b200 import Store, StoreConfig
+
+    rng = np.random.default_rng(n + d)
+    centres = rng.normal(size=(12, d)).astype(np.float32)
+    x = (centres[rng.integers(0, 12, n)] + 0.3 * rng.normal(size=(n, d))).astype(np.float32)
+    x[5] = x[9]  # duplicate rows
+    store = Store(StoreConfig(dimension=d, seed=4, split_threshold=target * 2, split_target=target,
+                              cache_enabled=False, splits_enabled=False, accelerator="none"))
+    store.bulk_build("static", list(x))
+    m, _ = bulk_build_model(x, 4, target)
+    cl = store.clusters.clusters
+    cids = sorted(cl)
+    assert cids == sorted(m.clusters)
+    for c in cids:
+        assert np.array_equal(cl[c].member_ids, m.clusters[c].ids)
+        assert np.array_equal(bits(cl[c].centroid), bits(m.clusters[c].centroid))
+    assert store.rng.random() == m.rng.random()
+    store.close()
