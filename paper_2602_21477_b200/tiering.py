@@ -121,23 +121,27 @@ class TierManager:
         clusters = self.store.clusters
         self._hot &= set(clusters)  # retired clusters left with their device copies
         live = [cid for cid in clusters if clusters[cid].size > 0]
-        ranked = sorted(live, key=lambda c: (-self.decayed_freq(c), c))
+        freq = {c: self.decayed_freq(c) for c in live}  # one evaluation per cluster
+        ranked = sorted(live, key=lambda c: (-freq[c], c))
         actions: list[tuple[str, int]] = []
         target: list[int] = []
         used = 0
         for cid in ranked:
             nb = clusters[cid].nbytes
-            if nb == 0 or self.decayed_freq(cid) <= 0.0:
+            if nb == 0 or freq[cid] <= 0.0:
                 continue
             if used + nb <= self.budget_bytes:
                 target.append(cid)
                 used += nb
         target_set = set(target)
+        # the displacers (admitted now, not hot before) are the same for every
+        # hot cluster examined below: retained clusters are already hot
+        displacers = target_set - self._hot
+        hottest = max((freq[c] for c in displacers), default=None)
         for cid in sorted(self._hot - target_set):
-            displacers = [c for c in target_set - self._hot]
-            if displacers:
-                hottest = max(self.decayed_freq(c) for c in displacers)
-                if hottest < self.hysteresis * self.decayed_freq(cid):
+            if hottest is not None:
+                fc = freq[cid] if cid in freq else self.decayed_freq(cid)
+                if hottest < self.hysteresis * fc:
                     target_set.add(cid)
                     continue
             actions.append(("evict", cid))
