@@ -103,8 +103,26 @@ struct Range {
 
 }  // namespace
 
+// Recursive mutex that counts acquisitions: a search may overlap its front
+// half with the previous search's scan only when no other call took the
+// index lock in between (nothing else was queued on the index stream).
+struct CountedMutex {
+  std::recursive_mutex m;
+  uint64_t n = 0;
+  void lock() {
+    m.lock();
+    n++;
+  }
+  bool try_lock() {
+    if (!m.try_lock()) return false;
+    n++;
+    return true;
+  }
+  void unlock() { m.unlock(); }
+};
+
 struct pk_index {
-  std::recursive_mutex mu;  // one caller at a time per index (Store read locks admit concurrent searches)
+  CountedMutex mu;  // one caller at a time per index (Store read locks admit concurrent searches)
   int device = 0;
   int64_t d = 0, dp = 0;
   int metric = 0;
@@ -136,20 +154,35 @@ struct pk_index {
   CoarseMaps cmaps;         // c[0..1]: 128 slots x 32 floats, SWIZZLE_128B (q[] per search)
   int32_t dirty_lo = INT32_MAX, dirty_hi = -1;
 
-  // search scratch
-  DevBuf q, qnorm, dc, probe, probe_key, counts, items, qpairs, slot_off, scanned,
-      cand_key, cand_id, cand_n, cand_list, out_ids, out_d, out_cid, out_n, scopes, assign_c,
-      assign_d;
+  // search scratch: two sets used by consecutive searches in turn, so the
+  // next batch's prep / coarse / pick / routing kernels (programmatic
+  // dependent launches) can run while this batch's re-rank merge drains
+  struct Scratch {
+    DevBuf q, qnorm, dc, probe, probe_key, counts, items, qpairs, slot_off, scanned, cand_key,
+        cand_id, cand_n, cand_list, out_ids, scopes, qnorm2, uq, cpool, ccount, qsw, qhi, qlo, qin,
+        ncand, nsurv;
+    void release() {
+      for (DevBuf* b : {&q, &qnorm, &dc, &probe, &probe_key, &counts, &items, &qpairs, &slot_off,
+                        &scanned, &cand_key, &cand_id, &cand_n, &cand_list, &out_ids, &scopes, &qnorm2,
+                        &uq, &cpool, &ccount, &qsw, &qhi, &qlo, &qin, &ncand, &nsurv})
+        b->release();
+    }
+  } scr[2];
+  int par = 0, last_par = 0;
+  // front-half overlap: the next batch's prep / coarse / pick / routing run on
+  // fst while this batch's scan and re-rank drain on st
+  cudaStream_t fst = nullptr;
+  cudaEvent_t ev_front = nullptr, ev_scan = nullptr, front_wait = nullptr;
+  uint64_t ev_scan_n = 0;  // lock count when ev_scan was last recorded
+  bool pipeline = true;    // PK_PIPELINE=0 turns the overlap off
+  DevBuf assign_q, assign_qn, assign_dc, assign_c, assign_d;
   int chunk_rows = 512;
   bool screen = true;  // screened scan + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
   bool tensor = true;  // screen dots on tcgen05 (TF32); PK_SCREEN=ffma uses CUDA-core FFMA
   bool coarse_tc = true;  // coarse quantizer on tcgen05 + exact re-rank; PK_COARSE=exact disables
   bool coarse_split = true;  // 3xTF32 hi/lo split (tight bound); PK_COARSE=tf32 for one product
-  DevBuf qhi, qlo, qin;
-  DevBuf ncand;
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
-  DevBuf qnorm2, uq, cpool, ccount, ckey, qsw;
-  DevBuf shard_in, shard_out, pb, pb_out, nsurv, sl_buf;
+  DevBuf shard_in, shard_out, pb, pb_out, sl_buf;
   uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
   size_t hout_bytes = 0;
 
@@ -517,14 +550,14 @@ struct pk_index {
     return PK_OK;
   }
   // Stream every cold list probed by the batch into arena staging ranges.
-  int stage_cold(int64_t B, int32_t nprobe) {
+  int stage_cold(int64_t B, int32_t nprobe, const int32_t* probe_dev) {
     bool any = false;
     for (int32_t s = 0; s < nslots && !any; s++)
       any = h_cid[s] >= 0 && !h_res[s] && h_len[s] > 0;
     st_lists_last = st_rows_last = 0;
     if (!any) return PK_OK;
     std::vector<int32_t> pr((size_t)B * nprobe);
-    CK(cudaMemcpyAsync(pr.data(), probe.p, pr.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(pr.data(), probe_dev, pr.size() * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     std::vector<uint8_t> seen(nslots, 0);
     std::vector<StageCopy> desc;
@@ -760,6 +793,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   if (const char* e = getenv("PK_SCAN_EXACT")) ix->screen = atoi(e) == 0;
   if (const char* e = getenv("PK_POOL_CAP")) ix->pool_cap = std::max(1, atoi(e));
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
+  if (const char* e = getenv("PK_PIPELINE")) ix->pipeline = atoi(e) != 0;
   if (const char* e = getenv("PK_STAGE")) ix->stage_dma = strcmp(e, "dma") == 0;
   if (const char* e = getenv("PK_COARSE")) {
     ix->coarse_tc = strcmp(e, "exact") != 0;
@@ -814,6 +848,12 @@ int pk_index_destroy(pk_index* ix) {
     a.blk.release();
   }
   if (ix->cst) cudaStreamDestroy(ix->cst);
+  if (ix->fst) {
+    cudaStreamSynchronize(ix->fst);
+    cudaStreamDestroy(ix->fst);
+  }
+  for (cudaEvent_t e : {ix->ev_front, ix->ev_scan})
+    if (e) cudaEventDestroy(e);
   for (uint8_t* p : ix->comb.opened) cudaIpcCloseMemHandle(p);
   if (ix->comb.area) cudaFree(ix->comb.area);
   if (ix->comb.d_peers) cudaFree(ix->comb.d_peers);
@@ -822,11 +862,9 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->hids) cudaFreeHost(ix->hids);
   ix->stage_desc.release();
   ix->tmp_rows.release();
-  for (DevBuf* b : {&ix->q, &ix->qnorm, &ix->dc, &ix->probe, &ix->probe_key, &ix->counts,
-                    &ix->items, &ix->qpairs, &ix->slot_off, &ix->scanned,
-                    &ix->cand_key, &ix->cand_id, &ix->cand_n, &ix->cand_list,
-                    &ix->out_ids, &ix->out_d, &ix->out_cid, &ix->out_n, &ix->scopes,
-                    &ix->assign_c, &ix->assign_d, &ix->qnorm2, &ix->uq, &ix->cpool, &ix->ccount, &ix->ckey, &ix->qsw, &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->nsurv, &ix->sl_buf, &ix->ncand, &ix->qhi, &ix->qlo, &ix->qin})
+  for (auto& sc : ix->scr) sc.release();
+  for (DevBuf* b : {&ix->assign_q, &ix->assign_qn, &ix->assign_dc, &ix->assign_c, &ix->assign_d,
+                    &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->sl_buf})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
   delete ix;
@@ -834,20 +872,20 @@ int pk_index_destroy(pk_index* ix) {
 }
 
 int pk_sync(pk_index* ix) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 void* pk_stream(pk_index* ix) { return ix ? (void*)ix->st : nullptr; }
 int pk_index_bytes(pk_index* ix, int64_t* bytes) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   *bytes = ix->arena_cap * (ix->dp * 4 + 8) + (int64_t)ix->slot_cap * (ix->dp * 4 + 28);
   return PK_OK;
 }
 
 int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* rows,
                    const int64_t* ids, int64_t n, float* out_centroid, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (n < 1) return fail(PK_ERR_USAGE, "create_cluster needs at least one seed item");
   if (ix->cid2slot.count(cid)) return fail(PK_ERR_USAGE, "cluster %lld exists", (long long)cid);
   CK(cudaSetDevice(ix->device));
@@ -905,7 +943,7 @@ int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* r
 }
 
 int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const float* centroid) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (ix->cid2slot.count(cid)) return fail(PK_ERR_USAGE, "cluster %lld exists", (long long)cid);
   if (!centroid) return fail(PK_ERR_USAGE, "remote list needs a centroid");
   CK(cudaSetDevice(ix->device));
@@ -942,7 +980,7 @@ int64_t pk_shard_block_bytes(int64_t B, int32_t kk) {
 int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int32_t kk,
                     int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
                     int64_t* out_scanned, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (R < 1 || B < 0) return fail(PK_ERR_USAGE, "bad shard count / batch");
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
   if ((int64_t)R * kk > shard_merge_cap())
@@ -985,7 +1023,7 @@ int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int3
 
 int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* ids, int64_t n,
                    int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (n <= 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   int32_t s;
@@ -1037,7 +1075,7 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
 
 int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const float* rows,
                          const int64_t* ids) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (n <= 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   // pre-pass: slots, per-slot counts, capacity (one relocation per list at most)
@@ -1119,7 +1157,7 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
 }
 
 int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1153,7 +1191,7 @@ int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
 }
 
 int pk_list_retire(pk_index* ix, int64_t cid) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   int32_t s;
   RET(ix->slot_of(cid, &s));
   if (ix->tiered) {
@@ -1175,7 +1213,7 @@ int pk_list_retire(pk_index* ix, int64_t cid) {
 }
 
 int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1196,7 +1234,7 @@ int pk_list_recompute(pk_index* ix, int64_t cid, float* out_centroid) {
 }
 
 int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1208,7 +1246,7 @@ int pk_list_set_centroid(pk_index* ix, int64_t cid, const float* centroid) {
 }
 
 int pk_list_size(pk_index* ix, int64_t cid, int64_t* n) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   int32_t s;
   RET(ix->slot_of(cid, &s));
   *n = ix->h_len[s];
@@ -1216,7 +1254,7 @@ int pk_list_size(pk_index* ix, int64_t cid, int64_t* n) {
 }
 
 int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   CK(cudaSetDevice(ix->device));
   int32_t s;
   RET(ix->slot_of(cid, &s));
@@ -1238,7 +1276,7 @@ int pk_list_read(pk_index* ix, int64_t cid, float* rows, int64_t* ids) {
 }
 
 int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (ix->tiered) return PK_OK;
   if (ix->cid2slot.size() > 0) return fail(PK_ERR_USAGE, "enable the cold tier before creating lists");
   CK(cudaSetDevice(ix->device));
@@ -1250,7 +1288,7 @@ int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows) {
 }
 
 int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!ix->tiered) return fail(PK_ERR_USAGE, "no cold tier: every list is HBM-resident");
   CK(cudaSetDevice(ix->device));
   int32_t s;
@@ -1293,7 +1331,7 @@ int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
 }
 
 int pk_list_residency(pk_index* ix, int64_t cid, int* state) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   int32_t s;
   RET(ix->slot_of(cid, &s));
   RET(ix->finish_migration(s, false));
@@ -1302,7 +1340,7 @@ int pk_list_residency(pk_index* ix, int64_t cid, int* state) {
 }
 
 int pk_tier_stats(pk_index* ix, int64_t* out, int n) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   int64_t v[10] = {0};
   if (ix->tiered) RET(ix->poll_migrations());
   for (int32_t s = 0; s < ix->nslots; s++) {
@@ -1344,43 +1382,64 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (B == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   cudaStream_t st = ix->st;
+  pk_index::Scratch& S = ix->scr[ix->par];
+  ix->last_par = ix->par;
+  ix->par ^= 1;
   if (ix->tiered) {
     RET(ix->release_staged());
     RET(ix->poll_migrations());
   }
+  const bool table_dirty = ix->dirty_hi >= ix->dirty_lo;
   RET(ix->sync_table());
   const int64_t dp = ix->dp;
   const int32_t ns = std::max<int32_t>(ix->nslots, 1);
+  // Front-half overlap (device outputs, tensor-core path): this batch's prep,
+  // coarse, pick and routing go to the front stream, which waits only for
+  // the point just before the previous search's scan -- so they run while
+  // that scan and its re-rank drain.  Safe because the front writes only
+  // this batch's scratch set (the other parity's), and nothing but searches
+  // touched the index since (lock count; table unchanged).
+  const bool pipelined = ix->pipeline && dev && in_dev && !probe_in && !probe_out && !ix->tiered &&
+                         !ix->prof && ix->screen && ix->tensor && ix->coarse_tc && !table_dirty &&
+                         ix->ev_scan && ix->mu.n == ix->ev_scan_n + 1;
+  cudaStream_t fs = st;
+  if (pipelined) {
+    if (!ix->fst) CK(cudaStreamCreateWithFlags(&ix->fst, cudaStreamNonBlocking));
+    fs = ix->fst;
+    CK(cudaStreamWaitEvent(fs, ix->ev_scan, 0));
+    if (ix->front_wait) CK(cudaStreamWaitEvent(fs, ix->front_wait, 0));
+  }
+  ix->front_wait = nullptr;
   // scratch
-  const bool fresh_q = ix->q.bytes < (size_t)B * dp * 4;
-  RET(ix->q.ensure((size_t)B * dp * 4));
-  if (fresh_q) CK(cudaMemsetAsync(ix->q.p, 0, ix->q.bytes, st));  // zero pad columns once
-  RET(ix->qnorm.ensure(B * 4));
-  RET(ix->dc.ensure((size_t)B * ns * 4));
-  RET(ix->probe.ensure((size_t)B * nprobe * 4));
-  RET(ix->probe_key.ensure((size_t)B * nprobe * 4));
-  RET(ix->counts.ensure((size_t)ns * 4));
+  const bool fresh_q = S.q.bytes < (size_t)B * dp * 4;
+  RET(S.q.ensure((size_t)B * dp * 4));
+  if (fresh_q) CK(cudaMemsetAsync(S.q.p, 0, S.q.bytes, fs));  // zero pad columns once
+  RET(S.qnorm.ensure(B * 4));
+  RET(S.dc.ensure((size_t)B * ns * 4));
+  RET(S.probe.ensure((size_t)B * nprobe * 4));
+  RET(S.probe_key.ensure((size_t)B * nprobe * 4));
+  RET(S.counts.ensure((size_t)ns * 4));
   int64_t maxlen = 0;
   for (int32_t s = 0; s < ix->nslots; s++)
     if (ix->h_cid[s] >= 0) maxlen = std::max(maxlen, ix->h_len[s]);
   const int64_t max_nch = std::max<int64_t>(1, (maxlen + ix->chunk_rows - 1) / ix->chunk_rows);
   const int64_t max_items = B * nprobe * max_nch;
-  RET(ix->items.ensure((size_t)max_items * sizeof(ScanItem)));
+  RET(S.items.ensure((size_t)max_items * sizeof(ScanItem)));
   const int64_t smax = nprobe * max_nch;  // output slots per query
   // per-list query buckets (B entries each) + lcount [ns] | n_items | work counter
-  RET(ix->qpairs.ensure((size_t)ns * B * sizeof(QPair)));
-  RET(ix->counts.ensure((size_t)(ns + 2) * 4));
-  RET(ix->slot_off.ensure((size_t)2 * B * 4));
-  RET(ix->scanned.ensure((size_t)B * 8));
-  RET(ix->cand_key.ensure((size_t)max_items * kk * 4));
-  RET(ix->cand_id.ensure((size_t)max_items * kk * 8));
-  RET(ix->cand_n.ensure((size_t)max_items * 4));
-  RET(ix->cand_list.ensure((size_t)max_items * 4));
-  RET(ix->scopes.ensure(64 * 4));
+  RET(S.qpairs.ensure((size_t)ns * B * sizeof(QPair)));
+  RET(S.counts.ensure((size_t)(ns + 2) * 4));
+  RET(S.slot_off.ensure((size_t)2 * B * 4));
+  RET(S.scanned.ensure((size_t)B * 8));
+  RET(S.cand_key.ensure((size_t)max_items * kk * 4));
+  RET(S.cand_id.ensure((size_t)max_items * kk * 8));
+  RET(S.cand_n.ensure((size_t)max_items * 4));
+  RET(S.cand_list.ensure((size_t)max_items * 4));
+  RET(S.scopes.ensure(64 * 4));
   const int pc = ix->prof_calls;
 #define PROF(stage) \
   if (ix->prof) RET(ix->prof_mark(pc, stage))
-  int32_t* lcount = ix->counts.as<int32_t>();  // [ns] | n_items | work counter
+  int32_t* lcount = S.counts.as<int32_t>();  // [ns] | n_items | work counter
   int32_t* n_items = lcount + ns;
   int32_t* work_ctr = lcount + ns + 1;
   const bool use_tc = ix->coarse_tc && !probe_in;
@@ -1391,115 +1450,126 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   RouteArgs ra;  // set when the coarse pick emits the routes itself
   PROF(0);
   if (!probe_in)
-    CK(cudaMemcpyAsync(ix->scopes.p, scope_codes, nscopes * 4,
-                       (in_dev && !host_scopes) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(S.scopes.p, scope_codes, nscopes * 4,
+                       (in_dev && !host_scopes) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
   const ListTable lt = ix->table();
   if (prep) {
     const float* qin = Q;
     if (!in_dev) {  // host rows: one contiguous H2D, the prep kernel pads them
-      RET(ix->qin.ensure((size_t)B * ix->d * 4));
-      CK(cudaMemcpyAsync(ix->qin.p, Q, (size_t)B * ix->d * 4, cudaMemcpyHostToDevice, st));
-      qin = ix->qin.as<float>();
+      RET(S.qin.ensure((size_t)B * ix->d * 4));
+      CK(cudaMemcpyAsync(S.qin.p, Q, (size_t)B * ix->d * 4, cudaMemcpyHostToDevice, fs));
+      qin = S.qin.as<float>();
     }
-    RET(ix->qnorm2.ensure(B * 4));
+    RET(S.qnorm2.ensure(B * 4));
     const bool sp = use_tc && ix->coarse_split;
     if (sp) {
-      RET(ix->qhi.ensure((size_t)B * dp * 4));
-      RET(ix->qlo.ensure((size_t)B * dp * 4));
+      RET(S.qhi.ensure((size_t)B * dp * 4));
+      RET(S.qlo.ensure((size_t)B * dp * 4));
     }
-    if (tc_scan) RET(ix->qsw.ensure((size_t)8 * B * dp * 4));
+    if (tc_scan) RET(S.qsw.ensure((size_t)8 * B * dp * 4));
     if (ix->screen) {
-      RET(ix->uq.ensure((size_t)B * 4));
-      RET(ix->ccount.ensure((size_t)B * 4));
+      RET(S.uq.ensure((size_t)B * 4));
+      RET(S.ccount.ensure((size_t)B * 4));
     }
-    launch_qprep(qin, ix->d, (int)ix->d, (int)B, (int)dp, ix->q.as<float>(), ix->qnorm2.as<float>(),
-                 sp ? ix->qhi.as<float>() : nullptr, sp ? ix->qlo.as<float>() : nullptr,
-                 tc_scan ? ix->qsw.as<float>() : nullptr, lcount, (int)(ns + 2),
-                 ix->screen ? ix->ccount.as<int32_t>() : nullptr, ix->screen ? (int)B : 0,
-                 ix->screen ? ix->uq.as<uint32_t>() : nullptr, ix->screen ? (int)B : 0, st);
+    launch_qprep(qin, ix->d, (int)ix->d, (int)B, (int)dp, S.q.as<float>(), S.qnorm2.as<float>(),
+                 sp ? S.qhi.as<float>() : nullptr, sp ? S.qlo.as<float>() : nullptr,
+                 tc_scan ? S.qsw.as<float>() : nullptr, lcount, (int)(ns + 2),
+                 ix->screen ? S.ccount.as<int32_t>() : nullptr, ix->screen ? (int)B : 0,
+                 ix->screen ? S.uq.as<uint32_t>() : nullptr, ix->screen ? (int)B : 0, fs);
   } else {
-    CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
-                         in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, st));
+    CK(cudaMemcpy2DAsync(S.q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
+                         in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
+    CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, fs));
   }
-  if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)B, (int)ix->d, ix->qnorm.as<float>(), st);
+  if (ix->metric == COSINE) launch_qnorm(S.q.as<float>(), dp, (int)B, (int)ix->d, S.qnorm.as<float>(), fs);
   PROF(1);
   // 1. coarse quantizer: distances to every list centroid, top-nprobe in scope
   if (probe_in) {
-    CK(cudaMemcpyAsync(ix->probe.p, probe_in, (size_t)B * nprobe * 4,
-                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(S.probe.p, probe_in, (size_t)B * nprobe * 4,
+                       in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
     PROF(2);
   } else if (ix->coarse_tc) {
-    RET(ix->ncand.ensure(B * 4));
+    RET(S.ncand.ensure(B * 4));
     const int ks = coarse_split_k(ix->nslots, (int)B, (int)dp, ix->num_sms);
-    RET(ix->dc.ensure((size_t)ks * B * ns * 4));
+    RET(S.dc.ensure((size_t)ks * B * ns * 4));
     if (ix->coarse_split) {
-      RET(ix->encode_2d(&ix->cmaps.q[0], ix->qhi.as<float>(), dp, B, 64));
-      RET(ix->encode_2d(&ix->cmaps.q[1], ix->qlo.as<float>(), dp, B, 64));
+      RET(ix->encode_2d(&ix->cmaps.q[0], S.qhi.as<float>(), dp, B, 64));
+      RET(ix->encode_2d(&ix->cmaps.q[1], S.qlo.as<float>(), dp, B, 64));
     } else {
-      RET(ix->encode_2d(&ix->cmaps.q[0], ix->q.as<float>(), dp, B, 64));
+      RET(ix->encode_2d(&ix->cmaps.q[0], S.q.as<float>(), dp, B, 64));
     }
     launch_coarse_tc(ix->coarse_split, ks, ix->cmaps, ix->nslots, (int)B, (int)dp,
-                     ix->dc.as<float>(), ns, st);
+                     S.dc.as<float>(), ns, fs);
     PROF(2);
     // the pick also routes its query unless the cold tier may still move lists
     if (!probe_out && !ix->tiered) {
       ra.lcount = lcount;
-      ra.bucket = ix->qpairs.as<QPair>();
-      ra.slot_off = ix->slot_off.as<int32_t>();
-      ra.scanned = ix->scanned.as<int64_t>();
+      ra.bucket = S.qpairs.as<QPair>();
+      ra.slot_off = S.slot_off.as<int32_t>();
+      ra.scanned = S.scanned.as<int64_t>();
       ra.chunk_rows = ix->chunk_rows;
       ra.smax = (int)smax;
       ra.bcap = (int)B;
     }
-    launch_coarse_pick(ix->metric, ix->coarse_split, ks, ix->dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, ix->q.as<float>(),
-                       ix->qnorm2.as<float>(), ix->scopes.as<int32_t>(), nscopes, nprobe,
-                       ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), ix->ncand.as<int32_t>(), ra, st);
+    launch_coarse_pick(ix->metric, ix->coarse_split, ks, S.dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, S.q.as<float>(),
+                       S.qnorm2.as<float>(), S.scopes.as<int32_t>(), nscopes, nprobe,
+                       S.probe.as<int32_t>(), S.probe_key.as<uint32_t>(), S.ncand.as<int32_t>(), ra, fs);
   } else {
-    launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
-                      ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
+    launch_dist_dense(ix->metric, S.q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
+                      S.qnorm.as<float>(), S.dc.as<float>(), ns, fs);
     PROF(2);
-    launch_coarse_select(ix->dc.as<float>(), ns, (int)B, lt, ix->scopes.as<int32_t>(), nscopes,
-                         nprobe, ix->probe.as<int32_t>(), ix->probe_key.as<uint32_t>(), st);
+    launch_coarse_select(S.dc.as<float>(), ns, (int)B, lt, S.scopes.as<int32_t>(), nscopes,
+                         nprobe, S.probe.as<int32_t>(), S.probe_key.as<uint32_t>(), fs);
   }
   PROF(3);
   if (probe_out) {
-    CK(cudaMemcpyAsync(probe_out, ix->probe.p, (size_t)B * nprobe * 4,
-                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(probe_out, S.probe.p, (size_t)B * nprobe * 4,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, fs));
     if (!dev) CK(cudaStreamSynchronize(st));
     return PK_OK;
   }
   // cold tier: stream the probed lists that are not HBM-resident into staging
-  if (ix->tiered) RET(ix->stage_cold(B, nprobe));
+  if (ix->tiered) RET(ix->stage_cold(B, nprobe, S.probe.as<int32_t>()));
   const ListTable lt2 = ix->table();  // staging may have grown the arena
   // 2. route (query -> lists) into (list -> queries) work items
-  launch_route(ix->probe.as<int32_t>(), (int)B, nprobe, lt2, ix->chunk_rows, (int)smax, (int)B,
-               lcount, ix->items.as<ScanItem>(), n_items, ix->qpairs.as<QPair>(),
-               ix->slot_off.as<int32_t>(), ix->scanned.as<int64_t>(), ra.lcount != nullptr, st);
+  launch_route(S.probe.as<int32_t>(), (int)B, nprobe, lt2, ix->chunk_rows, (int)smax, (int)B,
+               lcount, S.items.as<ScanItem>(), n_items, S.qpairs.as<QPair>(),
+               S.slot_off.as<int32_t>(), S.scanned.as<int64_t>(), ra.lcount != nullptr, fs);
+  if (pipelined) {
+    CK(cudaEventRecord(ix->ev_front, fs));
+    CK(cudaStreamWaitEvent(st, ix->ev_front, 0));
+  }
+  if (!ix->ev_front) {
+    CK(cudaEventCreateWithFlags(&ix->ev_front, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ix->ev_scan, cudaEventDisableTiming));
+  }
+  // everything before this batch's scan: where the next search's front may start
+  CK(cudaEventRecord(ix->ev_scan, st));
+  ix->ev_scan_n = ix->mu.n;
   // 3. fused scan + per-(query, list chunk) top-kk
   PROF(4);
   if (ix->screen) {
-    RET(ix->cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));  // uq / ccount reset by prep
+    RET(S.cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));  // uq / ccount reset by prep
     if (ix->tensor) {
-      launch_scan_tc(ix->metric, lt2, ix->maps, ix->q.as<float>(), (int)B, ix->qsw.as<float>(), true,
-                     ix->qnorm2.as<float>(), ix->items.as<ScanItem>(), n_items,
-                     (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
-                     work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
-                     ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
-                     ix->pool_cap, ix->scan_sms, st);
+      launch_scan_tc(ix->metric, lt2, ix->maps, S.q.as<float>(), (int)B, S.qsw.as<float>(), true,
+                     S.qnorm2.as<float>(), S.items.as<ScanItem>(), n_items,
+                     (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
+                     work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
+                     S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
+                     ix->pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined);
     } else {
-      launch_scan_screen(ix->metric, lt2, ix->maps, ix->q.as<float>(), ix->qnorm2.as<float>(),
-                         ix->items.as<ScanItem>(), n_items,
-                         (int)std::min<int64_t>(max_items, INT32_MAX), ix->qpairs.as<QPair>(), kk,
-                         work_ctr, ix->uq.as<uint32_t>(), ix->cand_key.as<uint32_t>(),
-                         ix->cand_n.as<int32_t>(), ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
+      launch_scan_screen(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm2.as<float>(),
+                         S.items.as<ScanItem>(), n_items,
+                         (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
+                         work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
+                         S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
                          ix->pool_cap, ix->num_sms, st);
     }
   } else
-    launch_scan(ix->metric, lt2, ix->maps, ix->q.as<float>(), ix->qnorm.as<float>(),
-                ix->items.as<ScanItem>(), n_items, (int)std::min<int64_t>(max_items, INT32_MAX),
-                ix->qpairs.as<QPair>(), kk, work_ctr, ix->cand_key.as<uint32_t>(),
-                ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(),
+    launch_scan(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm.as<float>(),
+                S.items.as<ScanItem>(), n_items, (int)std::min<int64_t>(max_items, INT32_MAX),
+                S.qpairs.as<QPair>(), kk, work_ctr, S.cand_key.as<uint32_t>(),
+                S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(),
                 ix->num_sms, st);
   PROF(5);
   // 4. merge per query
@@ -1511,29 +1581,33 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (!dev) {
     // results land in one device block (shard-block layout) and come back in
     // ONE copy into a pinned staging buffer, then fan out on the host
-    RET(ix->out_ids.ensure((size_t)ob));
-    uint8_t* base = ix->out_ids.as<uint8_t>();
+    RET(S.out_ids.ensure((size_t)ob));
+    uint8_t* base = S.out_ids.as<uint8_t>();
     const int64_t nkk = B * kk;
     o_ids = reinterpret_cast<int64_t*>(base);
     o_cid = reinterpret_cast<int64_t*>(base + 8 * nkk);
     o_d = reinterpret_cast<float*>(base + 16 * nkk + 8 * B);
     o_n = reinterpret_cast<int32_t*>(base + 20 * nkk + 8 * B);
   }
-  if (ix->screen) RET(ix->nsurv.ensure((size_t)B * 4));
+  if (ix->screen) RET(S.nsurv.ensure((size_t)B * 4));
+  // the re-rank also copies the per-query scanned counts out (no extra copy op)
+  int64_t* sc_dst = !dev ? reinterpret_cast<int64_t*>(S.out_ids.as<uint8_t>() + 16 * B * kk) : out_scanned;
   if (ix->screen)
-    launch_rerank_merge(ix->metric, (int)B, ix->cpool.as<int4>(), ix->ccount.as<int32_t>(),
-                        ix->pool_cap, ix->cand_key.as<uint32_t>(), ix->cand_n.as<int32_t>(),
-                        ix->slot_off.as<int32_t>(), lt2, ix->q.as<float>(), ix->probe.as<int32_t>(),
-                        nprobe, kk, o_ids, o_d, o_cid, o_n, ix->nsurv.as<int32_t>(), st);
+    launch_rerank_merge(ix->metric, (int)B, S.cpool.as<int4>(), S.ccount.as<int32_t>(),
+                        ix->pool_cap, S.cand_key.as<uint32_t>(), S.cand_n.as<int32_t>(),
+                        S.slot_off.as<int32_t>(), lt2, S.q.as<float>(), S.probe.as<int32_t>(),
+                        nprobe, kk, o_ids, o_d, o_cid, o_n, S.nsurv.as<int32_t>(),
+                        S.scanned.as<int64_t>(), sc_dst, st);
   else
-    launch_merge((int)B, ix->slot_off.as<int32_t>(), ix->cand_key.as<uint32_t>(),
-                 ix->cand_id.as<int64_t>(), ix->cand_n.as<int32_t>(), ix->cand_list.as<int32_t>(), kk,
+    launch_merge((int)B, S.slot_off.as<int32_t>(), S.cand_key.as<uint32_t>(),
+                 S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(), kk,
                  lt2, o_ids, o_d, o_cid, o_n, st);
   CK(cudaGetLastError());
   if (!dev) {
     const int64_t nkk = B * kk;
-    uint8_t* base = ix->out_ids.as<uint8_t>();
-    CK(cudaMemcpyAsync(base + 16 * nkk, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+    uint8_t* base = S.out_ids.as<uint8_t>();
+    if (!ix->screen)
+      CK(cudaMemcpyAsync(base + 16 * nkk, S.scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
     if ((int64_t)ix->hout_bytes < ob) {
       if (ix->hout) cudaFreeHost(ix->hout);
       ix->hout = nullptr;
@@ -1549,8 +1623,8 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     if (out_scanned) memcpy(out_scanned, h + 16 * nkk, B * 8);
     memcpy(out_dists, h + 16 * nkk + 8 * B, nkk * 4);
     memcpy(out_n, h + 20 * nkk + 8 * B, B * 4);
-  } else if (out_scanned) {
-    CK(cudaMemcpyAsync(out_scanned, ix->scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
+  } else if (out_scanned && !ix->screen) {
+    CK(cudaMemcpyAsync(out_scanned, S.scanned.p, (size_t)B * 8, cudaMemcpyDeviceToDevice, st));
   }
   PROF(6);
   if (ix->prof) ix->prof_calls++;
@@ -1558,7 +1632,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (out_probe) {
     // probe slots -> cids (host mirror); forces a sync
     std::vector<int32_t> ps((size_t)B * nprobe);
-    CK(cudaMemcpyAsync(ps.data(), ix->probe.p, ps.size() * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ps.data(), S.probe.p, ps.size() * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     std::vector<int64_t> pc(ps.size());
     for (size_t i = 0; i < ps.size(); i++) pc[i] = ps[i] >= 0 ? ix->h_cid[ps[i]] : -1;
@@ -1575,7 +1649,7 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
               int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids, float* out_dists,
               int64_t* out_cids, int32_t* out_n, int64_t* out_probe, int64_t* out_scanned,
               int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   const bool dev = flags & PK_DEVICE_PTRS;
   return search_core(ix, Q, B, scope_codes, nscopes, nprobe, kk, out_ids, out_dists, out_cids,
                      out_n, out_probe, out_scanned, dev, dev, nullptr, nullptr);
@@ -1583,7 +1657,7 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 
 int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
                      const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (slot < 0 || slot > 1) return fail(PK_ERR_USAGE, "slot must be 0 or 1");
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
   auto& a = ix->aslot[slot];
@@ -1612,6 +1686,7 @@ int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
   CK(cudaMemcpyAsync(a.qin.p, Q, (size_t)B * ix->d * 4, cudaMemcpyHostToDevice, ix->cst));
   CK(cudaEventRecord(a.copied, ix->cst));
   CK(cudaStreamWaitEvent(ix->st, a.copied, 0));
+  ix->front_wait = a.copied;  // an overlapped front half waits for the copy itself
   uint8_t* base = a.blk.as<uint8_t>();
   const int64_t nkk = B * kk;
   RET(search_core(ix, a.qin.as<float>(), B, scope_codes, nscopes, nprobe, kk,
@@ -1634,7 +1709,8 @@ int pk_search_collect(pk_index* ix, int32_t slot, int64_t* out_ids, float* out_d
   auto& a = ix->aslot[slot];
   if (!a.busy) return fail(PK_ERR_USAGE, "slot %d has no search in flight", slot);
   CK(cudaEventSynchronize(a.done));  // outside the index lock: the other slot may submit meanwhile
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  // uncounted: collecting queues nothing, so the next submit may still overlap
+  std::lock_guard<std::recursive_mutex> lock_(ix->mu.m);
   const int64_t B = a.B, nkk = B * a.kk;
   const uint8_t* h = a.hblk;
   memcpy(out_ids, h, nkk * 8);
@@ -1648,7 +1724,7 @@ int pk_search_collect(pk_index* ix, int32_t slot, int64_t* out_ids, float* out_d
 
 int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
                      int32_t nscopes, int32_t nprobe, int32_t* out_probe, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!out_probe) return fail(PK_ERR_USAGE, "out_probe is required");
   const bool dev = flags & PK_DEVICE_PTRS;
   return search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
@@ -1657,7 +1733,7 @@ int pk_search_coarse(pk_index* ix, const float* Q, int64_t B, const int32_t* sco
 
 int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe, int32_t nprobe,
                      int32_t kk, int64_t group, void* out_blocks, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!probe || !out_blocks) return fail(PK_ERR_USAGE, "probe and out_blocks are required");
   if (group < 1 || B % group != 0) return fail(PK_ERR_USAGE, "group must divide the batch");
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
@@ -1688,7 +1764,7 @@ int pk_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* pro
 
 int pk_combine_create(pk_index* ix, int32_t R, int32_t my_rank, int64_t group, int32_t kk,
                       void* ipc_handle_out) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (R < 1 || my_rank < 0 || my_rank >= R || group < 1 || kk < 1 || kk > KKMAX)
     return fail(PK_ERR_USAGE, "bad combine shape");
   if ((int64_t)R * kk > shard_merge_cap()) return fail(PK_ERR_USAGE, "ranks x kk above %d", shard_merge_cap());
@@ -1719,7 +1795,7 @@ int pk_combine_create(pk_index* ix, int32_t R, int32_t my_rank, int64_t group, i
 }
 
 int pk_combine_open(pk_index* ix, int32_t peer, const void* ipc_handle, void* area_ptr) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   auto& c = ix->comb;
   if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
   if (peer < 0 || peer >= c.R) return fail(PK_ERR_USAGE, "bad peer %d", peer);
@@ -1743,7 +1819,7 @@ void* pk_combine_area(pk_index* ix) { return ix ? ix->comb.area : nullptr; }
 
 int pk_combine_search_probed(pk_index* ix, const float* Q, int64_t B, const int32_t* probe,
                              int32_t nprobe, int64_t epoch, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   auto& c = ix->comb;
   if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
   if (!(flags & PK_DEVICE_PTRS)) return fail(PK_ERR_USAGE, "peer combine takes device pointers");
@@ -1773,7 +1849,7 @@ int pk_combine_search_probed(pk_index* ix, const float* Q, int64_t B, const int3
 
 int pk_combine_merge(pk_index* ix, int64_t epoch, double timeout_s, int64_t* out_ids, float* out_dists,
                      int64_t* out_cids, int32_t* out_n, int64_t* out_scanned, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   auto& c = ix->comb;
   if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
   if (!(flags & PK_DEVICE_PTRS)) return fail(PK_ERR_USAGE, "peer combine takes device pointers");
@@ -1785,7 +1861,7 @@ int pk_combine_merge(pk_index* ix, int64_t epoch, double timeout_s, int64_t* out
 }
 
 int pk_combine_status(pk_index* ix, int32_t* err) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!ix->comb.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
   CK(cudaMemcpyAsync(err, ix->comb.err, 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
@@ -1794,7 +1870,7 @@ int pk_combine_status(pk_index* ix, int32_t* err) {
 
 int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
                           int32_t nscopes, int32_t nprobe, int64_t* out_cids) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!out_cids) return fail(PK_ERR_USAGE, "out_cids is required");
   std::vector<int32_t> pr((size_t)std::max<int64_t>(B, 0) * std::max(nprobe, 1));
   RET(search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
@@ -1805,7 +1881,7 @@ int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t
 
 int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, int64_t* out_ids,
                   float* out_dists, int64_t* out_prefix) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (m < 0) return fail(PK_ERR_USAGE, "negative list count");
   out_prefix[0] = 0;
   if (m == 0) return PK_OK;
@@ -1852,41 +1928,44 @@ int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, 
 }
 
 int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
-  if ((size_t)B * 4 > ix->ccount.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
-  CK(cudaMemcpyAsync(out, ix->ccount.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
+  auto& S = ix->scr[ix->last_par];
+  if ((size_t)B * 4 > S.ccount.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
+  CK(cudaMemcpyAsync(out, S.ccount.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 
 int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!ix->screen) return fail(PK_ERR_USAGE, "no candidate pools: exact scan mode");
-  if ((size_t)B * 4 > ix->nsurv.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
-  CK(cudaMemcpyAsync(out, ix->nsurv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
+  auto& S = ix->scr[ix->last_par];
+  if ((size_t)B * 4 > S.nsurv.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
+  CK(cudaMemcpyAsync(out, S.nsurv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 
 int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!ix->coarse_tc) return fail(PK_ERR_USAGE, "exact coarse quantizer: no screened candidates");
-  if ((size_t)B * 4 > ix->ncand.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
-  CK(cudaMemcpyAsync(out, ix->ncand.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
+  auto& S = ix->scr[ix->last_par];
+  if ((size_t)B * 4 > S.ncand.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
+  CK(cudaMemcpyAsync(out, S.ncand.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
   return PK_OK;
 }
 
 int pk_profile_begin(pk_index* ix) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   ix->prof = true;
   ix->prof_calls = 0;
   return PK_OK;
 }
 
 int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   CK(cudaStreamSynchronize(ix->st));
   const int ns = std::min(nstages, pk_index::NSTAGE);
   for (int k = 0; k < nstages; k++) stage_ms[k] = 0.0;
@@ -1906,7 +1985,7 @@ int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls) {
 
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags) {
-  std::lock_guard<std::recursive_mutex> lock_(ix->mu);
+  std::lock_guard<CountedMutex> lock_(ix->mu);
   if (n < 0) return fail(PK_ERR_USAGE, "negative count");
   if (n == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
@@ -1915,21 +1994,21 @@ int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64
   RET(ix->sync_table());
   const int64_t dp = ix->dp;
   const int32_t ns = std::max<int32_t>(ix->nslots, 1);
-  const bool fresh_q = ix->q.bytes < (size_t)n * dp * 4;
-  RET(ix->q.ensure((size_t)n * dp * 4));
-  if (fresh_q) CK(cudaMemsetAsync(ix->q.p, 0, ix->q.bytes, st));
-  RET(ix->qnorm.ensure(n * 4));
-  RET(ix->dc.ensure((size_t)n * ns * 4));
+  const bool fresh_q = ix->assign_q.bytes < (size_t)n * dp * 4;
+  RET(ix->assign_q.ensure((size_t)n * dp * 4));
+  if (fresh_q) CK(cudaMemsetAsync(ix->assign_q.p, 0, ix->assign_q.bytes, st));
+  RET(ix->assign_qn.ensure(n * 4));
+  RET(ix->assign_dc.ensure((size_t)n * ns * 4));
   RET(ix->assign_c.ensure(n * 8));
   RET(ix->assign_d.ensure(n * 4));
-  CK(cudaMemcpy2DAsync(ix->q.p, dp * 4, X, ix->d * 4, ix->d * 4, n,
+  CK(cudaMemcpy2DAsync(ix->assign_q.p, dp * 4, X, ix->d * 4, ix->d * 4, n,
                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
-  if (ix->metric == COSINE) launch_qnorm(ix->q.as<float>(), dp, (int)n, (int)ix->d, ix->qnorm.as<float>(), st);
-  launch_dist_dense(ix->metric, ix->q.as<float>(), dp, (int)n, ix->d_cent, dp, ix->nslots, (int)dp,
-                    ix->qnorm.as<float>(), ix->dc.as<float>(), ns, st);
+  if (ix->metric == COSINE) launch_qnorm(ix->assign_q.as<float>(), dp, (int)n, (int)ix->d, ix->assign_qn.as<float>(), st);
+  launch_dist_dense(ix->metric, ix->assign_q.as<float>(), dp, (int)n, ix->d_cent, dp, ix->nslots, (int)dp,
+                    ix->assign_qn.as<float>(), ix->assign_dc.as<float>(), ns, st);
   int64_t* oc = dev ? out_cid : ix->assign_c.as<int64_t>();
   float* od = dev ? out_dist : ix->assign_d.as<float>();
-  launch_argmin(ix->dc.as<float>(), ns, (int)n, ix->table(), scope_code, oc, od, st);
+  launch_argmin(ix->assign_dc.as<float>(), ns, (int)n, ix->table(), scope_code, oc, od, st);
   CK(cudaGetLastError());
   if (!dev) {
     CK(cudaMemcpyAsync(out_cid, oc, n * 8, cudaMemcpyDeviceToHost, st));

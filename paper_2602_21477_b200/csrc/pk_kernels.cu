@@ -27,8 +27,8 @@ constexpr unsigned FULL = 0xffffffffu;
 // while the previous kernel on the stream drains; it calls pdl_wait() before
 // touching that kernel's outputs.
 template <typename... KArgs, typename... Args>
-static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args... args) {
+static void launch_maybe_pdl(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                             cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -38,8 +38,13 @@ static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  launch_maybe_pdl(true, kernel, grid, block, smem, st, args...);
 }
 
 template <int METRIC>
@@ -1751,7 +1756,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
                     float* qsw, bool qsw_ready, const float* qnorm2, const ScanItem* items,
                     const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
                     int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
-                    int32_t* ccount, int cap, int num_sms, cudaStream_t st) {
+                    int32_t* ccount, int cap, int num_sms, cudaStream_t st, bool pdl) {
   if (max_items <= 0) return;
   if (!qsw_ready) qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
   const size_t smem = tc_smem_bytes();
@@ -1764,7 +1769,8 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   {                                                                                              \
     auto k = scan_tc_kernel<M>;                                                                  \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
-    launch_pdl(k, dim3(grid), dim3(TC_THREADS), smem, st, maps, lt, (const float*)qsw, (int64_t)B, \
+    launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, lt, (const float*)qsw,   \
+               (int64_t)B, \
                qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
                ccount, cap, dbg_skip);                                                             \
   }
@@ -1833,9 +1839,10 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     const int32_t* __restrict__ slot_off, ListTable lt, const float* __restrict__ Qd,
     const int32_t* __restrict__ probe, int nprobe, int kk, int stage_floats, int64_t* __restrict__ out_ids,
     float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n,
-    int32_t* __restrict__ nsurv) {
+    int32_t* __restrict__ nsurv, const int64_t* __restrict__ scanned_src, int64_t* __restrict__ scanned_dst) {
   pdl_trigger();
   pdl_wait();
+  if (scanned_dst && threadIdx.x == 0) scanned_dst[blockIdx.x] = scanned_src[blockIdx.x];
   extern __shared__ __align__(16) uint8_t rr_smem[];
   Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [RR_CAP]
   float4* qs4 = reinterpret_cast<float4*>(rr_smem + RR_CAP * sizeof(Entry));     // [dp/4]
@@ -2033,7 +2040,8 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          const uint32_t* slot_hi, const int32_t* slot_n, const int32_t* slot_off,
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
-                         int32_t* nsurv, cudaStream_t st) {
+                         int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
+                         cudaStream_t st) {
   if (B <= 0) return;
   // column-block stage of ~56 KB (two CTAs per SM)
   const int stage_floats = 56 * 1024 / 4;
@@ -2043,7 +2051,8 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
     auto k = rerank_merge_kernel<M>;                                                            \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     launch_pdl(k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
-                                   nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv); \
+                                   nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv,  \
+                                   scanned_src, scanned_dst);                                    \
   }
   if (metric == SQ_L2) PK_RR(SQ_L2)
   else PK_RR(IP)

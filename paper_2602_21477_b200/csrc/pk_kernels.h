@@ -121,7 +121,8 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          const uint32_t* slot_hi, const int32_t* slot_n, const int32_t* slot_off,
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
-                         int32_t* nsurv, cudaStream_t st);
+                         int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
+                         cudaStream_t st);
 float screen_coef(int metric, int dp);
 float screen_coef_tf32(int metric, int dp);
 size_t tc_smem_bytes();
@@ -133,7 +134,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
                     float* qsw, bool qsw_ready, const float* qnorm2, const ScanItem* items,
                     const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
                     int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
-                    int32_t* ccount, int cap, int num_sms, cudaStream_t st);
+                    int32_t* ccount, int cap, int num_sms, cudaStream_t st, bool pdl = true);
 
 // Cross-shard merge of R per-shard result blocks (layout: pk_shard_block_bytes
 // in include/pancake_b200.h) into the global top-kk per query.

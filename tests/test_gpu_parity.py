@@ -384,6 +384,56 @@ def test_async_submit_collect_equals_search(pk):
     ix.close()
 
 
+def test_back_to_back_device_searches_overlap_safely(pk):
+    """Device-pointer searches issued back to back overlap the next batch's
+    front half (prep / coarse / pick / routing on a side stream) with the
+    previous batch's scan and re-rank; every batch still equals its own
+    synchronous answer, also across a mutation between two searches (which
+    turns the overlap off for the next one)."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    d, nlist = 128, 48
+    sizes = rng.integers(1, 900, nlist)
+    ix, lists, cents, cids = _random_index(pk, rng, d, nlist, sizes)
+    dev = torch.device("cuda:0")
+    codes = torch.zeros(1, dtype=torch.int32, device=dev)
+    plan = [(int(rng.integers(1, 300)), int(rng.integers(1, 20)), int(rng.integers(1, 65)))
+            for _ in range(12)]
+    batches = [rng.normal(size=(B, d)).astype(np.float32) for B, _, _ in plan]
+    extra = (rng.normal(size=(300, d)) + cents[4]).astype(np.float32)
+    extra_ids = np.arange(10**6, 10**6 + 300, dtype=np.int64)
+    outs = []
+    Qds = [torch.from_numpy(Q).to(dev) for Q in batches]
+    torch.cuda.synchronize()  # the index stream is not ordered after torch's
+    for i, ((B, nprobe, kk), Qd) in enumerate(zip(plan, Qds)):
+        if i == 8:  # a mutation between two device searches
+            ix.append(int(cids[4]), extra, extra_ids)
+        o = (torch.empty(B, kk, dtype=torch.int64, device=dev), torch.empty(B, kk, device=dev),
+             torch.empty(B, kk, dtype=torch.int64, device=dev), torch.empty(B, dtype=torch.int32, device=dev),
+             torch.empty(B, dtype=torch.int64, device=dev))
+        ix.search_device(Qd, codes, nprobe, kk, *o)
+        outs.append((Qd, o))
+    torch.cuda.synchronize()
+    # replay synchronously on a second index with the same history
+    rng2 = np.random.default_rng(21)
+    rng2.integers(1, 900, nlist)  # same draws as above: the same lists
+    ix2, *_ = _random_index(pk, rng2, d, nlist, sizes)
+    for i, ((B, nprobe, kk), Q) in enumerate(zip(plan, batches)):
+        if i == 8:
+            ix2.append(int(cids[4]), extra, extra_ids)
+        w = ix2.search(Q, [0], nprobe, kk)
+        ids, dd, cid, n, sc = (t.cpu().numpy() for t in outs[i][1])
+        assert np.array_equal(n, w.counts), i
+        for b in range(B):
+            m = int(n[b])
+            assert np.array_equal(ids[b, :m], w.ids[b, :m]), (i, b)
+            assert np.array_equal(bits(dd[b, :m]), bits(w.dists[b, :m])), (i, b)
+        assert np.array_equal(sc, w.scanned), i
+    ix.close()
+    ix2.close()
+
+
 def test_large_k_uses_the_per_query_pipeline(pk):
     """k above the batched device top-k (64) is answered exactly through the
     per-query pipeline (every probed row ranked, ref/engine.py:406-426)."""
