@@ -647,9 +647,38 @@ struct pk_index {
 
 // Default context for the stateless kernel-table entry points.
 namespace {
+// Pinned host staging: one packed DMA per call instead of pageable (driver
+// bounce-buffered, row-by-row 2-D) copies -- what small cache-pool and
+// centroid scans pay per call.
+struct PinnedBuf {
+  uint8_t* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t need) {
+    if (need <= bytes) return PK_OK;
+    size_t nb = std::max(need, bytes + bytes / 2);
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    CK(cudaHostAlloc((void**)&p, nb, cudaHostAllocDefault));
+    bytes = nb;
+    return PK_OK;
+  }
+};
+// rows [n][d] -> pinned [n][dp] (zero pad columns)
+void pack_padded(float* dst, const float* src, int64_t n, int64_t d, int64_t dp) {
+  if (d == dp) {
+    memcpy(dst, src, (size_t)n * d * 4);
+    return;
+  }
+  for (int64_t i = 0; i < n; i++) {
+    memcpy(dst + i * dp, src + i * d, (size_t)d * 4);
+    memset(dst + i * dp + d, 0, (size_t)(dp - d) * 4);
+  }
+}
 struct Ctx {
   cudaStream_t st = nullptr;
   DevBuf a, b, c, e;
+  PinnedBuf hin, hout;
   std::mutex mu;
 };
 Ctx& ctx() {
@@ -692,7 +721,17 @@ int pk_distances(const float* q, int64_t B, const float* mat, int64_t n, int64_t
   const bool inplace = dev && dp == d;
   const float* qa = q;
   const float* xa = mat;
-  if (!inplace) {
+  if (!dev) {  // host: pack [q | mat] padded into pinned memory, one DMA
+    const size_t nin = (size_t)(B + n) * dp;
+    RET(C.hin.ensure(nin * 4));
+    float* h = reinterpret_cast<float*>(C.hin.p);
+    pack_padded(h, q, B, d, dp);
+    pack_padded(h + (size_t)B * dp, mat, n, d, dp);
+    RET(C.a.ensure(nin * 4));
+    CK(cudaMemcpyAsync(C.a.p, h, nin * 4, cudaMemcpyHostToDevice, C.st));
+    qa = C.a.as<float>();
+    xa = qa + (size_t)B * dp;
+  } else if (!inplace) {
     RET(stage_padded(C.a, q, B, d, dp, dev, C.st));
     RET(stage_padded(C.b, mat, n, d, dp, dev, C.st));
     qa = C.a.as<float>();
@@ -703,12 +742,14 @@ int pk_distances(const float* q, int64_t B, const float* mat, int64_t n, int64_t
   float* D = out;
   if (!dev) {
     RET(C.c.ensure((size_t)B * n * 4));
+    RET(C.hout.ensure((size_t)B * n * 4));
     D = C.c.as<float>();
   }
   launch_dist_dense(metric, qa, dp, (int)B, xa, dp, n, (int)dp, C.e.as<float>(), D, n, C.st);
   CK(cudaGetLastError());
-  if (!dev) CK(cudaMemcpyAsync(out, D, (size_t)B * n * 4, cudaMemcpyDeviceToHost, C.st));
+  if (!dev) CK(cudaMemcpyAsync(C.hout.p, D, (size_t)B * n * 4, cudaMemcpyDeviceToHost, C.st));
   CK(cudaStreamSynchronize(C.st));
+  if (!dev) memcpy(out, C.hout.p, (size_t)B * n * 4);
   return PK_OK;
 }
 

@@ -76,14 +76,22 @@ __device__ __forceinline__ float step4(float acc, float4 x, float4 q) {
 // ref/core.py:98-109).  Used by the coarse quantizer over the centroid table,
 // by assign_nearest and by the kernel-table entry points.
 // =====================================================================
+// The block's 128 rows stream through shared memory in column blocks of DC
+// floats (coalesced 16-byte cp.async pieces, DD_RING-deep ring), so every
+// row chain runs from shared memory instead of one dependent global load per
+// float4 -- the latency that dominates small calls (cache pools, L1
+// centroids, a few hundred rows).
+constexpr int DD_RING = 3;
+constexpr int DD_RS = DC + 4;  // padded row stride in the ring (conflict-free float4 reads)
 template <int METRIC, int NQ>
 __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict__ Q, int64_t ldq,
                                                          int B, const float* __restrict__ X,
                                                          int64_t ldx, int64_t n, int dp,
                                                          const float* __restrict__ qnorm,
                                                          float* __restrict__ D, int64_t ldd) {
-  extern __shared__ float4 qs4[];  // [NQ][dp/4]
+  extern __shared__ float4 qs4[];  // [NQ][dp/4] | ring [DD_RING][128][DD_RS]
   const float* qs = reinterpret_cast<const float*>(qs4);
+  float* ring = reinterpret_cast<float*>(qs4) + (size_t)NQ * dp;
   const int b0 = blockIdx.y * NQ;
   const int nq = min(NQ, B - b0);
   const int dp4 = dp / 4;
@@ -94,21 +102,51 @@ __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict
     qs4[i] = v;
   }
   __syncthreads();
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t r = r0 + threadIdx.x;
   const bool valid = r < n;
-  const float* xr = X + (valid ? r : 0) * ldx;
+  const int nr = (int)(n - r0 < 128 ? n - r0 : 128);
+  // column block width: DC for a full block of rows, wider (fewer ring
+  // round trips) when the block holds few rows; a ring slot is 128 * DD_RS floats
+  int W = (128 * DD_RS / nr - 4) / DC * DC;
+  W = W < DC ? DC : (W > dp ? dp : W);
+  const int rs = W + 4;
+  const int nblk = (dp + W - 1) / W;
+  // block blk: rows [r0, r0 + nr) x columns [blk*W, +w)
+  auto issue = [&](int blk) {
+    if (blk < nblk) {
+      float* dst = ring + (size_t)(blk % DD_RING) * 128 * DD_RS;
+      const int w4 = min(W, dp - blk * W) / 4;
+      for (int i = threadIdx.x; i < nr * w4; i += 128) {
+        const int rr = i / w4, c = i - rr * w4;
+        cp_async16(dst + rr * rs + 4 * c, X + (r0 + rr) * ldx + blk * W + 4 * c);
+      }
+    }
+    cp_async_commit();  // empty groups keep the wait count uniform
+  };
+#pragma unroll
+  for (int i = 0; i < DD_RING - 1; i++) issue(i);
   float acc[NQ];
 #pragma unroll
   for (int a = 0; a < NQ; a++) acc[a] = 0.f;
   float nn = 0.f;
-  for (int j = 0; j < dp; j += 4) {
-    float4 x = __ldg(reinterpret_cast<const float4*>(xr + j));
+  for (int blk = 0; blk < nblk; blk++) {
+    issue(blk + DD_RING - 1);
+    cp_async_wait<DD_RING - 1>();
+    __syncthreads();
+    const float* xr = ring + (size_t)(blk % DD_RING) * 128 * DD_RS + (threadIdx.x < nr ? threadIdx.x : 0) * rs;
+    const int w = min(W, dp - blk * W);
+#pragma unroll 8
+    for (int j = 0; j < w; j += 4) {
+      const float4 x = *reinterpret_cast<const float4*>(xr + j);
 #pragma unroll
-    for (int a = 0; a < NQ; a++) {
-      float4 q = *reinterpret_cast<const float4*>(qs + a * dp + j);
-      acc[a] = step4<METRIC>(acc[a], x, q);
+      for (int a = 0; a < NQ; a++) {
+        float4 q = *reinterpret_cast<const float4*>(qs + a * dp + blk * W + j);
+        acc[a] = step4<METRIC>(acc[a], x, q);
+      }
+      if (METRIC == COSINE) nn = step4<IP>(nn, x, x);
     }
-    if (METRIC == COSINE) nn = step4<IP>(nn, x, x);
+    __syncthreads();  // slot blk % DD_RING is refilled by the next iteration's issue
   }
   if (!valid) return;
 #pragma unroll
@@ -127,7 +165,7 @@ static void dist_dense_dispatch(const float* Q, int64_t ldq, int B, const float*
   if (B <= 0 || n <= 0) return;
   int nq = B >= 16 ? 16 : (B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1)));
   while (nq > 1 && (size_t)nq * dp * 4 > 96 * 1024) nq >>= 1;
-  size_t smem = (size_t)nq * dp * 4;
+  size_t smem = (size_t)nq * dp * 4 + (size_t)DD_RING * 128 * DD_RS * 4;
   dim3 grid((unsigned)((n + 127) / 128), (unsigned)((B + nq - 1) / nq));
 #define PK_DD(NQV)                                                                                  \
   case NQV: {                                                                                       \

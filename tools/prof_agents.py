@@ -7,9 +7,10 @@ import sys
 import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.argv = ["x", "--agents", "4", "--rows", "50000", "--rounds", "8"]
+sys.argv = ["x"] + (sys.argv[1:] or ["--agents", "4", "--rows", "50000", "--rounds", "8"])
 import tools.bench_agents as BA  # noqa: E402
 
 cProfile.run("BA.main()", "/tmp/agents.prof")
 p = pstats.Stats("/tmp/agents.prof")
-p.sort_stats("tottime").print_stats(30)
+p.sort_stats("tottime").print_stats(35)
+p.sort_stats("cumulative").print_stats(45)
