@@ -456,20 +456,45 @@ __device__ int warp_compact64(Entry* buf, int n, int kk, bool dedup) {
 }
 // Sort buf[0..n) and keep the first kk (see cta_compact_sorted); small n runs
 // in warp 0 only.
+// Rank sort for n <= blockDim.x: thread i counts the entries ordered before
+// its own (ties by position: stable) and stores it at that rank -- n
+// independent shared-memory sweeps instead of log^2 dependent exchange
+// stages (measured ~10K cycles for the 64-entry warp bitonic).  With dedup
+// an entry equal (key, id) to an earlier one is dropped and ranks count the
+// first occurrences only (what cta_compact_sorted keeps).
+__device__ int block_rank_keep(Entry* buf, int n, int kk, bool dedup) {
+  __shared__ uint8_t s_dupf[1024];
+  const int t = threadIdx.x;
+  const bool act = t < n;
+  __syncthreads();
+  Entry e = act ? buf[t] : e_none();
+  bool dup = false;
+  if (dedup) {
+    if (act)
+      for (int j = 0; j < t; j++) {
+        const Entry o = buf[j];
+        dup |= (o.key == e.key) & (o.id == e.id);
+      }
+    s_dupf[t] = dup;
+    __syncthreads();
+  }
+  int rank = 0;
+  if (act && !dup)
+    for (int j = 0; j < n; j++) {
+      const Entry o = buf[j];
+      const bool eq = (o.key == e.key) & (o.id == e.id);
+      rank += dedup ? (e_less(o, e) & !s_dupf[j]) : (e_less(o, e) | (eq & (j < t)));
+    }
+  const int total = __syncthreads_count(act && !dup);  // also: every read of buf is done
+  if (act && !dup && rank < kk) buf[rank] = e;
+  __syncthreads();
+  return total < kk ? total : kk;
+}
+
 __device__ int block_sort_keep(Entry* buf, int n, int kk, bool dedup, int* s_cnt) {
-  if (n > 64) {
-    cta_bitonic_sort(buf, n);
-    return cta_compact_sorted(buf, n, kk, dedup, s_cnt);
-  }
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    warp_sort64(buf, n);
-    __syncwarp();
-    const int kept = warp_compact64(buf, n, kk, dedup);
-    if (threadIdx.x == 0) *s_cnt = kept;
-  }
-  __syncthreads();
-  return *s_cnt;
+  if (n <= (int)blockDim.x && n <= 1024) return block_rank_keep(buf, n, kk, dedup);
+  cta_bitonic_sort(buf, n);
+  return cta_compact_sorted(buf, n, kk, dedup, s_cnt);
 }
 
 constexpr int SEL_CAP = 4096;
@@ -1891,6 +1916,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
   __shared__ unsigned s_wu[RR_THREADS / 32];
 
   __shared__ uint32_t s_u[RR_THREADS / 32];
+  __shared__ int s_row[RR_THREADS];
   const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int dp4 = lt.dp / 4;
@@ -1973,43 +1999,50 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
       for (int g0 = 0; g0 < ns; g0 += chunk) {
         const int m = min(chunk, ns - g0);
         const int nd32 = dp4 / 8;
+        const int R = 2;  // (measured: 3-4 deep with narrower blocks is slower)
         int kq = 1;
         for (int k2 = nd32; k2 >= 1; k2--)
-          if (nd32 % k2 == 0 && 2 * m * (DC * k2 + 4) <= stage_floats) {
+          if (nd32 % k2 == 0 && R * m * (DC * k2 + 4) <= stage_floats) {
             kq = k2;
             break;
           }
         const int W = DC * kq, rs = W + 4, nblk = nd32 / kq;
+        // the survivors' arena rows, read once (not per 16-byte piece)
+        int4 my_e = make_int4(0, 0, 0, 0);
+        if (threadIdx.x < m) {
+          my_e = cpool[(int64_t)b * cap + surv[g0 + threadIdx.x]];
+          s_row[threadIdx.x] = my_e.x;
+        }
+        __syncthreads();
         auto issue = [&](int blk) {
-          float* dst = stage + (blk & 1) * m * rs;
-          const int w4 = W / 4;
-          for (int i = threadIdx.x; i < m * w4; i += RR_THREADS) {
-            const int r = i / w4, c = i - r * w4;
-            const int4 e = cpool[(int64_t)b * cap + surv[g0 + r]];
-            cp_async16(dst + r * rs + 4 * c, lt.rows + (int64_t)e.x * lt.dp + blk * W + 4 * c);
+          if (blk < nblk) {
+            float* dst = stage + (blk % R) * m * rs;
+            const int w4 = W / 4;
+            for (int i = threadIdx.x; i < m * w4; i += RR_THREADS) {
+              const int r = i / w4, c = i - r * w4;
+              cp_async16(dst + r * rs + 4 * c, lt.rows + (int64_t)s_row[r] * lt.dp + blk * W + 4 * c);
+            }
           }
-          cp_async_commit();
+          cp_async_commit();  // empty groups keep the wait count uniform
         };
-        issue(0);
+        for (int i = 0; i < R - 1; i++) issue(i);
         float acc = 0.f;
         for (int blk = 0; blk < nblk; blk++) {
-          if (blk + 1 < nblk) {
-            issue(blk + 1);
-            cp_async_wait<1>();
-          } else {
-            cp_async_wait<0>();
-          }
+          issue(blk + R - 1);
+          if (R == 4) cp_async_wait<3>();
+          else if (R == 3) cp_async_wait<2>();
+          else cp_async_wait<1>();
           __syncthreads();
           if (threadIdx.x < m) {
-            const float4* x4 = reinterpret_cast<const float4*>(stage + (blk & 1) * m * rs + threadIdx.x * rs);
+            const float4* x4 = reinterpret_cast<const float4*>(stage + (blk % R) * m * rs + threadIdx.x * rs);
             const float4* q4 = qs4 + blk * (W / 4);
 #pragma unroll 4
             for (int j = 0; j < W / 4; j++) acc = step4<METRIC>(acc, x4[j], q4[j]);
           }
-          __syncthreads();  // ring slot (blk & 1) is refilled for block blk + 2
+          __syncthreads();  // ring slot blk % R is refilled by the next issue
         }
         if (threadIdx.x < m) {
-          const int4 e = cpool[(int64_t)b * cap + surv[g0 + threadIdx.x]];
+          const int4 e = my_e;
           Entry en;
           en.key = f2key(finalize<METRIC>(acc, 0.f, 0.f));
           en.id = lt.ids[e.x];
@@ -2622,9 +2655,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
   pdl_wait();  // coarse partial dots
   auto mark = [&](int i) {  // phase timestamps (PK_DEBUG_PICK)
     if (dbg && threadIdx.x == 0) {
-      uint64_t t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      dbg[blockIdx.x * 8 + i] = t;
+      dbg[blockIdx.x * 8 + i] = (uint64_t)clock64();  // SM cycles (phase lengths within a CTA)
     }
   };
   mark(0);
@@ -2756,35 +2787,37 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     for (int c0 = kept; c0 < n; c0 += PICK_THREADS) {
       const int nr = min(PICK_THREADS, n - c0);
       const int nd32 = lt.dp / DC;
-      int k = 1;  // W = 32 k floats, k | dp/32, 2 * nr * (W + 4) floats fit the stage
+      // W = 32 k floats, k | dp/32, PICK_RING * nr * (W + 4) floats fit the stage
+      const int PICK_RING = 2;  // (measured: 3-4 deep with narrower blocks is slower)
+      int k = 1;
       for (int kk2 = nd32; kk2 >= 1; kk2--)
-        if (nd32 % kk2 == 0 && 2 * nr * (DC * kk2 + 4) <= stage_floats) {
+        if (nd32 % kk2 == 0 && PICK_RING * nr * (DC * kk2 + 4) <= stage_floats) {
           k = kk2;
           break;
         }
       const int W = DC * k, rs = W + 4, nblk = nd32 / k;
-      // every thread streams 16-byte pieces of the block (cp.async, 2-deep ring)
+      // every thread streams 16-byte pieces of the block (cp.async ring)
       auto issue = [&](int blk) {
-        float* dst = rows_st + (blk & 1) * nr * rs;
-        const int w4 = W / 4;
-        for (int i = tid; i < nr * w4; i += PICK_THREADS) {
-          const int r = i / w4, c = i - r * w4;
-          cp_async16(dst + r * rs + 4 * c, lt.cent + (int64_t)buf[c0 + r].pay * lt.dp + blk * W + 4 * c);
+        if (blk < nblk) {
+          float* dst = rows_st + (blk % PICK_RING) * nr * rs;
+          const int w4 = W / 4;
+          for (int i = tid; i < nr * w4; i += PICK_THREADS) {
+            const int r = i / w4, c = i - r * w4;
+            cp_async16(dst + r * rs + 4 * c, lt.cent + (int64_t)buf[c0 + r].pay * lt.dp + blk * W + 4 * c);
+          }
         }
-        cp_async_commit();
+        cp_async_commit();  // empty groups keep the wait count uniform
       };
-      issue(0);
+      for (int i = 0; i < PICK_RING - 1; i++) issue(i);
       float acc = 0.f;
       for (int blk = 0; blk < nblk; blk++) {
-        if (blk + 1 < nblk) {
-          issue(blk + 1);
-          cp_async_wait<1>();
-        } else {
-          cp_async_wait<0>();
-        }
+        issue(blk + PICK_RING - 1);
+        if (PICK_RING == 4) cp_async_wait<3>();
+        else if (PICK_RING == 3) cp_async_wait<2>();
+        else cp_async_wait<1>();
         __syncthreads();
         if (tid < nr) {
-          const float* x = rows_st + (blk & 1) * nr * rs + tid * rs;
+          const float* x = rows_st + (blk % PICK_RING) * nr * rs + tid * rs;
           const float* q = qs + blk * W;
           const int jn = min(W, lt.d - blk * W);
           int j = 0;
@@ -2793,7 +2826,7 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
                                 *reinterpret_cast<const float4*>(q + j));
           for (; j < jn; j++) acc = (METRIC == SQ_L2) ? sq_step(acc, x[j], q[j]) : ip_step(acc, x[j], q[j]);
         }
-        __syncthreads();  // ring slot (blk & 1) is refilled for block blk + 2
+        __syncthreads();  // ring slot blk % PICK_RING is refilled by the next issue
       }
       if (tid < nr) buf[c0 + tid].key = f2key(METRIC == SQ_L2 ? acc : -acc);
     }
@@ -2875,10 +2908,13 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
       t0 = std::min(t0, h[b * 8]);
       t1 = std::max(t1, h[b * 8 + 7]);
     }
-    fprintf(stderr, "pick phases (us, mean per CTA): prologue %.2f bounds %.2f radix %.2f collect %.2f "
-                    "exact %.2f sort %.2f out %.2f | span %.2f\n",
-            acc[1] / B / 1e3, acc[2] / B / 1e3, acc[3] / B / 1e3, acc[4] / B / 1e3, acc[5] / B / 1e3,
-            acc[6] / B / 1e3, acc[7] / B / 1e3, (t1 - t0) / 1e3);
+    (void)t0;
+    (void)t1;
+    const double cyc_us = 1965.0;  // SM cycles per us at the B200 boost clock
+    fprintf(stderr, "pick phases (us, mean per CTA @1965 MHz): prologue %.2f bounds %.2f radix %.2f "
+                    "collect %.2f exact %.2f sort %.2f out %.2f\n",
+            acc[1] / B / cyc_us, acc[2] / B / cyc_us, acc[3] / B / cyc_us, acc[4] / B / cyc_us,
+            acc[5] / B / cyc_us, acc[6] / B / cyc_us, acc[7] / B / cyc_us);
     cudaFreeAsync(dbg, st);
   }
 }
