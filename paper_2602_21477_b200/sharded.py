@@ -107,6 +107,7 @@ class ShardedIndex:
         self.local = local if local is not None else DeviceIndex(
             dimension, metric_code, device, reserve_rows=reserve_rows, reserve_lists=reserve_lists)
         self.owner: dict[int, int] = {}
+        self.dirty: dict[int, int] = {}  # rows appended per list since its last maintenance
 
     # ---- exchange -------------------------------------------------------
     def _all_gather(self, t):
@@ -166,6 +167,58 @@ class ShardedIndex:
                 self.local.add_remote_list(int(cids[i]), int(scopes[i]), allc[owners[i], pos[i]])
         self.owner = {int(c): int(o) for c, o in zip(cids, owners)}
         return owners
+
+    # ---- inserts ------------------------------------
+    def insert(self, X, ids, scope_code: int, maintenance_interval: int = 256) -> np.ndarray:
+        """Insert a batch that every rank receives (the ``agent=None`` path,
+        ref/engine.py:571-605 / 647-660): each vector goes to the nearest
+        in-scope list (assign_nearest, ref/clusters.py:268-279; ties -> lower
+        cid), computed identically on every rank from the replicated
+        centroids; the owner appends the row (Cluster.add).  When a list's
+        dirty count reaches ``maintenance_interval`` its owner recomputes the
+        centroid (fp64 row-order mean, ref/clusters.py:111-118, 294-299), the
+        new centroid is broadcast and every rank applies it before the next
+        vector is assigned -- the same op index everywhere, so the sharded
+        index stays equal to the single-GPU one.  Returns the assigned cids."""
+        import torch
+
+        X = np.ascontiguousarray(X, dtype=np.float32).reshape(-1, self.dimension)
+        ids = np.ascontiguousarray(ids, dtype=np.int64).reshape(-1)
+        if len(ids) != len(X):
+            raise ValueError("one id per row")
+        n = len(X)
+        out = np.empty(n, dtype=np.int64)
+        i = 0
+        while i < n:
+            cid, _ = self.local.assign(X[i:], scope_code)
+            j, fired = i, None
+            while j < n:  # up to (and including) the vector whose insert triggers maintenance
+                c = int(cid[j - i])
+                out[j] = c
+                self.dirty[c] = self.dirty.get(c, 0) + 1
+                j += 1
+                if self.dirty[c] >= maintenance_interval:
+                    fired = c
+                    break
+            for k in range(i, j):
+                c = int(out[k])
+                if self.owner.get(c) == self.rank:
+                    self.local.append(c, X[k:k + 1], ids[k:k + 1])
+            if fired is not None:
+                src = self.owner[fired]
+                cent = np.zeros(self.dimension, dtype=np.float32)
+                if src == self.rank:
+                    cent = np.asarray(self.local.recompute(fired), dtype=np.float32)
+                if self.world > 1:
+                    t = torch.from_numpy(cent).to(self.comm_device)
+                    g_src = src if self.group is None else self.dist.get_global_rank(self.group, src)
+                    self.dist.broadcast(t, g_src, group=self.group)
+                    cent = t.cpu().numpy()
+                if src != self.rank:
+                    self.local.set_centroid(fired, cent)
+                self.dirty[fired] = 0
+            i = j
+        return out
 
     # ---- search ---------------------------------------------------------
     def search(self, Q, scope_codes, nprobe: int, kk: int) -> SearchOutput:

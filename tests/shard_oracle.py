@@ -28,6 +28,36 @@ class OracleShard:
         self.lists.append((int(cid), int(scope), np.zeros((0, self.d), np.float32),
                            np.zeros(0, np.int64), np.asarray(centroid, np.float32)))
 
+    def _at(self, cid):
+        return next(i for i, l in enumerate(self.lists) if l[0] == int(cid))
+
+    def assign(self, X, scope_code):
+        """assign_nearest per row over the in-scope lists (ties -> lower cid)."""
+        X = np.ascontiguousarray(X, dtype=np.float32).reshape(-1, self.d)
+        cand = [l for l in self.lists if l[1] == int(scope_code)]
+        cents = np.stack([l[4] for l in cand])
+        cids = np.array([l[0] for l in cand], dtype=np.int64)
+        out = np.array([O.assign_nearest(x, cents, cids) for x in X], dtype=np.int64)
+        return out, np.zeros(len(X), np.float32)
+
+    def append(self, cid, rows, ids):
+        i = self._at(cid)
+        c, s, r, ii, cent = self.lists[i]
+        rows = np.ascontiguousarray(rows, dtype=np.float32).reshape(-1, self.d)
+        self.lists[i] = (c, s, np.concatenate([r, rows]), np.concatenate([ii, np.asarray(ids, np.int64)]), cent)
+
+    def recompute(self, cid):
+        i = self._at(cid)
+        c, s, r, ii, _ = self.lists[i]
+        cent = O.centroid(r)
+        self.lists[i] = (c, s, r, ii, cent)
+        return cent
+
+    def set_centroid(self, cid, centroid):
+        i = self._at(cid)
+        c, s, r, ii, _ = self.lists[i]
+        self.lists[i] = (c, s, r, ii, np.asarray(centroid, np.float32).copy())
+
     def centroid_of(self, rows):
         return O.centroid(np.ascontiguousarray(rows, dtype=np.float32).reshape(-1, self.d))
 

@@ -60,6 +60,36 @@ def _make_lists(seed, nlist, d):
     return [lists[c] for c in keep], [100 + 3 * c for c in keep], Q
 
 
+INS_INTERVAL = 5  # small, so maintenance fires many times inside one batch
+
+
+def _insert_batch(seed, d):
+    rng = np.random.default_rng(seed + 100)
+    X = (0.8 * rng.normal(size=(120, d))).astype(np.float32)
+    return X, np.arange(10**6, 10**6 + len(X), dtype=np.int64)
+
+
+def _sequential_inserts(lists, cids, X, ids, interval):
+    """The reference's per-vector insert (ref/engine.py:647-660): assign to the
+    nearest list, append, recompute the centroid when its dirty count
+    reaches the interval."""
+    lists = [(i.copy(), r.copy()) for i, r in lists]
+    cents = [O.centroid(r) for _, r in lists]
+    dirty = [0] * len(lists)
+    cid_arr = np.array(cids, np.int64)
+    assigned = []
+    for x, iid in zip(X, ids):
+        c = O.assign_nearest(x, np.stack(cents), cid_arr)
+        j = cids.index(c)
+        assigned.append(c)
+        lists[j] = (np.append(lists[j][0], iid), np.concatenate([lists[j][1], x[None]]))
+        dirty[j] += 1
+        if dirty[j] >= interval:
+            cents[j] = O.centroid(lists[j][1])
+            dirty[j] = 0
+    return lists, np.stack(cents), np.array(assigned, np.int64)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -85,9 +115,15 @@ def _worker(rank, world, port, outdir, seed, nprobe, kk):
     per = len(Q) // world
     mine = Q[rank * per:(rank + 1) * per]
     dsp = sh.search_dispatch(mine, [0], nprobe, kk)
+    # inserts (every rank the same batch): assignment over replicated centroids,
+    # owner appends, maintenance recompute broadcast from the owner
+    Xi, ids_i = _insert_batch(seed, d)
+    assigned = sh.insert(Xi, ids_i, 0, maintenance_interval=INS_INTERVAL)
+    ins = sh.search(Q, [0], nprobe, kk)
     np.savez(os.path.join(outdir, f"r{rank}.npz"), ids=out.ids, d=out.dists, cids=out.cids,
              n=out.counts, sc=out.scanned, owners=owners, dids=dsp.ids, dd=dsp.dists,
-             dc=dsp.cids, dn=dsp.counts, dsc=dsp.scanned)
+             dc=dsp.cids, dn=dsp.counts, dsc=dsp.scanned, assigned=assigned, iids=ins.ids,
+             idd=ins.dists, icids=ins.cids, in_=ins.counts, isc=ins.scanned)
     dist.destroy_process_group()
 
 
@@ -123,6 +159,22 @@ def test_gloo_sharded_search_equals_single_index(tmp_path, world):
         assert np.array_equal(x["dn"], cnt[sl])
         assert np.array_equal(x["dsc"], sc[sl])
         assert np.array_equal(x["dc"], exp_c[sl])
+    # inserts: same assignment as the sequential reference path, and the
+    # search after them equals the single index built by that path
+    Xi, ids_i = _insert_batch(seed, d)
+    lists2, cents2, assigned = _sequential_inserts(lists, cids, Xi, ids_i, INS_INTERVAL)
+    flat2 = O.FlatIVF.from_lists(lists2, cents2, np.array(cids, np.int64))
+    ids2, dd2, cnt2, _, sc2 = flat2.search(Q, nprobe, kk)
+    id2cid2 = {int(i): c for (ii, _), c in zip(lists2, cids) for i in ii}
+    for r in res:
+        assert np.array_equal(r["assigned"], assigned)
+        assert np.array_equal(r["iids"], ids2)
+        assert np.array_equal(r["idd"].view(np.uint32), dd2.view(np.uint32))
+        assert np.array_equal(r["in_"], cnt2)
+        assert np.array_equal(r["isc"], sc2)
+        assert np.array_equal(r["icids"], np.vectorize(lambda i: id2cid2.get(int(i), -1),
+                                                       otypes=[np.int64])(ids2))
+    assert not np.array_equal(cents2, np.stack([O.centroid(r) for _, r in lists]))
     # every rank derived the same placement, and both ranks own lists
     assert np.array_equal(res[0]["owners"], res[1]["owners"])
     assert set(res[0]["owners"].tolist()) == {0, 1}
