@@ -172,6 +172,24 @@ def profile_reorder(entries, default_order):
     return front + [lid for lid in default_order if lid not in seen]
 
 
+def profile_order(entries, size: int) -> np.ndarray:
+    """``profile_reorder(entries, range(size))`` as index arrays: the profile's
+    rows first (first occurrence, rows outside [0, size) skipped), then every
+    other row in order -- the per-probed-list scan order of scan_ids, without
+    a Python pass over all of the list's rows."""
+    if not entries:
+        return np.arange(size)
+    e = np.asarray(entries, dtype=np.int64)
+    e = e[(e >= 0) & (e < size)]
+    if len(e) == 0:
+        return np.arange(size)
+    _, first = np.unique(e, return_index=True)
+    front = e[np.sort(first)]
+    rest = np.ones(size, dtype=bool)
+    rest[front] = False
+    return np.concatenate([front, np.flatnonzero(rest)])
+
+
 def profile_promote(entries, hits, p_size):
     """ref/graph.py:454-463."""
     hit_seen, front = set(), []
@@ -403,7 +421,7 @@ class Store:
                 self.tier.record_access(cid)
                 if want_scan_ids:
                     if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
-                        order = profile_reorder(cl.profiles[agent], list(range(cl.size)))
+                        order = profile_order(cl.profiles[agent], cl.size)
                         scan_chunks.append(cl.member_ids[order])
                     else:
                         scan_chunks.append(cl.member_ids.copy())
@@ -476,7 +494,7 @@ class Store:
                     dist_chunks.append(all_d[pre[li]:pre[li + 1]])
                 stats.scanned_vectors += len(ids)
                 if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
-                    order = profile_reorder(cl.profiles[agent], list(range(cl.size)))
+                    order = profile_order(cl.profiles[agent], cl.size)
                     scan_chunks.append(cl.member_ids[order])
                 else:
                     scan_chunks.append(cl.member_ids.copy())

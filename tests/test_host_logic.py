@@ -86,6 +86,19 @@ def test_profiles():
     assert profile_promote([1, 2, 3], [3, 5, 3], 3) == [3, 5, 1]
 
 
+def test_profile_order_equals_reorder():
+    """The vectorised scan order equals profile_reorder over range(size)."""
+    from paper_2602_21477_b200.engine import profile_order, profile_reorder
+
+    rng = np.random.default_rng(4)
+    cases = [([], 5), ([3, 1, 3, 0], 4), ([9, 2, -1, 2], 3), ([0], 0), ([7, 7], 8)]
+    cases += [(rng.integers(-3, 40, int(rng.integers(0, 30))).tolist(), int(rng.integers(0, 40)))
+              for _ in range(200)]
+    for entries, size in cases:
+        want = profile_reorder(entries, list(range(size)))
+        assert profile_order(entries, size).tolist() == want
+
+
 def test_rwlock_and_runner():
     lock = RWLock()
     hits = []

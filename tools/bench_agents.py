@@ -102,6 +102,12 @@ def main():
         levels = {"L0": 0, "L1": 0, "L2": 0}
         early = 0
         t_s = t_i = 0.0
+        prof = None
+        if os.environ.get("PK_PROFILE_OPS") and alpha == 0.7:  # cProfile of the op loop only
+            import cProfile
+
+            prof = cProfile.Profile()
+            prof.enable()
         for r in range(a.rounds):
             for s in range(1, a.agents + 1):
                 ag = f"agent{s - 1}"
@@ -121,6 +127,13 @@ def main():
                     early += int(res.stats.early_terminated)
                 if r % 2 == 1:
                     store.end_request(ag)
+        if prof is not None:
+            import pstats
+
+            prof.disable()
+            st = pstats.Stats(prof, stream=sys.stderr)
+            st.sort_stats("tottime").print_stats(30)
+            st.sort_stats("cumulative").print_stats(40)
         out["modes"][f"alpha_et={alpha}"] = {
             "ms_per_op": 1000.0 * (t_s + t_i) / (n_s + n_i),
             "search_ms": 1000.0 * t_s / n_s, "insert8_ms": 1000.0 * t_i / n_i,
