@@ -1499,7 +1499,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   const int64_t smax = nprobe * max_nch;  // output slots per query
   // per-list query buckets (B entries each) + lcount [ns] | n_items | work counter
   RET(S.qpairs.ensure((size_t)ns * B * sizeof(QPair)));
-  RET(S.counts.ensure((size_t)(ns + 2) * 4));
+  RET(S.counts.ensure((size_t)(ns + 4) * 4));
   RET(S.slot_off.ensure((size_t)2 * B * 4));
   RET(S.scanned.ensure((size_t)B * 8));
   RET(S.cand_key.ensure((size_t)max_items * kk * 4));
@@ -1510,7 +1510,8 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   const int pc = ix->prof_calls;
 #define PROF(stage) \
   if (ix->prof) RET(ix->prof_mark(pc, stage))
-  int32_t* lcount = S.counts.as<int32_t>();  // [ns] | n_items | work counter
+  // [ns] | front items | work counter | tail items | tail base (route_items)
+  int32_t* lcount = S.counts.as<int32_t>();
   int32_t* n_items = lcount + ns;
   int32_t* work_ctr = lcount + ns + 1;
   const bool use_tc = ix->coarse_tc && !probe_in;
@@ -1544,13 +1545,13 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     }
     launch_qprep(qin, ix->d, (int)ix->d, (int)B, (int)dp, S.q.as<float>(), S.qnorm2.as<float>(),
                  sp ? S.qhi.as<float>() : nullptr, sp ? S.qlo.as<float>() : nullptr,
-                 tc_scan ? S.qsw.as<float>() : nullptr, lcount, (int)(ns + 2),
+                 tc_scan ? S.qsw.as<float>() : nullptr, lcount, (int)(ns + 3),
                  ix->screen ? S.ccount.as<int32_t>() : nullptr, ix->screen ? (int)B : 0,
                  ix->screen ? S.uq.as<uint32_t>() : nullptr, ix->screen ? (int)B : 0, fs);
   } else {
     CK(cudaMemcpy2DAsync(S.q.p, dp * 4, Q, ix->d * 4, ix->d * 4, B,
                          in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
-    CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 2) * 4, fs));
+    CK(cudaMemsetAsync(lcount, 0, (size_t)(ns + 3) * 4, fs));
   }
   if (ix->metric == COSINE) launch_qnorm(S.q.as<float>(), dp, (int)B, (int)ix->d, S.qnorm.as<float>(), fs);
   PROF(1);
@@ -1605,7 +1606,8 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // 2. route (query -> lists) into (list -> queries) work items
   launch_route(S.probe.as<int32_t>(), (int)B, nprobe, lt2, ix->chunk_rows, (int)smax, (int)B,
                lcount, S.items.as<ScanItem>(), n_items, S.qpairs.as<QPair>(),
-               S.slot_off.as<int32_t>(), S.scanned.as<int64_t>(), ra.lcount != nullptr, fs);
+               S.slot_off.as<int32_t>(), S.scanned.as<int64_t>(), ra.lcount != nullptr,
+               (int)std::min<int64_t>(max_items, INT32_MAX), fs);
   if (pipelined) {
     CK(cudaEventRecord(ix->ev_front, fs));
     CK(cudaStreamWaitEvent(st, ix->ev_front, 0));

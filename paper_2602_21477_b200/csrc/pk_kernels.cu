@@ -646,12 +646,18 @@ __global__ void __launch_bounds__(RE_THREADS) route_emit_kernel(
               bucket, slot_off, scanned);
 }
 
+// Items of at most chunk_rows / 2 rows (a list's short last chunk) are queued
+// after all the others: counters[0] counts the front items, counters[2] the
+// tail items, written backwards from tail_base (counters[3]), so the
+// persistent scan drains the big items first and its last, ragged round is
+// made of short ones (measured CTA end spread 40 us with one queue).
 __global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
                                    const int32_t* __restrict__ lcount, ScanItem* __restrict__ items,
-                                   int32_t* __restrict__ n_items) {
+                                   int32_t* __restrict__ counters, int tail_base) {
   pdl_trigger();
   pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) counters[3] = tail_base;
   if (s >= lt.nslots) return;
   const int cnt = lcount[s];
   if (cnt <= 0) return;
@@ -659,8 +665,13 @@ __global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
   const int nch = nchunks_of(len, chunk_rows);
   const int ng = (cnt + QG - 1) / QG;
   if (nch == 0) return;
-  int w = atomicAdd(n_items, nch * ng);
+  const int last_rows = (int)(len - (int64_t)(nch - 1) * chunk_rows);
+  const bool short_tail = last_rows <= chunk_rows / 2;
+  const int nfront = (short_tail ? nch - 1 : nch) * ng;
+  int w = nfront ? atomicAdd(&counters[0], nfront) : 0;
+  int wt = short_tail ? atomicAdd(&counters[2], ng) : 0;
   for (int c = 0; c < nch; c++) {
+    const bool tail = short_tail && c == nch - 1;
     for (int g = 0; g < ng; g++) {
       ScanItem it;
       it.lslot = s;
@@ -670,14 +681,15 @@ __global__ void route_items_kernel(ListTable lt, int chunk_rows, int bcap,
       it.nq = min(QG, cnt - g * QG);
       it.chunk = c;
       it.pad0 = it.pad1 = 0;
-      items[w++] = it;
+      if (tail) items[tail_base - wt++] = it;
+      else items[w++] = it;
     }
   }
 }
 
 void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows, int smax,
                   int bcap, int32_t* lcount, ScanItem* items, int32_t* n_items, QPair* bucket,
-                  int32_t* slot_off, int64_t* scanned, bool emitted, cudaStream_t st) {
+                  int32_t* slot_off, int64_t* scanned, bool emitted, int max_items, cudaStream_t st) {
   // lcount [nslots] and *n_items zeroed by the caller; `emitted`: the coarse
   // pick already ran emit_routes for every query
   if (B <= 0) return;
@@ -686,7 +698,7 @@ void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chu
                                                 bucket, slot_off, scanned);
   if (lt.nslots > 0)
     launch_pdl(route_items_kernel, dim3((lt.nslots + 255) / 256), dim3(256), 0, st, lt, chunk_rows, bcap,
-               lcount, items, n_items);
+               lcount, items, n_items, max_items - 1);
 }
 
 // =====================================================================
@@ -931,10 +943,12 @@ __device__ void topk_merge_tile(const ScanShared& S, int a, int rows, const int6
 template <int NSTAGE>
 __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMaps& maps,
                                               const ListTable& lt, const float* __restrict__ Qd,
-                                              const ScanItem* __restrict__ items, int n_items,
+                                              const ScanItem* __restrict__ items, const int32_t* __restrict__ nctr,
                                               const QPair* __restrict__ qpairs,
                                               int32_t* __restrict__ work_ctr, int nchunk_d,
                                               bool keep_in_l2, int64_t qsw_stride) {
+  // front items [0, nctr[0]) then the tail items, stored backwards from nctr[3]
+  const int n_front = nctr[0], n_items = n_front + nctr[2], tail_base = nctr[3];
   const int lane = threadIdx.x & 31;
   if (lane == 0)
     for (int i = 0; i < NBOX; i++) tma_prefetch_desc(&maps.box[i]);
@@ -947,7 +961,7 @@ __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMa
     it = __shfl_sync(FULL, it, 0);
     ScanItem item;
     if (it < n_items) {
-      item = items[it];
+      item = items[it < n_front ? it : tail_base - (it - n_front)];
     } else {
       item.nq = -1;
     }
@@ -1044,10 +1058,10 @@ __global__ void __launch_bounds__(SCAN_THREADS, 1)
   }
   __syncthreads();
   const int nchunk_d = lt.dp / DC;
-  const int n_items = *n_items_p;
+
 
   if (warp == NCW) {
-    scan_producer<STAGES>(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false, 0);
+    scan_producer<STAGES>(S, maps, lt, Qd, items, n_items_p, qpairs, work_ctr, nchunk_d, false, 0);
     return;
   }
 
@@ -1508,9 +1522,9 @@ __global__ void __launch_bounds__(SCREEN_THREADS, 1)
   }
   __syncthreads();
   const int nchunk_d = lt.dp / DC;
-  const int n_items = *n_items_p;
+
   if (warp == NCW_S) {
-    scan_producer<STAGES>(S, maps, lt, Qd, items, n_items, qpairs, work_ctr, nchunk_d, false, 0);
+    scan_producer<STAGES>(S, maps, lt, Qd, items, n_items_p, qpairs, work_ctr, nchunk_d, false, 0);
     return;
   }
 
@@ -1601,7 +1615,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    const QPair* __restrict__ qpairs, int kk, float coef,
                    int32_t* __restrict__ work_ctr, uint32_t* __restrict__ Uq,
                    uint32_t* __restrict__ slot_hi, int32_t* __restrict__ slot_n,
-                   int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap, int dbg_skip) {
+                   int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap, int dbg_skip,
+                   unsigned long long* __restrict__ dbg_t) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ScanShared S;
@@ -1654,13 +1669,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   pdl_trigger();
   pdl_wait();  // items, queries and counters come from the kernels before
+  if (dbg_t && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    dbg_t[2 * blockIdx.x] = globaltimer_ns();
+    dbg_t[2 * gridDim.x + blockIdx.x] = smid;
+  }
   const uint32_t tmem = *tmem_slot;
   const int nchunk_d = lt.dp / DC;
-  const int n_items = *n_items_p;
+
 
   if (warp == TC_EPI_WARPS) {
     // ---------------------------------------------------------- producer
-    scan_producer<TC_STAGES>(S, maps, lt, Qsw, items, n_items, qpairs, work_ctr, nchunk_d, false,
+    scan_producer<TC_STAGES>(S, maps, lt, Qsw, items, n_items_p, qpairs, work_ctr, nchunk_d, false,
                              qsw_stride);
   } else if (warp == TC_EPI_WARPS + 1) {
     // ---------------------------------------------------------- MMA issuer
@@ -1769,6 +1790,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (dbg_t && threadIdx.x == 0) dbg_t[2 * blockIdx.x + 1] = globaltimer_ns();
   if (warp == TC_EPI_WARPS + 1) tmem_dealloc(tmem, TC_TMEM_COLS);
 }
 
@@ -1828,6 +1850,10 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   // PK_DEBUG_SCAN_NOSELECT=1: skip the per-(query, item) selection (timing
   // experiments only -- results are wrong)
   static const int dbg_skip = getenv("PK_DEBUG_SCAN_NOSELECT") ? atoi(getenv("PK_DEBUG_SCAN_NOSELECT")) : 0;
+  // PK_DEBUG_SCAN_TIMES=1: per-CTA start / end timestamps, spread printed to stderr
+  static const bool dbg_times = getenv("PK_DEBUG_SCAN_TIMES") != nullptr;
+  unsigned long long* dbg_t = nullptr;
+  if (dbg_times) cudaMallocAsync((void**)&dbg_t, (size_t)grid * 24, st);
 #define PK_TC(M)                                                                                 \
   {                                                                                              \
     auto k = scan_tc_kernel<M>;                                                                  \
@@ -1835,11 +1861,35 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
     launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, lt, (const float*)qsw,   \
                (int64_t)B, \
                qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
-               ccount, cap, dbg_skip);                                                             \
+               ccount, cap, dbg_skip, dbg_t);                                                      \
   }
   if (metric == SQ_L2) PK_TC(SQ_L2)
   else PK_TC(IP)
 #undef PK_TC
+  if (dbg_t) {
+    std::vector<unsigned long long> h((size_t)grid * 3);
+    cudaMemcpyAsync(h.data(), dbg_t, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    unsigned long long s0 = ~0ull, s1 = 0;
+    std::vector<double> ends;
+    for (int c = 0; c < grid; c++) {
+      s0 = std::min(s0, h[2 * c]);
+      s1 = std::max(s1, h[2 * c]);
+    }
+    for (int c = 0; c < grid; c++) ends.push_back((h[2 * c + 1] - s0) / 1e3);
+    std::sort(ends.begin(), ends.end());
+    fprintf(stderr, "scan CTA times (us from first start): start spread %.1f | end min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f\n",
+            (s1 - s0) / 1e3, ends[0], ends[grid / 10], ends[grid / 2], ends[grid * 9 / 10], ends[grid - 1]);
+    if (getenv("PK_DEBUG_SCAN_SM")) {  // end time per SM id
+      std::vector<std::pair<unsigned long long, double>> sm;
+      for (int c = 0; c < grid; c++) sm.push_back({h[2 * grid + c], (h[2 * c + 1] - s0) / 1e3});
+      std::sort(sm.begin(), sm.end());
+      fprintf(stderr, "scan end by smid:");
+      for (auto& x : sm) fprintf(stderr, " %llu:%.0f", x.first, x.second);
+      fprintf(stderr, "\n");
+    }
+    cudaFreeAsync(dbg_t, st);
+  }
 }
 
 // Bound coefficient: |A - E| <= coef * (nx + nq) for d terms.

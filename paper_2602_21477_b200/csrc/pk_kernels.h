@@ -75,7 +75,7 @@ void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
 // bcap (query, slot base) pairs.  lcount [nslots] and *n_items must be zero.
 void launch_route(const int32_t* probe, int B, int nprobe, ListTable lt, int chunk_rows, int smax,
                   int bcap, int32_t* lcount, ScanItem* items, int32_t* n_items, QPair* bucket,
-                  int32_t* slot_off, int64_t* scanned, bool emitted, cudaStream_t st);
+                  int32_t* slot_off, int64_t* scanned, bool emitted, int max_items, cudaStream_t st);
 // Routing outputs for a kernel that emits its queries' routes itself (lcount
 // NULL = no routing).
 struct RouteArgs {

@@ -109,6 +109,12 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   return p;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------- cp.async
 // 16-byte asynchronous global -> shared copies (LDGSTS): many small requests
 // in flight per thread without the per-operation cost of a TMA bulk copy.
