@@ -1670,7 +1670,10 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                         ix->pool_cap, S.cand_key.as<uint32_t>(), S.cand_n.as<int32_t>(),
                         S.slot_off.as<int32_t>(), lt2, S.q.as<float>(), S.probe.as<int32_t>(),
                         nprobe, kk, o_ids, o_d, o_cid, o_n, S.nsurv.as<int32_t>(),
-                        S.scanned.as<int64_t>(), sc_dst, st);
+                        S.scanned.as<int64_t>(), sc_dst, st,
+                        // overlapped: launched after the scan, so its CTAs do not sit
+                        // waiting on the SMs the scan tail frees for the next front half
+                        /*pdl=*/!pipelined);
   else
     launch_merge((int)B, S.slot_off.as<int32_t>(), S.cand_key.as<uint32_t>(),
                  S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(), kk,

@@ -2162,7 +2162,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                          int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
-                         cudaStream_t st) {
+                         cudaStream_t st, bool pdl) {
   if (B <= 0) return;
   // column-block stage of ~56 KB (two CTAs per SM)
   const int stage_floats = 56 * 1024 / 4;
@@ -2171,7 +2171,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
   {                                                                                             \
     auto k = rerank_merge_kernel<M>;                                                            \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
-    launch_pdl(k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
+    launch_maybe_pdl(pdl, k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
                                    nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv,  \
                                    scanned_src, scanned_dst);                                    \
   }

@@ -122,7 +122,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                          int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
-                         cudaStream_t st);
+                         cudaStream_t st, bool pdl = true);
 float screen_coef(int metric, int dp);
 float screen_coef_tf32(int metric, int dp);
 size_t tc_smem_bytes();

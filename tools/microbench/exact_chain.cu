@@ -4,6 +4,29 @@
 // already in shared memory (compute only).
 #include "../../paper_2602_21477_b200/csrc/pk_kernels.cu"
 using namespace pk;
+// w floats (multiple of 16) of one chain, loads for the next 16 issued
+// before the current 16 are summed (register double buffer)
+template <int METRIC>
+__device__ __forceinline__ float chain_pipelined(float acc, const float* x, const float* q, int w) {
+  const float4* x4 = reinterpret_cast<const float4*>(x);
+  const float4* q4 = reinterpret_cast<const float4*>(q);
+  const int nv = w / 4;
+  float4 xa[4], qa[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) { xa[i] = x4[i]; qa[i] = q4[i]; }
+  for (int c = 0; c < nv; c += 4) {
+    float4 xb[4], qb[4];
+    if (c + 4 < nv) {
+#pragma unroll
+      for (int i = 0; i < 4; i++) { xb[i] = x4[c + 4 + i]; qb[i] = q4[c + 4 + i]; }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) acc = step4<METRIC>(acc, xa[i], qa[i]);
+#pragma unroll
+    for (int i = 0; i < 4; i++) { xa[i] = xb[i]; qa[i] = qb[i]; }
+  }
+  return acc;
+}
 __global__ void kexact(const float* cent, const int* pick, int n, int dp, int stage_floats, int mode,
                        long long* cyc, float* out) {
   extern __shared__ __align__(16) float sm[];
@@ -23,7 +46,7 @@ __global__ void kexact(const float* cent, const int* pick, int n, int dp, int st
     const int w4 = W / 4;
     for (int i = tid; i < nr * w4; i += blockDim.x) {
       const int r = i / w4, c = i - r * w4;
-      if (mode == 0) cp_async16(dst + r * rs + 4 * c, cent + (int64_t)pick[r] * dp + blk * W + 4 * c);
+      if (mode == 0 || mode == 2) cp_async16(dst + r * rs + 4 * c, cent + (int64_t)pick[r] * dp + blk * W + 4 * c);
     }
     cp_async_commit();
   };
@@ -35,6 +58,8 @@ __global__ void kexact(const float* cent, const int* pick, int n, int dp, int st
     if (tid < nr) {
       const float* x = rows_st + (blk & 1) * nr * rs + tid * rs;
       const float* q = qs + blk * W;
+      if (mode >= 2) acc = chain_pipelined<SQ_L2>(acc, x, q, W);
+      else
       for (int j = 0; j + 4 <= W; j += 4)
         acc = step4<SQ_L2>(acc, *reinterpret_cast<const float4*>(x + j), *reinterpret_cast<const float4*>(q + j));
     }
@@ -54,7 +79,7 @@ int main() {
   const int stage = 21000;
   const size_t smem = (size_t)(dp + stage) * 4;
   cudaFuncSetAttribute(kexact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int mode = 0; mode < 2; mode++)
+  for (int mode = 0; mode < 4; mode++)
     for (int n : {16, 32, 50, 64}) {
       for (int grid : {1, 256}) {
         kexact<<<grid, 256, smem>>>(cent, pick, n, dp, stage, mode, cyc, out);
@@ -62,7 +87,7 @@ int main() {
         cudaDeviceSynchronize();
         long long h[256]; cudaMemcpy(h, cyc, 8 * grid, cudaMemcpyDeviceToHost);
         double s = 0; for (int i = 0; i < grid; i++) s += h[i];
-        printf("{\"mode\": \"%s\", \"n\": %d, \"grid\": %d, \"cycles\": %.0f}\n", mode ? "compute-only" : "cp.async",
+        printf("{\"mode\": \"%s\", \"n\": %d, \"grid\": %d, \"cycles\": %.0f}\n", mode == 0 ? "cp.async" : mode == 1 ? "compute-only" : mode == 2 ? "cp.async+pipelined" : "compute-only+pipelined",
                n, grid, s / grid);
       }
     }
