@@ -65,6 +65,22 @@ def parse():
     return p.parse_args()
 
 
+def workload_name(a, world: int = 1) -> str:
+    """The BASELINE config these arguments describe (configs[1] by default)."""
+    shape = (a.n, a.d, a.nlist, a.nprobe, a.k, a.batch)
+    named = {(100_000, 384, 256, 16, 10, 32): "configs[0]",
+             (1_000_000, 768, 1024, 32, 10, 256): "configs[1]",
+             (10_000_000, 768, 8192, 32, 10, 256): "configs[3] shape on one GPU"}
+    tag = named.get(shape, "custom")
+    n = f"{a.n / 1e6:g}M" if a.n >= 1_000_000 else f"{a.n // 1000}K"
+    s = (f"{tag}: {n} x {a.d} fp32 IVF per GPU (nlist {a.nlist} per GPU), nprobe {a.nprobe}, "
+         f"k {a.k}, {a.batch} queries per GPU per step")
+    if world > 1:
+        s += (f"; {world} x {n} x {a.d} global index, nlist {world * a.nlist}, lists sharded by "
+              "rank (configs[3] shape)")
+    return s
+
+
 # ---------------------------------------------------------------- workload
 def make_base(n, d, seed):
     """Unit-sphere fp32 rows (bench/workload.py:108-111 semantics), PCG64."""
@@ -235,7 +251,7 @@ def run_reference(a):
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * t_total / a.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": "configs[1]: 1M x 768 fp32 IVF, nlist 1024, nprobe 32, k 10, batch 256",
+        "config": {"workload": workload_name(a),
                    "n": a.n, "d": a.d, "nlist": a.nlist, "nprobe": a.nprobe, "k": a.k,
                    "batch": a.batch, "sample_queries_per_step": sample},
         "cpu_baseline": {"value": qps, "unit": UNIT, "cores": threads, "kind": "port",
@@ -542,15 +558,11 @@ def run_ours(a):
             "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "configs[1]: 1M x 768 fp32 IVF per GPU (nlist 1024 per GPU), "
-                                   "nprobe 32, k 10, 256 queries per GPU per step"
-                                   + ("" if world == 1 else
-                                      f"; {world}M x 768 global index, nlist {world * a.nlist}, "
-                                      "lists sharded by rank (configs[3] shape)"),
+            "config": {"workload": workload_name(a, world),
                        "n_per_gpu": a.n, "d": a.d, "nlist_per_gpu": a.nlist, "nprobe": a.nprobe,
                        "k": a.k, "batch_per_gpu": a.batch,
-                       "l2": "inputs larger than L2 (index 3.1 GB per GPU; each batch reads "
-                             "~all lists)",
+                       "l2": (f"inputs larger than L2 (index {a.n * (4 * a.d + 8) / 1e9:.2f} GB per "
+                              "GPU vs 126 MB L2; each batch reads most lists)"),
                        "parallelism": f"list-sharded x{world}" + (
                            ", dispatch (NCCL all-gather of queries + list handles) / combine ("
                            + ("per-shard top-k written into the origin rank's HBM over NVLink P2P, "
