@@ -243,7 +243,11 @@ struct pk_index {
   // on the migration stream and switch it resident once the copy is done
   // (searches stay exact in every phase, ref/tiering.py:332-416).
   bool tiered = false;
-  bool stage_dma = false;    // PK_STAGE=dma: copy engines (measured 15 GB/s vs 31 GB/s zero-copy gather)
+  // PK_STAGE=dma: copy engines for the rows.  In the configs[4] stream the
+  // zero-copy gather kernel stays ahead (24.7 vs 19.9 GB/s effective, i.e.
+  // staged bytes over search time) although a bare 3 MB pinned copy runs at
+  // 52 GB/s on this link (tools/pcie_bw.py)
+  bool stage_dma = false;
   float* hrows = nullptr;    // [hcap][dp] pinned
   int64_t* hids = nullptr;   // [hcap] pinned
   float* hrows_d = nullptr;  // device aliases (mapped)
@@ -607,25 +611,23 @@ struct pk_index {
     CK(cudaMemcpyAsync(stage_desc.p, desc.data(), desc.size() * sizeof(StageCopy),
                        cudaMemcpyHostToDevice, st));
     if (stage_dma) {
-      // copy engines: one batched DMA submission for every staged list's rows
-      // and ids, then the norms kernel
-      std::vector<void*> dsts, srcs;
-      std::vector<size_t> sizes;
-      for (const StageCopy& c : desc) {
-        dsts.push_back(rows + c.dst_row * dp);
-        srcs.push_back(hrows + c.src_row * dp);
-        sizes.push_back((size_t)c.n * dp * 4);
-        dsts.push_back(ids + c.dst_row);
-        srcs.push_back(hids + c.src_row);
-        sizes.push_back((size_t)c.n * 8);
+      // copy engines for the rows: one DMA per run of lists contiguous on both
+      // sides (multi-MB transfers run at ~52-55 GB/s on Gen5 x16; the ids are
+      // too small for a DMA each and come with the norms kernel, zero-copy)
+      size_t i = 0;
+      while (i < desc.size()) {
+        size_t j = i + 1;
+        int64_t n = desc[i].n;
+        while (j < desc.size() && desc[j].src_row == desc[i].src_row + n &&
+               desc[j].dst_row == desc[i].dst_row + n) {
+          n += desc[j].n;
+          j++;
+        }
+        CK(cudaMemcpyAsync(rows + desc[i].dst_row * dp, hrows + desc[i].src_row * dp, (size_t)n * dp * 4,
+                           cudaMemcpyHostToDevice, st));
+        i = j;
       }
-      cudaMemcpyAttributes attr;
-      memset(&attr, 0, sizeof(attr));
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      size_t aidx = 0, fail_idx = 0;
-      CK(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &aidx, 1,
-                              &fail_idx, st));
-      launch_stage_norms(stage_desc.as<StageCopy>(), (int)desc.size(), rows, nrm, (int)dp, st);
+      launch_stage_norms(stage_desc.as<StageCopy>(), (int)desc.size(), rows, nrm, (int)dp, hids_d, ids, st);
     } else {
       launch_gather_rows(stage_desc.as<StageCopy>(), (int)desc.size(), hrows_d, hids_d, rows, ids, nrm,
                          (int)dp, st);

@@ -3020,9 +3020,13 @@ void launch_gather_rows(const StageCopy* desc, int ndesc, const float* hrows, co
 // Squared norms of the staged rows after a DMA (copy-engine) staging pass.
 __global__ void __launch_bounds__(256) stage_norms_kernel(const StageCopy* __restrict__ desc,
                                                           const float* __restrict__ rows,
-                                                          float* __restrict__ nrm, int dp) {
+                                                          float* __restrict__ nrm, int dp,
+                                                          const int64_t* __restrict__ hids,
+                                                          int64_t* __restrict__ ids) {
   const StageCopy c = desc[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (hids)  // the ids, read in place from the mapped host arena
+    for (int r = threadIdx.x; r < c.n; r += blockDim.x) ids[c.dst_row + r] = hids[c.src_row + r];
   for (int r = warp; r < c.n; r += 8) {
     const float4* x = reinterpret_cast<const float4*>(rows + (c.dst_row + r) * (int64_t)dp);
     float acc = 0.f;
@@ -3039,9 +3043,9 @@ __global__ void __launch_bounds__(256) stage_norms_kernel(const StageCopy* __res
   }
 }
 void launch_stage_norms(const StageCopy* desc, int ndesc, const float* rows, float* nrm, int dp,
-                        cudaStream_t st) {
+                        const int64_t* hids, int64_t* ids, cudaStream_t st) {
   if (ndesc <= 0) return;
-  stage_norms_kernel<<<ndesc, 256, 0, st>>>(desc, rows, nrm, dp);
+  stage_norms_kernel<<<ndesc, 256, 0, st>>>(desc, rows, nrm, dp, hids, ids);
 }
 
 }  // namespace pk

@@ -187,7 +187,7 @@ struct StageCopy {
 void launch_gather_rows(const StageCopy* desc, int ndesc, const float* hrows, const int64_t* hids,
                         float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st);
 void launch_stage_norms(const StageCopy* desc, int ndesc, const float* rows, float* nrm, int dp,
-                        cudaStream_t st);
+                        const int64_t* hids, int64_t* ids, cudaStream_t st);
 
 // Batched append: padded staging rows [n][dp] + ids -> arena rows dst_row[i], with norms.
 void launch_append_rows(const float* src, const int64_t* src_ids, const int64_t* dst_row, int n,

@@ -27,8 +27,14 @@ def _check(ix, lists, cents, cids, Q, nprobe, kk):
     assert np.array_equal(out.scanned, sc)
 
 
-def test_tiered_index_every_residency_state():
+@pytest.mark.parametrize("stage", ["gather", "dma"])
+def test_tiered_index_every_residency_state(stage, monkeypatch):
+    """Both staging paths: the zero-copy gather kernel (default) and the copy
+    engines (PK_STAGE=dma: one DMA per contiguous run of lists, ids and norms
+    by a kernel)."""
     from paper_2602_21477_b200 import DeviceIndex
+
+    monkeypatch.setenv("PK_STAGE", stage)
 
     rng = np.random.default_rng(21)
     d, nlist = 96, 30
