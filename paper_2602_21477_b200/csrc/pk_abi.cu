@@ -214,12 +214,13 @@ struct pk_index {
     DevBuf qin, blk;
     uint8_t* hblk = nullptr;  // pinned result block
     size_t hbytes = 0;
-    cudaEvent_t copied = nullptr, done = nullptr, consumed = nullptr;
+    cudaEvent_t copied = nullptr, done = nullptr, consumed = nullptr, ready = nullptr;
     int64_t B = 0;
     int32_t kk = 0;
     bool busy = false;
   } aslot[2];
-  cudaStream_t cst = nullptr;  // copy stream
+  cudaStream_t cst = nullptr;  // copy stream (query uploads)
+  cudaStream_t rst = nullptr;  // result read-back stream (off the index stream's critical path)
 
   // ---- peer combine (pk_combine_*): this rank's receive area (R shard blocks
   // + R flags, IPC-exported) and the peers' areas mapped into this process
@@ -882,7 +883,8 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
 int pk_index_destroy(pk_index* ix) {
   if (!ix) return PK_OK;
   cudaSetDevice(ix->device);
-  if (ix->st) cudaStreamSynchronize(ix->st);
+  for (cudaStream_t x : {ix->fst, ix->rst, ix->cst, ix->st})
+    if (x) cudaStreamSynchronize(x);
   cudaFree(ix->rows);
   cudaFree(ix->ids);
   cudaFree(ix->nrm);
@@ -908,10 +910,15 @@ int pk_index_destroy(pk_index* ix) {
     if (a.copied) cudaEventDestroy(a.copied);
     if (a.done) cudaEventDestroy(a.done);
     if (a.consumed) cudaEventDestroy(a.consumed);
+    if (a.ready) cudaEventDestroy(a.ready);
     a.qin.release();
     a.blk.release();
   }
   if (ix->cst) cudaStreamDestroy(ix->cst);
+  if (ix->rst) {
+    cudaStreamSynchronize(ix->rst);
+    cudaStreamDestroy(ix->rst);
+  }
   if (ix->fst) {
     cudaStreamSynchronize(ix->fst);
     cudaStreamDestroy(ix->fst);
@@ -1743,10 +1750,12 @@ int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
   if (B <= 0) return fail(PK_ERR_USAGE, "empty batch");
   CK(cudaSetDevice(ix->device));
   if (!ix->cst) CK(cudaStreamCreateWithFlags(&ix->cst, cudaStreamNonBlocking));
+  if (!ix->rst) CK(cudaStreamCreateWithFlags(&ix->rst, cudaStreamNonBlocking));
   if (!a.copied) {
     CK(cudaEventCreateWithFlags(&a.copied, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&a.consumed, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&a.ready, cudaEventDisableTiming));
     CK(cudaEventRecord(a.consumed, ix->st));
   }
   const int64_t ob = pk_shard_block_bytes(B, kk);
@@ -1773,8 +1782,12 @@ int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
                   nullptr, reinterpret_cast<int64_t*>(base + 16 * nkk), true, true, nullptr, nullptr,
                   /*host_scopes=*/true));
   CK(cudaEventRecord(a.consumed, ix->st));
-  CK(cudaMemcpyAsync(a.hblk, base, (size_t)ob, cudaMemcpyDeviceToHost, ix->st));
-  CK(cudaEventRecord(a.done, ix->st));
+  // read-back on its own stream: the next batch's scan on the index stream
+  // does not queue behind this copy
+  CK(cudaEventRecord(a.ready, ix->st));
+  CK(cudaStreamWaitEvent(ix->rst, a.ready, 0));
+  CK(cudaMemcpyAsync(a.hblk, base, (size_t)ob, cudaMemcpyDeviceToHost, ix->rst));
+  CK(cudaEventRecord(a.done, ix->rst));
   a.B = B;
   a.kk = kk;
   a.busy = true;
