@@ -203,6 +203,7 @@ struct pk_index {
   bool coarse_tc = true;  // coarse quantizer on tcgen05 + exact re-rank; PK_COARSE=exact disables
   bool coarse_split = true;  // 3xTF32 hi/lo split (tight bound); PK_COARSE=tf32 for one product
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
+  bool pool_cap_set = false;  // PK_POOL_CAP given: no growth with kk
   DevBuf shard_in, shard_out, pb, pb_out, sl_buf;
   uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
   size_t hout_bytes = 0;
@@ -854,7 +855,10 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   if (const char* e = getenv("PK_SCAN_SMS")) ix->scan_sms = std::max(1, std::min(ix->num_sms, atoi(e)));
   if (const char* e = getenv("PK_CHUNK_ROWS")) ix->chunk_rows = std::max(TILE, atoi(e) / TILE * TILE);
   if (const char* e = getenv("PK_SCAN_EXACT")) ix->screen = atoi(e) == 0;
-  if (const char* e = getenv("PK_POOL_CAP")) ix->pool_cap = std::max(1, atoi(e));
+  if (const char* e = getenv("PK_POOL_CAP")) {
+    ix->pool_cap = std::max(1, atoi(e));
+    ix->pool_cap_set = true;
+  }
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
   if (const char* e = getenv("PK_PIPELINE")) ix->pipeline = atoi(e) != 0;
   if (const char* e = getenv("PK_STAGE")) ix->stage_dma = strcmp(e, "dma") == 0;
@@ -1528,6 +1532,15 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // counter resets) on the screened paths; plain copies otherwise
   const bool prep = ix->screen || use_tc;
   const bool tc_scan = ix->screen && ix->tensor && !probe_out;
+  // candidates per query grow with kk (the screen keeps every row whose lower
+  // bound is under the kk-th upper bound): 4096 covers kk 10 with room, kk 64
+  // needed ~5x that on unit-sphere data, and an overflow takes the exact path
+  // (bounded to 1 GB of pool per scratch set)
+  const int pool_cap =
+      ix->pool_cap_set ? ix->pool_cap
+                       : std::max<int>(ix->pool_cap,
+                                       (int)std::min<int64_t>({(int64_t)kk * 512, 1 << 16,
+                                                               ((int64_t)1 << 30) / (std::max<int64_t>(B, 1) * 16)}));
   RouteArgs ra;  // set when the coarse pick emits the routes itself
   PROF(0);
   if (!probe_in)
@@ -1631,21 +1644,21 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // 3. fused scan + per-(query, list chunk) top-kk
   PROF(4);
   if (ix->screen) {
-    RET(S.cpool.ensure((size_t)B * ix->pool_cap * sizeof(int4)));  // uq / ccount reset by prep
+    RET(S.cpool.ensure((size_t)B * pool_cap * sizeof(int4)));  // uq / ccount reset by prep
     if (ix->tensor) {
       launch_scan_tc(ix->metric, lt2, ix->maps, S.q.as<float>(), (int)B, S.qsw.as<float>(), true,
                      S.qnorm2.as<float>(), S.items.as<ScanItem>(), n_items,
                      (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
                      work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
                      S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
-                     ix->pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined);
+                     pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined);
     } else {
       launch_scan_screen(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm2.as<float>(),
                          S.items.as<ScanItem>(), n_items,
                          (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
                          work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
                          S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
-                         ix->pool_cap, ix->num_sms, st);
+                         pool_cap, ix->num_sms, st);
     }
   } else
     launch_scan(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm.as<float>(),
@@ -1676,7 +1689,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   int64_t* sc_dst = !dev ? reinterpret_cast<int64_t*>(S.out_ids.as<uint8_t>() + 16 * B * kk) : out_scanned;
   if (ix->screen)
     launch_rerank_merge(ix->metric, (int)B, S.cpool.as<int4>(), S.ccount.as<int32_t>(),
-                        ix->pool_cap, S.cand_key.as<uint32_t>(), S.cand_n.as<int32_t>(),
+                        pool_cap, S.cand_key.as<uint32_t>(), S.cand_n.as<int32_t>(),
                         S.slot_off.as<int32_t>(), lt2, S.q.as<float>(), S.probe.as<int32_t>(),
                         nprobe, kk, o_ids, o_d, o_cid, o_n, S.nsurv.as<int32_t>(),
                         S.scanned.as<int64_t>(), sc_dst, st,
