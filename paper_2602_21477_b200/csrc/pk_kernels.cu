@@ -2004,18 +2004,42 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     int total_hi = 0;
     for (int w = 0; w < RR_THREADS / 32; w++) total_hi += s_u[w];
     __syncthreads();
-    if (fits && total_hi >= kk) {
-      // radix select of the kk-th smallest published hi (8 bits per pass)
+    if (!fits) {  // more published bounds than registers hold (large kk): count them in place
+      int c = 0;
+      for (int f = threadIdx.x; f < nflat; f += RR_THREADS) {
+        const int sl = so + f / kk, e = f - (f / kk) * kk;
+        c += e < slot_n[sl];
+      }
+      c = __reduce_add_sync(FULL, c);
+      if (lane == 0) s_u[warp] = c;
+      __syncthreads();
+      total_hi = 0;
+      for (int w = 0; w < RR_THREADS / 32; w++) total_hi += s_u[w];
+      __syncthreads();
+    }
+    if (total_hi >= kk) {
+      // radix select of the kk-th smallest published hi (8 bits per pass;
+      // from registers, or re-read from L2 each pass when they do not fit)
       uint32_t prefix = 0;
       int rem = kk;
       for (int shift = 24; shift >= 0; shift -= 8) {
         s_hist[threadIdx.x] = 0;
         __syncthreads();
         const uint32_t hmask = shift == 24 ? 0u : (0xffffffffu << (shift + 8));
+        if (fits) {
 #pragma unroll
-        for (int i = 0; i < RR_HI_PER; i++)
-          if (hv[i] != KEY_NONE && (hv[i] & hmask) == (prefix & hmask))
-            atomicAdd(&s_hist[(hv[i] >> shift) & 0xff], 1u);
+          for (int i = 0; i < RR_HI_PER; i++)
+            if (hv[i] != KEY_NONE && (hv[i] & hmask) == (prefix & hmask))
+              atomicAdd(&s_hist[(hv[i] >> shift) & 0xff], 1u);
+        } else {
+          for (int f = threadIdx.x; f < nflat; f += RR_THREADS) {
+            const int sl = so + f / kk, e = f - (f / kk) * kk;
+            if (e < slot_n[sl]) {
+              const uint32_t h = slot_hi[(int64_t)sl * kk + e];
+              if (h != KEY_NONE && (h & hmask) == (prefix & hmask)) atomicAdd(&s_hist[(h >> shift) & 0xff], 1u);
+            }
+          }
+        }
         __syncthreads();
         pick_bin(s_hist[threadIdx.x], rem, &s_bin, &s_below, s_wu);
         prefix |= (uint32_t)s_bin << shift;

@@ -158,7 +158,8 @@ def test_device_search_matches_oracle(pk, d, metric, scan_mode):
     ix, lists, cents, cids = _random_index(pk, rng, d, nlist, sizes, metric, dup=True)
     mname = ["sq_l2", "ip", "cosine"][metric]
     flat = O.FlatIVF.from_lists(lists, cents, cids, metric=mname)
-    for B, nprobe, kk in [(1, 1, 1), (7, 5, 10), (64, 8, 20), (200, 13, 64), (33, 40, 16)]:
+    # (50, 40, 64): > 2048 published bounds per query, the re-rank's in-place bound select
+    for B, nprobe, kk in [(1, 1, 1), (7, 5, 10), (64, 8, 20), (200, 13, 64), (33, 40, 16), (50, 40, 64)]:
         Q = rng.normal(size=(B, d)).astype(np.float32)
         Q[0] = lists[5][1][7]  # exact hit
         out = ix.search(Q, [0], nprobe, kk, want_probe=True)
