@@ -553,7 +553,7 @@ def run_ours(a):
                   "probe_mismatch": int((g.probe != r_p).sum())}
 
     if rank == 0:
-        per_step = 8 if sh is None else 11  # our kernels per search step
+        per_step = 6 if sh is None else 10  # our kernels per search step
         line = {
             "metric": METRIC, "value": qps, "unit": UNIT, "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
