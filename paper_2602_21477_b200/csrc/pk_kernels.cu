@@ -390,72 +390,6 @@ __device__ __forceinline__ void pick_bin(unsigned cnt, int rem, int* s_bin, int*
   __syncthreads();
 }
 
-// Small sorts (n <= 64) without block barriers: warp 0 holds two entries
-// per lane and runs the bitonic network with shuffles; the compaction keeps
-// the first `kk` entries (dropping adjacent duplicate (key, id) pairs when
-// dedup is set, the first-occurrence rule of ref/engine.py:414-418).
-__device__ __forceinline__ Entry shfl_entry(const Entry& e, int m) {
-  Entry o;
-  o.key = __shfl_xor_sync(FULL, e.key, m);
-  o.pay = __shfl_xor_sync(FULL, e.pay, m);
-  o.id = __shfl_xor_sync(FULL, e.id, m);
-  return o;
-}
-__device__ void warp_sort64(Entry* buf, int n) {
-  const int lane = threadIdx.x & 31;
-  Entry v[2];
-  v[0] = lane < n ? buf[lane] : e_none();
-  v[1] = lane + 32 < n ? buf[lane + 32] : e_none();
-  for (int k = 2; k <= 64; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j == 32) {  // partners are the lane's own two entries (k == 64: ascending)
-        if (e_less(v[1], v[0])) {
-          const Entry t = v[0];
-          v[0] = v[1];
-          v[1] = t;
-        }
-        continue;
-      }
-#pragma unroll
-      for (int r = 0; r < 2; r++) {
-        const int e = lane + 32 * r;
-        const Entry o = shfl_entry(v[r], j);
-        const bool asc = (e & k) == 0;
-        const bool low = (lane & j) == 0;
-        const bool take_o = (low == asc) ? e_less(o, v[r]) : e_less(v[r], o);
-        if (take_o) v[r] = o;
-      }
-    }
-  }
-  if (lane < n) buf[lane] = v[0];
-  if (lane + 32 < n) buf[lane + 32] = v[1];
-}
-__device__ int warp_compact64(Entry* buf, int n, int kk, bool dedup) {
-  const int lane = threadIdx.x & 31;
-  Entry v[2];
-  bool keep[2];
-#pragma unroll
-  for (int r = 0; r < 2; r++) {
-    const int i = lane + 32 * r;
-    keep[r] = i < n;
-    if (keep[r]) {
-      v[r] = buf[i];
-      if (dedup && i > 0) {
-        const Entry p = buf[i - 1];
-        keep[r] = !(p.id == v[r].id && p.key == v[r].key);
-      }
-    }
-  }
-  __syncwarp();
-  const unsigned b0 = __ballot_sync(FULL, keep[0]), b1 = __ballot_sync(FULL, keep[1]);
-  const unsigned below = (1u << lane) - 1u;
-  const int p0 = __popc(b0 & below), p1 = __popc(b0) + __popc(b1 & below);
-  if (keep[0] && p0 < kk) buf[p0] = v[0];
-  if (keep[1] && p1 < kk) buf[p1] = v[1];
-  return min(kk, __popc(b0) + __popc(b1));
-}
-// Sort buf[0..n) and keep the first kk (see cta_compact_sorted); small n runs
-// in warp 0 only.
 // Rank sort for n <= blockDim.x: thread i counts the entries ordered before
 // its own (ties by position: stable) and stores it at that rank -- n
 // independent shared-memory sweeps instead of log^2 dependent exchange

@@ -20,7 +20,6 @@ the probed lists in one call -- and the stop rules replayed on those values.
 
 from __future__ import annotations
 
-import math
 import os
 import threading
 from dataclasses import dataclass, field

@@ -4,7 +4,6 @@ import os
 import pstats
 import sys
 
-import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.argv = ["x"] + (sys.argv[1:] or ["--agents", "4", "--rows", "50000", "--rounds", "8"])
