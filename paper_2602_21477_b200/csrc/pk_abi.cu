@@ -180,6 +180,10 @@ struct pk_index {
     DevBuf q, qnorm, dc, probe, probe_key, counts, items, qpairs, slot_off, scanned, cand_key,
         cand_id, cand_n, cand_list, out_ids, scopes, qnorm2, uq, cpool, ccount, qsw, qhi, qlo, qin,
         ncand, nsurv;
+    // the coarse GEMM's query tensor maps for (pointers, rows) last encoded
+    CUtensorMap qmap[2];
+    const void* qmap_ptr[2] = {nullptr, nullptr};
+    int64_t qmap_rows = -1;
     void release() {
       for (DevBuf* b : {&q, &qnorm, &dc, &probe, &probe_key, &counts, &items, &qpairs, &slot_off,
                         &scanned, &cand_key, &cand_id, &cand_n, &cand_list, &out_ids, &scopes, &qnorm2,
@@ -305,6 +309,21 @@ struct pk_index {
   void mark(int32_t s) {
     dirty_lo = std::min(dirty_lo, s);
     dirty_hi = std::max(dirty_hi, s);
+    tver++;
+  }
+  // longest live list, recomputed only after a table change (every h_len /
+  // h_cid edit goes through mark(), which the device table sync relies on too)
+  uint64_t tver = 1, maxlen_ver = 0;
+  int64_t maxlen_cached = 0;
+  int64_t max_list_len() {
+    if (maxlen_ver != tver) {
+      int64_t m = 0;
+      for (int32_t s = 0; s < nslots; s++)
+        if (h_cid[s] >= 0) m = std::max(m, h_len[s]);
+      maxlen_cached = m;
+      maxlen_ver = tver;
+    }
+    return maxlen_cached;
   }
 
   int sync_table() {
@@ -1503,9 +1522,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   RET(S.probe.ensure((size_t)B * nprobe * 4));
   RET(S.probe_key.ensure((size_t)B * nprobe * 4));
   RET(S.counts.ensure((size_t)ns * 4));
-  int64_t maxlen = 0;
-  for (int32_t s = 0; s < ix->nslots; s++)
-    if (ix->h_cid[s] >= 0) maxlen = std::max(maxlen, ix->h_len[s]);
+  const int64_t maxlen = ix->max_list_len();
   const int64_t max_nch = std::max<int64_t>(1, (maxlen + ix->chunk_rows - 1) / ix->chunk_rows);
   const int64_t max_items = B * nprobe * max_nch;
   RET(S.items.ensure((size_t)max_items * sizeof(ScanItem)));
@@ -1586,12 +1603,19 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     RET(S.ncand.ensure(B * 4));
     const int ks = coarse_split_k(ix->nslots, (int)B, (int)dp, ix->num_sms);
     RET(S.dc.ensure((size_t)ks * B * ns * 4));
-    if (ix->coarse_split) {
-      RET(ix->encode_2d(&ix->cmaps.q[0], S.qhi.as<float>(), dp, B, 64));
-      RET(ix->encode_2d(&ix->cmaps.q[1], S.qlo.as<float>(), dp, B, 64));
-    } else {
-      RET(ix->encode_2d(&ix->cmaps.q[0], S.q.as<float>(), dp, B, 64));
+    // tensor maps of this scratch set's query tables, re-encoded only when the
+    // buffers or the batch size change (a driver call each otherwise)
+    const void* qp0 = ix->coarse_split ? S.qhi.p : S.q.p;
+    const void* qp1 = ix->coarse_split ? S.qlo.p : nullptr;
+    if (S.qmap_ptr[0] != qp0 || S.qmap_ptr[1] != qp1 || S.qmap_rows != B) {
+      RET(ix->encode_2d(&S.qmap[0], static_cast<const float*>(qp0), dp, B, 64));
+      if (qp1) RET(ix->encode_2d(&S.qmap[1], static_cast<const float*>(qp1), dp, B, 64));
+      S.qmap_ptr[0] = qp0;
+      S.qmap_ptr[1] = qp1;
+      S.qmap_rows = B;
     }
+    ix->cmaps.q[0] = S.qmap[0];
+    if (qp1) ix->cmaps.q[1] = S.qmap[1];
     launch_coarse_tc(ix->coarse_split, ks, ix->cmaps, ix->nslots, (int)B, (int)dp,
                      S.dc.as<float>(), ns, fs);
     PROF(2);

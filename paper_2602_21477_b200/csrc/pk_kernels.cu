@@ -47,6 +47,20 @@ static void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   launch_maybe_pdl(true, kernel, grid, block, smem, st, args...);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a launch needs
+// more than this kernel was last granted on this device (a host-side driver
+// call per launch otherwise)
+#define PK_SMEM_ATTR(kfn, smem)                                                              \
+  do {                                                                                      \
+    static int cur_[64] = {0};                                                              \
+    int dev_ = 0;                                                                           \
+    cudaGetDevice(&dev_);                                                                   \
+    if (dev_ < 0 || dev_ >= 64 || (int)(smem) > cur_[dev_]) {                                \
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(smem));   \
+      if (dev_ >= 0 && dev_ < 64) cur_[dev_] = (int)(smem);                                  \
+    }                                                                                       \
+  } while (0)
+
 template <int METRIC>
 __device__ __forceinline__ float finalize(float acc, float nn, float qn) {
   if (METRIC == SQ_L2) return acc;
@@ -170,7 +184,7 @@ static void dist_dense_dispatch(const float* Q, int64_t ldq, int B, const float*
 #define PK_DD(NQV)                                                                                  \
   case NQV: {                                                                                       \
     auto k = dist_dense_kernel<METRIC, NQV>;                                                        \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                \
+    PK_SMEM_ATTR(k, (int)smem);                \
     k<<<grid, 128, smem, st>>>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd);                            \
   } break;
   switch (nq) {
@@ -249,8 +263,7 @@ void launch_kmeans_assign(const float* X, int64_t ldx, int64_t n, const float* C
                           int64_t k, int dp, int64_t* labels, double* dists, cudaStream_t st) {
   if (n <= 0) return;
   size_t smem = (size_t)KM_G * dp * 4;
-  cudaFuncSetAttribute(kmeans_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  PK_SMEM_ATTR(kmeans_assign_kernel, (int)smem);
   kmeans_assign_kernel<<<(unsigned)((n + 127) / 128), 128, smem, st>>>(X, ldx, n, C, ldc, k, dp,
                                                                       labels, dists);
 }
@@ -490,8 +503,7 @@ void launch_coarse_select(const float* Dc, int64_t ldd, int B, ListTable lt,
                           uint32_t* probe_key, cudaStream_t st) {
   if (B <= 0) return;
   size_t smem = SEL_CAP * sizeof(Entry);
-  cudaFuncSetAttribute(coarse_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  PK_SMEM_ATTR(coarse_select_kernel, (int)smem);
   coarse_select_kernel<<<B, 256, smem, st>>>(Dc, ldd, lt, scope_codes, nscopes, nprobe, probe,
                                              probe_key);
 }
@@ -1068,7 +1080,7 @@ void launch_scan(int metric, ListTable lt, const ArenaMaps& maps, const float* Q
 #define PK_SCAN(M)                                                                                \
   {                                                                                               \
     auto k = scan_kernel<M>;                                                                      \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);              \
+    PK_SMEM_ATTR(k, (int)smem);              \
     k<<<grid, SCAN_THREADS, smem, st>>>(maps, lt, Qd, qnorm, items, n_items, qpairs, kk, work_ctr, \
                                         cand_key, cand_id, cand_n, cand_list);                    \
   }
@@ -1184,7 +1196,7 @@ void launch_merge(int B, const int32_t* slot_off, const uint32_t* cand_key, cons
                   cudaStream_t st) {
   if (B <= 0) return;
   size_t smem = MERGE_CAP * sizeof(Entry);
-  cudaFuncSetAttribute(merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  PK_SMEM_ATTR(merge_kernel, (int)smem);
   merge_kernel<<<B, 128, smem, st>>>(slot_off, cand_key, cand_id, cand_n, cand_list, kk, lt,
                                      out_ids, out_d, out_cid, out_n);
 }
@@ -1791,7 +1803,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
 #define PK_TC(M)                                                                                 \
   {                                                                                              \
     auto k = scan_tc_kernel<M>;                                                                  \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);             \
+    PK_SMEM_ATTR(k, (int)smem);             \
     launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, lt, (const float*)qsw,   \
                (int64_t)B, \
                qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
@@ -1848,13 +1860,13 @@ void launch_scan_screen(int metric, ListTable lt, const ArenaMaps& maps, const f
   static const int debug_nocompute = getenv("PK_DEBUG_SCAN_NOCOMPUTE") ? atoi(getenv("PK_DEBUG_SCAN_NOCOMPUTE")) : 0;
   if (metric == SQ_L2) {
     auto k = scan_screen_kernel<SQ_L2>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PK_SMEM_ATTR(k, (int)smem);
     k<<<grid, SCREEN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
                                           work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap,
                                           debug_nocompute);
   } else {
     auto k = scan_screen_kernel<IP>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PK_SMEM_ATTR(k, (int)smem);
     k<<<grid, SCREEN_THREADS, smem, st>>>(maps, lt, Qd, qnorm2, items, n_items, qpairs, kk, coef,
                                           work_ctr, Uq, slot_hi, slot_n, cpool, ccount, cap,
                                           debug_nocompute);
@@ -2128,7 +2140,7 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
 #define PK_RR(M)                                                                                \
   {                                                                                             \
     auto k = rerank_merge_kernel<M>;                                                            \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    PK_SMEM_ATTR(k, (int)smem);            \
     launch_maybe_pdl(pdl, k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
                                    nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv,  \
                                    scanned_src, scanned_dst);                                    \
@@ -2319,7 +2331,7 @@ void launch_shard_merge(const void* blocks, int64_t block_bytes, int R, int B, i
   int N = 1;
   while (N < R * kk) N <<= 1;
   size_t smem = (size_t)N * sizeof(Entry);
-  cudaFuncSetAttribute(shard_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  PK_SMEM_ATTR(shard_merge_kernel, (int)smem);
   shard_merge_kernel<<<B, 128, smem, st>>>(static_cast<const uint8_t*>(blocks), block_bytes, R, B,
                                            kk, out_ids, out_d, out_cid, out_n, out_scanned);
 }
@@ -2484,10 +2496,10 @@ void launch_coarse_tc(bool split, int ks, const CoarseMaps& maps, int nslots, in
   const size_t smem = coarse_tc_smem_bytes(split);
   dim3 grid((unsigned)((nslots + CT_M - 1) / CT_M), (unsigned)((B + CT_N - 1) / CT_N), (unsigned)ks);
   if (split) {
-    cudaFuncSetAttribute(coarse_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PK_SMEM_ATTR(coarse_tc_kernel<true>, (int)smem);
     launch_pdl(coarse_tc_kernel<true>, grid, dim3(128), smem, st, maps, nslots, B, dp / DC, Dout, lda);
   } else {
-    cudaFuncSetAttribute(coarse_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    PK_SMEM_ATTR(coarse_tc_kernel<false>, (int)smem);
     launch_pdl(coarse_tc_kernel<false>, grid, dim3(128), smem, st, maps, nslots, B, dp / DC, Dout, lda);
   }
 }
@@ -2897,7 +2909,7 @@ void launch_coarse_pick(int metric, bool split, int ks, const float* Aapp, int64
 #define PK_PK(M)                                                                                     \
   {                                                                                                  \
     auto k = coarse_pick_kernel<M>;                                                                  \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
+    PK_SMEM_ATTR(k, (int)smem);                 \
     launch_pdl(k, dim3(B), dim3(PICK_THREADS), smem, st, Aapp, lda, lt, cnrm, Qd, qn2, scope_codes, nscopes, nprobe, \
                                      coef, abs_coef, cap, stage_floats, ks, (int64_t)B * lda, probe, \
                                      probe_key, ncand, dbg, ra);                                     \
@@ -3254,7 +3266,7 @@ void launch_peer_merge(const void* area, int64_t block_bytes, int R, int B, int 
   int N = 1;
   while (N < R * kk) N <<= 1;
   const size_t smem = (size_t)N * sizeof(Entry);
-  cudaFuncSetAttribute(peer_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  PK_SMEM_ATTR(peer_merge_kernel, (int)smem);
   peer_merge_kernel<<<B, 128, smem, st>>>(static_cast<const uint8_t*>(area), block_bytes, R, B, kk, epoch,
                                           timeout_ns, err, out_ids, out_d, out_cid, out_n, out_scanned);
 }
