@@ -184,6 +184,10 @@ struct pk_index {
     CUtensorMap qmap[2];
     const void* qmap_ptr[2] = {nullptr, nullptr};
     int64_t qmap_rows = -1;
+    // the scan's gather4 map over the padded query batch
+    CUtensorMap qgmap;
+    const void* qg_ptr = nullptr;
+    int64_t qg_rows = -1;
     void release() {
       for (DevBuf* b : {&q, &qnorm, &dc, &probe, &probe_key, &counts, &items, &qpairs, &slot_off,
                         &scanned, &cand_key, &cand_id, &cand_n, &cand_list, &out_ids, &scopes, &qnorm2,
@@ -208,6 +212,9 @@ struct pk_index {
   bool coarse_split = true;  // 3xTF32 hi/lo split (tight bound); PK_COARSE=tf32 for one product
   int pool_cap = 4096;  // candidate pool per query (overflow -> exact slow path)
   bool pool_cap_set = false;  // PK_POOL_CAP given: no growth with kk
+  // scan query chunks by TMA gather4 (4 queries per op) instead of one bulk
+  // copy per query from 8 pre-swizzled batch copies; PK_QGATHER=0 for those
+  bool qgather = true;
   DevBuf shard_in, shard_out, pb, pb_out, sl_buf;
   uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
   size_t hout_bytes = 0;
@@ -880,6 +887,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   }
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
   if (const char* e = getenv("PK_PIPELINE")) ix->pipeline = atoi(e) != 0;
+  if (const char* e = getenv("PK_QGATHER")) ix->qgather = atoi(e) != 0;
   if (const char* e = getenv("PK_STAGE")) ix->stage_dma = strcmp(e, "dma") == 0;
   if (const char* e = getenv("PK_COARSE")) {
     ix->coarse_tc = strcmp(e, "exact") != 0;
@@ -1577,14 +1585,14 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
       RET(S.qhi.ensure((size_t)B * dp * 4));
       RET(S.qlo.ensure((size_t)B * dp * 4));
     }
-    if (tc_scan) RET(S.qsw.ensure((size_t)8 * B * dp * 4));
+    if (tc_scan && !ix->qgather) RET(S.qsw.ensure((size_t)8 * B * dp * 4));
     if (ix->screen) {
       RET(S.uq.ensure((size_t)B * 4));
       RET(S.ccount.ensure((size_t)B * 4));
     }
     launch_qprep(qin, ix->d, (int)ix->d, (int)B, (int)dp, S.q.as<float>(), S.qnorm2.as<float>(),
                  sp ? S.qhi.as<float>() : nullptr, sp ? S.qlo.as<float>() : nullptr,
-                 tc_scan ? S.qsw.as<float>() : nullptr, lcount, (int)(ns + 3),
+                 (tc_scan && !ix->qgather) ? S.qsw.as<float>() : nullptr, lcount, (int)(ns + 3),
                  ix->screen ? S.ccount.as<int32_t>() : nullptr, ix->screen ? (int)B : 0,
                  ix->screen ? S.uq.as<uint32_t>() : nullptr, ix->screen ? (int)B : 0, fs);
   } else {
@@ -1670,12 +1678,22 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (ix->screen) {
     RET(S.cpool.ensure((size_t)B * pool_cap * sizeof(int4)));  // uq / ccount reset by prep
     if (ix->tensor) {
+      // gather4 map over this scratch set's padded queries (box 32 x 1 row)
+      const CUtensorMap* qg = nullptr;
+      if (ix->qgather) {
+        if (S.qg_ptr != S.q.p || S.qg_rows != B) {
+          RET(ix->encode_2d(&S.qgmap, S.q.as<float>(), dp, B, 1));
+          S.qg_ptr = S.q.p;
+          S.qg_rows = B;
+        }
+        qg = &S.qgmap;
+      }
       launch_scan_tc(ix->metric, lt2, ix->maps, S.q.as<float>(), (int)B, S.qsw.as<float>(), true,
                      S.qnorm2.as<float>(), S.items.as<ScanItem>(), n_items,
                      (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
                      work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
                      S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
-                     pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined);
+                     pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined, qg);
     } else {
       launch_scan_screen(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm2.as<float>(),
                          S.items.as<ScanItem>(), n_items,

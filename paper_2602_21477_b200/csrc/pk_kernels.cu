@@ -892,7 +892,8 @@ __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMa
                                               const ScanItem* __restrict__ items, const int32_t* __restrict__ nctr,
                                               const QPair* __restrict__ qpairs,
                                               int32_t* __restrict__ work_ctr, int nchunk_d,
-                                              bool keep_in_l2, int64_t qsw_stride) {
+                                              bool keep_in_l2, int64_t qsw_stride,
+                                              const CUtensorMap* qg = nullptr) {
   // front items [0, nctr[0]) then the tail items, stored backwards from nctr[3]
   const int n_front = nctr[0], n_items = n_front + nctr[2], tail_base = nctr[3];
   const int lane = threadIdx.x & 31;
@@ -928,10 +929,23 @@ __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMa
     // lands SWIZZLE_128B-ready in row `lane` of the stage's query tile.
     const float* qrow =
         Qd + ((qsw_stride ? (int64_t)(lane & 7) * qsw_stride : 0) + qb) * (int64_t)lt.dp;
+    // qg: the item's query chunk comes in ceil(nq / 4) gathers of four rows
+    // of the (unswizzled) batch -- lane j < ngq issues group j, slots past nq
+    // repeat the last query (their dots are never read)
+    const int ngq = (item.nq + 3) >> 2;
+    int g0 = 0, g1 = 0, g2 = 0, g3 = 0;
+    if (qg) {
+      const int last = item.nq - 1;
+      g0 = __shfl_sync(FULL, qb, min(4 * lane + 0, last) & 31);
+      g1 = __shfl_sync(FULL, qb, min(4 * lane + 1, last) & 31);
+      g2 = __shfl_sync(FULL, qb, min(4 * lane + 2, last) & 31);
+      g3 = __shfl_sync(FULL, qb, min(4 * lane + 3, last) & 31);
+    }
+    const int qbytes = qg ? ngq * 4 * DC * 4 : item.nq * DC * 4;
     for (int t0 = 0; t0 < item.nrows; t0 += TILE) {
       const int rows = min(TILE, item.nrows - t0);
       const int rows8 = (rows + 7) & ~7;
-      const uint32_t bytes = (uint32_t)(rows8 * DC * 4 + item.nq * DC * 4);
+      const uint32_t bytes = (uint32_t)(rows8 * DC * 4 + qbytes);
       for (int c = 0; c < nchunk_d; c++) {
         mbar_wait(&S.empty[s], ph ^ 1);
         if (lane == 0) {
@@ -948,8 +962,13 @@ __device__ __forceinline__ void scan_producer(const ScanShared& S, const ArenaMa
           }
         }
         __syncwarp();
-        if (lane < item.nq)
+        if (qg) {
+          if (lane < ngq)
+            tma_gather4(S.Qc + (size_t)s * QG * DC + lane * 4 * DC, qg, &S.full[s], c * DC, g0, g1, g2, g3,
+                        pol);
+        } else if (lane < item.nq) {
           bulk_g2s(S.Qc + (size_t)s * QG * DC + lane * DC, qrow + c * DC, DC * 4, &S.full[s]);
+        }
         if (++s == NSTAGE) {
           s = 0;
           ph ^= 1;
@@ -1555,7 +1574,8 @@ size_t tc_smem_bytes() { return TcLayout::TOTAL + 1024; }
 
 template <int METRIC>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    scan_tc_kernel(const __grid_constant__ ArenaMaps maps, ListTable lt, const float* __restrict__ Qsw,
+    scan_tc_kernel(const __grid_constant__ ArenaMaps maps, const __grid_constant__ CUtensorMap qgmap,
+                   bool use_qg, ListTable lt, const float* __restrict__ Qsw,
                    int64_t qsw_stride, const float* __restrict__ qnorm2,
                    const ScanItem* __restrict__ items, const int32_t* __restrict__ n_items_p,
                    const QPair* __restrict__ qpairs, int kk, float coef,
@@ -1628,7 +1648,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == TC_EPI_WARPS) {
     // ---------------------------------------------------------- producer
     scan_producer<TC_STAGES>(S, maps, lt, Qsw, items, n_items_p, qpairs, work_ctr, nchunk_d, false,
-                             qsw_stride);
+                             qsw_stride, use_qg ? &qgmap : nullptr);
   } else if (warp == TC_EPI_WARPS + 1) {
     // ---------------------------------------------------------- MMA issuer
     const uint32_t idesc = umma_idesc_tf32(128, QG);
@@ -1787,9 +1807,14 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
                     float* qsw, bool qsw_ready, const float* qnorm2, const ScanItem* items,
                     const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
                     int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
-                    int32_t* ccount, int cap, int num_sms, cudaStream_t st, bool pdl) {
+                    int32_t* ccount, int cap, int num_sms, cudaStream_t st, bool pdl,
+                    const CUtensorMap* qgather) {
   if (max_items <= 0) return;
-  if (!qsw_ready) qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
+  if (!qgather && !qsw_ready) qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
+  CUtensorMap qg_dummy;
+  memset(&qg_dummy, 0, sizeof(qg_dummy));
+  const CUtensorMap& qgm = qgather ? *qgather : qg_dummy;
+  const bool use_qg = qgather != nullptr;
   const size_t smem = tc_smem_bytes();
   const int grid = std::min(num_sms, max_items);
   const float coef = screen_coef_tf32(metric, lt.dp);
@@ -1804,7 +1829,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   {                                                                                              \
     auto k = scan_tc_kernel<M>;                                                                  \
     PK_SMEM_ATTR(k, (int)smem);             \
-    launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, lt, (const float*)qsw,   \
+    launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, qgm, use_qg, lt, (const float*)qsw, \
                (int64_t)B, \
                qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
                ccount, cap, dbg_skip, dbg_t);                                                      \
