@@ -1923,9 +1923,14 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     const int32_t* __restrict__ slot_off, ListTable lt, const float* __restrict__ Qd,
     const int32_t* __restrict__ probe, int nprobe, int kk, int stage_floats, int64_t* __restrict__ out_ids,
     float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n,
-    int32_t* __restrict__ nsurv, const int64_t* __restrict__ scanned_src, int64_t* __restrict__ scanned_dst) {
+    int32_t* __restrict__ nsurv, const int64_t* __restrict__ scanned_src, int64_t* __restrict__ scanned_dst,
+    uint64_t* __restrict__ dbg) {
   pdl_trigger();
   pdl_wait();
+  auto mark = [&](int i) {  // phase cycle stamps (PK_DEBUG_RERANK)
+    if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 4 + i] = (uint64_t)clock64();
+  };
+  mark(0);
   if (scanned_dst && threadIdx.x == 0) scanned_dst[blockIdx.x] = scanned_src[blockIdx.x];
   extern __shared__ __align__(16) uint8_t rr_smem[];
   Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [RR_CAP]
@@ -2021,6 +2026,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     }
   }
   __syncthreads();
+  mark(1);
   int kept = 0, surv_total = 0;
   const int room = RR_CAP - kk;
   if (!overflow) {
@@ -2044,7 +2050,9 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
       for (int g0 = 0; g0 < ns; g0 += chunk) {
         const int m = min(chunk, ns - g0);
         const int nd32 = dp4 / 8;
-        const int R = 2;  // (measured: 3-4 deep with narrower blocks is slower)
+        // whole rows in one block when they fit, else a 2-deep ring of column
+        // blocks (measured: 3-4 deep with narrower blocks is slower)
+        const int R = m * (DC * nd32 + 4) <= stage_floats ? 1 : 2;
         int kq = 1;
         for (int k2 = nd32; k2 >= 1; k2--)
           if (nd32 % k2 == 0 && R * m * (DC * k2 + 4) <= stage_floats) {
@@ -2074,9 +2082,8 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
         float acc = 0.f;
         for (int blk = 0; blk < nblk; blk++) {
           issue(blk + R - 1);
-          if (R == 4) cp_async_wait<3>();
-          else if (R == 3) cp_async_wait<2>();
-          else cp_async_wait<1>();
+          if (R == 2) cp_async_wait<1>();
+          else cp_async_wait<0>();
           __syncthreads();
           if (threadIdx.x < m) {
             const float4* x4 = reinterpret_cast<const float4*>(stage + (blk % R) * m * rs + threadIdx.x * rs);
@@ -2134,6 +2141,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
       kept = cta_compact_sorted(buf, kept + m, kk, true, &s_cnt);
     }
   }
+  mark(2);
   for (int i = threadIdx.x; i < kk; i += blockDim.x) {
     const int64_t o = (int64_t)b * kk + i;
     if (i < kept) {
@@ -2150,6 +2158,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     out_n[b] = kept;
     if (nsurv) nsurv[b] = overflow ? -1 : surv_total;
   }
+  mark(3);
 }
 
 void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* ccount, int cap,
@@ -2159,8 +2168,12 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
                          cudaStream_t st, bool pdl) {
   if (B <= 0) return;
-  // column-block stage of ~56 KB (two CTAs per SM)
-  const int stage_floats = 56 * 1024 / 4;
+  static const bool debug = getenv("PK_DEBUG_RERANK") != nullptr;
+  uint64_t* dbg = nullptr;
+  if (debug) cudaMallocAsync((void**)&dbg, (size_t)B * 32, st);
+  // row stage of ~82 KB (two CTAs per SM): the typical ~26 survivors' whole
+  // rows fit at once (one load round trip instead of one per column block)
+  const int stage_floats = 82 * 1024 / 4;
   const size_t smem = RR_CAP * sizeof(Entry) + (size_t)lt.dp * 4 + (size_t)stage_floats * 4 + RR_SURV * 4;
 #define PK_RR(M)                                                                                \
   {                                                                                             \
@@ -2168,11 +2181,22 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
     PK_SMEM_ATTR(k, (int)smem);            \
     launch_maybe_pdl(pdl, k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
                                    nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv,  \
-                                   scanned_src, scanned_dst);                                    \
+                                   scanned_src, scanned_dst, dbg);                                    \
   }
   if (metric == SQ_L2) PK_RR(SQ_L2)
   else PK_RR(IP)
 #undef PK_RR
+  if (dbg) {
+    std::vector<uint64_t> h((size_t)B * 4);
+    cudaMemcpyAsync(h.data(), dbg, h.size() * 8, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double acc[4] = {0};
+    for (int b = 0; b < B; b++)
+      for (int i = 1; i < 4; i++) acc[i] += (double)(h[b * 4 + i] - h[b * 4 + i - 1]);
+    fprintf(stderr, "rerank phases (us, mean per CTA @1965 MHz): bound %.2f survivors+exact+sort %.2f out %.2f\n",
+            acc[1] / B / 1965.0, acc[2] / B / 1965.0, acc[3] / B / 1965.0);
+    cudaFreeAsync(dbg, st);
+  }
 }
 
 // =====================================================================
