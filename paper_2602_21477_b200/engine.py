@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _native as N
 from . import pnck
-from .cache import DEFAULT_KEY, MultiLevelCache, kth_smallest
+from .cache import DEFAULT_KEY, MultiLevelCache, RunningKth
 from .clusters import ClusterStore, SplitOutcome, kmeans_split_points
 from .fsm import PatternHint, PatternTable
 from .kernels import batch_distances
@@ -483,6 +483,11 @@ class Store:
             clusters = self.clusters.clusters
             total = sum(clusters[c].size for c in selected)
             all_ids, all_d, pre = self.index.scan_lists(q, selected, total)
+            run = None
+            if thresh is not None:  # stop rule over everything scanned so far
+                run = RunningKth(k)
+                for c in dist_chunks:
+                    run.add(c)
             for li, cid in enumerate(selected):
                 cl = clusters[cid]
                 cl.access_count += 1
@@ -491,6 +496,8 @@ class Store:
                 if len(ids):
                     id_chunks.append(ids)
                     dist_chunks.append(all_d[pre[li]:pre[li + 1]])
+                    if run is not None:
+                        run.add(dist_chunks[-1])
                 stats.scanned_vectors += len(ids)
                 if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
                     order = profile_order(cl.profiles[agent], cl.size)
@@ -498,7 +505,7 @@ class Store:
                 else:
                     scan_chunks.append(cl.member_ids.copy())
                 if thresh is not None and len(dist_chunks):
-                    kth = kth_smallest(dist_chunks, k)
+                    kth = run.kth()
                     if kth is not None and kth < thresh:
                         early = True
                         stats.early_terminated = True

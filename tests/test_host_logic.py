@@ -99,6 +99,72 @@ def test_profile_order_equals_reorder():
         assert profile_order(entries, size).tolist() == want
 
 
+@pytest.mark.parametrize("ordered", [True, False])
+def test_vector_pool_matches_list_model(ordered):
+    """VectorPool (head offset for FIFO pops, swap-with-last for unordered
+    pools) keeps the reference's row order (ref/pool.py:33-144)."""
+    from paper_2602_21477_b200.pool import VectorPool
+
+    rng = np.random.default_rng(11 if ordered else 12)
+    d = 5
+    pool = VectorPool(d, ordered=ordered)
+    model = []  # [(id, vec, scope, staged)] in scan order
+    nid = 0
+    for step in range(3000):
+        op = rng.integers(0, 4)
+        if op <= 1 or not model:
+            v = rng.normal(size=d).astype(np.float32)
+            sc, st = int(rng.integers(0, 3)), bool(rng.integers(0, 2))
+            assert pool.add(nid, v, sc, st)
+            model.append((nid, v, sc, st))
+            nid += 1
+        elif op == 2:
+            j = int(rng.integers(0, len(model)))
+            iid = model[j][0]
+            assert pool.remove(iid)
+            if ordered:
+                model.pop(j)
+            else:
+                last = model.pop()
+                if j < len(model):
+                    model[j] = last
+        else:
+            if ordered:
+                got = pool.pop_front()
+                want = model.pop(0)
+                assert got[0] == want[0] and np.array_equal(got[1], want[1]) and got[2:] == want[2:]
+            else:
+                iid = model[0][0]
+                pool.set_staged(iid, True)
+                model[0] = model[0][:3] + (True,)
+        assert len(pool) == len(model)
+        assert pool.ids.tolist() == [m[0] for m in model]
+        if model:
+            assert np.array_equal(pool.vectors, np.stack([m[1] for m in model]))
+            assert pool.scopes.tolist() == [m[2] for m in model]
+            j = int(rng.integers(0, len(model)))
+            assert pool.row_of(model[j][0]) == j
+            assert pool.staged_flag(model[j][0]) == model[j][3]
+            assert [r[0] for r in pool.rows()] == [m[0] for m in model]
+            assert pool.scope_mask([1]).tolist() == [m[2] == 1 for m in model]
+
+
+def test_running_kth_equals_kth_smallest():
+    """The incremental stop-rule statistic equals ref/cache.py:154-160's k-th
+    smallest of the concatenation after every chunk (duplicates counted)."""
+    from paper_2602_21477_b200.cache import RunningKth, kth_smallest
+
+    rng = np.random.default_rng(0)
+    for _ in range(500):
+        k = int(rng.integers(1, 30))
+        run, chunks = RunningKth(k), []
+        for _ in range(int(rng.integers(1, 8))):
+            c = rng.integers(0, 20, int(rng.integers(0, 40))).astype(np.float32)
+            chunks.append(c)
+            run.add(c)
+            assert run.kth() == kth_smallest(chunks, k)
+
+
 def test_rwlock_and_runner():
     lock = RWLock()
     hits = []
