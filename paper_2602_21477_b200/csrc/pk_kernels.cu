@@ -1376,40 +1376,52 @@ __device__ __forceinline__ void screen_select(const ScanShared& S, int a, int R,
       lk[i] = f2key(lo);
     }
   }
-  // U_item = kk-th smallest hi of the item (KEY_NONE when R < kk)
-  uint32_t Uitem = KEY_NONE;
-  if (R >= kk) {
-    uint32_t mn = KEY_NONE, mx = 0;
+  // Only this item's rows with hi <= the query's current bound U0 can matter:
+  // the re-rank's bound is the kk-th smallest published hi, which never
+  // exceeds Uq <= U0, and every value at or under it is <= U0 when published.
+  // So when fewer than kk rows are under U0 (the common case once the bound
+  // has tightened) they are published as they are, with no selection; else
+  // U_item = kk-th smallest hi (bisection over [min, U0]) tightens Uq and the
+  // item's kk smallest hi are published.
+  const uint32_t U0 = *(volatile uint32_t*)&Uq[b];
+  unsigned c0 = 0;
+  uint32_t mn = KEY_NONE, mx = 0;
 #pragma unroll
-    for (int i = 0; i < PER; i++) {
-      if (lane + 32 * i < R) {
-        mn = min(mn, hk[i]);
-        mx = max(mx, hk[i]);
-      }
+  for (int i = 0; i < PER; i++) {
+    if (lane + 32 * i < R && hk[i] <= U0) {
+      c0++;
+      mn = min(mn, hk[i]);
+      mx = max(mx, hk[i]);
     }
+  }
+  const unsigned cnt0 = __reduce_add_sync(FULL, c0);
+  uint32_t Uitem = KEY_NONE;
+  if (cnt0 >= (unsigned)kk) {
     uint32_t L = __reduce_min_sync(FULL, mn), H = __reduce_max_sync(FULL, mx);
     while (L < H) {
       const uint32_t mid = L + ((H - L) >> 1);
       unsigned cc = 0;
 #pragma unroll
-      for (int i = 0; i < PER; i++) cc += (hk[i] <= mid);
+      for (int i = 0; i < PER; i++) cc += (lane + 32 * i < R) && (hk[i] <= mid);
       if (__reduce_add_sync(FULL, cc) >= (unsigned)kk) H = mid;
       else L = mid + 1;
     }
     Uitem = L;
     if (lane == 0) atomicMin(&Uq[b], Uitem);
   }
-  // the item's kk smallest hi: every hi < U_item, then U_item repeated
   {
+    // cnt0 >= kk: every hi < U_item, then U_item repeated (kk values);
+    // else: every hi <= U0 (cnt0 < kk values)
+    const bool sel = cnt0 >= (unsigned)kk;
     int base = 0;
 #pragma unroll
     for (int i = 0; i < PER; i++) {
-      const bool below = (lane + 32 * i < R) && hk[i] < Uitem;
+      const bool below = (lane + 32 * i < R) && (sel ? hk[i] < Uitem : hk[i] <= U0);
       const unsigned bal = __ballot_sync(FULL, below);
       if (below) slot_hi[slot * kk + base + __popc(bal & ((1u << lane) - 1u))] = hk[i];
       base += __popc(bal);
     }
-    const int nfill = (R >= kk) ? kk : R;
+    const int nfill = sel ? kk : base;
     for (int l = base + lane; l < nfill; l += 32) slot_hi[slot * kk + l] = Uitem;
     if (lane == 0) slot_n[slot] = nfill;
   }
