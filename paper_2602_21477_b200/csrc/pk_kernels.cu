@@ -1355,7 +1355,8 @@ __device__ __forceinline__ void screen_select(const ScanShared& S, int a, int R,
                                               uint32_t* __restrict__ slot_hi,
                                               int32_t* __restrict__ slot_n,
                                               int4* __restrict__ cpool,
-                                              int32_t* __restrict__ ccount, int cap) {
+                                              int32_t* __restrict__ ccount, int cap,
+                                              uint32_t u0_pre = 0, bool have_u0 = false) {
   const int lane = threadIdx.x & 31;
   constexpr int PER = CHUNK_MAX / 32;
   uint32_t hk[PER], lk[PER];
@@ -1383,7 +1384,8 @@ __device__ __forceinline__ void screen_select(const ScanShared& S, int a, int R,
   // has tightened) they are published as they are, with no selection; else
   // U_item = kk-th smallest hi (bisection over [min, U0]) tightens Uq and the
   // item's kk smallest hi are published.
-  const uint32_t U0 = *(volatile uint32_t*)&Uq[b];
+  // (the tensor-core scan prefetches it while the item's A values are formed)
+  const uint32_t U0 = have_u0 ? u0_pre : *(volatile uint32_t*)&Uq[b];
   unsigned c0 = 0;
   uint32_t mn = KEY_NONE, mx = 0;
 #pragma unroll
@@ -1425,7 +1427,9 @@ __device__ __forceinline__ void screen_select(const ScanShared& S, int a, int R,
     for (int l = base + lane; l < nfill; l += 32) slot_hi[slot * kk + l] = Uitem;
     if (lane == 0) slot_n[slot] = nfill;
   }
-  const uint32_t U = min(Uitem, *(volatile uint32_t*)&Uq[b]);
+  // candidate bound: this item's own U_item and the query bound it started
+  // from (a concurrent tightening elsewhere only makes it looser, never wrong)
+  const uint32_t U = min(Uitem, have_u0 ? U0 : *(volatile uint32_t*)&Uq[b]);
   unsigned tot = 0;
 #pragma unroll
   for (int i = 0; i < PER; i++) tot += (lane + 32 * i < R && lk[i] <= U);
@@ -1752,6 +1756,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tcount++;
       }
       named_bar_sync(1, nthr);
+      // each warp's query bounds, loaded now so their L2 latency hides under
+      // the A computation below
+      const uint32_t u0a = warp < nq ? *(volatile uint32_t*)&Uq[qb_s[warp]] : 0u;
+      const uint32_t u0b = warp + TC_EPI_WARPS < nq ? *(volatile uint32_t*)&Uq[qb_s[warp + TC_EPI_WARPS]] : 0u;
       for (int i = threadIdx.x; i < nq * item.nrows; i += nthr) {
         const int a = i / item.nrows, row = i - a * item.nrows;
         const float dot = S.A[a * CHUNK_MAX + row];
@@ -1762,7 +1770,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int a = warp; a < nq && !dbg_skip; a += TC_EPI_WARPS)
         screen_select(S, a, item.nrows, kk, coef, nq2_s[a], qb_s[a], item.lslot, rbase,
                       (int64_t)qpairs[item.qoff + a].slotbase + item.chunk, Uq, slot_hi, slot_n,
-                      cpool, ccount, cap);
+                      cpool, ccount, cap,
+                      a == warp ? u0a : u0b, a < 2 * TC_EPI_WARPS);
       named_bar_sync(1, nthr);  // A / NX / qb_s reuse by the next item
     }
   }
