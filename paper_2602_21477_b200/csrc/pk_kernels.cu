@@ -1984,15 +1984,25 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     // flattened (slot, entry) index space; slots hold <= kk entries each
     const int nflat = (eo - so) * kk;
     bool fits = nflat <= RR_HI_PER * RR_THREADS;
+    // all loads first and independent (entries past a slot's count are read
+    // and dropped): one L2 round trip instead of two dependent ones per entry
+    int nn[RR_HI_PER];
+    uint32_t hraw[RR_HI_PER];
 #pragma unroll
     for (int i = 0; i < RR_HI_PER; i++) {
       const int f = threadIdx.x + i * RR_THREADS;
-      if (fits && f < nflat) {
-        const int sl = so + f / kk, e = f - (f / kk) * kk;
-        if (e < slot_n[sl]) {
-          hv[i] = slot_hi[(int64_t)sl * kk + e];
-          nh++;
-        }
+      const bool ok = fits && f < nflat;
+      const int sl = so + f / kk, e = f - (f / kk) * kk;
+      nn[i] = ok ? slot_n[sl] : 0;
+      hraw[i] = ok ? slot_hi[(int64_t)sl * kk + e] : KEY_NONE;
+    }
+#pragma unroll
+    for (int i = 0; i < RR_HI_PER; i++) {
+      const int f = threadIdx.x + i * RR_THREADS;
+      const int e = f - (f / kk) * kk;
+      if (fits && f < nflat && e < nn[i]) {
+        hv[i] = hraw[i];
+        nh++;
       }
     }
     int have = __reduce_add_sync(FULL, nh);
