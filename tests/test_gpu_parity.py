@@ -135,15 +135,18 @@ def _random_index(pk, rng, d, nlist, sizes, metric=0, dup=False, ids_shuffle=Tru
     return ix, lists, np.stack(cents), np.arange(nlist) * 2 + 5
 
 
-@pytest.fixture(params=["tensor", "ffma", "exact", "overflow"])
+@pytest.fixture(params=["tensor", "tensor_bulkq", "ffma", "exact", "overflow"])
 def scan_mode(request, monkeypatch):
-    """Every scan kernel: the tcgen05-screened one (default for sq_l2 / ip),
-    the CUDA-core FFMA-screened one (PK_SCREEN=ffma), the all-exact one
-    (PK_SCAN_EXACT=1; always used for cosine), and the screened one with a
-    3-entry candidate pool so every query takes the exact overflow path."""
+    """Every scan kernel: the tcgen05-screened one (default for sq_l2 / ip;
+    query chunks by TMA gather4, or by per-query bulk copies from pre-swizzled
+    copies with PK_QGATHER=0), the CUDA-core FFMA-screened one
+    (PK_SCREEN=ffma), the all-exact one (PK_SCAN_EXACT=1; always used for
+    cosine), and the screened one with a 3-entry candidate pool so every query
+    takes the exact overflow path."""
     monkeypatch.setenv("PK_SCAN_EXACT", "1" if request.param == "exact" else "0")
     monkeypatch.setenv("PK_POOL_CAP", "3" if request.param == "overflow" else "4096")
     monkeypatch.setenv("PK_SCREEN", "ffma" if request.param == "ffma" else "tc")
+    monkeypatch.setenv("PK_QGATHER", "0" if request.param == "tensor_bulkq" else "1")
     return request.param
 
 
