@@ -172,6 +172,13 @@ def test_device_search_matches_oracle(pk, d, metric, scan_mode):
         assert np.array_equal(out.ids, ids)
         assert np.array_equal(bits(out.dists), bits(dd))
         assert np.array_equal(out.scanned, scanned)
+        # without the probe output the pick only settles the probe SET
+        # (certainly-in lists skip the exact re-rank): same answers
+        out2 = ix.search(Q, [0], nprobe, kk)
+        assert np.array_equal(out2.counts, cnt)
+        assert np.array_equal(out2.ids, ids)
+        assert np.array_equal(bits(out2.dists), bits(dd))
+        assert np.array_equal(out2.scanned, scanned)
     ix.close()
 
 
@@ -337,6 +344,10 @@ def test_coarse_quantizer_matches_oracle(pk, kind, coarse, monkeypatch):
         assert np.array_equal(out.probe, probe), (kind, nprobe)
         assert np.array_equal(out.ids, ids)
         assert np.array_equal(bits(out.dists), bits(dd))
+        out2 = ix.search(Q, [0], nprobe, 10)  # probe set only (unordered pick)
+        assert np.array_equal(out2.ids, ids), (kind, nprobe)
+        assert np.array_equal(bits(out2.dists), bits(dd))
+        assert np.array_equal(out2.scanned, scanned)
     ix.close()
 
 
