@@ -1636,6 +1636,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
       ra.chunk_rows = ix->chunk_rows;
       ra.smax = (int)smax;
       ra.bcap = (int)B;
+      ra.unordered = out_probe == nullptr;  // nobody reads the probe order / keys
     }
     launch_coarse_pick(ix->metric, ix->coarse_split, ks, S.dc.as<float>(), ns, (int)B, lt, ix->d_cnrm, S.q.as<float>(),
                        S.qnorm2.as<float>(), S.scopes.as<int32_t>(), nscopes, nprobe,

@@ -2879,16 +2879,59 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
     }
     const int n = s_cnt;
     ncand += n - kept;
+    // Unordered mode, whole candidate set in one round: a candidate with
+    // hk <= U is certainly among the first nprobe when at most nprobe
+    // candidates have lk <= its hk (every list that could rank before it is a
+    // candidate, since lk <= hk <= U); those skip the exact chain (key 0, so
+    // they sort first) and only the uncertain ones -- moved to the front --
+    // are re-ranked, with their whole rows staged at once when they fit.
+    // The probe SET equals the exact quantizer's; order and keys are not
+    // produced in this mode.
+    int nex = n;  // candidates buf[kept, nex) take the exact chain
+    if (ra.unordered && staged && kept == 0 && s_end >= lt.nslots && n <= PICK_THREADS) {
+      __shared__ uint32_t c_lk[PICK_THREADS];
+      __shared__ int s_u0, s_u1;
+      Entry e;
+      uint32_t my_hk = KEY_NONE;
+      if (tid < n) {
+        e = buf[tid];
+        my_hk = hks[e.pay];
+        c_lk[tid] = lks[e.pay];
+      }
+      if (tid == 0) {
+        s_u0 = 0;
+        s_u1 = 0;
+      }
+      __syncthreads();
+      bool certain = false;
+      if (tid < n && my_hk <= U) {
+        int c = 0;
+        for (int j2 = 0; j2 < n; j2++) c += c_lk[j2] <= my_hk;
+        certain = c <= nprobe;
+      }
+      if (tid < n) {
+        if (certain) {
+          e.key = 0;
+          buf[n - 1 - atomicAdd(&s_u1, 1)] = e;
+        } else {
+          buf[atomicAdd(&s_u0, 1)] = e;
+        }
+      }
+      __syncthreads();
+      nex = s_u0;
+    }
     mark(4);
     // exact distances of this round's candidates buf[kept, n) (<= PICK_THREADS):
     // thread t runs candidate t's chain; the rows stream through shared memory
     // in column blocks of W floats (bulk copies, 2-deep ring) so every chain
     // advances together
-    for (int c0 = kept; c0 < n; c0 += PICK_THREADS) {
-      const int nr = min(PICK_THREADS, n - c0);
+    for (int c0 = kept; c0 < nex; c0 += PICK_THREADS) {
+      const int nr = min(PICK_THREADS, nex - c0);
       const int nd32 = lt.dp / DC;
-      // W = 32 k floats, k | dp/32, PICK_RING * nr * (W + 4) floats fit the stage
-      const int PICK_RING = 2;  // (measured: 3-4 deep with narrower blocks is slower)
+      // whole rows in one block when they fit (one load round trip), else
+      // W = 32 k floats, k | dp/32, in a 2-deep ring of PICK_RING * nr * (W + 4)
+      // floats (measured: 3-4 deep with narrower blocks is slower)
+      const int PICK_RING = nr * (DC * nd32 + 4) <= stage_floats ? 1 : 2;
       int k = 1;
       for (int kk2 = nd32; kk2 >= 1; kk2--)
         if (nd32 % kk2 == 0 && PICK_RING * nr * (DC * kk2 + 4) <= stage_floats) {
@@ -2912,9 +2955,8 @@ __global__ void __launch_bounds__(PICK_THREADS) coarse_pick_kernel(
       float acc = 0.f;
       for (int blk = 0; blk < nblk; blk++) {
         issue(blk + PICK_RING - 1);
-        if (PICK_RING == 4) cp_async_wait<3>();
-        else if (PICK_RING == 3) cp_async_wait<2>();
-        else cp_async_wait<1>();
+        if (PICK_RING == 2) cp_async_wait<1>();
+        else cp_async_wait<0>();
         __syncthreads();
         if (tid < nr) {
           const float* x = rows_st + (blk % PICK_RING) * nr * rs + tid * rs;

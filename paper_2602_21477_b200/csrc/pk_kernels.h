@@ -84,6 +84,9 @@ struct RouteArgs {
   int32_t* slot_off = nullptr;
   int64_t* scanned = nullptr;
   int chunk_rows = 0, smax = 0, bcap = 0;
+  // nonzero: only the probe SET matters (no caller reads the probe order or
+  // keys), so lists certainly in the first nprobe skip the exact re-rank
+  int unordered = 0;
 };
 // Persistent fused scan + per-(query, item) top-kk.
 void launch_scan(int metric, ListTable lt, const ArenaMaps& maps, const float* Qd,
