@@ -1694,7 +1694,8 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                      (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
                      work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
                      S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
-                     pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined, qg);
+                     pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined, qg,
+                     /*overlapped: release some SMs early for the next front half*/ pipelined);
     } else {
       launch_scan_screen(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm2.as<float>(),
                          S.items.as<ScanItem>(), n_items,

@@ -1836,7 +1836,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
                     const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
                     int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
                     int32_t* ccount, int cap, int num_sms, cudaStream_t st, bool pdl,
-                    const CUtensorMap* qgather) {
+                    const CUtensorMap* qgather, bool overlapped) {
   if (max_items <= 0) return;
   if (!qgather && !qsw_ready) qswizzle_kernel<<<num_sms * 4, 256, 0, st>>>(Qd, B, lt.dp, qsw);
   CUtensorMap qg_dummy;
@@ -1855,8 +1855,8 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   if (dbg_times) cudaMallocAsync((void**)&dbg_t, (size_t)grid * 24, st);
   // The first E = 32 CTAs stop claiming items once 70% of them are taken
   // (PK_SCAN_EARLY="E:F" overrides, "0:1" turns it off): the scan itself ends
-  // ~6 us later, but those SMs start the next batch's front half (overlapped
-  // searches) that much sooner -- measured step 500.7 -> 488 us (swept E in
+  // ~6 us later, but those SMs start the next batch's front half that much
+  // sooner (applied only to overlapped searches, where that front half exists) -- measured step 500.7 -> 488 us (swept E in
   // 16-64, F in 0.5-0.95 on one box).
   static int early_ctas = 32;
   static float early_frac = 0.7f;
@@ -1872,7 +1872,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
     launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, qgm, use_qg, lt, (const float*)qsw, \
                (int64_t)B, \
                qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
-               ccount, cap, dbg_skip, dbg_t, early_ctas, early_frac);                              \
+               ccount, cap, dbg_skip, dbg_t, overlapped ? early_ctas : 0, early_frac);            \
   }
   if (metric == SQ_L2) PK_TC(SQ_L2)
   else PK_TC(IP)

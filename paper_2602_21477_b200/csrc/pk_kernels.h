@@ -138,7 +138,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
                     const int32_t* n_items, int max_items, const QPair* qpairs, int kk,
                     int32_t* work_ctr, uint32_t* Uq, uint32_t* slot_hi, int32_t* slot_n, int4* cpool,
                     int32_t* ccount, int cap, int num_sms, cudaStream_t st, bool pdl = true,
-                    const CUtensorMap* qgather = nullptr);
+                    const CUtensorMap* qgather = nullptr, bool overlapped = false);
 
 // Cross-shard merge of R per-shard result blocks (layout: pk_shard_block_bytes
 // in include/pancake_b200.h) into the global top-kk per query.
