@@ -148,9 +148,10 @@ int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, 
  *   switches resident when the copy completes, MigrationTicket phases
  *   tiering.py:332-416), 0 = evict (release the HBM copy).
  * pk_list_residency: 0 cold, 1 resident, 2 admission in flight.
- * pk_tier_stats out[10]: resident lists, cold lists, resident HBM bytes,
+ * pk_tier_stats out[12]: resident lists, cold lists, resident HBM bytes,
  *   lists / bytes staged by the last search, bytes staged in total, searches
- *   that staged, admissions started, admissions completed, host arena bytes. */
+ *   that staged, admissions started, admissions completed, host arena bytes,
+ *   HBM arena rows in use (bump pointer) and allocated. */
 int pk_index_enable_tier(pk_index* ix, int64_t reserve_rows);
 int pk_list_set_resident(pk_index* ix, int64_t cid, int resident);
 int pk_list_residency(pk_index* ix, int64_t cid, int* state);

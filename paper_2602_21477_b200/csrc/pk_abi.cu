@@ -120,6 +120,29 @@ struct Range {
   int64_t off, cap;
 };
 
+// Return [off, off+cap) to a first-fit free list.  The list is kept sorted by
+// offset and coalesced, and a free range that reaches the bump pointer gives
+// its rows back to it, so per-batch staging ranges of varying sizes do not
+// fragment the arena.
+static void free_coalesce(std::vector<Range>& fr, int64_t& top, int64_t off, int64_t cap) {
+  if (cap <= 0) return;
+  auto it = std::lower_bound(fr.begin(), fr.end(), off,
+                             [](const Range& r, int64_t o) { return r.off < o; });
+  it = fr.insert(it, Range{off, cap});
+  if (it + 1 != fr.end() && it->off + it->cap == (it + 1)->off) {
+    it->cap += (it + 1)->cap;
+    fr.erase(it + 1);
+  }
+  if (it != fr.begin() && (it - 1)->off + (it - 1)->cap == it->off) {
+    (it - 1)->cap += it->cap;
+    it = fr.erase(it) - 1;
+  }
+  if (it->off + it->cap == top) {
+    top = it->off;
+    fr.erase(it);
+  }
+}
+
 }  // namespace
 
 // Recursive mutex that counts acquisitions: a search may overlap its front
@@ -275,7 +298,8 @@ struct pk_index {
   cudaStream_t mst = nullptr;        // migration side stream
   std::vector<Range> staged;         // arena ranges of the last batch's cold lists
   cudaEvent_t stage_ev = nullptr;
-  bool stage_pending = false;
+  bool stage_pending = false;   // `staged` holds ranges of an enqueued batch
+  bool stage_recorded = false;  // stage_ev marks the end of the last staging batch
   int64_t st_lists_last = 0, st_rows_last = 0, st_rows_total = 0, st_batches = 0;
   int64_t mig_started = 0, mig_done = 0;
   DevBuf stage_desc, tmp_rows;
@@ -429,14 +453,7 @@ struct pk_index {
     arena_top += cap;
     return PK_OK;
   }
-  void free_range(int64_t off, int64_t cap) {
-    if (cap <= 0) return;
-    if (off + cap == arena_top) {
-      arena_top = off;
-      return;
-    }
-    free_ranges.push_back({off, cap});
-  }
+  void free_range(int64_t off, int64_t cap) { free_coalesce(free_ranges, arena_top, off, cap); }
 
   int grow_slots(int32_t need) {
     int32_t ncap = std::max<int32_t>({need, slot_cap * 2, 64});
@@ -539,18 +556,12 @@ struct pk_index {
     htop += cap;
     return PK_OK;
   }
-  void host_free(int64_t off, int64_t cap) {
-    if (cap <= 0) return;
-    if (off + cap == htop) {
-      htop = off;
-      return;
-    }
-    hfree.push_back({off, cap});
-  }
+  void host_free(int64_t off, int64_t cap) { free_coalesce(hfree, htop, off, cap); }
   // n rows (d floats each, host or device source) into host arena rows at `at`
   // (padded to dp with zeros), ids alongside.
   int host_put(int64_t at, const float* src, const int64_t* src_ids, int64_t n, bool dev) {
     if (n <= 0) return PK_OK;
+    RET(host_fence());
     if (dev) {
       CK(cudaMemcpy2DAsync(hrows + at * dp, dp * 4, src, d * 4, d * 4, n, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(hids + at, src_ids, n * 8, cudaMemcpyDeviceToHost, st));
@@ -593,13 +604,22 @@ struct pk_index {
     mig_list.swap(keep);
     return PK_OK;
   }
-  // Free the previous batch's staging ranges once that batch has finished.
+  // Return the previous batch's staging ranges to the arena.  No host wait:
+  // every later reader / writer of arena rows on the index stream is ordered
+  // after that batch, and the migration stream waits for the index stream
+  // before each admission copy (pk_list_set_resident).
   int release_staged() {
     if (!stage_pending) return PK_OK;
-    CK(cudaEventSynchronize(stage_ev));
     for (const Range& r : staged) free_range(r.off, r.cap);
     staged.clear();
     stage_pending = false;
+    return PK_OK;
+  }
+  // Before the host writes into the pinned host arena: the last batch's
+  // zero-copy gather (or staging DMA) may still be reading it.
+  int host_fence() {
+    if (stage_recorded) CK(cudaEventSynchronize(stage_ev));
+    stage_recorded = false;
     return PK_OK;
   }
   // Stream every cold list probed by the batch into arena staging ranges.
@@ -661,6 +681,11 @@ struct pk_index {
                          (int)dp, st);
     }
     CK(cudaGetLastError());
+    // the batch's device work reads these ranges; the next search frees them
+    // (stream-ordered) and host-arena writers wait for stage_ev
+    CK(cudaEventRecord(stage_ev, st));
+    stage_pending = true;
+    stage_recorded = true;
     return sync_table();
   }
   // Padded device copy of slot s's rows (resident: the arena itself).
@@ -1090,6 +1115,9 @@ int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int3
   if (B == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
   const bool dev = flags & PK_DEVICE_PTRS;
+  // a device merge touches neither the list table nor the search scratch, so
+  // a search -> merge -> search sequence keeps the front-half overlap
+  if (dev && ix->ev_scan && ix->mu.n == ix->ev_scan_n + 2) ix->ev_scan_n++;
   cudaStream_t st = ix->st;
   const int64_t bb = pk_shard_block_bytes(B, kk);
   const void* src = blocks;
@@ -1134,6 +1162,7 @@ int pk_list_append(pk_index* ix, int64_t cid, const float* rows, const int64_t* 
   const int64_t len = ix->h_len[s];
   if (ix->tiered) {
     RET(ix->finish_migration(s, true));
+    RET(ix->host_fence());
     if (len + n > ix->h_hcap[s]) {  // relocate the host copy (x1.5)
       const int64_t ncap = std::max<int64_t>(len + n, ix->h_hcap[s] + ix->h_hcap[s] / 2) + 16;
       int64_t noff;
@@ -1194,6 +1223,7 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
     const int64_t len = ix->h_len[s], m = kv.second;
     if (ix->tiered) {
       RET(ix->finish_migration(s, true));
+      RET(ix->host_fence());
       if (len + m > ix->h_hcap[s]) {
         const int64_t ncap = std::max<int64_t>(len + m, ix->h_hcap[s] + ix->h_hcap[s] / 2) + 16;
         int64_t noff;
@@ -1277,6 +1307,7 @@ int pk_list_remove_row(pk_index* ix, int64_t cid, int64_t row) {
   const int64_t last = len - 1, off = ix->h_off[s];
   if (ix->tiered) {
     RET(ix->finish_migration(s, true));
+    RET(ix->host_fence());
     const int64_t ho = ix->h_hoff[s];
     if (row != last) {
       memcpy(ix->hrows + (ho + row) * ix->dp, ix->hrows + (ho + last) * ix->dp, ix->dp * 4);
@@ -1413,6 +1444,11 @@ int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
     const int64_t cap = len + len / 4 + 16;  // 25% device slack (ref/tiering.py:356)
     int64_t off;
     RET(ix->alloc_range(cap, &off));
+    // the range may have held rows (an evicted list, a finished batch's
+    // staging) that searches already enqueued on the index stream still read
+    CK(cudaEventRecord(ix->stage_ev, ix->st));
+    CK(cudaStreamWaitEvent(ix->mst, ix->stage_ev, 0));
+    ix->stage_recorded = true;
     if (len > 0) {
       CK(cudaMemcpyAsync(ix->rows + off * ix->dp, ix->hrows + ix->h_hoff[s] * ix->dp,
                          (size_t)len * ix->dp * 4, cudaMemcpyHostToDevice, ix->mst));
@@ -1452,7 +1488,7 @@ int pk_list_residency(pk_index* ix, int64_t cid, int* state) {
 
 int pk_tier_stats(pk_index* ix, int64_t* out, int n) {
   std::lock_guard<CountedMutex> lock_(ix->mu);
-  int64_t v[10] = {0};
+  int64_t v[12] = {0};
   if (ix->tiered) RET(ix->poll_migrations());
   for (int32_t s = 0; s < ix->nslots; s++) {
     if (ix->h_cid[s] < 0 || ix->h_remote[s]) continue;
@@ -1470,7 +1506,9 @@ int pk_tier_stats(pk_index* ix, int64_t* out, int n) {
   v[7] = ix->mig_started;
   v[8] = ix->mig_done;
   v[9] = ix->tiered ? ix->hcap * (ix->dp * 4 + 8) : 0;
-  for (int i = 0; i < n && i < 10; i++) out[i] = v[i];
+  v[10] = ix->arena_top;  // HBM arena high-water mark (rows)
+  v[11] = ix->arena_cap;  // HBM arena capacity (rows)
+  for (int i = 0; i < n && i < 12; i++) out[i] = v[i];
   return PK_OK;
 }
 

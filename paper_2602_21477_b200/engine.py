@@ -372,7 +372,11 @@ class Store:
         nprobe = nprobe if nprobe is not None else self.cfg.default_nprobe
         if nprobe < 1:
             raise UsageError("nprobe must be >= 1")
-        if self._agent_path(agent, scopes, k=k):  # per-query pipeline, B calls of search()
+        if self._agent_path(agent, scopes, k=k) or (agent is not None and self.cfg.profiles_enabled):
+            # per-query pipeline, B calls of search(): with agent profiles on,
+            # each query's scan order depends on the profile updates of the
+            # queries before it (ref/engine.py:488-496), so they cannot share
+            # one read phase
             return [self.search(agent, scopes, Q[b], k, nprobe) for b in range(Q.shape[0])]
         with self._serialized(agent):
             self._lock.acquire_read()
@@ -398,7 +402,10 @@ class Store:
         in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
         dev_nprobe = max(1, min(eff_nprobe, in_scope))
         if dev_nprobe > N.NPROBE_MAX:
-            raise UsageError(f"nprobe above {N.NPROBE_MAX} in-scope lists is not supported")
+            # more probed lists than the fused pass selects: the per-query
+            # pipeline (exact centroid order + every probed row) serves it
+            return [self._search_read_phase(agent, scopes, Q[b], k, nprobe, True, True)[0]
+                    for b in range(B)]
         codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
         need_probe = True  # access counters + scan_ids follow the probe order
         out = self.index.search(Q, codes, dev_nprobe, k, want_probe=need_probe)
@@ -474,11 +481,7 @@ class Store:
             selected = []
             if in_scope:
                 dev_nprobe = max(1, min(eff_nprobe, in_scope))
-                if dev_nprobe > N.NPROBE_MAX:
-                    raise UsageError(f"nprobe above {N.NPROBE_MAX} in-scope lists is not supported")
-                codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
-                selected = [int(c) for c in self.index.coarse_cids(q[None, :], codes, dev_nprobe)[0]
-                            if c >= 0]
+                selected = self._coarse_select(q, scopes, dev_nprobe)
             thresh = cache.threshold() if (cache is not None and not exhaustive_edge) else None
             clusters = self.clusters.clusters
             total = sum(clusters[c].size for c in selected)
@@ -513,6 +516,21 @@ class Store:
         extended = self._topk(id_chunks, dist_chunks, max(k, self.cfg.kappa * k))
         scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
         return SearchResult(extended[:k], stats, scan_ids), hint, extended
+
+    def _coarse_select(self, q, scopes, nprobe: int) -> list[int]:
+        """Coarse top-nprobe over the in-scope lists, ordered by (distance,
+        cid) (ref/graph.py:392-396 at exhaustive ef).  Up to NPROBE_MAX lists
+        come from the fused device pick; above it (verify-mode full searches
+        at nlist 8192, ref/engine.py:503-512) the exact distances to every
+        in-scope centroid are computed on the device in one call and ordered."""
+        codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
+        if nprobe <= N.NPROBE_MAX:
+            return [int(c) for c in self.index.coarse_cids(q[None, :], codes, nprobe)[0] if c >= 0]
+        cids = np.asarray(sorted(c for s in scopes for c in self.clusters.by_scope[s]),
+                          dtype=np.int64)
+        cents = np.stack([self.clusters.clusters[int(c)].centroid for c in cids])
+        d = batch_distances(q, cents, self.metric)
+        return cids[np.lexsort((cids, d))][:nprobe].tolist()
 
     def _topk(self, id_chunks, dist_chunks, k):
         """ref/engine.py:406-426: lexsort by (dist, id), first occurrence per

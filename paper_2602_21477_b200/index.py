@@ -265,7 +265,8 @@ class DeviceIndex:
     # ---- cold tier (TierManager residency, ref/tiering.py:175-448) --------
     TIER_STATS = ("resident_lists", "cold_lists", "resident_bytes", "staged_lists_last",
                   "staged_bytes_last", "staged_bytes_total", "staged_searches",
-                  "admissions_started", "admissions_done", "host_arena_bytes")
+                  "admissions_started", "admissions_done", "host_arena_bytes",
+                  "arena_top_rows", "arena_cap_rows")
 
     def enable_tier(self, reserve_rows: int = 0):
         """Cold tier on: lists live in pinned host memory, HBM holds the

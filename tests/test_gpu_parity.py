@@ -479,6 +479,41 @@ def test_large_k_uses_the_per_query_pipeline(pk):
     store.close()
 
 
+def test_nprobe_above_device_pick_limit(pk):
+    """More probed lists than the fused pick selects (NPROBE_MAX = 2048): the
+    exhaustive edge and verify-mode full searches at nlist 8192 probe every
+    list (ref/engine.py:366-369, 503-512).  Store.search and search_batch
+    serve it exactly (this used to raise UsageError)."""
+    from oracle.store_model import StoreModel
+    from paper_2602_21477_b200 import Store, StoreConfig
+
+    rng = np.random.default_rng(13)
+    d, nlist = 16, 2300
+    store = Store(StoreConfig(dimension=d, cache_enabled=False, accelerator="none",
+                              splits_enabled=False, seed=3))
+    model = StoreModel(d, seed=3)
+    lists, nid = [], 0
+    for c in range(nlist):
+        n = int(rng.integers(1, 4))
+        lists.append((np.arange(nid, nid + n, dtype=np.int64),
+                      rng.normal(size=(n, d)).astype(np.float32)))
+        nid += n
+    store.load_lists("static", lists)
+    model.load("static", lists)
+    Q = rng.normal(size=(4, d)).astype(np.float32)
+    for nprobe in (2100, 2300, 5000):
+        res = store.search_batch(None, ["static"], Q, 10, nprobe, want_scan_ids=True)
+        for b in range(len(Q)):
+            hits, scanned, scan_ids = model.search(["static"], Q[b], 10, nprobe)
+            one = store.search(None, ["static"], Q[b], 10, nprobe)
+            for r in (res[b], one):
+                assert r.ids == [h[0] for h in hits]
+                assert np.array_equal(bits(r.distances), bits([h[1] for h in hits]))
+                assert r.stats.scanned_vectors == scanned
+                assert np.array_equal(r.scan_ids, scan_ids)
+    store.close()
+
+
 @pytest.mark.parametrize("n,d,target", [(20000, 48, 1500), (6000, 100, 700)])
 def test_bulk_build_device_kmeans_matches_oracle(pk, n, d, target):
     """bulk_build's k-means with the matrix resident in HBM (seeding distances,

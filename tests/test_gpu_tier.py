@@ -110,3 +110,82 @@ def test_store_trace_with_native_cold_tier(name, budget):
     assert any(m["tier_cold_lists"] > 0 for m in log), "budget never left a list cold"
     assert any(m["tier_resident_lists"] > 0 for m in log), "hotset never admitted a list"
     assert max(m["tier_staged_searches"] for m in log) > 0
+
+
+@pytest.mark.parametrize("mode", ["host", "device", "async"])
+def test_staging_ranges_recycled(mode):
+    """Every tiered batch stages its probed cold lists into HBM arena ranges;
+    those ranges go back to the arena after the batch (they used to
+    leak, so the arena grew by the staged bytes on every search).  Over many
+    batches -- host-pointer, device-pointer and async searches, with host-arena
+    mutations (appends, swap-with-last removals) between them -- the arena's
+    high-water mark stays bounded and every result stays exact."""
+    import torch
+
+    from paper_2602_21477_b200 import DeviceIndex
+
+    rng = np.random.default_rng(5)
+    d, nlist = 64, 40
+    ix = DeviceIndex(d)
+    ix.enable_tier()
+    centers = rng.normal(size=(nlist, d)).astype(np.float32)
+    lists, cents, cids, nid = [], [], [], 0
+    for c in range(nlist):
+        n = int(rng.integers(50, 700))
+        rows = (centers[c] + 0.5 * rng.normal(size=(n, d))).astype(np.float32)
+        ids = np.arange(nid, nid + n, dtype=np.int64)
+        nid += n
+        cents.append(ix.create_list(c, 0, rows, ids))
+        lists.append([ids, rows])
+        cids.append(c)
+    for c in cids[::4]:
+        ix.set_resident(c, True)
+    ix.sync()
+    total_rows = sum(len(x[0]) for x in lists)
+    tops = []
+    dev = torch.device("cuda", 0)
+    for it in range(40):
+        Q = (centers[rng.integers(0, nlist, 32)] + 0.5 * rng.normal(size=(32, d))).astype(np.float32)
+        nprobe = int(rng.integers(3, 12))
+        if mode == "host":
+            out = ix.search(Q, [0], nprobe, 10)
+            ids_g = out.ids
+        elif mode == "device":
+            Qd = torch.from_numpy(Q).to(dev)
+            codes = torch.zeros(1, dtype=torch.int32, device=dev)
+            o_ids = torch.empty(32, 10, dtype=torch.int64, device=dev)
+            o_d = torch.empty(32, 10, dtype=torch.float32, device=dev)
+            o_c = torch.empty(32, 10, dtype=torch.int64, device=dev)
+            o_n = torch.empty(32, dtype=torch.int32, device=dev)
+            o_s = torch.empty(32, dtype=torch.int64, device=dev)
+            ix.search_device(Qd, codes, nprobe, 10, o_ids, o_d, o_c, o_n, o_s)
+            ix.sync()
+            ids_g = o_ids.cpu().numpy()
+        else:
+            t = ix.search_submit(Q, [0], nprobe, 10)
+            ids_g = ix.search_collect(t).ids
+        flat = O.FlatIVF.from_lists([tuple(x) for x in lists], np.stack(cents),
+                                    np.asarray(cids, np.int64))
+        r_ids = flat.search(Q, nprobe, 10, threads=8)[0]
+        assert np.array_equal(ids_g, r_ids), f"batch {it}"
+        # host-arena mutations between batches (the last gather may be in flight)
+        j = int(rng.integers(0, nlist))
+        add = (centers[j] + 0.5 * rng.normal(size=(5, d))).astype(np.float32)
+        aid = np.arange(nid, nid + 5, dtype=np.int64)
+        nid += 5
+        ix.append(cids[j], add, aid)
+        lists[j][0] = np.concatenate([lists[j][0], aid])
+        lists[j][1] = np.concatenate([lists[j][1], add])
+        r = int(rng.integers(0, len(lists[j][0])))
+        ix.remove_row(cids[j], r)
+        last = len(lists[j][0]) - 1
+        lists[j][0][r] = lists[j][0][last]
+        lists[j][1][r] = lists[j][1][last]
+        lists[j][0] = lists[j][0][:last]
+        lists[j][1] = lists[j][1][:last]
+        cents[j] = ix.recompute(cids[j])
+        tops.append(ix.tier_stats()["arena_top_rows"])
+    # resident quarter (+25% slack) plus at most ~two batches of staging
+    assert max(tops) < 3 * total_rows, tops
+    assert max(tops[20:]) <= 1.5 * max(tops[:20]), tops
+    ix.close()
