@@ -72,20 +72,32 @@ class NativeAccelerator:
         self.allocated_bytes = 0
         self.fail_next_alloc = False
         self.fail_next_scan = False
-        self._metric = metric
+        self._metric = _as_metric(metric)
         self._device = device
         self._dimension = dimension
         self._index: DeviceIndex | None = None
         self._next_handle = 0
         self._live: dict[int, int] = {}  # handle -> rows held
+        self._cid: dict[int, int] = {}   # handle -> list id in the shared device index
         self._mem = _MemView(self)
 
-    # ---- device index (created at the first upload: the dimension is the
-    # first matrix's width unless given) ----------------------------------------
+    # ---- device index: one per (device, dimension, metric), shared by every
+    # executor of this process (a TierManager per cluster store, as the
+    # reference's tests build thousands of, must not each pay an index
+    # creation); created at the first upload -- the dimension is the first
+    # matrix's width unless given ---------------------------------------------
+    _shared: dict = {}
+    _next_cid = 0
+
     def _ix(self, d: int) -> DeviceIndex:
         if self._index is None:
             self._dimension = self._dimension or d
-            self._index = DeviceIndex(self._dimension, self._metric.wire_code, self._device)
+            key = (self._device, self._dimension, self._metric)
+            ix = NativeAccelerator._shared.get(key)
+            if ix is None:
+                ix = DeviceIndex(self._dimension, self._metric.wire_code, self._device)
+                NativeAccelerator._shared[key] = ix
+            self._index = ix
         if d != self._dimension:
             raise AcceleratorError(f"dimension mismatch: {d} vs {self._dimension}")
         return self._index
@@ -94,12 +106,13 @@ class NativeAccelerator:
         n = self._live[handle]
         if n == 0 or self._index is None:
             return (np.empty((0, 0), dtype=np.float32), np.empty(0, dtype=np.int64))
-        rows, ids = self._index.read(handle)
+        rows, ids = self._index.read(self._cid[handle])
         return rows, ids
 
     def _drop(self, handle):
-        if self._live.pop(handle, 0) > 0 and self._index is not None:
-            self._index.retire(handle)
+        cid = self._cid.pop(handle, None)
+        if self._live.pop(handle, 0) > 0 and self._index is not None and cid is not None:
+            self._index.retire(cid)
 
     # ---- protocol (ref/tiering.py:101-147) -------------------------------
     def alloc(self, nbytes: int) -> int:
@@ -122,9 +135,12 @@ class NativeAccelerator:
         if len(ids):
             ix = self._ix(mat.shape[1])
             if self._live[handle] == 0:  # first rows: the list comes into existence
-                ix.create_list(handle, 0, mat, ids)
+                cid = NativeAccelerator._next_cid
+                NativeAccelerator._next_cid += 1
+                ix.create_list(cid, 0, mat, ids)
+                self._cid[handle] = cid
             else:
-                ix.append(handle, mat, ids)
+                ix.append(self._cid[handle], mat, ids)
             self._live[handle] += len(ids)
         kb = (self._live[handle] * (self._dimension or 0) * 4) / 1024.0
         rate = self.model.tier_local_per_kb_us if tier_local else self.model.cross_tier_per_kb_us
@@ -148,9 +164,9 @@ class NativeAccelerator:
         self.simulated_us += self.model.accel_scan_us(n)
         if n == 0:
             return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float32)
-        if metric is not self._metric:
+        if _as_metric(metric) is not self._metric:
             raise AcceleratorError(f"index built for {self._metric}, scan asked {metric}")
-        ids, dists, _ = self._index.scan_lists(np.asarray(q, dtype=np.float32), [handle], n)
+        ids, dists, _ = self._index.scan_lists(np.asarray(q, dtype=np.float32), [self._cid[handle]], n)
         return ids, dists
 
     def kmeans(self, mat, k, rng, base_delta):
@@ -160,6 +176,20 @@ class NativeAccelerator:
                                    device=self._device)
 
     def close(self):
-        if self._index is not None:
-            self._index.close()
-            self._index = None
+        """Release every list this executor still holds (the shared device
+        index stays for the other executors)."""
+        for handle in list(self._live):
+            self._drop(handle)
+        self._index = None
+
+    def __del__(self):  # pragma: no cover - garbage collection order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _as_metric(m) -> Metric:
+    """This package's Metric for a Metric of either package (the reference's
+    TierManager passes its own enum members; same values)."""
+    return m if isinstance(m, Metric) else Metric(getattr(m, "value", m))

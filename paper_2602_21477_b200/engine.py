@@ -93,8 +93,8 @@ class StoreConfig:
     device: int = 0
 
     def __post_init__(self):
-        if isinstance(self.metric, str):
-            self.metric = Metric(self.metric)
+        if not isinstance(self.metric, Metric):  # a name, or another package's Metric member
+            self.metric = Metric(getattr(self.metric, "value", self.metric))
         if self.dimension < 1:
             raise UsageError(f"dimension must be >= 1, got {self.dimension}")
         if not 0.0 <= self.alpha_et <= 1.0:
