@@ -19,7 +19,10 @@ plus the observable attributes the reference and its tests read:
 ``allocated_bytes``, ``call_log``, ``simulated_us`` (cost-model accounting,
 unchanged), ``fail_next_alloc`` / ``fail_next_scan`` and ``_mem[handle] ->
 (mat, ids)`` (read back from the device, tiering.py:387-390).  Errors raise
-``AcceleratorError`` as the protocol expects.
+``AcceleratorError`` as the protocol expects -- this package's, or the host's own
+class when given (``error_type``: a maintainer plugging this executor into the
+reference's ``TierManager`` passes ``agentmem.tiering.AcceleratorError``, the
+type its host-fallback handlers catch, ref/tiering.py:308-311, 357-361).
 """
 
 from __future__ import annotations
@@ -65,7 +68,8 @@ class NativeAccelerator:
     capabilities = frozenset({"scan", "kmeans"})
 
     def __init__(self, model: CostModel | None = None, dimension: int | None = None,
-                 metric: Metric = Metric.SQUARED_EUCLIDEAN, device: int = 0):
+                 metric: Metric = Metric.SQUARED_EUCLIDEAN, device: int = 0,
+                 error_type: type = AcceleratorError):
         self.model = model or CostModel()
         self.call_log: list[tuple] = []
         self.simulated_us = 0.0
@@ -73,6 +77,7 @@ class NativeAccelerator:
         self.fail_next_alloc = False
         self.fail_next_scan = False
         self._metric = _as_metric(metric)
+        self._err = error_type
         self._device = device
         self._dimension = dimension
         self._index: DeviceIndex | None = None
@@ -99,7 +104,7 @@ class NativeAccelerator:
                 NativeAccelerator._shared[key] = ix
             self._index = ix
         if d != self._dimension:
-            raise AcceleratorError(f"dimension mismatch: {d} vs {self._dimension}")
+            raise self._err(f"dimension mismatch: {d} vs {self._dimension}")
         return self._index
 
     def _read(self, handle):
@@ -118,7 +123,7 @@ class NativeAccelerator:
     def alloc(self, nbytes: int) -> int:
         if self.fail_next_alloc:
             self.fail_next_alloc = False
-            raise AcceleratorError("allocation failed")
+            raise self._err("allocation failed")
         handle = self._next_handle
         self._next_handle += 1
         self._live[handle] = 0
@@ -129,7 +134,7 @@ class NativeAccelerator:
 
     def upload(self, handle: int, mat: np.ndarray, ids: np.ndarray, tier_local: bool):
         if handle not in self._live:
-            raise AcceleratorError(f"unknown handle {handle}")
+            raise self._err(f"unknown handle {handle}")
         mat = np.ascontiguousarray(mat, dtype=np.float32)
         ids = np.ascontiguousarray(ids, dtype=np.int64)
         if len(ids):
@@ -156,16 +161,16 @@ class NativeAccelerator:
     def scan(self, handle: int, q: np.ndarray, metric: Metric):
         if self.fail_next_scan:
             self.fail_next_scan = False
-            raise AcceleratorError("device scan failed")
+            raise self._err("device scan failed")
         if handle not in self._live:
-            raise AcceleratorError(f"unknown handle {handle}")
+            raise self._err(f"unknown handle {handle}")
         n = self._live[handle]
         self.call_log.append(("scan", handle, n))
         self.simulated_us += self.model.accel_scan_us(n)
         if n == 0:
             return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.float32)
         if _as_metric(metric) is not self._metric:
-            raise AcceleratorError(f"index built for {self._metric}, scan asked {metric}")
+            raise self._err(f"index built for {self._metric}, scan asked {metric}")
         ids, dists, _ = self._index.scan_lists(np.asarray(q, dtype=np.float32), [self._cid[handle]], n)
         return ids, dists
 

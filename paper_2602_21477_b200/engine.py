@@ -91,6 +91,10 @@ class StoreConfig:
     threads: int = 0
     request_window: int = 64
     device: int = 0
+    # new: under torch.distributed (one process per GPU, every rank making the
+    # same calls) the posting lists are partitioned over the ranks' HBM,
+    # agents' lists co-located per rank (sharded.ShardedStoreIndex)
+    sharded: bool = False
 
     def __post_init__(self):
         if not isinstance(self.metric, Metric):  # a name, or another package's Metric member
@@ -212,7 +216,12 @@ class Store:
         self.rng = np.random.default_rng(np.random.PCG64(seed))
         self.metric = cfg.metric
         self.scope_codes = ScopeCodes()
-        self.index = DeviceIndex(cfg.dimension, cfg.metric.wire_code, cfg.device)
+        if cfg.sharded:
+            from .sharded import ShardedStoreIndex
+
+            self.index = ShardedStoreIndex(cfg.dimension, cfg.metric.wire_code, cfg.device)
+        else:
+            self.index = DeviceIndex(cfg.dimension, cfg.metric.wire_code, cfg.device)
         native_tier = cfg.accelerator == "native"
         if native_tier:  # cold tier: pinned host memory, HBM holds the hotset
             self.index.enable_tier()

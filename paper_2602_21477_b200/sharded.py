@@ -331,3 +331,164 @@ class ShardedIndex:
         self.local.combine_search_probed_device(qa, pa, self._epoch)
         self.local.combine_merge_device(self._epoch, out_ids, out_d, out_cid, out_n, out_scanned)
 
+
+
+# ---------------------------------------------------------------- Store behind the shards
+class ShardedStoreIndex:
+    """The device index of a ``Store`` whose clusters AND agents are sharded
+    over the ranks of a process group (BASELINE north_star: "clusters and
+    agents are sharded across the 8 GPUs of one box").
+
+    Every rank runs the same Store (SPMD: the same API calls in the same
+    order), so the host side -- cluster bookkeeping, the coarse graph's RNG
+    draws, caches, hotset policy -- is replicated and stays identical; only
+    the posting-list ROWS are partitioned, each list living in the HBM of
+    one owner rank:
+
+    * agent scopes are co-located: every list of agent scope code ``c`` lives
+      on rank ``(c - 1) % world`` (agents in registration order round-robin);
+    * static lists go to the rank holding the fewest rows at creation
+      (ties: lowest rank) -- greedy size balancing as lists arrive;
+    * centroids are replicated: the owner computes a list's centroid (create,
+      maintenance) and broadcasts it, so every rank's coarse quantizer and
+      ``assign_nearest`` see the same table;
+    * a batched search scans each rank's own probed lists into one shard
+      result block, the blocks are all-gathered and merged by
+      (distance, id) -- the single-index answer (the k smallest of a union
+      lie in the union of the parts' k smallest);
+    * the per-query pipeline's exact per-list scans (``scan_lists``) are run
+      by the owners and exchanged.
+
+    Implements the ``DeviceIndex`` methods the Store / ClusterStore /
+    TierManager call."""
+
+    def __init__(self, dimension: int, metric_code: int, device: int, group=None):
+        self.sh = ShardedIndex(dimension, metric_code, device, group=group)
+        self.local = self.sh.local
+        self.rank, self.world = self.sh.rank, self.sh.world
+        self.dimension = int(dimension)
+        self.device = self.local.device
+        self.owner: dict[int, int] = {}
+        self.nrows: dict[int, int] = {}  # rows per list (host bookkeeping, identical on all ranks)
+        self.rows_on = np.zeros(self.world, dtype=np.int64)
+
+    # ---- placement / replication ------------------------------------------------
+    def _place(self, scope_code: int, n: int) -> int:
+        if scope_code != 0:
+            return (int(scope_code) - 1) % self.world
+        return int(np.argmin(self.rows_on))  # first minimum: lowest rank on ties
+
+    def _bcast_centroid(self, src: int, cent) -> np.ndarray:
+        import torch
+
+        c = np.zeros(self.dimension, dtype=np.float32) if cent is None else np.asarray(cent, np.float32)
+        if self.world > 1:
+            t = torch.from_numpy(c.copy()).to(self.sh.comm_device)
+            g = src if self.sh.group is None else self.sh.dist.get_global_rank(self.sh.group, src)
+            self.sh.dist.broadcast(t, g, group=self.sh.group)
+            c = t.cpu().numpy()
+        return c
+
+    def owner_of(self, cid: int) -> int:
+        return self.owner[int(cid)]
+
+    # ---- posting lists ---------------------------------------------------------
+    def create_list(self, cid: int, scope_code: int, rows, ids) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        r = self._place(scope_code, len(ids))
+        self.owner[int(cid)] = r
+        self.nrows[int(cid)] = len(ids)
+        self.rows_on[r] += len(ids)
+        cent = self.local.create_list(cid, scope_code, rows, ids) if r == self.rank else None
+        cent = self._bcast_centroid(r, cent)
+        if r != self.rank:
+            self.local.add_remote_list(cid, scope_code, cent)
+        return cent
+
+    def append(self, cid: int, rows, ids):
+        r = self.owner[int(cid)]
+        n = len(np.asarray(ids).reshape(-1))
+        self.nrows[int(cid)] += n
+        self.rows_on[r] += n
+        if r == self.rank:
+            self.local.append(cid, rows, ids)
+
+    def remove_row(self, cid: int, row: int):
+        r = self.owner[int(cid)]
+        self.nrows[int(cid)] -= 1
+        self.rows_on[r] -= 1
+        if r == self.rank:
+            self.local.remove_row(cid, row)
+
+    def retire(self, cid: int):
+        r = self.owner.pop(int(cid))
+        self.rows_on[r] -= self.nrows.pop(int(cid))
+        self.local.retire(cid)
+
+    def recompute(self, cid: int) -> np.ndarray:
+        r = self.owner[int(cid)]
+        cent = self.local.recompute(cid) if r == self.rank else None
+        cent = self._bcast_centroid(r, cent)
+        if r != self.rank:
+            self.local.set_centroid(cid, cent)
+        return cent
+
+    def size(self, cid: int) -> int:
+        return self.nrows[int(cid)]
+
+    def read(self, cid: int):
+        """Rows / ids of a list this rank owns."""
+        if self.owner[int(cid)] != self.rank:
+            raise UsageError(f"cluster {cid} lives on rank {self.owner[int(cid)]}")
+        return self.local.read(cid)
+
+    def assign(self, X, scope_code: int):
+        return self.local.assign(X, scope_code)  # replicated centroids: same answer everywhere
+
+    def coarse_cids(self, Q, scope_codes, nprobe: int):
+        return self.local.coarse_cids(Q, scope_codes, nprobe)
+
+    # ---- search ------------------------------------------------------------------
+    def search(self, Q, scope_codes, nprobe: int, kk: int, want_probe: bool = False) -> SearchOutput:
+        out = self.sh.search(Q, scope_codes, nprobe, kk)
+        if want_probe:
+            out.probe = self.local.coarse_cids(Q, scope_codes, nprobe)
+        return out
+
+    def scan_lists(self, q, cids, total: int):
+        """(ids, dists, prefix offsets) of every row of ``cids`` in that order:
+        each owner scans its lists, the pieces are exchanged."""
+        cids = [int(c) for c in cids]
+        mine = [c for c in cids if self.owner[c] == self.rank]
+        ids, dd, pre = self.local.scan_lists(q, mine, sum(self.nrows[c] for c in mine))
+        part = {c: (ids[pre[i]:pre[i + 1]], dd[pre[i]:pre[i + 1]]) for i, c in enumerate(mine)}
+        if self.world > 1:
+            parts = [None] * self.world
+            self.sh.dist.all_gather_object(parts, part, group=self.sh.group)
+            for p in parts:
+                part.update(p)
+        out_ids = [part[c][0] for c in cids]
+        out_d = [part[c][1] for c in cids]
+        pre = np.zeros(len(cids) + 1, dtype=np.int64)
+        pre[1:] = np.cumsum([len(x) for x in out_ids])
+        cat = (lambda xs, dt: np.concatenate(xs) if xs else np.empty(0, dtype=dt))
+        return cat(out_ids, np.int64), cat(out_d, np.float32), pre
+
+    # ---- tier / lifecycle ----------------------------------------------------------
+    def enable_tier(self, reserve_rows: int = 0):
+        raise UsageError("the native cold tier is per GPU; a sharded Store keeps every list in HBM")
+
+    def nbytes(self) -> int:
+        return self.local.nbytes()
+
+    def tier_stats(self) -> dict:
+        return self.local.tier_stats()
+
+    def flush(self):
+        self.local.flush()
+
+    def sync(self):
+        self.local.sync()
+
+    def close(self):
+        self.local.close()

@@ -199,6 +199,10 @@ AGENT_TRACE_SPECS = {
     # pool empties -- its zero centroid has no cosine distance, ref/core.py:106-109)
     "agents_many": dict(d=48, n_base=3000, nlist=24, n_agents=5, n_ops=700, seed=35, k=8,
                         nprobe=4, n_p=6, l0=12, l1=40, window=8, alpha=0.6, verify=False),
+    # the coordinated multi-agent shape of configs[2] scaled to the reference's
+    # CPU speed: 16 agents, k 10, mixed insert / search stream
+    "agents_16": dict(d=64, n_base=6000, nlist=24, n_agents=16, n_ops=1600, seed=36, k=10,
+                      nprobe=4, n_p=8, l0=16, l1=64, window=8, alpha=0.7, verify=False),
 }
 
 

@@ -119,7 +119,10 @@ def replay_store(spec, batch_searches=False, overrides=None, tier_log=None):
     rec["final/live"] = np.array(store.live_count())
     rec["final/rng"] = np.array(store.rng.random())
     # device rows must mirror the host rows exactly
+    owned = getattr(store.index, "owner", None)  # sharded Store: this rank's lists only
     for c in cids:
+        if owned is not None and owned[c] != store.index.rank:
+            continue
         rows, ids = store.index.read(c)
         assert np.array_equal(ids, cl[c].member_ids), f"device ids of cluster {c} diverged"
         assert np.array_equal(rows.view(np.uint32), cl[c].vectors.view(np.uint32)), f"device rows {c}"

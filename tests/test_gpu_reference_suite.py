@@ -93,7 +93,7 @@ def _load_suites():
 
     # the executor plugin: the reference TierManager drives the native executor
     def native_executor(model=None):
-        return NativeAccelerator(model)
+        return NativeAccelerator(model, error_type=ref.tiering.AcceleratorError)
 
     ref.tiering.SimulatedAccelerator = native_executor
 
