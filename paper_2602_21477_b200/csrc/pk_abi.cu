@@ -221,6 +221,7 @@ struct pk_index {
   int par = 0, last_par = 0;
   PinnedBuf hstage;  // append staging (mapped)
   PinnedBuf hsl;     // pk_scan_lists staging (mapped)
+  PinnedBuf hasg;    // pk_assign host path: padded rows in, (cid, dist) out (mapped)
   // front-half overlap: the next batch's prep / coarse / pick / routing run on
   // fst while this batch's scan and re-rank drain on st
   cudaStream_t fst = nullptr;
@@ -961,6 +962,7 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->hout) cudaFreeHost(ix->hout);
   if (ix->hstage.p) cudaFreeHost(ix->hstage.p);
   if (ix->hsl.p) cudaFreeHost(ix->hsl.p);
+  if (ix->hasg.p) cudaFreeHost(ix->hasg.p);
   for (auto& a : ix->aslot) {
     if (a.hblk) cudaFreeHost(a.hblk);
     if (a.copied) cudaEventDestroy(a.copied);
@@ -2199,19 +2201,36 @@ int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64
   RET(ix->assign_dc.ensure((size_t)n * ns * 4));
   RET(ix->assign_c.ensure(n * 8));
   RET(ix->assign_d.ensure(n * 4));
-  CK(cudaMemcpy2DAsync(ix->assign_q.p, dp * 4, X, ix->d * 4, ix->d * 4, n,
-                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  // host path (the insert path's batch of 8): the rows go over in ONE DMA
+  // from pinned staging, padded on the host, and the argmin writes (cid,
+  // dist) straight into mapped pinned memory -- no pageable 2-D copies, no
+  // read-back copies, one synchronisation
+  int64_t* oc = out_cid;
+  float* od = out_dist;
+  if (dev) {
+    CK(cudaMemcpy2DAsync(ix->assign_q.p, dp * 4, X, ix->d * 4, ix->d * 4, n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    const size_t in_b = (size_t)n * dp * 4;
+    RET(ix->hasg.ensure(in_b + (size_t)n * 12));
+    float* hq = reinterpret_cast<float*>(ix->hasg.p);
+    for (int64_t r = 0; r < n; r++) {
+      memcpy(hq + r * dp, X + r * ix->d, ix->d * 4);
+      if (dp > ix->d) memset(hq + r * dp + ix->d, 0, (dp - ix->d) * 4);
+    }
+    CK(cudaMemcpyAsync(ix->assign_q.p, hq, in_b, cudaMemcpyHostToDevice, st));
+    oc = reinterpret_cast<int64_t*>(ix->hasg.dev + in_b);
+    od = reinterpret_cast<float*>(ix->hasg.dev + in_b + (size_t)n * 8);
+  }
   if (ix->metric == COSINE) launch_qnorm(ix->assign_q.as<float>(), dp, (int)n, (int)ix->d, ix->assign_qn.as<float>(), st);
   launch_dist_dense(ix->metric, ix->assign_q.as<float>(), dp, (int)n, ix->d_cent, dp, ix->nslots, (int)dp,
                     ix->assign_qn.as<float>(), ix->assign_dc.as<float>(), ns, st);
-  int64_t* oc = dev ? out_cid : ix->assign_c.as<int64_t>();
-  float* od = dev ? out_dist : ix->assign_d.as<float>();
   launch_argmin(ix->assign_dc.as<float>(), ns, (int)n, ix->table(), scope_code, oc, od, st);
   CK(cudaGetLastError());
   if (!dev) {
-    CK(cudaMemcpyAsync(out_cid, oc, n * 8, cudaMemcpyDeviceToHost, st));
-    if (out_dist) CK(cudaMemcpyAsync(out_dist, od, n * 4, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    const size_t in_b = (size_t)n * dp * 4;
+    memcpy(out_cid, ix->hasg.p + in_b, n * 8);
+    if (out_dist) memcpy(out_dist, ix->hasg.p + in_b + (size_t)n * 8, n * 4);
   }
   return PK_OK;
 }

@@ -747,19 +747,59 @@ class Store:
             if not cands:
                 self.clusters.create_cluster(scope, [(iid, vec)])
                 assigned = None
-            else:
-                if assigned is None:
-                    assigned = self.clusters.assign_nearest_batch(np.stack(vecs[i:]), scope)
-                    assigned_from = i
-                cid = int(assigned[i - assigned_from])
-                self.tier.buffered_insert(cid, iid, vec)
-                if self._after_cluster_mutation(cid):
-                    assigned = None  # a centroid moved: later vectors re-assign
+                if agent is not None:
+                    self._append_sequence(agent, vec)
+                accepted.append(iid)
+                i += 1
+                continue
+            if assigned is None:
+                assigned = self.clusters.assign_nearest_batch(np.stack(vecs[i:]), scope)
+                assigned_from = i
+            # the longest run of vectors whose inserts fire no split and no
+            # maintenance (the reference checks after every vector,
+            # ref/engine.py:647-660): placed together, in order, then the
+            # firing vector's cluster mutates and later vectors re-assign
+            j, fired = self._insert_run(assigned, assigned_from, i, n)
+            run_ids = [iid] + [self._take_id(ids[t] if ids is not None else None)
+                               for t in range(i + 1, j)]
+            for t in range(i + 1, j):
+                p_ = payloads[t]
+                self.payloads[run_ids[t - i]] = p_.encode("utf-8") if isinstance(p_, str) else p_
+            run_cids = assigned[i - assigned_from:j - assigned_from]
+            run_vecs = np.stack(vecs[i:j])
+            run_ids_a = np.asarray(run_ids, dtype=np.int64)
+            for cid in dict.fromkeys(run_cids.tolist()):  # clusters in first-touch order
+                sel = np.flatnonzero(run_cids == cid)
+                self.tier.buffered_insert_many(int(cid), run_ids_a[sel], run_vecs[sel])
+            if fired:
+                self._after_cluster_mutation(int(run_cids[-1]))
+                assigned = None  # a centroid moved: later vectors re-assign
             if agent is not None:
-                self._append_sequence(agent, vec)
-            accepted.append(iid)
-            i += 1
+                for t in range(i, j):
+                    self._append_sequence(agent, vecs[t])
+            accepted.extend(run_ids)
+            i = j
         return accepted
+
+    def _insert_run(self, assigned, base: int, i: int, n: int):
+        """(j, fired): vectors i..j-1 go to their assigned clusters; fired when
+        the insert of vector j-1 makes its cluster split or recompute (the
+        predicates _after_cluster_mutation evaluates after each insert)."""
+        clusters = self.clusters.clusters
+        split_at = self.clusters.split_threshold if self.cfg.splits_enabled else None
+        maint_at = self.clusters.maintenance_interval if self.cfg.lazy_maintenance else None
+        added: dict[int, int] = {}
+        j = i
+        while j < n:
+            cid = int(assigned[j - base])
+            k = added.get(cid, 0) + 1
+            added[cid] = k
+            cl = clusters[cid]
+            j += 1
+            if (split_at is not None and cl.size + k >= split_at) or \
+                    (maint_at is not None and cl.dirty + k >= maint_at):
+                return j, True
+        return j, False
 
     def _take_id(self, explicit) -> int:
         if explicit is None:

@@ -179,6 +179,10 @@ class TierManager:
             return "DirectHost"
         return "DeviceInPlace"
 
+    def buffered_insert_many(self, cid: int, item_ids: np.ndarray, vectors: np.ndarray):
+        """buffered_insert of consecutive items of one cluster."""
+        self.store.add_members(cid, item_ids, vectors)
+
     # --- splitting (ref/tiering.py:420-434) ---
     def split_offload(self, cid: int):
         cl = self.store.clusters[cid]
