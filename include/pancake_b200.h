@@ -244,6 +244,10 @@ int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B);
 /* Lists re-ranked exactly per query by the last search's tensor-core coarse
  * quantizer (host int32[B]). */
 int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B);
+/* Fault injection (the reference's fail_next_alloc seam, tiering.py:101-104,
+ * 357-361): the next n admission allocations (pk_list_set_resident(.., 1))
+ * fail with PK_ERR_NOMEM and leave the list cold and unchanged. */
+int pk_debug_fail_next_alloc(pk_index* ix, int n);
 /* Pool entries that survived the final bound and were re-ranked exactly per
  * query by the last screened search (host int32[B]; -1 = overflow path). */
 int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B);

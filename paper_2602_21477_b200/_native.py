@@ -64,6 +64,7 @@ _SIGS = [
     ("pk_profile_end", [_vp, _vp, _int, _i32p], _int),
     ("pk_debug_pool_counts", [_vp, _vp, _i64], _int),
     ("pk_debug_coarse_counts", [_vp, _vp, _i64], _int),
+    ("pk_debug_fail_next_alloc", [_vp, _int], _int),
     ("pk_debug_rerank_counts", [_vp, _vp, _i64], _int),
     ("pk_search_coarse", [_vp, _vp, _i64, _vp, _i32, _i32, _vp, _int], _int),
     ("pk_search_probed", [_vp, _vp, _i64, _vp, _i32, _i32, _i64, _vp, _int], _int),

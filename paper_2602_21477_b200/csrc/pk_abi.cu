@@ -299,6 +299,7 @@ struct pk_index {
   cudaStream_t mst = nullptr;        // migration side stream
   std::vector<Range> staged;         // arena ranges of the last batch's cold lists
   cudaEvent_t stage_ev = nullptr;
+  int fail_alloc = 0;           // pk_debug_fail_next_alloc
   bool stage_pending = false;   // `staged` holds ranges of an enqueued batch
   bool stage_recorded = false;  // stage_ev marks the end of the last staging batch
   int64_t st_lists_last = 0, st_rows_last = 0, st_rows_total = 0, st_batches = 0;
@@ -1444,6 +1445,10 @@ int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
     // poll once the copy event completes (TierManager.step_migration)
     const int64_t len = ix->h_len[s];
     const int64_t cap = len + len / 4 + 16;  // 25% device slack (ref/tiering.py:356)
+    if (ix->fail_alloc > 0) {
+      ix->fail_alloc--;
+      return fail(PK_ERR_NOMEM, "admission of cluster %lld: injected allocation failure", (long long)cid);
+    }
     int64_t off;
     RET(ix->alloc_range(cap, &off));
     // the range may have held rows (an evicted list, a finished batch's
@@ -2144,6 +2149,12 @@ int pk_debug_rerank_counts(pk_index* ix, int32_t* out, int64_t B) {
   if ((size_t)B * 4 > S.nsurv.bytes) return fail(PK_ERR_USAGE, "batch larger than the last search");
   CK(cudaMemcpyAsync(out, S.nsurv.p, (size_t)B * 4, cudaMemcpyDeviceToHost, ix->st));
   CK(cudaStreamSynchronize(ix->st));
+  return PK_OK;
+}
+
+int pk_debug_fail_next_alloc(pk_index* ix, int n) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  ix->fail_alloc = std::max(n, 0);
   return PK_OK;
 }
 

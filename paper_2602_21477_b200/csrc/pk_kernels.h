@@ -106,6 +106,32 @@ void launch_argmin(const float* D, int64_t ldd, int B, ListTable lt, int32_t sco
 void launch_scatter_rows(const float* src, int64_t lds, const int64_t* src_ids, int n,
                          const int64_t* dst_row, float* dst, int64_t* dst_ids, int dp,
                          cudaStream_t st);
+// ---- hybrid coarse graph (pk_graph.cu): the reference's graph traversal
+constexpr int GRAPH_MAX_SCOPES = 64;
+struct GraphDev {          // slot-indexed, uploaded by pk_graph_set
+  const int8_t* level;     // [ns] node level, -1 = not a graph node
+  const int32_t* nbr0;     // [ns][M] layer-0 neighbors (slots, list order, -1 padded)
+  const int32_t* up_off;   // [ns] offset of the node's layer-1 block in up[]
+  const int32_t* up;       // layers 1..level, M entries each
+  const int32_t* por_off;  // [ns + 1] portal CSR
+  const int32_t* por;      // portal targets (slots, insertion order)
+  int M;
+  int ns;
+};
+struct GraphQuery {        // one batch's scope set
+  const uint8_t* flags;    // [ns] bit0: list in the searched scopes, bit1: in scopes + static
+  int static_entry, static_maxl;  // static graph entry slot (-1: empty)
+  int n_sc;                // searched scopes (any order; the traversal is order-free)
+  int sc_entry[GRAPH_MAX_SCOPES], sc_maxl[GRAPH_MAX_SCOPES];
+  uint8_t sc_static[GRAPH_MAX_SCOPES];
+  int ef, nprobe, mode;    // mode 0: search (hybrid), 1: search_independent (per_agent)
+};
+// probe[b][nprobe] (slots, (d, cid) order, -1 padded), counter[b] = distance
+// computations; D = exact distances [B][ldd] to every slot's centroid.
+// Scratch: stamps [B][ns] u32, hk [B][2 ns + 2] u64, hv [B][2 ns + 2] i32.
+void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, const GraphQuery& gq,
+                         const int64_t* cid, uint32_t* stamps, uint64_t* hk, int32_t* hv, int32_t* probe,
+                         int32_t* counter, cudaStream_t st);
 size_t scan_smem_bytes();
 size_t screen_smem_bytes();
 // Screened persistent scan (sq_l2 / neg_ip): FFMA screen with a proven error

@@ -278,6 +278,10 @@ class DeviceIndex:
         self.flush()
         N.check(N.lib().pk_list_set_resident(self._h, int(cid), 1 if resident else 0))
 
+    def fail_next_alloc(self, n: int = 1):
+        """Fault injection: the next n admissions fail (pk_debug_fail_next_alloc)."""
+        N.check(N.lib().pk_debug_fail_next_alloc(self._h, int(n)))
+
     def residency(self, cid: int) -> int:
         """0 cold, 1 HBM-resident, 2 admission in flight."""
         self.flush()

@@ -95,6 +95,8 @@ class TierManager:
         self._hot: set[int] = set()
         self.resident_bytes = 0
         self.flush_count = 0
+        self.aborted = 0
+        self._fail_next = False
         self.migration_us: list[float] = []
 
     # --- frequency tracking (ref/tiering.py:210-218) ---
@@ -151,11 +153,33 @@ class TierManager:
             self._admit(cid)
         return actions
 
+    @property
+    def fail_next_alloc(self) -> bool:
+        return self._fail_next
+    @fail_next_alloc.setter
+    def fail_next_alloc(self, v: bool):
+        """The reference's fault-injection seam (``accel.fail_next_alloc``,
+        ref/tiering.py:101-104): the next admission's HBM allocation fails in
+        the device index (pk_debug_fail_next_alloc)."""
+        self._fail_next = bool(v)
+        if self.native:
+            self.index.fail_next_alloc(1 if v else 0)
+
     def _admit(self, cid: int):
+        """Pending -> Allocated -> Copying -> Switching (device side stream);
+        an allocation failure aborts the admission (ref/tiering.py:357-361,
+        404-416): the list stays cold with every item, searches unaffected."""
         cl = self.store.clusters[cid]
         nbytes = int(cl.size * cl.dimension * 4 * (1 + self.slack_fraction))
-        self.index.set_resident(cid, True)
+        try:
+            self.index.set_resident(cid, True)
+        except AcceleratorError:
+            self._fail_next = False
+            self.aborted += 1
+            return
+        self._fail_next = False
         cl.resident = ResidentCopy(cid, cl.member_ids.copy(), nbytes)
+        cl.buffer_pending = 0
         self.resident_bytes += nbytes
         self._hot.add(cid)
 
@@ -177,11 +201,28 @@ class TierManager:
         cl = self.store.clusters[cid]
         if self.native and cl.resident is None:
             return "DirectHost"
+        self._count_flushes(cl, 1)
         return "DeviceInPlace"
 
     def buffered_insert_many(self, cid: int, item_ids: np.ndarray, vectors: np.ndarray):
         """buffered_insert of consecutive items of one cluster."""
         self.store.add_members(cid, item_ids, vectors)
+        cl = self.store.clusters[cid]
+        if not (self.native and cl.resident is None):
+            self._count_flushes(cl, len(item_ids))
+
+    def _count_flushes(self, cl, n: int):
+        """``buffer_flush_count`` keeps the reference's meaning on the native
+        tier: the reference buffers inserts into a resident cluster and flushes
+        them to the device every ``b_insert`` (ref/tiering.py:280-290); here
+        the rows reach HBM in place, and a flush is counted at each
+        ``b_insert``-th insert into a resident list."""
+        if not self.native:
+            return
+        cl.buffer_pending = getattr(cl, "buffer_pending", 0) + n
+        while cl.buffer_pending >= self.b_insert:
+            cl.buffer_pending -= self.b_insert
+            self.flush_count += 1
 
     # --- splitting (ref/tiering.py:420-434) ---
     def split_offload(self, cid: int):
@@ -209,6 +250,7 @@ class TierManager:
         out = {
             "residency_ratio": ratio,
             "buffer_flush_count": self.flush_count,
+            "aborted_admissions": self.aborted,
             "migration_us": list(self.migration_us),
             "resident_bytes": self.resident_bytes if self.native else sum(c.nbytes for c in live),
             "host_us": 0.0,

@@ -189,3 +189,48 @@ def test_staging_ranges_recycled(mode):
     assert max(tops) < 3 * total_rows, tops
     assert max(tops[20:]) <= 1.5 * max(tops[:20]), tops
     ix.close()
+
+
+def test_native_admission_abort_and_flush_count():
+    """The native tier's counterparts of the reference's fault seam and flush
+    criterion (ref/tiering.py:280-290, 357-361, 404-416; pkg/tests
+    test_acceptance.py:256-266): an injected admission-allocation failure
+    aborts the admission -- the cluster stays cold with all of its items and
+    searches stay exact -- and the next hotset pass admits it; inserts into a
+    resident cluster count a flush exactly at every b_insert-th insert."""
+    from paper_2602_21477_b200 import Store, StoreConfig
+
+    rng = np.random.default_rng(9)
+    d = 16
+    store = Store(StoreConfig(dimension=d, accelerator="native", budget_bytes=1 << 30,
+                              cache_enabled=False, splits_enabled=False, hotset_interval=1 << 30))
+    base = rng.normal(size=(400, d)).astype(np.float32)
+    store.load_lists("static", [(np.arange(i * 100, (i + 1) * 100), base[i * 100:(i + 1) * 100])
+                                for i in range(4)])
+    tier = store.tier
+    for c in store.clusters.clusters:
+        tier.record_access(c)
+    tier.fail_next_alloc = True
+    tier.hotset_update()  # first admission aborts, the other three go in
+    assert tier.aborted == 1 and not tier.fail_next_alloc
+    cold = [c for c, cl in store.clusters.clusters.items() if cl.resident is None]
+    assert len(cold) == 1
+    assert store.index.residency(cold[0]) == 0 and store.clusters.clusters[cold[0]].size == 100
+    q = rng.normal(size=d).astype(np.float32)
+    res = store.search(None, ["static"], q, 10, 4)
+    dd = O.distances(q, base)
+    want = np.lexsort((np.arange(400), dd))[:10]
+    assert res.ids == want.tolist()
+    assert np.array_equal(bits(res.distances), bits(dd[want]))
+    tier.hotset_update()  # retried: admitted now
+    assert all(cl.resident is not None for cl in store.clusters.clusters.values())
+    assert tier.metrics()["aborted_admissions"] == 1
+    # flush equivalent: every b_insert-th insert into a resident list
+    target = next(iter(store.clusters.clusters))
+    cent = store.clusters.clusters[target].centroid
+    assert tier.flush_count == 0
+    for i in range(1, tier.b_insert + 1):
+        v = (cent + 1e-3 * rng.normal(size=d)).astype(np.float32)
+        store.insert(None, "static", [v])
+        assert tier.flush_count == (1 if i >= tier.b_insert else 0), i
+    store.close()
