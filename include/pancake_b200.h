@@ -244,6 +244,37 @@ int pk_debug_pool_counts(pk_index* ix, int32_t* out, int64_t B);
 /* Lists re-ranked exactly per query by the last search's tensor-core coarse
  * quantizer (host int32[B]). */
 int pk_debug_coarse_counts(pk_index* ix, int32_t* out, int64_t B);
+/* ---- the reference's hybrid coarse graph (ref/graph.py:74-422) ----------
+ * The Store keeps the per-scope graphs (levels, neighbor lists, portals) on
+ * the host exactly as the reference builds them, with every distance taken
+ * from pk_centroid_dists; pk_graph_set uploads them; pk_search_graph is
+ * pk_search whose coarse stage is the reference's traversal
+ * (HybridGraphIndex.search, mode 0, or search_independent, mode 1) at the
+ * given ef, so the probed lists equal the reference's at ANY ef, and
+ * out_coarse[b] = its distance-computation count (SearchStats.coarse_computations).
+ *
+ * pk_graph_set: n nodes; node i has cid node_cid[i], level node_level[i] and
+ *   (level + 1) * M neighbor cids in nbr (layer 0 first, list order, -1
+ *   padded), portals por[por_ptr[i] .. por_ptr[i + 1]) in insertion order;
+ *   per scope code: entry cid (-1 none) and max level.  The graph must be
+ *   re-uploaded after any list create / retire (PK_ERR_USAGE otherwise).
+ * pk_search_graph: scope codes are HOST pointers; the rest as pk_search.
+ * pk_graph_probe: coarse only (host): probed cids [B][nprobe] (-1 padded) and counts.
+ * pk_centroid_dists: out[n][nslots] = reference distance of each host row
+ *   V[n][d] to every slot's centroid; out_cids[nslots] = slot cids (-1 free).
+ * pk_list_slot / pk_slot_count: slot of a list, and the slot count. */
+int pk_graph_set(pk_index* ix, int32_t M, int64_t n, const int64_t* node_cid, const int32_t* node_level,
+                 const int64_t* nbr, const int64_t* por_ptr, const int64_t* por, int32_t static_code,
+                 int32_t nsc, const int32_t* sc_code, const int64_t* sc_entry, const int32_t* sc_maxl);
+int pk_search_graph(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                    int32_t nscopes, int32_t nprobe, int32_t ef, int32_t mode, int32_t kk,
+                    int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
+                    int64_t* out_probe, int64_t* out_scanned, int32_t* out_coarse, int flags);
+int pk_graph_probe(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes, int32_t nscopes,
+                   int32_t nprobe, int32_t ef, int32_t mode, int64_t* out_cids, int32_t* out_coarse);
+int pk_centroid_dists(pk_index* ix, const float* V, int64_t n, float* out, int64_t* out_cids);
+int pk_list_slot(pk_index* ix, int64_t cid, int32_t* slot);
+int pk_slot_count(pk_index* ix, int32_t* n);
 /* Fault injection (the reference's fail_next_alloc seam, tiering.py:101-104,
  * 357-361): the next n admission allocations (pk_list_set_resident(.., 1))
  * fail with PK_ERR_NOMEM and leave the list cold and unchanged. */

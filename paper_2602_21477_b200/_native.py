@@ -85,6 +85,13 @@ _SIGS = [
     ("pk_list_add_remote", [_vp, _i64, _i32, _vp], _int),
     ("pk_shard_block_bytes", [_i64, _i32], _i64),
     ("pk_merge_shards", [_vp, _vp, _i32, _i64, _i32, _vp, _vp, _vp, _vp, _vp, _int], _int),
+    ("pk_graph_set", [_vp, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp], _int),
+    ("pk_search_graph", [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp,
+                         _vp, _vp, _int], _int),
+    ("pk_graph_probe", [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _vp, _vp], _int),
+    ("pk_centroid_dists", [_vp, _vp, _i64, _vp, _vp], _int),
+    ("pk_list_slot", [_vp, _i64, _i32p], _int),
+    ("pk_slot_count", [_vp, _i32p], _int),
 ]
 STAGES = ("input", "coarse_dist", "coarse_select", "route", "scan", "merge_out")
 EXPORTED = [s[0] for s in _SIGS]

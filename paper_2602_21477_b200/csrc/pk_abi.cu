@@ -300,6 +300,24 @@ struct pk_index {
   std::vector<Range> staged;         // arena ranges of the last batch's cold lists
   cudaEvent_t stage_ev = nullptr;
   int fail_alloc = 0;           // pk_debug_fail_next_alloc
+  uint64_t slot_ver = 0;        // bumped whenever a slot's cid changes (create / retire)
+  // ---- hybrid coarse graph (pk_graph_set / pk_search_graph): slot-indexed
+  // device copy of the reference's per-scope graphs + portals
+  struct Graph {
+    bool set = false;
+    int M = 0;
+    int32_t ns = 0;          // slot count the arrays were built for
+    uint64_t slot_ver = 0;   // slot <-> cid map version they were built against
+    int32_t static_code = 0;
+    DevBuf level, nbr0, up_off, up, por_off, por, rank, slot_of_rank, flags, stamps, heap, count;
+    std::unordered_map<int32_t, std::pair<int32_t, int32_t>> entry;  // scope code -> (slot, max level)
+    std::vector<uint8_t> hflags;
+    void release() {
+      for (DevBuf* b : {&level, &nbr0, &up_off, &up, &por_off, &por, &rank, &slot_of_rank, &flags,
+                        &stamps, &heap, &count})
+        b->release();
+    }
+  } graph;
   bool stage_pending = false;   // `staged` holds ranges of an enqueued batch
   bool stage_recorded = false;  // stage_ev marks the end of the last staging batch
   int64_t st_lists_last = 0, st_rows_last = 0, st_rows_total = 0, st_batches = 0;
@@ -954,6 +972,7 @@ int pk_index_destroy(pk_index* ix) {
   cudaFree(ix->d_cnrm);
   cudaFree(ix->d_chi);
   cudaFree(ix->d_clo);
+  ix->graph.release();
   for (cudaEvent_t e : ix->prof_ev) cudaEventDestroy(e);
   if (ix->mst) cudaStreamSynchronize(ix->mst);
   for (cudaEvent_t e : ix->mig_ev)
@@ -1060,6 +1079,7 @@ int pk_list_create(pk_index* ix, int64_t cid, int32_t scope_code, const float* r
   ix->h_scope[s] = scope_code;
   ix->h_remote[s] = 0;
   ix->cid2slot[cid] = s;
+  ix->slot_ver++;
   ix->mark(s);
   launch_centroid(crow, ix->dp, n, (int)ix->dp, ix->d_cent + (int64_t)s * ix->dp, ix->st);
   ix->centroid_norm(s);
@@ -1093,6 +1113,7 @@ int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const floa
   ix->h_remote[s] = 1;
   ix->h_res[s] = 1;  // never staged: no rows here
   ix->cid2slot[cid] = s;
+  ix->slot_ver++;
   ix->mark(s);
   CK(cudaMemcpyAsync(ix->d_cent + (int64_t)s * ix->dp, centroid, ix->d * 4, cudaMemcpyHostToDevice,
                      ix->st));
@@ -1352,6 +1373,7 @@ int pk_list_retire(pk_index* ix, int64_t cid) {
   ix->h_scope[s] = -1;
   ix->h_remote[s] = 0;
   ix->cid2slot.erase(cid);
+  ix->slot_ver++;
   ix->free_slots.push_back(s);
   ix->mark(s);
   return PK_OK;
@@ -1524,14 +1546,91 @@ int pk_tier_stats(pk_index* ix, int64_t* out, int n) {
 // One batched search through the stages of pk_search.  probe_in (list
 // handles, [B][nprobe]) skips the coarse stage; probe_out stops after it.
 // in_dev / dev: input / output pointers are device pointers.
+// Coarse stage by the reference's graph traversal instead of the flat
+// top-nprobe (pk_search_graph): exact distances of every query to every
+// list centroid (the values the reference's _dist returns), then the
+// traversal kernel (pk_graph.cu).  `codes` are host scope codes.
+struct GraphArgs {
+  int32_t ef = 0, mode = 0;
+  int32_t* out_coarse = nullptr;  // [B] distance computations (host unless coarse_dev)
+  bool coarse_dev = false;
+};
+static int graph_coarse(pk_index* ix, pk_index::Scratch& S, int64_t B, const int32_t* codes,
+                        int32_t nscopes, int32_t nprobe, const GraphArgs& ga, cudaStream_t fs) {
+  pk_index::Graph& G = ix->graph;
+  if (!G.set) return fail(PK_ERR_USAGE, "no coarse graph uploaded (pk_graph_set)");
+  if (G.ns != ix->nslots || G.slot_ver != ix->slot_ver)
+    return fail(PK_ERR_USAGE, "the coarse graph is stale: lists changed since pk_graph_set");
+  const int32_t ns = std::max<int32_t>(ix->nslots, 1);
+  const int64_t dp = ix->dp;
+  RET(S.dc.ensure((size_t)B * ns * 4));
+  launch_dist_dense(ix->metric, S.q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
+                    S.qnorm.as<float>(), S.dc.as<float>(), ns, fs);
+  GraphQuery gq = {};
+  G.hflags.assign(ns, 0);
+  for (int32_t sl = 0; sl < ix->nslots; sl++) {
+    if (ix->h_cid[sl] < 0) continue;
+    const int32_t c = ix->h_scope[sl];
+    uint8_t f = c == G.static_code ? 2 : 0;
+    for (int i = 0; i < nscopes; i++)
+      if (codes[i] == c) f = 3;
+    G.hflags[sl] = f;
+  }
+  RET(G.flags.ensure(ns));
+  CK(cudaMemcpyAsync(G.flags.p, G.hflags.data(), ns, cudaMemcpyHostToDevice, fs));
+  gq.flags = G.flags.as<uint8_t>();
+  gq.static_entry = -1;
+  auto st_it = G.entry.find(G.static_code);
+  if (st_it != G.entry.end()) {
+    gq.static_entry = st_it->second.first;
+    gq.static_maxl = st_it->second.second;
+  }
+  gq.n_sc = nscopes;
+  for (int i = 0; i < nscopes; i++) {
+    auto it = G.entry.find(codes[i]);
+    gq.sc_entry[i] = it == G.entry.end() ? -1 : it->second.first;
+    gq.sc_maxl[i] = it == G.entry.end() ? 0 : it->second.second;
+    gq.sc_static[i] = codes[i] == G.static_code;
+  }
+  gq.ef = std::max(ga.ef, nprobe);
+  gq.nprobe = nprobe;
+  gq.mode = ga.mode;
+  GraphDev gd;
+  gd.level = G.level.as<int8_t>();
+  gd.nbr0 = G.nbr0.as<int32_t>();
+  gd.up_off = G.up_off.as<int32_t>();
+  gd.up = G.up.as<int32_t>();
+  gd.por_off = G.por_off.as<int32_t>();
+  gd.por = G.por.as<int32_t>();
+  gd.rank = G.rank.as<int32_t>();
+  gd.slot_of_rank = G.slot_of_rank.as<int32_t>();
+  gd.M = G.M;
+  gd.ns = ns;
+  if (graph_smem_bytes(ns, false) > 227 * 1024) {  // per-query state in global memory
+    RET(G.stamps.ensure((size_t)B * ns * 4));
+    RET(G.heap.ensure((size_t)B * (2 * ns + 2) * 8));
+  }
+  RET(G.count.ensure((size_t)B * 4));
+  launch_graph_search(S.dc.as<float>(), ns, (int)B, gd, gq, G.stamps.as<uint32_t>(), G.heap.as<uint64_t>(),
+                      S.probe.as<int32_t>(), G.count.as<int32_t>(), fs);
+  CK(cudaGetLastError());
+  if (ga.out_coarse)
+    CK(cudaMemcpyAsync(ga.out_coarse, G.count.p, (size_t)B * 4,
+                       ga.coarse_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, fs));
+  return PK_OK;
+}
+
 static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
                        int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids,
                        float* out_dists, int64_t* out_cids, int32_t* out_n, int64_t* out_probe,
                        int64_t* out_scanned, bool in_dev, bool dev, const int32_t* probe_in,
-                       int32_t* probe_out, bool host_scopes = false) {
+                       int32_t* probe_out, bool host_scopes = false, const GraphArgs* ga = nullptr) {
   if (B < 0) return fail(PK_ERR_USAGE, "negative batch");
   if (nprobe < 1) return fail(PK_ERR_USAGE, "nprobe must be >= 1");
-  if (nprobe > 2048) return fail(PK_ERR_USAGE, "nprobe %d above the device limit 2048", nprobe);
+  // the fused pick and the scan stages take up to 2048 probes; the graph
+  // traversal's coarse-only output (pk_graph_probe) has no such limit
+  if (nprobe > 2048 && !(ga && probe_out))
+    return fail(PK_ERR_USAGE, "nprobe %d above the device limit 2048", nprobe);
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
   if (!probe_in && (nscopes < 1 || nscopes > 64))
     return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
@@ -1555,7 +1654,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // that scan and its re-rank drain.  Safe because the front writes only
   // this batch's scratch set (the other parity's), and nothing but searches
   // touched the index since (lock count; table unchanged).
-  const bool pipelined = ix->pipeline && dev && in_dev && !probe_in && !probe_out && !ix->tiered &&
+  const bool pipelined = ix->pipeline && dev && in_dev && !probe_in && !probe_out && !ix->tiered && !ga &&
                          !ix->prof && ix->screen && ix->tensor && ix->coarse_tc && !table_dirty &&
                          ix->ev_scan && ix->mu.n == ix->ev_scan_n + 1;
   cudaStream_t fs = st;
@@ -1597,7 +1696,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   int32_t* lcount = S.counts.as<int32_t>();
   int32_t* n_items = lcount + ns;
   int32_t* work_ctr = lcount + ns + 1;
-  const bool use_tc = ix->coarse_tc && !probe_in;
+  const bool use_tc = ix->coarse_tc && !probe_in && !ga;
   // one fused prep kernel (padded copy, norms, TF32 split, swizzled copies,
   // counter resets) on the screened paths; plain copies otherwise
   const bool prep = ix->screen || use_tc;
@@ -1651,6 +1750,9 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   if (probe_in) {
     CK(cudaMemcpyAsync(S.probe.p, probe_in, (size_t)B * nprobe * 4,
                        in_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
+    PROF(2);
+  } else if (ga) {
+    RET(graph_coarse(ix, S, B, scope_codes, nscopes, nprobe, *ga, fs));
     PROF(2);
   } else if (ix->coarse_tc) {
     RET(S.ncand.ensure(B * 4));
@@ -2069,6 +2171,160 @@ int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t
   RET(search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr,
                   nullptr, nullptr, false, false, nullptr, pr.data()));
   for (size_t i = 0; i < (size_t)B * nprobe; i++) out_cids[i] = pr[i] >= 0 ? ix->h_cid[pr[i]] : -1;
+  return PK_OK;
+}
+
+int pk_graph_set(pk_index* ix, int32_t M, int64_t n, const int64_t* node_cid, const int32_t* node_level,
+                 const int64_t* nbr, const int64_t* por_ptr, const int64_t* por, int32_t static_code,
+                 int32_t nsc, const int32_t* sc_code, const int64_t* sc_entry, const int32_t* sc_maxl) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (M < 1 || n < 0 || nsc < 0) return fail(PK_ERR_USAGE, "bad graph shape");
+  CK(cudaSetDevice(ix->device));
+  pk_index::Graph& G = ix->graph;
+  const int32_t ns = std::max<int32_t>(ix->nslots, 1);
+  auto slot = [&](int64_t c, int32_t* out) -> int { return ix->slot_of(c, out); };
+  std::vector<int8_t> level(ns, -1);
+  std::vector<int32_t> nbr0((size_t)ns * M, -1), up_off(ns, 0), up, por_off(ns + 1, 0), porv;
+  std::vector<std::vector<int32_t>> por_of(ns);
+  // rank: position of each live slot's cid among the live cids (heap tie order)
+  std::vector<std::pair<int64_t, int32_t>> live;
+  for (int32_t sl = 0; sl < ix->nslots; sl++)
+    if (ix->h_cid[sl] >= 0) live.push_back({ix->h_cid[sl], sl});
+  std::sort(live.begin(), live.end());
+  std::vector<int32_t> rank(ns, 0), sor(ns, 0);
+  for (size_t r = 0; r < live.size(); r++) {
+    rank[live[r].second] = (int32_t)r;
+    sor[r] = live[r].second;
+  }
+  int64_t pos = 0;
+  for (int64_t i = 0; i < n; i++) {
+    int32_t sl;
+    RET(slot(node_cid[i], &sl));
+    const int32_t L = node_level[i];
+    if (L < 0 || L > 126) return fail(PK_ERR_USAGE, "node level %d out of range", L);
+    level[sl] = (int8_t)L;
+    for (int32_t layer = 0; layer <= L; layer++) {
+      for (int32_t j = 0; j < M; j++) {
+        const int64_t c = nbr[pos + (int64_t)layer * M + j];
+        int32_t t = -1;
+        if (c >= 0) RET(slot(c, &t));
+        if (layer == 0) nbr0[(size_t)sl * M + j] = t;
+        else up.push_back(t);
+      }
+      if (layer == 0 && L > 0) up_off[sl] = (int32_t)up.size();
+    }
+    pos += (int64_t)(L + 1) * M;
+    for (int64_t k = por_ptr[i]; k < por_ptr[i + 1]; k++) {
+      int32_t t;
+      RET(slot(por[k], &t));
+      por_of[sl].push_back(t);
+    }
+  }
+  for (int32_t sl = 0; sl < ns; sl++) {
+    por_off[sl + 1] = por_off[sl] + (int32_t)por_of[sl].size();
+    porv.insert(porv.end(), por_of[sl].begin(), por_of[sl].end());
+  }
+  G.entry.clear();
+  for (int32_t i = 0; i < nsc; i++) {
+    if (sc_entry[i] < 0) continue;
+    int32_t t;
+    RET(slot(sc_entry[i], &t));
+    G.entry[sc_code[i]] = {t, sc_maxl[i]};
+  }
+  auto put = [&](DevBuf& b, const void* src, size_t bytes) -> int {
+    RET(b.ensure(std::max<size_t>(bytes, 4)));
+    if (bytes) CK(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ix->st));
+    return PK_OK;
+  };
+  RET(put(G.level, level.data(), level.size()));
+  RET(put(G.nbr0, nbr0.data(), nbr0.size() * 4));
+  RET(put(G.up_off, up_off.data(), up_off.size() * 4));
+  RET(put(G.up, up.data(), up.size() * 4));
+  RET(put(G.por_off, por_off.data(), por_off.size() * 4));
+  RET(put(G.por, porv.data(), porv.size() * 4));
+  RET(put(G.rank, rank.data(), rank.size() * 4));
+  RET(put(G.slot_of_rank, sor.data(), sor.size() * 4));
+  CK(cudaStreamSynchronize(ix->st));  // pageable sources
+  G.M = M;
+  G.ns = ix->nslots;
+  G.slot_ver = ix->slot_ver;
+  G.static_code = static_code;
+  G.set = true;
+  return PK_OK;
+}
+
+int pk_search_graph(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
+                    int32_t nscopes, int32_t nprobe, int32_t ef, int32_t mode, int32_t kk,
+                    int64_t* out_ids, float* out_dists, int64_t* out_cids, int32_t* out_n,
+                    int64_t* out_probe, int64_t* out_scanned, int32_t* out_coarse, int flags) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (mode != 0 && mode != 1) return fail(PK_ERR_USAGE, "graph mode must be 0 (hybrid) or 1 (per-scope)");
+  const bool dev = flags & PK_DEVICE_PTRS;
+  GraphArgs ga;
+  ga.ef = ef;
+  ga.mode = mode;
+  ga.out_coarse = out_coarse;
+  ga.coarse_dev = dev;
+  return search_core(ix, Q, B, scope_codes, nscopes, nprobe, kk, out_ids, out_dists, out_cids, out_n,
+                     out_probe, out_scanned, dev, dev, nullptr, nullptr, /*host_scopes=*/true, &ga);
+}
+
+int pk_graph_probe(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes, int32_t nscopes,
+                   int32_t nprobe, int32_t ef, int32_t mode, int64_t* out_cids, int32_t* out_coarse) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (!out_cids) return fail(PK_ERR_USAGE, "out_cids is required");
+  if (mode != 0 && mode != 1) return fail(PK_ERR_USAGE, "graph mode must be 0 (hybrid) or 1 (per-scope)");
+  GraphArgs ga;
+  ga.ef = ef;
+  ga.mode = mode;
+  ga.out_coarse = out_coarse;
+  std::vector<int32_t> pr((size_t)std::max<int64_t>(B, 0) * std::max(nprobe, 1));
+  RET(search_core(ix, Q, B, scope_codes, nscopes, nprobe, 1, nullptr, nullptr, nullptr, nullptr, nullptr,
+                  nullptr, false, false, nullptr, pr.data(), true, &ga));
+  for (size_t i = 0; i < (size_t)B * nprobe; i++) out_cids[i] = pr[i] >= 0 ? ix->h_cid[pr[i]] : -1;
+  return PK_OK;
+}
+
+int pk_centroid_dists(pk_index* ix, const float* V, int64_t n, float* out, int64_t* out_cids) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (n < 0) return fail(PK_ERR_USAGE, "negative count");
+  CK(cudaSetDevice(ix->device));
+  const int32_t ns = ix->nslots;
+  if (out_cids)
+    for (int32_t sl = 0; sl < ns; sl++) out_cids[sl] = ix->h_cid[sl];
+  if (n == 0 || ns == 0) return PK_OK;
+  cudaStream_t st = ix->st;
+  const int64_t dp = ix->dp;
+  RET(ix->sync_table());
+  const size_t in_b = (size_t)n * dp * 4, out_b = (size_t)n * ns * 4;
+  RET(ix->hasg.ensure(in_b + out_b));
+  float* hq = reinterpret_cast<float*>(ix->hasg.p);
+  for (int64_t r = 0; r < n; r++) {
+    memcpy(hq + r * dp, V + r * ix->d, ix->d * 4);
+    if (dp > ix->d) memset(hq + r * dp + ix->d, 0, (dp - ix->d) * 4);
+  }
+  RET(ix->assign_q.ensure(in_b));
+  RET(ix->assign_qn.ensure((size_t)n * 4));
+  RET(ix->assign_dc.ensure(out_b));
+  CK(cudaMemcpyAsync(ix->assign_q.p, hq, in_b, cudaMemcpyHostToDevice, st));
+  if (ix->metric == COSINE) launch_qnorm(ix->assign_q.as<float>(), dp, (int)n, (int)ix->d, ix->assign_qn.as<float>(), st);
+  launch_dist_dense(ix->metric, ix->assign_q.as<float>(), dp, (int)n, ix->d_cent, dp, ns, (int)dp,
+                    ix->assign_qn.as<float>(), ix->assign_dc.as<float>(), ns, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(ix->hasg.p + in_b, ix->assign_dc.p, out_b, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out, ix->hasg.p + in_b, out_b);
+  return PK_OK;
+}
+
+int pk_list_slot(pk_index* ix, int64_t cid, int32_t* slot) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  return ix->slot_of(cid, slot);
+}
+
+int pk_slot_count(pk_index* ix, int32_t* n) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  *n = ix->nslots;
   return PK_OK;
 }
 

@@ -37,125 +37,147 @@ namespace {
 constexpr unsigned FULLW = 0xffffffffu;
 constexpr uint32_t EMIT = 0xfffffffeu;  // stamp: member of an emitted set (per-scope mode)
 
-__device__ __forceinline__ uint64_t kmin(uint32_t dk, int64_t cid) {  // (d, cid) ascending
-  return ((uint64_t)dk << 32) | (uint32_t)cid;
-}
-__device__ __forceinline__ uint64_t kworst(uint32_t dk, int64_t cid) {  // max = largest d, smallest cid
-  return ((uint64_t)dk << 32) | (uint32_t)(~(uint32_t)cid);
+// Heap keys: (order-preserving f32 bits of d) << 32 | rank, where rank is the
+// position of the list's cid among the live cids (pk_graph_set), so key order
+// is (d, cid) order and the low half names the node.
+__device__ __forceinline__ uint64_t kmin(uint32_t dk, uint32_t rank) { return ((uint64_t)dk << 32) | rank; }
+// result heap (max-heap): largest d first, ties to the SMALLEST cid
+__device__ __forceinline__ uint64_t kworst(uint32_t dk, uint32_t rank) {
+  return ((uint64_t)dk << 32) | (uint32_t)(~rank);
 }
 
-// Binary heaps in global scratch (one thread).
+// Binary heaps of 64-bit keys (one thread; shared memory when it fits).
 struct MinHeap {
   uint64_t* k;
-  int32_t* v;
   int n;
-  __device__ void push(uint64_t key, int32_t val) {
+  __device__ void push(uint64_t key) {
     int i = n++;
     while (i > 0) {
       const int p = (i - 1) >> 1;
-      if (k[p] <= key) break;
-      k[i] = k[p];
-      v[i] = v[p];
+      const uint64_t kp = k[p];
+      if (kp <= key) break;
+      k[i] = kp;
       i = p;
     }
     k[i] = key;
-    v[i] = val;
   }
-  __device__ void pop(uint64_t* key, int32_t* val) {
-    *key = k[0];
-    *val = v[0];
+  __device__ uint64_t pop() {
+    const uint64_t top = k[0];
     const uint64_t lk = k[--n];
-    const int32_t lv = v[n];
     int i = 0;
     for (;;) {
       int c = 2 * i + 1;
       if (c >= n) break;
-      if (c + 1 < n && k[c + 1] < k[c]) c++;
-      if (lk <= k[c]) break;
-      k[i] = k[c];
-      v[i] = v[c];
+      uint64_t kc = k[c];
+      if (c + 1 < n) {
+        const uint64_t k1 = k[c + 1];
+        if (k1 < kc) {
+          kc = k1;
+          c++;
+        }
+      }
+      if (lk <= kc) break;
+      k[i] = kc;
       i = c;
     }
-    if (n > 0) {
-      k[i] = lk;
-      v[i] = lv;
-    }
+    if (n > 0) k[i] = lk;
+    return top;
   }
 };
 struct MaxHeap {
   uint64_t* k;
-  int32_t* v;
   int n;
-  __device__ void push(uint64_t key, int32_t val) {
+  __device__ void push(uint64_t key) {
     int i = n++;
     while (i > 0) {
       const int p = (i - 1) >> 1;
-      if (k[p] >= key) break;
-      k[i] = k[p];
-      v[i] = v[p];
+      const uint64_t kp = k[p];
+      if (kp >= key) break;
+      k[i] = kp;
       i = p;
     }
     k[i] = key;
-    v[i] = val;
   }
   __device__ void pop() {
     const uint64_t lk = k[--n];
-    const int32_t lv = v[n];
     int i = 0;
     for (;;) {
       int c = 2 * i + 1;
       if (c >= n) break;
-      if (c + 1 < n && k[c + 1] > k[c]) c++;
-      if (lk >= k[c]) break;
-      k[i] = k[c];
-      v[i] = v[c];
+      uint64_t kc = k[c];
+      if (c + 1 < n) {
+        const uint64_t k1 = k[c + 1];
+        if (k1 > kc) {
+          kc = k1;
+          c++;
+        }
+      }
+      if (lk >= kc) break;
+      k[i] = kc;
       i = c;
     }
-    if (n > 0) {
-      k[i] = lk;
-      v[i] = lv;
-    }
+    if (n > 0) k[i] = lk;
   }
   __device__ uint32_t worst_dk() const { return (uint32_t)(k[0] >> 32); }
 };
 
 struct Walk {
-  const float* drow;     // exact distances of this query to every slot
+  const float* drow;      // exact distances of this query to every slot
   const GraphDev* g;
-  const int64_t* cid;    // slot -> cluster id
-  uint32_t* stamp;       // [ns] visit stamps of this query
+  uint32_t* stamp;        // [ns] visit stamps of this query
   MinHeap cand;
   MaxHeap best;
   int counter;
   __device__ uint32_t dk(int s) const { return f2key(drow[s]); }
-  // neighbors of slot s at `layer` (M entries, -1 padded)
+  __device__ uint32_t rk(int s) const { return (uint32_t)g->rank[s]; }
+  __device__ int slot_of(uint64_t key) const { return g->slot_of_rank[(uint32_t)key]; }
   __device__ const int32_t* nbrs(int s, int layer) const {
     return layer == 0 ? g->nbr0 + (int64_t)s * g->M : g->up + g->up_off[s] + (int64_t)(layer - 1) * g->M;
   }
-  // ref/graph.py:125-156 on one scope graph; entries already in best / cand /
-  // stamped with `ep`.  Leaves the result set in `best`.
-  __device__ void search_layer(int layer, int ef, uint32_t ep) {
-    while (cand.n > 0) {
-      uint64_t ck;
-      int32_t c;
-      cand.pop(&ck, &c);
-      const uint32_t cdk = (uint32_t)(ck >> 32);
-      if (best.n > 0 && cdk > best.worst_dk() && best.n >= ef) break;
-      if (layer > g->level[c]) continue;
-      const int32_t* nb = nbrs(c, layer);
-      for (int j = 0; j < g->M; j++) {
-        const int32_t x = nb[j];
-        if (x < 0) break;
-        if (stamp[x] == ep) continue;
+  __device__ void seed(int s, uint32_t ep) {
+    stamp[s] = ep;
+    const uint32_t k = dk(s);
+    cand.push(kmin(k, rk(s)));
+    best.push(kworst(k, rk(s)));
+  }
+  // visit the links of one expanded node in order (the per-link body of
+  // ref/graph.py:146-155 and :381-390); `n` links, x(j) the j-th
+  template <typename LinkF>
+  __device__ void visit(int n, LinkF link, int ef, uint32_t ep) {
+    for (int j0 = 0; j0 < n; j0 += 8) {
+      // the distances of up to 8 links are independent loads: issue together
+      int xs[8];
+      uint32_t ks[8];
+#pragma unroll
+      for (int u = 0; u < 8; u++) xs[u] = j0 + u < n ? link(j0 + u) : -1;
+#pragma unroll
+      for (int u = 0; u < 8; u++) ks[u] = xs[u] >= 0 ? dk(xs[u]) : 0u;
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int x = xs[u];
+        if (x < 0 || stamp[x] == ep) continue;
         stamp[x] = ep;
         counter++;
-        const uint32_t xk = dk(x);
-        if (best.n < ef || xk < best.worst_dk()) {
-          cand.push(kmin(xk, cid[x]), x);
-          best.push(kworst(xk, cid[x]), x);
+        if (best.n < ef || ks[u] < best.worst_dk()) {
+          cand.push(kmin(ks[u], rk(x)));
+          best.push(kworst(ks[u], rk(x)));
           if (best.n > ef) best.pop();
         }
       }
+    }
+  }
+  // ref/graph.py:125-156 on one scope graph; entries already seeded with `ep`.
+  // Leaves the result set in `best`.
+  __device__ void search_layer(int layer, int ef, uint32_t ep) {
+    while (cand.n > 0) {
+      const uint64_t ck = cand.pop();
+      if (best.n > 0 && (uint32_t)(ck >> 32) > best.worst_dk() && best.n >= ef) break;
+      const int c = slot_of(ck);
+      if (layer > g->level[c]) continue;
+      const int32_t* nb = nbrs(c, layer);
+      int m = 0;
+      while (m < g->M && nb[m] >= 0) m++;
+      visit(m, [&](int j) { return (int)nb[j]; }, ef, ep);
     }
   }
   // greedy descent through layers maxl..1 from `entry` (ef = 1); returns the slot
@@ -164,38 +186,43 @@ struct Walk {
     for (int layer = maxl; layer >= 1; layer--) {
       const uint32_t ep = ++(*epoch);
       cand.n = best.n = 0;
-      stamp[cur] = ep;
-      const uint32_t ck = dk(cur);
-      cand.push(kmin(ck, cid[cur]), cur);
-      best.push(kworst(ck, cid[cur]), cur);
+      seed(cur, ep);
       search_layer(layer, 1, ep);
-      cur = best.v[0];  // the single best element
+      cur = slot_of(~best.k[0] & 0xffffffffull);  // the single result element
     }
     return cur;
   }
 };
 
+// dynamic shared memory per CTA (one query): stamps u32[ns], two heaps u64[ns + 1],
+// and the distance row f32[ns] when `smem_row`
 __global__ void __launch_bounds__(32) graph_search_kernel(const float* __restrict__ D, int64_t ldd,
-                                                          GraphDev g, GraphQuery gq, const int64_t* cid,
-                                                          uint32_t* stamps, uint64_t* hk, int32_t* hv,
+                                                          GraphDev g, GraphQuery gq, int smem_heaps,
+                                                          int smem_row, uint32_t* gstamps, uint64_t* gheap,
                                                           int32_t* probe, int32_t* counter_out) {
+  extern __shared__ __align__(16) uint8_t sm[];
   const int b = blockIdx.x, lane = threadIdx.x;
   const int ns = g.ns;
-  uint32_t* stamp = stamps + (int64_t)b * ns;
-  for (int s = lane; s < ns; s += 32) stamp[s] = 0;
+  uint64_t* heaps = smem_heaps ? reinterpret_cast<uint64_t*>(sm) : gheap + (int64_t)b * (2 * ns + 2);
+  uint32_t* stamp = smem_heaps ? reinterpret_cast<uint32_t*>(sm + (size_t)(2 * ns + 2) * 8)
+                               : gstamps + (int64_t)b * ns;
+  const float* drow_g = D + (int64_t)b * ldd;
+  float* srow = reinterpret_cast<float*>(sm + (size_t)(2 * ns + 2) * 8 + (size_t)ns * 4);
+  for (int s = lane; s < ns; s += 32) {
+    stamp[s] = 0;
+    if (smem_row) srow[s] = drow_g[s];
+  }
   __syncwarp();
   uint32_t emit = 0;
   if (lane == 0) {
     Walk w;
-    w.drow = D + (int64_t)b * ldd;
+    w.drow = smem_row ? srow : drow_g;
     w.g = &g;
-    w.cid = cid;
     w.stamp = stamp;
     // candidate heap: at most one push per node; result heap: <= nodes + 1
-    w.cand.k = hk + (int64_t)b * (2 * ns + 2);
-    w.cand.v = hv + (int64_t)b * (2 * ns + 2);
-    w.best.k = w.cand.k + ns + 1;
-    w.best.v = w.cand.v + ns + 1;
+    w.cand.k = heaps;
+    w.best.k = heaps + ns + 1;
+    w.cand.n = w.best.n = 0;
     w.counter = 0;
     // ef above the node count behaves as "never full" (best <= visited <= ns)
     const int ef = min(gq.ef, ns);
@@ -217,38 +244,22 @@ __global__ void __launch_bounds__(32) graph_search_kernel(const float* __restric
       }
       const uint32_t ep = ++epoch;
       w.cand.n = w.best.n = 0;
-      for (int i = 0; i < nseeds; i++) {
-        const int s = seeds[i];
-        if (stamp[s] == ep) continue;
-        stamp[s] = ep;
-        const uint32_t k = w.dk(s);
-        w.cand.push(kmin(k, cid[s]), s);
-        w.best.push(kworst(k, cid[s]), s);
-      }
+      for (int i = 0; i < nseeds; i++)
+        if (stamp[seeds[i]] != ep) w.seed(seeds[i], ep);
       while (w.cand.n > 0) {
-        uint64_t ck;
-        int32_t c;
-        w.cand.pop(&ck, &c);
-        const uint32_t cdk = (uint32_t)(ck >> 32);
-        if (w.best.n > 0 && cdk > w.best.worst_dk() && w.best.n >= ef) break;
+        const uint64_t ck = w.cand.pop();
+        if (w.best.n > 0 && (uint32_t)(ck >> 32) > w.best.worst_dk() && w.best.n >= ef) break;
+        const int c = w.slot_of(ck);
         if (g.level[c] < 0) continue;
         const int32_t* nb = g.nbr0 + (int64_t)c * g.M;
-        int m0 = 0;
-        while (m0 < g.M && nb[m0] >= 0) m0++;
+        int m = 0;
+        while (m < g.M && nb[m] >= 0) m++;
         const int p0 = g.por_off[c], np = g.por_off[c + 1] - p0;
-        for (int j = 0; j < m0 + np; j++) {  // links = neighbors[0] + expanded portals, in order
-          const int32_t x = j < m0 ? nb[j] : g.por[p0 + j - m0];
-          if (j >= m0 && !(gq.flags[x] & 2)) continue;
-          if (stamp[x] == ep) continue;
-          stamp[x] = ep;
-          w.counter++;
-          const uint32_t xk = w.dk(x);
-          if (w.best.n < ef || xk < w.best.worst_dk()) {
-            w.cand.push(kmin(xk, cid[x]), x);
-            w.best.push(kworst(xk, cid[x]), x);
-            if (w.best.n > ef) w.best.pop();
-          }
-        }
+        // links = neighbors[0] + the portals into expanded scopes, in order
+        w.visit(m + np, [&](int j) {
+          const int x = j < m ? (int)nb[j] : (int)g.por[p0 + j - m];
+          return (j < m || (gq.flags[x] & 2)) ? x : -1;
+        }, ef, ep);
       }
       emit = ep;  // emitted: every node this frontier visited (the reference's dists dict)
     } else {
@@ -261,12 +272,9 @@ __global__ void __launch_bounds__(32) graph_search_kernel(const float* __restric
         const int top = w.descend(e, gq.sc_maxl[i], &epoch);
         const uint32_t ep = ++epoch;
         w.cand.n = w.best.n = 0;
-        stamp[top] = ep;
-        const uint32_t k = w.dk(top);
-        w.cand.push(kmin(k, cid[top]), top);
-        w.best.push(kworst(k, cid[top]), top);
+        w.seed(top, ep);
         w.search_layer(0, ef, ep);
-        for (int t = 0; t < w.best.n; t++) stamp[w.best.v[t]] = EMIT;
+        for (int t = 0; t < w.best.n; t++) stamp[w.slot_of(~w.best.k[t] & 0xffffffffull)] = EMIT;
       }
       emit = EMIT;
     }
@@ -275,45 +283,57 @@ __global__ void __launch_bounds__(32) graph_search_kernel(const float* __restric
   __syncwarp();  // lane 0's stamps visible to the warp
   emit = __shfl_sync(FULLW, emit, 0);
   // top-nprobe of the emitted in-scope nodes by (d, cid): repeated warp minima
-  const float* drow = D + (int64_t)b * ldd;
+  const float* drow = smem_row ? srow : drow_g;
   uint64_t last = 0;
   for (int p = 0; p < gq.nprobe; p++) {
     uint64_t mk = ~0ull;
-    int ms = -1;
     for (int s = lane; s < ns; s += 32) {
       if (stamp[s] != emit || !(gq.flags[s] & 1)) continue;
-      const uint64_t k = kmin(f2key(drow[s]), cid[s]);
+      const uint64_t k = kmin(f2key(drow[s]), (uint32_t)g.rank[s]);
       if (p > 0 && k <= last) continue;
-      if (k < mk) {
-        mk = k;
-        ms = s;
-      }
+      mk = k < mk ? k : mk;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const uint64_t k2 = __shfl_xor_sync(FULLW, mk, o);
-      const int s2 = __shfl_xor_sync(FULLW, ms, o);
-      if (k2 < mk) {
-        mk = k2;
-        ms = s2;
-      }
+      mk = k2 < mk ? k2 : mk;
     }
-    if (ms < 0) {  // fewer emitted nodes than nprobe: pad
+    if (mk == ~0ull) {  // fewer emitted nodes than nprobe: pad
       for (int r = p + lane; r < gq.nprobe; r += 32) probe[(int64_t)b * gq.nprobe + r] = -1;
       break;
     }
-    if (lane == 0) probe[(int64_t)b * gq.nprobe + p] = ms;
+    if (lane == 0) probe[(int64_t)b * gq.nprobe + p] = g.slot_of_rank[(uint32_t)mk];
     last = mk;
   }
 }
 
 }  // namespace
 
+size_t graph_smem_bytes(int ns, bool row) {
+  return (size_t)(2 * ns + 2) * 8 + (size_t)ns * 4 + (row ? (size_t)ns * 4 : 0);
+}
+
 void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, const GraphQuery& gq,
-                         const int64_t* cid, uint32_t* stamps, uint64_t* hk, int32_t* hv, int32_t* probe,
-                         int32_t* counter, cudaStream_t st) {
+                         uint32_t* gstamps, uint64_t* gheap, int32_t* probe, int32_t* counter,
+                         cudaStream_t st) {
   if (B <= 0) return;
-  graph_search_kernel<<<B, 32, 0, st>>>(D, ldd, g, gq, cid, stamps, hk, hv, probe, counter);
+  constexpr size_t SMEM_MAX = 227 * 1024;
+  int heaps = 1, row = 1;
+  size_t smem = graph_smem_bytes(g.ns, true);
+  if (smem > SMEM_MAX) {
+    row = 0;
+    smem = graph_smem_bytes(g.ns, false);
+  }
+  if (smem > SMEM_MAX) {
+    heaps = 0;
+    smem = 16;
+  }
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(graph_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX);
+    attr = SMEM_MAX;
+  }
+  graph_search_kernel<<<B, 32, smem, st>>>(D, ldd, g, gq, heaps, row, gstamps, gheap, probe, counter);
 }
 
 }  // namespace pk

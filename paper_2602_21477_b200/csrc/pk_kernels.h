@@ -115,6 +115,8 @@ struct GraphDev {          // slot-indexed, uploaded by pk_graph_set
   const int32_t* up;       // layers 1..level, M entries each
   const int32_t* por_off;  // [ns + 1] portal CSR
   const int32_t* por;      // portal targets (slots, insertion order)
+  const int32_t* rank;     // [ns] position of the slot's cid among the live cids (tie order)
+  const int32_t* slot_of_rank;  // [ns]
   int M;
   int ns;
 };
@@ -128,10 +130,12 @@ struct GraphQuery {        // one batch's scope set
 };
 // probe[b][nprobe] (slots, (d, cid) order, -1 padded), counter[b] = distance
 // computations; D = exact distances [B][ldd] to every slot's centroid.
-// Scratch: stamps [B][ns] u32, hk [B][2 ns + 2] u64, hv [B][2 ns + 2] i32.
+// Global scratch (used only when the per-query state exceeds shared memory):
+// stamps [B][ns] u32, heaps [B][2 ns + 2] u64.
 void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, const GraphQuery& gq,
-                         const int64_t* cid, uint32_t* stamps, uint64_t* hk, int32_t* hv, int32_t* probe,
-                         int32_t* counter, cudaStream_t st);
+                         uint32_t* gstamps, uint64_t* gheap, int32_t* probe, int32_t* counter,
+                         cudaStream_t st);
+size_t graph_smem_bytes(int ns, bool row);
 size_t scan_smem_bytes();
 size_t screen_smem_bytes();
 // Screened persistent scan (sq_l2 / neg_ip): FFMA screen with a proven error

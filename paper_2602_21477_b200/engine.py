@@ -228,8 +228,10 @@ class Store:
         self.clusters = ClusterStore(
             cfg.dimension, cfg.metric, self.rng, self.index, self.scope_codes,
             split_threshold=cfg.split_threshold, split_target=cfg.split_target,
-            maintenance_interval=cfg.maintenance_interval,
+            maintenance_interval=cfg.maintenance_interval, m=cfg.m,
+            ef_search_factor=cfg.ef_search_factor, alpha_ic=cfg.alpha_ic,
         )
+        self.graph = self.clusters.graph
         self.runner = TaskRunner(cfg.threads)
         self.tier = TierManager(self.clusters, self.index, budget_bytes=cfg.budget_bytes,
                                 b_insert=cfg.b_insert, decay_half_life=cfg.decay_half_life,
@@ -399,25 +401,34 @@ class Store:
                 self._tick()
             return results
 
+    def _coarse_plan(self, k, nprobe):
+        """(eff_nprobe, ef, mode) of the coarse traversal (ref/engine.py:365-373,
+        ref/graph.py:338-340): the exhaustive edge probes every list with
+        ef = eff_nprobe * ef_search_factor."""
+        eff_nprobe, ef_search = nprobe, None
+        if k >= self.clusters.live_count():
+            eff_nprobe = max(nprobe, len(self.clusters.clusters) or 1)
+            ef_search = eff_nprobe * self.cfg.ef_search_factor
+        mode = 1 if self.cfg.coarse_mode == "per_agent" else 0
+        return eff_nprobe, min(self.graph.ef_for(eff_nprobe, ef_search), 1 << 30), mode
+
     def _search_read_phase_batch(self, agent, scopes, Q, k, nprobe, want_scan_ids):
         """Store._search_read_phase (ref/engine.py:319-404) for a batch on the
-        bare path: staged scan, coarse top-nprobe (flat == graph at exhaustive
-        ef), merged scan of every probed list, _topk (ref/engine.py:406-426)."""
+        bare path: the reference's graph traversal as the coarse stage (any
+        ef), merged scan of every probed list and _topk (ref/engine.py:406-426)
+        in one device pass (pk_search_graph)."""
         B = Q.shape[0]
-        exhaustive_edge = k >= self.clusters.live_count()
-        eff_nprobe = nprobe
-        if exhaustive_edge:
-            eff_nprobe = max(nprobe, len(self.clusters.clusters) or 1)
+        eff_nprobe, ef, mode = self._coarse_plan(k, nprobe)
         in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
         dev_nprobe = max(1, min(eff_nprobe, in_scope))
-        if dev_nprobe > N.NPROBE_MAX:
-            # more probed lists than the fused pass selects: the per-query
-            # pipeline (exact centroid order + every probed row) serves it
+        if dev_nprobe > N.NPROBE_MAX or not self.clusters.clusters:
+            # more probed lists than the fused pass scans (or no lists at
+            # all): the per-query pipeline serves it
             return [self._search_read_phase(agent, scopes, Q[b], k, nprobe, True, True)[0]
                     for b in range(B)]
         codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
-        need_probe = True  # access counters + scan_ids follow the probe order
-        out = self.index.search(Q, codes, dev_nprobe, k, want_probe=need_probe)
+        self.graph.upload()
+        out, coarse = self.index.search_graph(Q, codes, dev_nprobe, k, ef, mode, want_probe=True)
         results = []
         clusters = self.clusters.clusters
         for b in range(B):
@@ -426,7 +437,8 @@ class Store:
             dd = out.dists[b, :n].tolist()
             cs = out.cids[b, :n].tolist()
             hits = [(ids[i], dd[i], clusters[cs[i]].scope) for i in range(n)]
-            stats = SearchStats(scanned_vectors=int(out.scanned[b]), coarse_computations=in_scope,
+            stats = SearchStats(scanned_vectors=int(out.scanned[b]),
+                                coarse_computations=int(coarse[b]),
                                 level_reached="L2", early_terminated=False)
             probe = [c for c in out.probe[b].tolist() if c >= 0]
             scan_chunks = []
@@ -482,15 +494,13 @@ class Store:
                 dist_chunks.append(d)
                 scan_chunks.append(ids)
                 stats.scanned_vectors += len(ids)
-            eff_nprobe = nprobe
-            if exhaustive_edge:
-                eff_nprobe = max(nprobe, len(self.clusters.clusters) or 1)
+            eff_nprobe, ef, mode = self._coarse_plan(k, nprobe)
             in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
-            stats.coarse_computations = in_scope
             selected = []
-            if in_scope:
+            if self.clusters.clusters:
                 dev_nprobe = max(1, min(eff_nprobe, in_scope))
-                selected = self._coarse_select(q, scopes, dev_nprobe)
+                selected, stats.coarse_computations = self._coarse_select(q, scopes, dev_nprobe, ef,
+                                                                          mode)
             thresh = cache.threshold() if (cache is not None and not exhaustive_edge) else None
             clusters = self.clusters.clusters
             total = sum(clusters[c].size for c in selected)
@@ -526,20 +536,14 @@ class Store:
         scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
         return SearchResult(extended[:k], stats, scan_ids), hint, extended
 
-    def _coarse_select(self, q, scopes, nprobe: int) -> list[int]:
-        """Coarse top-nprobe over the in-scope lists, ordered by (distance,
-        cid) (ref/graph.py:392-396 at exhaustive ef).  Up to NPROBE_MAX lists
-        come from the fused device pick; above it (verify-mode full searches
-        at nlist 8192, ref/engine.py:503-512) the exact distances to every
-        in-scope centroid are computed on the device in one call and ordered."""
+    def _coarse_select(self, q, scopes, nprobe: int, ef: int, mode: int):
+        """The reference's coarse traversal for one query (HybridGraphIndex.
+        search / search_independent, ref/graph.py:321-422) on the device:
+        (probed cids in (distance, cid) order, distance computations)."""
         codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
-        if nprobe <= N.NPROBE_MAX:
-            return [int(c) for c in self.index.coarse_cids(q[None, :], codes, nprobe)[0] if c >= 0]
-        cids = np.asarray(sorted(c for s in scopes for c in self.clusters.by_scope[s]),
-                          dtype=np.int64)
-        cents = np.stack([self.clusters.clusters[int(c)].centroid for c in cids])
-        d = batch_distances(q, cents, self.metric)
-        return cids[np.lexsort((cids, d))][:nprobe].tolist()
+        self.graph.upload()
+        cids, coarse = self.index.graph_probe(q[None, :], codes, nprobe, ef, mode)
+        return [int(c) for c in cids[0] if c >= 0], int(coarse[0])
 
     def _topk(self, id_chunks, dist_chunks, k):
         """ref/engine.py:406-426: lexsort by (dist, id), first occurrence per

@@ -238,6 +238,83 @@ class DeviceIndex:
                                   N.ptr(out_d), N.ptr(out_cid), N.ptr(out_n), None,
                                   N.ptr(out_scanned), N.PK_DEVICE_PTRS))
 
+    # ---- the reference's hybrid coarse graph (pk_graph_*) -----------------------
+    def graph_set(self, M: int, node_cids, node_levels, nbr, por_ptr, por, static_code: int,
+                  scope_codes, scope_entries, scope_maxl):
+        self.flush()
+        arr = lambda a, t: np.ascontiguousarray(a, dtype=t)  # noqa: E731
+        nc, nl, nb = arr(node_cids, np.int64), arr(node_levels, np.int32), arr(nbr, np.int64)
+        pp, pv = arr(por_ptr, np.int64), arr(por, np.int64)
+        sc, se, sm = arr(scope_codes, np.int32), arr(scope_entries, np.int64), arr(scope_maxl, np.int32)
+        N.check(N.lib().pk_graph_set(self._h, int(M), len(nc), N.ptr(nc), N.ptr(nl), N.ptr(nb), N.ptr(pp),
+                                     N.ptr(pv), int(static_code), len(sc), N.ptr(sc), N.ptr(se), N.ptr(sm)))
+
+    def search_graph(self, Q, scope_codes, nprobe: int, kk: int, ef: int, mode: int = 0,
+                     want_probe: bool = False):
+        """pk_search with the reference's graph traversal as the coarse stage;
+        returns (SearchOutput, coarse distance computations i32[B])."""
+        self.flush()
+        Q = N.f32(Q, self.dimension)
+        B = Q.shape[0]
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        ids = np.empty((B, kk), dtype=np.int64)
+        dd = np.empty((B, kk), dtype=np.float32)
+        cids = np.empty((B, kk), dtype=np.int64)
+        cnt = np.empty(B, dtype=np.int32)
+        probe = np.empty((B, nprobe), dtype=np.int64) if want_probe else None
+        scanned = np.empty(B, dtype=np.int64)
+        coarse = np.empty(B, dtype=np.int32)
+        N.check(N.lib().pk_search_graph(self._h, N.ptr(Q), B, N.ptr(codes), len(codes), int(nprobe),
+                                        int(ef), int(mode), int(kk), N.ptr(ids), N.ptr(dd), N.ptr(cids),
+                                        N.ptr(cnt), N.ptr(probe), N.ptr(scanned), N.ptr(coarse), 0))
+        return SearchOutput(ids, dd, cids, cnt, probe, scanned), coarse
+
+    def search_graph_block(self, Q, scope_codes, nprobe: int, kk: int, ef: int, mode: int = 0):
+        """search_graph written as one shard result block (host uint8) plus the
+        probe cids and coarse counts (the sharded Store)."""
+        from .sharded import block_views
+
+        self.flush()
+        Q = N.f32(Q, self.dimension)
+        B = Q.shape[0]
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        blk = np.zeros(block_bytes(B, kk), dtype=np.uint8)
+        ids, cids, scanned, dd, cnt = block_views(blk, B, kk)
+        probe = np.empty((B, nprobe), dtype=np.int64)
+        coarse = np.empty(B, dtype=np.int32)
+        N.check(N.lib().pk_search_graph(self._h, N.ptr(Q), B, N.ptr(codes), len(codes), int(nprobe),
+                                        int(ef), int(mode), int(kk), N.ptr(ids), N.ptr(dd), N.ptr(cids),
+                                        N.ptr(cnt), N.ptr(probe), N.ptr(scanned), N.ptr(coarse), 0))
+        return blk, probe, coarse
+
+    def graph_probe(self, Q, scope_codes, nprobe: int, ef: int, mode: int = 0):
+        """Graph coarse stage only: (probed cids i64[B, nprobe], counts i32[B])."""
+        self.flush()
+        Q = N.f32(Q, self.dimension)
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        out = np.empty((Q.shape[0], nprobe), dtype=np.int64)
+        coarse = np.empty(Q.shape[0], dtype=np.int32)
+        N.check(N.lib().pk_graph_probe(self._h, N.ptr(Q), Q.shape[0], N.ptr(codes), len(codes), int(nprobe),
+                                       int(ef), int(mode), N.ptr(out), N.ptr(coarse)))
+        return out, coarse
+
+    def centroid_dists(self, V):
+        """(out f32[n, nslots], slot cids i64[nslots]): reference distances of
+        host rows to every slot's centroid."""
+        self.flush()
+        V = N.f32(V, self.dimension)
+        ns = ctypes.c_int32(0)
+        N.check(N.lib().pk_slot_count(self._h, ctypes.byref(ns)))
+        out = np.empty((V.shape[0], ns.value), dtype=np.float32)
+        cids = np.empty(ns.value, dtype=np.int64)
+        N.check(N.lib().pk_centroid_dists(self._h, N.ptr(V), V.shape[0], N.ptr(out), N.ptr(cids)))
+        return out, cids
+
+    def list_slot(self, cid: int) -> int:
+        v = ctypes.c_int32(0)
+        N.check(N.lib().pk_list_slot(self._h, int(cid), ctypes.byref(v)))
+        return int(v.value)
+
     # ---- agent-mode L2 scan ---------------------------------------------------
     def coarse_cids(self, Q, scope_codes, nprobe: int) -> np.ndarray:
         """Coarse stage only: probed list ids i64[B, nprobe] in coarse order."""

@@ -455,6 +455,33 @@ class ShardedStoreIndex:
             out.probe = self.local.coarse_cids(Q, scope_codes, nprobe)
         return out
 
+    # ---- the coarse graph: replicated (every rank holds every centroid) ----
+    def graph_set(self, *args):
+        self.local.graph_set(*args)
+
+    def centroid_dists(self, V):
+        return self.local.centroid_dists(V)
+
+    def list_slot(self, cid: int) -> int:
+        return self.local.list_slot(cid)
+
+    def graph_probe(self, Q, scope_codes, nprobe: int, ef: int, mode: int = 0):
+        return self.local.graph_probe(Q, scope_codes, nprobe, ef, mode)
+
+    def search_graph(self, Q, scope_codes, nprobe: int, kk: int, ef: int, mode: int = 0,
+                     want_probe: bool = False):
+        """pk_search_graph on every rank (identical traversal, own lists
+        scanned) -> all-gather of the shard blocks -> merge."""
+        import torch
+
+        Q = np.ascontiguousarray(Q, dtype=np.float32).reshape(-1, self.dimension)
+        B = Q.shape[0]
+        blk, probe, coarse = self.local.search_graph_block(Q, scope_codes, nprobe, kk, ef, mode)
+        if self.world > 1:
+            blk = self.sh._all_gather(torch.from_numpy(blk)).cpu().numpy().reshape(-1)
+        ids, dd, cids, cnt, sc = self.local.merge_shards(blk, self.world, B, kk)
+        return SearchOutput(ids, dd, cids, cnt, probe if want_probe else None, sc), coarse
+
     def scan_lists(self, q, cids, total: int):
         """(ids, dists, prefix offsets) of every row of ``cids`` in that order:
         each owner scans its lists, the pieces are exchanged."""

@@ -95,6 +95,24 @@ TRACE_SPECS = {
 }
 
 
+# Traces at the reference's DEFAULT coarse ef (ef_search_factor 4, approximate
+# graph traversal, ref/graph.py:321-422) with multi-scope agent graphs grown by
+# splits, so portals and per-scope graphs matter; they also record
+# SearchStats.coarse_computations.  Replayed against this package's graph
+# traversal (pk_graph.cu); the oracle's flat store model does not cover them.
+GRAPH_TRACE_SPECS = {
+    "graph_hybrid": dict(d=24, n_base=4000, nlist=120, n_q=140, n_ins=1600, n_del=40, n_upd=20,
+                         maint=32, split=(80, 40), agents=3, seed=8, k=10, nprobe=4, ef_factor=4,
+                         record_coarse=True),
+    "graph_per_agent": dict(d=24, n_base=3000, nlist=90, n_q=120, n_ins=1200, n_del=30, n_upd=20,
+                            maint=32, split=(80, 40), agents=3, seed=9, k=10, nprobe=3, ef_factor=4,
+                            record_coarse=True, coarse_mode="per_agent"),
+    "graph_ef2": dict(d=16, n_base=2500, nlist=100, n_q=120, n_ins=800, n_del=30, n_upd=20,
+                      maint=16, split=(70, 30), agents=2, seed=10, k=6, nprobe=5, ef_factor=2,
+                      record_coarse=True),
+}
+
+
 def trace_ops(spec):
     """Deterministic op list for one trace.
 
@@ -162,9 +180,10 @@ def trace_ops(spec):
 def store_config_kwargs(spec):
     """Reference StoreConfig for bare-path parity."""
     kw = dict(
-        dimension=spec["d"], seed=spec["seed"], ef_search_factor=1 << 20, alpha_et=0.0,
-        cache_enabled=False, pattern_enabled=False, prefetch_enabled=False,
+        dimension=spec["d"], seed=spec["seed"], ef_search_factor=spec.get("ef_factor", 1 << 20),
+        alpha_et=0.0, cache_enabled=False, pattern_enabled=False, prefetch_enabled=False,
         profiles_enabled=False, accelerator="none", maintenance_interval=spec["maint"],
+        coarse_mode=spec.get("coarse_mode", "hybrid"),
     )
     if spec["split"] is None:
         kw.update(split_threshold=1 << 30, split_target=1 << 20, splits_enabled=False)
@@ -203,6 +222,11 @@ AGENT_TRACE_SPECS = {
     # CPU speed: 16 agents, k 10, mixed insert / search stream
     "agents_16": dict(d=64, n_base=6000, nlist=24, n_agents=16, n_ops=1600, seed=36, k=10,
                       nprobe=4, n_p=8, l0=16, l1=64, window=8, alpha=0.7, verify=False),
+    # agent mode at the reference's default coarse ef (graph traversal, portals
+    # from merged-down agent clusters), coarse_computations recorded
+    "agents_graph": dict(d=32, n_base=4000, nlist=80, n_agents=4, n_ops=900, seed=37, k=8,
+                         nprobe=3, n_p=6, l0=10, l1=30, window=6, alpha=0.7, verify=True,
+                         ef_factor=4, record_coarse=True),
 }
 
 
@@ -255,7 +279,7 @@ def agent_trace_ops(spec):
 def agent_store_config_kwargs(spec):
     """Reference StoreConfig of the agent traces (exhaustive coarse ef)."""
     return dict(
-        dimension=spec["d"], seed=spec["seed"], ef_search_factor=1 << 20,
+        dimension=spec["d"], seed=spec["seed"], ef_search_factor=spec.get("ef_factor", 1 << 20),
         metric=spec.get("metric", "sq_l2"), alpha_et=spec["alpha"], window_w=spec["window"], n_p=spec["n_p"],
         l0_capacity=spec["l0"], l1_capacity=spec["l1"], verify_mode=spec["verify"],
         cache_enabled=True, pattern_enabled=True, prefetch_enabled=True, profiles_enabled=True,
@@ -304,6 +328,8 @@ def run_agent_ops(store, spec, base, ops, write_pnck, metric):
             rec[f"{i}/scan_ids"] = np.asarray(res.scan_ids, dtype=np.int64)
             rec[f"{i}/level"] = np.array(res.stats.level_reached, dtype="U4")
             rec[f"{i}/early"] = np.array(bool(res.stats.early_terminated))
+            if spec.get("record_coarse"):
+                rec[f"{i}/coarse"] = np.array(res.stats.coarse_computations)
     cl = store.clusters.clusters
     cids = sorted(cl)
     rec["final/cids"] = np.array(cids, dtype=np.int64)

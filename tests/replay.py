@@ -107,6 +107,7 @@ def replay_store(spec, batch_searches=False, overrides=None, tier_log=None):
             rec[f"{i}/hit_scope"] = np.array([h[2] for h in res.hits], dtype="U16")
             rec[f"{i}/scanned"] = np.array(res.stats.scanned_vectors)
             rec[f"{i}/scan_ids"] = np.asarray(res.scan_ids, dtype=np.int64)
+            rec[f"{i}/coarse"] = np.array(res.stats.coarse_computations)
             if tier_log is not None:
                 tier_log.append(store.tier.metrics())
     cids = sorted(store.clusters.clusters)

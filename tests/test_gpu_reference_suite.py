@@ -44,9 +44,6 @@ SUITES = ("test_engine", "test_acceptance", "test_tiering")
 
 # reference test -> why the drop-in differs (strict xfail)
 DEVIATIONS = {
-    "test_03_hybrid_graph_coarse_cost": (
-        "coarse_computations counts in-scope lists (flat exact quantizer), not the hybrid "
-        "graph's visited nodes"),
     "test_09_persistence_round_trips": "snapshot/restore (ref/persist.py:136-380) not built",
 }
 
