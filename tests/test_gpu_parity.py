@@ -489,8 +489,10 @@ def test_nprobe_above_device_pick_limit(pk):
 
     rng = np.random.default_rng(13)
     d, nlist = 16, 2300
+    # exhaustive coarse ef: the flat oracle equals the reference's graph only
+    # there; default-ef graph parity is tests/test_gpu_graph.py
     store = Store(StoreConfig(dimension=d, cache_enabled=False, accelerator="none",
-                              splits_enabled=False, seed=3))
+                              splits_enabled=False, seed=3, ef_search_factor=1 << 20))
     model = StoreModel(d, seed=3)
     lists, nid = [], 0
     for c in range(nlist):
