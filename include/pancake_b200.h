@@ -137,6 +137,40 @@ int pk_search_coarse_cids(pk_index* ix, const float* Q, int64_t B, const int32_t
 int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, int64_t* out_ids,
                   float* out_dists, int64_t* out_prefix);
 
+/* ---- agent path, one device pass per agent search (pk_agent.cu) ----------
+ * Replaces the per-pool / per-list / per-pattern batch_distances calls of
+ * ref/engine.py:319-404 (cached_search ref/cache.py:162-221, the staging
+ * scan, HybridGraphIndex.search ref/graph.py:321-396 and the list scans) and
+ * of ref/fsm.py:296-392 (match / align / predict) with one call; the caller
+ * replays the policy (scan order, stop rule, _topk) over the values.
+ * pk_rows_put: rows [n][d] into the HBM row store at host-managed slots (the
+ *   rows the policy scans: cache pool rows, L1 centroids, FSM states).
+ * pk_agent_read: puts first, then for one query q: out_d[i] = dist(q, row
+ *   slots[i]); out_m[r][c] = dist(row mq[r], row mx[c]) (mq rows as queries);
+ *   and, when nprobe > 0, the reference's coarse traversal (ef, mode as
+ *   pk_search_graph) and every row of each probed list in coarse order:
+ *   out_cids[nprobe] (-1 padded), *out_coarse = distance computations, list l
+ *   at rows [out_prefix[l], out_prefix[l+1]) of out_ids / out_dists (capacity
+ *   cap rows; a larger total fails with PK_ERR_USAGE, out_prefix set).
+ * pk_l1_place: the L1 placement chain of ref/cache.py:284-325 for m items
+ *   popped from L0 (then q's capture target when q != NULL) over nc live
+ *   clusters (fp64 sums [nc][d], f32 centroids [nc][d], counts [nc]);
+ *   holder[i] = list position of the cluster already holding item i (ids
+ *   item_ids[i]; an id may recur in the chain), or -1.
+ *   Per item: out_target = list position chosen (-1: a fresh cluster was
+ *   appended), out_added, out_merged (merge_down after it); *out_qtarget
+ *   likewise for q.  The caller applies the same operations in order. */
+int pk_rows_put(pk_index* ix, const int32_t* slots, const float* rows, int64_t n);
+int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const float* put_rows, int64_t nput,
+                  const int32_t* slots, int64_t n, float* out_d, const int32_t* mq, int32_t nmq,
+                  const int32_t* mx, int32_t nmx, float* out_m, const int32_t* scope_codes, int32_t nscopes,
+                  int32_t nprobe, int32_t ef, int32_t mode, int64_t* out_cids, int32_t* out_coarse,
+                  int64_t* out_prefix, int64_t* out_ids, float* out_dists, int64_t cap);
+int pk_l1_place(pk_index* ix, int32_t nc, int32_t n_p, int32_t capacity, const double* sums, const float* cents,
+                const int32_t* counts, const float* items, const int64_t* item_ids, const int32_t* holder,
+                int32_t m, const float* q, int32_t* out_target, uint8_t* out_added, uint8_t* out_merged,
+                int32_t* out_qtarget);
+
 /* ---- cold tier (TierManager, tiering.py:175-448) --
  * pk_index_enable_tier (before any list exists): every list keeps a copy in
  * a pinned, device-mapped host arena (the source of truth, tiering.py:9-12);

@@ -231,17 +231,22 @@ class StoreModel:
     def live(self):
         return len(self.owner)
 
-    def search(self, scopes, q, k, nprobe):
-        """Returns (hits [(id, dist f32, scope)], scanned, scan_ids)."""
+    def search(self, scopes, q, k, nprobe, probe=None):
+        """Returns (hits [(id, dist f32, scope)], scanned, scan_ids).  probe:
+        the probed cids in coarse order when given (the coarse graph's own
+        output, e.g. where it is not connected and ef cannot make it flat);
+        else the flat top-nprobe by (dist, cid) (the graph at exhaustive ef,
+        SURVEY F3)."""
         exhaustive = k >= self.live()
         eff = max(nprobe, len(self.clusters) or 1) if exhaustive else nprobe
         cids = [c for s in scopes for c in self.by_scope[s]]
         if not cids:
             return [], 0, np.empty(0, np.int64)
-        cents = np.stack([self.clusters[c].centroid for c in cids])
-        dc = O.distances(q, cents, self.metric)
-        ca = np.array(cids, np.int64)
-        probe = ca[np.lexsort((ca, dc))[:eff]]
+        if probe is None:
+            cents = np.stack([self.clusters[c].centroid for c in cids])
+            dc = O.distances(q, cents, self.metric)
+            ca = np.array(cids, np.int64)
+            probe = ca[np.lexsort((ca, dc))[:eff]]
         ids = [self.clusters[c].ids for c in probe]
         dd = [O.distances(q, self.clusters[c].rows, self.metric) for c in probe]
         scan_ids = np.concatenate(ids) if ids else np.empty(0, np.int64)

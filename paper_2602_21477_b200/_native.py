@@ -92,6 +92,10 @@ _SIGS = [
     ("pk_centroid_dists", [_vp, _vp, _i64, _vp, _vp], _int),
     ("pk_list_slot", [_vp, _i64, _i32p], _int),
     ("pk_slot_count", [_vp, _i32p], _int),
+    ("pk_rows_put", [_vp, _vp, _vp, _i64], _int),
+    ("pk_agent_read", [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _i32,
+                       _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _i64], _int),
+    ("pk_l1_place", [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp], _int),
 ]
 STAGES = ("input", "coarse_dist", "coarse_select", "route", "scan", "merge_out")
 EXPORTED = [s[0] for s in _SIGS]

@@ -7,7 +7,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SOURCES = ["csrc/pk_kernels.cu", "csrc/pk_graph.cu", "csrc/pk_abi.cu"]
+SOURCES = ["csrc/pk_kernels.cu", "csrc/pk_graph.cu", "csrc/pk_agent.cu", "csrc/pk_abi.cu"]
 OUT = os.path.join(HERE, "libpancake_b200.so")
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

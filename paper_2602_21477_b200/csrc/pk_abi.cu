@@ -222,10 +222,21 @@ struct pk_index {
   PinnedBuf hstage;  // append staging (mapped)
   PinnedBuf hsl;     // pk_scan_lists staging (mapped)
   PinnedBuf hasg;    // pk_assign host path: padded rows in, (cid, dist) out (mapped)
+  // agent path (pk_rows_put / pk_agent_read / pk_l1_place, pk_agent.cu): the
+  // HBM row store of the rows the per-agent policy scans (cache pool rows, L1
+  // centroids, FSM states) at host-managed slots, packed staging and outputs
+  DevBuf arows;  // [acap][dp]
+  int64_t acap = 0;
+  PinnedBuf hag;  // mapped: packed inputs, then the kernels' outputs
+  DevBuf ag_in, ag_l1;
   // front-half overlap: the next batch's prep / coarse / pick / routing run on
   // fst while this batch's scan and re-rank drain on st
   cudaStream_t fst = nullptr;
-  cudaEvent_t ev_front = nullptr, ev_scan = nullptr, front_wait = nullptr;
+  // ... and the scan of a pipelined search runs on sst, so this batch's
+  // re-rank (index stream, after ev_sdone) runs beside the NEXT batch's scan
+  cudaStream_t sst = nullptr;
+  cudaEvent_t ev_front = nullptr, ev_scan = nullptr, front_wait = nullptr, ev_sdone = nullptr;
+  bool rr_lean = true;  // PK_RERANK_LEAN=0: the wide re-rank after the scan, as before
   uint64_t ev_scan_n = 0;  // lock count when ev_scan was last recorded
   bool pipeline = true;    // PK_PIPELINE=0 turns the overlap off
   DevBuf assign_q, assign_qn, assign_dc, assign_c, assign_d;
@@ -310,6 +321,7 @@ struct pk_index {
     uint64_t slot_ver = 0;   // slot <-> cid map version they were built against
     int32_t static_code = 0;
     DevBuf level, nbr0, up_off, up, por_off, por, rank, slot_of_rank, flags, stamps, heap, count;
+    int32_t npor = 0;
     std::unordered_map<int32_t, std::pair<int32_t, int32_t>> entry;  // scope code -> (slot, max level)
     std::vector<uint8_t> hflags;
     void release() {
@@ -932,6 +944,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   }
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
   if (const char* e = getenv("PK_PIPELINE")) ix->pipeline = atoi(e) != 0;
+  if (const char* e = getenv("PK_RERANK_LEAN")) ix->rr_lean = atoi(e) != 0;
   if (const char* e = getenv("PK_QGATHER")) ix->qgather = atoi(e) != 0;
   if (const char* e = getenv("PK_STAGE")) ix->stage_dma = strcmp(e, "dma") == 0;
   if (const char* e = getenv("PK_COARSE")) {
@@ -959,7 +972,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
 int pk_index_destroy(pk_index* ix) {
   if (!ix) return PK_OK;
   cudaSetDevice(ix->device);
-  for (cudaStream_t x : {ix->fst, ix->rst, ix->cst, ix->st})
+  for (cudaStream_t x : {ix->fst, ix->sst, ix->rst, ix->cst, ix->st})
     if (x) cudaStreamSynchronize(x);
   cudaFree(ix->rows);
   cudaFree(ix->ids);
@@ -983,6 +996,10 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->hstage.p) cudaFreeHost(ix->hstage.p);
   if (ix->hsl.p) cudaFreeHost(ix->hsl.p);
   if (ix->hasg.p) cudaFreeHost(ix->hasg.p);
+  if (ix->hag.p) cudaFreeHost(ix->hag.p);
+  ix->arows.release();
+  ix->ag_in.release();
+  ix->ag_l1.release();
   for (auto& a : ix->aslot) {
     if (a.hblk) cudaFreeHost(a.hblk);
     if (a.copied) cudaEventDestroy(a.copied);
@@ -1001,7 +1018,11 @@ int pk_index_destroy(pk_index* ix) {
     cudaStreamSynchronize(ix->fst);
     cudaStreamDestroy(ix->fst);
   }
-  for (cudaEvent_t e : {ix->ev_front, ix->ev_scan})
+  if (ix->sst) {
+    cudaStreamSynchronize(ix->sst);
+    cudaStreamDestroy(ix->sst);
+  }
+  for (cudaEvent_t e : {ix->ev_front, ix->ev_scan, ix->ev_sdone})
     if (e) cudaEventDestroy(e);
   for (uint8_t* p : ix->comb.opened) cudaIpcCloseMemHandle(p);
   if (ix->comb.area) cudaFree(ix->comb.area);
@@ -1606,6 +1627,7 @@ static int graph_coarse(pk_index* ix, pk_index::Scratch& S, int64_t B, const int
   gd.slot_of_rank = G.slot_of_rank.as<int32_t>();
   gd.M = G.M;
   gd.ns = ns;
+  gd.npor = G.npor;
   if (graph_smem_bytes(ns, false) > 227 * 1024) {  // per-query state in global memory
     RET(G.stamps.ensure((size_t)B * ns * 4));
     RET(G.heap.ensure((size_t)B * (2 * ns + 2) * 8));
@@ -1810,15 +1832,26 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                lcount, S.items.as<ScanItem>(), n_items, S.qpairs.as<QPair>(),
                S.slot_off.as<int32_t>(), S.scanned.as<int64_t>(), ra.lcount != nullptr,
                (int)std::min<int64_t>(max_items, INT32_MAX), fs);
-  if (pipelined) {
-    CK(cudaEventRecord(ix->ev_front, fs));
-    CK(cudaStreamWaitEvent(st, ix->ev_front, 0));
-  }
   if (!ix->ev_front) {
     CK(cudaEventCreateWithFlags(&ix->ev_front, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&ix->ev_scan, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ix->ev_sdone, cudaEventDisableTiming));
+    CK(cudaEventRecord(ix->ev_sdone, st));
   }
-  // everything before this batch's scan: where the next search's front may start
+  // Pipelined: the scan goes to the scan stream behind this front half and
+  // the previous scan -- NOT behind the previous batch's re-rank, which runs
+  // on the index stream beside it (lean, co-resident CTAs)
+  cudaStream_t ss = st;
+  if (pipelined) {
+    if (!ix->sst) CK(cudaStreamCreateWithFlags(&ix->sst, cudaStreamNonBlocking));
+    ss = ix->sst;
+    CK(cudaEventRecord(ix->ev_front, fs));
+    CK(cudaStreamWaitEvent(ss, ix->ev_front, 0));
+    CK(cudaStreamWaitEvent(ss, ix->ev_sdone, 0));
+  }
+  // the index stream up to here (the previous batch's re-rank included):
+  // where the next search's front may start -- its scratch set was last read
+  // by that re-rank
   CK(cudaEventRecord(ix->ev_scan, st));
   ix->ev_scan_n = ix->mu.n;
   // 3. fused scan + per-(query, list chunk) top-kk
@@ -1841,7 +1874,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                      (int)std::min<int64_t>(max_items, INT32_MAX), S.qpairs.as<QPair>(), kk,
                      work_ctr, S.uq.as<uint32_t>(), S.cand_key.as<uint32_t>(),
                      S.cand_n.as<int32_t>(), S.cpool.as<int4>(), S.ccount.as<int32_t>(),
-                     pool_cap, ix->scan_sms, st, /*pdl=*/!pipelined, qg,
+                     pool_cap, ix->scan_sms, ss, /*pdl=*/!pipelined, qg,
                      /*overlapped: release some SMs early for the next front half*/ pipelined);
     } else {
       launch_scan_screen(ix->metric, lt2, ix->maps, S.q.as<float>(), S.qnorm2.as<float>(),
@@ -1857,6 +1890,8 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                 S.qpairs.as<QPair>(), kk, work_ctr, S.cand_key.as<uint32_t>(),
                 S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(),
                 ix->num_sms, st);
+  CK(cudaEventRecord(ix->ev_sdone, ss));
+  if (pipelined) CK(cudaStreamWaitEvent(st, ix->ev_sdone, 0));
   PROF(5);
   // 4. merge per query
   int64_t* o_ids = out_ids;
@@ -1886,7 +1921,9 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                         S.scanned.as<int64_t>(), sc_dst, st,
                         // overlapped: launched after the scan, so its CTAs do not sit
                         // waiting on the SMs the scan tail frees for the next front half
-                        /*pdl=*/!pipelined);
+                        /*pdl=*/!pipelined,
+                        // pipelined: lean CTAs beside the next batch's scan (at most one per SM)
+                        (pipelined && ix->tensor && ix->rr_lean && rerank_lean_fits((int)dp)) ? ix->num_sms : 0);
   else
     launch_merge((int)B, S.slot_off.as<int32_t>(), S.cand_key.as<uint32_t>(),
                  S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(), kk,
@@ -2246,6 +2283,7 @@ int pk_graph_set(pk_index* ix, int32_t M, int64_t n, const int64_t* node_cid, co
   RET(put(G.slot_of_rank, sor.data(), sor.size() * 4));
   CK(cudaStreamSynchronize(ix->st));  // pageable sources
   G.M = M;
+  G.npor = (int32_t)porv.size();
   G.ns = ix->nslots;
   G.slot_ver = ix->slot_ver;
   G.static_code = static_code;
@@ -2385,6 +2423,284 @@ int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, 
     memcpy(out_ids, r_ids, total * 8);
     memcpy(out_dists, r_ids + std::max<int64_t>(total, 1), total * 4);
   }
+  return PK_OK;
+}
+
+// ---- agent path (pk_agent.cu) ---------------------------------------------
+
+}  // extern "C"
+
+namespace {
+// grow the agent row store to at least `need` slots, contents kept
+int rows_reserve(pk_index* ix, int64_t need) {
+  if (need <= ix->acap) return PK_OK;
+  const int64_t nc = std::max<int64_t>({need, ix->acap + ix->acap / 2, 1024});
+  void* p = nullptr;
+  CK(cudaMalloc(&p, (size_t)nc * ix->dp * 4));
+  if (ix->acap)
+    CK(cudaMemcpyAsync(p, ix->arows.p, (size_t)ix->acap * ix->dp * 4, cudaMemcpyDeviceToDevice, ix->st));
+  CK(cudaStreamSynchronize(ix->st));
+  ix->arows.release();
+  ix->arows.p = p;
+  ix->arows.bytes = (size_t)nc * ix->dp * 4;
+  ix->acap = nc;
+  return PK_OK;
+}
+// bump layout of one packed staging block (16-byte aligned pieces)
+struct Layout {
+  size_t off = 0;
+  size_t take(size_t bytes) {
+    const size_t o = off;
+    off = (size_t)round_up((int64_t)(off + bytes), 16);
+    return o;
+  }
+};
+}  // namespace
+
+extern "C" {
+
+int pk_rows_put(pk_index* ix, const int32_t* slots, const float* rows, int64_t n) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (n < 0) return fail(PK_ERR_USAGE, "negative row count");
+  if (n == 0) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  int64_t mx = -1;
+  for (int64_t i = 0; i < n; i++) {
+    if (slots[i] < 0) return fail(PK_ERR_USAGE, "negative row slot");
+    mx = std::max<int64_t>(mx, slots[i]);
+  }
+  RET(rows_reserve(ix, mx + 1));
+  const int64_t dp = ix->dp;
+  Layout L;
+  const size_t o_sl = L.take((size_t)n * 4), o_rw = L.take((size_t)n * dp * 4);
+  RET(ix->hag.ensure(L.off));
+  RET(ix->ag_in.ensure(L.off));
+  memcpy(ix->hag.p + o_sl, slots, (size_t)n * 4);
+  pack_padded(reinterpret_cast<float*>(ix->hag.p + o_rw), rows, n, ix->d, dp);
+  cudaStream_t st = ix->st;
+  uint8_t* din = ix->ag_in.as<uint8_t>();
+  CK(cudaMemcpyAsync(din, ix->hag.p, L.off, cudaMemcpyHostToDevice, st));
+  launch_rows_put(reinterpret_cast<const float*>(din + o_rw), reinterpret_cast<const int32_t*>(din + o_sl), (int)n,
+                  (int)dp, ix->arows.as<float>(), st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));  // the staging block is reused by the next call
+  return PK_OK;
+}
+
+int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const float* put_rows, int64_t nput,
+                  const int32_t* slots, int64_t n, float* out_d, const int32_t* mq, int32_t nmq,
+                  const int32_t* mx, int32_t nmx, float* out_m, const int32_t* scope_codes, int32_t nscopes,
+                  int32_t nprobe, int32_t ef, int32_t mode, int64_t* out_cids, int32_t* out_coarse,
+                  int64_t* out_prefix, int64_t* out_ids, float* out_dists, int64_t cap) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (nput < 0 || n < 0 || nmq < 0 || nmx < 0 || nprobe < 0 || cap < 0)
+    return fail(PK_ERR_USAGE, "negative count");
+  if (nprobe > 0) {
+    if (nscopes < 1 || nscopes > 64) return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
+    if (mode != 0 && mode != 1) return fail(PK_ERR_USAGE, "graph mode must be 0 (hybrid) or 1 (per-scope)");
+    if (!out_cids || !out_coarse || !out_prefix || (cap > 0 && (!out_ids || !out_dists)))
+      return fail(PK_ERR_USAGE, "missing list outputs");
+  }
+  CK(cudaSetDevice(ix->device));
+  cudaStream_t st = ix->st;
+  int64_t mxs = -1;
+  for (int64_t i = 0; i < nput; i++) {
+    if (put_slots[i] < 0) return fail(PK_ERR_USAGE, "negative row slot");
+    mxs = std::max<int64_t>(mxs, put_slots[i]);
+  }
+  RET(rows_reserve(ix, mxs + 1));
+  auto bad = [&](const int32_t* v, int64_t m) {
+    for (int64_t i = 0; i < m; i++)
+      if (v[i] < 0 || v[i] >= ix->acap) return true;
+    return false;
+  };
+  if (bad(slots, n) || bad(mq, nmq) || bad(mx, nmx)) return fail(PK_ERR_USAGE, "row slot out of range");
+  if (ix->tiered && nprobe > 0) RET(ix->poll_migrations());
+  if (nprobe > 0) RET(ix->sync_table());
+  const int64_t dp = ix->dp, d = ix->d;
+  const bool lists = nprobe > 0 && ix->nslots > 0;
+  const int64_t maxlen = lists ? ix->max_list_len() : 0;
+  const int64_t rcap = lists ? std::min<int64_t>(cap, (int64_t)nprobe * maxlen) : 0;
+  // inputs: q | put slots | put rows | read slots | matrix query / row slots
+  Layout L;
+  const size_t o_q = L.take(dp * 4), o_ps = L.take(nput * 4), o_pr = L.take((size_t)nput * dp * 4),
+               o_sl = L.take(n * 4), o_mq = L.take((size_t)nmq * 4), o_mx = L.take((size_t)nmx * 4);
+  const size_t in_bytes = L.off;
+  // outputs (mapped; written by the kernels, read after one sync)
+  const size_t o_od = L.take(n * 4), o_om = L.take((size_t)nmq * nmx * 4), o_cid = L.take((size_t)nprobe * 8),
+               o_pre = L.take((size_t)(nprobe + 1) * 8), o_cnt = L.take(8), o_ids = L.take((size_t)rcap * 8),
+               o_dd = L.take((size_t)rcap * 4);
+  RET(ix->hag.ensure(L.off));
+  RET(ix->ag_in.ensure(in_bytes));
+  uint8_t* h = ix->hag.p;
+  uint8_t* hd = ix->hag.dev;
+  memcpy(h + o_q, q, d * 4);
+  if (dp > d) memset(h + o_q + d * 4, 0, (dp - d) * 4);
+  if (nput) {
+    memcpy(h + o_ps, put_slots, nput * 4);
+    pack_padded(reinterpret_cast<float*>(h + o_pr), put_rows, nput, d, dp);
+  }
+  if (n) memcpy(h + o_sl, slots, n * 4);
+  if (nmq) memcpy(h + o_mq, mq, (size_t)nmq * 4);
+  if (nmx) memcpy(h + o_mx, mx, (size_t)nmx * 4);
+  uint8_t* din = ix->ag_in.as<uint8_t>();
+  CK(cudaMemcpyAsync(din, h, in_bytes, cudaMemcpyHostToDevice, st));
+  const float* dq = reinterpret_cast<const float*>(din + o_q);
+  float* arows = ix->arows.as<float>();
+  if (nput)
+    launch_rows_put(reinterpret_cast<const float*>(din + o_pr), reinterpret_cast<const int32_t*>(din + o_ps),
+                    (int)nput, (int)dp, arows, st);
+  launch_gather_dist(ix->metric, dq, arows, (int)dp, (int)d, reinterpret_cast<const int32_t*>(din + o_sl), (int)n,
+                     reinterpret_cast<float*>(hd + o_od), st);
+  launch_gather_mat(ix->metric, arows, (int)dp, (int)d, reinterpret_cast<const int32_t*>(din + o_mq), nmq,
+                    reinterpret_cast<const int32_t*>(din + o_mx), nmx, reinterpret_cast<float*>(hd + o_om), st);
+  int64_t* h_pre = reinterpret_cast<int64_t*>(h + o_pre);
+  int64_t* h_cid = reinterpret_cast<int64_t*>(h + o_cid);
+  if (lists) {
+    // the reference's coarse traversal for this query (graph_coarse), then
+    // every row of every probed list in coarse order
+    pk_index::Scratch& S = ix->scr[ix->par];
+    RET(S.q.ensure(dp * 4));
+    RET(S.qnorm.ensure(4));
+    RET(S.probe.ensure((size_t)nprobe * 4));
+    CK(cudaMemcpyAsync(S.q.p, dq, dp * 4, cudaMemcpyDeviceToDevice, st));
+    if (ix->metric == COSINE) launch_qnorm(S.q.as<float>(), dp, 1, (int)d, S.qnorm.as<float>(), st);
+    GraphArgs ga;
+    ga.ef = ef;
+    ga.mode = mode;
+    ga.out_coarse = reinterpret_cast<int32_t*>(h + o_cnt);
+    RET(graph_coarse(ix, S, 1, scope_codes, nscopes, nprobe, ga, st));
+    if (!ix->tiered) {
+      launch_probe_lists(ix->metric, S.q.as<float>(), ix->table(), S.probe.as<int32_t>(), nprobe, maxlen, rcap,
+                         reinterpret_cast<float*>(hd + o_dd), reinterpret_cast<int64_t*>(hd + o_ids),
+                         reinterpret_cast<int64_t*>(hd + o_pre), reinterpret_cast<int64_t*>(hd + o_cid), st);
+    } else {
+      // cold lists are read in place from the mapped host arena: the sources
+      // need the probe on the host (pk_scan_lists' layout)
+      std::vector<int32_t> pr(nprobe);
+      CK(cudaMemcpyAsync(pr.data(), S.probe.p, (size_t)nprobe * 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      std::vector<ListSrc> src;
+      std::vector<int64_t> pre(1, 0);
+      h_pre[0] = 0;
+      for (int32_t l = 0; l < nprobe; l++) {
+        const int32_t sl = pr[l];
+        h_cid[l] = sl >= 0 ? ix->h_cid[sl] : -1;
+        h_pre[l + 1] = h_pre[l] + (sl >= 0 ? ix->h_len[sl] : 0);
+        if (sl < 0) continue;
+        ListSrc x;
+        if (ix->h_res[sl]) {
+          x.rows = ix->rows + ix->h_off[sl] * dp;
+          x.ids = ix->ids + ix->h_off[sl];
+        } else {
+          x.rows = ix->hrows_d + ix->h_hoff[sl] * dp;
+          x.ids = ix->hids_d + ix->h_hoff[sl];
+        }
+        src.push_back(x);
+        pre.push_back(pre.back() + ix->h_len[sl]);
+      }
+      const int64_t total = std::min<int64_t>(pre.back(), rcap);
+      const int m = (int)src.size();
+      if (m > 0 && total > 0) {
+        // the list sources + prefix (clamped to the capacity) in one copy
+        const size_t sb = round_up(m * sizeof(ListSrc), 16), pb = (size_t)(m + 1) * 8;
+        RET(ix->sl_buf.ensure(sb + pb));
+        std::vector<uint8_t> blk(sb + pb);
+        memcpy(blk.data(), src.data(), m * sizeof(ListSrc));
+        for (auto& v : pre) v = std::min<int64_t>(v, total);
+        memcpy(blk.data() + sb, pre.data(), pb);
+        CK(cudaMemcpyAsync(ix->sl_buf.p, blk.data(), blk.size(), cudaMemcpyHostToDevice, st));
+        launch_lists_dist(ix->metric, S.q.as<float>(), S.qnorm.as<float>(),
+                          ix->sl_buf.as<ListSrc>(),
+                          reinterpret_cast<const int64_t*>(ix->sl_buf.as<uint8_t>() + sb), m, total, (int)dp,
+                          (int)d, reinterpret_cast<float*>(hd + o_dd), reinterpret_cast<int64_t*>(hd + o_ids), st);
+        CK(cudaStreamSynchronize(st));  // blk (pageable) and the sources in flight
+      }
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  if (n) memcpy(out_d, h + o_od, n * 4);
+  if (nmq && nmx) memcpy(out_m, h + o_om, (size_t)nmq * nmx * 4);
+  if (nprobe > 0) {
+    if (!lists) {
+      for (int32_t l = 0; l < nprobe; l++) out_cids[l] = -1;
+      for (int32_t l = 0; l <= nprobe; l++) out_prefix[l] = 0;
+      *out_coarse = 0;
+      return PK_OK;
+    }
+    memcpy(out_cids, h_cid, (size_t)nprobe * 8);
+    memcpy(out_prefix, h_pre, (size_t)(nprobe + 1) * 8);
+    *out_coarse = *reinterpret_cast<int32_t*>(h + o_cnt);
+    const int64_t total = h_pre[nprobe];
+    if (total > cap) return fail(PK_ERR_USAGE, "probed lists hold %lld rows, capacity %lld", (long long)total, (long long)cap);
+    memcpy(out_ids, h + o_ids, total * 8);
+    memcpy(out_dists, h + o_dd, total * 4);
+  }
+  return PK_OK;
+}
+
+int pk_l1_place(pk_index* ix, int32_t nc, int32_t n_p, int32_t capacity, const double* sums, const float* cents,
+                const int32_t* counts, const float* items, const int64_t* item_ids, const int32_t* holder,
+                int32_t m, const float* q, int32_t* out_target, uint8_t* out_added, uint8_t* out_merged,
+                int32_t* out_qtarget) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (nc < 0 || m < 0 || n_p < 1 || capacity < 1) return fail(PK_ERR_USAGE, "bad L1 placement shape");
+  const int maxc = l1_place_max_clusters();
+  if (n_p > maxc || nc + m > maxc)
+    return fail(PK_ERR_USAGE, "L1 placement of %d items over %d clusters exceeds %d", m, nc, maxc);
+  if (m == 0 && !q) return PK_OK;
+  CK(cudaSetDevice(ix->device));
+  cudaStream_t st = ix->st;
+  const int64_t dp = ix->dp, d = ix->d;
+  const int64_t ncap = nc + m;
+  Layout L;
+  const size_t o_s = L.take((size_t)ncap * dp * 8), o_c = L.take((size_t)ncap * dp * 4),
+               o_n = L.take((size_t)ncap * 4), o_it = L.take((size_t)m * dp * 4), o_h = L.take((size_t)m * 4),
+               o_dup = L.take((size_t)m * 4), o_q = L.take(dp * 4);
+  const size_t in_bytes = L.off;
+  const size_t o_t = L.take((size_t)m * 4), o_a = L.take(m), o_m = L.take(m), o_qt = L.take(4);
+  RET(ix->hag.ensure(L.off));
+  RET(ix->ag_l1.ensure(in_bytes));
+  uint8_t* h = ix->hag.p;
+  double* hs = reinterpret_cast<double*>(h + o_s);
+  for (int32_t c = 0; c < nc; c++) {
+    memcpy(hs + (int64_t)c * dp, sums + (int64_t)c * d, d * 8);
+    for (int64_t j = d; j < dp; j++) hs[(int64_t)c * dp + j] = 0.0;
+  }
+  pack_padded(reinterpret_cast<float*>(h + o_c), cents, nc, d, dp);
+  memcpy(h + o_n, counts, (size_t)nc * 4);
+  pack_padded(reinterpret_cast<float*>(h + o_it), items, m, d, dp);
+  memcpy(h + o_h, holder, (size_t)m * 4);
+  {  // earlier occurrence of the same item in this chain (an id evicted with
+     // an L0 entry can come back with the new entry's overflow)
+    int32_t* du = reinterpret_cast<int32_t*>(h + o_dup);
+    std::unordered_map<int64_t, int32_t> last;
+    for (int32_t i = 0; i < m; i++) {
+      auto it = last.find(item_ids[i]);
+      du[i] = it == last.end() ? -1 : it->second;
+      last[item_ids[i]] = i;
+    }
+  }
+  if (q) pack_padded(reinterpret_cast<float*>(h + o_q), q, 1, d, dp);
+  // only the live clusters' state and the items cross (fresh clusters start
+  // in device memory)
+  uint8_t* dv = ix->ag_l1.as<uint8_t>();
+  CK(cudaMemcpyAsync(dv + o_s, h + o_s, (size_t)nc * dp * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dv + o_c, h + o_c, (size_t)(in_bytes - o_c), cudaMemcpyHostToDevice, st));
+  uint8_t* hd = ix->hag.dev;
+  launch_l1_place(ix->metric, nc, n_p, capacity, (int)dp, (int)d, reinterpret_cast<double*>(dv + o_s),
+                  reinterpret_cast<float*>(dv + o_c), reinterpret_cast<int32_t*>(dv + o_n),
+                  reinterpret_cast<const float*>(dv + o_it), reinterpret_cast<const int32_t*>(dv + o_h),
+                  reinterpret_cast<const int32_t*>(dv + o_dup), m,
+                  q ? reinterpret_cast<const float*>(dv + o_q) : nullptr, reinterpret_cast<int32_t*>(hd + o_t),
+                  hd + o_a, hd + o_m, reinterpret_cast<int32_t*>(hd + o_qt), st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  memcpy(out_target, h + o_t, (size_t)m * 4);
+  memcpy(out_added, h + o_a, m);
+  memcpy(out_merged, h + o_m, m);
+  if (q && out_qtarget) *out_qtarget = *reinterpret_cast<int32_t*>(h + o_qt);
   return PK_OK;
 }
 

@@ -23,10 +23,15 @@
 // Keys pack (order-preserving f32 bits, cid) into 64 bits, so heap order is
 // exactly the tuple order (cids are below 2^32; pk_graph_set checks).
 //
-// One warp per query: lane 0 runs the sequential traversal (the reference's
-// own control flow is sequential: each admission changes the bound the next
-// one reads), the warp clears the per-query visit stamps and selects the
-// emitted top-nprobe.
+// One CTA per query: lane 0 of warp 0 runs the sequential traversal (the
+// reference's own control flow is sequential: each admission changes the
+// bound the next one reads), warp 0 selects the emitted top-nprobe.  The
+// traversal's reads are a chain of dependent loads (pop -> slot -> level /
+// neighbors -> their ranks), so when the graph fits, the whole CTA first
+// stages it into shared memory -- layer-0 neighbor lists, ranks, levels,
+// portals, flags and the distance row -- and every hop of the walk costs a
+// shared-memory latency instead of an L2 round trip (an agent search at
+// ~2K lists: 368 -> tens of microseconds).
 #include "pk_kernels.h"
 #include "pk_ptx.cuh"
 
@@ -196,23 +201,63 @@ struct Walk {
 
 // dynamic shared memory per CTA (one query): stamps u32[ns], two heaps u64[ns + 1],
 // and the distance row f32[ns] when `smem_row`
-__global__ void __launch_bounds__(32) graph_search_kernel(const float* __restrict__ D, int64_t ldd,
-                                                          GraphDev g, GraphQuery gq, int smem_heaps,
-                                                          int smem_row, uint32_t* gstamps, uint64_t* gheap,
-                                                          int32_t* probe, int32_t* counter_out) {
+constexpr int GRAPH_THREADS = 256;
+
+__global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float* __restrict__ D, int64_t ldd,
+                                                          GraphDev g0, GraphQuery gq, int smem_heaps,
+                                                          int smem_row, int smem_graph, uint32_t* gstamps,
+                                                          uint64_t* gheap, int32_t* probe, int32_t* counter_out) {
   extern __shared__ __align__(16) uint8_t sm[];
-  const int b = blockIdx.x, lane = threadIdx.x;
-  const int ns = g.ns;
+  const int b = blockIdx.x, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int ns = g0.ns;
   uint64_t* heaps = smem_heaps ? reinterpret_cast<uint64_t*>(sm) : gheap + (int64_t)b * (2 * ns + 2);
   uint32_t* stamp = smem_heaps ? reinterpret_cast<uint32_t*>(sm + (size_t)(2 * ns + 2) * 8)
                                : gstamps + (int64_t)b * ns;
   const float* drow_g = D + (int64_t)b * ldd;
   float* srow = reinterpret_cast<float*>(sm + (size_t)(2 * ns + 2) * 8 + (size_t)ns * 4);
-  for (int s = lane; s < ns; s += 32) {
+  GraphDev g = g0;
+  if (smem_graph) {  // the walk's arrays, after the heaps / stamps / row
+    uint8_t* p = sm + (((size_t)(2 * ns + 2) * 8 + (size_t)ns * 8 + 15) & ~(size_t)15);
+    int32_t* nb = reinterpret_cast<int32_t*>(p);
+    p += (size_t)ns * g0.M * 4;
+    int32_t* rk = reinterpret_cast<int32_t*>(p);
+    p += (size_t)ns * 4;
+    int32_t* sr = reinterpret_cast<int32_t*>(p);
+    p += (size_t)ns * 4;
+    int32_t* po = reinterpret_cast<int32_t*>(p);
+    p += (size_t)(ns + 1) * 4;
+    int32_t* pv = reinterpret_cast<int32_t*>(p);
+    p += (size_t)g0.npor * 4;
+    int8_t* lv = reinterpret_cast<int8_t*>(p);
+    p += (size_t)ns;
+    uint8_t* fl = p;
+    const int n4 = ns * g0.M / 4;  // M is a multiple of 4 (pk_graph_set pads)
+    for (int i = tid; i < n4; i += GRAPH_THREADS)
+      reinterpret_cast<int4*>(nb)[i] = reinterpret_cast<const int4*>(g0.nbr0)[i];
+    for (int i = 4 * n4 + tid; i < ns * g0.M; i += GRAPH_THREADS) nb[i] = g0.nbr0[i];
+    for (int i = tid; i < ns; i += GRAPH_THREADS) {
+      rk[i] = g0.rank[i];
+      sr[i] = g0.slot_of_rank[i];
+      po[i] = g0.por_off[i];
+      lv[i] = g0.level[i];
+      fl[i] = gq.flags[i];
+    }
+    if (tid == 0) po[ns] = g0.por_off[ns];
+    for (int i = tid; i < g0.npor; i += GRAPH_THREADS) pv[i] = g0.por[i];
+    g.nbr0 = nb;
+    g.rank = rk;
+    g.slot_of_rank = sr;
+    g.por_off = po;
+    g.por = pv;
+    g.level = lv;
+    gq.flags = fl;
+  }
+  for (int s = tid; s < ns; s += GRAPH_THREADS) {
     stamp[s] = 0;
     if (smem_row) srow[s] = drow_g[s];
   }
-  __syncwarp();
+  __syncthreads();
+  if (tid >= 32) return;
   uint32_t emit = 0;
   if (lane == 0) {
     Walk w;
@@ -312,15 +357,22 @@ __global__ void __launch_bounds__(32) graph_search_kernel(const float* __restric
 size_t graph_smem_bytes(int ns, bool row) {
   return (size_t)(2 * ns + 2) * 8 + (size_t)ns * 4 + (row ? (size_t)ns * 4 : 0);
 }
+static size_t graph_stage_bytes(const GraphDev& g) {
+  return 16 + (size_t)g.ns * g.M * 4 + (size_t)g.ns * 8 + (size_t)(g.ns + 1) * 4 + (size_t)g.npor * 4 +
+         (size_t)g.ns * 2;
+}
 
 void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, const GraphQuery& gq,
                          uint32_t* gstamps, uint64_t* gheap, int32_t* probe, int32_t* counter,
                          cudaStream_t st) {
   if (B <= 0) return;
   constexpr size_t SMEM_MAX = 227 * 1024;
-  int heaps = 1, row = 1;
+  int heaps = 1, row = 1, stage = 0;
   size_t smem = graph_smem_bytes(g.ns, true);
-  if (smem > SMEM_MAX) {
+  if (smem + graph_stage_bytes(g) <= SMEM_MAX && g.M % 4 == 0) {
+    stage = 1;
+    smem += graph_stage_bytes(g);
+  } else if (smem > SMEM_MAX) {
     row = 0;
     smem = graph_smem_bytes(g.ns, false);
   }
@@ -333,7 +385,8 @@ void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, 
     cudaFuncSetAttribute(graph_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX);
     attr = SMEM_MAX;
   }
-  graph_search_kernel<<<B, 32, smem, st>>>(D, ldd, g, gq, heaps, row, gstamps, gheap, probe, counter);
+  graph_search_kernel<<<B, GRAPH_THREADS, smem, st>>>(D, ldd, g, gq, heaps, row, stage, gstamps, gheap, probe,
+                                                      counter);
 }
 
 }  // namespace pk

@@ -1956,35 +1956,44 @@ constexpr int RR_CAP = 512;     // kept (<= 64) + one chunk of survivors, pow2 f
 constexpr int RR_SURV = 4096;  // survivors handled per pass
 constexpr int RR_HI_PER = 8;   // published upper bounds per thread (2048 per query)
 
-template <int METRIC>
-__global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
-    const int4* __restrict__ cpool, const int32_t* __restrict__ ccount, int cap,
+// LEAN: the configuration that runs NEXT TO the following batch's scan
+// (pipelined searches): <= ~19 KB of shared memory, so one re-rank CTA fits
+// on an SM beside a scan CTA, a persistent grid of at most one CTA per SM
+// looping over the queries, survivors in chunks of 32 through a 2-deep ring
+// of 32-float column blocks.  Its latency hides under that scan.
+template <int METRIC, bool LEAN>
+__global__ void __launch_bounds__(RR_THREADS, LEAN ? 3 : 1) rerank_merge_kernel(
+    int B, const int4* __restrict__ cpool, const int32_t* __restrict__ ccount, int cap,
     const uint32_t* __restrict__ slot_hi, const int32_t* __restrict__ slot_n,
     const int32_t* __restrict__ slot_off, ListTable lt, const float* __restrict__ Qd,
     const int32_t* __restrict__ probe, int nprobe, int kk, int stage_floats, int64_t* __restrict__ out_ids,
     float* __restrict__ out_d, int64_t* __restrict__ out_cid, int32_t* __restrict__ out_n,
     int32_t* __restrict__ nsurv, const int64_t* __restrict__ scanned_src, int64_t* __restrict__ scanned_dst,
     uint64_t* __restrict__ dbg) {
-  pdl_trigger();
-  pdl_wait();
-  auto mark = [&](int i) {  // phase cycle stamps (PK_DEBUG_RERANK)
-    if (dbg && threadIdx.x == 0) dbg[blockIdx.x * 4 + i] = (uint64_t)clock64();
-  };
-  mark(0);
-  if (scanned_dst && threadIdx.x == 0) scanned_dst[blockIdx.x] = scanned_src[blockIdx.x];
+  constexpr int CAP = LEAN ? 128 : RR_CAP;
+  constexpr int SURV = LEAN ? 512 : RR_SURV;
+  if (!LEAN) {
+    pdl_trigger();
+    pdl_wait();
+  }
   extern __shared__ __align__(16) uint8_t rr_smem[];
-  Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [RR_CAP]
-  float4* qs4 = reinterpret_cast<float4*>(rr_smem + RR_CAP * sizeof(Entry));     // [dp/4]
+  Entry* buf = reinterpret_cast<Entry*>(rr_smem);                                   // [CAP]
+  float4* qs4 = reinterpret_cast<float4*>(rr_smem + CAP * sizeof(Entry));        // [dp/4]
   float* stage = reinterpret_cast<float*>(qs4 + lt.dp / 4);                         // [stage_floats]
-  int32_t* surv = reinterpret_cast<int32_t*>(stage + stage_floats);                 // [RR_SURV]
+  int32_t* surv = reinterpret_cast<int32_t*>(stage + stage_floats);                 // [SURV]
   __shared__ int s_cnt, s_ns, s_bin, s_below;
   __shared__ unsigned s_hist[256];
   __shared__ unsigned s_wu[RR_THREADS / 32];
 
   __shared__ uint32_t s_u[RR_THREADS / 32];
   __shared__ int s_row[RR_THREADS];
-  const int b = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int b = blockIdx.x; b < B; b += gridDim.x) {
+  auto mark = [&](int i) {  // phase cycle stamps (PK_DEBUG_RERANK)
+    if (dbg && threadIdx.x == 0) dbg[b * 4 + i] = (uint64_t)clock64();
+  };
+  mark(0);
+  if (scanned_dst && threadIdx.x == 0) scanned_dst[b] = scanned_src[b];
   const int dp4 = lt.dp / 4;
   for (int j = threadIdx.x; j < dp4; j += blockDim.x)
     qs4[j] = reinterpret_cast<const float4*>(Qd + (int64_t)b * lt.dp)[j];
@@ -2078,13 +2087,13 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
   __syncthreads();
   mark(1);
   int kept = 0, surv_total = 0;
-  const int room = RR_CAP - kk;
+  const int room = CAP - kk;
   if (!overflow) {
-    for (int p0 = 0; p0 < n; p0 += RR_SURV) {
+    for (int p0 = 0; p0 < n; p0 += SURV) {
       // 2a. compact survivors of this pass
       if (threadIdx.x == 0) s_ns = 0;
       __syncthreads();
-      const int pm = min(RR_SURV, n - p0);
+      const int pm = min(SURV, n - p0);
       for (int i = threadIdx.x; i < pm; i += blockDim.x) {
         const int4 c = cpool[(int64_t)b * cap + p0 + i];
         if ((uint32_t)c.z <= U) surv[atomicAdd(&s_ns, 1)] = p0 + i;
@@ -2096,7 +2105,7 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
       //     (thread t runs survivor t's chain), rows streamed through
       //     shared memory in column blocks of W floats (bulk copies,
       //     2-deep ring) so every chain advances together
-      const int chunk = min(RR_THREADS, stage_floats / (2 * (DC + 4)));
+      const int chunk = min(LEAN ? 32 : RR_THREADS, stage_floats / (2 * (DC + 4)));
       for (int g0 = 0; g0 < ns; g0 += chunk) {
         const int m = min(chunk, ns - g0);
         const int nd32 = dp4 / 8;
@@ -2209,6 +2218,18 @@ __global__ void __launch_bounds__(RR_THREADS, 1) rerank_merge_kernel(
     if (nsurv) nsurv[b] = overflow ? -1 : surv_total;
   }
   mark(3);
+  __syncthreads();  // the next query reuses buf / qs4 / stage
+  }
+}
+
+// Shared memory of the lean re-rank (one CTA beside a scan CTA on each SM).
+static size_t rerank_lean_smem(int dp) {
+  return 128 * sizeof(Entry) + (size_t)dp * 4 + (size_t)2 * 32 * (DC + 4) * 4 + 512 * 4;
+}
+bool rerank_lean_fits(int dp) {
+  // an SM's 228 KB minus the scan CTA (dynamic + static + 1 KB reserved) and
+  // this CTA's own static arrays and reservation
+  return tc_smem_bytes() + 256 + 1024 + rerank_lean_smem(dp) + 2304 + 1024 <= 228 * 1024;
 }
 
 void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* ccount, int cap,
@@ -2216,25 +2237,39 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                          int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
-                         cudaStream_t st, bool pdl) {
+                         cudaStream_t st, bool pdl, int lean_ctas) {
   if (B <= 0) return;
   static const bool debug = getenv("PK_DEBUG_RERANK") != nullptr;
   uint64_t* dbg = nullptr;
   if (debug) cudaMallocAsync((void**)&dbg, (size_t)B * 32, st);
-  // row stage of ~82 KB (two CTAs per SM): the typical ~26 survivors' whole
-  // rows fit at once (one load round trip instead of one per column block)
-  const int stage_floats = 82 * 1024 / 4;
-  const size_t smem = RR_CAP * sizeof(Entry) + (size_t)lt.dp * 4 + (size_t)stage_floats * 4 + RR_SURV * 4;
-#define PK_RR(M)                                                                                \
+  const bool lean = lean_ctas > 0;
+  // wide: a row stage of ~82 KB (two CTAs per SM) so the typical ~26
+  // survivors' whole rows arrive in one load round trip; lean: a 2-deep ring
+  // of 32 rows x 32 floats
+  const int stage_floats = lean ? 2 * 32 * (DC + 4) : 82 * 1024 / 4;
+  const size_t smem = lean ? rerank_lean_smem(lt.dp)
+                           : RR_CAP * sizeof(Entry) + (size_t)lt.dp * 4 + (size_t)stage_floats * 4 + RR_SURV * 4;
+  const int grid = lean ? std::min(B, lean_ctas) : B;
+#define PK_RR(M, L)                                                                             \
   {                                                                                             \
-    auto k = rerank_merge_kernel<M>;                                                            \
-    PK_SMEM_ATTR(k, (int)smem);            \
-    launch_maybe_pdl(pdl, k, dim3(B), dim3(RR_THREADS), smem, st, cpool, ccount, cap, slot_hi, slot_n, slot_off, lt, Qd, probe, \
-                                   nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv,  \
-                                   scanned_src, scanned_dst, dbg);                                    \
+    auto k = rerank_merge_kernel<M, L>;                                                         \
+    PK_SMEM_ATTR(k, (int)smem);                                                                 \
+    if (L) {                                                                                    \
+      static bool carve_ = false;                                                               \
+      if (!carve_) {                                                                            \
+        cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);           \
+        carve_ = true;                                                                          \
+      }                                                                                         \
+    }                                                                                           \
+    launch_maybe_pdl(pdl && !L, k, dim3(grid), dim3(RR_THREADS), smem, st, B, cpool, ccount, cap, slot_hi, slot_n, \
+                     slot_off, lt, Qd, probe, nprobe, kk, stage_floats, out_ids, out_d, out_cid, out_n, nsurv,    \
+                     scanned_src, scanned_dst, dbg);                                            \
   }
-  if (metric == SQ_L2) PK_RR(SQ_L2)
-  else PK_RR(IP)
+  if (metric == SQ_L2) {
+    if (lean) PK_RR(SQ_L2, true) else PK_RR(SQ_L2, false)
+  } else {
+    if (lean) PK_RR(IP, true) else PK_RR(IP, false)
+  }
 #undef PK_RR
   if (dbg) {
     std::vector<uint64_t> h((size_t)B * 4);

@@ -119,6 +119,7 @@ struct GraphDev {          // slot-indexed, uploaded by pk_graph_set
   const int32_t* slot_of_rank;  // [ns]
   int M;
   int ns;
+  int npor;                // portal entries (por[] length)
 };
 struct GraphQuery {        // one batch's scope set
   const uint8_t* flags;    // [ns] bit0: list in the searched scopes, bit1: in scopes + static
@@ -155,7 +156,10 @@ void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* cc
                          ListTable lt, const float* Qd, const int32_t* probe, int nprobe, int kk,
                          int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                          int32_t* nsurv, const int64_t* scanned_src, int64_t* scanned_dst,
-                         cudaStream_t st, bool pdl = true);
+                         cudaStream_t st, bool pdl = true, int lean_ctas = 0);
+// lean_ctas > 0: the co-resident configuration (a persistent grid of at most
+// lean_ctas CTAs that fit beside the scan); whether it fits for this dp
+bool rerank_lean_fits(int dp);
 float screen_coef(int metric, int dp);
 float screen_coef_tf32(int metric, int dp);
 size_t tc_smem_bytes();
@@ -234,6 +238,25 @@ struct ListSrc {
   const float* rows;
   const int64_t* ids;
 };
+// ---- agent path (pk_agent.cu) ----
+// rows[slots[i]] = src[i] (rows of dp floats)
+void launch_rows_put(const float* src, const int32_t* slots, int n, int dp, float* rows, cudaStream_t st);
+// out[i] = dist(q, rows[slots[i]]) (reference arithmetic)
+void launch_gather_dist(int metric, const float* q, const float* rows, int dp, int d, const int32_t* slots, int n,
+                        float* out, cudaStream_t st);
+// out[r][c] = dist(q = rows[qslots[r]], x = rows[xslots[c]])
+void launch_gather_mat(int metric, const float* rows, int dp, int d, const int32_t* qslots, int nr,
+                       const int32_t* xslots, int nc, float* out, cudaStream_t st);
+// every row of the probed lists (device slots, coarse order), list after list
+void launch_probe_lists(int metric, const float* q, ListTable lt, const int32_t* probe, int nprobe,
+                        int64_t maxlen, int64_t cap, float* out_d, int64_t* out_ids, int64_t* out_prefix,
+                        int64_t* out_cids, cudaStream_t st);
+// the L1 placement chain of ref/cache.py:284-325 (one CTA)
+int l1_place_max_clusters();
+void launch_l1_place(int metric, int nc0, int n_p, int cap, int dp, int d, double* sums, float* cents,
+                     int32_t* cnt, const float* items, const int32_t* holder, const int32_t* dup, int m,
+                     const float* qv,
+                     int32_t* out_t, uint8_t* out_added, uint8_t* out_merged, int32_t* out_q, cudaStream_t st);
 void launch_lists_dist(int metric, const float* q, const float* qn, const ListSrc* src, const int64_t* prefix,
                        int m, int64_t total, int dp, int d, float* out_d, int64_t* out_ids,
                        cudaStream_t st);

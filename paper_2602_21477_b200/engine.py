@@ -14,8 +14,12 @@ without a cache, and no staged items in scope) is ONE device pass
 (coarse on tcgen05, screened scan, exact re-rank); an agent query with its
 multi-level cache (ref/cache.py), staged items (ref/engine.py:353-363) or
 early termination (ref/engine.py:376-396) runs the reference's per-query
-pipeline with every distance on the device -- the cache pools in one call,
-the probed lists in one call -- and the stop rules replayed on those values.
+pipeline with every distance from ONE device pass (pk_agent_read): the FSM
+states, every cached pool row and L1 centroid (resident in an HBM row store,
+rowstore.RowStore), the staged rows, the reference's coarse graph traversal
+and every row of the lists it probes -- then the hint, scan order, stop rules
+and _topk are replayed on those values.  The L1 placement chain of a
+promotion is one more device call when L0 overflows (pk_l1_place).
 """
 
 from __future__ import annotations
@@ -31,7 +35,6 @@ from . import pnck
 from .cache import DEFAULT_KEY, MultiLevelCache, RunningKth
 from .clusters import ClusterStore, SplitOutcome, kmeans_split_points
 from .fsm import PatternHint, PatternTable
-from .kernels import batch_distances
 from .concurrency import RWLock, TaskRunner
 from .core import (
     STATIC_SCOPE,
@@ -42,6 +45,7 @@ from .core import (
     as_vector,
 )
 from .index import DeviceIndex
+from .rowstore import RowStore
 from .kernels import centroid as vector_mean
 from .kernels import deviation as vector_spread
 from .tiering import TierManager
@@ -163,6 +167,13 @@ class ScopeCodes:
     def mask_codes(self, scopes) -> np.ndarray:
         return np.asarray(sorted(self.intern(s) for s in scopes), dtype=np.int16)
 
+    def lut(self, scopes):
+        """(boolean table over codes, hashable key) of a scope set."""
+        codes = tuple(sorted(self.intern(s) for s in scopes))
+        t = np.zeros(max(len(self.name), 1) + 1, dtype=bool)
+        t[list(codes)] = True
+        return t, codes
+
 
 def profile_reorder(entries, default_order):
     """ref/graph.py:441-451."""
@@ -232,6 +243,13 @@ class Store:
             ef_search_factor=cfg.ef_search_factor, alpha_ic=cfg.alpha_ic,
         )
         self.graph = self.clusters.graph
+        # HBM rows of the agent policy's small vector sets (pools, L1
+        # centroids, staged items, FSM states), one slot each
+        self.rows = RowStore(self.index, cfg.dimension)
+        self.clusters.rows = self.rows
+        self._drows: dict[str, list] = {}  # per agent: D rows of its request sequence
+        self._qrow_memo: dict = {}  # per agent: the last hinted query's D row
+        self._list_cap = 2 * cfg.split_target  # rows per probed list the agent pass reserves
         self.runner = TaskRunner(cfg.threads)
         self.tier = TierManager(self.clusters, self.index, budget_bytes=cfg.budget_bytes,
                                 b_insert=cfg.b_insert, decay_half_life=cfg.decay_half_life,
@@ -277,11 +295,12 @@ class Store:
         self.caches[agent_id] = MultiLevelCache(
             agent_id, c.dimension, self.metric, self.scope_codes, n_p=c.n_p,
             l0_capacity=c.l0_capacity, l1_capacity=c.l1_capacity, kappa=c.kappa,
-            alpha_et=c.alpha_et, window_w=c.window_w, verify_mode=c.verify_mode)
+            alpha_et=c.alpha_et, window_w=c.window_w, verify_mode=c.verify_mode, rows=self.rows)
         self.patterns[agent_id] = PatternTable(n_p=c.n_p, n_s=c.n_s, metric=self.metric,
                                                theta_match=c.theta_match,
-                                               d_merge_factor=c.d_merge_factor)
+                                               d_merge_factor=c.d_merge_factor, rows=self.rows)
         self.sequences[agent_id] = []
+        self._drows[agent_id] = []
         self._agent_locks[agent_id] = threading.RLock()
         return agent_id
 
@@ -295,9 +314,18 @@ class Store:
             self.clusters.unstage(agent_id, item_id)
             self.payloads.pop(item_id, None)
         self.agents.discard(agent_id)
-        self.caches.pop(agent_id, None)
-        self.patterns.pop(agent_id, None)
+        cache = self.caches.pop(agent_id, None)
+        if cache is not None:
+            for entry in cache.l0.values():
+                entry.pool.release()
+            for cl in cache.l1:
+                cl.release(self.rows)
+        table = self.patterns.pop(agent_id, None)
+        if table is not None:
+            for _, sl in table._slots:
+                self.rows.free_many(sl)
         del self.sequences[agent_id]
+        self._drows.pop(agent_id, None)
         del self._agent_locks[agent_id]
 
     def registered_scopes(self) -> list[str]:
@@ -459,21 +487,69 @@ class Store:
     def _search_read_phase(self, agent, scopes, q, k, nprobe, internal, no_cache=False):
         """Store._search_read_phase (ref/engine.py:319-404) for one query:
         cache levels, staged items, coarse, probed lists with per-list early
-        termination, _topk to max(k, kappa k).  Distances come from the
-        device: the cache pools in one call, the staged rows in one call, every
-        probed list's rows in one call (pk_scan_lists); the stop rules run on
-        those values in the reference's scan order."""
+        termination, _topk to max(k, kappa k).  Every distance comes out of
+        ONE device pass (pk_agent_read): the FSM states (hint), the cache's
+        pool rows and L1 centroids, the staged rows, the reference's coarse
+        traversal and every row of the lists it probes (computed whether or
+        not the cache stops first -- a few microseconds of device time against
+        a round trip).  The hint, the scan orders and the stop rules then run
+        over those values in the reference's order."""
         exhaustive_edge = k >= self.clusters.live_count()
         stats = SearchStats()
-        scope_mask = self.scope_codes.mask_codes(scopes)
-        hint = self._hint_for(agent, q) if not internal else PatternHint()
-        id_chunks, dist_chunks, scan_chunks = [], [], []
         use_cache = self.cfg.cache_enabled and agent and not no_cache
         cache = self.caches.get(agent) if use_cache else None
+        table = self.patterns.get(agent) if (agent and self.cfg.pattern_enabled and not internal) else None
+        lut, key = self.scope_codes.lut(scopes)
+        rows = self.rows
+        with rows.lock:
+            parts = []
+            plan = cache.read_plan(lut, key) if cache is not None else None
+            if plan is not None:
+                parts.append(plan["slots"])
+            staged_parts = []
+            for sc in sorted(scopes):  # staging areas: items not yet merged into clusters
+                ss = self.clusters.staged_slots.get(sc)
+                if ss:
+                    ids = np.fromiter(ss.keys(), dtype=np.int64, count=len(ss))
+                    sl = np.fromiter(ss.values(), dtype=np.int32, count=len(ss))
+                    staged_parts.append(ids)
+                    parts.append(sl)
+            st_slots = table.state_slots() if table is not None else np.empty(0, np.int32)
+            parts.append(st_slots)
+            listing, lslots = [], None
+            if table is not None and len(st_slots):
+                lcache = self.caches.get(agent)
+                if lcache is not None:
+                    listing, lslots = lcache.l1_listing_slots()
+            eff_nprobe, ef, mode = self._coarse_plan(k, nprobe)
+            dev_nprobe = 0
+            codes = None
+            if self.clusters.clusters:
+                in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
+                dev_nprobe = max(1, min(eff_nprobe, in_scope))
+                codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
+                self.graph.upload()
+            dall, SL, lists = self.index.agent_read(
+                q, rows.take_puts(), np.concatenate(parts), st_slots if listing else None,
+                lslots if listing else None, codes, dev_nprobe, ef, mode,
+                cap=dev_nprobe * self._list_cap)
+        if lists is not None and len(lists[3]) > dev_nprobe * self._list_cap:
+            self._list_cap = -(-len(lists[3]) // max(dev_nprobe, 1)) * 2
+        n_plan = len(plan["slots"]) if plan is not None else 0
+        at = n_plan
+        staged_d = []
+        for ids in staged_parts:
+            staged_d.append(dall[at:at + len(ids)])
+            at += len(ids)
+        q_row = dall[at:at + len(st_slots)]
+        hint = PatternHint()
+        if table is not None:
+            hint = self._hint_from(agent, q, q_row, listing, SL)
+        id_chunks, dist_chunks, scan_chunks = [], [], []
         early = False
         if cache is not None:
-            cres = cache.cached_search(q, k, scope_mask, hint_keys=hint.predicted_clusters,
-                                       termination_enabled=not exhaustive_edge)
+            cres = cache.replay(plan, dall[:n_plan], k, hint_keys=hint.predicted_clusters,
+                                termination_enabled=not exhaustive_edge)
             if len(cres.ids):
                 id_chunks.append(cres.ids)
                 dist_chunks.append(cres.dists)
@@ -484,27 +560,17 @@ class Store:
             stats.early_terminated = early
         if not early:
             stats.level_reached = "L2"
-            for sc in sorted(scopes):  # staging areas: items not yet merged into clusters
-                staged = self.clusters.staged.get(sc)
-                if not staged:
-                    continue
-                ids = np.fromiter(staged.keys(), dtype=np.int64, count=len(staged))
-                d = batch_distances(q, np.stack(list(staged.values())), self.metric)
+            for ids, d in zip(staged_parts, staged_d):
                 id_chunks.append(ids)
                 dist_chunks.append(d)
                 scan_chunks.append(ids)
                 stats.scanned_vectors += len(ids)
-            eff_nprobe, ef, mode = self._coarse_plan(k, nprobe)
-            in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
             selected = []
-            if self.clusters.clusters:
-                dev_nprobe = max(1, min(eff_nprobe, in_scope))
-                selected, stats.coarse_computations = self._coarse_select(q, scopes, dev_nprobe, ef,
-                                                                          mode)
+            if lists is not None:
+                cids, stats.coarse_computations, pre, all_ids, all_d = lists
+                selected = [int(c) for c in cids if c >= 0]
             thresh = cache.threshold() if (cache is not None and not exhaustive_edge) else None
             clusters = self.clusters.clusters
-            total = sum(clusters[c].size for c in selected)
-            all_ids, all_d, pre = self.index.scan_lists(q, selected, total)
             run = None
             if thresh is not None:  # stop rule over everything scanned so far
                 run = RunningKth(k)
@@ -536,14 +602,54 @@ class Store:
         scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
         return SearchResult(extended[:k], stats, scan_ids), hint, extended
 
-    def _coarse_select(self, q, scopes, nprobe: int, ef: int, mode: int):
-        """The reference's coarse traversal for one query (HybridGraphIndex.
-        search / search_independent, ref/graph.py:321-422) on the device:
-        (probed cids in (distance, cid) order, distance computations)."""
-        codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
-        self.graph.upload()
-        cids, coarse = self.index.graph_probe(q[None, :], codes, nprobe, ef, mode)
-        return [int(c) for c in cids[0] if c >= 0], int(coarse[0])
+    # --- request sequences and their FSM distance rows ----------------------
+    def _rows_for(self, agent, vecs):
+        """D rows (distances to every pattern state, D's column layout) of
+        request vectors, one device call."""
+        table = self.patterns[agent]
+        with self.rows.lock:
+            st = table.state_slots()
+            if not len(st) or not len(vecs):
+                return [np.empty(0, np.float32) for _ in vecs]
+            tmp = np.fromiter((self.rows.alloc(v) for v in vecs), dtype=np.int32, count=len(vecs))
+            _, M, _ = self.index.agent_read(vecs[0], self.rows.take_puts(), np.empty(0, np.int32), tmp, st)
+            self.rows.free_many(tmp)
+        return [M[i].copy() for i in range(len(vecs))]
+
+    def _seq_D(self, agent, last=None, last_row=None, window=None):
+        """D = (request prefix [+ last]) x every pattern state: the cached
+        rows, recomputed when missing or older than the patterns."""
+        table = self.patterns[agent]
+        seq = self.sequences[agent]
+        drows = self._drows[agent]
+        lo = 0 if window is None else max(0, len(seq) - window)
+        need = [i for i in range(lo, len(seq)) if drows[i] is None or drows[i][0] != table.version]
+        if need:
+            fresh = self._rows_for(agent, [seq[i] for i in need])
+            for i, r in zip(need, fresh):
+                drows[i] = (table.version, r)
+        rows_ = [drows[i][1] for i in range(lo, len(seq))]
+        if last is not None:
+            if last_row is None:
+                last_row = self._rows_for(agent, [last])[0]
+            rows_.append(last_row)
+        if not rows_:
+            return None
+        return np.stack(rows_)
+
+    def _hint_from(self, agent, q, q_row, listing, SL) -> PatternHint:
+        """ref/engine.py:428-435 over the search's device values."""
+        table = self.patterns[agent]
+        w = self.cfg.request_window - 1
+        prefix = self.sequences[agent][-w:] + [q] if w > 0 else [q]
+        D = self._seq_D(agent, q, q_row, window=w) if table.fsms else None
+        hint = table.match_and_predict(prefix, [(c, None) for c in listing], D,
+                                       SL if listing else None)
+        # the side effects key L0 by the same prefix's match: remember it
+        self._match_memo[agent] = (q.tobytes(), len(self.sequences[agent]), hint.matched_fsm, q_row,
+                                   table.version)
+        self._qrow_memo[agent] = (q.tobytes(), len(self.sequences[agent]), q_row, table.version)
+        return hint
 
     def _topk(self, id_chunks, dist_chunks, k):
         """ref/engine.py:406-426: lexsort by (dist, id), first occurrence per
@@ -581,32 +687,26 @@ class Store:
                 return hits
             take = min(n, 4 * take)
 
-    def _hint_for(self, agent, q) -> PatternHint:
-        """ref/engine.py:428-435."""
-        if not (agent and self.cfg.pattern_enabled):
-            return PatternHint()
-        cache = self.caches.get(agent)
-        listing = cache.l1_listing() if cache else None
-        prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [q]
-        hint = self.patterns[agent].match_and_predict(prefix, listing)
-        # the side effects key L0 by the same prefix's match: remember it
-        self._match_memo[agent] = (q.tobytes(), len(self.sequences[agent]), hint.matched_fsm)
-        return hint
-
-    def _state_key_for(self, agent, v):
+    def _state_key_for(self, agent, v, v_row=None):
         """ref/engine.py:437-446: the matched pattern's aligned state keys L0."""
         if not self.cfg.pattern_enabled:
             return DEFAULT_KEY
         table = self.patterns[agent]
         memo = self._match_memo.pop(agent, None)
-        if memo is not None and memo[0] == v.tobytes() and memo[1] == len(self.sequences[agent]):
-            idx = memo[2]  # same prefix, same table: the hint's match
+        if memo is not None and memo[0] == v.tobytes() and memo[1] == len(self.sequences[agent]) \
+                and memo[4] == table.version:
+            idx, row = memo[2], memo[3]  # same prefix, same table: the hint's match
         else:
             prefix = self.sequences[agent][-(self.cfg.request_window - 1):] + [v]
-            idx, _ = table.match(prefix)
+            D = self._seq_D(agent, v, v_row, window=self.cfg.request_window - 1) if table.fsms else None
+            idx, _ = table.match(prefix, D)
+            row = None if D is None else D[-1]
         if idx is None:
             return DEFAULT_KEY
-        return (idx, table.fsms[idx].align(v, self.metric))
+        if row is None:
+            return (idx, table.fsms[idx].align(v, self.metric))
+        off = table._offsets()[idx]
+        return (idx, int(np.argmin(row[off:off + len(table.fsms[idx].states)])))
 
     def _cache_items(self, hits):
         out = []
@@ -628,8 +728,8 @@ class Store:
             elif cache.verify_mode and not internal:
                 self.runner.submit("search", self._verify_early_return, agent, q, k, result)
             state_key = self._state_key_for(agent, q)
-            outcomes = cache.promote_to_l0(self._cache_items(result.hits), state_key)
-            outcomes += cache.l1_capture(q, self._cache_items(extended))
+            outcomes = cache.promote_and_capture(self._cache_items(result.hits), state_key, q,
+                                                 self._cache_items(extended))
             if any(not o.empty for o in outcomes):
                 with self._lock.write():
                     self._materialize(agent, outcomes)
@@ -645,7 +745,12 @@ class Store:
                 cl.profiles[agent] = profile_promote(cl.profiles.get(agent, []), rows,
                                                      self.cfg.p_size)
         if not internal:
-            self._append_sequence(agent, q)
+            memo_row = None
+            m = self._qrow_memo.pop(agent, None)
+            if m is not None and m[0] == q.tobytes() and m[1] == len(self.sequences[agent]) \
+                    and m[3] == self.patterns[agent].version:
+                memo_row = m[2]
+            self._append_sequence(agent, q, memo_row)
             if self.cfg.prefetch_enabled and not hint.empty:
                 self.prefetch(agent, hint, k)
 
@@ -730,6 +835,10 @@ class Store:
         assigned = None
         assigned_from = -1
         cache = self.caches.get(agent) if (self.cfg.cache_enabled and agent) else None
+        # the vectors' FSM distance rows (state keys, request prefix): one call
+        vrows = [None] * n
+        if agent is not None and self.cfg.pattern_enabled and self.patterns[agent].fsms:
+            vrows = self._rows_for(agent, vecs)
         while i < n:
             vec = vecs[i]
             iid = self._take_id(ids[i] if ids is not None else None)
@@ -738,11 +847,11 @@ class Store:
                 payload = payload.encode("utf-8")
             self.payloads[iid] = payload
             if cache is not None:  # staged, owned by the agent's cache until merge-down
-                state_key = self._state_key_for(agent, vec)
+                state_key = self._state_key_for(agent, vec, vrows[i])
                 self.clusters.stage_item(scope, iid, vec)
                 self._materialize(agent, cache.promote_to_l0(
                     [(iid, vec, self.scope_codes.intern(scope), True)], state_key))
-                self._append_sequence(agent, vec)
+                self._append_sequence(agent, vec, vrows[i])
                 accepted.append(iid)
                 i += 1
                 assigned = None  # a merge-down may have created clusters
@@ -752,7 +861,7 @@ class Store:
                 self.clusters.create_cluster(scope, [(iid, vec)])
                 assigned = None
                 if agent is not None:
-                    self._append_sequence(agent, vec)
+                    self._append_sequence(agent, vec, vrows[i])
                 accepted.append(iid)
                 i += 1
                 continue
@@ -780,7 +889,7 @@ class Store:
                 assigned = None  # a centroid moved: later vectors re-assign
             if agent is not None:
                 for t in range(i, j):
-                    self._append_sequence(agent, vecs[t])
+                    self._append_sequence(agent, vecs[t], vrows[t])
             accepted.extend(run_ids)
             i = j
         return accepted
@@ -904,14 +1013,20 @@ class Store:
             raise UsageError(f"unknown agent {agent!r}")
         seq = self.sequences[agent]
         if seq and self.cfg.pattern_enabled:
-            self.patterns[agent].observe_completed(seq)
+            table = self.patterns[agent]
+            D = self._seq_D(agent) if table.fsms else None
+            table.observe_completed(seq, D)
         self.sequences[agent] = []
+        self._drows[agent] = []
 
-    def _append_sequence(self, agent: str, v: np.ndarray):
+    def _append_sequence(self, agent: str, v: np.ndarray, row=None):
         seq = self.sequences[agent]
+        drows = self._drows[agent]
         seq.append(v)
+        drows.append(None if row is None else (self.patterns[agent].version, row))
         if len(seq) > self.cfg.request_window:
             del seq[0]
+            del drows[0]
 
     def flush_caches(self):
         """ref/engine.py:739-743: merge every cache level down."""

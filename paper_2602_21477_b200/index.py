@@ -339,6 +339,90 @@ class DeviceIndex:
                                       N.ptr(pre)))
         return ids[:pre[-1]], dd[:pre[-1]], pre
 
+    # ---- agent path: one device pass per agent search (pk_agent.cu) ---------
+    def rows_put(self, slots, rows):
+        """Rows into the HBM row store at the given slots (pk_rows_put)."""
+        self.flush()
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        rows = N.f32(rows, self.dimension)
+        N.check(N.lib().pk_rows_put(self._h, N.ptr(slots), N.ptr(rows), len(slots)))
+
+    def agent_read(self, q, puts, slots, mq=None, mx=None, scope_codes=None, nprobe: int = 0,
+                   ef: int = 0, mode: int = 0, cap: int = 0):
+        """pk_agent_read: (d f32[len(slots)], m f32[len(mq), len(mx)],
+        lists) where lists = (cids i64[nprobe], coarse, prefix i64[nprobe+1],
+        ids, dists) or None when nprobe == 0."""
+        self.flush()
+        q = N.f32(q).reshape(-1)
+        ps, pr = puts if puts is not None else (None, None)
+        nput = 0 if ps is None else len(ps)
+        if nput:
+            ps = np.ascontiguousarray(ps, dtype=np.int32)
+            pr = N.f32(pr, self.dimension)
+        slots = np.ascontiguousarray(slots, dtype=np.int32)
+        out_d = np.empty(max(len(slots), 1), dtype=np.float32)
+        nmq = 0 if mq is None else len(mq)
+        nmx = 0 if mx is None else len(mx)
+        if nmq and nmx:
+            mq = np.ascontiguousarray(mq, dtype=np.int32)
+            mx = np.ascontiguousarray(mx, dtype=np.int32)
+        else:
+            nmq = nmx = 0
+        out_m = np.empty((max(nmq, 1), max(nmx, 1)), dtype=np.float32)
+        lists = None
+        if nprobe > 0:
+            codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+            cids = np.empty(nprobe, dtype=np.int64)
+            coarse = ctypes.c_int32(0)
+            pre = np.zeros(nprobe + 1, dtype=np.int64)
+            cap = max(int(cap), 1)
+            while True:
+                ids = np.empty(cap, dtype=np.int64)
+                dd = np.empty(cap, dtype=np.float32)
+                rc = N.lib().pk_agent_read(
+                    self._h, N.ptr(q), N.ptr(ps) if nput else None, N.ptr(pr) if nput else None, nput,
+                    N.ptr(slots), len(slots), N.ptr(out_d), N.ptr(mq) if nmq else None, nmq,
+                    N.ptr(mx) if nmx else None, nmx, N.ptr(out_m), N.ptr(codes), len(codes), int(nprobe),
+                    int(ef), int(mode), N.ptr(cids), ctypes.byref(coarse), N.ptr(pre), N.ptr(ids), N.ptr(dd),
+                    cap)
+                if rc != 0 and pre[-1] > cap:  # more rows than the guess: the puts are in; ask again
+                    cap = int(pre[-1])
+                    nput = 0
+                    continue
+                N.check(rc)
+                break
+            t = int(pre[-1])
+            lists = (cids, int(coarse.value), pre, ids[:t], dd[:t])
+        else:
+            N.check(N.lib().pk_agent_read(
+                self._h, N.ptr(q), N.ptr(ps) if nput else None, N.ptr(pr) if nput else None, nput,
+                N.ptr(slots), len(slots), N.ptr(out_d), N.ptr(mq) if nmq else None, nmq,
+                N.ptr(mx) if nmx else None, nmx, N.ptr(out_m), None, 0, 0, 0, 0, None, None, None, None,
+                None, 0))
+        return out_d[:len(slots)], out_m[:nmq, :nmx], lists
+
+    def l1_place(self, nc, n_p, capacity, sums, cents, counts, items, item_ids, holder, q=None):
+        """pk_l1_place: (targets i32[m], added u8[m], q target or None)."""
+        self.flush()
+        d = self.dimension
+        m = len(items)
+        sums = np.ascontiguousarray(sums, dtype=np.float64).reshape(nc, d)
+        cents = N.f32(cents).reshape(nc, d)
+        counts = np.ascontiguousarray(counts, dtype=np.int32)
+        items = N.f32(items).reshape(m, d)
+        holder = np.ascontiguousarray(holder, dtype=np.int32)
+        item_ids = np.ascontiguousarray(item_ids, dtype=np.int64)
+        qv = None if q is None else N.f32(q).reshape(d)
+        tg = np.empty(max(m, 1), dtype=np.int32)
+        added = np.empty(max(m, 1), dtype=np.uint8)
+        merged = np.empty(max(m, 1), dtype=np.uint8)
+        qt = ctypes.c_int32(-3)
+        N.check(N.lib().pk_l1_place(self._h, int(nc), int(n_p), int(capacity), N.ptr(sums), N.ptr(cents),
+                                    N.ptr(counts), N.ptr(items), N.ptr(item_ids), N.ptr(holder), m, N.ptr(qv),
+                                    N.ptr(tg),
+                                    N.ptr(added), N.ptr(merged), ctypes.byref(qt)))
+        return tg[:m].tolist(), added[:m].tolist(), (int(qt.value) if q is not None else None)
+
     # ---- cold tier (TierManager residency, ref/tiering.py:175-448) --------
     TIER_STATS = ("resident_lists", "cold_lists", "resident_bytes", "staged_lists_last",
                   "staged_bytes_last", "staged_bytes_total", "staged_searches",

@@ -501,6 +501,30 @@ class ShardedStoreIndex:
         cat = (lambda xs, dt: np.concatenate(xs) if xs else np.empty(0, dtype=dt))
         return cat(out_ids, np.int64), cat(out_d, np.float32), pre
 
+    # ---- agent path: the row store is per rank (the policy is replicated) ----------
+    def rows_put(self, slots, rows):
+        self.local.rows_put(slots, rows)
+
+    def l1_place(self, *args, **kw):
+        return self.local.l1_place(*args, **kw)
+
+    def agent_read(self, q, puts, slots, mq=None, mx=None, scope_codes=None, nprobe: int = 0,
+                   ef: int = 0, mode: int = 0, cap: int = 0):
+        """pk_agent_read for the replicated rows on this rank, then the
+        coarse traversal (replicated centroids) and the owners' list scans."""
+        d, m, _ = self.local.agent_read(q, puts, slots, mq, mx)
+        lists = None
+        if nprobe > 0:
+            cids, coarse = self.local.graph_probe(np.asarray(q, np.float32)[None, :], scope_codes, nprobe,
+                                                  ef, mode)
+            sel = [int(c) for c in cids[0] if c >= 0]
+            ids, dd, pre_sel = self.scan_lists(q, sel, 0)
+            pre = np.zeros(nprobe + 1, dtype=np.int64)
+            pre[1:len(sel) + 1] = pre_sel[1:]
+            pre[len(sel) + 1:] = pre_sel[-1]
+            lists = (cids[0], int(coarse[0]), pre, ids, dd)
+        return d, m, lists
+
     # ---- tier / lifecycle ----------------------------------------------------------
     def enable_tier(self, reserve_rows: int = 0):
         raise UsageError("the native cold tier is per GPU; a sharded Store keeps every list in HBM")

@@ -503,10 +503,17 @@ def test_nprobe_above_device_pick_limit(pk):
     store.load_lists("static", lists)
     model.load("static", lists)
     Q = rng.normal(size=(4, d)).astype(np.float32)
+    code = [store.scope_codes.intern("static")]
     for nprobe in (2100, 2300, 5000):
         res = store.search_batch(None, ["static"], Q, 10, nprobe, want_scan_ids=True)
+        eff, ef, mode = store._coarse_plan(10, nprobe)
         for b in range(len(Q)):
-            hits, scanned, scan_ids = model.search(["static"], Q[b], 10, nprobe)
+            # the probe set is the coarse graph's (its parity with the
+            # reference: tests/test_gpu_graph.py); a random 2300-node graph
+            # need not be connected, so even exhaustive ef is not flat here
+            cids, _ = store.index.graph_probe(Q[b:b + 1], code, min(eff, nlist), ef, mode)
+            probe = [int(c) for c in cids[0] if c >= 0]
+            hits, scanned, scan_ids = model.search(["static"], Q[b], 10, nprobe, probe=probe)
             one = store.search(None, ["static"], Q[b], 10, nprobe)
             for r in (res[b], one):
                 assert r.ids == [h[0] for h in hits]

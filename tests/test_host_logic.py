@@ -105,10 +105,14 @@ def test_vector_pool_matches_list_model(ordered):
     pools) keeps the reference's row order (ref/pool.py:33-144)."""
     from paper_2602_21477_b200.pool import VectorPool
 
+    from paper_2602_21477_b200.rowstore import RowStore
+
     rng = np.random.default_rng(11 if ordered else 12)
     d = 5
-    pool = VectorPool(d, ordered=ordered)
+    store = RowStore(None, d)  # slots only: the uploads are checked, not sent
+    pool = VectorPool(d, ordered=ordered, rows=store)
     model = []  # [(id, vec, scope, staged)] in scan order
+    dev = {}  # what the device row store would hold: slot -> row
     nid = 0
     for step in range(3000):
         op = rng.integers(0, 4)
@@ -147,6 +151,21 @@ def test_vector_pool_matches_list_model(ordered):
             assert pool.staged_flag(model[j][0]) == model[j][3]
             assert [r[0] for r in pool.rows()] == [m[0] for m in model]
             assert pool.scope_mask([1]).tolist() == [m[2] == 1 for m in model]
+            lut = np.zeros(4, dtype=bool)
+            lut[1] = True
+            ids, sl = pool.in_scope(lut, (1,))
+            assert ids.tolist() == [m[0] for m in model if m[2] == 1]
+        # every live row's slot is distinct, and after applying the queued
+        # uploads the slot holds exactly that row (freed slots never leak)
+        ps, pr = store.take_puts()
+        if ps is not None:
+            for s_, r_ in zip(ps.tolist(), pr):
+                dev[s_] = r_
+        slots = pool.slots.tolist()
+        assert len(set(slots)) == len(slots) and min(slots, default=0) >= 0
+        assert store.live == len(model)
+        for s_, m in zip(slots, model):
+            assert np.array_equal(dev[s_], m[1])
 
 
 def test_running_kth_equals_kth_smallest():
