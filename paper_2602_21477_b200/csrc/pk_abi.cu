@@ -227,6 +227,8 @@ struct pk_index {
   // centroids, FSM states) at host-managed slots, packed staging and outputs
   DevBuf arows;  // [acap][dp]
   int64_t acap = 0;
+  cudaStream_t ast = nullptr;  // row-store distances beside the coarse traversal
+  cudaEvent_t ev_ag0 = nullptr, ev_ag1 = nullptr;
   PinnedBuf hag;  // mapped: packed inputs, then the kernels' outputs
   DevBuf ag_in, ag_l1;
   // front-half overlap: the next batch's prep / coarse / pick / routing run on
@@ -236,7 +238,11 @@ struct pk_index {
   // re-rank (index stream, after ev_sdone) runs beside the NEXT batch's scan
   cudaStream_t sst = nullptr;
   cudaEvent_t ev_front = nullptr, ev_scan = nullptr, front_wait = nullptr, ev_sdone = nullptr;
-  bool rr_lean = true;  // PK_RERANK_LEAN=0: the wide re-rank after the scan, as before
+  // lean re-rank beside the next scan: -1 = for batches up to 64 queries
+  // (configs[0]: +1%; at 256 queries it lengthened the step),
+  // PK_RERANK_LEAN=0/1 forces it off / on
+  int rr_lean = -1;
+  int rr_lean_ctas = 148;  // PK_RERANK_LEAN_CTAS: the lean grid (default: one per SM)
   uint64_t ev_scan_n = 0;  // lock count when ev_scan was last recorded
   bool pipeline = true;    // PK_PIPELINE=0 turns the overlap off
   DevBuf assign_q, assign_qn, assign_dc, assign_c, assign_d;
@@ -324,10 +330,14 @@ struct pk_index {
     int32_t npor = 0;
     std::unordered_map<int32_t, std::pair<int32_t, int32_t>> entry;  // scope code -> (slot, max level)
     std::vector<uint8_t> hflags;
+    std::vector<int32_t> flags_codes;  // scope set the device flags were built for
+    uint64_t flags_ver = 0;
+    int32_t flags_ns = 0;
     void release() {
       for (DevBuf* b : {&level, &nbr0, &up_off, &up, &por_off, &por, &rank, &slot_of_rank, &flags,
                         &stamps, &heap, &count})
         b->release();
+      flags_codes.clear();
     }
   } graph;
   bool stage_pending = false;   // `staged` holds ranges of an enqueued batch
@@ -944,7 +954,9 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   }
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
   if (const char* e = getenv("PK_PIPELINE")) ix->pipeline = atoi(e) != 0;
-  if (const char* e = getenv("PK_RERANK_LEAN")) ix->rr_lean = atoi(e) != 0;
+  if (const char* e = getenv("PK_RERANK_LEAN")) ix->rr_lean = atoi(e) != 0 ? 1 : 0;
+  ix->rr_lean_ctas = ix->num_sms;
+  if (const char* e = getenv("PK_RERANK_LEAN_CTAS")) ix->rr_lean_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("PK_QGATHER")) ix->qgather = atoi(e) != 0;
   if (const char* e = getenv("PK_STAGE")) ix->stage_dma = strcmp(e, "dma") == 0;
   if (const char* e = getenv("PK_COARSE")) {
@@ -1022,6 +1034,12 @@ int pk_index_destroy(pk_index* ix) {
     cudaStreamSynchronize(ix->sst);
     cudaStreamDestroy(ix->sst);
   }
+  if (ix->ast) {
+    cudaStreamSynchronize(ix->ast);
+    cudaStreamDestroy(ix->ast);
+  }
+  for (cudaEvent_t e : {ix->ev_ag0, ix->ev_ag1})
+    if (e) cudaEventDestroy(e);
   for (cudaEvent_t e : {ix->ev_front, ix->ev_scan, ix->ev_sdone})
     if (e) cudaEventDestroy(e);
   for (uint8_t* p : ix->comb.opened) cudaIpcCloseMemHandle(p);
@@ -1588,17 +1606,27 @@ static int graph_coarse(pk_index* ix, pk_index::Scratch& S, int64_t B, const int
   launch_dist_dense(ix->metric, S.q.as<float>(), dp, (int)B, ix->d_cent, dp, ix->nslots, (int)dp,
                     S.qnorm.as<float>(), S.dc.as<float>(), ns, fs);
   GraphQuery gq = {};
-  G.hflags.assign(ns, 0);
-  for (int32_t sl = 0; sl < ix->nslots; sl++) {
-    if (ix->h_cid[sl] < 0) continue;
-    const int32_t c = ix->h_scope[sl];
-    uint8_t f = c == G.static_code ? 2 : 0;
-    for (int i = 0; i < nscopes; i++)
-      if (codes[i] == c) f = 3;
-    G.hflags[sl] = f;
+  // per-slot scope flags: rebuilt (and uploaded) only when the scope set or
+  // the list table changed since the last traversal (agent searches repeat
+  // the same scope set query after query)
+  std::vector<int32_t> key(codes, codes + nscopes);
+  std::sort(key.begin(), key.end());
+  if (key != G.flags_codes || G.flags_ver != ix->tver || G.flags_ns != ns) {
+    G.hflags.assign(ns, 0);
+    for (int32_t sl = 0; sl < ix->nslots; sl++) {
+      if (ix->h_cid[sl] < 0) continue;
+      const int32_t c = ix->h_scope[sl];
+      uint8_t f = c == G.static_code ? 2 : 0;
+      for (int i = 0; i < nscopes; i++)
+        if (codes[i] == c) f = 3;
+      G.hflags[sl] = f;
+    }
+    RET(G.flags.ensure(ns));
+    CK(cudaMemcpyAsync(G.flags.p, G.hflags.data(), ns, cudaMemcpyHostToDevice, fs));
+    G.flags_codes = key;
+    G.flags_ver = ix->tver;
+    G.flags_ns = ns;
   }
-  RET(G.flags.ensure(ns));
-  CK(cudaMemcpyAsync(G.flags.p, G.hflags.data(), ns, cudaMemcpyHostToDevice, fs));
   gq.flags = G.flags.as<uint8_t>();
   gq.static_entry = -1;
   auto st_it = G.entry.find(G.static_code);
@@ -1923,7 +1951,8 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                         // waiting on the SMs the scan tail frees for the next front half
                         /*pdl=*/!pipelined,
                         // pipelined: lean CTAs beside the next batch's scan (at most one per SM)
-                        (pipelined && ix->tensor && ix->rr_lean && rerank_lean_fits((int)dp)) ? ix->num_sms : 0);
+                        (pipelined && ix->tensor && (ix->rr_lean > 0 || (ix->rr_lean < 0 && B <= 64)) &&
+                         rerank_lean_fits((int)dp)) ? ix->rr_lean_ctas : 0);
   else
     launch_merge((int)B, S.slot_off.as<int32_t>(), S.cand_key.as<uint32_t>(),
                  S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(), kk,
@@ -2284,6 +2313,7 @@ int pk_graph_set(pk_index* ix, int32_t M, int64_t n, const int64_t* node_cid, co
   CK(cudaStreamSynchronize(ix->st));  // pageable sources
   G.M = M;
   G.npor = (int32_t)porv.size();
+  G.flags_codes.clear();  // rebuilt for the new graph at the next traversal
   G.ns = ix->nslots;
   G.slot_ver = ix->slot_ver;
   G.static_code = static_code;
@@ -2544,16 +2574,46 @@ int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const 
   if (nmq) memcpy(h + o_mq, mq, (size_t)nmq * 4);
   if (nmx) memcpy(h + o_mx, mx, (size_t)nmx * 4);
   uint8_t* din = ix->ag_in.as<uint8_t>();
+  // PK_DEBUG_AGENT=1: per-phase device time (events; measurement only)
+  static const bool dbg = getenv("PK_DEBUG_AGENT") != nullptr;
+  static cudaEvent_t dev_[8];
+  static double dacc[8] = {0};
+  static long dcalls = 0;
+  static bool dinit = false;
+  if (dbg && !dinit) {
+    for (auto& e : dev_) cudaEventCreate(&e);
+    dinit = true;
+  }
+  auto mark = [&](int i) {
+    if (dbg) cudaEventRecord(dev_[i], st);
+  };
+  mark(0);
   CK(cudaMemcpyAsync(din, h, in_bytes, cudaMemcpyHostToDevice, st));
   const float* dq = reinterpret_cast<const float*>(din + o_q);
   float* arows = ix->arows.as<float>();
   if (nput)
     launch_rows_put(reinterpret_cast<const float*>(din + o_pr), reinterpret_cast<const int32_t*>(din + o_ps),
                     (int)nput, (int)dp, arows, st);
+  mark(1);
+  // the row-store distances run on a side stream, beside the coarse traversal
+  // and the list scan (independent inputs; joined before the sync)
+  if (!ix->ast) {
+    CK(cudaStreamCreateWithFlags(&ix->ast, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ix->ev_ag0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ix->ev_ag1, cudaEventDisableTiming));
+  }
+  cudaStream_t as = dbg ? st : ix->ast;
+  if (!dbg) {
+    CK(cudaEventRecord(ix->ev_ag0, st));
+    CK(cudaStreamWaitEvent(as, ix->ev_ag0, 0));
+  }
   launch_gather_dist(ix->metric, dq, arows, (int)dp, (int)d, reinterpret_cast<const int32_t*>(din + o_sl), (int)n,
-                     reinterpret_cast<float*>(hd + o_od), st);
+                     reinterpret_cast<float*>(hd + o_od), as);
+  mark(2);
   launch_gather_mat(ix->metric, arows, (int)dp, (int)d, reinterpret_cast<const int32_t*>(din + o_mq), nmq,
-                    reinterpret_cast<const int32_t*>(din + o_mx), nmx, reinterpret_cast<float*>(hd + o_om), st);
+                    reinterpret_cast<const int32_t*>(din + o_mx), nmx, reinterpret_cast<float*>(hd + o_om), as);
+  if (!dbg) CK(cudaEventRecord(ix->ev_ag1, as));
+  mark(3);
   int64_t* h_pre = reinterpret_cast<int64_t*>(h + o_pre);
   int64_t* h_cid = reinterpret_cast<int64_t*>(h + o_cid);
   if (lists) {
@@ -2570,6 +2630,7 @@ int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const 
     ga.mode = mode;
     ga.out_coarse = reinterpret_cast<int32_t*>(h + o_cnt);
     RET(graph_coarse(ix, S, 1, scope_codes, nscopes, nprobe, ga, st));
+    mark(4);
     if (!ix->tiered) {
       launch_probe_lists(ix->metric, S.q.as<float>(), ix->table(), S.probe.as<int32_t>(), nprobe, maxlen, rcap,
                          reinterpret_cast<float*>(hd + o_dd), reinterpret_cast<int64_t*>(hd + o_ids),
@@ -2618,8 +2679,23 @@ int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const 
       }
     }
   }
+  mark(5);
+  if (!dbg) CK(cudaStreamWaitEvent(st, ix->ev_ag1, 0));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));
+  if (dbg) {
+    float ms;
+    const int last = lists ? 5 : 3;
+    for (int i = 1; i <= last; i++) {
+      if (!lists && i > 3) break;
+      cudaEventElapsedTime(&ms, dev_[i - 1], dev_[i]);
+      dacc[i] += ms;
+    }
+    if (++dcalls % 512 == 0)
+      fprintf(stderr, "agent_read device us/call (%ld calls): h2d+puts %.1f gather %.1f mat %.1f coarse %.1f lists %.1f\n",
+              dcalls, 1e3 * dacc[1] / dcalls, 1e3 * dacc[2] / dcalls, 1e3 * dacc[3] / dcalls, 1e3 * dacc[4] / dcalls,
+              1e3 * dacc[5] / dcalls);
+  }
   if (n) memcpy(out_d, h + o_od, n * 4);
   if (nmq && nmx) memcpy(out_m, h + o_om, (size_t)nmq * nmx * 4);
   if (nprobe > 0) {
@@ -2649,6 +2725,10 @@ int pk_l1_place(pk_index* ix, int32_t nc, int32_t n_p, int32_t capacity, const d
   const int maxc = l1_place_max_clusters();
   if (n_p > maxc || nc + m > maxc)
     return fail(PK_ERR_USAGE, "L1 placement of %d items over %d clusters exceeds %d", m, nc, maxc);
+  if (nc > n_p) return fail(PK_ERR_USAGE, "%d live L1 clusters above n_p %d", nc, n_p);
+  if ((int64_t)(n_p + 1) * ix->dp * 4 > 227 * 1024)
+    return fail(PK_ERR_USAGE, "n_p %d x dimension %lld exceeds the placement kernel's shared memory", n_p,
+                (long long)ix->d);
   if (m == 0 && !q) return PK_OK;
   CK(cudaSetDevice(ix->device));
   cudaStream_t st = ix->st;

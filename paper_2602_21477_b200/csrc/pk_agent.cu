@@ -101,31 +101,104 @@ __global__ void rows_put_kernel(const float* __restrict__ src, const int32_t* __
   }
 }
 
-// out[i] = dist(q, rows[slots[i]]), one thread per row
+// Up to 128 rows (pointers in rowp[]) streamed through shared memory in
+// column blocks of W floats by coalesced 16-byte cp.async pieces (a 3-deep
+// ring; W wider when the block holds few rows), one thread per row running
+// the reference's sequential chain over the padded row from shared memory --
+// the rows' bytes arrive at streaming rate instead of one dependent global
+// load per float4 per thread.  (The padding columns are zero: they add +0.)
+constexpr int AG_RING = 3;
+constexpr int AG_RS = 32 + 4;
+constexpr size_t AG_RING_FLOATS = (size_t)AG_RING * 128 * AG_RS;
+template <int METRIC>
+__device__ __forceinline__ float staged_dist(const float* const* rowp, int nr, const float* qs, float qn, int dp,
+                                             float* ring) {
+  int W = (128 * AG_RS / max(nr, 1) - 4) / 32 * 32;
+  W = W < 32 ? 32 : (W > dp ? dp : W);
+  const int rs = W + 4;
+  const int nblk = (dp + W - 1) / W;
+  auto issue = [&](int blk) {
+    if (blk < nblk) {
+      float* dst = ring + (size_t)(blk % AG_RING) * 128 * AG_RS;
+      const int w4 = min(W, dp - blk * W) / 4;
+      for (int i = threadIdx.x; i < nr * w4; i += blockDim.x) {
+        const int rr = i / w4, c = i - rr * w4;
+        cp_async16(dst + rr * rs + 4 * c, rowp[rr] + blk * W + 4 * c);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < AG_RING - 1; i++) issue(i);
+  float acc = 0.f, nn = 0.f;
+  for (int blk = 0; blk < nblk; blk++) {
+    issue(blk + AG_RING - 1);
+    cp_async_wait<AG_RING - 1>();
+    __syncthreads();
+    const float* xr = ring + (size_t)(blk % AG_RING) * 128 * AG_RS + (threadIdx.x < nr ? threadIdx.x : 0) * rs;
+    const float* qb = qs + blk * W;
+    const int w = min(W, dp - blk * W);
+#pragma unroll 8
+    for (int j = 0; j < w; j += 4) {
+      const float4 xv = *reinterpret_cast<const float4*>(xr + j);
+      const float4 qv = *reinterpret_cast<const float4*>(qb + j);
+      if (METRIC == SQ_L2) {
+        acc = sq_step(acc, xv.x, qv.x);
+        acc = sq_step(acc, xv.y, qv.y);
+        acc = sq_step(acc, xv.z, qv.z);
+        acc = sq_step(acc, xv.w, qv.w);
+      } else {
+        acc = ip_step(acc, xv.x, qv.x);
+        acc = ip_step(acc, xv.y, qv.y);
+        acc = ip_step(acc, xv.z, qv.z);
+        acc = ip_step(acc, xv.w, qv.w);
+        if (METRIC == COSINE) {
+          nn = ip_step(nn, xv.x, xv.x);
+          nn = ip_step(nn, xv.y, xv.y);
+          nn = ip_step(nn, xv.z, xv.z);
+          nn = ip_step(nn, xv.w, xv.w);
+        }
+      }
+    }
+    __syncthreads();  // the slot is refilled by the next issue
+  }
+  return fin<METRIC>(acc, nn, qn);
+}
+
+// out[i] = dist(q, rows[slots[i]]): blocks of 128 rows
 template <int METRIC>
 __global__ void __launch_bounds__(128) gather_dist_kernel(const float* __restrict__ q, const float* __restrict__ rows,
                                                           int dp, int d, const int32_t* __restrict__ slots, int n,
-                                                          float* __restrict__ out) {
-  extern __shared__ __align__(16) float ag_q[];
+                                                          float* __restrict__ out, int rpb) {
+  extern __shared__ __align__(16) float ag_sm[];  // q [dp] | ring
+  __shared__ const float* rowp[128];
   __shared__ float qn_s;
-  stage_q<METRIC>(q, ag_q, &qn_s, dp, d);
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  out[i] = ref_dist<METRIC>(rows + (int64_t)slots[i] * dp, ag_q, d, METRIC == COSINE ? qn_s : 0.f);
+  const int i0 = blockIdx.x * rpb;
+  const int nr = min(rpb, n - i0);
+  if (threadIdx.x < nr) rowp[threadIdx.x] = rows + (int64_t)slots[i0 + threadIdx.x] * dp;
+  stage_q<METRIC>(q, ag_sm, &qn_s, dp, d);
+  const float v = staged_dist<METRIC>(rowp, nr, ag_sm, METRIC == COSINE ? qn_s : 0.f, dp, ag_sm + dp);
+  if (threadIdx.x < nr) out[i0 + threadIdx.x] = v;
 }
 
-// out[r][c] = dist(q = rows[qs[r]], x = rows[xs[c]]): the query roles of the
-// reference's _dmat(A, B) (ref/fsm.py; batch_distances(A[r], B))
+// out[r][c] = dist(q = rows[qslots[r]], x = rows[xslots[c]]): block (x, r)
+// covers columns [128 x, 128 x + 128) of query row r (the query roles of the
+// reference's _dmat(A, B): batch_distances(A[r], B), ref/fsm.py)
 template <int METRIC>
 __global__ void __launch_bounds__(128) gather_mat_kernel(const float* __restrict__ rows, int dp, int d,
                                                          const int32_t* __restrict__ qslots, int nr,
                                                          const int32_t* __restrict__ xslots, int nc,
                                                          float* __restrict__ out) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= (int64_t)nr * nc) return;
-  const int r = (int)(i / nc), c = (int)(i - (int64_t)r * nc);
-  const float* q = rows + (int64_t)qslots[r] * dp;
-  out[i] = ref_dist<METRIC>(rows + (int64_t)xslots[c] * dp, q, d, METRIC == COSINE ? seq_norm(q, d) : 0.f);
+  extern __shared__ __align__(16) float ag_sm[];
+  __shared__ const float* rowp[128];
+  __shared__ float qn_s;
+  const int r = blockIdx.y;
+  const int c0 = blockIdx.x * 128;
+  const int m = min(128, nc - c0);
+  if (threadIdx.x < m) rowp[threadIdx.x] = rows + (int64_t)xslots[c0 + threadIdx.x] * dp;
+  stage_q<METRIC>(rows + (int64_t)qslots[r] * dp, ag_sm, &qn_s, dp, d);
+  const float v = staged_dist<METRIC>(rowp, m, ag_sm, METRIC == COSINE ? qn_s : 0.f, dp, ag_sm + dp);
+  if (threadIdx.x < m) out[(int64_t)r * nc + c0 + threadIdx.x] = v;
 }
 
 // Every row of the probed lists (device probe slots, coarse order), laid out
@@ -135,19 +208,21 @@ __global__ void __launch_bounds__(128) probe_lists_kernel(const float* __restric
                                                           const int32_t* __restrict__ probe, int nprobe, int64_t cap,
                                                           float* __restrict__ out_d, int64_t* __restrict__ out_ids,
                                                           int64_t* __restrict__ out_prefix,
-                                                          int64_t* __restrict__ out_cids) {
-  extern __shared__ __align__(16) float ag_q[];
+                                                          int64_t* __restrict__ out_cids, int rpb) {
+  extern __shared__ __align__(16) float ag_sm[];
+  __shared__ const float* rowp[128];
   __shared__ float qn_s;
   __shared__ int64_t pre_s;
   const int p = blockIdx.y;
   const int sl = probe[p];
   const int64_t len = sl >= 0 ? lt.len[sl] : 0;
-  if ((int64_t)blockIdx.x * 128 >= len && !(blockIdx.x == 0)) return;
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  if (r0 >= len && blockIdx.x != 0) return;
   if (threadIdx.x == 0) {
     int64_t pre = 0;
     for (int i = 0; i < p; i++) {
-      const int s = probe[i];
-      pre += s >= 0 ? lt.len[s] : 0;
+      const int s2 = probe[i];
+      pre += s2 >= 0 ? lt.len[s2] : 0;
     }
     pre_s = pre;
     if (blockIdx.x == 0) {
@@ -156,12 +231,16 @@ __global__ void __launch_bounds__(128) probe_lists_kernel(const float* __restric
       if (p == 0) out_prefix[0] = 0;
     }
   }
-  stage_q<METRIC>(q, ag_q, &qn_s, lt.dp, lt.d);
-  const int64_t r = (int64_t)blockIdx.x * 128 + threadIdx.x;
-  if (r >= len || pre_s + r >= cap) return;  // past the caller's capacity: it sees the total and asks again
-  const int64_t arow = lt.off[sl] + r;
-  out_d[pre_s + r] = ref_dist<METRIC>(lt.rows + arow * lt.dp, ag_q, lt.d, METRIC == COSINE ? qn_s : 0.f);
-  out_ids[pre_s + r] = lt.ids[arow];
+  const int64_t left = len - r0;
+  const int nr = left <= 0 ? 0 : (left < rpb ? (int)left : rpb);
+  if (threadIdx.x < nr) rowp[threadIdx.x] = lt.rows + (lt.off[sl] + r0 + threadIdx.x) * lt.dp;
+  stage_q<METRIC>(q, ag_sm, &qn_s, lt.dp, lt.d);
+  if (nr == 0) return;
+  const float v = staged_dist<METRIC>(rowp, nr, ag_sm, METRIC == COSINE ? qn_s : 0.f, lt.dp, ag_sm + lt.dp);
+  const int64_t r = r0 + threadIdx.x;
+  if (threadIdx.x >= nr || pre_s + r >= cap) return;  // past the caller's capacity: it sees the total and asks again
+  out_d[pre_s + r] = v;
+  out_ids[pre_s + r] = lt.ids[lt.off[sl] + r];
 }
 
 // argmin order of np.argmin: the first minimum, NaN before everything
@@ -192,54 +271,62 @@ __global__ void __launch_bounds__(256) l1_place_kernel(int nc0, int n_p, int cap
                                                        const float* __restrict__ qv, int32_t* __restrict__ out_t,
                                                        uint8_t* __restrict__ out_added,
                                                        uint8_t* __restrict__ out_merged, int32_t* __restrict__ out_q) {
+  // the live clusters' centroids live in shared memory (n_p rows, a slot per
+  // live cluster) with the item being placed: every chain step reads shared
+  // memory, not L2
+  extern __shared__ __align__(16) float l1s[];  // [n_p][dp] centroids | [dp] item
+  float* vs = l1s + (size_t)n_p * dp;
   __shared__ int order[L1_MAXC];
   __shared__ uint8_t merged[L1_MAXC];
-  __shared__ int hold[L1_MAXC];  // per chain item: the cluster holding its id after it
+  __shared__ int hold[L1_MAXC];   // per chain item: the cluster holding its id after it
+  __shared__ int sslot[L1_MAXC];  // physical cluster -> shared-memory row
+  __shared__ int sfree[L1_MAXC];
   __shared__ float dist_s[L1_MAXC];
-  __shared__ int n_live, next_phys, s_tpos, s_add;
+  __shared__ int n_live, next_phys, s_tpos, s_add, n_free;
   const int tid = threadIdx.x;
   if (tid < L1_MAXC) {
     order[tid] = tid;
     merged[tid] = 0;
+    sslot[tid] = tid < nc0 ? tid : -1;
   }
   if (tid == 0) {
     n_live = nc0;
     next_phys = nc0;
+    n_free = 0;
+    for (int i = n_p - 1; i >= nc0; i--) sfree[n_free++] = i;
   }
+  for (int i = tid; i < nc0 * dp; i += blockDim.x) l1s[i] = cents[i];
   __syncthreads();
-  auto nearest = [&](const float* v) -> int {  // list position of the first nearest centroid
-    const int nl = n_live;
-    if (tid < nl) {
-      const float* c = cents + (int64_t)order[tid] * dp;
-      dist_s[tid] = ref_dist<METRIC>(c, v, d, METRIC == COSINE ? seq_norm(v, d) : 0.f);
-    }
-    __syncthreads();
-    int best = 0;
-    for (int i = 1; i < nl; i++)
-      if (am_better(dist_s[i], dist_s[best])) best = i;
-    __syncthreads();
-    return best;
-  };
   for (int it = 0; it <= m; it++) {
     const bool is_q = it == m;
     if (is_q && qv == nullptr) break;
     const float* v = is_q ? qv : items + (int64_t)it * dp;
-    int tpos;
-    if (n_live < n_p) {
-      tpos = -1;  // _nearest_l1 appends a fresh cluster
-    } else {
-      tpos = nearest(v);
+    for (int j = tid; j < dp; j += blockDim.x) vs[j] = v[j];
+    __syncthreads();
+    int tpos = -1;  // _nearest_l1 appends a fresh cluster while fewer than n_p
+    const int nl = n_live;
+    if (nl >= n_p) {  // the first nearest centroid (list order)
+      if (tid < nl) {
+        const float* c = l1s + (size_t)sslot[order[tid]] * dp;
+        dist_s[tid] = ref_dist<METRIC>(c, vs, d, METRIC == COSINE ? seq_norm(vs, d) : 0.f);
+      }
+      __syncthreads();
+      tpos = 0;
+      for (int i = 1; i < nl; i++)
+        if (am_better(dist_s[i], dist_s[tpos])) tpos = i;
     }
     if (is_q) {
       if (tid == 0) *out_q = tpos;
       break;
     }
+    __syncthreads();
     if (tid == 0) {
       int t;
       if (tpos < 0) {
         t = next_phys++;
         order[n_live++] = t;
         cnt[t] = 0;
+        sslot[t] = sfree[--n_free];
       } else {
         t = order[tpos];
       }
@@ -254,28 +341,30 @@ __global__ void __launch_bounds__(256) l1_place_kernel(int nc0, int n_p, int cap
     }
     __syncthreads();
     const int t = s_tpos;
+    float* cs = l1s + (size_t)sslot[t] * dp;
     if (s_add) {
       const int n1 = cnt[t] + 1;
       for (int j = tid; j < dp; j += blockDim.x) {
-        double* s = sums + (int64_t)t * dp + j;
-        const double nv = (tpos < 0 ? 0.0 : *s) + (double)items[(int64_t)it * dp + j];
-        *s = nv;
-        cents[(int64_t)t * dp + j] = (float)(nv / (double)n1);
+        double* sp = sums + (int64_t)t * dp + j;
+        const double nv = (tpos < 0 ? 0.0 : *sp) + (double)vs[j];
+        *sp = nv;
+        cs[j] = (float)(nv / (double)n1);
       }
       __syncthreads();
       if (tid == 0) cnt[t] = n1;
     } else if (tpos < 0) {
       for (int j = tid; j < dp; j += blockDim.x) {  // a fresh cluster that stays empty
         sums[(int64_t)t * dp + j] = 0.0;
-        cents[(int64_t)t * dp + j] = 0.f;
+        cs[j] = 0.f;
       }
     }
     __syncthreads();
     if (tid == 0) {
       const bool full = cnt[t] >= cap;
       out_merged[it] = full;
-      if (full) {  // merge_down: the cluster leaves the list
+      if (full) {  // merge_down: the cluster leaves the list, its row is free
         merged[t] = 1;
+        sfree[n_free++] = sslot[t];
         int w = 0;
         for (int i = 0; i < n_live; i++)
           if (order[i] != t) order[w++] = order[i];
@@ -295,55 +384,76 @@ void launch_rows_put(const float* src, const int32_t* slots, int n, int dp, floa
   rows_put_kernel<<<grid, 256, 0, st>>>(src, slots, n, dp, rows);
 }
 
+static size_t ag_smem(int dp) { return (size_t)dp * 4 + AG_RING_FLOATS * 4; }
+template <typename K>
+static void ag_attr(K k, size_t smem) {
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 void launch_gather_dist(int metric, const float* q, const float* rows, int dp, int d, const int32_t* slots, int n,
                         float* out, cudaStream_t st) {
   if (n <= 0) return;
-  const unsigned grid = (unsigned)((n + 127) / 128);
-  const size_t sm = (size_t)dp * 4;
-  if (metric == SQ_L2) gather_dist_kernel<SQ_L2><<<grid, 128, sm, st>>>(q, rows, dp, d, slots, n, out);
-  else if (metric == IP) gather_dist_kernel<IP><<<grid, 128, sm, st>>>(q, rows, dp, d, slots, n, out);
-  else gather_dist_kernel<COSINE><<<grid, 128, sm, st>>>(q, rows, dp, d, slots, n, out);
+  // fewer rows per block when a call would leave most SMs idle: wider column
+  // blocks, fewer ring round trips per block
+  int rpb = 128;
+  while (rpb > 32 && (n + rpb - 1) / rpb < 148) rpb >>= 1;
+  const unsigned grid = (unsigned)((n + rpb - 1) / rpb);
+  const size_t sm = ag_smem(dp);
+#define AG_GD(M)                                                                \
+  {                                                                           \
+    ag_attr(gather_dist_kernel<M>, sm);                                       \
+    gather_dist_kernel<M><<<grid, 128, sm, st>>>(q, rows, dp, d, slots, n, out, rpb); \
+  }
+  if (metric == SQ_L2) AG_GD(SQ_L2) else if (metric == IP) AG_GD(IP) else AG_GD(COSINE)
+#undef AG_GD
 }
 
 void launch_gather_mat(int metric, const float* rows, int dp, int d, const int32_t* qslots, int nr,
                        const int32_t* xslots, int nc, float* out, cudaStream_t st) {
-  const int64_t n = (int64_t)nr * nc;
-  if (n <= 0) return;
-  const unsigned grid = (unsigned)((n + 127) / 128);
-  if (metric == SQ_L2) gather_mat_kernel<SQ_L2><<<grid, 128, 0, st>>>(rows, dp, d, qslots, nr, xslots, nc, out);
-  else if (metric == IP) gather_mat_kernel<IP><<<grid, 128, 0, st>>>(rows, dp, d, qslots, nr, xslots, nc, out);
-  else gather_mat_kernel<COSINE><<<grid, 128, 0, st>>>(rows, dp, d, qslots, nr, xslots, nc, out);
+  if (nr <= 0 || nc <= 0) return;
+  const dim3 grid((unsigned)((nc + 127) / 128), (unsigned)nr);
+  const size_t sm = ag_smem(dp);
+#define AG_GM(M)                                                                          \
+  {                                                                                     \
+    ag_attr(gather_mat_kernel<M>, sm);                                                  \
+    gather_mat_kernel<M><<<grid, 128, sm, st>>>(rows, dp, d, qslots, nr, xslots, nc, out); \
+  }
+  if (metric == SQ_L2) AG_GM(SQ_L2) else if (metric == IP) AG_GM(IP) else AG_GM(COSINE)
+#undef AG_GM
 }
 
 void launch_probe_lists(int metric, const float* q, ListTable lt, const int32_t* probe, int nprobe,
-                        int64_t maxlen, int64_t cap, float* out_d, int64_t* out_ids, int64_t* out_prefix, int64_t* out_cids,
-                        cudaStream_t st) {
+                        int64_t maxlen, int64_t cap, float* out_d, int64_t* out_ids, int64_t* out_prefix,
+                        int64_t* out_cids, cudaStream_t st) {
   if (nprobe <= 0) return;
-  const dim3 grid((unsigned)std::max<int64_t>(1, (maxlen + 127) / 128), (unsigned)nprobe);
-  const size_t sm = (size_t)lt.dp * 4;
-  if (metric == SQ_L2)
-    probe_lists_kernel<SQ_L2><<<grid, 128, sm, st>>>(q, lt, probe, nprobe, cap, out_d, out_ids, out_prefix, out_cids);
-  else if (metric == IP)
-    probe_lists_kernel<IP><<<grid, 128, sm, st>>>(q, lt, probe, nprobe, cap, out_d, out_ids, out_prefix, out_cids);
-  else
-    probe_lists_kernel<COSINE><<<grid, 128, sm, st>>>(q, lt, probe, nprobe, cap, out_d, out_ids, out_prefix, out_cids);
+  int rpb = 128;
+  while (rpb > 32 && ((maxlen + rpb - 1) / rpb) * nprobe < 296) rpb >>= 1;
+  const dim3 grid((unsigned)std::max<int64_t>(1, (maxlen + rpb - 1) / rpb), (unsigned)nprobe);
+  const size_t sm = ag_smem(lt.dp);
+#define AG_PL(M)                                                                                  \
+  {                                                                                             \
+    ag_attr(probe_lists_kernel<M>, sm);                                                         \
+    probe_lists_kernel<M><<<grid, 128, sm, st>>>(q, lt, probe, nprobe, cap, out_d, out_ids, out_prefix, out_cids, rpb); \
+  }
+  if (metric == SQ_L2) AG_PL(SQ_L2) else if (metric == IP) AG_PL(IP) else AG_PL(COSINE)
+#undef AG_PL
 }
 
 int l1_place_max_clusters() { return L1_MAXC; }
 
 void launch_l1_place(int metric, int nc0, int n_p, int cap, int dp, int d, double* sums, float* cents,
                      int32_t* cnt, const float* items, const int32_t* holder, const int32_t* dup, int m,
-                     const float* qv,
-                     int32_t* out_t, uint8_t* out_added, uint8_t* out_merged, int32_t* out_q, cudaStream_t st) {
-  if (metric == SQ_L2)
-    l1_place_kernel<SQ_L2><<<1, 256, 0, st>>>(nc0, n_p, cap, dp, d, sums, cents, cnt, items, holder, dup, m, qv, out_t,
-                                               out_added, out_merged, out_q);
-  else if (metric == IP)
-    l1_place_kernel<IP><<<1, 256, 0, st>>>(nc0, n_p, cap, dp, d, sums, cents, cnt, items, holder, dup, m, qv, out_t,
-                                            out_added, out_merged, out_q);
-  else
-    l1_place_kernel<COSINE><<<1, 256, 0, st>>>(nc0, n_p, cap, dp, d, sums, cents, cnt, items, holder, dup, m, qv, out_t,
-                                                out_added, out_merged, out_q);
+                     const float* qv, int32_t* out_t, uint8_t* out_added, uint8_t* out_merged, int32_t* out_q,
+                     cudaStream_t st) {
+  const size_t sm = (size_t)(n_p + 1) * dp * 4;
+#define AG_L1(M)                                                                                       \
+  {                                                                                                  \
+    ag_attr(l1_place_kernel<M>, sm);                                                                 \
+    l1_place_kernel<M><<<1, 256, sm, st>>>(nc0, n_p, cap, dp, d, sums, cents, cnt, items, holder, dup, m, qv, \
+                                            out_t, out_added, out_merged, out_q);                     \
+  }
+  if (metric == SQ_L2) AG_L1(SQ_L2) else if (metric == IP) AG_L1(IP) else AG_L1(COSINE)
+#undef AG_L1
 }
 
 }  // namespace pk

@@ -199,6 +199,137 @@ struct Walk {
   }
 };
 
+// The same walk with the whole warp (ef <= 32): the result set lives in
+// registers as an ascending array of (-d, cid)-ordered keys, one per lane
+// (insertion = ballot + shuffle, the worst element = lane n-1), the links of
+// an expansion are loaded, de-duplicated and stamped by 32 lanes at once, and
+// only the admissions -- each reads the bound the previous one moved -- and
+// the candidate heap stay sequential (lane 0 owns the heap).  Every decision
+// is the single-thread walk's.
+struct WarpWalk {
+  const float* drow;
+  const GraphDev* g;
+  uint32_t* stamp;
+  // candidates: an unsorted array (shared memory) -- the pop is a warp
+  // argmin (keys are unique), the hole refilled from the end; cheaper than a
+  // one-lane binary heap at the sizes an ef <= 32 walk reaches
+  uint64_t* ck;
+  int cn;
+  uint64_t bv;   // this lane's result-set element (valid when lane < bn)
+  int bn;
+  int counter;
+  int lane;
+  __device__ uint32_t dk(int s) const { return f2key(drow[s]); }
+  __device__ uint32_t worst_dk() const { return (uint32_t)(__shfl_sync(FULLW, bv, bn - 1) >> 32); }
+  __device__ void best_insert(uint64_t k, int ef) {
+    const bool less = lane < bn && bv < k;
+    const int pos = __popc(__ballot_sync(FULLW, less));
+    const uint64_t up = __shfl_up_sync(FULLW, bv, 1);
+    if (lane > pos) bv = up;
+    if (lane == pos) bv = k;
+    bn = min(bn + 1, ef);  // full: the old worst fell off the end
+  }
+  __device__ void cand_push(uint64_t k) {
+    if (lane == 0) ck[cn] = k;
+    cn++;
+  }
+  __device__ bool cand_pop(uint64_t* k) {
+    __syncwarp();
+    if (cn == 0) return false;
+    uint64_t best = ~0ull;
+    int bi = 0;
+    for (int i = lane; i < cn; i += 32) {
+      const uint64_t v = ck[i];
+      if (v < best) {
+        best = v;
+        bi = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t ob = __shfl_xor_sync(FULLW, best, o);
+      const int oi = __shfl_xor_sync(FULLW, bi, o);
+      if (ob < best) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ck[bi] = ck[cn - 1];
+    cn--;
+    *k = best;
+    return true;
+  }
+  __device__ void seed(int s, uint32_t ep, int ef) {
+    if (lane == 0) stamp[s] = ep;
+    __syncwarp();
+    const uint32_t k = dk(s), r = (uint32_t)g->rank[s];
+    cand_push(kmin(k, r));
+    best_insert(kworst(k, r), ef);
+  }
+  // links of one expanded node, in order (x(j) < 0: not a link)
+  template <typename LinkF>
+  __device__ void visit(int nl, LinkF link, int ef, uint32_t ep) {
+    for (int j0 = 0; j0 < nl; j0 += 32) {
+      const int j = j0 + lane;
+      const int x = j < nl ? link(j) : -1;
+      bool fresh = x >= 0 && stamp[x] != ep;
+      const unsigned same = __match_any_sync(FULLW, x);
+      if (fresh && __ffs(same) - 1 != lane) fresh = false;  // a repeat of an earlier link
+      unsigned fm = __ballot_sync(FULLW, fresh);
+      uint32_t k = 0, r = 0;
+      if (fresh) {
+        stamp[x] = ep;
+        k = dk(x);
+        r = (uint32_t)g->rank[x];
+      }
+      counter += __popc(fm);
+      while (fm) {  // admissions in link order
+        const int L = __ffs(fm) - 1;
+        fm &= fm - 1;
+        const uint32_t kL = __shfl_sync(FULLW, k, L), rL = __shfl_sync(FULLW, r, L);
+        if (bn < ef || kL < worst_dk()) {
+          cand_push(kmin(kL, rL));
+          best_insert(kworst(kL, rL), ef);
+        }
+      }
+      __syncwarp();  // stamps visible to the next chunk
+    }
+  }
+  __device__ int slot_of(uint64_t key) const { return g->slot_of_rank[(uint32_t)key]; }
+  __device__ const int32_t* nbrs(int s, int layer) const {
+    return layer == 0 ? g->nbr0 + (int64_t)s * g->M : g->up + g->up_off[s] + (int64_t)(layer - 1) * g->M;
+  }
+  __device__ int degree(const int32_t* nb) const {  // valid prefix of a -1 padded neighbor list
+    const unsigned v = __ballot_sync(FULLW, lane < g->M && nb[min(lane, g->M - 1)] >= 0);
+    const unsigned inv = ~v & ((g->M >= 32) ? FULLW : ((1u << g->M) - 1u));
+    return inv ? __ffs(inv) - 1 : g->M;
+  }
+  __device__ void search_layer(int layer, int ef, uint32_t ep) {
+    uint64_t ck;
+    while (cand_pop(&ck)) {
+      if (bn > 0 && (uint32_t)(ck >> 32) > worst_dk() && bn >= ef) break;
+      const int c = slot_of(ck);
+      if (layer > g->level[c]) continue;
+      const int32_t* nb = nbrs(c, layer);
+      const int m = degree(nb);
+      visit(m, [&](int jj) { return (int)nb[jj]; }, ef, ep);
+    }
+  }
+  __device__ int descend(int entry, int maxl, uint32_t* epoch) {
+    int cur = entry;
+    for (int layer = maxl; layer >= 1; layer--) {
+      const uint32_t ep = ++(*epoch);
+      cn = 0;
+      bn = 0;
+      seed(cur, ep, 1);
+      search_layer(layer, 1, ep);
+      cur = slot_of(~__shfl_sync(FULLW, bv, 0) & 0xffffffffull);
+    }
+    return cur;
+  }
+};
+
 // dynamic shared memory per CTA (one query): stamps u32[ns], two heaps u64[ns + 1],
 // and the distance row f32[ns] when `smem_row`
 constexpr int GRAPH_THREADS = 256;
@@ -224,13 +355,14 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
     p += (size_t)ns * 4;
     int32_t* sr = reinterpret_cast<int32_t*>(p);
     p += (size_t)ns * 4;
-    int32_t* po = reinterpret_cast<int32_t*>(p);
-    p += (size_t)(ns + 1) * 4;
-    int32_t* pv = reinterpret_cast<int32_t*>(p);
-    p += (size_t)g0.npor * 4;
     int8_t* lv = reinterpret_cast<int8_t*>(p);
     p += (size_t)ns;
     uint8_t* fl = p;
+    p += (size_t)ns;
+    p = reinterpret_cast<uint8_t*>(((uintptr_t)p + 15) & ~(uintptr_t)15);
+    int32_t* po = reinterpret_cast<int32_t*>(p);  // portals: only when smem_graph == 2
+    p += (size_t)(ns + 1) * 4;
+    int32_t* pv = reinterpret_cast<int32_t*>(p);
     const int n4 = ns * g0.M / 4;  // M is a multiple of 4 (pk_graph_set pads)
     for (int i = tid; i < n4; i += GRAPH_THREADS)
       reinterpret_cast<int4*>(nb)[i] = reinterpret_cast<const int4*>(g0.nbr0)[i];
@@ -238,17 +370,18 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
     for (int i = tid; i < ns; i += GRAPH_THREADS) {
       rk[i] = g0.rank[i];
       sr[i] = g0.slot_of_rank[i];
-      po[i] = g0.por_off[i];
       lv[i] = g0.level[i];
       fl[i] = gq.flags[i];
     }
-    if (tid == 0) po[ns] = g0.por_off[ns];
-    for (int i = tid; i < g0.npor; i += GRAPH_THREADS) pv[i] = g0.por[i];
+    if (smem_graph == 2) {
+      for (int i = tid; i <= ns; i += GRAPH_THREADS) po[i] = g0.por_off[i];
+      for (int i = tid; i < g0.npor; i += GRAPH_THREADS) pv[i] = g0.por[i];
+      g.por_off = po;
+      g.por = pv;
+    }
     g.nbr0 = nb;
     g.rank = rk;
     g.slot_of_rank = sr;
-    g.por_off = po;
-    g.por = pv;
     g.level = lv;
     gq.flags = fl;
   }
@@ -259,7 +392,72 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
   __syncthreads();
   if (tid >= 32) return;
   uint32_t emit = 0;
-  if (lane == 0) {
+  if (gq.warp) {
+    // ef <= 32 and no more seeds than ef: the warp walk
+    WarpWalk w;
+    w.drow = smem_row ? srow : drow_g;
+    w.g = &g;
+    w.stamp = stamp;
+    w.ck = heaps;
+    w.cn = 0;
+    w.bn = 0;
+    w.bv = 0;
+    w.counter = 0;
+    w.lane = lane;
+    const int ef = min(gq.ef, ns);
+    uint32_t epoch = 0;
+    if (gq.mode == 0) {
+      int nseeds = 0;
+      int seeds[1 + GRAPH_MAX_SCOPES];
+      if (gq.static_entry >= 0) {
+        w.counter++;
+        seeds[nseeds++] = w.descend(gq.static_entry, gq.static_maxl, &epoch);
+      }
+      for (int i = 0; i < gq.n_sc; i++) {
+        if (gq.sc_static[i] || gq.sc_entry[i] < 0) continue;
+        w.counter++;
+        seeds[nseeds++] = gq.sc_entry[i];
+      }
+      const uint32_t ep = ++epoch;
+      w.cn = 0;
+      w.bn = 0;
+      for (int i = 0; i < nseeds; i++) {
+        __syncwarp();
+        if (stamp[seeds[i]] != ep) w.seed(seeds[i], ep, ef);
+      }
+      uint64_t ck;
+      while (w.cand_pop(&ck)) {
+        if (w.bn > 0 && (uint32_t)(ck >> 32) > w.worst_dk() && w.bn >= ef) break;
+        const int c = w.slot_of(ck);
+        if (g.level[c] < 0) continue;
+        const int32_t* nb = g.nbr0 + (int64_t)c * g.M;
+        const int m = w.degree(nb);
+        const int p0 = g.por_off[c], np = g.por_off[c + 1] - p0;
+        w.visit(m + np, [&](int j) {
+          const int x = j < m ? (int)nb[j] : (int)g.por[p0 + j - m];
+          return (j < m || (gq.flags[x] & 2)) ? x : -1;
+        }, ef, ep);
+      }
+      emit = ep;
+    } else {
+      for (int i = 0; i < gq.n_sc; i++) {
+        const int e = gq.sc_entry[i];
+        if (e < 0) continue;
+        w.counter++;
+        const int top = w.descend(e, gq.sc_maxl[i], &epoch);
+        const uint32_t ep = ++epoch;
+        w.cn = 0;
+        w.bn = 0;
+        w.seed(top, ep, ef);
+        w.search_layer(0, ef, ep);
+        __syncwarp();
+        if (lane < w.bn) stamp[w.slot_of(~w.bv & 0xffffffffull)] = EMIT;
+        __syncwarp();
+      }
+      emit = EMIT;
+    }
+    if (lane == 0) counter_out[b] = w.counter;
+  } else if (lane == 0) {
     Walk w;
     w.drow = smem_row ? srow : drow_g;
     w.g = &g;
@@ -327,14 +525,25 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
   }
   __syncwarp();  // lane 0's stamps visible to the warp
   emit = __shfl_sync(FULLW, emit, 0);
-  // top-nprobe of the emitted in-scope nodes by (d, cid): repeated warp minima
+  // top-nprobe of the emitted in-scope nodes by (d, cid): the emitted keys are
+  // compacted once into the (now free) heap space, then repeated warp minima
+  // run over that short list instead of every slot
   const float* drow = smem_row ? srow : drow_g;
+  uint64_t* ek = heaps;
+  int ne = 0;
+  for (int s0 = 0; s0 < ns; s0 += 32) {
+    const int s = s0 + lane;
+    const bool hit = s < ns && stamp[s] == emit && (gq.flags[s] & 1);
+    const unsigned m = __ballot_sync(FULLW, hit);
+    if (hit) ek[ne + __popc(m & ((1u << lane) - 1u))] = kmin(f2key(drow[s]), (uint32_t)g.rank[s]);
+    ne += __popc(m);
+  }
+  __syncwarp();
   uint64_t last = 0;
   for (int p = 0; p < gq.nprobe; p++) {
     uint64_t mk = ~0ull;
-    for (int s = lane; s < ns; s += 32) {
-      if (stamp[s] != emit || !(gq.flags[s] & 1)) continue;
-      const uint64_t k = kmin(f2key(drow[s]), (uint32_t)g.rank[s]);
+    for (int i = lane; i < ne; i += 32) {
+      const uint64_t k = ek[i];
       if (p > 0 && k <= last) continue;
       mk = k < mk ? k : mk;
     }
@@ -357,9 +566,10 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
 size_t graph_smem_bytes(int ns, bool row) {
   return (size_t)(2 * ns + 2) * 8 + (size_t)ns * 4 + (row ? (size_t)ns * 4 : 0);
 }
-static size_t graph_stage_bytes(const GraphDev& g) {
-  return 16 + (size_t)g.ns * g.M * 4 + (size_t)g.ns * 8 + (size_t)(g.ns + 1) * 4 + (size_t)g.npor * 4 +
-         (size_t)g.ns * 2;
+// the walk's per-hop arrays (neighbors, ranks, levels, flags) [+ portals]
+static size_t graph_stage_bytes(const GraphDev& g, bool portals) {
+  return 32 + (size_t)g.ns * g.M * 4 + (size_t)g.ns * 8 + (size_t)g.ns * 2 +
+         (portals ? (size_t)(g.ns + 1) * 4 + (size_t)g.npor * 4 : 0);
 }
 
 void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, const GraphQuery& gq,
@@ -369,9 +579,12 @@ void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, 
   constexpr size_t SMEM_MAX = 227 * 1024;
   int heaps = 1, row = 1, stage = 0;
   size_t smem = graph_smem_bytes(g.ns, true);
-  if (smem + graph_stage_bytes(g) <= SMEM_MAX && g.M % 4 == 0) {
+  if (smem + graph_stage_bytes(g, true) <= SMEM_MAX && g.M % 4 == 0) {
+    stage = 2;
+    smem += graph_stage_bytes(g, true);
+  } else if (smem + graph_stage_bytes(g, false) <= SMEM_MAX && g.M % 4 == 0) {
     stage = 1;
-    smem += graph_stage_bytes(g);
+    smem += graph_stage_bytes(g, false);
   } else if (smem > SMEM_MAX) {
     row = 0;
     smem = graph_smem_bytes(g.ns, false);
@@ -385,7 +598,13 @@ void launch_graph_search(const float* D, int64_t ldd, int B, const GraphDev& g, 
     cudaFuncSetAttribute(graph_search_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_MAX);
     attr = SMEM_MAX;
   }
-  graph_search_kernel<<<B, GRAPH_THREADS, smem, st>>>(D, ldd, g, gq, heaps, row, stage, gstamps, gheap, probe,
+  // the warp walk holds the result set in registers (ef <= 32, one element
+  // per lane) and needs every seed to fit in it (PK_GRAPH_WARP=0: off)
+  static const bool warp_ok = !getenv("PK_GRAPH_WARP") || atoi(getenv("PK_GRAPH_WARP")) != 0;
+  GraphQuery q2 = gq;
+  const int ef = std::min(gq.ef, g.ns);
+  q2.warp = warp_ok && ef <= 32 && g.M <= 32 && (gq.mode == 1 || 1 + gq.n_sc <= ef);
+  graph_search_kernel<<<B, GRAPH_THREADS, smem, st>>>(D, ldd, g, q2, heaps, row, stage, gstamps, gheap, probe,
                                                       counter);
 }
 

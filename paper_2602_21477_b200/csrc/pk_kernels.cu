@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict
                                                          int B, const float* __restrict__ X,
                                                          int64_t ldx, int64_t n, int dp,
                                                          const float* __restrict__ qnorm,
-                                                         float* __restrict__ D, int64_t ldd) {
+                                                         float* __restrict__ D, int64_t ldd, int rpb) {
   extern __shared__ float4 qs4[];  // [NQ][dp/4] | ring [DD_RING][128][DD_RS]
   const float* qs = reinterpret_cast<const float*>(qs4);
   float* ring = reinterpret_cast<float*>(qs4) + (size_t)NQ * dp;
@@ -116,10 +116,12 @@ __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict
     qs4[i] = v;
   }
   __syncthreads();
-  const int64_t r0 = (int64_t)blockIdx.x * blockDim.x;
+  // rpb rows per block (128, or fewer when a small call would leave most SMs
+  // idle: wider column blocks, fewer ring round trips per block)
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  const int nr = (int)(n - r0 < rpb ? n - r0 : rpb);
   const int64_t r = r0 + threadIdx.x;
-  const bool valid = r < n;
-  const int nr = (int)(n - r0 < 128 ? n - r0 : 128);
+  const bool valid = (int)threadIdx.x < nr;
   // column block width: DC for a full block of rows, wider (fewer ring
   // round trips) when the block holds few rows; a ring slot is 128 * DD_RS floats
   int W = (128 * DD_RS / nr - 4) / DC * DC;
@@ -180,12 +182,15 @@ static void dist_dense_dispatch(const float* Q, int64_t ldq, int B, const float*
   int nq = B >= 16 ? 16 : (B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1)));
   while (nq > 1 && (size_t)nq * dp * 4 > 96 * 1024) nq >>= 1;
   size_t smem = (size_t)nq * dp * 4 + (size_t)DD_RING * 128 * DD_RS * 4;
-  dim3 grid((unsigned)((n + 127) / 128), (unsigned)((B + nq - 1) / nq));
+  const int64_t ny = (B + nq - 1) / nq;
+  int rpb = 128;
+  while (rpb > 32 && ((n + rpb - 1) / rpb) * ny < 148) rpb >>= 1;
+  dim3 grid((unsigned)((n + rpb - 1) / rpb), (unsigned)ny);
 #define PK_DD(NQV)                                                                                  \
   case NQV: {                                                                                       \
     auto k = dist_dense_kernel<METRIC, NQV>;                                                        \
     PK_SMEM_ATTR(k, (int)smem);                \
-    k<<<grid, 128, smem, st>>>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd);                            \
+    k<<<grid, 128, smem, st>>>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, rpb);                       \
   } break;
   switch (nq) {
     PK_DD(1) PK_DD(2) PK_DD(4) PK_DD(8) PK_DD(16)
@@ -1971,7 +1976,7 @@ __global__ void __launch_bounds__(RR_THREADS, LEAN ? 3 : 1) rerank_merge_kernel(
     int32_t* __restrict__ nsurv, const int64_t* __restrict__ scanned_src, int64_t* __restrict__ scanned_dst,
     uint64_t* __restrict__ dbg) {
   constexpr int CAP = LEAN ? 128 : RR_CAP;
-  constexpr int SURV = LEAN ? 512 : RR_SURV;
+  constexpr int SURV = LEAN ? 256 : RR_SURV;
   if (!LEAN) {
     pdl_trigger();
     pdl_wait();
@@ -2224,12 +2229,33 @@ __global__ void __launch_bounds__(RR_THREADS, LEAN ? 3 : 1) rerank_merge_kernel(
 
 // Shared memory of the lean re-rank (one CTA beside a scan CTA on each SM).
 static size_t rerank_lean_smem(int dp) {
-  return 128 * sizeof(Entry) + (size_t)dp * 4 + (size_t)2 * 32 * (DC + 4) * 4 + 512 * 4;
+  return 128 * sizeof(Entry) + (size_t)dp * 4 + (size_t)2 * 32 * (DC + 4) * 4 + 256 * 4;
 }
 bool rerank_lean_fits(int dp) {
-  // an SM's 228 KB minus the scan CTA (dynamic + static + 1 KB reserved) and
-  // this CTA's own static arrays and reservation
-  return tc_smem_bytes() + 256 + 1024 + rerank_lean_smem(dp) + 2304 + 1024 <= 228 * 1024;
+  // the SM's shared memory must hold a scan CTA and a lean re-rank CTA:
+  // dynamic + static + the per-CTA reservation of each (measured from the
+  // kernels' attributes, not assumed)
+  static int cached_dp = -1;
+  static bool cached = false;
+  if (dp == cached_dp) return cached;
+  int dev = 0, per_sm = 0, reserved = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaFuncAttributes fs = {}, fr = {};
+  cudaFuncGetAttributes(&fs, scan_tc_kernel<SQ_L2>);
+  cudaFuncGetAttributes(&fr, rerank_merge_kernel<SQ_L2, true>);
+  const size_t need = tc_smem_bytes() + fs.sharedSizeBytes + rerank_lean_smem(dp) + fr.sharedSizeBytes +
+                      2 * (size_t)reserved;
+  cached = need <= (size_t)per_sm;
+  cached_dp = dp;
+  static bool said = false;
+  if (!said && getenv("PK_DEBUG_RERANK")) {
+    fprintf(stderr, "lean re-rank beside the scan: need %zu of %d B per SM -> %s\n", need, per_sm,
+            cached ? "fits" : "does not fit");
+    said = true;
+  }
+  return cached;
 }
 
 void launch_rerank_merge(int metric, int B, const int4* cpool, const int32_t* ccount, int cap,

@@ -128,6 +128,7 @@ struct GraphQuery {        // one batch's scope set
   int sc_entry[GRAPH_MAX_SCOPES], sc_maxl[GRAPH_MAX_SCOPES];
   uint8_t sc_static[GRAPH_MAX_SCOPES];
   int ef, nprobe, mode;    // mode 0: search (hybrid), 1: search_independent (per_agent)
+  int warp;                // the warp walk (set by the launcher when ef and the seed count allow)
 };
 // probe[b][nprobe] (slots, (d, cid) order, -1 padded), counter[b] = distance
 // computations; D = exact distances [B][ldd] to every slot's centroid.

@@ -32,7 +32,7 @@ import numpy as np
 
 from . import _native as N
 from . import pnck
-from .cache import DEFAULT_KEY, MultiLevelCache, RunningKth
+from .cache import DEFAULT_KEY, MultiLevelCache
 from .clusters import ClusterStore, SplitOutcome, kmeans_split_points
 from .fsm import PatternHint, PatternTable
 from .concurrency import RWLock, TaskRunner
@@ -571,12 +571,21 @@ class Store:
                 selected = [int(c) for c in cids if c >= 0]
             thresh = cache.threshold() if (cache is not None and not exhaustive_edge) else None
             clusters = self.clusters.clusters
-            run = None
-            if thresh is not None:  # stop rule over everything scanned so far
-                run = RunningKth(k)
-                for c in dist_chunks:
-                    run.add(c)
-            for li, cid in enumerate(selected):
+            stop_at = len(selected)
+            if thresh is not None and selected:
+                # the stop rule after list li (k-th smallest of everything
+                # scanned < thresh) holds exactly when >= k scanned distances
+                # are below thresh: the first such li, from prefix counts
+                below = sum(int(np.count_nonzero(c < thresh)) for c in dist_chunks)
+                cb = np.concatenate(([0], np.cumsum(all_d < thresh)))
+                cum = below + cb[pre[1:len(selected) + 1]]
+                ok = np.flatnonzero(cum >= k)
+                if len(ok):
+                    stop_at = int(ok[0]) + 1
+                    early = True
+                    stats.early_terminated = True
+            for li in range(stop_at):
+                cid = selected[li]
                 cl = clusters[cid]
                 cl.access_count += 1
                 self.tier.record_access(cid)
@@ -584,20 +593,12 @@ class Store:
                 if len(ids):
                     id_chunks.append(ids)
                     dist_chunks.append(all_d[pre[li]:pre[li + 1]])
-                    if run is not None:
-                        run.add(dist_chunks[-1])
                 stats.scanned_vectors += len(ids)
                 if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
                     order = profile_order(cl.profiles[agent], cl.size)
                     scan_chunks.append(cl.member_ids[order])
                 else:
                     scan_chunks.append(cl.member_ids.copy())
-                if thresh is not None and len(dist_chunks):
-                    kth = run.kth()
-                    if kth is not None and kth < thresh:
-                        early = True
-                        stats.early_terminated = True
-                        break
         extended = self._topk(id_chunks, dist_chunks, max(k, self.cfg.kappa * k))
         scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
         return SearchResult(extended[:k], stats, scan_ids), hint, extended

@@ -317,3 +317,28 @@ class TestHotsetPolicy:
         counts = np.bincount(trace, minlength=1000)
         oracle = counts[np.argsort(-counts)[:100]].sum()
         assert hits / len(trace) >= oracle / len(trace) - 0.05
+
+
+def test_stop_rule_by_count_equals_kth():
+    """The agent path's stop rule, kth_smallest(scanned, k) < thresh
+    (ref/cache.py:154-160, 199-203; ref/engine.py:391-396), is evaluated as
+    "at least k scanned distances are below thresh" (cache.replay and the L2
+    list loop): the same decision for every prefix, NaNs and ties included."""
+    from paper_2602_21477_b200.cache import kth_smallest
+
+    rng = np.random.default_rng(5)
+    for trial in range(400):
+        k = int(rng.integers(1, 12))
+        chunks = []
+        for _ in range(int(rng.integers(1, 9))):
+            c = rng.integers(0, 6, size=int(rng.integers(0, 7))).astype(np.float32) / 2
+            if rng.random() < 0.2 and len(c):
+                c[rng.integers(0, len(c))] = np.nan
+            chunks.append(c)
+        thresh = float(rng.integers(0, 7)) / 2 if rng.random() < 0.9 else float("nan")
+        below = 0
+        for j in range(len(chunks)):
+            kth = kth_smallest([c for c in chunks[:j + 1] if len(c)], k) if any(len(c) for c in chunks[:j + 1]) else None
+            want = kth is not None and kth < thresh
+            below += int(np.count_nonzero(chunks[j] < thresh))
+            assert (below >= k) == want, (trial, j)

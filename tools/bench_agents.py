@@ -213,6 +213,41 @@ def main():
             store.load_lists(sc, lists)
             del lists
         build_s = time.perf_counter() - t0
+        timers = {}
+        if os.environ.get("PK_TIME_CALLS"):  # garbage-collector pauses
+            gc_t = [0.0]
+
+            def gc_cb(phase, info, _t=[0.0]):
+                if phase == "start":
+                    _t[0] = time.perf_counter()
+                else:
+                    e = timers.setdefault(f"gc.gen{info['generation']}", [0, 0.0])
+                    e[0] += 1
+                    e[1] += time.perf_counter() - _t[0]
+            gc.callbacks.append(gc_cb)
+        if os.environ.get("PK_TIME_CALLS"):  # wall time per wrapped call (no profiler overhead)
+            def wrap(obj, name, label):
+                fn = getattr(obj, name)
+
+                def timed(*args, **kw):
+                    t = time.perf_counter()
+                    try:
+                        return fn(*args, **kw)
+                    finally:
+                        e = timers.setdefault(label, [0, 0.0])
+                        e[0] += 1
+                        e[1] += time.perf_counter() - t
+                setattr(obj, name, timed)
+            idx = store.index
+            for m in ("agent_read", "l1_place", "rows_put", "create_list", "graph_set", "append", "assign",
+                      "flush"):
+                if hasattr(idx, m):
+                    wrap(idx, m, "index." + m)
+            for m in ("_insert_impl", "_rows_for", "_materialize", "_search_read_phase", "_search_side_effects",
+                      "_topk", "end_request", "_tick", "_state_key_for"):
+                wrap(store, m, "store." + m)
+            wrap(store.graph, "upload", "graph.upload")
+            wrap(store.clusters, "create_cluster", "clusters.create_cluster")
         prof = None
         if os.environ.get("PK_PROFILE_OPS"):
             import cProfile
@@ -227,6 +262,10 @@ def main():
             st = pstats.Stats(prof, stream=sys.stderr)
             st.sort_stats("tottime").print_stats(30)
             st.sort_stats("cumulative").print_stats(50)
+        if timers:
+            res["call_ms"] = {k: {"calls": v[0], "total_ms": round(1e3 * v[1], 2),
+                                  "ms_per_call": round(1e3 * v[1] / max(v[0], 1), 4)}
+                              for k, v in sorted(timers.items(), key=lambda kv: -kv[1][1])}
         res["build_s"] = build_s
         res["clusters_after"] = len(store.clusters.clusters)
         out["modes"][f"alpha_et={alpha}"] = res
