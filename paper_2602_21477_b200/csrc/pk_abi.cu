@@ -15,6 +15,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -219,7 +220,13 @@ struct pk_index {
     }
   } scr[2];
   int par = 0, last_par = 0;
-  PinnedBuf hstage;  // append staging (mapped)
+  // append staging (mapped), two buffers in turn: an append returns once its
+  // scatter is enqueued; the buffer is rewritten only after the event of its
+  // previous use (the call before last) has passed
+  PinnedBuf hstage2[2];
+  cudaEvent_t hstage_ev[2] = {nullptr, nullptr};
+  int hstage_i = 0;
+  DevBuf tmp_rows2[2];
   PinnedBuf hsl;     // pk_scan_lists staging (mapped)
   PinnedBuf hasg;    // pk_assign host path: padded rows in, (cid, dist) out (mapped)
   // agent path (pk_rows_put / pk_agent_read / pk_l1_place, pk_agent.cu): the
@@ -246,6 +253,7 @@ struct pk_index {
   uint64_t ev_scan_n = 0;  // lock count when ev_scan was last recorded
   bool pipeline = true;    // PK_PIPELINE=0 turns the overlap off
   DevBuf assign_q, assign_qn, assign_dc, assign_c, assign_d;
+  DevBuf assign_part, assign_ctr;  // fused argmin: block minima, finished-block counter
   int chunk_rows = 512;
   bool screen = true;  // screened scan + exact re-rank (sq_l2 / ip); PK_SCAN_EXACT=1 disables
   bool tensor = true;  // screen dots on tcgen05 (TF32); PK_SCREEN=ffma uses CUDA-core FFMA
@@ -1005,7 +1013,11 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->stage_ev) cudaEventDestroy(ix->stage_ev);
   if (ix->mst) cudaStreamDestroy(ix->mst);
   if (ix->hout) cudaFreeHost(ix->hout);
-  if (ix->hstage.p) cudaFreeHost(ix->hstage.p);
+  for (int i = 0; i < 2; i++) {
+    if (ix->hstage2[i].p) cudaFreeHost(ix->hstage2[i].p);
+    if (ix->hstage_ev[i]) cudaEventDestroy(ix->hstage_ev[i]);
+    ix->tmp_rows2[i].release();
+  }
   if (ix->hsl.p) cudaFreeHost(ix->hsl.p);
   if (ix->hasg.p) cudaFreeHost(ix->hasg.p);
   if (ix->hag.p) cudaFreeHost(ix->hag.p);
@@ -1051,7 +1063,7 @@ int pk_index_destroy(pk_index* ix) {
   ix->stage_desc.release();
   ix->tmp_rows.release();
   for (auto& sc : ix->scr) sc.release();
-  for (DevBuf* b : {&ix->assign_q, &ix->assign_qn, &ix->assign_dc, &ix->assign_c, &ix->assign_d,
+  for (DevBuf* b : {&ix->assign_part, &ix->assign_ctr, &ix->assign_q, &ix->assign_qn, &ix->assign_dc, &ix->assign_c, &ix->assign_d,
                     &ix->shard_in, &ix->shard_out, &ix->pb, &ix->pb_out, &ix->sl_buf})
     b->release();
   if (ix->st) cudaStreamDestroy(ix->st);
@@ -1335,8 +1347,14 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
     // memory; small batches are read by the scatter kernel in place (no DMA
     // operations), larger ones go over in one copy
     const size_t bytes = (size_t)m * ix->dp * 4 + (size_t)m * 16;
-    RET(ix->hstage.ensure(bytes));
-    float* h_src = reinterpret_cast<float*>(ix->hstage.p);
+    const int bi = ix->hstage_i;
+    ix->hstage_i ^= 1;
+    PinnedBuf& hs = ix->hstage2[bi];
+    if (!ix->hstage_ev[bi]) CK(cudaEventCreateWithFlags(&ix->hstage_ev[bi], cudaEventDisableTiming));
+    else CK(cudaEventSynchronize(ix->hstage_ev[bi]));  // its previous scatter has read it
+    if (hs.bytes < bytes) CK(cudaStreamSynchronize(ix->st));  // (re)allocation frees the old buffer
+    RET(hs.ensure(bytes));
+    float* h_src = reinterpret_cast<float*>(hs.p);
     int64_t* h_ids = reinterpret_cast<int64_t*>(h_src + m * ix->dp);
     int64_t* h_dst = h_ids + m;
     for (int64_t j = 0; j < m; j++) {
@@ -1345,17 +1363,18 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
       h_ids[j] = ids[pick[j]];
       h_dst[j] = dst[j];
     }
-    const uint8_t* base = ix->hstage.dev;
+    const uint8_t* base = hs.dev;
     if (bytes > ((size_t)1 << 20)) {
-      RET(ix->tmp_rows.ensure(bytes));
-      CK(cudaMemcpyAsync(ix->tmp_rows.p, ix->hstage.p, bytes, cudaMemcpyHostToDevice, ix->st));
-      base = ix->tmp_rows.as<uint8_t>();
+      if (ix->tmp_rows2[bi].bytes < bytes) CK(cudaStreamSynchronize(ix->st));
+      RET(ix->tmp_rows2[bi].ensure(bytes));
+      CK(cudaMemcpyAsync(ix->tmp_rows2[bi].p, hs.p, bytes, cudaMemcpyHostToDevice, ix->st));
+      base = ix->tmp_rows2[bi].as<uint8_t>();
     }
     const float* d_src = reinterpret_cast<const float*>(base);
     const int64_t* d_ids = reinterpret_cast<const int64_t*>(d_src + m * ix->dp);
     launch_append_rows(d_src, d_ids, d_ids + m, (int)m, ix->rows, ix->ids, ix->nrm, (int)ix->dp, ix->st);
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(ix->st));  // the staging buffer is reused by the next call
+    CK(cudaEventRecord(ix->hstage_ev[bi], ix->st));  // no host wait: ordered on the index stream
   }
   return PK_OK;
 }
@@ -2848,7 +2867,19 @@ int pk_profile_end(pk_index* ix, double* stage_ms, int nstages, int* ncalls) {
 
 int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64_t* out_cid,
               float* out_dist, int flags) {
+  // PK_DEBUG_ASSIGN=1: host-side microseconds per step (measurement only)
+  static const bool dbg = getenv("PK_DEBUG_ASSIGN") != nullptr;
+  static double tacc[8] = {0};
+  static long tcalls = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  auto tick = [&](int i) {
+    if (!dbg) return;
+    auto t = std::chrono::steady_clock::now();
+    tacc[i] += std::chrono::duration<double, std::micro>(t - t0).count();
+    t0 = t;
+  };
   std::lock_guard<CountedMutex> lock_(ix->mu);
+  tick(0);
   if (n < 0) return fail(PK_ERR_USAGE, "negative count");
   if (n == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
@@ -2864,6 +2895,7 @@ int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64
   RET(ix->assign_dc.ensure((size_t)n * ns * 4));
   RET(ix->assign_c.ensure(n * 8));
   RET(ix->assign_d.ensure(n * 4));
+  tick(1);
   // host path (the insert path's batch of 8): the rows go over in ONE DMA
   // from pinned staging, padded on the host, and the argmin writes (cid,
   // dist) straight into mapped pinned memory -- no pageable 2-D copies, no
@@ -2884,13 +2916,35 @@ int pk_assign(pk_index* ix, const float* X, int64_t n, int32_t scope_code, int64
     oc = reinterpret_cast<int64_t*>(ix->hasg.dev + in_b);
     od = reinterpret_cast<float*>(ix->hasg.dev + in_b + (size_t)n * 8);
   }
+  tick(2);
   if (ix->metric == COSINE) launch_qnorm(ix->assign_q.as<float>(), dp, (int)n, (int)ix->d, ix->assign_qn.as<float>(), st);
-  launch_dist_dense(ix->metric, ix->assign_q.as<float>(), dp, (int)n, ix->d_cent, dp, ix->nslots, (int)dp,
-                    ix->assign_qn.as<float>(), ix->assign_dc.as<float>(), ns, st);
-  launch_argmin(ix->assign_dc.as<float>(), ns, (int)n, ix->table(), scope_code, oc, od, st);
+  // one launch: distances + argmin by (dist, cid) (cids below 2^32: the
+  // packed key), else the dense matrix and a separate argmin
+  bool small_cids = true;
+  for (int32_t sl = 0; sl < ix->nslots && small_cids; sl++) small_cids = ix->h_cid[sl] < ((int64_t)1 << 32);
+  if (small_cids && ix->nslots > 0) {
+    const size_t pb = (size_t)dense_argmin_blocks(ix->nslots, (int)n) * 8;
+    if (ix->assign_part.bytes < pb) RET(ix->assign_part.ensure(pb));
+    if (!ix->assign_ctr.p) {
+      RET(ix->assign_ctr.ensure(64));
+      CK(cudaMemsetAsync(ix->assign_ctr.p, 0, 64, st));
+    }
+    launch_dense_argmin(ix->metric, ix->assign_q.as<float>(), dp, (int)n, ix->d_cent, ix->nslots, (int)dp,
+                        ix->assign_qn.as<float>(), ix->table(), scope_code,
+                        ix->assign_part.as<unsigned long long>(), ix->assign_ctr.as<unsigned>(), oc, od, st);
+  } else {
+    launch_dist_dense(ix->metric, ix->assign_q.as<float>(), dp, (int)n, ix->d_cent, dp, ix->nslots, (int)dp,
+                      ix->assign_qn.as<float>(), ix->assign_dc.as<float>(), ns, st);
+    launch_argmin(ix->assign_dc.as<float>(), ns, (int)n, ix->table(), scope_code, oc, od, st);
+  }
   CK(cudaGetLastError());
+  tick(3);
   if (!dev) {
     CK(cudaStreamSynchronize(st));
+    tick(4);
+    if (dbg && ++tcalls % 1000 == 0)
+      fprintf(stderr, "pk_assign host us/call: lock %.1f setup %.1f stage+h2d %.1f launches %.1f sync %.1f\n",
+              tacc[0] / tcalls, tacc[1] / tcalls, tacc[2] / tcalls, tacc[3] / tcalls, tacc[4] / tcalls);
     const size_t in_b = (size_t)n * dp * 4;
     memcpy(out_cid, ix->hasg.p + in_b, n * 8);
     if (out_dist) memcpy(out_dist, ix->hasg.p + in_b + (size_t)n * 8, n * 4);

@@ -97,12 +97,26 @@ __device__ __forceinline__ float step4(float acc, float4 x, float4 q) {
 // centroids, a few hundred rows).
 constexpr int DD_RING = 3;
 constexpr int DD_RS = DC + 4;  // padded row stride in the ring (conflict-free float4 reads)
+// Optional fused argmin (assign_nearest, ref/clusters.py:268-279): instead
+// of writing D, every block reduces its rows' (dist, cid) keys per query, and
+// the last block to finish reduces the blocks' minima and writes (cid, dist)
+// -- one launch for the whole assignment (the insert path's batch of 8).
+struct DenseArgmin {
+  const int64_t* cid = nullptr;   // [n] row -> cid (< 2^32), -1 = free
+  const int32_t* scope = nullptr;  // [n] row -> scope code
+  int32_t scope_code = 0;
+  unsigned long long* part = nullptr;  // [blocks][B] block minima (null: off)
+  unsigned* counter = nullptr;    // finished blocks (reset by the last one)
+  int64_t* out_cid = nullptr;
+  float* out_d = nullptr;
+};
 template <int METRIC, int NQ>
 __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict__ Q, int64_t ldq,
                                                          int B, const float* __restrict__ X,
                                                          int64_t ldx, int64_t n, int dp,
                                                          const float* __restrict__ qnorm,
-                                                         float* __restrict__ D, int64_t ldd, int rpb) {
+                                                         float* __restrict__ D, int64_t ldd, int rpb,
+                                                         DenseArgmin am) {
   extern __shared__ float4 qs4[];  // [NQ][dp/4] | ring [DD_RING][128][DD_RS]
   const float* qs = reinterpret_cast<const float*>(qs4);
   float* ring = reinterpret_cast<float*>(qs4) + (size_t)NQ * dp;
@@ -164,23 +178,75 @@ __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict
     }
     __syncthreads();  // slot blk % DD_RING is refilled by the next iteration's issue
   }
-  if (!valid) return;
+  if (am.part == nullptr) {
+    if (!valid) return;
+#pragma unroll
+    for (int a = 0; a < NQ; a++) {
+      if (a < nq) {
+        float qn = (METRIC == COSINE) ? qnorm[b0 + a] : 0.f;
+        D[(int64_t)(b0 + a) * ldd + r] = finalize<METRIC>(acc[a], nn, qn);
+      }
+    }
+    return;
+  }
+  // fused argmin by (dist, cid) over the in-scope rows
+  __shared__ unsigned long long s_m[4][NQ];
+  __shared__ unsigned s_ticket;
+  const bool in = valid && am.cid[r] >= 0 && am.scope[r] == am.scope_code;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int a = 0; a < NQ; a++) {
-    if (a < nq) {
-      float qn = (METRIC == COSINE) ? qnorm[b0 + a] : 0.f;
-      D[(int64_t)(b0 + a) * ldd + r] = finalize<METRIC>(acc[a], nn, qn);
+    unsigned long long k = ~0ull;
+    if (in && a < nq) {
+      const float qn = (METRIC == COSINE) ? qnorm[b0 + a] : 0.f;
+      k = ((unsigned long long)f2key(finalize<METRIC>(acc[a], nn, qn)) << 32) | (unsigned)am.cid[r];
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long k2 = __shfl_xor_sync(0xffffffffu, k, o);
+      k = k2 < k ? k2 : k;
+    }
+    if (lane == 0) s_m[warp][a] = k;
   }
+  __syncthreads();
+  const int nblk_all = gridDim.x * gridDim.y;
+  const int blk = blockIdx.y * gridDim.x + blockIdx.x;
+  if (threadIdx.x < NQ) {
+    unsigned long long k = s_m[0][threadIdx.x];
+    for (int w = 1; w < 4; w++) k = s_m[w][threadIdx.x] < k ? s_m[w][threadIdx.x] : k;
+    am.part[(int64_t)blk * NQ + threadIdx.x] = k;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_ticket = atomicAdd(am.counter, 1u);
+  __syncthreads();
+  if (s_ticket != (unsigned)(nblk_all - 1)) return;
+  __threadfence();
+  // the last block: per query, the minimum over the row blocks of its group
+  for (int b = threadIdx.x; b < B; b += blockDim.x) {
+    const int gy = b / NQ, a = b - gy * NQ;
+    unsigned long long k = ~0ull;
+    for (int bx = 0; bx < (int)gridDim.x; bx++) {
+      const unsigned long long v = *(volatile unsigned long long*)&am.part[(int64_t)(gy * gridDim.x + bx) * NQ + a];
+      k = v < k ? v : k;
+    }
+    am.out_cid[b] = k == ~0ull ? -1 : (int64_t)(unsigned)(k & 0xffffffffull);
+    if (am.out_d) am.out_d[b] = key2f((uint32_t)(k >> 32));
+  }
+  if (threadIdx.x == 0) *am.counter = 0;
 }
 
 template <int METRIC>
 static void dist_dense_dispatch(const float* Q, int64_t ldq, int B, const float* X, int64_t ldx,
                                 int64_t n, int dp, const float* qnorm, float* D, int64_t ldd,
-                                cudaStream_t st) {
+                                cudaStream_t st, DenseArgmin am = DenseArgmin()) {
   if (B <= 0 || n <= 0) return;
   int nq = B >= 16 ? 16 : (B >= 8 ? 8 : (B >= 4 ? 4 : (B >= 2 ? 2 : 1)));
   while (nq > 1 && (size_t)nq * dp * 4 > 96 * 1024) nq >>= 1;
+  // small calls (an insert batch's assignment): fewer queries per block until
+  // the grid covers the GPU twice -- each thread's chains are sequential, so
+  // a block with 8 queries takes 8x as long as one with 1
+  while (nq > 1 && B <= 16 && ((n + 31) / 32) * ((B + nq - 1) / nq) < 296) nq >>= 1;
   size_t smem = (size_t)nq * dp * 4 + (size_t)DD_RING * 128 * DD_RS * 4;
   const int64_t ny = (B + nq - 1) / nq;
   int rpb = 128;
@@ -190,7 +256,7 @@ static void dist_dense_dispatch(const float* Q, int64_t ldq, int B, const float*
   case NQV: {                                                                                       \
     auto k = dist_dense_kernel<METRIC, NQV>;                                                        \
     PK_SMEM_ATTR(k, (int)smem);                \
-    k<<<grid, 128, smem, st>>>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, rpb);                       \
+    k<<<grid, 128, smem, st>>>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, rpb, am);                   \
   } break;
   switch (nq) {
     PK_DD(1) PK_DD(2) PK_DD(4) PK_DD(8) PK_DD(16)
@@ -204,6 +270,28 @@ void launch_dist_dense(int metric, const float* Q, int64_t ldq, int B, const flo
   if (metric == SQ_L2) dist_dense_dispatch<SQ_L2>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, st);
   else if (metric == IP) dist_dense_dispatch<IP>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, st);
   else dist_dense_dispatch<COSINE>(Q, ldq, B, X, ldx, n, dp, qnorm, D, ldd, st);
+}
+
+int dense_argmin_blocks(int64_t n, int B) {
+  // partial entries: blocks (<= ceil(n / 32) row blocks x ceil(B / nq) query
+  // groups) x nq entries each <= ceil(n / 32) x (B + 16)
+  return (int)(((n + 31) / 32) * (B + 16));
+}
+
+void launch_dense_argmin(int metric, const float* Q, int64_t ldq, int B, const float* C, int64_t n, int dp,
+                         const float* qnorm, ListTable lt, int32_t scope_code, unsigned long long* part,
+                         unsigned* counter, int64_t* out_cid, float* out_d, cudaStream_t st) {
+  DenseArgmin am;
+  am.cid = lt.cid;
+  am.scope = lt.scope;
+  am.scope_code = scope_code;
+  am.part = part;
+  am.counter = counter;
+  am.out_cid = out_cid;
+  am.out_d = out_d;
+  if (metric == SQ_L2) dist_dense_dispatch<SQ_L2>(Q, ldq, B, C, dp, n, dp, qnorm, nullptr, 0, st, am);
+  else if (metric == IP) dist_dense_dispatch<IP>(Q, ldq, B, C, dp, n, dp, qnorm, nullptr, 0, st, am);
+  else dist_dense_dispatch<COSINE>(Q, ldq, B, C, dp, n, dp, qnorm, nullptr, 0, st, am);
 }
 
 // =====================================================================

@@ -55,6 +55,15 @@ struct ListTable {
 void launch_dist_dense(int metric, const float* Q, int64_t ldq, int B, const float* X, int64_t ldx,
                        int64_t n, int dp, const float* qnorm, float* D, int64_t ldd,
                        cudaStream_t st);
+// assign_nearest in ONE launch: distances of B rows of Q to the n centroid
+// slots of C with the argmin by (dist, cid) over the slots of scope_code fused
+// in (block minima in part[], the last block reduces; counter starts at 0 and
+// is left at 0).  Requires cids < 2^32.  part needs dense_argmin_blocks(n, B)
+// entries.
+int dense_argmin_blocks(int64_t n, int B);
+void launch_dense_argmin(int metric, const float* Q, int64_t ldq, int B, const float* C, int64_t n, int dp,
+                         const float* qnorm, ListTable lt, int32_t scope_code, unsigned long long* part,
+                         unsigned* counter, int64_t* out_cid, float* out_d, cudaStream_t st);
 // kmeans_assign arithmetic (fp32 square, fp64 sum), fused argmin over k rows of C.
 void launch_kmeans_assign(const float* X, int64_t ldx, int64_t n, const float* C, int64_t ldc,
                           int64_t k, int dp, int64_t* labels, double* dists, cudaStream_t st);

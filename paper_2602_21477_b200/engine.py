@@ -819,7 +819,7 @@ class Store:
         assignments computed in one device call and recomputed only after a
         centroid change."""
         self._check_writable(agent, scope)
-        vecs = [as_vector(v, self.cfg.dimension) for v in vectors]
+        vecs = self._vectors(vectors)
         if payloads is None:
             payloads = [b""] * len(vecs)
         if len(payloads) != len(vecs):
@@ -867,7 +867,7 @@ class Store:
                 i += 1
                 continue
             if assigned is None:
-                assigned = self.clusters.assign_nearest_batch(np.stack(vecs[i:]), scope)
+                assigned = self.clusters.assign_nearest_batch(vecs[i:], scope)
                 assigned_from = i
             # the longest run of vectors whose inserts fire no split and no
             # maintenance (the reference checks after every vector,
@@ -880,11 +880,7 @@ class Store:
                 p_ = payloads[t]
                 self.payloads[run_ids[t - i]] = p_.encode("utf-8") if isinstance(p_, str) else p_
             run_cids = assigned[i - assigned_from:j - assigned_from]
-            run_vecs = np.stack(vecs[i:j])
-            run_ids_a = np.asarray(run_ids, dtype=np.int64)
-            for cid in dict.fromkeys(run_cids.tolist()):  # clusters in first-touch order
-                sel = np.flatnonzero(run_cids == cid)
-                self.tier.buffered_insert_many(int(cid), run_ids_a[sel], run_vecs[sel])
+            self.tier.buffered_insert_batch(run_cids, np.asarray(run_ids, dtype=np.int64), vecs[i:j])
             if fired:
                 self._after_cluster_mutation(int(run_cids[-1]))
                 assigned = None  # a centroid moved: later vectors re-assign
@@ -894,6 +890,20 @@ class Store:
             accepted.extend(run_ids)
             i = j
         return accepted
+
+    def _vectors(self, vectors) -> np.ndarray:
+        """The batch as one [n, d] float32 matrix with as_vector's checks
+        (ref/core.py:74-86): validated in one pass; anything irregular goes
+        through as_vector row by row for the same error."""
+        d = self.cfg.dimension
+        try:
+            m = np.ascontiguousarray(vectors, dtype=np.float32)
+        except (ValueError, TypeError):
+            m = None
+        if m is None or m.ndim != 2 or m.shape[1] != d or not np.isfinite(m).all():
+            rows = [as_vector(v, d) for v in vectors]  # raises the reference's error
+            return np.stack(rows) if rows else np.empty((0, d), np.float32)
+        return m
 
     def _insert_run(self, assigned, base: int, i: int, n: int):
         """(j, fired): vectors i..j-1 go to their assigned clusters; fired when

@@ -141,6 +141,16 @@ class DeviceIndex:
             with self._pend_lock:
                 self._pend.append((int(cid), rows, ids))
 
+    def append_rows(self, cids, rows, ids):
+        """Appends of several clusters at once (cids per row; each cluster's
+        rows in order), queued like ``append``."""
+        rows = N.f32(rows, self.dimension)
+        ids = np.ascontiguousarray(ids, dtype=np.int64)
+        cids = np.ascontiguousarray(cids, dtype=np.int64)
+        if len(ids):
+            with self._pend_lock:
+                self._pend.append((cids, rows, ids))
+
     def flush(self):
         if not self._pend:
             return
@@ -148,7 +158,8 @@ class DeviceIndex:
             pend, self._pend = self._pend, []
         if not pend:
             return
-        cids = np.concatenate([np.full(len(i), c, dtype=np.int64) for c, _, i in pend])
+        cids = np.concatenate([c if isinstance(c, np.ndarray) else np.full(len(i), c, dtype=np.int64)
+                               for c, _, i in pend])
         rows = np.ascontiguousarray(np.concatenate([r for _, r, _ in pend]))
         ids = np.ascontiguousarray(np.concatenate([i for _, _, i in pend]))
         N.check(N.lib().pk_list_append_batch(self._h, len(ids), N.ptr(cids), N.ptr(rows), N.ptr(ids)))

@@ -413,6 +413,14 @@ class ShardedStoreIndex:
         if r == self.rank:
             self.local.append(cid, rows, ids)
 
+    def append_rows(self, cids, rows, ids):
+        cids = np.asarray(cids, dtype=np.int64)
+        rows = np.asarray(rows, dtype=np.float32).reshape(len(cids), self.dimension)
+        ids = np.asarray(ids, dtype=np.int64)
+        for c in dict.fromkeys(cids.tolist()):
+            sel = np.flatnonzero(cids == c)
+            self.append(c, rows[sel], ids[sel])
+
     def remove_row(self, cid: int, row: int):
         r = self.owner[int(cid)]
         self.nrows[int(cid)] -= 1

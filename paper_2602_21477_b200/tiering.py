@@ -211,6 +211,14 @@ class TierManager:
         if not (self.native and cl.resident is None):
             self._count_flushes(cl, len(item_ids))
 
+    def buffered_insert_batch(self, cids: np.ndarray, item_ids: np.ndarray, vectors: np.ndarray):
+        """buffered_insert of a run of items (per cluster in batch order): one
+        queued device append for the run, the host mirrors per cluster."""
+        for cid, n in self.store.add_members_batch(cids, item_ids, vectors):
+            cl = self.store.clusters[cid]
+            if not (self.native and cl.resident is None):
+                self._count_flushes(cl, n)
+
     def _count_flushes(self, cl, n: int):
         """``buffer_flush_count`` keeps the reference's meaning on the native
         tier: the reference buffers inserts into a resident cluster and flushes
