@@ -208,7 +208,8 @@ struct Walk {
 // is the single-thread walk's.
 struct WarpWalk {
   const float* drow;
-  const GraphDev* g;
+  GraphDev g;  // by value: its pointers stay in registers (an address-taken
+               // local would live in local memory, one load per hop)
   uint32_t* stamp;
   // candidates: an unsorted array (shared memory) -- the pop is a warp
   // argmin (keys are unique), the hole refilled from the end; cheaper than a
@@ -263,7 +264,7 @@ struct WarpWalk {
   __device__ void seed(int s, uint32_t ep, int ef) {
     if (lane == 0) stamp[s] = ep;
     __syncwarp();
-    const uint32_t k = dk(s), r = (uint32_t)g->rank[s];
+    const uint32_t k = dk(s), r = (uint32_t)g.rank[s];
     cand_push(kmin(k, r));
     best_insert(kworst(k, r), ef);
   }
@@ -281,7 +282,7 @@ struct WarpWalk {
       if (fresh) {
         stamp[x] = ep;
         k = dk(x);
-        r = (uint32_t)g->rank[x];
+        r = (uint32_t)g.rank[x];
       }
       counter += __popc(fm);
       while (fm) {  // admissions in link order
@@ -296,21 +297,21 @@ struct WarpWalk {
       __syncwarp();  // stamps visible to the next chunk
     }
   }
-  __device__ int slot_of(uint64_t key) const { return g->slot_of_rank[(uint32_t)key]; }
+  __device__ int slot_of(uint64_t key) const { return g.slot_of_rank[(uint32_t)key]; }
   __device__ const int32_t* nbrs(int s, int layer) const {
-    return layer == 0 ? g->nbr0 + (int64_t)s * g->M : g->up + g->up_off[s] + (int64_t)(layer - 1) * g->M;
+    return layer == 0 ? g.nbr0 + (int64_t)s * g.M : g.up + g.up_off[s] + (int64_t)(layer - 1) * g.M;
   }
   __device__ int degree(const int32_t* nb) const {  // valid prefix of a -1 padded neighbor list
-    const unsigned v = __ballot_sync(FULLW, lane < g->M && nb[min(lane, g->M - 1)] >= 0);
-    const unsigned inv = ~v & ((g->M >= 32) ? FULLW : ((1u << g->M) - 1u));
-    return inv ? __ffs(inv) - 1 : g->M;
+    const unsigned v = __ballot_sync(FULLW, lane < g.M && nb[min(lane, g.M - 1)] >= 0);
+    const unsigned inv = ~v & ((g.M >= 32) ? FULLW : ((1u << g.M) - 1u));
+    return inv ? __ffs(inv) - 1 : g.M;
   }
   __device__ void search_layer(int layer, int ef, uint32_t ep) {
     uint64_t ck;
     while (cand_pop(&ck)) {
       if (bn > 0 && (uint32_t)(ck >> 32) > worst_dk() && bn >= ef) break;
       const int c = slot_of(ck);
-      if (layer > g->level[c]) continue;
+      if (layer > g.level[c]) continue;
       const int32_t* nb = nbrs(c, layer);
       const int m = degree(nb);
       visit(m, [&](int jj) { return (int)nb[jj]; }, ef, ep);
@@ -347,6 +348,9 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
   const float* drow_g = D + (int64_t)b * ldd;
   float* srow = reinterpret_cast<float*>(sm + (size_t)(2 * ns + 2) * 8 + (size_t)ns * 4);
   GraphDev g = g0;
+  // the scope flags (staged below); the kernel parameter gq stays read-only,
+  // so it is read from the parameter bank rather than copied to local memory
+  const uint8_t* flags = gq.flags;
   if (smem_graph) {  // the walk's arrays, after the heaps / stamps / row
     uint8_t* p = sm + (((size_t)(2 * ns + 2) * 8 + (size_t)ns * 8 + 15) & ~(size_t)15);
     int32_t* nb = reinterpret_cast<int32_t*>(p);
@@ -383,7 +387,7 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
     g.rank = rk;
     g.slot_of_rank = sr;
     g.level = lv;
-    gq.flags = fl;
+    flags = fl;
   }
   for (int s = tid; s < ns; s += GRAPH_THREADS) {
     stamp[s] = 0;
@@ -396,7 +400,7 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
     // ef <= 32 and no more seeds than ef: the warp walk
     WarpWalk w;
     w.drow = smem_row ? srow : drow_g;
-    w.g = &g;
+    w.g = g;
     w.stamp = stamp;
     w.ck = heaps;
     w.cn = 0;
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
         const int p0 = g.por_off[c], np = g.por_off[c + 1] - p0;
         w.visit(m + np, [&](int j) {
           const int x = j < m ? (int)nb[j] : (int)g.por[p0 + j - m];
-          return (j < m || (gq.flags[x] & 2)) ? x : -1;
+          return (j < m || (flags[x] & 2)) ? x : -1;
         }, ef, ep);
       }
       emit = ep;
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
         // links = neighbors[0] + the portals into expanded scopes, in order
         w.visit(m + np, [&](int j) {
           const int x = j < m ? (int)nb[j] : (int)g.por[p0 + j - m];
-          return (j < m || (gq.flags[x] & 2)) ? x : -1;
+          return (j < m || (flags[x] & 2)) ? x : -1;
         }, ef, ep);
       }
       emit = ep;  // emitted: every node this frontier visited (the reference's dists dict)
@@ -533,7 +537,7 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
   int ne = 0;
   for (int s0 = 0; s0 < ns; s0 += 32) {
     const int s = s0 + lane;
-    const bool hit = s < ns && stamp[s] == emit && (gq.flags[s] & 1);
+    const bool hit = s < ns && stamp[s] == emit && (flags[s] & 1);
     const unsigned m = __ballot_sync(FULLW, hit);
     if (hit) ek[ne + __popc(m & ((1u << lane) - 1u))] = kmin(f2key(drow[s]), (uint32_t)g.rank[s]);
     ne += __popc(m);

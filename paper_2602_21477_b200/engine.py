@@ -709,12 +709,18 @@ class Store:
         off = table._offsets()[idx]
         return (idx, int(np.argmin(row[off:off + len(table.fsms[idx].states)])))
 
-    def _cache_items(self, hits):
+    def _cache_items(self, hits, positions: bool = False):
+        """(id, vector, scope code, staged=False) of the hits that are still
+        live; with positions, (index in hits, item) pairs.  The vectors are
+        views: the pools copy what they keep."""
         out = []
-        for iid, _, sc in hits:
-            vec = self._vector_of(iid)
+        code = self.scope_codes.code
+        for pos, (iid, _, sc) in enumerate(hits):
+            vec = self._vector_view(iid)
             if vec is not None:
-                out.append((iid, vec, self.scope_codes.intern(sc), False))
+                c = code.get(sc)
+                item = (iid, vec, c if c is not None else self.scope_codes.intern(sc), False)
+                out.append((pos, item) if positions else item)
         return out
 
     def _search_side_effects(self, agent, q, k, hint, result, extended, internal):
@@ -729,8 +735,12 @@ class Store:
             elif cache.verify_mode and not internal:
                 self.runner.submit("search", self._verify_early_return, agent, q, k, result)
             state_key = self._state_key_for(agent, q)
-            outcomes = cache.promote_and_capture(self._cache_items(result.hits), state_key, q,
-                                                 self._cache_items(extended))
+            # the hits are the extended list's first k entries: one lookup each
+            ext_items = self._cache_items(extended, positions=True)
+            nh = len(result.hits)
+            hit_items = [it for pos, it in ext_items if pos < nh] if extended[:nh] == result.hits \
+                else [it for _, it in self._cache_items(result.hits, positions=True)]
+            outcomes = cache.promote_and_capture(hit_items, state_key, q, [it for _, it in ext_items])
             if any(not o.empty for o in outcomes):
                 with self._lock.write():
                     self._materialize(agent, outcomes)
@@ -1058,6 +1068,10 @@ class Store:
 
     # --- item access -------------------------------------------------------
     def _vector_of(self, item_id: int):
+        v = self._vector_view(item_id)
+        return None if v is None else v.copy()
+
+    def _vector_view(self, item_id: int):
         owner = self.clusters.owner.get(item_id)
         if owner is None:
             return None
@@ -1065,7 +1079,7 @@ class Store:
             return self.clusters.staged[owner[1]].get(item_id)
         cl = self.clusters.clusters[owner[1]]
         row = cl.id_to_row.get(item_id)
-        return cl.vectors[row].copy() if row is not None else None
+        return cl.vectors[row] if row is not None else None
 
     def get_item(self, item_id: int):
         vec = self._vector_of(item_id)
