@@ -128,16 +128,16 @@ struct MaxHeap {
 
 struct Walk {
   const float* drow;      // exact distances of this query to every slot
-  const GraphDev* g;
+  GraphDev g;  // by value (no address-taken local: it would live in local memory)
   uint32_t* stamp;        // [ns] visit stamps of this query
   MinHeap cand;
   MaxHeap best;
   int counter;
   __device__ uint32_t dk(int s) const { return f2key(drow[s]); }
-  __device__ uint32_t rk(int s) const { return (uint32_t)g->rank[s]; }
-  __device__ int slot_of(uint64_t key) const { return g->slot_of_rank[(uint32_t)key]; }
+  __device__ uint32_t rk(int s) const { return (uint32_t)g.rank[s]; }
+  __device__ int slot_of(uint64_t key) const { return g.slot_of_rank[(uint32_t)key]; }
   __device__ const int32_t* nbrs(int s, int layer) const {
-    return layer == 0 ? g->nbr0 + (int64_t)s * g->M : g->up + g->up_off[s] + (int64_t)(layer - 1) * g->M;
+    return layer == 0 ? g.nbr0 + (int64_t)s * g.M : g.up + g.up_off[s] + (int64_t)(layer - 1) * g.M;
   }
   __device__ void seed(int s, uint32_t ep) {
     stamp[s] = ep;
@@ -178,10 +178,10 @@ struct Walk {
       const uint64_t ck = cand.pop();
       if (best.n > 0 && (uint32_t)(ck >> 32) > best.worst_dk() && best.n >= ef) break;
       const int c = slot_of(ck);
-      if (layer > g->level[c]) continue;
+      if (layer > g.level[c]) continue;
       const int32_t* nb = nbrs(c, layer);
       int m = 0;
-      while (m < g->M && nb[m] >= 0) m++;
+      while (m < g.M && nb[m] >= 0) m++;
       visit(m, [&](int j) { return (int)nb[j]; }, ef, ep);
     }
   }
@@ -220,9 +220,9 @@ struct WarpWalk {
   int bn;
   int counter;
   int lane;
-  __device__ uint32_t dk(int s) const { return f2key(drow[s]); }
-  __device__ uint32_t worst_dk() const { return (uint32_t)(__shfl_sync(FULLW, bv, bn - 1) >> 32); }
-  __device__ void best_insert(uint64_t k, int ef) {
+  __device__ __forceinline__ uint32_t dk(int s) const { return f2key(drow[s]); }
+  __device__ __forceinline__ uint32_t worst_dk() const { return (uint32_t)(__shfl_sync(FULLW, bv, bn - 1) >> 32); }
+  __device__ __forceinline__ void best_insert(uint64_t k, int ef) {
     const bool less = lane < bn && bv < k;
     const int pos = __popc(__ballot_sync(FULLW, less));
     const uint64_t up = __shfl_up_sync(FULLW, bv, 1);
@@ -230,13 +230,16 @@ struct WarpWalk {
     if (lane == pos) bv = k;
     bn = min(bn + 1, ef);  // full: the old worst fell off the end
   }
-  __device__ void cand_push(uint64_t k) {
+  __device__ __forceinline__ void cand_push(uint64_t k) {
     if (lane == 0) ck[cn] = k;
     cn++;
   }
-  __device__ bool cand_pop(uint64_t* k) {
+  // the smallest candidate, removed; ~0 when none is left (no key is all
+  // ones: ranks are below the slot count).  Returned by value: an
+  // out-parameter would put the key in local memory on every pop.
+  __device__ __forceinline__ uint64_t cand_pop() {
     __syncwarp();
-    if (cn == 0) return false;
+    if (cn == 0) return ~0ull;
     uint64_t best = ~0ull;
     int bi = 0;
     for (int i = lane; i < cn; i += 32) {
@@ -258,10 +261,9 @@ struct WarpWalk {
     __syncwarp();
     if (lane == 0) ck[bi] = ck[cn - 1];
     cn--;
-    *k = best;
-    return true;
+    return best;
   }
-  __device__ void seed(int s, uint32_t ep, int ef) {
+  __device__ __forceinline__ void seed(int s, uint32_t ep, int ef) {
     if (lane == 0) stamp[s] = ep;
     __syncwarp();
     const uint32_t k = dk(s), r = (uint32_t)g.rank[s];
@@ -270,7 +272,7 @@ struct WarpWalk {
   }
   // links of one expanded node, in order (x(j) < 0: not a link)
   template <typename LinkF>
-  __device__ void visit(int nl, LinkF link, int ef, uint32_t ep) {
+  __device__ __forceinline__ void visit(int nl, LinkF link, int ef, uint32_t ep) {
     for (int j0 = 0; j0 < nl; j0 += 32) {
       const int j = j0 + lane;
       const int x = j < nl ? link(j) : -1;
@@ -297,18 +299,17 @@ struct WarpWalk {
       __syncwarp();  // stamps visible to the next chunk
     }
   }
-  __device__ int slot_of(uint64_t key) const { return g.slot_of_rank[(uint32_t)key]; }
-  __device__ const int32_t* nbrs(int s, int layer) const {
+  __device__ __forceinline__ int slot_of(uint64_t key) const { return g.slot_of_rank[(uint32_t)key]; }
+  __device__ __forceinline__ const int32_t* nbrs(int s, int layer) const {
     return layer == 0 ? g.nbr0 + (int64_t)s * g.M : g.up + g.up_off[s] + (int64_t)(layer - 1) * g.M;
   }
-  __device__ int degree(const int32_t* nb) const {  // valid prefix of a -1 padded neighbor list
+  __device__ __forceinline__ int degree(const int32_t* nb) const {  // valid prefix of a -1 padded neighbor list
     const unsigned v = __ballot_sync(FULLW, lane < g.M && nb[min(lane, g.M - 1)] >= 0);
     const unsigned inv = ~v & ((g.M >= 32) ? FULLW : ((1u << g.M) - 1u));
     return inv ? __ffs(inv) - 1 : g.M;
   }
-  __device__ void search_layer(int layer, int ef, uint32_t ep) {
-    uint64_t ck;
-    while (cand_pop(&ck)) {
+  __device__ __forceinline__ void search_layer(int layer, int ef, uint32_t ep) {
+    for (uint64_t ck = cand_pop(); ck != ~0ull; ck = cand_pop()) {
       if (bn > 0 && (uint32_t)(ck >> 32) > worst_dk() && bn >= ef) break;
       const int c = slot_of(ck);
       if (layer > g.level[c]) continue;
@@ -317,10 +318,11 @@ struct WarpWalk {
       visit(m, [&](int jj) { return (int)nb[jj]; }, ef, ep);
     }
   }
-  __device__ int descend(int entry, int maxl, uint32_t* epoch) {
+  uint32_t epoch;  // visit-stamp epoch (a member: no address-taken local)
+  __device__ __forceinline__ int descend(int entry, int maxl) {
     int cur = entry;
     for (int layer = maxl; layer >= 1; layer--) {
-      const uint32_t ep = ++(*epoch);
+      const uint32_t ep = ++epoch;
       cn = 0;
       bn = 0;
       seed(cur, ep, 1);
@@ -335,7 +337,7 @@ struct WarpWalk {
 // and the distance row f32[ns] when `smem_row`
 constexpr int GRAPH_THREADS = 256;
 
-__global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float* __restrict__ D, int64_t ldd,
+__global__ void __launch_bounds__(GRAPH_THREADS, 1) graph_search_kernel(const float* __restrict__ D, int64_t ldd,
                                                           GraphDev g0, GraphQuery gq, int smem_heaps,
                                                           int smem_row, int smem_graph, uint32_t* gstamps,
                                                           uint64_t* gheap, int32_t* probe, int32_t* counter_out) {
@@ -408,29 +410,28 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
     w.bv = 0;
     w.counter = 0;
     w.lane = lane;
+    w.epoch = 0;
     const int ef = min(gq.ef, ns);
-    uint32_t epoch = 0;
     if (gq.mode == 0) {
       int nseeds = 0;
       int seeds[1 + GRAPH_MAX_SCOPES];
       if (gq.static_entry >= 0) {
         w.counter++;
-        seeds[nseeds++] = w.descend(gq.static_entry, gq.static_maxl, &epoch);
+        seeds[nseeds++] = w.descend(gq.static_entry, gq.static_maxl);
       }
       for (int i = 0; i < gq.n_sc; i++) {
         if (gq.sc_static[i] || gq.sc_entry[i] < 0) continue;
         w.counter++;
         seeds[nseeds++] = gq.sc_entry[i];
       }
-      const uint32_t ep = ++epoch;
+      const uint32_t ep = ++w.epoch;
       w.cn = 0;
       w.bn = 0;
       for (int i = 0; i < nseeds; i++) {
         __syncwarp();
         if (stamp[seeds[i]] != ep) w.seed(seeds[i], ep, ef);
       }
-      uint64_t ck;
-      while (w.cand_pop(&ck)) {
+      for (uint64_t ck = w.cand_pop(); ck != ~0ull; ck = w.cand_pop()) {
         if (w.bn > 0 && (uint32_t)(ck >> 32) > w.worst_dk() && w.bn >= ef) break;
         const int c = w.slot_of(ck);
         if (g.level[c] < 0) continue;
@@ -448,8 +449,8 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
         const int e = gq.sc_entry[i];
         if (e < 0) continue;
         w.counter++;
-        const int top = w.descend(e, gq.sc_maxl[i], &epoch);
-        const uint32_t ep = ++epoch;
+        const int top = w.descend(e, gq.sc_maxl[i]);
+        const uint32_t ep = ++w.epoch;
         w.cn = 0;
         w.bn = 0;
         w.seed(top, ep, ef);
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(GRAPH_THREADS) graph_search_kernel(const float
   } else if (lane == 0) {
     Walk w;
     w.drow = smem_row ? srow : drow_g;
-    w.g = &g;
+    w.g = g;
     w.stamp = stamp;
     // candidate heap: at most one push per node; result heap: <= nodes + 1
     w.cand.k = heaps;

@@ -307,6 +307,59 @@ def test_screen_adversarial(pk, kind, scan_mode):
         ix.close()
 
 
+def _fuzz_rows(rng, kind, n, d, scale):
+    if kind == "gauss":
+        x = rng.normal(size=(n, d))
+    elif kind == "uniform_pos":
+        x = rng.random(size=(n, d))
+    elif kind == "sparse":
+        x = rng.normal(size=(n, d)) * (rng.random(size=(n, d)) < 0.05)
+    elif kind == "heavy":
+        x = np.clip(rng.standard_cauchy(size=(n, d)), -1e3, 1e3)
+    elif kind == "near_dup":
+        base = rng.normal(size=(4, d))
+        x = base[rng.integers(0, 4, n)] + 1e-4 * rng.normal(size=(n, d))
+    else:  # "mixed": per-dimension magnitudes over 6 decades
+        x = rng.normal(size=(n, d)) * (10.0 ** rng.uniform(-3, 3, size=d))
+    return (x * scale).astype(np.float32)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_screen_fuzz_sweep(pk, seed):
+    """Fuzz sweep of the TF32 screens' error bound: random
+    dimensions (odd, below / above one 32-float chunk, up to 1536), scales over
+    12 decades and six value distributions, both screened metrics; the
+    tcgen05 scan + exact re-rank and the 3xTF32 coarse quantizer must give the
+    oracle's probe sets, ids and distance bits."""
+    from paper_2602_21477_b200 import DeviceIndex
+
+    rng = np.random.default_rng(1000 + seed)
+    kinds = ["gauss", "uniform_pos", "sparse", "heavy", "near_dup", "mixed"]
+    d = int(rng.choice([7, 17, 31, 33, 64, 100, 255, 384, 513, 768, 1024, 1536]))
+    scale = float(10.0 ** rng.uniform(-6, 6))
+    kind = kinds[seed % len(kinds)]
+    nl = int(rng.integers(4, 12))
+    lists = []
+    for c in range(nl):
+        n = int(rng.integers(1, 400))
+        lists.append((np.arange(c * 1000, c * 1000 + n, dtype=np.int64), _fuzz_rows(rng, kind, n, d, scale)))
+    Q = _fuzz_rows(rng, kind, 40, d, scale)
+    Q[0] = lists[0][1][0]  # an exact hit
+    for metric in (0, 1):
+        ix = DeviceIndex(d, metric, 0)
+        cents = np.stack([ix.create_list(c, 0, rows, ids) for c, (ids, rows) in enumerate(lists)])
+        flat = O.FlatIVF.from_lists(lists, cents, np.arange(nl), metric=["sq_l2", "ip"][metric])
+        for nprobe, kk in ((1, 10), (min(3, nl), 1), (nl, 64)):
+            out = ix.search(Q, [0], nprobe, kk, want_probe=True)
+            ids, dd, cnt, probe, scanned = flat.search(Q, nprobe, kk, threads=8)
+            ctx = (kind, d, scale, metric, nprobe, kk)
+            assert np.array_equal(out.probe, probe), ctx
+            assert np.array_equal(out.counts, cnt), ctx
+            assert np.array_equal(out.ids, ids), ctx
+            assert np.array_equal(bits(out.dists), bits(dd)), ctx
+        ix.close()
+
+
 @pytest.mark.parametrize("coarse", ["tc", "tf32", "exact"])
 @pytest.mark.parametrize("kind", ["random", "dup_centroids", "shell", "many"])
 def test_coarse_quantizer_matches_oracle(pk, kind, coarse, monkeypatch):

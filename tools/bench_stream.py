@@ -91,8 +91,11 @@ def main():
     del X, order
     torch.cuda.empty_cache()
     budget = int(a.budget_gb * (1 << 30))
+    # the same coarse ef as the reference arm (exhaustive: the flat oracle
+    # over the final index applies, and both stores probe the same lists)
     cfg = StoreConfig(dimension=a.d, accelerator="native", budget_bytes=budget, hotset_interval=64,
-                      cache_enabled=False, splits_enabled=False, seed=0)
+                      cache_enabled=False, splits_enabled=False, seed=0,
+                      ef_search_factor=max(4, -(-a.nlist // 32) * 2))
     store = Store(cfg)
     lists = [(ids_h[offs[c]:offs[c] + lens[c]], rows_h[offs[c]:offs[c] + lens[c]])
              for c in range(a.nlist) if lens[c] > 0]
