@@ -384,6 +384,7 @@ struct pk_index {
     t.nslots = nslots;
     t.dp = (int32_t)dp;
     t.d = (int32_t)d;
+    t.metric = metric;
     return t;
   }
 
@@ -1212,7 +1213,7 @@ int pk_merge_shards(pk_index* ix, const void* blocks, int32_t R, int64_t B, int3
     o_d = reinterpret_cast<float*>(base + 16 * nkk + 8 * B);
     o_n = reinterpret_cast<int32_t*>(base + 20 * nkk + 8 * B);
   }
-  launch_shard_merge(src, bb, R, (int)B, kk, o_ids, o_d, (dev && !out_cids) ? nullptr : o_cid, o_n,
+  launch_shard_merge(ix->metric, src, bb, R, (int)B, kk, o_ids, o_d, (dev && !out_cids) ? nullptr : o_cid, o_n,
                      (dev && !out_scanned) ? nullptr : o_sc, st);
   CK(cudaGetLastError());
   if (!dev) {
@@ -2234,7 +2235,7 @@ int pk_combine_merge(pk_index* ix, int64_t epoch, double timeout_s, int64_t* out
   if (!c.area) return fail(PK_ERR_USAGE, "pk_combine_create first");
   if (!(flags & PK_DEVICE_PTRS)) return fail(PK_ERR_USAGE, "peer combine takes device pointers");
   CK(cudaSetDevice(ix->device));
-  launch_peer_merge(c.area, c.bb, c.R, (int)c.group, c.kk, (uint64_t)epoch, (int64_t)(timeout_s * 1e9),
+  launch_peer_merge(ix->metric, c.area, c.bb, c.R, (int)c.group, c.kk, (uint64_t)epoch, (int64_t)(timeout_s * 1e9),
                     c.err, out_ids, out_dists, out_cids, out_n, out_scanned, ix->st);
   CK(cudaGetLastError());
   return PK_OK;

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(128) dist_dense_kernel(const float* __restrict
       k = v < k ? v : k;
     }
     am.out_cid[b] = k == ~0ull ? -1 : (int64_t)(unsigned)(k & 0xffffffffull);
-    if (am.out_d) am.out_d[b] = key2f((uint32_t)(k >> 32));
+    if (am.out_d) am.out_d[b] = key2dist((uint32_t)(k >> 32), METRIC);
   }
   if (threadIdx.x == 0) *am.counter = 0;
 }
@@ -1297,7 +1297,7 @@ __global__ void __launch_bounds__(128) merge_kernel(const int32_t* __restrict__ 
     const int64_t o = (int64_t)b * kk + i;
     if (i < kept) {
       out_ids[o] = mbuf[i].id;
-      out_d[o] = key2f(mbuf[i].key);
+      out_d[o] = key2dist(mbuf[i].key, lt.metric);
       if (out_cid) out_cid[o] = lt.cid[mbuf[i].pay];
     } else {
       out_ids[o] = -1;
@@ -2298,7 +2298,7 @@ __global__ void __launch_bounds__(RR_THREADS, LEAN ? 3 : 1) rerank_merge_kernel(
     const int64_t o = (int64_t)b * kk + i;
     if (i < kept) {
       out_ids[o] = buf[i].id;
-      out_d[o] = key2f(buf[i].key);
+      out_d[o] = key2dist(buf[i].key, METRIC);
       if (out_cid) out_cid[o] = lt.cid[buf[i].pay];
     } else {
       out_ids[o] = -1;
@@ -2442,7 +2442,7 @@ __global__ void __launch_bounds__(256) argmin_kernel(const float* __restrict__ D
         bi = s_i[w];
       }
     out_cid[b] = bi == ID_NONE ? -1 : bi;
-    if (out_d) out_d[b] = key2f(bk);
+    if (out_d) out_d[b] = key2dist(bk, lt.metric);
   }
 }
 void launch_argmin(const float* D, int64_t ldd, int B, ListTable lt, int32_t scope_code,
@@ -2481,7 +2481,7 @@ namespace pk {
 // in the union of every part's k smallest.  One CTA per query.
 // =====================================================================
 constexpr int SHM_CAP = 1024;  // R * kk <= 1024 (R <= 16 at kk 64)
-__global__ void __launch_bounds__(128) shard_merge_kernel(const uint8_t* __restrict__ blocks,
+__global__ void __launch_bounds__(128) shard_merge_kernel(int metric, const uint8_t* __restrict__ blocks,
                                                           int64_t block_bytes, int R, int B, int kk,
                                                           int64_t* __restrict__ out_ids,
                                                           float* __restrict__ out_d,
@@ -2519,7 +2519,7 @@ __global__ void __launch_bounds__(128) shard_merge_kernel(const uint8_t* __restr
       const int r = src / kk, e = src - r * kk;
       const uint8_t* blk = blocks + (int64_t)r * block_bytes;
       out_ids[o] = sbuf[i].id;
-      out_d[o] = key2f(sbuf[i].key);
+      out_d[o] = key2dist(sbuf[i].key, metric);
       if (out_cid) out_cid[o] = reinterpret_cast<const int64_t*>(blk + nkk * 8)[(int64_t)b * kk + e];
     } else {
       out_ids[o] = -1;
@@ -2572,7 +2572,7 @@ void launch_reblock(const int64_t* ids, const int64_t* cids, const int64_t* sc, 
       ids, cids, sc, d, n, B, group, kk, block_bytes, static_cast<uint8_t*>(dst));
 }
 
-void launch_shard_merge(const void* blocks, int64_t block_bytes, int R, int B, int kk,
+void launch_shard_merge(int metric, const void* blocks, int64_t block_bytes, int R, int B, int kk,
                         int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                         int64_t* out_scanned, cudaStream_t st) {
   if (B <= 0) return;
@@ -2580,7 +2580,7 @@ void launch_shard_merge(const void* blocks, int64_t block_bytes, int R, int B, i
   while (N < R * kk) N <<= 1;
   size_t smem = (size_t)N * sizeof(Entry);
   PK_SMEM_ATTR(shard_merge_kernel, (int)smem);
-  shard_merge_kernel<<<B, 128, smem, st>>>(static_cast<const uint8_t*>(blocks), block_bytes, R, B,
+  shard_merge_kernel<<<B, 128, smem, st>>>(metric, static_cast<const uint8_t*>(blocks), block_bytes, R, B,
                                            kk, out_ids, out_d, out_cid, out_n, out_scanned);
 }
 
@@ -3469,7 +3469,7 @@ void launch_peer_send(const int64_t* ids, const int64_t* cids, const int64_t* sc
                                          my_rank, epoch, done_ctr);
 }
 
-__global__ void __launch_bounds__(128) peer_merge_kernel(const uint8_t* __restrict__ area,
+__global__ void __launch_bounds__(128) peer_merge_kernel(int metric, const uint8_t* __restrict__ area,
                                                          int64_t block_bytes, int R, int B, int kk,
                                                          uint64_t epoch, int64_t timeout_ns,
                                                          int32_t* __restrict__ err,
@@ -3529,7 +3529,7 @@ __global__ void __launch_bounds__(128) peer_merge_kernel(const uint8_t* __restri
       const int src = sbuf[i].pay;
       const int r = src / kk, e = src - r * kk;
       out_ids[o] = sbuf[i].id;
-      out_d[o] = key2f(sbuf[i].key);
+      out_d[o] = key2dist(sbuf[i].key, metric);
       if (out_cid)
         out_cid[o] = reinterpret_cast<const int64_t*>(area + (int64_t)r * block_bytes + nkk * 8)[(int64_t)b * kk + e];
     } else {
@@ -3549,7 +3549,7 @@ __global__ void __launch_bounds__(128) peer_merge_kernel(const uint8_t* __restri
   }
 }
 
-void launch_peer_merge(const void* area, int64_t block_bytes, int R, int B, int kk, uint64_t epoch,
+void launch_peer_merge(int metric, const void* area, int64_t block_bytes, int R, int B, int kk, uint64_t epoch,
                        int64_t timeout_ns, int32_t* err, int64_t* out_ids, float* out_d,
                        int64_t* out_cid, int32_t* out_n, int64_t* out_scanned, cudaStream_t st) {
   if (B <= 0) return;
@@ -3557,7 +3557,7 @@ void launch_peer_merge(const void* area, int64_t block_bytes, int R, int B, int 
   while (N < R * kk) N <<= 1;
   const size_t smem = (size_t)N * sizeof(Entry);
   PK_SMEM_ATTR(peer_merge_kernel, (int)smem);
-  peer_merge_kernel<<<B, 128, smem, st>>>(static_cast<const uint8_t*>(area), block_bytes, R, B, kk, epoch,
+  peer_merge_kernel<<<B, 128, smem, st>>>(metric, static_cast<const uint8_t*>(area), block_bytes, R, B, kk, epoch,
                                           timeout_ns, err, out_ids, out_d, out_cid, out_n, out_scanned);
 }
 

@@ -48,6 +48,7 @@ struct ListTable {
   int32_t nslots;
   int32_t dp;            // padded row stride (multiple of DC)
   int32_t d;             // true dimension
+  int32_t metric;        // the index metric (output sign of zero distances)
 };
 
 // ---- launchers (all async on `st`) ----
@@ -190,7 +191,7 @@ int shard_merge_cap();
 void launch_reblock(const int64_t* ids, const int64_t* cids, const int64_t* sc, const float* d,
                     const int32_t* n, int B, int group, int kk, int64_t block_bytes, void* dst,
                     cudaStream_t st);
-void launch_shard_merge(const void* blocks, int64_t block_bytes, int R, int B, int kk,
+void launch_shard_merge(int metric, const void* blocks, int64_t block_bytes, int R, int B, int kk,
                         int64_t* out_ids, float* out_d, int64_t* out_cid, int32_t* out_n,
                         int64_t* out_scanned, cudaStream_t st);
 
@@ -277,7 +278,7 @@ void launch_peer_send(const int64_t* ids, const int64_t* cids, const int64_t* sc
                       const int32_t* n, int B, int group, int kk, int64_t block_bytes,
                       uint8_t* const* peers, int R, int my_rank, uint64_t epoch, uint32_t* done_ctr,
                       cudaStream_t st);
-void launch_peer_merge(const void* area, int64_t block_bytes, int R, int B, int kk, uint64_t epoch,
+void launch_peer_merge(int metric, const void* area, int64_t block_bytes, int R, int B, int kk, uint64_t epoch,
                        int64_t timeout_ns, int32_t* err, int64_t* out_ids, float* out_d,
                        int64_t* out_cid, int32_t* out_n, int64_t* out_scanned, cudaStream_t st);
 

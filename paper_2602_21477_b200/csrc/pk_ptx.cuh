@@ -34,6 +34,14 @@ __host__ __device__ __forceinline__ uint32_t key2bits(uint32_t k) {
   return (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
 }
 __device__ __forceinline__ float key2f(uint32_t k) { return __uint_as_float(key2bits(k)); }
+// A distance back from its key.  Keys fold -0.0 into +0.0 (they order equal);
+// the reference's zero distances have a fixed sign per metric -- neg_ip
+// returns -acc and acc is never -0.0 (it starts at +0 and RN sums that cancel
+// give +0), so an inner-product zero is -0.0; sq_l2 and cosine zeros are +0.0
+__device__ __forceinline__ float key2dist(uint32_t k, int metric) {
+  const float v = key2f(k);
+  return (metric == 1 && v == 0.f) ? __uint_as_float(0x80000000u) : v;
+}
 __host__ __device__ __forceinline__ bool lex_less(uint32_t ka, int64_t ia, uint32_t kb, int64_t ib) {
   return ka < kb || (ka == kb && ia < ib);
 }

@@ -342,3 +342,35 @@ def test_stop_rule_by_count_equals_kth():
             want = kth is not None and kth < thresh
             below += int(np.count_nonzero(chunks[j] < thresh))
             assert (below >= k) == want, (trial, j)
+
+
+def test_batched_adds_equal_sequential():
+    """VectorPool.add_many / L1Cluster.add_many (the capture's batched adds)
+    leave the same rows, slots' uploads and bit-identical fp64 running sums as
+    add() one item at a time (ref/cache.py:44-51)."""
+    from paper_2602_21477_b200.cache import L1Cluster
+    from paper_2602_21477_b200.rowstore import RowStore
+
+    rng = np.random.default_rng(3)
+    d = 37
+    for trial in range(20):
+        sa, sb = RowStore(None, d), RowStore(None, d)
+        a, b = L1Cluster(d, sa), L1Cluster(d, sb)
+        base = [(int(i), (rng.normal(size=d) * 10 ** rng.uniform(-3, 3)).astype(np.float32),
+                 int(rng.integers(0, 3)), bool(rng.integers(0, 2))) for i in range(int(rng.integers(0, 9)))]
+        for it in base:
+            a.add(*it)
+            b.add(*it)
+        new = [(100 + i, (rng.normal(size=d) * 10 ** rng.uniform(-3, 3)).astype(np.float32),
+                int(rng.integers(0, 3)), bool(rng.integers(0, 2))) for i in range(int(rng.integers(1, 25)))]
+        for it in new:
+            a.add(*it)
+        b.add_many(new)
+        assert a._sum.tobytes() == b._sum.tobytes()
+        assert a.centroid.tobytes() == b.centroid.tobytes()
+        assert a.pool.ids.tolist() == b.pool.ids.tolist()
+        assert np.array_equal(a.pool.vectors, b.pool.vectors)
+        assert a.pool.scopes.tolist() == b.pool.scopes.tolist()
+        assert [a.pool.staged_flag(i) for i in a.pool.ids] == [b.pool.staged_flag(i) for i in b.pool.ids]
+        pa, pb = sa.take_puts(), sb.take_puts()
+        assert sorted(pa[0].tolist()) == sorted(pb[0].tolist())
