@@ -2746,7 +2746,7 @@ int pk_l1_place(pk_index* ix, int32_t nc, int32_t n_p, int32_t capacity, const d
   if (n_p > maxc || nc + m > maxc)
     return fail(PK_ERR_USAGE, "L1 placement of %d items over %d clusters exceeds %d", m, nc, maxc);
   if (nc > n_p) return fail(PK_ERR_USAGE, "%d live L1 clusters above n_p %d", nc, n_p);
-  if ((int64_t)(n_p + 1) * ix->dp * 4 > 227 * 1024)
+  if (((int64_t)n_p * (ix->dp + 4) + ix->dp) * 4 > 227 * 1024)
     return fail(PK_ERR_USAGE, "n_p %d x dimension %lld exceeds the placement kernel's shared memory", n_p,
                 (long long)ix->d);
   if (m == 0 && !q) return PK_OK;

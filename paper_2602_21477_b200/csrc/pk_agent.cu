@@ -274,8 +274,12 @@ __global__ void __launch_bounds__(256) l1_place_kernel(int nc0, int n_p, int cap
   // the live clusters' centroids live in shared memory (n_p rows, a slot per
   // live cluster) with the item being placed: every chain step reads shared
   // memory, not L2
-  extern __shared__ __align__(16) float l1s[];  // [n_p][dp] centroids | [dp] item
-  float* vs = l1s + (size_t)n_p * dp;
+  // rows at a stride of dp + 4 floats: the chains (one thread per cluster)
+  // read the same column of different rows at once, and a multiple-of-32
+  // stride would put all of them in one bank
+  extern __shared__ __align__(16) float l1s[];  // [n_p][dp + 4] centroids | [dp] item
+  const int ls = dp + 4;
+  float* vs = l1s + (size_t)n_p * ls;
   __shared__ int order[L1_MAXC];
   __shared__ uint8_t merged[L1_MAXC];
   __shared__ int hold[L1_MAXC];   // per chain item: the cluster holding its id after it
@@ -295,7 +299,10 @@ __global__ void __launch_bounds__(256) l1_place_kernel(int nc0, int n_p, int cap
     n_free = 0;
     for (int i = n_p - 1; i >= nc0; i--) sfree[n_free++] = i;
   }
-  for (int i = tid; i < nc0 * dp; i += blockDim.x) l1s[i] = cents[i];
+  for (int i = tid; i < nc0 * dp; i += blockDim.x) {
+    const int r = i / dp;
+    l1s[(size_t)r * ls + (i - r * dp)] = cents[i];
+  }
   __syncthreads();
   for (int it = 0; it <= m; it++) {
     const bool is_q = it == m;
@@ -307,7 +314,7 @@ __global__ void __launch_bounds__(256) l1_place_kernel(int nc0, int n_p, int cap
     const int nl = n_live;
     if (nl >= n_p) {  // the first nearest centroid (list order)
       if (tid < nl) {
-        const float* c = l1s + (size_t)sslot[order[tid]] * dp;
+        const float* c = l1s + (size_t)sslot[order[tid]] * ls;
         dist_s[tid] = ref_dist<METRIC>(c, vs, d, METRIC == COSINE ? seq_norm(vs, d) : 0.f);
       }
       __syncthreads();
@@ -341,7 +348,7 @@ __global__ void __launch_bounds__(256) l1_place_kernel(int nc0, int n_p, int cap
     }
     __syncthreads();
     const int t = s_tpos;
-    float* cs = l1s + (size_t)sslot[t] * dp;
+    float* cs = l1s + (size_t)sslot[t] * ls;
     if (s_add) {
       const int n1 = cnt[t] + 1;
       for (int j = tid; j < dp; j += blockDim.x) {
@@ -445,7 +452,7 @@ void launch_l1_place(int metric, int nc0, int n_p, int cap, int dp, int d, doubl
                      int32_t* cnt, const float* items, const int32_t* holder, const int32_t* dup, int m,
                      const float* qv, int32_t* out_t, uint8_t* out_added, uint8_t* out_merged, int32_t* out_q,
                      cudaStream_t st) {
-  const size_t sm = (size_t)(n_p + 1) * dp * 4;
+  const size_t sm = ((size_t)n_p * (dp + 4) + dp) * 4;
 #define AG_L1(M)                                                                                       \
   {                                                                                                  \
     ag_attr(l1_place_kernel<M>, sm);                                                                 \
