@@ -218,8 +218,24 @@ struct pk_index {
                         &uq, &cpool, &ccount, &qsw, &qhi, &qlo, &qin, &ncand, &nsurv})
         b->release();
     }
-  } scr[2];
+  } scr[3];
   int par = 0, last_par = 0;
+  // the last re-rank that read each scratch set (a front half reuses a set
+  // once it is done); three sets: a deferred re-rank of batch i may still read
+  // set i while the fronts of batches i+1 and i+2 fill theirs
+  cudaEvent_t ev_free[3] = {nullptr, nullptr, nullptr};
+  // PK_RERANK_DEFER (default 1): pipelined scans and fronts on higher-priority
+  // streams than the index stream's re-rank, so batch i's re-rank yields the
+  // SMs to batch i+1's scan and runs in its tail; fronts wait only for the
+  // re-rank of their own scratch set
+  bool rr_defer = true;
+  // PK_DEBUG_TIMELINE=1: timing events around each pipelined search's front
+  // half, scan and re-rank (no synchronisation; printed once after 48 searches)
+  struct Timeline {
+    bool on = false, printed = false;
+    int n = 0;
+    std::vector<cudaEvent_t> ev;  // [48][6]: front begin/end, scan begin/end, re-rank begin/end
+  } tl;
   // append staging (mapped), two buffers in turn: an append returns once its
   // scatter is enqueued; the buffer is rewritten only after the event of its
   // previous use (the call before last) has passed
@@ -964,6 +980,8 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   if (const char* e = getenv("PK_SCREEN")) ix->tensor = strcmp(e, "ffma") != 0;
   if (const char* e = getenv("PK_PIPELINE")) ix->pipeline = atoi(e) != 0;
   if (const char* e = getenv("PK_RERANK_LEAN")) ix->rr_lean = atoi(e) != 0 ? 1 : 0;
+  if (const char* e = getenv("PK_RERANK_DEFER")) ix->rr_defer = atoi(e) != 0;
+  ix->tl.on = getenv("PK_DEBUG_TIMELINE") != nullptr;
   ix->rr_lean_ctas = ix->num_sms;
   if (const char* e = getenv("PK_RERANK_LEAN_CTAS")) ix->rr_lean_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("PK_QGATHER")) ix->qgather = atoi(e) != 0;
@@ -1053,7 +1071,7 @@ int pk_index_destroy(pk_index* ix) {
   }
   for (cudaEvent_t e : {ix->ev_ag0, ix->ev_ag1})
     if (e) cudaEventDestroy(e);
-  for (cudaEvent_t e : {ix->ev_front, ix->ev_scan, ix->ev_sdone})
+  for (cudaEvent_t e : {ix->ev_front, ix->ev_scan, ix->ev_sdone, ix->ev_free[0], ix->ev_free[1], ix->ev_free[2]})
     if (e) cudaEventDestroy(e);
   for (uint8_t* p : ix->comb.opened) cudaIpcCloseMemHandle(p);
   if (ix->comb.area) cudaFree(ix->comb.area);
@@ -1708,8 +1726,9 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   CK(cudaSetDevice(ix->device));
   cudaStream_t st = ix->st;
   pk_index::Scratch& S = ix->scr[ix->par];
+  const int setno = ix->par;
   ix->last_par = ix->par;
-  ix->par ^= 1;
+  ix->par = (ix->par + 1) % 3;
   if (ix->tiered) {
     RET(ix->release_staged());
     RET(ix->poll_migrations());
@@ -1729,12 +1748,27 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                          ix->ev_scan && ix->mu.n == ix->ev_scan_n + 1;
   cudaStream_t fs = st;
   if (pipelined) {
-    if (!ix->fst) CK(cudaStreamCreateWithFlags(&ix->fst, cudaStreamNonBlocking));
+    if (!ix->fst) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      CK(cudaStreamCreateWithPriority(&ix->fst, cudaStreamNonBlocking, ix->rr_defer ? hi : lo));
+    }
     fs = ix->fst;
     CK(cudaStreamWaitEvent(fs, ix->ev_scan, 0));
+    if (ix->ev_free[setno]) CK(cudaStreamWaitEvent(fs, ix->ev_free[setno], 0));
     if (ix->front_wait) CK(cudaStreamWaitEvent(fs, ix->front_wait, 0));
   }
   ix->front_wait = nullptr;
+  const int tli = (pipelined && ix->tl.on && !ix->tl.printed && ix->tl.n < 48) ? ix->tl.n++ : -1;
+  auto tlrec = [&](int k, cudaStream_t s2) {
+    if (tli < 0) return;
+    if (ix->tl.ev.empty()) {
+      ix->tl.ev.resize(48 * 6);
+      for (auto& e : ix->tl.ev) cudaEventCreate(&e);
+    }
+    cudaEventRecord(ix->tl.ev[tli * 6 + k], s2);
+  };
+  tlrec(0, fs);
   // scratch
   const bool fresh_q = S.q.bytes < (size_t)B * dp * 4;
   RET(S.q.ensure((size_t)B * dp * 4));
@@ -1890,19 +1924,27 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // the previous scan -- NOT behind the previous batch's re-rank, which runs
   // on the index stream beside it (lean, co-resident CTAs)
   cudaStream_t ss = st;
+  tlrec(1, fs);
   if (pipelined) {
-    if (!ix->sst) CK(cudaStreamCreateWithFlags(&ix->sst, cudaStreamNonBlocking));
+    if (!ix->sst) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      CK(cudaStreamCreateWithPriority(&ix->sst, cudaStreamNonBlocking, ix->rr_defer ? hi : lo));
+    }
     ss = ix->sst;
     CK(cudaEventRecord(ix->ev_front, fs));
     CK(cudaStreamWaitEvent(ss, ix->ev_front, 0));
     CK(cudaStreamWaitEvent(ss, ix->ev_sdone, 0));
   }
-  // the index stream up to here (the previous batch's re-rank included):
-  // where the next search's front may start -- its scratch set was last read
-  // by that re-rank
-  CK(cudaEventRecord(ix->ev_scan, st));
+  // the index stream up to here: where the next search's front may start.
+  // Deferred re-ranks: a pipelined search leaves the point of the last
+  // non-pipelined one (nothing but searches touched the index since; the
+  // scratch sets are guarded by ev_free), so the next front does not wait
+  // for this batch's predecessor's re-rank
+  if (!(pipelined && ix->rr_defer)) CK(cudaEventRecord(ix->ev_scan, st));
   ix->ev_scan_n = ix->mu.n;
   // 3. fused scan + per-(query, list chunk) top-kk
+  tlrec(2, ss);
   PROF(4);
   if (ix->screen) {
     RET(S.cpool.ensure((size_t)B * pool_cap * sizeof(int4)));  // uq / ccount reset by prep
@@ -1938,8 +1980,10 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                 S.qpairs.as<QPair>(), kk, work_ctr, S.cand_key.as<uint32_t>(),
                 S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(),
                 ix->num_sms, st);
+  tlrec(3, ss);
   CK(cudaEventRecord(ix->ev_sdone, ss));
   if (pipelined) CK(cudaStreamWaitEvent(st, ix->ev_sdone, 0));
+  tlrec(4, st);
   PROF(5);
   // 4. merge per query
   int64_t* o_ids = out_ids;
@@ -1977,6 +2021,23 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     launch_merge((int)B, S.slot_off.as<int32_t>(), S.cand_key.as<uint32_t>(),
                  S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(), kk,
                  lt2, o_ids, o_d, o_cid, o_n, st);
+  tlrec(5, st);
+  if (tli == 47) {  // print the timeline of searches 8..47 relative to the first scan's end
+    cudaDeviceSynchronize();
+    ix->tl.printed = true;
+    auto at = [&](int i, int k) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ix->tl.ev[8 * 6 + 3], ix->tl.ev[i * 6 + k]);
+      return 1e3 * ms;
+    };
+    fprintf(stderr, "timeline (us from search 8's scan end): search: front[begin end] scan[begin end] rerank[begin end]\n");
+    for (int i = 9; i < 48; i++)
+      fprintf(stderr, "  %2d: front[%8.1f %8.1f] scan[%8.1f %8.1f] rerank[%8.1f %8.1f]\n", i, at(i, 0), at(i, 1),
+              at(i, 2), at(i, 3), at(i, 4), at(i, 5));
+  }
+  // this scratch set is free again once the re-rank has read it
+  if (!ix->ev_free[setno]) CK(cudaEventCreateWithFlags(&ix->ev_free[setno], cudaEventDisableTiming));
+  CK(cudaEventRecord(ix->ev_free[setno], st));
   CK(cudaGetLastError());
   if (!dev) {
     const int64_t nkk = B * kk;

@@ -1946,13 +1946,15 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   static const bool dbg_times = getenv("PK_DEBUG_SCAN_TIMES") != nullptr;
   unsigned long long* dbg_t = nullptr;
   if (dbg_times) cudaMallocAsync((void**)&dbg_t, (size_t)grid * 24, st);
-  // The first E = 32 CTAs stop claiming items once 70% of them are taken
+  // The first E = 32 CTAs stop claiming items once 50% of them are taken
   // (PK_SCAN_EARLY="E:F" overrides, "0:1" turns it off): the scan itself ends
-  // ~6 us later, but those SMs start the next batch's front half that much
-  // sooner (applied only to overlapped searches, where that front half exists) -- measured step 500.7 -> 488 us (swept E in
-  // 16-64, F in 0.5-0.95 on one box).
+  // a few us later, but those SMs run the next batch's front half beside it,
+  // so the next scan starts ~2.5 us after this one ends (applied only to
+  // overlapped searches, where that front half exists).  Swept E in 16-96,
+  // F in 0.2-0.8 on two boxes: 32:0.5 beats 32:0.7 by ~1.3% on configs[1];
+  // E >= 64 loses the scan more than it gains.
   static int early_ctas = 32;
-  static float early_frac = 0.7f;
+  static float early_frac = 0.5f;
   static bool early_read = false;
   if (!early_read) {
     if (const char* e = getenv("PK_SCAN_EARLY")) sscanf(e, "%d:%f", &early_ctas, &early_frac);
@@ -3170,7 +3172,8 @@ static int pick_cap(int nprobe) {
 static int pick_stage_floats(int dp, int nslots, int nprobe) {
   const size_t fixed = pick_cap(nprobe) * sizeof(Entry) + (size_t)dp * 4 +
                        (nslots <= PICK_SMEM_SLOTS ? (size_t)nslots * 8 : 0);
-  const size_t want = 110 * 1024;
+  // PK_PICK_SMEM_KB: the per-CTA budget (110: two CTAs per SM, ~72: three)
+  static const size_t want = (getenv("PK_PICK_SMEM_KB") ? (size_t)atoi(getenv("PK_PICK_SMEM_KB")) : 110) * 1024;
   const size_t minf = 2 * PICK_THREADS * (DC + 4);
   size_t f = fixed < want ? (want - fixed) / 4 : 0;
   return (int)std::max(f, minf);
