@@ -68,6 +68,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "search QPS at recall@10 (=CPU ref) + scan HBM GB/s, 1/2/4/8 B200"
 UNIT = "queries/s"
+E2E_DEPTH = int(os.environ.get("PK_BENCH_E2E_DEPTH", "4"))  # host batches in flight on the e2e path (<= 4 slots)
 
 CONFIGS = {
     0: dict(n=100_000, d=384, nlist=256, nprobe=16, k=10, batch=32),
@@ -618,9 +619,11 @@ def run_ours(a):
         Qpin = torch.from_numpy(Qall_h).pin_memory().numpy().reshape(a.warmup + a.steps, a.batch, a.d)
 
         def host_run(first, count):
-            """count host batches: N=1 pipelines two in flight (submit batch
-            s+1, then collect batch s: its H2D and the host work overlap the
-            device pass of batch s); N>1 runs the sharded host path."""
+            """count host batches: N=1 keeps E2E_DEPTH in flight (submit
+            batch s+3, then collect batch s: the H2D and host work of the next
+            batches overlap the device pass, and the next batch's front half
+            is queued before the current scan ends); N>1 runs the sharded
+            host path."""
             if weak:
                 for s in range(first, first + count):
                     sh.search_dispatch(Qpin[s], [0], a.nprobe, kk)
@@ -629,13 +632,13 @@ def run_ours(a):
                 for s in range(first, first + count):
                     sh.search(Qpin[s], [0], a.nprobe, kk)
                 return
-            prev = None
+            inflight = []
             for s in range(first, first + count):
-                t = ix.search_submit(Qpin[s], [0], a.nprobe, kk)
-                if prev is not None:
-                    ix.search_collect(prev)
-                prev = t
-            ix.search_collect(prev)
+                inflight.append(ix.search_submit(Qpin[s], [0], a.nprobe, kk))
+                if len(inflight) == E2E_DEPTH:
+                    ix.search_collect(inflight.pop(0))
+            for t in inflight:
+                ix.search_collect(t)
 
         host_run(0, min(a.warmup, 3))
         if dist:
@@ -643,8 +646,9 @@ def run_ours(a):
         t0 = time.perf_counter()
         host_run(a.warmup, a.steps)
         e2e_s = gather_max(dist, dev, time.perf_counter() - t0)
-        path = ("DeviceIndex.search_submit / search_collect (pk_search_submit / pk_search_collect "
-                "C-ABI, two batches in flight: batch s+1 submitted before batch s is collected)"
+        path = (f"DeviceIndex.search_submit / search_collect (pk_search_submit / pk_search_collect "
+                f"C-ABI, {E2E_DEPTH} batches in flight: batch s+{E2E_DEPTH - 1} submitted before batch s is "
+                "collected)"
                 if sh is None else
                 "ShardedIndex.search_dispatch (pk_search_coarse / NCCL / pk_search_probed / "
                 "pk_merge_shards)" if weak else

@@ -211,12 +211,15 @@ int pk_list_add_remote(pk_index* ix, int64_t cid, int32_t scope_code, const floa
  * padded to 16 bytes.  pk_search (PK_DEVICE_PTRS) writes one straight into
  * these offsets. */
 int64_t pk_shard_block_bytes(int64_t B, int32_t kk);
-/* Asynchronous host-pointer search in two slots: pk_search_submit copies Q
- * (host, pinned for best overlap) on a copy stream and queues the device pass;
- * pk_search_collect(slot) waits for that batch and fills the host outputs
- * (same meaning as pk_search's).  With both slots in use the H2D and the
- * caller's host work for batch i+1 overlap the device pass of batch i.
- * scope_codes are host pointers here. */
+/* Asynchronous host-pointer search in PK_ASYNC_SLOTS slots: pk_search_submit
+ * copies Q (host, pinned for best overlap) on a copy stream and queues the
+ * device pass; pk_search_collect(slot) waits for that batch and fills the host
+ * outputs (same meaning as pk_search's).  With several slots in use the H2D
+ * and the caller's host work for the next batches overlap the device pass of
+ * the one in flight (small batches need three in flight: the next batch's
+ * front half runs beside the current scan).  A slot is reused only after it
+ * was collected.  scope_codes are host pointers here. */
+#define PK_ASYNC_SLOTS 4
 int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
                      const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk);
 int pk_search_collect(pk_index* ix, int32_t slot, int64_t* out_ids, float* out_dists, int64_t* out_cids,

@@ -23,6 +23,7 @@ PK_ERR_USAGE = 1
 PK_ERR_DEVICE = 2
 PK_ERR_NOMEM = 3
 PK_DEVICE_PTRS = 1
+PK_ASYNC_SLOTS = 4  # include/pancake_b200.h
 KKMAX = 64
 NPROBE_MAX = 2048
 

@@ -284,9 +284,9 @@ struct pk_index {
   uint8_t* hout = nullptr;  // pinned staging of the host path's packed results
   size_t hout_bytes = 0;
 
-  // ---- asynchronous host-pointer searches (pk_search_submit / collect): two
-  // slots, so the H2D of batch i+1 (copy stream) and the caller's host work
-  // overlap the device pass of batch i
+  // ---- asynchronous host-pointer searches (pk_search_submit / collect):
+  // PK_ASYNC_SLOTS slots, so the H2D of the next batches (copy stream) and the
+  // caller's host work overlap the device pass of the batch in flight
   struct AsyncSlot {
     DevBuf qin, blk;
     uint8_t* hblk = nullptr;  // pinned result block
@@ -295,7 +295,7 @@ struct pk_index {
     int64_t B = 0;
     int32_t kk = 0;
     bool busy = false;
-  } aslot[2];
+  } aslot[PK_ASYNC_SLOTS];
   cudaStream_t cst = nullptr;  // copy stream (query uploads)
   cudaStream_t rst = nullptr;  // result read-back stream (off the index stream's critical path)
 
@@ -2094,7 +2094,7 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
 int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
                      const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk) {
   std::lock_guard<CountedMutex> lock_(ix->mu);
-  if (slot < 0 || slot > 1) return fail(PK_ERR_USAGE, "slot must be 0 or 1");
+  if (slot < 0 || slot >= PK_ASYNC_SLOTS) return fail(PK_ERR_USAGE, "slot must lie in [0, %d)", PK_ASYNC_SLOTS);
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
   auto& a = ix->aslot[slot];
   if (a.busy) return fail(PK_ERR_USAGE, "slot %d has an uncollected search", slot);
@@ -2147,7 +2147,7 @@ int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
 
 int pk_search_collect(pk_index* ix, int32_t slot, int64_t* out_ids, float* out_dists, int64_t* out_cids,
                       int32_t* out_n, int64_t* out_scanned) {
-  if (slot < 0 || slot > 1) return fail(PK_ERR_USAGE, "slot must be 0 or 1");
+  if (slot < 0 || slot >= PK_ASYNC_SLOTS) return fail(PK_ERR_USAGE, "slot must lie in [0, %d)", PK_ASYNC_SLOTS);
   auto& a = ix->aslot[slot];
   if (!a.busy) return fail(PK_ERR_USAGE, "slot %d has no search in flight", slot);
   CK(cudaEventSynchronize(a.done));  // outside the index lock: the other slot may submit meanwhile

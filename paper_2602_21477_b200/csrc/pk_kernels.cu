@@ -1687,6 +1687,15 @@ struct TcLayout {
 };
 size_t tc_smem_bytes() { return TcLayout::TOTAL + 1024; }
 
+// Items taken before the early CTAs stop claiming: a fraction of the queue,
+// or none at all when the queue is short (fewer than early_small items per
+// CTA): such a scan is latency-bound, and the next front half (one pick CTA
+// per query) is the pipeline's critical path -- it gets those SMs from the
+// start (configs[0]: step 49.6 -> 40.0 us).
+__device__ __forceinline__ int early_at_of(int n_items, float early_frac, int early_small) {
+  return n_items < early_small * (int)gridDim.x ? 0 : (int)(early_frac * (float)n_items);
+}
+
 template <int METRIC>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     scan_tc_kernel(const __grid_constant__ ArenaMaps maps, const __grid_constant__ CUtensorMap qgmap,
@@ -1697,7 +1706,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    int32_t* __restrict__ work_ctr, uint32_t* __restrict__ Uq,
                    uint32_t* __restrict__ slot_hi, int32_t* __restrict__ slot_n,
                    int4* __restrict__ cpool, int32_t* __restrict__ ccount, int cap, int dbg_skip,
-                   unsigned long long* __restrict__ dbg_t, int early_ctas, float early_frac) {
+                   unsigned long long* __restrict__ dbg_t, int early_ctas, float early_frac,
+                   int early_small) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   ScanShared S;
@@ -1764,7 +1774,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------------------------------------------------- producer
     scan_producer<TC_STAGES>(S, maps, lt, Qsw, items, n_items_p, qpairs, work_ctr, nchunk_d, false,
                              qsw_stride, use_qg ? &qgmap : nullptr, early_ctas,
-                             (int)(early_frac * (float)(n_items_p[0] + n_items_p[2])));
+                             early_at_of(n_items_p[0] + n_items_p[2], early_frac, early_small));
   } else if (warp == TC_EPI_WARPS + 1) {
     // ---------------------------------------------------------- MMA issuer
     const uint32_t idesc = umma_idesc_tf32(128, QG);
@@ -1955,9 +1965,10 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   // E >= 64 loses the scan more than it gains.
   static int early_ctas = 32;
   static float early_frac = 0.5f;
+  static int early_small = 4;  // "E:F:T": T items per CTA, below which F = 0
   static bool early_read = false;
   if (!early_read) {
-    if (const char* e = getenv("PK_SCAN_EARLY")) sscanf(e, "%d:%f", &early_ctas, &early_frac);
+    if (const char* e = getenv("PK_SCAN_EARLY")) sscanf(e, "%d:%f:%d", &early_ctas, &early_frac, &early_small);
     early_read = true;
   }
 #define PK_TC(M)                                                                                 \
@@ -1967,7 +1978,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
     launch_maybe_pdl(pdl, k, dim3(grid), dim3(TC_THREADS), smem, st, maps, qgm, use_qg, lt, (const float*)qsw, \
                (int64_t)B, \
                qnorm2, items, n_items, qpairs, kk, coef, work_ctr, Uq, slot_hi, slot_n, cpool,      \
-               ccount, cap, dbg_skip, dbg_t, overlapped ? early_ctas : 0, early_frac);            \
+               ccount, cap, dbg_skip, dbg_t, overlapped ? early_ctas : 0, early_frac, early_small);            \
   }
   if (metric == SQ_L2) PK_TC(SQ_L2)
   else PK_TC(IP)

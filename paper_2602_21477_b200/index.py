@@ -216,13 +216,14 @@ class DeviceIndex:
         return SearchOutput(ids, dd, cids, cnt, probe, scanned)
 
     def search_submit(self, Q, scope_codes, nprobe: int, kk: int):
-        """Asynchronous search of a host batch (two slots in flight); returns
-        a ticket for search_collect.  Keep Q alive (ideally pinned) until
-        collected."""
+        """Asynchronous search of a host batch (up to N.PK_ASYNC_SLOTS in
+        flight, slots used round-robin: collect a ticket before submitting
+        that many more); returns a ticket for search_collect.  Keep Q alive
+        (ideally pinned) until collected."""
         self.flush()
         Q = N.f32(Q, self.dimension)
         slot = self._next_slot
-        self._next_slot ^= 1
+        self._next_slot = (slot + 1) % N.PK_ASYNC_SLOTS
         codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
         N.check(N.lib().pk_search_submit(self._h, slot, N.ptr(Q), Q.shape[0], N.ptr(codes), len(codes),
                                          int(nprobe), int(kk)))

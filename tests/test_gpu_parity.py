@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from paper_2602_21477_b200.core import UsageError
 from replay import compare_records, gen, load_golden, replay_store
 
 pytestmark = pytest.mark.gpu
@@ -429,26 +430,33 @@ def test_concurrent_searches_equal_serial(pk):
     store.close()
 
 
-def test_async_submit_collect_equals_search(pk):
-    """pk_search_submit / pk_search_collect (two slots in flight) return
-    exactly pk_search's answers, in submission order."""
+@pytest.mark.parametrize("depth", [1, 2, 3, 4])
+def test_async_submit_collect_equals_search(pk, depth):
+    """pk_search_submit / pk_search_collect (depth slots in flight, up to
+    PK_ASYNC_SLOTS) return exactly pk_search's answers, in submission order;
+    a slot still in flight refuses a new batch."""
     rng = np.random.default_rng(8)
     d, nlist = 96, 30
     sizes = rng.integers(1, 600, nlist)
     ix, lists, cents, cids = _random_index(pk, rng, d, nlist, sizes)
-    batches = [rng.normal(size=(int(rng.integers(1, 90)), d)).astype(np.float32) for _ in range(7)]
+    batches = [rng.normal(size=(int(rng.integers(1, 90)), d)).astype(np.float32) for _ in range(9)]
     want = [ix.search(Q, [0], 6, 12) for Q in batches]
-    got, prev = [], None
+    got, inflight = [], []
     for Q in batches:
-        t = ix.search_submit(Q, [0], 6, 12)
-        if prev is not None:
-            got.append(ix.search_collect(prev))
-        prev = t
-    got.append(ix.search_collect(prev))
+        inflight.append(ix.search_submit(Q, [0], 6, 12))
+        if len(inflight) == depth:
+            got.append(ix.search_collect(inflight.pop(0)))
+    got += [ix.search_collect(t) for t in inflight]
     for w, g in zip(want, got):
         assert np.array_equal(w.ids, g.ids) and np.array_equal(w.counts, g.counts)
         assert np.array_equal(bits(w.dists), bits(g.dists)) and np.array_equal(w.cids, g.cids)
         assert np.array_equal(w.scanned, g.scanned)
+    if depth == 4:  # all slots busy: the next submit is a usage error
+        ts = [ix.search_submit(batches[0], [0], 6, 12) for _ in range(4)]
+        with pytest.raises(UsageError):
+            ix.search_submit(batches[0], [0], 6, 12)
+        for t in ts:
+            ix.search_collect(t)
     ix.close()
 
 
