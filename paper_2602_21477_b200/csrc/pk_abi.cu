@@ -260,6 +260,14 @@ struct pk_index {
   // ... and the scan of a pipelined search runs on sst, so this batch's
   // re-rank (index stream, after ev_sdone) runs beside the NEXT batch's scan
   cudaStream_t sst = nullptr;
+  // Consecutive pipelined scans alternate between sst and sst2 and do not
+  // wait for each other (they share no scratch: three sets, no tier), so scan
+  // i+1's CTAs take the SMs scan i's CTAs leave -- its tail -- instead of
+  // starting after the last one exits (configs[1] 538K -> 566K QPS,
+  // configs[0] 783K -> 894K).  PK_SCAN_OVERLAP=0 serialises.
+  bool scan_ovl = true;
+  int sturn = 0;
+  cudaStream_t sst2 = nullptr;
   cudaEvent_t ev_front = nullptr, ev_scan = nullptr, front_wait = nullptr, ev_sdone = nullptr;
   // lean re-rank beside the next scan: -1 = for batches up to 64 queries
   // (configs[0]: +1%; at 256 queries it lengthened the step),
@@ -982,6 +990,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
   if (const char* e = getenv("PK_RERANK_LEAN")) ix->rr_lean = atoi(e) != 0 ? 1 : 0;
   if (const char* e = getenv("PK_RERANK_DEFER")) ix->rr_defer = atoi(e) != 0;
   ix->tl.on = getenv("PK_DEBUG_TIMELINE") != nullptr;
+  if (const char* e = getenv("PK_SCAN_OVERLAP")) ix->scan_ovl = atoi(e) != 0;
   ix->rr_lean_ctas = ix->num_sms;
   if (const char* e = getenv("PK_RERANK_LEAN_CTAS")) ix->rr_lean_ctas = std::max(1, atoi(e));
   if (const char* e = getenv("PK_QGATHER")) ix->qgather = atoi(e) != 0;
@@ -1011,7 +1020,7 @@ int pk_index_create(int64_t dim, int metric, int device, int64_t reserve_rows,
 int pk_index_destroy(pk_index* ix) {
   if (!ix) return PK_OK;
   cudaSetDevice(ix->device);
-  for (cudaStream_t x : {ix->fst, ix->sst, ix->rst, ix->cst, ix->st})
+  for (cudaStream_t x : {ix->fst, ix->sst, ix->sst2, ix->rst, ix->cst, ix->st})
     if (x) cudaStreamSynchronize(x);
   cudaFree(ix->rows);
   cudaFree(ix->ids);
@@ -1061,10 +1070,11 @@ int pk_index_destroy(pk_index* ix) {
     cudaStreamSynchronize(ix->fst);
     cudaStreamDestroy(ix->fst);
   }
-  if (ix->sst) {
-    cudaStreamSynchronize(ix->sst);
-    cudaStreamDestroy(ix->sst);
-  }
+  for (cudaStream_t x : {ix->sst, ix->sst2})
+    if (x) {
+      cudaStreamSynchronize(x);
+      cudaStreamDestroy(x);
+    }
   if (ix->ast) {
     cudaStreamSynchronize(ix->ast);
     cudaStreamDestroy(ix->ast);
@@ -1930,11 +1940,16 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
       int lo = 0, hi = 0;
       cudaDeviceGetStreamPriorityRange(&lo, &hi);
       CK(cudaStreamCreateWithPriority(&ix->sst, cudaStreamNonBlocking, ix->rr_defer ? hi : lo));
+      CK(cudaStreamCreateWithPriority(&ix->sst2, cudaStreamNonBlocking, ix->rr_defer ? hi : lo));
     }
     ss = ix->sst;
+    if (ix->scan_ovl) {
+      ss = ix->sturn ? ix->sst2 : ix->sst;
+      ix->sturn ^= 1;
+    }
     CK(cudaEventRecord(ix->ev_front, fs));
     CK(cudaStreamWaitEvent(ss, ix->ev_front, 0));
-    CK(cudaStreamWaitEvent(ss, ix->ev_sdone, 0));
+    if (!ix->scan_ovl) CK(cudaStreamWaitEvent(ss, ix->ev_sdone, 0));
   }
   // the index stream up to here: where the next search's front may start.
   // Deferred re-ranks: a pipelined search leaves the point of the last

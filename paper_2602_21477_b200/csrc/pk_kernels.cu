@@ -1964,7 +1964,7 @@ void launch_scan_tc(int metric, ListTable lt, const ArenaMaps& maps, const float
   // F in 0.2-0.8 on two boxes: 32:0.5 beats 32:0.7 by ~1.3% on configs[1];
   // E >= 64 loses the scan more than it gains.
   static int early_ctas = 32;
-  static float early_frac = 0.5f;
+  static float early_frac = 0.3f;
   static int early_small = 4;  // "E:F:T": T items per CTA, below which F = 0
   static bool early_read = false;
   if (!early_read) {

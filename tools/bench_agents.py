@@ -247,6 +247,19 @@ def main():
                       "_topk", "end_request", "_tick", "_state_key_for"):
                 wrap(store, m, "store." + m)
             wrap(store.graph, "upload", "graph.upload")
+            if os.environ.get("PK_TIME_CALLS") == "2":  # finer: the host policy's pieces (class level)
+                from paper_2602_21477_b200 import cache as _c, fsm as _f, engine as _e
+                for m in ("read_plan", "replay", "promote_and_capture", "_l1_decide", "_l1_place",
+                          "_l1_capture", "threshold", "l1_listing_slots", "promote_to_l0"):
+                    if hasattr(_c.MultiLevelCache, m):
+                        wrap(_c.MultiLevelCache, m, "cache." + m)
+                for m in ("match_and_predict", "match", "state_slots", "observe_completed"):
+                    if hasattr(_f.PatternTable, m):
+                        wrap(_f.PatternTable, m, "fsm." + m)
+                for m in ("_hint_from", "_seq_D", "_cache_items", "_append_sequence", "_coarse_plan", "prefetch",
+                          "_materialize"):
+                    wrap(store, m, "store." + m)
+                wrap(_e, "profile_order", "engine.profile_order")
             wrap(store.clusters, "create_cluster", "clusters.create_cluster")
         prof = None
         if os.environ.get("PK_PROFILE_OPS"):
