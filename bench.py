@@ -633,14 +633,24 @@ def run_ours(a):
                     sh.search(Qpin[s], [0], a.nprobe, kk)
                 return
             inflight = []
+            ht = os.environ.get("PK_BENCH_HOST_TIMES")  # host seconds inside submit / collect
+            tsub = tcol = 0.0
             for s in range(first, first + count):
+                t0_ = time.perf_counter()
                 inflight.append(ix.search_submit(Qpin[s], [0], a.nprobe, kk))
+                t1_ = time.perf_counter()
+                tsub += t1_ - t0_
                 if len(inflight) == E2E_DEPTH:
                     ix.search_collect(inflight.pop(0))
+                    tcol += time.perf_counter() - t1_
             for t in inflight:
                 ix.search_collect(t)
+            if ht and count > 10:
+                print(f"e2e host us/batch: submit {1e6 * tsub / count:.1f} collect {1e6 * tcol / count:.1f}",
+                      file=sys.stderr)
 
-        host_run(0, min(a.warmup, 3))
+        # every async slot touched (its buffers allocated) before the timed region
+        host_run(0, min(a.warmup + a.steps, max(a.warmup, 2 * E2E_DEPTH)))
         if dist:
             dist.barrier()
         t0 = time.perf_counter()

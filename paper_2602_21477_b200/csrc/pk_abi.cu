@@ -2106,8 +2106,25 @@ int pk_search(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_code
                      out_n, out_probe, out_scanned, dev, dev, nullptr, nullptr);
 }
 
+static int search_submit_impl(pk_index* ix, int32_t slot, const float* Q, int64_t B,
+                              const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk);
+
 int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
                      const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk) {
+  // PK_DEBUG_SUBMIT=1: host microseconds inside this call, printed every 2000
+  static const bool dbg = getenv("PK_DEBUG_SUBMIT") != nullptr;
+  if (!dbg) return search_submit_impl(ix, slot, Q, B, scope_codes, nscopes, nprobe, kk);
+  static double acc = 0;
+  static long calls = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  const int rc = search_submit_impl(ix, slot, Q, B, scope_codes, nscopes, nprobe, kk);
+  acc += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  if (++calls % 2000 == 0) fprintf(stderr, "pk_search_submit host us/call: %.1f\n", acc / calls);
+  return rc;
+}
+
+static int search_submit_impl(pk_index* ix, int32_t slot, const float* Q, int64_t B,
+                              const int32_t* scope_codes, int32_t nscopes, int32_t nprobe, int32_t kk) {
   std::lock_guard<CountedMutex> lock_(ix->mu);
   if (slot < 0 || slot >= PK_ASYNC_SLOTS) return fail(PK_ERR_USAGE, "slot must lie in [0, %d)", PK_ASYNC_SLOTS);
   if (kk < 1 || kk > KKMAX) return fail(PK_ERR_USAGE, "kk must lie in [1, %d]", KKMAX);
