@@ -208,6 +208,10 @@ struct pk_index {
     CUtensorMap qmap[2];
     const void* qmap_ptr[2] = {nullptr, nullptr};
     int64_t qmap_rows = -1;
+    // host scope codes last uploaded into `scopes` (-1: unknown / device
+    // codes): an unchanged set skips the pageable copy
+    int32_t scopes_h[64];
+    int32_t nscopes_h = -1;
     // the scan's gather4 map over the padded query batch
     CUtensorMap qgmap;
     const void* qg_ptr = nullptr;
@@ -1718,6 +1722,12 @@ static int graph_coarse(pk_index* ix, pk_index::Scratch& S, int64_t B, const int
   return PK_OK;
 }
 
+// PK_DEBUG_SUBMIT=2: host microseconds per search_core phase (accumulated;
+// printed by pk_search_submit): setup, front launches, scan, re-rank, tail
+static double g_hphase[6];
+static long g_hcalls;
+static bool g_hdbg = getenv("PK_DEBUG_SUBMIT") && atoi(getenv("PK_DEBUG_SUBMIT")) >= 2;
+
 static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes,
                        int32_t nscopes, int32_t nprobe, int32_t kk, int64_t* out_ids,
                        float* out_dists, int64_t* out_cids, int32_t* out_n, int64_t* out_probe,
@@ -1734,6 +1744,14 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
     return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
   if (B == 0) return PK_OK;
   CK(cudaSetDevice(ix->device));
+  auto hp_t = std::chrono::steady_clock::now();
+  auto hmark = [&](int k) {
+    if (!g_hdbg) return;
+    const auto t = std::chrono::steady_clock::now();
+    g_hphase[k] += std::chrono::duration<double, std::micro>(t - hp_t).count();
+    hp_t = t;
+  };
+  if (g_hdbg) g_hcalls++;
   cudaStream_t st = ix->st;
   pk_index::Scratch& S = ix->scr[ix->par];
   const int setno = ix->par;
@@ -1825,10 +1843,17 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                                        (int)std::min<int64_t>({(int64_t)kk * 512, 1 << 16,
                                                                ((int64_t)1 << 30) / (std::max<int64_t>(B, 1) * 16)}));
   RouteArgs ra;  // set when the coarse pick emits the routes itself
+  hmark(0);
   PROF(0);
-  if (!probe_in)
-    CK(cudaMemcpyAsync(S.scopes.p, scope_codes, nscopes * 4,
-                       (in_dev && !host_scopes) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
+  if (!probe_in) {
+    const bool dev_codes = in_dev && !host_scopes;
+    if (dev_codes || S.nscopes_h != nscopes || memcmp(S.scopes_h, scope_codes, (size_t)nscopes * 4) != 0) {
+      CK(cudaMemcpyAsync(S.scopes.p, scope_codes, nscopes * 4,
+                         dev_codes ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, fs));
+      S.nscopes_h = dev_codes ? -1 : nscopes;
+      if (!dev_codes) memcpy(S.scopes_h, scope_codes, (size_t)nscopes * 4);
+    }
+  }
   const ListTable lt = ix->table();
   if (prep) {
     const float* qin = Q;
@@ -1935,6 +1960,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   // on the index stream beside it (lean, co-resident CTAs)
   cudaStream_t ss = st;
   tlrec(1, fs);
+  hmark(1);
   if (pipelined) {
     if (!ix->sst) {
       int lo = 0, hi = 0;
@@ -1999,6 +2025,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
   CK(cudaEventRecord(ix->ev_sdone, ss));
   if (pipelined) CK(cudaStreamWaitEvent(st, ix->ev_sdone, 0));
   tlrec(4, st);
+  hmark(2);
   PROF(5);
   // 4. merge per query
   int64_t* o_ids = out_ids;
@@ -2037,6 +2064,7 @@ static int search_core(pk_index* ix, const float* Q, int64_t B, const int32_t* s
                  S.cand_id.as<int64_t>(), S.cand_n.as<int32_t>(), S.cand_list.as<int32_t>(), kk,
                  lt2, o_ids, o_d, o_cid, o_n, st);
   tlrec(5, st);
+  hmark(3);
   if (tli == 47) {  // print the timeline of searches 8..47 relative to the first scan's end
     cudaDeviceSynchronize();
     ix->tl.printed = true;
@@ -2119,7 +2147,12 @@ int pk_search_submit(pk_index* ix, int32_t slot, const float* Q, int64_t B,
   const auto t0 = std::chrono::steady_clock::now();
   const int rc = search_submit_impl(ix, slot, Q, B, scope_codes, nscopes, nprobe, kk);
   acc += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-  if (++calls % 2000 == 0) fprintf(stderr, "pk_search_submit host us/call: %.1f\n", acc / calls);
+  if (++calls % 2000 == 0) {
+    fprintf(stderr, "pk_search_submit host us/call: %.1f\n", acc / calls);
+    if (g_hcalls)
+      fprintf(stderr, "  search_core us/call: setup %.1f front %.1f scan %.1f rerank %.1f\n",
+              g_hphase[0] / g_hcalls, g_hphase[1] / g_hcalls, g_hphase[2] / g_hcalls, g_hphase[3] / g_hcalls);
+  }
   return rc;
 }
 

@@ -9,7 +9,7 @@ nvidia-smi -L > gpurun_out/host.txt; nproc >> gpurun_out/host.txt; free -g >> gp
 # configs[1] (the headline), its reference arm, configs[0], configs[3] on one GPU
 timeout 600 python bench.py --steps 50 > gpurun_out/r02_${V}_c1_bench.json 2> gpurun_out/c1.err; echo "c1 rc=$?"
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/r02_${V}_c1_bench_ref.json 2> gpurun_out/c1r.err; echo "c1 ref rc=$?"
-timeout 600 python bench.py --config 0 --steps 400 > gpurun_out/r02_${V}_c0_bench.json 2> gpurun_out/c0.err; echo "c0 rc=$?"
+timeout 600 python bench.py --config 0 --steps 2000 > gpurun_out/r02_${V}_c0_bench.json 2> gpurun_out/c0.err; echo "c0 rc=$?"
 timeout 600 python bench.py --config 0 --impl reference --steps 5 --warmup 3 > gpurun_out/r02_${V}_c0_bench_ref.json 2> gpurun_out/c0r.err; echo "c0 ref rc=$?"
 timeout 900 python bench.py --config 3 --steps 20 > gpurun_out/r02_${V}_c3_1gpu_bench.json 2> gpurun_out/c3.err; echo "c3 rc=$?"
 # configs[2]: agents, with the reference Store on the same stream
