@@ -122,19 +122,35 @@ class TierManager:
             return []
         clusters = self.store.clusters
         self._hot &= set(clusters)  # retired clusters left with their device copies
-        live = [cid for cid in clusters if clusters[cid].size > 0]
-        freq = {c: self.decayed_freq(c) for c in live}  # one evaluation per cluster
-        ranked = sorted(live, key=lambda c: (-freq[c], c))
+        live = [cid for cid, cl in clusters.items() if cl.size > 0]
+        # decayed_freq per cluster, the same float expression in the same
+        # order (one evaluation each); ranking (-freq, cid) by one lexsort
+        clock, hl, get = self.clock, self.decay_half_life, self.freq.get
+        fl = []
+        for c in live:
+            value, last = get(c, (0.0, clock))
+            fl.append(value * (0.5 ** ((clock - last) / hl)))
+        freq = dict(zip(live, fl))
         actions: list[tuple[str, int]] = []
         target: list[int] = []
-        used = 0
-        for cid in ranked:
-            nb = clusters[cid].nbytes
-            if nb == 0 or freq[cid] <= 0.0:
-                continue
-            if used + nb <= self.budget_bytes:
-                target.append(cid)
-                used += nb
+        if live:
+            cid_a = np.fromiter(live, dtype=np.int64, count=len(live))
+            f_a = np.fromiter(fl, dtype=np.float64, count=len(live))
+            nb_a = np.fromiter((clusters[c].nbytes for c in live), dtype=np.int64, count=len(live))
+            order = np.lexsort((cid_a, -f_a))
+            keep = order[(nb_a[order] > 0) & (f_a[order] > 0.0)]
+            # greedy under the budget in rank order: the whole prefix that
+            # fits at once, then the rest one by one (a later, smaller
+            # cluster may still fit)
+            cum = np.cumsum(nb_a[keep])
+            n_fit = int(np.searchsorted(cum, self.budget_bytes, side="right"))
+            target = cid_a[keep[:n_fit]].tolist()
+            used = int(cum[n_fit - 1]) if n_fit else 0
+            budget = self.budget_bytes
+            for cid, nb in zip(cid_a[keep[n_fit:]].tolist(), nb_a[keep[n_fit:]].tolist()):
+                if used + nb <= budget:
+                    target.append(cid)
+                    used += nb
         target_set = set(target)
         # the displacers (admitted now, not hot before) are the same for every
         # hot cluster examined below: retained clusters are already hot

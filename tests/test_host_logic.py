@@ -283,6 +283,37 @@ class TestHotsetPolicy:
         assert sum(st.clusters[c].nbytes for c in tier.hotset) <= tier.budget_bytes
         assert tier.hotset == {5, 4, 3}  # hottest first, greedy under the budget
 
+    def test_vectorised_update_equals_the_loop(self):
+        """hotset_update ranks and fills the budget with arrays; the target
+        set equals the reference loop's (sorted by (-freq, cid), greedy
+        under the budget, skipping empty / never-accessed clusters) over
+        random sizes, access streams, ties and budgets."""
+        rng = np.random.default_rng(5)
+        for trial in range(40):
+            n = int(rng.integers(1, 60))
+            budget = int(rng.integers(0, 8 * 4 * 40 * n // 3 + 2))
+            st, ix, tier = _tier(budget)
+            for g in range(n):
+                st.clusters[g] = _FakeCluster(g, int(rng.integers(0, 40)))
+            for _ in range(int(rng.integers(0, 4 * n))):
+                tier.record_access(int(rng.integers(0, n)))
+            if trial % 3 == 0:  # exact ties: same counts, same recency pattern
+                for g in range(n):
+                    tier.freq[g] = (1.0, tier.clock)
+            clusters = st.clusters
+            live = [c for c in clusters if clusters[c].size > 0]
+            freq = {c: tier.decayed_freq(c) for c in live}
+            want, used = set(), 0
+            for cid in sorted(live, key=lambda c: (-freq[c], c)):
+                nb = clusters[cid].nbytes
+                if nb == 0 or freq[cid] <= 0.0:
+                    continue
+                if used + nb <= budget:
+                    want.add(cid)
+                    used += nb
+            tier.hotset_update()
+            assert tier.hotset == want
+
     def test_hysteresis_and_eviction(self):
         st, ix, tier = _tier(8 * 4 * 10)  # room for one 10-vector cluster
         st.clusters[0] = _FakeCluster(0, 10)

@@ -150,7 +150,14 @@ def main():
     n_q = 0
     staged0 = store.tier.metrics()["tier_staged_bytes_total"]
     same = None
+    prof = None
+    if os.environ.get("PK_PROFILE_STREAM"):  # cProfile of the insert path (batches 2000..)
+        import cProfile
+
+        prof = cProfile.Profile()
     for b in range(nbatches):
+        if prof is not None and b == min(2000, nbatches // 2):
+            prof.enable()
         vecs = stream[b] if b < ref_batches else draw(8, 0.05)
         t = time.perf_counter()
         store.insert(None, "static", list(vecs))
@@ -170,6 +177,11 @@ def main():
             torch.cuda.synchronize(dev)
             t_srch += time.perf_counter() - t
             n_q += 256
+    if prof is not None:
+        import pstats
+
+        prof.disable()
+        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(30)
     m = store.tier.metrics()
     # parity: a query sample against the oracle over the final index
     from oracle import oracle as O
