@@ -1135,12 +1135,19 @@ class Store:
 
     # --- persistence / ingestion -------------------------------------------
     def snapshot(self, path):
-        raise NotImplementedError("snapshot/restore (ref/persist.py:136-380) is out of scope; "
-                                  "use export_ivf / load_external_ivf")
+        """ref/engine.py:811-812 -> ref/persist.py:136-241 (same file format)."""
+        from . import persist
+
+        self.index.flush()
+        persist.snapshot(self, path)
 
     @classmethod
-    def restore(cls, path):
-        raise NotImplementedError("snapshot/restore (ref/persist.py:136-380) is out of scope")
+    def restore(cls, path, **overrides) -> "Store":
+        """ref/engine.py:814-816 -> ref/persist.py:244-380; ``overrides`` sets
+        this package's own StoreConfig fields (``device``, ``sharded``)."""
+        from . import persist
+
+        return persist.restore(cls, path, **overrides)
 
     def export_ivf(self, path, scopes=None):
         """ref/persist.py:386-394."""
@@ -1208,3 +1215,27 @@ class Store:
                 if limit is not None and len(vecs) >= limit:
                     break
         return self.insert(None, scope, vecs)
+
+    def ingest_jsonl(self, path) -> int:
+        """ref/engine.py:828-839 over ref/persist.py:464-477's records
+        ({id?, vector, payload?, scope} per line), one insert each."""
+        import json
+
+        from .core import ParseError
+
+        count = 0
+        with open(path, "r", encoding="utf-8") as f:
+            for lineno, line in enumerate(f, 1):
+                line = line.strip()
+                if not line:
+                    continue
+                try:
+                    rec = json.loads(line)
+                except json.JSONDecodeError as e:
+                    raise ParseError(f"bad JSON on line {lineno}: {e.msg}", e.pos) from e
+                if "vector" not in rec or "scope" not in rec:
+                    raise ParseError(f"line {lineno} missing vector/scope", 0)
+                self.insert(None, rec["scope"], [rec["vector"]], [rec.get("payload", "")],
+                            ids=[rec["id"]] if "id" in rec else None)
+                count += 1
+        return count

@@ -41,8 +41,9 @@ def write_pnck(path, dimension: int, metric: Metric, clusters, sections=None):
             f.write(payload)
 
 
-def read_pnck(path):
-    """Returns (dimension, metric, [(centroid, ids i64, rows f32[n, d])])."""
+def read_pnck(path, with_sections: bool = False):
+    """Returns (dimension, metric, [(centroid, ids i64, rows f32[n, d])]), plus
+    {tag: payload} of the tagged sections when ``with_sections``."""
     with open(path, "rb") as f:
         buf = f.read()
     off = 0
@@ -74,11 +75,15 @@ def read_pnck(path):
         r = np.frombuffer(buf, dtype=rec, count=n, offset=off)
         off += n * rec.itemsize
         out.append((cent, r["id"].astype(np.int64), np.ascontiguousarray(r["v"], dtype=np.float32)))
-    # tagged sections: validated and skipped
+    # tagged sections: validated (and skipped by cluster importers)
+    sections = {}
     while off < len(buf):
         if off + 4 > len(buf):
             raise ParseError("truncated section tag", off)
+        tag = buf[off:off + 4]
         off += 4
         (length,) = struct.unpack("<Q", take(8, "section length"))
-        take(length, "section")
+        sections[tag] = take(length, f"section {tag!r}")
+    if with_sections:
+        return dimension, metric, out, sections
     return dimension, metric, out

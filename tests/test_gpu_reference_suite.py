@@ -40,12 +40,10 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
-SUITES = ("test_engine", "test_acceptance", "test_tiering")
+SUITES = ("test_engine", "test_acceptance", "test_tiering", "test_persist")
 
 # reference test -> why the drop-in differs (strict xfail)
-DEVIATIONS = {
-    "test_09_persistence_round_trips": "snapshot/restore (ref/persist.py:136-380) not built",
-}
+DEVIATIONS: dict[str, str] = {}
 
 
 def _reference_paths():
@@ -87,6 +85,10 @@ def _load_suites():
         setattr(ref.engine, name, getattr(pk_engine, name))
     ref.bench.runner.Store = pk.Store
     ref.bench.runner.StoreConfig = pk.StoreConfig
+    # the reference's file helpers the tests call directly (read_fvecs) raise
+    # the boundary's error types
+    for name in ("ParseError", "UsageError", "VersionMismatchError"):
+        setattr(ref.persist, name, getattr(pk, name))
 
     # the executor plugin: the reference TierManager drives the native executor
     def native_executor(model=None):

@@ -51,6 +51,25 @@ class TestPnck:
         assert recs[0][1].tolist() == [3, 1, 2 ** 40]
         assert np.array_equal(recs[0][2], cl[0][2]) and np.array_equal(recs[0][0], cl[0][0])
         assert len(recs[1][1]) == 0
+        # the snapshot's tagged sections come back in order (persist.restore)
+        write_pnck(p, d, Metric.COSINE, cl, sections=[(b"CMET", b'{"a":1}'), (b"META", b"")])
+        *_, secs = read_pnck(p, with_sections=True)
+        assert list(secs) == [b"CMET", b"META"] and secs[b"CMET"] == b'{"a":1}' and secs[b"META"] == b""
+        p.write_bytes(p.read_bytes() + b"TAG")  # truncated section
+        with pytest.raises(ParseError):
+            read_pnck(p, with_sections=True)
+
+    def test_snapshot_config_fields_are_the_references(self):
+        """CONF carries exactly the reference's StoreConfig fields, so the
+        reference's StoreConfig(**conf) accepts our snapshots."""
+        import dataclasses
+
+        from paper_2602_21477_b200.engine import StoreConfig
+        from paper_2602_21477_b200.persist import REFERENCE_CONFIG_FIELDS
+
+        ours = [f.name for f in dataclasses.fields(StoreConfig)]
+        assert [f for f in ours if f not in REFERENCE_CONFIG_FIELDS] == ["device", "sharded"]
+        assert all(f in ours for f in REFERENCE_CONFIG_FIELDS)
 
     def test_layout_bytes(self, tmp_path):
         """Byte layout of ref/persist.py:66-94."""
