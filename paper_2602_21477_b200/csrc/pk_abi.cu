@@ -421,6 +421,9 @@ struct pk_index {
     dirty_hi = std::max(dirty_hi, s);
     tver++;
   }
+  // a length change the caller writes into the device table itself
+  // (stream-ordered, e.g. the append kernel): host-side caches only
+  void touch() { tver++; }
   // longest live list, recomputed only after a table change (every h_len /
   // h_cid edit goes through mark(), which the device table sync relies on too)
   uint64_t tver = 1, maxlen_ver = 0;
@@ -436,15 +439,32 @@ struct pk_index {
     return maxlen_cached;
   }
 
+  // the dirty range of the list table goes over from a pinned snapshot (true
+  // async copies; pageable sources cost a driver staging pass each -- ~7 us
+  // per insert batch for four of them); the snapshot is rewritten only once
+  // the previous sync's copies have read it
+  // (two snapshots used in turn, so a sync rarely waits for the last one)
+  PinnedBuf tstage[2];
+  cudaEvent_t tstage_ev[2] = {nullptr, nullptr};
+  int tstage_i = 0;
   int sync_table() {
     if (dirty_hi < dirty_lo) return PK_OK;
     const int32_t lo = dirty_lo, n = dirty_hi - dirty_lo + 1;
-    // pageable sources: the driver stages them before returning, so the host
-    // mirror may change right after.
-    CK(cudaMemcpyAsync(d_off + lo, h_off.data() + lo, n * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_len + lo, h_len.data() + lo, n * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_cid + lo, h_cid.data() + lo, n * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(d_scope + lo, h_scope.data() + lo, n * 4, cudaMemcpyHostToDevice, st));
+    const int bi = tstage_i;
+    tstage_i ^= 1;
+    if (tstage_ev[bi]) CK(cudaEventSynchronize(tstage_ev[bi]));
+    else CK(cudaEventCreateWithFlags(&tstage_ev[bi], cudaEventDisableTiming));
+    RET(tstage[bi].ensure((size_t)n * 28));
+    uint8_t* p = tstage[bi].p;
+    memcpy(p, h_off.data() + lo, (size_t)n * 8);
+    memcpy(p + (size_t)n * 8, h_len.data() + lo, (size_t)n * 8);
+    memcpy(p + (size_t)n * 16, h_cid.data() + lo, (size_t)n * 8);
+    memcpy(p + (size_t)n * 24, h_scope.data() + lo, (size_t)n * 4);
+    CK(cudaMemcpyAsync(d_off + lo, p, n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_len + lo, p + (size_t)n * 8, n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_cid + lo, p + (size_t)n * 16, n * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_scope + lo, p + (size_t)n * 24, n * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(tstage_ev[bi], st));
     dirty_lo = INT32_MAX;
     dirty_hi = -1;
     return PK_OK;
@@ -1052,6 +1072,10 @@ int pk_index_destroy(pk_index* ix) {
   }
   if (ix->hsl.p) cudaFreeHost(ix->hsl.p);
   if (ix->hasg.p) cudaFreeHost(ix->hasg.p);
+  for (int i = 0; i < 2; i++) {
+    if (ix->tstage[i].p) cudaFreeHost(ix->tstage[i].p);
+    if (ix->tstage_ev[i]) cudaEventDestroy(ix->tstage_ev[i]);
+  }
   if (ix->hag.p) cudaFreeHost(ix->hag.p);
   ix->arows.release();
   ix->ag_in.release();
@@ -1326,6 +1350,7 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
       return fail(PK_ERR_USAGE, "cluster %lld is owned by another shard", (long long)cids[i]);
     add[slot[i]] += 1;
   }
+  std::unordered_map<int32_t, bool> moved;  // slots whose arena range changed
   for (auto& kv : add) {
     const int32_t s = kv.first;
     const int64_t len = ix->h_len[s], m = kv.second;
@@ -1359,6 +1384,7 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
       ix->free_range(ooff, ix->h_cap[s]);
       ix->h_off[s] = noff;
       ix->h_cap[s] = ncap;
+      moved[s] = true;
     }
   }
   // placement in batch order; host copies now, device rows by one scatter
@@ -1372,14 +1398,27 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
       dst.push_back(ix->h_off[s] + pos);
       pick.push_back(i);
     }
-    ix->mark(s);
+  }
+  // resident lists that only grew: their new lengths ride with the scatter
+  // (len_pairs); any other change goes through the table sync
+  std::vector<int64_t> lp;
+  for (auto& kv : add) {
+    const int32_t s = kv.first;
+    if (ix->h_res[s] && !moved.count(s)) {
+      lp.push_back(s);
+      lp.push_back(ix->h_len[s]);
+      ix->touch();
+    } else {
+      ix->mark(s);
+    }
   }
   const int64_t m = (int64_t)dst.size();
+  const int nlp = (int)(lp.size() / 2);
   if (m > 0) {
-    // [rows padded | ids | destinations] packed once into mapped pinned
-    // memory; small batches are read by the scatter kernel in place (no DMA
-    // operations), larger ones go over in one copy
-    const size_t bytes = (size_t)m * ix->dp * 4 + (size_t)m * 16;
+    // [rows padded | ids | destinations | (slot, len) pairs] packed once into
+    // mapped pinned memory; small batches are read by the scatter kernel in
+    // place (no DMA operations), larger ones go over in one copy
+    const size_t bytes = (size_t)m * ix->dp * 4 + (size_t)m * 16 + lp.size() * 8;
     const int bi = ix->hstage_i;
     ix->hstage_i ^= 1;
     PinnedBuf& hs = ix->hstage2[bi];
@@ -1396,6 +1435,7 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
       h_ids[j] = ids[pick[j]];
       h_dst[j] = dst[j];
     }
+    if (nlp) memcpy(h_dst + m, lp.data(), lp.size() * 8);
     const uint8_t* base = hs.dev;
     if (bytes > ((size_t)1 << 20)) {
       if (ix->tmp_rows2[bi].bytes < bytes) CK(cudaStreamSynchronize(ix->st));
@@ -1405,7 +1445,8 @@ int pk_list_append_batch(pk_index* ix, int64_t n, const int64_t* cids, const flo
     }
     const float* d_src = reinterpret_cast<const float*>(base);
     const int64_t* d_ids = reinterpret_cast<const int64_t*>(d_src + m * ix->dp);
-    launch_append_rows(d_src, d_ids, d_ids + m, (int)m, ix->rows, ix->ids, ix->nrm, (int)ix->dp, ix->st);
+    launch_append_rows(d_src, d_ids, d_ids + m, (int)m, ix->rows, ix->ids, ix->nrm, (int)ix->dp, ix->st,
+                       d_ids + 2 * m, nlp, ix->d_len);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ix->hstage_ev[bi], ix->st));  // no host wait: ordered on the index stream
   }

@@ -3334,7 +3334,13 @@ __global__ void __launch_bounds__(256) append_rows_kernel(const float* __restric
                                                           const int64_t* __restrict__ dst_row, int n,
                                                           float* __restrict__ rows,
                                                           int64_t* __restrict__ ids,
-                                                          float* __restrict__ nrm, int dp) {
+                                                          float* __restrict__ nrm, int dp,
+                                                          const int64_t* __restrict__ len_pairs, int nlen,
+                                                          int64_t* __restrict__ d_len) {
+  // the appended lists' new lengths (slot, len) go into the device table here,
+  // stream-ordered with the rows (no separate table upload)
+  if (blockIdx.x == 0)
+    for (int t = threadIdx.x; t < nlen; t += blockDim.x) d_len[len_pairs[2 * t]] = len_pairs[2 * t + 1];
   const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (i >= n) return;
@@ -3358,9 +3364,11 @@ __global__ void __launch_bounds__(256) append_rows_kernel(const float* __restric
   }
 }
 void launch_append_rows(const float* src, const int64_t* src_ids, const int64_t* dst_row, int n,
-                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st) {
-  if (n <= 0) return;
-  append_rows_kernel<<<(n + 7) / 8, 256, 0, st>>>(src, src_ids, dst_row, n, rows, ids, nrm, dp);
+                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st,
+                        const int64_t* len_pairs, int nlen, int64_t* d_len) {
+  if (n <= 0 && nlen <= 0) return;
+  append_rows_kernel<<<std::max((n + 7) / 8, 1), 256, 0, st>>>(src, src_ids, dst_row, n, rows, ids, nrm, dp,
+                                                               len_pairs, nlen, d_len);
 }
 
 }  // namespace pk

@@ -240,7 +240,8 @@ void launch_stage_norms(const StageCopy* desc, int ndesc, const float* rows, flo
 
 // Batched append: padded staging rows [n][dp] + ids -> arena rows dst_row[i], with norms.
 void launch_append_rows(const float* src, const int64_t* src_ids, const int64_t* dst_row, int n,
-                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st);
+                        float* rows, int64_t* ids, float* nrm, int dp, cudaStream_t st,
+                        const int64_t* len_pairs = nullptr, int nlen = 0, int64_t* d_len = nullptr);
 
 // Per-list exact distances of one query (agent-mode L2 scan): list l's rows
 // at src[l].rows ([n][dp], HBM or mapped host), ids at src[l].ids; rows of

@@ -158,10 +158,13 @@ class DeviceIndex:
             pend, self._pend = self._pend, []
         if not pend:
             return
-        cids = np.concatenate([c if isinstance(c, np.ndarray) else np.full(len(i), c, dtype=np.int64)
-                               for c, _, i in pend])
-        rows = np.ascontiguousarray(np.concatenate([r for _, r, _ in pend]))
-        ids = np.ascontiguousarray(np.concatenate([i for _, _, i in pend]))
+        if len(pend) == 1 and isinstance(pend[0][0], np.ndarray):  # one append_rows (an insert run)
+            cids, rows, ids = pend[0]
+        else:
+            cids = np.concatenate([c if isinstance(c, np.ndarray) else np.full(len(i), c, dtype=np.int64)
+                                   for c, _, i in pend])
+            rows = np.ascontiguousarray(np.concatenate([r for _, r, _ in pend]))
+            ids = np.ascontiguousarray(np.concatenate([i for _, _, i in pend]))
         N.check(N.lib().pk_list_append_batch(self._h, len(ids), N.ptr(cids), N.ptr(rows), N.ptr(ids)))
 
     def remove_row(self, cid: int, row: int):
