@@ -150,6 +150,28 @@ def main():
     n_q = 0
     staged0 = store.tier.metrics()["tier_staged_bytes_total"]
     same = None
+    T = {}
+    if os.environ.get("PK_TIME_CALLS"):  # wall time per wrapped call (no profiler overhead)
+        def wrap(obj, name, label):
+            fn = getattr(obj, name)
+
+            def timed(*a_, **k_):
+                t_ = time.perf_counter()
+                try:
+                    return fn(*a_, **k_)
+                finally:
+                    e = T.setdefault(label, [0, 0.0])
+                    e[0] += 1
+                    e[1] += time.perf_counter() - t_
+            setattr(obj, name, timed)
+        for m in ("_vectors", "_insert_run", "_tick"):
+            wrap(store, m, "store." + m)
+        wrap(store.clusters, "assign_nearest_batch", "clusters.assign_nearest_batch")
+        wrap(store.clusters, "add_members_batch", "clusters.add_members_batch")
+        wrap(store.index, "flush", "index.flush")
+        wrap(store.index, "set_resident", "index.set_resident")
+        wrap(store.tier, "hotset_update", "tier.hotset_update")
+        wrap(store.tier, "buffered_insert_batch", "tier.buffered_insert_batch")
     prof = None
     if os.environ.get("PK_PROFILE_STREAM"):  # cProfile of the insert path (batches 2000..)
         import cProfile
@@ -182,6 +204,10 @@ def main():
 
         prof.disable()
         pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(30)
+    if T:
+        for k, (n_, s_) in sorted(T.items(), key=lambda kv: -kv[1][1]):
+            print(f"  {k:32s} calls/batch {n_ / nbatches:6.3f}  us/batch {1e6 * s_ / nbatches:8.1f}",
+                  file=sys.stderr)
     m = store.tier.metrics()
     # parity: a query sample against the oracle over the final index
     from oracle import oracle as O
