@@ -546,6 +546,7 @@ class Store:
         if table is not None:
             hint = self._hint_from(agent, q, q_row, listing, SL)
         id_chunks, dist_chunks, scan_chunks = [], [], []
+        big = None
         early = False
         if cache is not None:
             cres = cache.replay(plan, dall[:n_plan], k, hint_keys=hint.predicted_clusters,
@@ -577,8 +578,14 @@ class Store:
                 # scanned < thresh) holds exactly when >= k scanned distances
                 # are below thresh: the first such li, from prefix counts
                 below = sum(int(np.count_nonzero(c < thresh)) for c in dist_chunks)
-                cb = np.concatenate(([0], np.cumsum(all_d < thresh)))
-                cum = below + cb[pre[1:len(selected) + 1]]
+                nsel = len(selected)
+                # per-list counts by one segmented sum (a False sentinel keeps
+                # every segment start in range; empty lists count 0)
+                m2 = np.zeros(int(pre[nsel]) + 1, dtype=bool)
+                np.less(all_d[:pre[nsel]], thresh, out=m2[:-1])
+                cnt = np.add.reduceat(m2, pre[:nsel], dtype=np.int64)
+                cnt[pre[:nsel] == pre[1:nsel + 1]] = 0
+                cum = below + np.cumsum(cnt)
                 ok = np.flatnonzero(cum >= k)
                 if len(ok):
                     stop_at = int(ok[0]) + 1
@@ -589,17 +596,16 @@ class Store:
                 cl = clusters[cid]
                 cl.access_count += 1
                 self.tier.record_access(cid)
-                ids = all_ids[pre[li]:pre[li + 1]]
-                if len(ids):
-                    id_chunks.append(ids)
-                    dist_chunks.append(all_d[pre[li]:pre[li + 1]])
-                stats.scanned_vectors += len(ids)
                 if self.cfg.profiles_enabled and agent and cl.profiles.get(agent):
                     order = profile_order(cl.profiles[agent], cl.size)
                     scan_chunks.append(cl.member_ids[order])
                 else:
                     scan_chunks.append(cl.member_ids.copy())
-        extended = self._topk(id_chunks, dist_chunks, max(k, self.cfg.kappa * k))
+            if stop_at:  # the scanned lists are one prefix of the device's rows
+                n_rows = int(pre[stop_at])
+                big = (all_ids[:n_rows], all_d[:n_rows])
+                stats.scanned_vectors += n_rows
+        extended = self._topk(id_chunks, dist_chunks, max(k, self.cfg.kappa * k), big)
         scan_ids = np.concatenate(scan_chunks) if scan_chunks else np.empty(0, dtype=np.int64)
         return SearchResult(extended[:k], stats, scan_ids), hint, extended
 
@@ -652,39 +658,60 @@ class Store:
         self._qrow_memo[agent] = (q.tobytes(), len(self.sequences[agent]), q_row, table.version)
         return hint
 
-    def _topk(self, id_chunks, dist_chunks, k):
+    def _topk(self, id_chunks, dist_chunks, k, big=None):
         """ref/engine.py:406-426: lexsort by (dist, id), first occurrence per
         id, owners only (a cached copy of a deleted item is skipped).  Only a
         prefix of the order is ever consumed, so it sorts the smallest
         entries first (every entry tied with the cut is included) and falls
-        back to the full order when duplicates / deleted ids exhaust it."""
-        if not id_chunks:
+        back to the full order when duplicates / deleted ids exhaust it.
+        ``big``: (ids, dists) of the probed lists' rows as one view, kept
+        apart from the small chunks so they are not copied (the candidates
+        of the cut come out of each part; the order over their union is the
+        same whichever chunk an entry came from)."""
+        if big is not None and len(big[0]) == 0:
+            big = None
+        if not id_chunks and big is None:
             return []
-        ids = np.concatenate(id_chunks)
-        dists = np.concatenate(dist_chunks).astype(np.float32)
-        n = len(ids)
+        ids = np.concatenate(id_chunks) if id_chunks else np.empty(0, np.int64)
+        dists = np.concatenate(dist_chunks).astype(np.float32) if dist_chunks else np.empty(0, np.float32)
+        if big is not None:
+            bi, bd = big[0], big[1].astype(np.float32, copy=False)
+        n = len(ids) + (len(bi) if big is not None else 0)
         take = min(n, 4 * k + 16)
         while True:
-            if take < n:
-                cut = np.partition(dists, take - 1)[take - 1]
-                sel = np.nonzero(dists <= cut)[0]  # ties at the cut kept whole
+            if big is None:
+                if take < n:
+                    cut = np.partition(dists, take - 1)[take - 1]
+                    sel = np.nonzero(dists <= cut)[0]  # ties at the cut kept whole
+                else:
+                    sel = np.arange(n)
+                cids, cds = ids[sel], dists[sel]
             else:
-                sel = np.arange(n)
-            order = sel[np.lexsort((ids[sel], dists[sel]))]
+                if take < n:
+                    # the take-th smallest of the union: within the big part's
+                    # take smallest and the small chunks
+                    head = np.partition(bd, take - 1)[:take] if len(bd) > take else bd
+                    cut = np.partition(np.concatenate((head, dists)), take - 1)[take - 1]
+                    sb, ss = np.nonzero(bd <= cut)[0], np.nonzero(dists <= cut)[0]
+                else:
+                    sb, ss = np.arange(len(bd)), np.arange(len(dists))
+                cids = np.concatenate((bi[sb], ids[ss]))
+                cds = np.concatenate((bd[sb], dists[ss]))
+            order = np.lexsort((cids, cds))
             hits, seen = [], set()
-            for idx in order:
-                iid = int(ids[idx])
+            owners, clusters = self.clusters.owner, self.clusters.clusters
+            for iid, dv in zip(cids[order].tolist(), cds[order].tolist()):
                 if iid in seen:
                     continue
                 seen.add(iid)
-                owner = self.clusters.owner.get(iid)
+                owner = owners.get(iid)
                 if owner is None:
                     continue
-                scope = owner[1] if owner[0] == "staged" else self.clusters.clusters[owner[1]].scope
-                hits.append((iid, float(dists[idx]), scope))
+                scope = owner[1] if owner[0] == "staged" else clusters[owner[1]].scope
+                hits.append((iid, dv, scope))
                 if len(hits) >= k:
                     return hits
-            if len(sel) >= n:
+            if len(cids) >= n:
                 return hits
             take = min(n, 4 * take)
 

@@ -424,3 +424,50 @@ def test_batched_adds_equal_sequential():
         assert [a.pool.staged_flag(i) for i in a.pool.ids] == [b.pool.staged_flag(i) for i in b.pool.ids]
         pa, pb = sa.take_puts(), sb.take_puts()
         assert sorted(pa[0].tolist()) == sorted(pb[0].tolist())
+
+
+def test_topk_big_part_equals_chunks():
+    """Store._topk with the probed lists' rows passed as one view (``big``)
+    returns exactly what the chunked call returns: ties at the cut, ids
+    duplicated across chunks, deleted ids (no owner) and the expansion past
+    4k + 16 candidates included."""
+    from types import SimpleNamespace
+
+    from paper_2602_21477_b200.engine import Store
+
+    rng = np.random.default_rng(11)
+    for trial in range(200):
+        n_big, n_small = int(rng.integers(0, 400)), int(rng.integers(0, 60))
+        pool = int(rng.integers(5, 300))
+        bi = rng.integers(0, pool, n_big).astype(np.int64)
+        bd = rng.integers(0, 40, n_big).astype(np.float32) / 8  # many exact ties
+        si = rng.integers(0, pool, n_small).astype(np.int64)
+        sd = rng.integers(0, 40, n_small).astype(np.float32) / 8
+        owner = {i: ("cluster", 0) for i in range(pool) if rng.random() < 0.7}
+        fake = SimpleNamespace(clusters=SimpleNamespace(owner=owner, clusters={0: SimpleNamespace(scope="s")}))
+        k = int(rng.integers(1, 25))
+        small = [si[:n_small // 2], si[n_small // 2:]]
+        smalld = [sd[:n_small // 2], sd[n_small // 2:]]
+        want = Store._topk(fake, [bi[:n_big // 3], bi[n_big // 3:]] + small,
+                           [bd[:n_big // 3], bd[n_big // 3:]] + smalld, k)
+        got = Store._topk(fake, small, smalld, k, (bi, bd))
+        assert got == want, trial
+
+
+def test_stop_rule_segment_counts():
+    """The read phase's per-list below-threshold counts (segmented sum with a
+    sentinel, empty lists 0) equal the prefix-count formulation."""
+    rng = np.random.default_rng(12)
+    for _ in range(300):
+        lens = rng.integers(0, 6, int(rng.integers(1, 12)))
+        lens[rng.random(len(lens)) < 0.3] = 0
+        pre = np.concatenate(([0], np.cumsum(lens)))
+        all_d = rng.random(int(pre[-1])).astype(np.float32)
+        thresh = float(rng.random())
+        nsel = int(rng.integers(1, len(lens) + 1))
+        m2 = np.zeros(int(pre[nsel]) + 1, dtype=bool)
+        np.less(all_d[:pre[nsel]], thresh, out=m2[:-1])
+        cnt = np.add.reduceat(m2, pre[:nsel], dtype=np.int64)
+        cnt[pre[:nsel] == pre[1:nsel + 1]] = 0
+        cb = np.concatenate(([0], np.cumsum(all_d < thresh)))
+        assert np.array_equal(np.cumsum(cnt), cb[pre[1:nsel + 1]])
