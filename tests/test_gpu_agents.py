@@ -32,3 +32,31 @@ def test_agent_trace_matches_reference(name):
     if spec["verify"]:
         assert sum(int(want[f"final/agent{a}/verified"]) for a in range(spec["n_agents"])) > 0
     store.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_most_similar_pattern_pair_equals_pairwise_loop(seed):
+    """observe_completed's pattern-table merge choice from one device matrix
+    over every pattern's states equals the reference's pairwise loop of
+    fsm_pair_similarity (ref/fsm.py:372-378), ties included."""
+    from paper_2602_21477_b200.core import Metric
+    from paper_2602_21477_b200.fsm import (AccessPatternFsm, FsmState, _most_similar_pair,
+                                           fsm_pair_similarity)
+
+    rng = np.random.default_rng(seed)
+    d = 32
+    base = rng.normal(size=(6, d)).astype(np.float32)
+    fsms = []
+    for _ in range(int(rng.integers(3, 18))):
+        n = int(rng.integers(1, 9))
+        # shared rows make exact ties between pairs
+        c = [base[int(rng.integers(0, 6))] if rng.random() < 0.4 else rng.normal(size=d).astype(np.float32)
+             for _ in range(n)]
+        fsms.append(AccessPatternFsm([FsmState(v, 0.1, 1, 1) for v in c], {}, [0] * n, 0.1))
+    best = (0, 1, -1.0)
+    for i in range(len(fsms) - 1):
+        for j in range(i + 1, len(fsms)):
+            s = fsm_pair_similarity(fsms[i], fsms[j], Metric.SQUARED_EUCLIDEAN)
+            if s > best[2]:
+                best = (i, j, s)
+    assert _most_similar_pair(fsms, Metric.SQUARED_EUCLIDEAN) == best[:2]
