@@ -828,7 +828,9 @@ class Store:
         self.runner.submit("cache", run)
 
     def _materialize(self, agent, outcomes):
-        """ref/engine.py:662-678: merged-down staged items become base clusters."""
+        """ref/engine.py:662-678: merged-down staged items become base clusters.
+        Returns the ids that were merged."""
+        merged_all = set()
         for outcome in outcomes:
             for scope_code, items in outcome.staged.items():
                 scope = self.scope_codes.name[scope_code]
@@ -841,6 +843,8 @@ class Store:
                 merged = {iid for iid, _ in live}
                 for c in self.caches.values():
                     c.mark_merged(merged)
+                merged_all |= merged
+        return merged_all
 
     # --- mutation ---------------------------------------------------------
     def insert(self, agent, scope: str, vectors, payloads=None, ids=None) -> list[int]:
@@ -877,6 +881,23 @@ class Store:
         vrows = [None] * n
         if agent is not None and self.cfg.pattern_enabled and self.patterns[agent].fsms:
             vrows = self._rows_for(agent, vecs)
+        if cache is not None:  # staged, owned by the agent's cache until merge-down
+            # every vector's L0 promotion in order, their L1 side in one
+            # placement chain (MultiLevelCache.promote_many_to_l0)
+            code = self.scope_codes.intern(scope)
+            proms = []
+            for i in range(n):
+                vec = vecs[i]
+                iid = self._take_id(ids[i] if ids is not None else None)
+                payload = payloads[i]
+                self.payloads[iid] = payload.encode("utf-8") if isinstance(payload, str) else payload
+                state_key = self._state_key_for(agent, vec, vrows[i])
+                self.clusters.stage_item(scope, iid, vec)
+                proms.append(([(iid, vec, code, True)], state_key))
+                self._append_sequence(agent, vec, vrows[i])
+                accepted.append(iid)
+            cache.promote_many_to_l0(proms, lambda outs: self._materialize(agent, outs))
+            return accepted
         while i < n:
             vec = vecs[i]
             iid = self._take_id(ids[i] if ids is not None else None)
@@ -884,16 +905,6 @@ class Store:
             if isinstance(payload, str):
                 payload = payload.encode("utf-8")
             self.payloads[iid] = payload
-            if cache is not None:  # staged, owned by the agent's cache until merge-down
-                state_key = self._state_key_for(agent, vec, vrows[i])
-                self.clusters.stage_item(scope, iid, vec)
-                self._materialize(agent, cache.promote_to_l0(
-                    [(iid, vec, self.scope_codes.intern(scope), True)], state_key))
-                self._append_sequence(agent, vec, vrows[i])
-                accepted.append(iid)
-                i += 1
-                assigned = None  # a merge-down may have created clusters
-                continue
             cands = self.clusters.by_scope[scope]
             if not cands:
                 self.clusters.create_cluster(scope, [(iid, vec)])
