@@ -159,7 +159,21 @@ int pk_scan_lists(pk_index* ix, const float* q, const int64_t* cids, int32_t m, 
  *   item_ids[i]; an id may recur in the chain), or -1.
  *   Per item: out_target = list position chosen (-1: a fresh cluster was
  *   appended), out_added, out_merged (merge_down after it); *out_qtarget
- *   likewise for q.  The caller applies the same operations in order. */
+ *   likewise for q.  The caller applies the same operations in order.
+ * pk_agent_lists: the list half of pk_agent_read (nprobe > 0) for B queries
+ *   Q [B][d] in one pass -- an agent's search batch, whose queries the Store
+ *   still answers one by one (ref/engine.py:287-317) -- query b's outputs at
+ *   out_cids + b*nprobe, out_prefix + b*(nprobe+1), out_coarse[b] and rows
+ *   [b*cap, b*cap + min(total, cap)) of out_ids / out_dists (a total above cap
+ *   is only reported).  *out_version = pk_list_version at the time: the
+ *   results stand for the lists, centroids and graph of that version.  Not on
+ *   a tiered index.
+ * pk_list_version: a counter bumped by every change of a list's rows, length,
+ *   centroid or slot and by pk_graph_set. */
+int pk_agent_lists(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes, int32_t nscopes,
+                   int32_t nprobe, int32_t ef, int32_t mode, int64_t cap, int64_t* out_cids, int32_t* out_coarse,
+                   int64_t* out_prefix, int64_t* out_ids, float* out_dists, uint64_t* out_version);
+int pk_list_version(pk_index* ix, uint64_t* version);
 int pk_rows_put(pk_index* ix, const int32_t* slots, const float* rows, int64_t n);
 int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const float* put_rows, int64_t nput,
                   const int32_t* slots, int64_t n, float* out_d, const int32_t* mq, int32_t nmq,

@@ -258,6 +258,8 @@ struct pk_index {
   cudaEvent_t ev_ag0 = nullptr, ev_ag1 = nullptr;
   PinnedBuf hag;  // mapped: packed inputs, then the kernels' outputs
   DevBuf ag_in, ag_l1;
+  PinnedBuf hal;  // pk_agent_lists: packed queries, then the traversal / list outputs (mapped)
+  DevBuf al_in;
   // front-half overlap: the next batch's prep / coarse / pick / routing run on
   // fst while this batch's scan and re-rank drain on st
   cudaStream_t fst = nullptr;
@@ -504,6 +506,7 @@ struct pk_index {
   // Squared norm of slot s's centroid (coarse screen input).
   // Derived centroid data of slot s: squared norm and the TF32 hi/lo split.
   void centroid_norm(int32_t s) {
+    tver++;  // the coarse distances change (pk_list_version readers)
     launch_row_norms(d_cent + (int64_t)s * dp, 1, (int)dp, d_cnrm + s, st);
     launch_tf32_split(d_cent + (int64_t)s * dp, 1, (int)dp, d_chi + (int64_t)s * dp,
                       d_clo + (int64_t)s * dp, st);
@@ -1077,6 +1080,8 @@ int pk_index_destroy(pk_index* ix) {
     if (ix->tstage_ev[i]) cudaEventDestroy(ix->tstage_ev[i]);
   }
   if (ix->hag.p) cudaFreeHost(ix->hag.p);
+  if (ix->hal.p) cudaFreeHost(ix->hal.p);
+  ix->al_in.release();
   ix->arows.release();
   ix->ag_in.release();
   ix->ag_l1.release();
@@ -2505,6 +2510,7 @@ int pk_graph_set(pk_index* ix, int32_t M, int64_t n, const int64_t* node_cid, co
   G.slot_ver = ix->slot_ver;
   G.static_code = static_code;
   G.set = true;
+  ix->tver++;  // a new graph: earlier traversals are stale (pk_list_version)
   return PK_OK;
 }
 
@@ -2900,6 +2906,81 @@ int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const 
     memcpy(out_ids, h + o_ids, total * 8);
     memcpy(out_dists, h + o_dd, total * 4);
   }
+  return PK_OK;
+}
+
+int pk_list_version(pk_index* ix, uint64_t* version) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (!version) return fail(PK_ERR_USAGE, "null output");
+  *version = ix->tver;
+  return PK_OK;
+}
+
+int pk_agent_lists(pk_index* ix, const float* Q, int64_t B, const int32_t* scope_codes, int32_t nscopes,
+                   int32_t nprobe, int32_t ef, int32_t mode, int64_t cap, int64_t* out_cids, int32_t* out_coarse,
+                   int64_t* out_prefix, int64_t* out_ids, float* out_dists, uint64_t* out_version) {
+  // The list half of pk_agent_read for B queries at once: the reference's
+  // coarse traversal of each (one CTA per query) and every row of the lists
+  // it probes, query b's rows in [b * cap, (b + 1) * cap) (a total above cap
+  // is reported by the prefix, the rows past it are not written).  Valid as
+  // long as pk_list_version still returns *out_version.
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (B < 0 || nprobe < 1 || cap < 0) return fail(PK_ERR_USAGE, "bad count");
+  if (nscopes < 1 || nscopes > 64) return fail(PK_ERR_USAGE, "scope count must lie in [1, 64]");
+  if (mode != 0 && mode != 1) return fail(PK_ERR_USAGE, "graph mode must be 0 (hybrid) or 1 (per-scope)");
+  if (ix->tiered) return fail(PK_ERR_USAGE, "pk_agent_lists: the tiered index reads cold lists per query");
+  if (!out_cids || !out_coarse || !out_prefix || !out_version || (cap > 0 && (!out_ids || !out_dists)))
+    return fail(PK_ERR_USAGE, "missing outputs");
+  if (B == 0 || ix->nslots == 0) {
+    for (int64_t i = 0; i < B * nprobe; i++) out_cids[i] = -1;
+    for (int64_t i = 0; i < B * (nprobe + 1); i++) out_prefix[i] = 0;
+    for (int64_t i = 0; i < B; i++) out_coarse[i] = 0;
+    *out_version = ix->tver;
+    return PK_OK;
+  }
+  CK(cudaSetDevice(ix->device));
+  cudaStream_t st = ix->st;
+  RET(ix->sync_table());
+  const int64_t dp = ix->dp, d = ix->d;
+  const int64_t maxlen = ix->max_list_len();
+  const int64_t rcap = std::min<int64_t>(cap, (int64_t)nprobe * maxlen);
+  Layout L;
+  const size_t o_q = L.take((size_t)B * dp * 4);
+  const size_t in_bytes = L.off;
+  const size_t o_cid = L.take((size_t)B * nprobe * 8), o_pre = L.take((size_t)B * (nprobe + 1) * 8),
+               o_cnt = L.take((size_t)B * 4), o_ids = L.take((size_t)B * rcap * 8),
+               o_dd = L.take((size_t)B * rcap * 4);
+  RET(ix->hal.ensure(L.off));
+  RET(ix->al_in.ensure(in_bytes));
+  uint8_t* h = ix->hal.p;
+  uint8_t* hd = ix->hal.dev;
+  pack_padded(reinterpret_cast<float*>(h + o_q), Q, B, d, dp);
+  CK(cudaMemcpyAsync(ix->al_in.p, h, in_bytes, cudaMemcpyHostToDevice, st));
+  pk_index::Scratch& S = ix->scr[ix->par];
+  RET(S.q.ensure((size_t)B * dp * 4));
+  RET(S.qnorm.ensure((size_t)B * 4));
+  RET(S.probe.ensure((size_t)B * nprobe * 4));
+  CK(cudaMemcpyAsync(S.q.p, ix->al_in.p, (size_t)B * dp * 4, cudaMemcpyDeviceToDevice, st));
+  if (ix->metric == COSINE) launch_qnorm(S.q.as<float>(), dp, (int)B, (int)d, S.qnorm.as<float>(), st);
+  GraphArgs ga;
+  ga.ef = ef;
+  ga.mode = mode;
+  ga.out_coarse = reinterpret_cast<int32_t*>(h + o_cnt);
+  RET(graph_coarse(ix, S, B, scope_codes, nscopes, nprobe, ga, st));
+  launch_probe_lists(ix->metric, S.q.as<float>(), ix->table(), S.probe.as<int32_t>(), nprobe, maxlen, rcap,
+                     reinterpret_cast<float*>(hd + o_dd), reinterpret_cast<int64_t*>(hd + o_ids),
+                     reinterpret_cast<int64_t*>(hd + o_pre), reinterpret_cast<int64_t*>(hd + o_cid), st, (int)B);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));
+  memcpy(out_cids, h + o_cid, (size_t)B * nprobe * 8);
+  memcpy(out_prefix, h + o_pre, (size_t)B * (nprobe + 1) * 8);
+  memcpy(out_coarse, h + o_cnt, (size_t)B * 4);
+  for (int64_t b = 0; b < B; b++) {
+    const int64_t tot = std::min<int64_t>(out_prefix[b * (nprobe + 1) + nprobe], rcap);
+    memcpy(out_ids + b * cap, h + o_ids + (size_t)b * rcap * 8, tot * 8);
+    memcpy(out_dists + b * cap, h + o_dd + (size_t)b * rcap * 4, tot * 4);
+  }
+  *out_version = ix->tver;
   return PK_OK;
 }
 

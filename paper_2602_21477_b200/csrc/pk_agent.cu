@@ -213,6 +213,14 @@ __global__ void __launch_bounds__(128) probe_lists_kernel(const float* __restric
   __shared__ const float* rowp[128];
   __shared__ float qn_s;
   __shared__ int64_t pre_s;
+  // batched (pk_agent_lists): query z's vector, probe and output blocks
+  const int z = blockIdx.z;
+  q += (int64_t)z * lt.dp;
+  probe += (int64_t)z * nprobe;
+  out_d += z * cap;
+  out_ids += z * cap;
+  out_prefix += (int64_t)z * (nprobe + 1);
+  out_cids += (int64_t)z * nprobe;
   const int p = blockIdx.y;
   const int sl = probe[p];
   const int64_t len = sl >= 0 ? lt.len[sl] : 0;
@@ -431,11 +439,11 @@ void launch_gather_mat(int metric, const float* rows, int dp, int d, const int32
 
 void launch_probe_lists(int metric, const float* q, ListTable lt, const int32_t* probe, int nprobe,
                         int64_t maxlen, int64_t cap, float* out_d, int64_t* out_ids, int64_t* out_prefix,
-                        int64_t* out_cids, cudaStream_t st) {
-  if (nprobe <= 0) return;
+                        int64_t* out_cids, cudaStream_t st, int nq) {
+  if (nprobe <= 0 || nq <= 0) return;
   int rpb = 128;
-  while (rpb > 32 && ((maxlen + rpb - 1) / rpb) * nprobe < 296) rpb >>= 1;
-  const dim3 grid((unsigned)std::max<int64_t>(1, (maxlen + rpb - 1) / rpb), (unsigned)nprobe);
+  while (rpb > 32 && ((maxlen + rpb - 1) / rpb) * nprobe * nq < 296) rpb >>= 1;
+  const dim3 grid((unsigned)std::max<int64_t>(1, (maxlen + rpb - 1) / rpb), (unsigned)nprobe, (unsigned)nq);
   const size_t sm = ag_smem(lt.dp);
 #define AG_PL(M)                                                                                  \
   {                                                                                             \

@@ -262,7 +262,8 @@ void launch_gather_mat(int metric, const float* rows, int dp, int d, const int32
 // every row of the probed lists (device slots, coarse order), list after list
 void launch_probe_lists(int metric, const float* q, ListTable lt, const int32_t* probe, int nprobe,
                         int64_t maxlen, int64_t cap, float* out_d, int64_t* out_ids, int64_t* out_prefix,
-                        int64_t* out_cids, cudaStream_t st);
+                        int64_t* out_cids, cudaStream_t st, int nq = 1);  // nq queries: q [nq][dp],
+                        // probe [nq][nprobe], outputs in blocks of cap / nprobe + 1 / nprobe per query
 // the L1 placement chain of ref/cache.py:284-325 (one CTA)
 int l1_place_max_clusters();
 void launch_l1_place(int metric, int nc0, int n_p, int cap, int dp, int d, double* sums, float* cents,

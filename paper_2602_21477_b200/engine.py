@@ -250,6 +250,8 @@ class Store:
         self._drows: dict[str, list] = {}  # per agent: D rows of its request sequence
         self._qrow_memo: dict = {}  # per agent: the last hinted query's D row
         self._list_cap = 2 * cfg.split_target  # rows per probed list the agent pass reserves
+        self._tiered_native = native_tier
+        self._lists_pf = None  # an agent search batch's prefetched lists (_prefetch_lists)
         self.runner = TaskRunner(cfg.threads)
         self.tier = TierManager(self.clusters, self.index, budget_bytes=cfg.budget_bytes,
                                 b_insert=cfg.b_insert, decay_half_life=cfg.decay_half_life,
@@ -415,8 +417,16 @@ class Store:
             # per-query pipeline, B calls of search(): with agent profiles on,
             # each query's scan order depends on the profile updates of the
             # queries before it (ref/engine.py:488-496), so they cannot share
-            # one read phase
-            return [self.search(agent, scopes, Q[b], k, nprobe) for b in range(Q.shape[0])]
+            # one read phase.  What they can share is the device half that
+            # no side effect changes: the coarse traversal and the probed
+            # lists' rows of every query, in one pass (used while the lists,
+            # centroids and graph are unchanged)
+            if Q.shape[0] > 1 and self._agent_path(agent, scopes, k=k):
+                self._prefetch_lists(scopes, Q, k, nprobe)
+            try:
+                return [self.search(agent, scopes, Q[b], k, nprobe) for b in range(Q.shape[0])]
+            finally:
+                self._lists_pf = None
         with self._serialized(agent):
             self._lock.acquire_read()
             try:
@@ -428,6 +438,35 @@ class Store:
                     self._search_side_effects(agent, Q[b], k, PatternHint(), res, None, False)
                 self._tick()
             return results
+
+    def _prefetch_lists(self, scopes, Q, k, nprobe):
+        """pk_agent_lists for the queries of an agent's search batch: what
+        _search_read_phase's agent_read would compute for their lists, keyed
+        by the query bytes and the plan, stamped with the list version."""
+        self._lists_pf = None
+        if self._tiered_native or not hasattr(self.index, "agent_lists") or not self.clusters.clusters:
+            return
+        self._lock.acquire_read()
+        try:
+            eff_nprobe, ef, mode = self._coarse_plan(k, nprobe)
+            in_scope = sum(len(self.clusters.by_scope[s]) for s in scopes)
+            dev_nprobe = max(1, min(eff_nprobe, in_scope))
+            codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
+            self.graph.upload()
+            ver, outs = self.index.agent_lists(Q, codes, dev_nprobe, ef, mode, dev_nprobe * self._list_cap)
+            plan = (tuple(codes), dev_nprobe, ef, mode)
+            self._lists_pf = (ver, plan, {Q[b].tobytes(): o for b, o in enumerate(outs) if o is not None})
+        finally:
+            self._lock.release_read()
+
+    def _prefetched_lists(self, q, plan):
+        pf = self._lists_pf
+        if pf is None or pf[1] != plan:
+            return None
+        lists = pf[2].get(q.tobytes())
+        if lists is None or pf[0] != self.index.list_version():
+            return None
+        return lists
 
     def _coarse_plan(self, k, nprobe):
         """(eff_nprobe, ef, mode) of the coarse traversal (ref/engine.py:365-373,
@@ -529,10 +568,13 @@ class Store:
                 dev_nprobe = max(1, min(eff_nprobe, in_scope))
                 codes = [self.scope_codes.intern(s) for s in sorted(scopes)]
                 self.graph.upload()
-            dall, SL, lists = self.index.agent_read(
+            lists = self._prefetched_lists(q, (tuple(codes), dev_nprobe, ef, mode)) if dev_nprobe else None
+            dall, SL, read_lists = self.index.agent_read(
                 q, rows.take_puts(), np.concatenate(parts), st_slots if listing else None,
-                lslots if listing else None, codes, dev_nprobe, ef, mode,
+                lslots if listing else None, codes, 0 if lists is not None else dev_nprobe, ef, mode,
                 cap=dev_nprobe * self._list_cap)
+            if lists is None:
+                lists = read_lists
         if lists is not None and len(lists[3]) > dev_nprobe * self._list_cap:
             self._list_cap = -(-len(lists[3]) // max(dev_nprobe, 1)) * 2
         n_plan = len(plan["slots"]) if plan is not None else 0

@@ -416,6 +416,37 @@ class DeviceIndex:
                 None, 0))
         return out_d[:len(slots)], out_m[:nmq, :nmx], lists
 
+    def agent_lists(self, Q, scope_codes, nprobe: int, ef: int, mode: int, cap: int):
+        """pk_agent_lists: the coarse traversal and probed-list rows of B
+        queries in one pass.  Returns (version, [lists_b]) with lists_b as
+        agent_read's lists, or None for a query whose rows exceed cap."""
+        self.flush()
+        Q = N.f32(Q, self.dimension)
+        B = Q.shape[0]
+        codes = np.ascontiguousarray(scope_codes, dtype=np.int32)
+        cap = max(int(cap), 1)
+        cids = np.empty((B, nprobe), dtype=np.int64)
+        coarse = np.empty(B, dtype=np.int32)
+        pre = np.zeros((B, nprobe + 1), dtype=np.int64)
+        ids = np.empty((B, cap), dtype=np.int64)
+        dd = np.empty((B, cap), dtype=np.float32)
+        ver = ctypes.c_uint64(0)
+        N.check(N.lib().pk_agent_lists(self._h, N.ptr(Q), B, N.ptr(codes), len(codes), int(nprobe), int(ef),
+                                       int(mode), cap, N.ptr(cids), N.ptr(coarse), N.ptr(pre), N.ptr(ids),
+                                       N.ptr(dd), ctypes.byref(ver)))
+        out = []
+        for b in range(B):
+            t = int(pre[b, -1])
+            out.append(None if t > cap else (cids[b], int(coarse[b]), pre[b], ids[b, :t], dd[b, :t]))
+        return int(ver.value), out
+
+    def list_version(self) -> int:
+        """pk_list_version (after the queued appends are applied)."""
+        self.flush()
+        v = ctypes.c_uint64(0)
+        N.check(N.lib().pk_list_version(self._h, ctypes.byref(v)))
+        return int(v.value)
+
     def l1_place(self, nc, n_p, capacity, sums, cents, counts, items, item_ids, holder, q=None):
         """pk_l1_place: (targets i32[m], added u8[m], q target or None)."""
         self.flush()

@@ -288,17 +288,30 @@ def agent_store_config_kwargs(spec):
     )
 
 
-def run_agent_ops(store, spec, base, ops, write_pnck, metric):
+def run_agent_ops(store, spec, base, ops, write_pnck, metric, group_searches=False):
     """Apply an agent trace to a Store (the reference's or this package's --
-    the same code drives both sides) and record what it returns."""
+    the same code drives both sides) and record what it returns.
+    group_searches: each run of consecutive searches with the same (agent,
+    scopes, k, nprobe) goes through ONE search_batch call (this package only;
+    equal to the searches one by one)."""
     import os
     import tempfile
 
     rec = {"digest": np.array(digest(base)), "n_ops": np.array(len(ops))}
     for a in range(spec["n_agents"]):
         store.register_agent(f"agent{a}")
+    batched = {}
     for i, op in enumerate(ops):
         kind = op[0]
+        if group_searches and kind == "search" and i not in batched:
+            key = (op[1], tuple(op[2]), op[4], op[5])
+            j = i
+            while j + 1 < len(ops) and ops[j + 1][0] == "search" and \
+                    (ops[j + 1][1], tuple(ops[j + 1][2]), ops[j + 1][4], ops[j + 1][5]) == key:
+                j += 1
+            res = store.search_batch(op[1], op[2], np.stack([ops[t][3] for t in range(i, j + 1)]), op[4], op[5],
+                                     want_scan_ids=True)
+            batched.update({t: res[t - i] for t in range(i, j + 1)})
         if kind == "load":
             _, scope, lists = op
             with tempfile.TemporaryDirectory() as td:
@@ -320,7 +333,7 @@ def run_agent_ops(store, spec, base, ops, write_pnck, metric):
             store.flush_caches()
         elif kind == "search":
             _, agent, scopes, q, k, nprobe = op
-            res = store.search(agent, scopes, q, k, nprobe)
+            res = batched.pop(i) if group_searches else store.search(agent, scopes, q, k, nprobe)
             rec[f"{i}/hit_ids"] = np.array([h[0] for h in res.hits], dtype=np.int64)
             rec[f"{i}/hit_d"] = np.array([h[1] for h in res.hits], dtype=np.float32)
             rec[f"{i}/hit_scope"] = np.array([h[2] for h in res.hits], dtype="U16")

@@ -15,6 +15,42 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("name", list(gen.AGENT_TRACE_SPECS))
+def test_agent_trace_search_batches(name):
+    """The same traces with each run of an agent's searches submitted as one
+    search_batch: the queries are answered one by one (each one's side
+    effects shape the next), their coarse traversals and probed-list rows
+    come from ONE device pass (pk_agent_lists) while the lists are unchanged."""
+    from paper_2602_21477_b200 import Store, StoreConfig
+    from paper_2602_21477_b200.core import Metric
+    from paper_2602_21477_b200.pnck import write_pnck
+
+    spec = gen.AGENT_TRACE_SPECS[name]
+    want = load_golden(f"agent_{name}.npz")
+    base, ops = gen.agent_trace_ops(spec)
+    store = Store(StoreConfig(**gen.agent_store_config_kwargs(spec)))
+    calls = [0, 0]  # batched passes, searches answered from one
+    lists_fn, pf_fn = store.index.agent_lists, store._prefetched_lists
+
+    def counted_lists(*a, **kw):
+        calls[0] += 1
+        return lists_fn(*a, **kw)
+
+    def counted_pf(*a, **kw):
+        out = pf_fn(*a, **kw)
+        calls[1] += out is not None
+        return out
+
+    store.index.agent_lists = counted_lists
+    store._prefetched_lists = counted_pf
+    got = gen.run_agent_ops(store, spec, base, ops, write_pnck, Metric(spec.get("metric", "sq_l2")),
+                            group_searches=True)
+    mism = compare_records(got, want)
+    assert not mism, "\n".join(mism[:10])
+    assert calls[0] > 0 and calls[1] > 0, calls
+    store.close()
+
+
+@pytest.mark.parametrize("name", list(gen.AGENT_TRACE_SPECS))
 def test_agent_trace_matches_reference(name):
     from paper_2602_21477_b200 import Store, StoreConfig
     from paper_2602_21477_b200.core import Metric

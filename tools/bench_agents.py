@@ -239,7 +239,7 @@ def main():
                         e[1] += time.perf_counter() - t
                 setattr(obj, name, timed)
             idx = store.index
-            for m in ("agent_read", "l1_place", "rows_put", "create_list", "graph_set", "append", "assign",
+            for m in ("agent_read", "agent_lists", "l1_place", "rows_put", "create_list", "graph_set", "append", "assign",
                       "flush"):
                 if hasattr(idx, m):
                     wrap(idx, m, "index." + m)
