@@ -134,8 +134,32 @@ def test_vector_pool_matches_list_model(ordered):
     dev = {}  # what the device row store would hold: slot -> row
     nid = 0
     for step in range(3000):
-        op = rng.integers(0, 4)
-        if op <= 1 or not model:
+        op = rng.integers(0, 5)
+        if op == 4 and model:
+            # promote_many: remove (staged |= prior) + add per item, in order
+            items = []
+            for j in rng.permutation(len(model))[:int(rng.integers(1, 5))].tolist():
+                iid, v = model[j][0], model[j][1]
+                if rng.integers(0, 4) == 0:
+                    v = rng.normal(size=d).astype(np.float32)  # a changed vector: re-uploaded
+                items.append((iid, v, int(rng.integers(0, 3)), bool(rng.integers(0, 2))))
+            for _ in range(int(rng.integers(0, 3))):
+                items.append((nid, rng.normal(size=d).astype(np.float32), int(rng.integers(0, 3)),
+                              bool(rng.integers(0, 2))))
+                nid += 1
+            pool.promote_many(items)
+            for iid, v, sc, st in items:
+                at = [m[0] for m in model].index(iid) if iid in [m[0] for m in model] else None
+                if at is not None:
+                    st = st or model[at][3]
+                    if ordered:
+                        model.pop(at)
+                    else:
+                        last = model.pop()
+                        if at < len(model):
+                            model[at] = last
+                model.append((iid, v, sc, st))
+        elif op <= 1 or not model:
             v = rng.normal(size=d).astype(np.float32)
             sc, st = int(rng.integers(0, 3)), bool(rng.integers(0, 2))
             assert pool.add(nid, v, sc, st)
