@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <sys/mman.h>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -83,6 +84,8 @@ struct PinnedBuf {
   int ensure(size_t need) {
     if (need <= bytes) return PK_OK;
     size_t nb = std::max(need, bytes + bytes / 2);
+    static const bool dbg = getenv("PK_DEBUG_GROW") != nullptr;  // (measurement only)
+    if (dbg) fprintf(stderr, "pinned buffer grow %zu -> %zu bytes\n", bytes, nb);
     if (p) cudaFreeHost(p);
     p = dev = nullptr;
     bytes = 0;
@@ -344,6 +347,15 @@ struct pk_index {
   int64_t* hids = nullptr;   // [hcap] pinned
   float* hrows_d = nullptr;  // device aliases (mapped)
   int64_t* hids_d = nullptr;
+  // In-place growth: the arena is one reserved virtual range, registered
+  // (pinned + mapped) in segments as it grows, so a growth pins only the new
+  // rows and moves nothing (a copying growth of a multi-GB arena costs
+  // seconds).  hseg: the first row of every segment; DMA copies never cross
+  // one (for_host_pieces).  hva_rows == nullptr: cudaHostAlloc arena.
+  float* hva_rows = nullptr;
+  int64_t* hva_ids = nullptr;
+  size_t hva_rows_bytes = 0, hva_ids_bytes = 0;
+  std::vector<int64_t> hseg;
   int64_t hcap = 0, htop = 0;
   std::vector<Range> hfree;
   std::vector<int64_t> h_hoff, h_hcap;
@@ -623,9 +635,25 @@ struct pk_index {
 
   // ---- cold tier helpers ----------------------------------------------
   int host_grow(int64_t need) {
+    static const bool dbg = getenv("PK_DEBUG_GROW") != nullptr;  // (measurement only)
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t ncap = std::max<int64_t>({need, hcap + hcap / 2, 1024});
+    struct Report {
+      bool on;
+      int64_t from, to;
+      std::chrono::steady_clock::time_point t0;
+      ~Report() {
+        if (on)
+          fprintf(stderr, "host arena grow %lld -> %lld rows: %.1f ms\n", (long long)from, (long long)to,
+                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+      }
+    } rep{dbg, hcap, ncap, t0};
+    if (host_grow_in_place(ncap)) {  // nothing moves: no wait for readers of the arena
+      rep.to = hcap;
+      return PK_OK;
+    }
     if (st) CK(cudaStreamSynchronize(st));  // gathers / migrations read the old host arena
     if (mst) CK(cudaStreamSynchronize(mst));
-    const int64_t ncap = std::max<int64_t>({need, hcap + hcap / 2, 1024});
     float* nr = nullptr;
     int64_t* ni = nullptr;
     CK(cudaHostAlloc((void**)&nr, (size_t)ncap * dp * 4, cudaHostAllocMapped | cudaHostAllocPortable));
@@ -641,6 +669,76 @@ struct pk_index {
     hcap = ncap;
     CK(cudaHostGetDevicePointer((void**)&hrows_d, hrows, 0));
     CK(cudaHostGetDevicePointer((void**)&hids_d, hids, 0));
+    return PK_OK;
+  }
+  // Grow the reserved-range arena to >= ncap rows in place; false: not
+  // available (no reservation, mapping not at the host address), the caller
+  // falls back to a copying growth.
+  bool host_grow_in_place(int64_t ncap) {
+    constexpr int64_t G = 4096;  // segment granularity in rows: page- and row-aligned for rows and ids
+    if (hrows && !hva_rows) return false;  // a cudaHostAlloc arena stays one
+    if (!hva_rows) {
+      int can = 0;
+      cudaDeviceGetAttribute(&can, cudaDevAttrCanUseHostPointerForRegisteredMem, device);
+      if (!can || getenv("PK_HOST_ARENA_COPY")) return false;
+      hva_rows_bytes = (size_t)1 << 40;  // address space only (MAP_NORESERVE)
+      hva_ids_bytes = (size_t)1 << 37;
+      void* a = mmap(nullptr, hva_rows_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+      void* b = mmap(nullptr, hva_ids_bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+      if (a == MAP_FAILED || b == MAP_FAILED) {
+        if (a != MAP_FAILED) munmap(a, hva_rows_bytes);
+        if (b != MAP_FAILED) munmap(b, hva_ids_bytes);
+        return false;
+      }
+      // transparent huge pages where the system allows them: 512x fewer
+      // pages for cudaHostRegister to pin (advice only; harmless if refused)
+      madvise(a, hva_rows_bytes, MADV_HUGEPAGE);
+      madvise(b, hva_ids_bytes, MADV_HUGEPAGE);
+      hva_rows = static_cast<float*>(a);
+      hva_ids = static_cast<int64_t*>(b);
+    }
+    const int64_t from = hcap;
+    const int64_t to = (ncap + G - 1) / G * G;
+    if ((size_t)to * dp * 4 > hva_rows_bytes || (size_t)to * 8 > hva_ids_bytes) return false;
+    char* r0 = reinterpret_cast<char*>(hva_rows) + (size_t)from * dp * 4;
+    char* i0 = reinterpret_cast<char*>(hva_ids) + (size_t)from * 8;
+    const size_t rb = (size_t)(to - from) * dp * 4, ib = (size_t)(to - from) * 8;
+    if (cudaHostRegister(r0, rb, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    if (cudaHostRegister(i0, ib, cudaHostRegisterMapped | cudaHostRegisterPortable) != cudaSuccess) {
+      cudaGetLastError();
+      cudaHostUnregister(r0);
+      return false;
+    }
+    void *dr = nullptr, *di = nullptr;
+    cudaHostGetDevicePointer(&dr, r0, 0);
+    cudaHostGetDevicePointer(&di, i0, 0);
+    if (dr != r0 || di != i0) {  // the kernels index one contiguous device range
+      cudaHostUnregister(r0);
+      cudaHostUnregister(i0);
+      cudaGetLastError();
+      return false;
+    }
+    hseg.push_back(from);
+    hrows = hrows_d = hva_rows;
+    hids = hids_d = hva_ids;
+    hcap = to;
+    return true;
+  }
+  // f(first row, count) over [row0, row0 + n) cut at segment starts (a DMA
+  // copy must stay inside one host registration)
+  template <class F>
+  int for_host_pieces(int64_t row0, int64_t n, F f) {
+    while (n > 0) {
+      int64_t end = row0 + n;
+      for (int64_t b : hseg)
+        if (b > row0 && b < end) end = b;
+      RET(f(row0, end - row0));
+      n -= end - row0;
+      row0 = end;
+    }
     return PK_OK;
   }
   int host_alloc(int64_t cap, int64_t* off) {
@@ -665,8 +763,12 @@ struct pk_index {
     if (n <= 0) return PK_OK;
     RET(host_fence());
     if (dev) {
-      CK(cudaMemcpy2DAsync(hrows + at * dp, dp * 4, src, d * 4, d * 4, n, cudaMemcpyDeviceToHost, st));
-      CK(cudaMemcpyAsync(hids + at, src_ids, n * 8, cudaMemcpyDeviceToHost, st));
+      RET(for_host_pieces(at, n, [&](int64_t r0, int64_t m) {
+        CK(cudaMemcpy2DAsync(hrows + r0 * dp, dp * 4, src + (r0 - at) * d, d * 4, d * 4, m,
+                             cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(hids + r0, src_ids + (r0 - at), m * 8, cudaMemcpyDeviceToHost, st));
+        return PK_OK;
+      }));
       CK(cudaStreamSynchronize(st));
     } else {
       for (int64_t r = 0; r < n; r++) memcpy(hrows + (at + r) * dp, src + r * d, d * 4);
@@ -773,8 +875,12 @@ struct pk_index {
           n += desc[j].n;
           j++;
         }
-        CK(cudaMemcpyAsync(rows + desc[i].dst_row * dp, hrows + desc[i].src_row * dp, (size_t)n * dp * 4,
-                           cudaMemcpyHostToDevice, st));
+        const int64_t s0 = desc[i].src_row, d0 = desc[i].dst_row;
+        RET(for_host_pieces(s0, n, [&](int64_t r0, int64_t m) {
+          CK(cudaMemcpyAsync(rows + (d0 + r0 - s0) * dp, hrows + r0 * dp, (size_t)m * dp * 4,
+                             cudaMemcpyHostToDevice, st));
+          return PK_OK;
+        }));
         i = j;
       }
       launch_stage_norms(stage_desc.as<StageCopy>(), (int)desc.size(), rows, nrm, (int)dp, hids_d, ids, st);
@@ -797,8 +903,11 @@ struct pk_index {
       return PK_OK;
     }
     RET(tmp_rows.ensure((size_t)std::max<int64_t>(h_len[s], 1) * dp * 4));
-    CK(cudaMemcpyAsync(tmp_rows.p, hrows + h_hoff[s] * dp, (size_t)h_len[s] * dp * 4,
-                       cudaMemcpyHostToDevice, st));
+    RET(for_host_pieces(h_hoff[s], h_len[s], [&](int64_t r0, int64_t m) {
+      CK(cudaMemcpyAsync(tmp_rows.as<float>() + (r0 - h_hoff[s]) * dp, hrows + r0 * dp, (size_t)m * dp * 4,
+                         cudaMemcpyHostToDevice, st));
+      return PK_OK;
+    }));
     *out = tmp_rows.as<float>();
     return PK_OK;
   }
@@ -1120,8 +1229,17 @@ int pk_index_destroy(pk_index* ix) {
   if (ix->comb.area) cudaFree(ix->comb.area);
   if (ix->comb.d_peers) cudaFree(ix->comb.d_peers);
   if (ix->comb.done_ctr) cudaFree(ix->comb.done_ctr);
-  if (ix->hrows) cudaFreeHost(ix->hrows);
-  if (ix->hids) cudaFreeHost(ix->hids);
+  if (ix->hva_rows) {
+    for (size_t i = 0; i < ix->hseg.size(); i++) {
+      cudaHostUnregister(reinterpret_cast<char*>(ix->hva_rows) + (size_t)ix->hseg[i] * ix->dp * 4);
+      cudaHostUnregister(reinterpret_cast<char*>(ix->hva_ids) + (size_t)ix->hseg[i] * 8);
+    }
+    munmap(ix->hva_rows, ix->hva_rows_bytes);
+    munmap(ix->hva_ids, ix->hva_ids_bytes);
+  } else {
+    if (ix->hrows) cudaFreeHost(ix->hrows);
+    if (ix->hids) cudaFreeHost(ix->hids);
+  }
   ix->stage_desc.release();
   ix->tmp_rows.release();
   for (auto& sc : ix->scr) sc.release();
@@ -1616,10 +1734,14 @@ int pk_list_set_resident(pk_index* ix, int64_t cid, int resident) {
     CK(cudaStreamWaitEvent(ix->mst, ix->stage_ev, 0));
     ix->stage_recorded = true;
     if (len > 0) {
-      CK(cudaMemcpyAsync(ix->rows + off * ix->dp, ix->hrows + ix->h_hoff[s] * ix->dp,
-                         (size_t)len * ix->dp * 4, cudaMemcpyHostToDevice, ix->mst));
-      CK(cudaMemcpyAsync(ix->ids + off, ix->hids + ix->h_hoff[s], (size_t)len * 8,
-                         cudaMemcpyHostToDevice, ix->mst));
+      const int64_t h0 = ix->h_hoff[s];
+      RET(ix->for_host_pieces(h0, len, [&](int64_t r0, int64_t m) {
+        CK(cudaMemcpyAsync(ix->rows + (off + r0 - h0) * ix->dp, ix->hrows + r0 * ix->dp,
+                           (size_t)m * ix->dp * 4, cudaMemcpyHostToDevice, ix->mst));
+        CK(cudaMemcpyAsync(ix->ids + off + r0 - h0, ix->hids + r0, (size_t)m * 8, cudaMemcpyHostToDevice,
+                           ix->mst));
+        return PK_OK;
+      }));
       launch_row_norms(ix->rows + off * ix->dp, len, (int)ix->dp, ix->nrm + off, ix->mst);
       CK(cudaGetLastError());
     }
@@ -2657,7 +2779,19 @@ namespace {
 // grow the agent row store to at least `need` slots, contents kept
 int rows_reserve(pk_index* ix, int64_t need) {
   if (need <= ix->acap) return PK_OK;
+  static const bool dbg = getenv("PK_DEBUG_GROW") != nullptr;  // (measurement only)
+  const auto t0 = std::chrono::steady_clock::now();
   const int64_t nc = std::max<int64_t>({need, ix->acap + ix->acap / 2, 1024});
+  struct Report {
+    bool on;
+    int64_t from, to;
+    std::chrono::steady_clock::time_point t0;
+    ~Report() {
+      if (on)
+        fprintf(stderr, "row store grow %lld -> %lld rows: %.1f ms\n", (long long)from, (long long)to,
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+  } rep{dbg, ix->acap, nc, t0};
   void* p = nullptr;
   CK(cudaMalloc(&p, (size_t)nc * ix->dp * 4));
   if (ix->acap)
