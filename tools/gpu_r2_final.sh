@@ -3,7 +3,7 @@
 # tools/ncu_summary.py for the ncu summaries).
 #   V=v2 bash tools/gpu_r2_final.sh
 set -u
-V=${V:-v2}
+V=${V:-v5}
 mkdir -p gpurun_out
 nvidia-smi -L > gpurun_out/host.txt; nproc >> gpurun_out/host.txt; free -g >> gpurun_out/host.txt
 # configs[1] (the headline), its reference arm, configs[0], configs[3] on one GPU
