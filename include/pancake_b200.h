@@ -174,6 +174,10 @@ int pk_agent_lists(pk_index* ix, const float* Q, int64_t B, const int32_t* scope
                    int32_t nprobe, int32_t ef, int32_t mode, int64_t cap, int64_t* out_cids, int32_t* out_coarse,
                    int64_t* out_prefix, int64_t* out_ids, float* out_dists, uint64_t* out_version);
 int pk_list_version(pk_index* ix, uint64_t* version);
+/* pk_rows_reserve: capacity for n row-store slots now (a growth copies the store
+ * and frees the old one, which can stall for hundreds of ms; the Store reserves
+ * each agent's bound when it registers the agent). */
+int pk_rows_reserve(pk_index* ix, int64_t n);
 int pk_rows_put(pk_index* ix, const int32_t* slots, const float* rows, int64_t n);
 int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const float* put_rows, int64_t nput,
                   const int32_t* slots, int64_t n, float* out_d, const int32_t* mq, int32_t nmq,

@@ -99,6 +99,7 @@ _SIGS = [
     ("pk_l1_place", [_vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp, _vp, _vp, _vp, _vp], _int),
     ("pk_agent_lists", [_vp, _vp, _i64, _vp, _i32, _i32, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _vp, _vp], _int),
     ("pk_list_version", [_vp, _vp], _int),
+    ("pk_rows_reserve", [_vp, _i64], _int),
 ]
 STAGES = ("input", "coarse_dist", "coarse_select", "route", "scan", "merge_out")
 EXPORTED = [s[0] for s in _SIGS]

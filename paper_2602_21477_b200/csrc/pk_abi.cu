@@ -3043,6 +3043,13 @@ int pk_agent_read(pk_index* ix, const float* q, const int32_t* put_slots, const 
   return PK_OK;
 }
 
+int pk_rows_reserve(pk_index* ix, int64_t n) {
+  std::lock_guard<CountedMutex> lock_(ix->mu);
+  if (n < 0) return fail(PK_ERR_USAGE, "negative count");
+  CK(cudaSetDevice(ix->device));
+  return rows_reserve(ix, n);
+}
+
 int pk_list_version(pk_index* ix, uint64_t* version) {
   std::lock_guard<CountedMutex> lock_(ix->mu);
   if (!version) return fail(PK_ERR_USAGE, "null output");

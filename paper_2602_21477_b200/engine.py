@@ -304,6 +304,9 @@ class Store:
         self.sequences[agent_id] = []
         self._drows[agent_id] = []
         self._agent_locks[agent_id] = threading.RLock()
+        # the agent's bound in the HBM row store -- n_p L0 pools, n_p L1 pools
+        # and n_p patterns of n_s states -- reserved now, not grown mid-stream
+        self.rows.reserve(c.n_p * (c.l0_capacity + c.l1_capacity + c.n_s) + 64)
         return agent_id
 
     def unregister_agent(self, agent_id: str):

@@ -355,6 +355,10 @@ class DeviceIndex:
         return ids[:pre[-1]], dd[:pre[-1]], pre
 
     # ---- agent path: one device pass per agent search (pk_agent.cu) ---------
+    def rows_reserve(self, n: int):
+        """Capacity for n row-store slots (pk_rows_reserve)."""
+        N.check(N.lib().pk_rows_reserve(self._h, int(n)))
+
     def rows_put(self, slots, rows):
         """Rows into the HBM row store at the given slots (pk_rows_put)."""
         self.flush()

@@ -55,6 +55,11 @@ class RowStore:
                     self._pend.pop(s, None)
                     self._free.append(s)
 
+    def reserve(self, extra: int):
+        """Device capacity for ``extra`` more slots than are allocated now."""
+        self._reserved = max(getattr(self, "_reserved", 0), self._next) + int(extra)
+        self.index.rows_reserve(self._reserved)
+
     @property
     def live(self) -> int:
         return self._next - len(self._free)

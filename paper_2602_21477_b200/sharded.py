@@ -513,6 +513,9 @@ class ShardedStoreIndex:
     def rows_put(self, slots, rows):
         self.local.rows_put(slots, rows)
 
+    def rows_reserve(self, n):
+        self.local.rows_reserve(n)
+
     def l1_place(self, *args, **kw):
         return self.local.l1_place(*args, **kw)
 
